@@ -1,0 +1,674 @@
+"""CPU ORACLE for the hybrid LU-QR hot path of arXiv 1401.5522 -- TEST INFRASTRUCTURE ONLY.
+
+Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s `cpu_baseline` / `--impl reference` legs
+may import this module.  The product path (`paper_1401_5522_b200`, `libhlq.so`) never calls it and
+shares no code with it (no kernels, headers, helpers, tables or constants).
+
+It is a plain, slow, obviously-correct float64 numpy implementation that follows the paper step by
+step in its own order and notation.  "P:<line>" cites /root/reference/PAPER.md (absent on the GPU
+box; citations only), "S:<line>" its SPEC.md.  Tiles are 0-based here (paper: 1-based): step k of
+the code is step k+1 of Alg. 1.  Library primitives used as single steps: numpy matmul, scipy
+solve_triangular (TRSM / triangular inverse).  The trailing updates of Alg. 2 / Alg. 4 loop over
+(i, j) tile pairs; here the j loop (and for GEMM the i loop) is handed to one matmul over the
+trailing block -- every output element is the same sum of the same products, nothing is fused or
+reordered across tiles.
+
+Readings where the paper is silent / garbled follow SURVEY §8c's ambiguity ledger; each is listed
+in DESIGN.md "Readings" and cited at its use below as "ledger <n>".
+
+Pins (tests/test_oracle_pins.py, -m "not gpu"): every public function is pinned to something other
+than itself -- scipy/numpy library routines, closed forms, the paper's worked example
+and bounds, brute force on 2x2/3x3-tile matrices.  parity unpinned: the MUMPS M2
+reading (`mumps_reading=1`) beyond its nb=1 hand values, see DESIGN.md.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+from scipy.linalg import solve_triangular
+
+LU, QR = 0, 1
+CRIT_MAX, CRIT_SUM, CRIT_MUMPS = 0, 1, 2
+EPS_HPL = 2.0 ** -53  # ledger 20: LAPACK dlamch('E'), as HPL uses ("machine precision")
+
+# status bits (mirrors the meaning, not the code, of include/hlq.h)
+ST_NONFINITE, ST_SINGULAR, ST_ZERO_PIVOT_FORCED = 1, 2, 3
+
+
+# ----------------------------------------------------------------------------------------------
+# a0: tile geometry (ragged last tile P:445-449, ledger 19)
+# ----------------------------------------------------------------------------------------------
+def ntiles(N: int, nb: int) -> int:
+    return (N + nb - 1) // nb
+
+
+def tsl(N: int, nb: int, i: int) -> slice:
+    """Rows (or columns) of tile index i, clipped to N (ragged last tile)."""
+    return slice(i * nb, min((i + 1) * nb, N))
+
+
+# ----------------------------------------------------------------------------------------------
+# a1: panel statistics (Eq. 2, Eq. 3, MUMPS P:570-574; 1-norm P:583)
+# ----------------------------------------------------------------------------------------------
+def norm1(T: np.ndarray) -> float:
+    """Matrix 1-norm: maximum over columns of the column absolute sums ("uses the 1-norm")."""
+    if T.size == 0:
+        return 0.0
+    return float(np.max(np.sum(np.abs(T), axis=0)))
+
+
+def panel_stats(A: np.ndarray, N: int, nb: int, k: int):
+    """s_i = ||A_ik||_1 for i>k; local_max(j), away_max(j) over the panel.
+
+    Tile-local pivoting (north_star): the "diagonal domain" of the MUMPS definitions is the diagonal
+    tile itself (ledger 8), so local_max is over A_kk and away_max over the tiles i > k.
+    """
+    n = ntiles(N, nb)
+    rk, ck = tsl(N, nb, k), tsl(N, nb, k)
+    s = np.array([norm1(A[tsl(N, nb, i), ck]) for i in range(k + 1, n)], dtype=np.float64)
+    local_max = np.max(np.abs(A[rk, ck]), axis=0)
+    if k + 1 < n:
+        away_max = np.max(np.abs(A[rk.stop:N, ck]), axis=0)
+    else:
+        away_max = np.zeros(ck.stop - ck.start)
+    return s, local_max, away_max
+
+
+# ----------------------------------------------------------------------------------------------
+# a2: GETRF with partial pivoting local to the tile (Alg. 2)
+# ----------------------------------------------------------------------------------------------
+def getrf(T: np.ndarray):
+    """P*T = L*U, unblocked right-looking Gaussian elimination with partial pivoting.
+
+    Pivot = first maximum of |column| (ledger 6, LAPACK idamax).  ipiv uses LAPACK's sequential-swap
+    semantics (0-based): at column c rows c and ipiv[c] were exchanged across all columns of the tile.
+    Exact zero pivot: the column is left unscaled and flagged (ledger 7).
+    Returns (W packed LU, ipiv int32, zero_pivot bool).
+    """
+    W = np.array(T, dtype=np.float64, copy=True)
+    b = W.shape[0]
+    ipiv = np.zeros(b, dtype=np.int32)
+    zero_pivot = False
+    for c in range(b):
+        p = c + int(np.argmax(np.abs(W[c:, c])))
+        ipiv[c] = p
+        if p != c:
+            W[[c, p], :] = W[[p, c], :]
+        if W[c, c] == 0.0:
+            zero_pivot = True
+            continue
+        W[c + 1:, c] = W[c + 1:, c] / W[c, c]
+        W[c + 1:, c + 1:] -= np.outer(W[c + 1:, c], W[c, c + 1:])
+    return W, ipiv, zero_pivot
+
+
+# ----------------------------------------------------------------------------------------------
+# a3: ||A_kk^-1||_1 exactly from the L and U factors (ledger 3) and MUMPS pivots
+# ----------------------------------------------------------------------------------------------
+def inv_norm1_from_lu(W: np.ndarray) -> float:
+    """||A_kk^-1||_1 = ||U^-1 L^-1 P||_1 = ||U^-1 L^-1||_1 (a column permutation keeps the 1-norm)."""
+    b = W.shape[0]
+    L = np.tril(W, -1) + np.eye(b)
+    U = np.triu(W)
+    with np.errstate(all="ignore"):
+        Y = solve_triangular(L, np.eye(b), lower=True, unit_diagonal=True, check_finite=False)
+        X = solve_triangular(U, Y, lower=False, check_finite=False)
+    return norm1(X)
+
+
+# ----------------------------------------------------------------------------------------------
+# a4: the criteria (Eq. 2 Max P:495, Eq. 3 Sum P:537, Eq. 4 MUMPS P:576-579) and the decision
+# ----------------------------------------------------------------------------------------------
+def _rel_margin(lhs: float, rhs: float) -> float:
+    """ledger 21: (lhs - rhs) / max(lhs, rhs); 1 when both sides are 0 (vacuous LU)."""
+    den = max(lhs, rhs)
+    if den == 0.0:
+        return 1.0
+    return (lhs - rhs) / den
+
+
+def criterion_max_sum(crit: int, alpha: float, inv_norm: float, s: np.ndarray):
+    """Eq. 2: alpha*||A_kk^-1||^-1 >= max_{i>k} ||A_ik||_1 ;  Eq. 3: ... >= sum_{i>k} ||A_ik||_1.
+
+    The Sum is accumulated in ascending i (deterministic order, both sides).  Returns (lu, margin).
+    """
+    lhs = alpha / inv_norm
+    if s.size == 0:
+        rhs = 0.0  # ledger 5: last step, no sub-diagonal tiles
+    elif crit == CRIT_MAX:
+        rhs = float(np.max(s))
+    else:
+        rhs = 0.0
+        for v in s:  # ascending i
+            rhs = rhs + float(v)
+    if math.isnan(lhs) or math.isnan(rhs):
+        return False, float("nan")  # ledger 22
+    return lhs >= rhs, _rel_margin(lhs, rhs)
+
+
+def criterion_mumps(alpha: float, W: np.ndarray, local_max: np.ndarray, away_max: np.ndarray,
+                    reading: int = 0):
+    """Eq. 4.  pivot(j) = |U_jj|; growth_factor(j) = pivot(j)/local_max(j);
+    estimate_max initialised to away_max and updated "for each step i" of the tile LU.
+
+    reading 0 (M1, default, ledger 1): at step i only column i's estimate is scaled by its own
+    growth factor -> estimate(j) = away_max(j) * growth_factor(j).
+    reading 1 (M2): at step i every later column j > i is scaled by growth_factor(i).
+    Guards (ledger 1): away_max(j) = 0 => estimate(j) = 0; local_max(j) = 0 < pivot => growth = +inf.
+    LU iff for all j alpha*pivot(j) >= estimate(j); margin = min_j relative margin.
+    """
+    b = W.shape[0]
+    pivot = np.abs(np.diag(W)).astype(np.float64)
+    growth = np.empty(b)
+    for j in range(b):
+        if local_max[j] == 0.0:
+            growth[j] = math.inf if pivot[j] > 0.0 else 0.0
+        else:
+            growth[j] = pivot[j] / local_max[j]
+    est = np.array(away_max, dtype=np.float64, copy=True)
+    for i in range(b):  # step i of the tile LU
+        if reading == 0:
+            targets = [i]
+        else:
+            targets = range(i + 1, b)
+        for j in targets:
+            if est[j] != 0.0:
+                est[j] = est[j] * growth[i]
+    lu = True
+    margin = math.inf
+    nonfinite = False
+    for j in range(b):
+        lhs = alpha * pivot[j]
+        rhs = est[j]
+        if math.isnan(lhs) or math.isnan(rhs):
+            nonfinite = True
+            continue
+        if math.isinf(rhs):
+            mj = -1.0
+        else:
+            mj = _rel_margin(lhs, rhs)
+        if not (lhs >= rhs):
+            lu = False
+        margin = min(margin, mj)
+    if nonfinite:
+        return False, float("nan")
+    if b == 0:
+        margin = 1.0
+    return lu, margin
+
+
+# ----------------------------------------------------------------------------------------------
+# a5/a6/a7: LU step, variant A1 (Alg. 2)
+# ----------------------------------------------------------------------------------------------
+def lu_step(A: np.ndarray, N: int, nb: int, k: int, W: np.ndarray, ipiv: np.ndarray):
+    n = ntiles(N, nb)
+    rk = tsl(N, nb, k)
+    k0, k1 = rk.start, rk.stop
+    b = k1 - k0
+    # Factor: A_kk <- GETRF(A_kk) (the speculative W is committed)
+    A[k0:k1, k0:k1] = W
+    if k + 1 == n:
+        return
+    U = np.triu(W)
+    L = np.tril(W, -1) + np.eye(b)
+    # Eliminate: A_ik <- A_ik U_kk^-1 for i > k
+    with np.errstate(all="ignore"):
+        A[k1:N, k0:k1] = solve_triangular(U, A[k1:N, k0:k1].T, trans="T", lower=False,
+                                          check_finite=False).T
+    # Apply: A_kj <- L_kk^-1 P_kk A_kj for j > k  (ledger 12, ledger 23: columns > k only)
+    C = A[k0:k1, k1:N]
+    for c in range(b):
+        p = int(ipiv[c])
+        if p != c:
+            C[[c, p], :] = C[[p, c], :]
+    with np.errstate(all="ignore"):
+        A[k0:k1, k1:N] = solve_triangular(L, C, lower=True, unit_diagonal=True, check_finite=False)
+    # Update: A_ij <- A_ij - A_ik A_kj for i, j > k
+    with np.errstate(all="ignore"):
+        A[k1:N, k1:N] -= A[k1:N, k0:k1] @ A[k0:k1, k1:N]
+
+
+def lu_step_update_variant(A, N, nb, k, chunks=4):
+    """Noise-floor variant of the Update (BASELINE "reversed inner-product order"): the rank-b
+    product is summed over K chunks in reverse order.  Same mathematics, different rounding."""
+    rk = tsl(N, nb, k)
+    k0, k1 = rk.start, rk.stop
+    b = k1 - k0
+    edges = np.linspace(0, b, chunks + 1).astype(int)
+    acc = np.zeros((N - k1, N - k1))
+    for c in reversed(range(chunks)):
+        lo, hi = k0 + edges[c], k0 + edges[c + 1]
+        acc += A[k1:N, lo:hi] @ A[lo:hi, k1:N]
+    A[k1:N, k1:N] -= acc
+
+
+# ----------------------------------------------------------------------------------------------
+# Householder kernels (Alg. 4).  LAPACK dlarfg convention (ledger 14); ib-blocked T
+# in forward column-wise dlarft form (ledger 15).
+# ----------------------------------------------------------------------------------------------
+def larfg(alpha: float, x: np.ndarray):
+    """H = I - tau [1; v][1; v]^T with H [alpha; x] = [beta; 0].  Returns (beta, tau, v).
+    beta = -sign(alpha)*||(alpha, x)||_2 (sign(0)=+), tau = (beta-alpha)/beta, v = x/(alpha-beta);
+    x == 0 -> tau = 0, H = I."""
+    ssq = float(np.dot(x, x)) if x.size else 0.0
+    if ssq == 0.0:
+        return alpha, 0.0, np.zeros_like(x)
+    nrm = math.sqrt(alpha * alpha + ssq)
+    beta = -nrm if alpha >= 0.0 else nrm
+    tau = (beta - alpha) / beta
+    v = x / (alpha - beta)
+    return beta, tau, v
+
+
+def geqrt(Tile: np.ndarray, ib: int):
+    """GEQRT: Householder QR of one tile, V (unit lower, below the diagonal) and R in place,
+    T stored as ib x b (block bi occupies columns bi*ib .. , its sb x sb upper triangle).
+    Returns the T array.  Blocked as PLASMA: per ib-panel, dgeqr2 + dlarft, then dlarfb on the rest."""
+    mrow, b = Tile.shape
+    T = np.zeros((ib, b))
+    for i0 in range(0, b, ib):
+        sb = min(ib, b - i0)
+        for j in range(i0, i0 + sb):
+            if j >= mrow:
+                break  # wide ragged tile: reflectors j >= mrow are the identity (tau = 0, T = 0)
+            beta, tau, v = larfg(Tile[j, j], Tile[j + 1:, j].copy())
+            Tile[j, j] = beta
+            Tile[j + 1:, j] = v
+            # apply H_j to the remaining columns of the panel
+            if j + 1 < i0 + sb and tau != 0.0:
+                cols = slice(j + 1, i0 + sb)
+                w = Tile[j, cols] + v @ Tile[j + 1:, cols]
+                Tile[j, cols] -= tau * w
+                Tile[j + 1:, cols] -= tau * np.outer(v, w)
+            # dlarft column j:  T[0:jj, jj] = -tau * T[0:jj,0:jj] @ (V[:,0:jj]^T v_j)
+            jj = j - i0
+            T[jj, i0 + jj] = tau
+            if jj > 0:
+                Vp = _unit_lower(Tile, i0, j)  # columns i0..j-1 of V, rows i0..
+                vj = np.concatenate(([1.0], v))  # v_j on rows j..
+                z = Vp[j - i0:, :].T @ vj
+                T[0:jj, i0 + jj] = -tau * (T[0:jj, i0:i0 + jj] @ z)
+        # dlarfb: C <- (I - V T V^T)^T C = C - V T^T (V^T C) on trailing columns
+        if i0 + sb < b:
+            V = _unit_lower(Tile, i0, i0 + sb)
+            Tb = np.triu(T[0:sb, i0:i0 + sb])
+            C = Tile[i0:, i0 + sb:]
+            Wm = Tb.T @ (V.T @ C)
+            Tile[i0:, i0 + sb:] = C - V @ Wm
+    return T
+
+
+def _unit_lower(Tile, i0, j1):
+    """Unit lower-trapezoidal V of columns i0..j1-1 of a GEQRT tile, rows i0..end."""
+    V = np.tril(Tile[i0:, i0:j1], -1)
+    for c in range(min(j1 - i0, V.shape[0])):
+        V[c, c] = 1.0
+    return V
+
+
+def unmqr(Vtile: np.ndarray, T: np.ndarray, ib: int, C: np.ndarray):
+    """UNMQR: C <- Q^T C with Q from a GEQRT tile; blocks applied in order 0,1,..."""
+    mrow, b = Vtile.shape
+    for i0 in range(0, b, ib):
+        sb = min(ib, b - i0)
+        V = _unit_lower(Vtile, i0, i0 + sb)
+        Tb = np.triu(T[0:sb, i0:i0 + sb])
+        Cb = C[i0:, :]
+        C[i0:, :] = Cb - V @ (Tb.T @ (V.T @ Cb))
+
+
+def tsqrt(R: np.ndarray, A2: np.ndarray, ib: int, tt: bool = False):
+    """TSQRT: QR of [R (upper b x b); A2 (m2 x b)].  R updated in place, V2 stored in A2
+    (the top part of each reflector is e_j, implicit), T returned (ib x b).
+    tt=True gives TTQRT: A2 is upper triangular and V2 stays upper triangular; the
+    strictly-lower part of A2 is ignored (treated as exact zeros) and left untouched."""
+    m2, b = A2.shape
+    T = np.zeros((ib, b))
+    if tt:
+        lowmask = np.tril(np.ones((m2, b), dtype=bool), -1)
+        saved_low = A2[lowmask].copy()
+        A2[lowmask] = 0.0
+    for i0 in range(0, b, ib):
+        sb = min(ib, b - i0)
+        for j in range(i0, i0 + sb):
+            beta, tau, v = larfg(R[j, j], A2[:, j].copy())
+            R[j, j] = beta
+            A2[:, j] = v
+            if j + 1 < i0 + sb and tau != 0.0:
+                cols = slice(j + 1, i0 + sb)
+                w = R[j, cols] + v @ A2[:, cols]
+                R[j, cols] -= tau * w
+                A2[:, cols] -= tau * np.outer(v, w)
+            jj = j - i0
+            T[jj, i0 + jj] = tau
+            if jj > 0:
+                z = A2[:, i0:j].T @ v  # top parts e_i . e_j = 0
+                T[0:jj, i0 + jj] = -tau * (T[0:jj, i0:i0 + jj] @ z)
+        if i0 + sb < b:
+            V2 = A2[:, i0:i0 + sb]
+            Tb = np.triu(T[0:sb, i0:i0 + sb])
+            C1 = R[i0:i0 + sb, i0 + sb:]
+            C2 = A2[:, i0 + sb:]
+            Wm = Tb.T @ (C1 + V2.T @ C2)
+            R[i0:i0 + sb, i0 + sb:] = C1 - Wm
+            A2[:, i0 + sb:] = C2 - V2 @ Wm
+    if tt:
+        A2[lowmask] = saved_low
+    return T
+
+
+def tsmqr(V2: np.ndarray, T: np.ndarray, ib: int, C1: np.ndarray, C2: np.ndarray, tt: bool = False):
+    """TSMQR / TTMQR: [C1; C2] <- Q^T [C1; C2], Q = prod_b (I - [E_b; V2_b] T_b [..]^T).
+    C1 rows are the eliminator tile's rows (b of them), C2 the eliminated tile's rows."""
+    b = V2.shape[1]
+    Vfull = np.triu(V2) if tt else V2
+    for i0 in range(0, b, ib):
+        sb = min(ib, b - i0)
+        Vb = Vfull[:, i0:i0 + sb]
+        Tb = np.triu(T[0:sb, i0:i0 + sb])
+        Wm = Tb.T @ (C1[i0:i0 + sb, :] + Vb.T @ C2)
+        C1[i0:i0 + sb, :] -= Wm
+        C2 -= Vb @ Wm
+
+
+# ----------------------------------------------------------------------------------------------
+# a8-a11: QR step = HQR elimination list (Alg. 3, Alg. 4), plan(k, n, D)
+# ----------------------------------------------------------------------------------------------
+def qr_plan(k: int, n: int, D: int):
+    """ledger 16: domains by (i mod D); head h_d = first row i >= k of domain d (h = k for k's own).
+    Returns (heads ascending, {head: [rows i > head of that domain ascending]}, tt_heads ascending).
+    Flat TS inside a domain onto its head, then flat TT of the other heads onto k."""
+    heads = []
+    members = {}
+    for d in range(D):
+        rows = [i for i in range(k, n) if i % D == d]
+        if rows:
+            heads.append(rows[0])
+            members[rows[0]] = rows[1:]
+    heads.sort()
+    tt_heads = [h for h in heads if h != k]
+    return heads, members, tt_heads
+
+
+@dataclass
+class QRStepData:
+    T_geqrt: dict = field(default_factory=dict)  # head -> T (ib x b)
+    T_ts: dict = field(default_factory=dict)     # i -> T
+    T_tt: dict = field(default_factory=dict)     # head -> T
+
+
+def qr_step(A: np.ndarray, N: int, nb: int, k: int, D: int, ib: int) -> QRStepData:
+    n = ntiles(N, nb)
+    ck = tsl(N, nb, k)
+    right = slice(ck.stop, N)
+    data = QRStepData()
+    heads, members, tt_heads = qr_plan(k, n, D)
+    # GEQRT + UNMQR on every head (Alg. 4a lines 1, 4; Alg. 4b lines 1-2, 4-5)
+    for h in heads:
+        rh = tsl(N, nb, h)
+        tile = A[rh, ck]
+        T = geqrt(tile, ib)
+        A[rh, ck] = tile
+        data.T_geqrt[h] = T
+        if right.start < N:
+            C = A[rh, right]
+            unmqr(tile, T, ib, C)
+            A[rh, right] = C
+    # TS chains (Alg. 4a lines 2, 5) in plan order
+    for h in heads:
+        rh = tsl(N, nb, h)
+        for i in members[h]:
+            ri = tsl(N, nb, i)
+            R = A[rh, ck]
+            Rv = np.triu(R)
+            A2 = A[ri, ck]
+            T = tsqrt(Rv, A2, ib)
+            R[np.triu_indices_from(R)] = Rv[np.triu_indices_from(Rv)]
+            A[rh, ck] = R
+            A[ri, ck] = A2
+            data.T_ts[i] = T
+            if right.start < N:
+                C1 = A[rh, right]
+                C2 = A[ri, right]
+                tsmqr(A2, T, ib, C1, C2)
+                A[rh, right] = C1
+                A[ri, right] = C2
+    # TT merges of the other heads onto k (Alg. 4b lines 6-9)
+    rk = tsl(N, nb, k)
+    for h in tt_heads:
+        rh = tsl(N, nb, h)
+        R = A[rk, ck]
+        Rv = np.triu(R)
+        Ht = A[rh, ck]
+        T = tsqrt(Rv, Ht, ib, tt=True)
+        R[np.triu_indices_from(R)] = Rv[np.triu_indices_from(Rv)]
+        A[rk, ck] = R
+        A[rh, ck] = Ht
+        data.T_tt[h] = T
+        if right.start < N:
+            C1 = A[rk, right]
+            C2 = A[rh, right]
+            tsmqr(Ht, T, ib, C1, C2, tt=True)
+            A[rk, right] = C1
+            A[rh, right] = C2
+    return data
+
+
+# ----------------------------------------------------------------------------------------------
+# a12 growth (ledger 17) and Alg. 1 driver
+# ----------------------------------------------------------------------------------------------
+def max_tile_norm(A: np.ndarray, N: int, nb: int, k: int) -> float:
+    """max over i, j >= k of ||A_ij||_1 (valid extents).  max_ij max_col(colsum) is the max over all
+    (tile row i, column) column-segment abs-sums, so it is computed as one reduceat per tile row."""
+    k0 = k * nb
+    if k0 >= N:
+        return 0.0
+    B = np.abs(A[k0:N, k0:N])
+    starts = np.arange(0, N - k0, nb)
+    return float(np.max(np.add.reduceat(B, starts, axis=0)))
+
+
+@dataclass
+class Factors:
+    A: np.ndarray
+    N: int
+    nb: int
+    n: int
+    ib: int
+    D: int
+    dec: np.ndarray
+    margin: np.ndarray
+    near_tie: np.ndarray
+    ipiv: dict
+    qr: dict
+    growth: float
+    status: int
+    stats: list
+
+
+def hybrid_factor(A_in: np.ndarray, nb: int, crit: int = CRIT_MAX, alpha: float = 1.0, D: int = 1,
+                  ib: int = 32, mumps_reading: int = 0, forced=None, track_growth: bool = True,
+                  tie_tol: float = 1e-10, variant: int = 0, on_step=None) -> Factors:
+    """Alg. 1: for each step, speculative tile LU, criterion, LU or QR step.
+
+    forced: decision vector used verbatim (C3); variant=1 uses the reversed-chunk GEMM (noise floor).
+    on_step(k, A_before, A_after, d): optional test hook called after each step with copies.
+    """
+    A = np.array(A_in, dtype=np.float64, order="F", copy=True)
+    N = A.shape[0]
+    n = ntiles(N, nb)
+    dec = np.zeros(n, dtype=np.uint8)
+    margin = np.zeros(n)
+    near_tie = np.zeros(n, dtype=bool)
+    ipivs, qrs, stats = {}, {}, []
+    status = 0
+    g0 = max_tile_norm(A, N, nb, 0) if track_growth else 1.0
+    g = g0
+    for k in range(n):
+        rk = tsl(N, nb, k)
+        A_before = A.copy() if on_step is not None else None
+        s, lmax, amax = panel_stats(A, N, nb, k)
+        # Factor (speculative, out of place: the paper's Backup Panel P:634-640 becomes a copy)
+        W, ipiv, zp = getrf(A[rk, rk])
+        inv = float("nan")
+        mg = float("nan")
+        if forced is not None:
+            d = int(forced[k])
+            if d == LU and zp and status == 0:
+                status = ST_ZERO_PIVOT_FORCED
+            mg = float("nan")
+        elif alpha == 0.0:
+            d = QR  # ledger 4
+        elif zp:
+            d = QR  # ledger 7
+        elif math.isinf(alpha):
+            d = LU  # ledger 4
+        else:
+            if crit in (CRIT_MAX, CRIT_SUM):
+                inv = inv_norm1_from_lu(W)
+                lu, mg = criterion_max_sum(crit, alpha, inv, s)
+            else:
+                lu, mg = criterion_mumps(alpha, W, lmax, amax, mumps_reading)
+            if math.isnan(mg):
+                status = ST_NONFINITE
+                d = QR
+            else:
+                d = LU if lu else QR
+                near_tie[k] = abs(mg) < tie_tol
+        dec[k] = d
+        margin[k] = mg
+        stats.append({"k": k, "s": s, "local_max": lmax, "away_max": amax, "inv_norm": inv,
+                      "zero_pivot": zp})
+        if d == LU:
+            lu_step(A, N, nb, k, W, ipiv)
+            if variant == 1 and k + 1 < n:
+                # undo the standard update and redo it with the reversed-chunk order
+                k0, k1 = rk.start, rk.stop
+                A[k1:N, k1:N] += A[k1:N, k0:k1] @ A[k0:k1, k1:N]
+                lu_step_update_variant(A, N, nb, k)
+            ipivs[k] = ipiv
+        else:
+            qrs[k] = qr_step(A, N, nb, k, D, ib)
+        if track_growth and k + 1 < n:
+            g = max(g, max_tile_norm(A, N, nb, k + 1))
+        if on_step is not None:
+            on_step(k, A_before, A.copy(), d)
+    zp_forced = status == ST_ZERO_PIVOT_FORCED
+    if not np.all(np.isfinite(A)) or status == ST_NONFINITE:
+        status = ST_NONFINITE
+    elif zp_forced:
+        status = ST_ZERO_PIVOT_FORCED
+    elif np.any(np.diag(A) == 0.0):
+        status = ST_SINGULAR
+    else:
+        status = 0
+    growth = (g / g0) if (track_growth and g0 > 0) else float("nan")
+    if track_growth and not np.isfinite(g):
+        growth = math.inf
+    return Factors(A, N, nb, n, ib, D, dec, margin, near_tie, ipivs, qrs, growth, status, stats)
+
+
+# ----------------------------------------------------------------------------------------------
+# a13: solve by a second pass over b + back substitution
+# ----------------------------------------------------------------------------------------------
+def apply_transforms(f: Factors, x: np.ndarray) -> np.ndarray:
+    """Replay every step's transformation on x (a vector or a column block), in step order."""
+    A, N, nb, n, ib = f.A, f.N, f.nb, f.n, f.ib
+    x = np.array(x, dtype=np.float64, copy=True)
+    vec = x.ndim == 1
+    if vec:
+        x = x[:, None]
+    for k in range(n):
+        rk = tsl(N, nb, k)
+        k0, k1 = rk.start, rk.stop
+        if f.dec[k] == LU:
+            ipiv = f.ipiv[k]
+            for c in range(k1 - k0):
+                p = int(ipiv[c])
+                if p != c:
+                    x[[k0 + c, k0 + p], :] = x[[k0 + p, k0 + c], :]
+            Lkk = np.tril(A[rk, rk], -1) + np.eye(k1 - k0)
+            x[rk, :] = solve_triangular(Lkk, x[rk, :], lower=True, unit_diagonal=True,
+                                        check_finite=False)
+            if k1 < N:
+                x[k1:N, :] -= A[k1:N, k0:k1] @ x[rk, :]
+        else:
+            d = f.qr[k]
+            heads, members, tt_heads = qr_plan(k, n, f.D)
+            for h in heads:
+                rh = tsl(N, nb, h)
+                xh = x[rh, :].copy()
+                unmqr(A[rh, rk], d.T_geqrt[h], ib, xh)
+                x[rh, :] = xh
+            for h in heads:
+                rh = tsl(N, nb, h)
+                for i in members[h]:
+                    ri = tsl(N, nb, i)
+                    c1, c2 = x[rh, :].copy(), x[ri, :].copy()
+                    tsmqr(A[ri, rk], d.T_ts[i], ib, c1, c2)
+                    x[rh, :], x[ri, :] = c1, c2
+            for h in tt_heads:
+                rh = tsl(N, nb, h)
+                c1, c2 = x[rk, :].copy(), x[rh, :].copy()
+                tsmqr(A[rh, rk], d.T_tt[h], ib, c1, c2, tt=True)
+                x[rk, :], x[rh, :] = c1, c2
+    return x[:, 0] if vec else x
+
+
+def back_substitute(f: Factors, y: np.ndarray) -> np.ndarray:
+    """x_k = U_kk^-1 (y_k - sum_{j>k} A_kj x_j), k = n..1 (the N-by-N triangular solve)."""
+    A, N, nb, n = f.A, f.N, f.nb, f.n
+    x = np.array(y, dtype=np.float64, copy=True)
+    for k in reversed(range(n)):
+        rk = tsl(N, nb, k)
+        r = x[rk].copy()
+        if rk.stop < N:
+            r = r - A[rk, rk.stop:N] @ x[rk.stop:N]
+        x[rk] = solve_triangular(np.triu(A[rk, rk]), r, lower=False, check_finite=False)
+    return x
+
+
+def solve(f: Factors, b: np.ndarray) -> np.ndarray:
+    with np.errstate(all="ignore"):
+        return back_substitute(f, apply_transforms(f, b))
+
+
+def hpl3(A: np.ndarray, x: np.ndarray, b: np.ndarray) -> float:
+    """HPL3 = ||Ax-b||_inf / (||A||_inf ||x||_inf eps N), eps = 2^-53 (ledger 20)."""
+    N = A.shape[0]
+    r = A @ x - b
+    return float(np.max(np.abs(r)) / (np.max(np.sum(np.abs(A), axis=1)) * np.max(np.abs(x))
+                                      * EPS_HPL * N))
+
+
+# ----------------------------------------------------------------------------------------------
+# Flop accounting (Table I; normalised / true GFLOP/s P:750)
+# ----------------------------------------------------------------------------------------------
+def step_flops(N: int, nb: int, k: int, d: int) -> float:
+    """Table I with valid sizes: LU = 2/3 b^3 + M b^2 (TRSM) + b^2 M (SWPTRSM) + 2 M^2 b (GEMM),
+    b = diagonal tile order, M = rows below it; a QR step costs exactly twice (Table I columns)."""
+    rk = tsl(N, nb, k)
+    b = rk.stop - rk.start
+    M = N - rk.stop
+    lu = 2.0 / 3.0 * b ** 3 + 2.0 * M * b * b + 2.0 * M * M * b
+    return lu * (2.0 if d == QR else 1.0)
+
+
+def true_flops(N: int, nb: int, dec) -> float:
+    return float(sum(step_flops(N, nb, k, int(d)) for k, d in enumerate(dec)))
+
+
+def fake_flops(N: int) -> float:
+    return 2.0 / 3.0 * float(N) ** 3
+
+
+def paper_true_flops(N: int, f_lu: float) -> float:
+    """(2/3 f_LU + 4/3 (1 - f_LU)) N^3."""
+    return (2.0 / 3.0 * f_lu + 4.0 / 3.0 * (1.0 - f_lu)) * float(N) ** 3
+
+
+def factor_diff(Fa: np.ndarray, Fb: np.ndarray) -> float:
+    """Normwise relative difference of packed factor arrays ||Fa - Fb||_F / ||Fb||_F."""
+    return float(np.linalg.norm(Fa - Fb) / np.linalg.norm(Fb))

@@ -1,0 +1,424 @@
+"""Pins for the CPU oracle (-m "not gpu"): each oracle function is checked against something other
+than itself -- LAPACK routines (scipy.linalg.lapack), numpy dense formulas, the paper's worked example
+and bounds, brute force on tiny tiled matrices.  See DESIGN.md "Oracle pins"."""
+import itertools
+import math
+import os
+
+import numpy as np
+import pytest
+import scipy.linalg as sl
+import scipy.linalg.lapack as lapack
+
+import hlq_inputs as I
+from oracle import hlq_oracle as O
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+RNG = np.random.default_rng(1234)
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+# ---------------------------------------------------------------- P1: tile kernels
+def test_norm1_hand_values():
+    assert O.norm1(np.array([[1.0, -2.0], [3.0, 4.0]])) == 6.0
+    assert O.norm1(np.eye(5)) == 1.0
+    T = RNG.standard_normal((7, 7))
+    assert O.norm1(T) == pytest.approx(np.linalg.norm(T, 1), rel=1e-15)
+
+
+@pytest.mark.parametrize("b", [1, 2, 5, 16, 64])
+def test_getrf_matches_lapack_dgetrf(b):
+    for _ in range(3):
+        T = RNG.standard_normal((b, b))
+        W, ipiv, zp = O.getrf(T)
+        lu, piv, info = lapack.dgetrf(T)
+        assert not zp and info == 0
+        np.testing.assert_array_equal(ipiv, piv)
+        assert rel(W, lu) < 1e-13
+
+
+def test_getrf_forced_swap_and_zero_pivot():
+    W, ipiv, zp = O.getrf(np.array([[0.0, 1.0], [1.0, 0.0]]))  # SPEC: [[0,1],[1,0]] -> swap, U = I
+    assert list(ipiv) == [1, 1] and not zp
+    np.testing.assert_array_equal(np.triu(W), np.eye(2))
+    W, ipiv, zp = O.getrf(np.array([[1.0, 2.0], [2.0, 4.0]]))
+    assert zp  # singular tile: exact zero pivot flagged (ledger 7)
+    # tie-break: first maximum (ledger 6)
+    W, ipiv, zp = O.getrf(np.array([[1.0, 0.0, 0.0], [-3.0, 1.0, 0.0], [3.0, 0.0, 1.0]]))
+    assert ipiv[0] == 1
+
+
+@pytest.mark.parametrize("b", [1, 3, 32, 100])
+def test_inv_norm_matches_dense_inverse(b):
+    T = RNG.standard_normal((b, b))
+    W, _, _ = O.getrf(T)
+    assert O.inv_norm1_from_lu(W) == pytest.approx(np.linalg.norm(np.linalg.inv(T), 1), rel=1e-11)
+    W, _, _ = O.getrf(np.diag([2.0, 0.5]))
+    assert O.inv_norm1_from_lu(W) == 2.0
+
+
+@pytest.mark.parametrize("b,ib", [(8, 4), (32, 32), (64, 16), (50, 16), (128, 32)])
+def test_geqrt_matches_lapack_dgeqrt(b, ib):
+    T0 = RNG.standard_normal((b, b))
+    tile = T0.copy()
+    Tf = O.geqrt(tile, ib)
+    a, t, info = lapack.dgeqrt(ib, T0.copy())
+    assert info == 0
+    assert rel(tile, a) < 1e-12  # V below the diagonal and R on/above it
+    assert rel(Tf, t) < 1e-12
+    # R equals numpy's QR R up to row signs
+    R = np.linalg.qr(T0, mode="r")
+    assert rel(np.abs(np.triu(tile)), np.abs(R)) < 1e-12
+
+
+def test_unmqr_matches_dgemqrt_and_is_orthogonal():
+    b, ib, nc = 64, 16, 40
+    T0 = RNG.standard_normal((b, b))
+    tile = T0.copy()
+    Tf = O.geqrt(tile, ib)
+    C = RNG.standard_normal((b, nc))
+    C1 = C.copy()
+    O.unmqr(tile, Tf, ib, C1)
+    V = np.tril(tile, -1) + np.eye(b)
+    ref, info = lapack.dgemqrt(V, Tf, C.copy(), side="L", trans="T")
+    assert rel(C1, ref) < 1e-12
+    # Q^T from applying to the identity: orthogonal and Q^T T0 = R
+    Qt = np.eye(b)
+    O.unmqr(tile, Tf, ib, Qt)
+    assert np.linalg.norm(Qt @ Qt.T - np.eye(b)) < 10 * b * 2.2e-16
+    assert rel(Qt @ T0, np.triu(tile)) < 1e-13
+
+
+@pytest.mark.parametrize("tt", [False, True])
+@pytest.mark.parametrize("b,ib", [(16, 4), (64, 32), (48, 16)])
+def test_tsqrt_tsmqr_match_lapack_dtpqrt(tt, b, ib):
+    R0 = np.triu(RNG.standard_normal((b, b)))
+    A2 = RNG.standard_normal((b, b))
+    if tt:
+        low = np.tril(RNG.standard_normal((b, b)), -1)  # junk below: must be ignored and preserved
+        A2 = np.triu(A2) + low
+    R = R0.copy()
+    B = A2.copy()
+    T = O.tsqrt(R, B, ib, tt=tt)
+    l = b if tt else 0
+    a_ref, b_ref, t_ref, info = lapack.dtpqrt(l, ib, R0.copy(), (np.triu(A2) if tt else A2).copy())
+    assert info == 0
+    assert rel(np.triu(R), np.triu(a_ref)) < 1e-12
+    Bv = np.triu(B) if tt else B
+    assert rel(Bv, (np.triu(b_ref) if tt else b_ref)) < 1e-12
+    assert rel(T, t_ref) < 1e-12
+    if tt:
+        np.testing.assert_array_equal(np.tril(B, -1), low)
+    # TSMQR / TTMQR against dtpmqrt
+    nc = 24
+    C1 = RNG.standard_normal((b, nc))
+    C2 = RNG.standard_normal((b, nc))
+    c1, c2 = C1.copy(), C2.copy()
+    O.tsmqr(B, T, ib, c1, c2, tt=tt)
+    r1, r2, info = lapack.dtpmqrt(l, Bv, T, C1.copy(), C2.copy(), side="L", trans="T")
+    assert rel(c1, r1) < 1e-12 and rel(c2, r2) < 1e-12
+    # applying the transform to its own input annihilates the bottom tile
+    c1, c2 = R0.copy(), (np.triu(A2) if tt else A2).copy()
+    O.tsmqr(B, T, ib, c1, c2, tt=tt)
+    assert np.linalg.norm(c2) < 1e-12 * np.linalg.norm(A2)
+    assert rel(c1, np.triu(R)) < 1e-12
+
+
+def test_larfg_matches_lapack():
+    x = RNG.standard_normal(9)
+    beta, tau, v = O.larfg(x[0], x[1:].copy())
+    b2, xv, t2 = lapack.dlarfg(9, x[0], x[1:].copy())
+    assert beta == pytest.approx(b2, rel=1e-14) and tau == pytest.approx(t2, rel=1e-14)
+    np.testing.assert_allclose(v, xv, rtol=1e-13)
+    beta, tau, v = O.larfg(3.0, np.zeros(4))
+    assert tau == 0.0 and beta == 3.0
+
+
+# ---------------------------------------------------------------- criteria hand values (SPEC)
+def _one_step_decision(A, crit, alpha, reading=0):
+    f = O.hybrid_factor(np.asfortranarray(A), 1, crit, alpha, mumps_reading=reading)
+    return f.dec[0]
+
+
+def test_criteria_hand_values():
+    # Max, nb=1: A_kk=2, below {1}, alpha=1 -> 2 >= 1 -> LU
+    A = np.array([[2.0, 0.3], [1.0, 1.7]])
+    assert _one_step_decision(A, O.CRIT_MAX, 1.0) == O.LU
+    # Sum stricter: A_kk=2, below {1,1,1}: Max LU, Sum 2 < 3 -> QR
+    A = np.eye(4) * 2.0
+    A[1:, 0] = 1.0
+    assert _one_step_decision(A, O.CRIT_MAX, 1.0) == O.LU
+    assert _one_step_decision(A, O.CRIT_SUM, 1.0) == O.QR
+    # MUMPS nb=1: pivot 4, away 3, alpha 2.1 -> 8.4 >= 3 LU;  pivot 1, away 3 -> 2.1 < 3 QR
+    for reading in (0, 1):
+        A = np.array([[4.0, 0.0, 0.0], [1.0, 1.0, 0.0], [3.0, 0.0, 1.0]])
+        assert _one_step_decision(A, O.CRIT_MUMPS, 2.1, reading) == O.LU
+        A = np.array([[1.0, 0.0], [3.0, 1.0]])
+        assert _one_step_decision(A, O.CRIT_MUMPS, 2.1, reading) == O.QR
+    # alpha specials (ledger 4): alpha = 0 -> QR everywhere, alpha = inf -> LU everywhere
+    A = I.uniform_matrix(7, 64)
+    assert set(O.hybrid_factor(A, 16, O.CRIT_MAX, 0.0).dec) == {O.QR}
+    assert set(O.hybrid_factor(A, 16, O.CRIT_MAX, math.inf).dec) == {O.LU}
+
+
+def test_mumps_m1_equals_dense_formula():
+    """M1 (ledger 1) algebra: with nonzero pivots, estimate(j) = away_max(j) * pivot(j)/local_max(j),
+    so alpha*pivot(j) >= estimate(j)  <=>  alpha*local_max(j) >= away_max(j)."""
+    for trial in range(40):
+        b = 8
+        T = RNG.standard_normal((b, b))
+        below = RNG.standard_normal((3 * b, b)) * RNG.uniform(0.2, 3.0)
+        W, _, _ = O.getrf(T)
+        lm = np.max(np.abs(T), axis=0)
+        am = np.max(np.abs(below), axis=0)
+        alpha = RNG.uniform(0.5, 4.0)
+        lu, margin = O.criterion_mumps(alpha, W, lm, am, 0)
+        dense = bool(np.all(alpha * lm >= am))
+        ratio = np.min(alpha * lm / am)
+        if abs(ratio - 1.0) > 1e-12:
+            assert lu == dense
+
+
+def test_sum_implies_max_and_alpha_monotone():
+    A = I.uniform_matrix(11, 96)
+    for alpha in (1e3, 1e4, 3e4):
+        fs = O.hybrid_factor(A, 16, O.CRIT_SUM, alpha)
+        stats = fs.stats[0]
+        inv = stats["inv_norm"]
+        lu_sum, _ = O.criterion_max_sum(O.CRIT_SUM, alpha, inv, stats["s"])
+        lu_max, _ = O.criterion_max_sum(O.CRIT_MAX, alpha, inv, stats["s"])
+        assert (not lu_sum) or lu_max
+        lu_big, _ = O.criterion_max_sum(O.CRIT_MAX, alpha * 2, inv, stats["s"])
+        assert (not lu_max) or lu_big
+
+
+# ---------------------------------------------------------------- P5: growth bounds, worst case
+def _golden_rows(name):
+    rows = []
+    for line in open(os.path.join(GOLD, name)):
+        line = line.strip()
+        if line and not line.startswith("#"):
+            rows.append(line.split())
+    return rows
+
+
+@pytest.mark.parametrize("row", _golden_rows("worst_case_max.txt"))
+def test_worst_case_matrix_attains_max_bound(row):
+    alpha, n, nb, growth, decs = float(row[0]), int(row[1]), int(row[2]), float(row[3]), row[4]
+    A = I.kron_lift(I.worst_case_max(n, alpha), nb) if nb > 1 else np.asfortranarray(
+        I.worst_case_max(n, alpha))
+    f = O.hybrid_factor(A, nb, O.CRIT_MAX, alpha)
+    assert "".join("LQ"[d] for d in f.dec) == decs
+    assert f.growth == growth  # exact: (1+alpha)^(n-1)
+    assert growth == (1 + alpha) ** (n - 1)
+    assert all(abs(m) < 1e-10 for m in f.margin[:-1])  # exact ties; last step vacuous
+
+
+def test_block_diagonally_dominant_all_lu_and_sum_bound():
+    """BDD (by columns, 1-norm) => Max and Sum with alpha >= 1 pass at every step;
+    Sum with alpha = 1 bounds the growth by n."""
+    n, nb = 6, 8
+    N = n * nb
+    A = RNG.standard_normal((N, N))
+    for j in range(n):
+        cj = slice(j * nb, (j + 1) * nb)
+        off = sum(O.norm1(A[i * nb:(i + 1) * nb, cj]) for i in range(n) if i != j)
+        A[cj, cj] = np.eye(nb) * (off + 1.0)
+    A = np.asfortranarray(A)
+    for crit in (O.CRIT_MAX, O.CRIT_SUM):
+        f = O.hybrid_factor(A, nb, crit, 1.0)
+        assert set(f.dec) == {O.LU}
+        assert f.growth <= n
+    # scalar diagonally dominant: growth <= 2
+    Ad = RNG.standard_normal((24, 24))
+    Ad += np.diag(np.sum(np.abs(Ad), axis=0) + 1.0)
+    f = O.hybrid_factor(np.asfortranarray(Ad), 1, O.CRIT_SUM, 1.0)
+    assert set(f.dec) == {O.LU} and f.growth <= 2.0
+
+
+def _tile_norms(A, N, nb, k):
+    n = O.ntiles(N, nb)
+    return np.array([[O.norm1(A[O.tsl(N, nb, i), O.tsl(N, nb, j)]) for j in range(n)]
+                     for i in range(n)])
+
+
+def test_per_step_growth_inequalities_on_mixed_run():
+    """Max: ||A_ij^(k+1)|| <= (1+alpha) max_{i'>=k} ||A_i'j^(k)|| on LU steps;
+    Sum (alpha=1): sum_{i>k} ||A_ij^(k+1)|| <= sum_{i>=k} ||A_ij^(k)||;
+    QR steps preserve the 2-norms of the active columns."""
+    N, nb = 192, 16
+    A = I.uniform_matrix(21, N)
+    checks = {"lu": 0, "qr": 0}
+
+    for crit, alpha in ((O.CRIT_MAX, 1.1e4), (O.CRIT_MAX, 3e4), (O.CRIT_SUM, 1.0)):
+        def hook(k, Ab, Aa, d):
+            n = O.ntiles(N, nb)
+            if k + 1 >= n:
+                return
+            tb, ta = _tile_norms(Ab, N, nb, k), _tile_norms(Aa, N, nb, k)
+            k0 = k * nb
+            if d == O.LU:
+                checks["lu"] += 1
+                for j in range(k + 1, n):
+                    if crit == O.CRIT_MAX:
+                        bound = (1 + alpha) * tb[k:, j].max()
+                        assert ta[k + 1:, j].max() <= bound * (1 + 1e-12)
+                    else:
+                        assert ta[k + 1:, j].sum() <= tb[k:, j].sum() * (1 + 1e-12)
+            else:
+                checks["qr"] += 1
+                k1 = k0 + nb  # trailing columns: whole active column; panel: only R (V is stored below)
+                np.testing.assert_allclose(np.linalg.norm(Aa[k0:, k1:], axis=0),
+                                           np.linalg.norm(Ab[k0:, k1:], axis=0), rtol=1e-12)
+                np.testing.assert_allclose(np.linalg.norm(np.triu(Aa[k0:k1, k0:k1]), axis=0),
+                                           np.linalg.norm(Ab[k0:, k0:k1], axis=0), rtol=1e-12)
+        O.hybrid_factor(A, nb, crit, alpha, on_step=hook)
+    assert checks["lu"] > 0 and checks["qr"] > 0
+
+
+# ---------------------------------------------------------------- P2/P3: the two extreme paths
+def _restricted_pivot_ge(A, nb):
+    """Independent scalar Gaussian elimination (ledger 24): pivot search at column c over rows
+    c .. end of c's diagonal block; swaps on columns >= that block's start; eliminate all rows below."""
+    A = np.array(A, dtype=np.float64, copy=True)
+    N = A.shape[0]
+    piv = np.zeros(N, dtype=np.int64)
+    for c in range(N):
+        blk0 = (c // nb) * nb
+        blk1 = min(blk0 + nb, N)
+        p = c + int(np.argmax(np.abs(A[c:blk1, c])))
+        piv[c] = p
+        if p != c:
+            A[[c, p], blk0:] = A[[p, c], blk0:]
+        A[c + 1:, c] /= A[c, c]
+        A[c + 1:, c + 1:] -= np.outer(A[c + 1:, c], A[c, c + 1:])
+    return A, piv
+
+
+@pytest.mark.parametrize("N,nb", [(96, 32), (100, 32), (128, 16)])
+def test_all_lu_path_is_restricted_pivot_gaussian_elimination(N, nb):
+    A = I.uniform_matrix(3, N)
+    f = O.hybrid_factor(A, nb, O.CRIT_MAX, math.inf)
+    G, piv = _restricted_pivot_ge(A, nb)
+    for k, ip in f.ipiv.items():
+        np.testing.assert_array_equal(ip + k * nb, piv[k * nb:k * nb + len(ip)])
+    assert rel(f.A, G) < 1e-11
+
+
+@pytest.mark.parametrize("N,nb,D", [(128, 32, 1), (160, 32, 2), (150, 32, 3)])
+def test_all_qr_path_reproduces_householder_R(N, nb, D):
+    A, b = I.normal_system(9, N)
+    f = O.hybrid_factor(A, nb, O.CRIT_MAX, 0.0, D=D)
+    R = np.linalg.qr(A, mode="r")
+    assert rel(np.abs(np.triu(f.A)), np.abs(R)) < 1e-12
+    x = O.solve(f, b)
+    assert rel(x, np.linalg.solve(A, b)) < 1e-10
+
+
+@pytest.mark.parametrize("crit,alpha", [(O.CRIT_MAX, 1.0), (O.CRIT_MAX, 1e4), (O.CRIT_SUM, 4.0),
+                                        (O.CRIT_MUMPS, 1.5), (O.CRIT_MUMPS, 4.0)])
+def test_solve_matches_numpy_and_hpl3(crit, alpha):
+    N, nb = 256, 32
+    A, b = I.normal_system(2, N)
+    f = O.hybrid_factor(A, nb, crit, alpha)
+    x = O.solve(f, b)
+    assert rel(x, np.linalg.solve(A, b)) < 1e-9
+    assert O.hpl3(A, x, b) < 16
+
+
+def test_hpl3_hand_value():
+    A = 2.0 * np.eye(2)
+    x = np.array([1.0, 1.0])
+    d = 2.0 ** -40
+    b = np.array([2.0, 2.0 + d])
+    assert O.hpl3(A, x, b) == pytest.approx(d / (2.0 * 1.0 * 2.0 ** -53 * 2))
+
+
+# ---------------------------------------------------------------- P4: brute force on tiny tiled matrices
+def _dense_criterion(Ab, N, nb, k, crit, alpha):
+    n = O.ntiles(N, nb)
+    rk = O.tsl(N, nb, k)
+    Akk = Ab[rk, rk]
+    lhs = alpha / np.linalg.norm(np.linalg.inv(Akk), 1)
+    norms = [np.linalg.norm(Ab[O.tsl(N, nb, i), rk], 1) for i in range(k + 1, n)]
+    rhs = (max(norms) if crit == O.CRIT_MAX else sum(norms)) if norms else 0.0
+    return lhs, rhs
+
+
+@pytest.mark.parametrize("n", [2, 3])
+@pytest.mark.parametrize("nb", [1, 2, 4])
+def test_brute_force_all_decision_vectors(n, nb):
+    N = n * nb
+    A = np.asfortranarray(RNG.standard_normal((N, N)))
+    b = RNG.standard_normal(N)
+    xs = np.linalg.solve(A, b)
+    for vec in itertools.product([0, 1], repeat=n):
+        f = O.hybrid_factor(A, nb, forced=np.array(vec, dtype=np.uint8))
+        # (M_n ... M_1) A = U : replay every step on A's columns
+        U = O.apply_transforms(f, A)
+        assert np.linalg.norm(np.tril(U, -1)) < 10 * N * 2.2e-16 * np.linalg.norm(A) * 1e3
+        assert rel(np.triu(U), np.triu(f.A)) < 1e-10
+        assert rel(O.solve(f, b), xs) < 1e-8
+    # the criterion's decision vector is self-consistent with dense recomputation at every step
+    for crit, alpha in ((O.CRIT_MAX, 1.0), (O.CRIT_MAX, 3.0), (O.CRIT_SUM, 2.0)):
+        def hook(k, Ab, Aa, d):
+            lhs, rhs = _dense_criterion(Ab, N, nb, k, crit, alpha)
+            if abs(lhs - rhs) > 1e-9 * max(lhs, rhs):
+                assert d == (O.LU if lhs >= rhs else O.QR)
+        O.hybrid_factor(A, nb, crit, alpha, on_step=hook)
+
+
+# ---------------------------------------------------------------- P9 ragged == padded; P8 flops
+@pytest.mark.parametrize("crit,alpha", [(O.CRIT_MAX, 1.0), (O.CRIT_MAX, math.inf),
+                                        (O.CRIT_MUMPS, 2.0)])
+def test_ragged_equals_padded(crit, alpha):
+    N, nb = 200, 64
+    A = I.uniform_matrix(5, N)
+    npad = O.ntiles(N, nb) * nb
+    P = np.eye(npad)
+    P[:N, :N] = A
+    fr = O.hybrid_factor(A, nb, crit, alpha)
+    fp = O.hybrid_factor(np.asfortranarray(P), nb, crit, alpha)
+    np.testing.assert_array_equal(fr.dec[:-1], fp.dec[:-1])
+    assert rel(fr.A[:N, :N], fp.A[:N, :N]) < 1e-12
+
+
+def test_table_i_sums_and_table_ii_arithmetic():
+    for N, nb in ((1024, 128), (16384, 256), (32768, 256)):
+        n = N // nb
+        assert O.true_flops(N, nb, [0] * n) == pytest.approx(O.fake_flops(N), rel=1e-12)
+        assert O.true_flops(N, nb, [1] * n) == pytest.approx(2 * O.fake_flops(N), rel=1e-12)
+    for row in _golden_rows("table2.txt"):
+        t, pct, fake, true = float(row[2]), float(row[3]), float(row[4]), float(row[5])
+        assert O.fake_flops(20000) / t / 1e9 == pytest.approx(fake, rel=5e-3)
+        if row[0].startswith("LUQR") or row[0] == "HQR":
+            assert O.paper_true_flops(20000, pct / 100) / t / 1e9 == pytest.approx(true, rel=5e-3)
+
+
+# ---------------------------------------------------------------- generator
+def _splitmix_ref(seed, idx):
+    M = (1 << 64) - 1
+    g = 0x9E3779B97F4A7C15
+
+    def mix(z):
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+        return z ^ (z >> 31)
+    kk = mix((seed + g) & M)
+    u = mix((kk + (idx + 1) * g) & M)
+    return (u >> 11) * 2.0 ** -53 - 0.5
+
+
+def test_counter_generator_matches_plain_int_reference():
+    idx = np.array([0, 1, 2, 12345, 2 ** 34 + 7, 131072 ** 2 + 5], dtype=np.uint64)
+    got = I.uniform_counter(2, idx)
+    for v, i in zip(got, idx):
+        assert v == _splitmix_ref(2, int(i))
+    A = I.uniform_matrix(0, 8)
+    assert A[3, 5] == _splitmix_ref(0, 5 * 8 + 3)
+    assert A.flags["F_CONTIGUOUS"]
+    u = I.uniform_matrix(0, 256).ravel()
+    assert -0.5 <= u.min() and u.max() < 0.5 and abs(u.mean()) < 0.01
