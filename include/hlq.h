@@ -1,0 +1,152 @@
+/* hlq.h -- C ABI of the B200-native hybrid LU-QR hot path (arXiv 1401.5522).
+ *
+ * The library (paper_1401_5522_b200/libhlq.so, sm_100a) factors a square FP64 matrix A, stored as
+ * n x n tiles of nb x nb, by the hybrid algorithm of Alg. 1:
+ * at every step k a robustness criterion (Max Eq. 2, Sum Eq. 3, MUMPS Eq. 4)
+ * evaluated ON THE DEVICE picks an LU step (Alg. 2: GETRF with pivoting local to the
+ * diagonal tile, TRSM, SWPTRSM, DGEMM update) or a QR step (Algs. 3-4 P:310-346: GEQRT, TTQRT,
+ * UNMQR, TTMQR on the HQR greedy tree).  hlq_solve then replays the stored transformations on b
+ * (the "second pass" of P:441-442) and back-substitutes with the N x N upper triangle.
+ *
+ * Conventions (all functions):
+ *   - Matrices and vectors are FP64, COLUMN-MAJOR (LAPACK layout), element (i,j) at A[j*lda + i].
+ *   - Unless a function name ends in _host, pointers to matrix/vector data are CUDA DEVICE pointers
+ *     on the current device; host arrays are marked "host".
+ *   - Work is enqueued on opt->stream (a cudaStream_t; NULL = the legacy default stream).  Calls are
+ *     BLOCKING by default (they return after completion so the hlq_get_* getters are valid).
+ *   - Return value: 0 = OK; -i = argument i invalid (LAPACK style); HLQ_ERR_* (< -99) = CUDA /
+ *     out-of-memory errors; positive HLQ_ST_* = informational, the factorization completed.
+ *   - Thread-compatible: one handle per host thread.  No exceptions cross the ABI.
+ */
+#ifndef HLQ_H
+#define HLQ_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* criteria (Eqs. 2-4) */
+enum { HLQ_CRIT_MAX = 0, HLQ_CRIT_SUM = 1, HLQ_CRIT_MUMPS = 2 };
+/* decision of a step (Alg. 1 "Perform an LU step" / "Perform a QR step") */
+enum { HLQ_DEC_LU = 0, HLQ_DEC_QR = 1 };
+/* QR elimination tree (Alg. 3 + HQR trees P:358-364) */
+enum { HLQ_TREE_GREEDY = 0 };
+
+/* error / status codes */
+enum {
+  HLQ_OK = 0,
+  HLQ_ST_NONFINITE = 1,         /* Inf/NaN met (criterion inputs or factors); growth = +inf     */
+  HLQ_ST_SINGULAR = 2,          /* exact zero on the final U/R diagonal; hlq_solve refuses       */
+  HLQ_ST_ZERO_PIVOT_FORCED = 3, /* a forced LU step met an exact zero pivot in GETRF             */
+  HLQ_ERR_CUDA = -100,
+  HLQ_ERR_NCCL = -101,
+  HLQ_ERR_NOMEM = -102,
+  HLQ_ERR_STATE = -103          /* handle not in a state that allows the call                   */
+};
+
+/* per-step flag bits returned by hlq_get_step_flags */
+enum {
+  HLQ_FLAG_ZERO_PIVOT = 1,  /* exact zero pivot in the speculative GETRF (ledger 7)              */
+  HLQ_FLAG_NEAR_TIE = 2,    /* |own margin| < tie_rel_tol                                        */
+  HLQ_FLAG_FORCED = 4,      /* decision taken verbatim from opt.forced                           */
+  HLQ_FLAG_HINTED = 8,      /* near tie resolved with opt.ref_dec (the oracle's decision)        */
+  HLQ_FLAG_NONFINITE = 16   /* NaN among the criterion inputs: QR                                */
+};
+
+typedef struct hlq_factors_s* hlq_factors_t; /* opaque; owned by the library */
+
+typedef struct {
+  int32_t struct_size;       /* = sizeof(hlq_options) (ABI versioning)                          */
+  int64_t lda;               /* leading dimension of A (0 -> N)                                  */
+  int32_t ib;                /* inner block of the stored Householder T factors (0 -> 32)        */
+  int32_t tree_domains;      /* D: QR-tree domains = tile rows mod D (0 -> 1 on one GPU)         */
+  int32_t tree;              /* HLQ_TREE_GREEDY                                                  */
+  int32_t mumps_reading;     /* 0 = M1 (default, reading 1), 1 = M2                    */
+  const uint8_t* forced;     /* host, n entries or NULL: decision vector used verbatim (C3)      */
+  const uint8_t* ref_dec;    /* host, n entries or NULL: reference (oracle) decisions            */
+  const double* ref_margin;  /* host, n entries or NULL: reference margins                       */
+  double tie_rel_tol;        /* 0 -> 1e-10: step k takes ref_dec[k] iff |own margin| or
+                                |ref_margin[k]| < tol (BASELINE parity rule)                     */
+  int32_t track_growth;      /* 1 (default): compute the tile-norm growth factor     */
+  int32_t blocking;          /* 1 (default): synchronise opt.stream before returning             */
+  void* stream;              /* cudaStream_t                                                     */
+} hlq_options;
+
+typedef struct {
+  int64_t N;
+  int32_t nb, n, ib, D;
+  int32_t qr_steps;          /* number of QR steps                                               */
+  int32_t near_ties;         /* steps with |margin| < tie_rel_tol                                */
+  int32_t hinted;            /* near ties resolved by ref_dec                                    */
+  int32_t status;            /* HLQ_OK or HLQ_ST_*                                               */
+  double growth;             /* max_k max_{i,j>=k} ||S^(k)_ij||_1 / max ||A_ij||_1 (valid extents) */
+  double fake_flops;         /* 2/3 N^3                                                  */
+  double true_flops;         /* Table I summed with the actual decisions             */
+} hlq_info;
+
+/* Fill *opt with the defaults above.  Returns 0. */
+int hlq_default_options(hlq_options* opt);
+
+/* Factor A in place (north_star: hlq_factor(A, N, nb, criterion, alpha)).
+ *   A      device, N x N, lda = N, overwritten with the packed factors: on/above the diagonal of
+ *          every diagonal tile U_kk (LU) or R_kk (QR); tiles right of the diagonal the final rows;
+ *          below: L_ik (LU step) or the GEQRT reflectors V (strictly lower part of tile
+ *          (i,k)) plus the TT reflectors (upper triangle of tile (i,k), i>k).  The handle BORROWS A:
+ *          keep it alive and unmodified until hlq_free if hlq_solve is to be called.
+ *   N >= 1, 1 <= nb;  N need not be a multiple of nb (ragged last tile).
+ *   criterion HLQ_CRIT_*;  alpha >= 0 (0 -> every step QR, +inf -> every step LU; NaN invalid).
+ *   out    receives a new handle (free with hlq_free) even when the status is positive.
+ * Errors: -1 A NULL, -2 N, -3 nb, -4 criterion, -5 alpha, -6 options, HLQ_ERR_*. */
+int hlq_factor(double* A, int64_t N, int32_t nb, int32_t criterion, double alpha,
+               hlq_factors_t* out);
+int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double alpha,
+                  const hlq_options* opt, hlq_factors_t* out);
+
+/* x = A^-1 b with the factors of f (device vectors of N entries; x may alias b).  b is not
+ * modified unless x == b.  Stream-ordered on the factorization's stream; blocking if the
+ * factorization was.  Errors: -1 f, -2 b, -3 x, HLQ_ST_SINGULAR, HLQ_ERR_*. */
+int hlq_solve(hlq_factors_t f, const double* b, double* x);
+
+/* End-to-end convenience (the bench "e2e" path): HOST A (N x N, lda = N, not modified), host b,
+ * host x; allocates device memory, copies A and b to the device, factors, solves, copies x back.
+ * info (host, may be NULL) receives the factorization info. */
+int hlq_gesv_host(const double* A_host, const double* b_host, double* x_host, int64_t N,
+                  int32_t nb, int32_t criterion, double alpha, const hlq_options* opt,
+                  hlq_info* info);
+
+/* Getters (host output buffers). */
+int hlq_get_info(hlq_factors_t f, hlq_info* info);
+int hlq_get_decisions(hlq_factors_t f, uint8_t* dec);       /* n entries, HLQ_DEC_*          */
+int hlq_get_margins(hlq_factors_t f, double* margin);       /* n entries (NaN when forced)   */
+int hlq_get_step_flags(hlq_factors_t f, int32_t* flags);    /* n entries, HLQ_FLAG_* bits    */
+int hlq_get_growth(hlq_factors_t f, double* growth);
+int hlq_get_pivots(hlq_factors_t f, int32_t* ipiv);         /* n*nb entries: step k at k*nb, 0-based
+                                                               row within the tile (LAPACK sequential
+                                                               swaps); only LU steps are meaningful */
+/* Householder T factors of tile (i,k), i >= k, kind 0 = GEQRT, 1 = TTQRT: ib x nb, column-major
+ * (ld = ib) into host buffer T.  Errors: -2/-3 bad indices. */
+int hlq_get_T(hlq_factors_t f, int32_t i, int32_t k, int32_t kind, double* T);
+void hlq_free(hlq_factors_t f);
+const char* hlq_status_string(int code);
+
+/* Seeded counter-based generator (bit-identical to hlq_inputs):
+ * dst(r, c) = G_u(seed, idx0 + c*idx_ld + r) in [-0.5, 0.5) for r < rows, c < cols; dst device,
+ * column-major with leading dimension ld.  Used to build C5-size inputs on the device. */
+int hlq_generate_uniform(double* dst, int64_t rows, int64_t cols, int64_t ld, uint64_t seed,
+                         uint64_t idx0, int64_t idx_ld, void* stream);
+
+/* ||A x - b||_inf, ||A||_inf, ||x||_inf for the HPL3 residual on the device:
+ * A device N x N (lda), x, b device; out3 host receives the three numbers.  A is an ORIGINAL copy
+ * (not the factors).  Row sums/residuals accumulate in fixed order. */
+int hlq_residual(const double* A, int64_t N, int64_t lda, const double* x, const double* b,
+                 double* out3, void* stream);
+
+/* ABI self-description for bindings: sizeof(hlq_options), sizeof(hlq_info), version (1). */
+int hlq_abi(int32_t* sizeof_options, int32_t* sizeof_info, int32_t* version);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HLQ_H */

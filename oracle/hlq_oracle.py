@@ -376,83 +376,105 @@ def tsmqr(V2: np.ndarray, T: np.ndarray, ib: int, C1: np.ndarray, C2: np.ndarray
 # ----------------------------------------------------------------------------------------------
 # a8-a11: QR step = HQR elimination list (Alg. 3, Alg. 4), plan(k, n, D)
 # ----------------------------------------------------------------------------------------------
-def qr_plan(k: int, n: int, D: int):
-    """ledger 16: domains by (i mod D); head h_d = first row i >= k of domain d (h = k for k's own).
-    Returns (heads ascending, {head: [rows i > head of that domain ascending]}, tt_heads ascending).
-    Flat TS inside a domain onto its head, then flat TT of the other heads onto k."""
-    heads = []
-    members = {}
-    for d in range(D):
-        rows = [i for i in range(k, n) if i % D == d]
-        if rows:
-            heads.append(rows[0])
-            members[rows[0]] = rows[1:]
-    heads.sort()
-    tt_heads = [h for h in heads if h != k]
-    return heads, members, tt_heads
+def _domains(k: int, n: int, D: int):
+    """Rows k..n-1 split into domains by (i mod D) (2D block-cyclic rows), each ascending,
+    domains ordered by their first row."""
+    doms = [[i for i in range(k, n) if i % D == d] for d in range(D)]
+    doms = [dm for dm in doms if dm]
+    doms.sort(key=lambda dm: dm[0])
+    return doms
+
+
+def _halving_levels(rows):
+    """Greedy halving tree on an ordered list of live rows: with r live rows, the bottom floor(r/2)
+    are eliminated (TT) by the top ones, row rows[t] killing rows[h+t], h = ceil(r/2); repeat."""
+    levels = []
+    live = list(rows)
+    while len(live) > 1:
+        r = len(live)
+        h = (r + 1) // 2
+        levels.append([(live[t], live[h + t]) for t in range(r - h)])
+        live = live[:h]
+    return levels
+
+
+def qr_plan(k: int, n: int, D: int, tree: str = "greedy"):
+    """The elimination list of a QR step (Alg. 3, HQR trees P:358-364, ledger 16).
+
+    Returns (geqrt_rows, ts_list, tt_levels):
+      geqrt_rows: rows whose tile (i,k) is factored by GEQRT (+ UNMQR on row i),
+      ts_list:    ordered (eliminator, i) TSQRT/TSMQR eliminations (Alg. 4a),
+      tt_levels:  list of levels, each a list of disjoint (eliminator, i) TTQRT/TTMQR pairs (Alg. 4b).
+    tree="greedy" (default, the paper's intra-node tree P:683-688): every tile is triangularised
+      (GEQRT) and the rows of each domain are merged by the halving tree; the domain heads are then
+      merged by the same halving tree (the inter-domain level).  Critical path O(log m).
+    tree="flat": flat TS inside each domain onto its head, then flat TT of the heads onto k.
+    """
+    doms = _domains(k, n, D)
+    heads = [dm[0] for dm in doms]
+    if tree == "flat":
+        ts_list = [(dm[0], i) for dm in doms for i in dm[1:]]
+        tt_levels = [[(k, h)] for h in sorted(heads) if h != k]
+        return sorted(heads), ts_list, tt_levels
+    if tree != "greedy":
+        raise ValueError(tree)
+    per_dom = [_halving_levels(dm) for dm in doms]
+    depth = max((len(lv) for lv in per_dom), default=0)
+    tt_levels = []
+    for l in range(depth):
+        lvl = []
+        for lv in per_dom:
+            if l < len(lv):
+                lvl.extend(lv[l])
+        tt_levels.append(lvl)
+    tt_levels.extend(_halving_levels(sorted(heads)))
+    return list(range(k, n)), [], tt_levels
 
 
 @dataclass
 class QRStepData:
-    T_geqrt: dict = field(default_factory=dict)  # head -> T (ib x b)
-    T_ts: dict = field(default_factory=dict)     # i -> T
-    T_tt: dict = field(default_factory=dict)     # head -> T
+    T_geqrt: dict = field(default_factory=dict)  # row i -> T (ib x b) of GEQRT(A_ik)
+    T_ts: dict = field(default_factory=dict)     # row i -> T of TSQRT(A_e,k ; A_ik)
+    T_tt: dict = field(default_factory=dict)     # row i -> T of TTQRT(A_e,k ; A_ik)
 
 
-def qr_step(A: np.ndarray, N: int, nb: int, k: int, D: int, ib: int) -> QRStepData:
+def qr_step(A: np.ndarray, N: int, nb: int, k: int, D: int, ib: int,
+            tree: str = "greedy") -> QRStepData:
     n = ntiles(N, nb)
     ck = tsl(N, nb, k)
     right = slice(ck.stop, N)
     data = QRStepData()
-    heads, members, tt_heads = qr_plan(k, n, D)
-    # GEQRT + UNMQR on every head (Alg. 4a lines 1, 4; Alg. 4b lines 1-2, 4-5)
-    for h in heads:
+    geqrt_rows, ts_list, tt_levels = qr_plan(k, n, D, tree)
+    # GEQRT + UNMQR (Alg. 4a lines 1, 4; Alg. 4b lines 1-2, 4-5); rows are independent
+    for h in geqrt_rows:
         rh = tsl(N, nb, h)
         tile = A[rh, ck]
-        T = geqrt(tile, ib)
-        A[rh, ck] = tile
-        data.T_geqrt[h] = T
+        data.T_geqrt[h] = geqrt(tile, ib)
         if right.start < N:
-            C = A[rh, right]
-            unmqr(tile, T, ib, C)
-            A[rh, right] = C
-    # TS chains (Alg. 4a lines 2, 5) in plan order
-    for h in heads:
-        rh = tsl(N, nb, h)
-        for i in members[h]:
-            ri = tsl(N, nb, i)
-            R = A[rh, ck]
-            Rv = np.triu(R)
-            A2 = A[ri, ck]
-            T = tsqrt(Rv, A2, ib)
-            R[np.triu_indices_from(R)] = Rv[np.triu_indices_from(Rv)]
-            A[rh, ck] = R
-            A[ri, ck] = A2
-            data.T_ts[i] = T
-            if right.start < N:
-                C1 = A[rh, right]
-                C2 = A[ri, right]
-                tsmqr(A2, T, ib, C1, C2)
-                A[rh, right] = C1
-                A[ri, right] = C2
-    # TT merges of the other heads onto k (Alg. 4b lines 6-9)
-    rk = tsl(N, nb, k)
-    for h in tt_heads:
-        rh = tsl(N, nb, h)
-        R = A[rk, ck]
+            unmqr(tile, data.T_geqrt[h], ib, A[rh, right])
+    # TS eliminations in plan order (Alg. 4a lines 2, 5)
+    for e, i in ts_list:
+        re_, ri = tsl(N, nb, e), tsl(N, nb, i)
+        R = A[re_, ck]
         Rv = np.triu(R)
-        Ht = A[rh, ck]
-        T = tsqrt(Rv, Ht, ib, tt=True)
-        R[np.triu_indices_from(R)] = Rv[np.triu_indices_from(Rv)]
-        A[rk, ck] = R
-        A[rh, ck] = Ht
-        data.T_tt[h] = T
+        A2 = A[ri, ck]
+        data.T_ts[i] = tsqrt(Rv, A2, ib)
+        iu = np.triu_indices(R.shape[0], m=R.shape[1])
+        R[iu] = Rv[iu]
         if right.start < N:
-            C1 = A[rk, right]
-            C2 = A[rh, right]
-            tsmqr(Ht, T, ib, C1, C2, tt=True)
-            A[rk, right] = C1
-            A[rh, right] = C2
+            tsmqr(A2, data.T_ts[i], ib, A[re_, right], A[ri, right])
+    # TT eliminations level by level (Alg. 4b lines 6-9); pairs inside a level are disjoint
+    for level in tt_levels:
+        for e, i in level:
+            re_, ri = tsl(N, nb, e), tsl(N, nb, i)
+            R = A[re_, ck]
+            Rv = np.triu(R)
+            Ht = A[ri, ck]
+            data.T_tt[i] = tsqrt(Rv, Ht, ib, tt=True)
+            iu = np.triu_indices(R.shape[0], m=R.shape[1])
+            R[iu] = Rv[iu]
+            if right.start < N:
+                tsmqr(Ht, data.T_tt[i], ib, A[re_, right], A[ri, right], tt=True)
     return data
 
 
@@ -478,6 +500,7 @@ class Factors:
     n: int
     ib: int
     D: int
+    tree: str
     dec: np.ndarray
     margin: np.ndarray
     near_tie: np.ndarray
@@ -490,7 +513,8 @@ class Factors:
 
 def hybrid_factor(A_in: np.ndarray, nb: int, crit: int = CRIT_MAX, alpha: float = 1.0, D: int = 1,
                   ib: int = 32, mumps_reading: int = 0, forced=None, track_growth: bool = True,
-                  tie_tol: float = 1e-10, variant: int = 0, on_step=None) -> Factors:
+                  tie_tol: float = 1e-10, variant: int = 0, on_step=None,
+                  tree: str = "greedy") -> Factors:
     """Alg. 1: for each step, speculative tile LU, criterion, LU or QR step.
 
     forced: decision vector used verbatim (C3); variant=1 uses the reversed-chunk GEMM (noise floor).
@@ -550,7 +574,7 @@ def hybrid_factor(A_in: np.ndarray, nb: int, crit: int = CRIT_MAX, alpha: float 
                 lu_step_update_variant(A, N, nb, k)
             ipivs[k] = ipiv
         else:
-            qrs[k] = qr_step(A, N, nb, k, D, ib)
+            qrs[k] = qr_step(A, N, nb, k, D, ib, tree)
         if track_growth and k + 1 < n:
             g = max(g, max_tile_norm(A, N, nb, k + 1))
         if on_step is not None:
@@ -567,7 +591,7 @@ def hybrid_factor(A_in: np.ndarray, nb: int, crit: int = CRIT_MAX, alpha: float 
     growth = (g / g0) if (track_growth and g0 > 0) else float("nan")
     if track_growth and not np.isfinite(g):
         growth = math.inf
-    return Factors(A, N, nb, n, ib, D, dec, margin, near_tie, ipivs, qrs, growth, status, stats)
+    return Factors(A, N, nb, n, ib, D, tree, dec, margin, near_tie, ipivs, qrs, growth, status, stats)
 
 
 # ----------------------------------------------------------------------------------------------
@@ -596,24 +620,17 @@ def apply_transforms(f: Factors, x: np.ndarray) -> np.ndarray:
                 x[k1:N, :] -= A[k1:N, k0:k1] @ x[rk, :]
         else:
             d = f.qr[k]
-            heads, members, tt_heads = qr_plan(k, n, f.D)
-            for h in heads:
+            geqrt_rows, ts_list, tt_levels = qr_plan(k, n, f.D, f.tree)
+            for h in geqrt_rows:
                 rh = tsl(N, nb, h)
-                xh = x[rh, :].copy()
-                unmqr(A[rh, rk], d.T_geqrt[h], ib, xh)
-                x[rh, :] = xh
-            for h in heads:
-                rh = tsl(N, nb, h)
-                for i in members[h]:
-                    ri = tsl(N, nb, i)
-                    c1, c2 = x[rh, :].copy(), x[ri, :].copy()
-                    tsmqr(A[ri, rk], d.T_ts[i], ib, c1, c2)
-                    x[rh, :], x[ri, :] = c1, c2
-            for h in tt_heads:
-                rh = tsl(N, nb, h)
-                c1, c2 = x[rk, :].copy(), x[rh, :].copy()
-                tsmqr(A[rh, rk], d.T_tt[h], ib, c1, c2, tt=True)
-                x[rk, :], x[rh, :] = c1, c2
+                unmqr(A[rh, rk], d.T_geqrt[h], ib, x[rh, :])
+            for e, i in ts_list:
+                re_, ri = tsl(N, nb, e), tsl(N, nb, i)
+                tsmqr(A[ri, rk], d.T_ts[i], ib, x[re_, :], x[ri, :])
+            for level in tt_levels:
+                for e, i in level:
+                    re_, ri = tsl(N, nb, e), tsl(N, nb, i)
+                    tsmqr(A[ri, rk], d.T_tt[i], ib, x[re_, :], x[ri, :], tt=True)
     return x[:, 0] if vec else x
 
 

@@ -1,0 +1,255 @@
+"""ctypes binding of include/hlq.h (marshalling only: every step of the path runs in libhlq.so).
+
+Device buffers are torch CUDA float64 tensors used purely as memory: an N x N column-major matrix
+is a contiguous tensor whose storage holds A in LAPACK order (see `to_colmajor`).  Streams are torch
+CUDA streams (the current stream by default).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "libhlq.so")
+
+CRIT_MAX, CRIT_SUM, CRIT_MUMPS = 0, 1, 2
+DEC_LU, DEC_QR = 0, 1
+FLAG_ZERO_PIVOT, FLAG_NEAR_TIE, FLAG_FORCED, FLAG_HINTED, FLAG_NONFINITE = 1, 2, 4, 8, 16
+
+
+class HlqError(RuntimeError):
+    pass
+
+
+class HlqOptions(C.Structure):
+    _fields_ = [("struct_size", C.c_int32), ("lda", C.c_int64), ("ib", C.c_int32),
+                ("tree_domains", C.c_int32), ("tree", C.c_int32), ("mumps_reading", C.c_int32),
+                ("forced", C.c_void_p), ("ref_dec", C.c_void_p), ("ref_margin", C.c_void_p),
+                ("tie_rel_tol", C.c_double), ("track_growth", C.c_int32), ("blocking", C.c_int32),
+                ("stream", C.c_void_p)]
+
+
+class HlqInfo(C.Structure):
+    _fields_ = [("N", C.c_int64), ("nb", C.c_int32), ("n", C.c_int32), ("ib", C.c_int32),
+                ("D", C.c_int32), ("qr_steps", C.c_int32), ("near_ties", C.c_int32),
+                ("hinted", C.c_int32), ("status", C.c_int32), ("growth", C.c_double),
+                ("fake_flops", C.c_double), ("true_flops", C.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+def _load():
+    if not os.path.exists(lib_path):
+        raise HlqError(f"libhlq.so not built at {lib_path}: run `python -c 'import __graft_entry__ as g;"
+                       f" g.build()'` (no CPU fallback exists)")
+    L = C.CDLL(lib_path)
+    P, I32, I64, D, U64 = C.c_void_p, C.c_int32, C.c_int64, C.c_double, C.c_uint64
+    sig = {
+        "hlq_abi": ([P, P, P], I32),
+        "hlq_default_options": ([P], I32),
+        "hlq_factor": ([P, I64, I32, I32, D, P], I32),
+        "hlq_factor_ex": ([P, I64, I32, I32, D, P, P], I32),
+        "hlq_solve": ([P, P, P], I32),
+        "hlq_gesv_host": ([P, P, P, I64, I32, I32, D, P, P], I32),
+        "hlq_get_info": ([P, P], I32),
+        "hlq_get_decisions": ([P, P], I32),
+        "hlq_get_margins": ([P, P], I32),
+        "hlq_get_step_flags": ([P, P], I32),
+        "hlq_get_growth": ([P, P], I32),
+        "hlq_get_pivots": ([P, P], I32),
+        "hlq_get_T": ([P, I32, I32, I32, P], I32),
+        "hlq_free": ([P], None),
+        "hlq_status_string": ([I32], C.c_char_p),
+        "hlq_generate_uniform": ([P, I64, I64, I64, U64, U64, I64, P], I32),
+        "hlq_residual": ([P, I64, I64, P, P, P, P], I32),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    so, si, ver = C.c_int32(), C.c_int32(), C.c_int32()
+    L.hlq_abi(C.byref(so), C.byref(si), C.byref(ver))
+    if so.value != C.sizeof(HlqOptions) or si.value != C.sizeof(HlqInfo):
+        raise HlqError(f"ABI mismatch: C sizeof(options/info) = {so.value}/{si.value}, "
+                       f"binding {C.sizeof(HlqOptions)}/{C.sizeof(HlqInfo)}")
+    return L
+
+
+lib = _load()
+
+
+def _check(rc, what):
+    if rc < 0:
+        raise HlqError(f"{what} failed: {rc} ({lib.hlq_status_string(rc).decode()})")
+    return rc
+
+
+def hlq_abi():
+    so, si, ver = C.c_int32(), C.c_int32(), C.c_int32()
+    lib.hlq_abi(C.byref(so), C.byref(si), C.byref(ver))
+    return so.value, si.value, ver.value
+
+
+def hlq_default_options() -> HlqOptions:
+    o = HlqOptions()
+    lib.hlq_default_options(C.byref(o))
+    return o
+
+
+def _stream_ptr(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _dptr(t):
+    return C.c_void_p(t.data_ptr())
+
+
+# ------------------------------------------------------------------- layout helpers (plumbing)
+def to_colmajor(A_host: np.ndarray, device="cuda"):
+    """numpy (N x N) -> torch CUDA tensor whose storage is A in column-major (LAPACK) order."""
+    import torch
+    AT = np.ascontiguousarray(np.asarray(A_host, dtype=np.float64).T)
+    return torch.from_numpy(AT).to(device)
+
+
+def from_colmajor(t) -> np.ndarray:
+    """inverse of to_colmajor (device tensor -> numpy N x N)."""
+    return t.detach().cpu().numpy().T
+
+
+class Factors:
+    """Owns an hlq_factors_t handle (the factorization borrows the device matrix `A`)."""
+
+    def __init__(self, handle, A, status, keep=()):
+        self.handle = C.c_void_p(handle)
+        self.A = A
+        self.status = status
+        self._keep = keep
+
+    def __del__(self):
+        self.free()
+
+    def free(self):
+        if getattr(self, "handle", None) and self.handle.value:
+            lib.hlq_free(self.handle)
+            self.handle = C.c_void_p(None)
+
+    def info(self) -> dict:
+        inf = HlqInfo()
+        _check(lib.hlq_get_info(self.handle, C.byref(inf)), "hlq_get_info")
+        return inf.as_dict()
+
+    @property
+    def n(self):
+        return self.info()["n"]
+
+    def decisions(self) -> np.ndarray:
+        d = np.zeros(self.n, dtype=np.uint8)
+        _check(lib.hlq_get_decisions(self.handle, d.ctypes.data_as(C.c_void_p)), "decisions")
+        return d
+
+    def margins(self) -> np.ndarray:
+        m = np.zeros(self.n, dtype=np.float64)
+        _check(lib.hlq_get_margins(self.handle, m.ctypes.data_as(C.c_void_p)), "margins")
+        return m
+
+    def step_flags(self) -> np.ndarray:
+        f = np.zeros(self.n, dtype=np.int32)
+        _check(lib.hlq_get_step_flags(self.handle, f.ctypes.data_as(C.c_void_p)), "flags")
+        return f
+
+    def growth(self) -> float:
+        g = C.c_double()
+        _check(lib.hlq_get_growth(self.handle, C.byref(g)), "growth")
+        return g.value
+
+    def pivots(self) -> np.ndarray:
+        inf = self.info()
+        p = np.zeros(inf["n"] * inf["nb"], dtype=np.int32)
+        _check(lib.hlq_get_pivots(self.handle, p.ctypes.data_as(C.c_void_p)), "pivots")
+        return p.reshape(inf["n"], inf["nb"])
+
+    def T(self, i, k, kind=0) -> np.ndarray:
+        inf = self.info()
+        t = np.zeros(inf["ib"] * inf["nb"], dtype=np.float64)
+        _check(lib.hlq_get_T(self.handle, i, k, kind, t.ctypes.data_as(C.c_void_p)), "T")
+        return t.reshape(inf["nb"], inf["ib"]).T
+
+    def solve(self, b, x=None):
+        import torch
+        if x is None:
+            x = torch.empty_like(b)
+        hlq_solve(self, b, x)
+        return x
+
+
+def hlq_factor_ex(A, N: int, nb: int, criterion: int = CRIT_MAX, alpha: float = 1.0,
+                  opt: HlqOptions | None = None, *, forced=None, ref_dec=None, ref_margin=None,
+                  stream=None, **fields) -> Factors:
+    """Factor the device matrix A (torch float64 CUDA tensor, column-major storage) in place."""
+    if opt is None:
+        opt = hlq_default_options()
+    for k, v in fields.items():
+        setattr(opt, k, v)
+    keep = []
+    if forced is not None:
+        fa = np.ascontiguousarray(forced, dtype=np.uint8)
+        keep.append(fa)
+        opt.forced = fa.ctypes.data
+    if ref_dec is not None:
+        ra = np.ascontiguousarray(ref_dec, dtype=np.uint8)
+        rm = np.ascontiguousarray(ref_margin, dtype=np.float64)
+        keep += [ra, rm]
+        opt.ref_dec = ra.ctypes.data
+        opt.ref_margin = rm.ctypes.data
+    opt.stream = _stream_ptr(stream).value
+    h = C.c_void_p()
+    rc = lib.hlq_factor_ex(_dptr(A), N, nb, criterion, float(alpha), C.byref(opt), C.byref(h))
+    if rc < 0:
+        if h.value:
+            lib.hlq_free(h)
+        _check(rc, "hlq_factor_ex")
+    return Factors(h.value, A, rc, tuple(keep))
+
+
+def hlq_factor(A, N: int, nb: int, criterion: int = CRIT_MAX, alpha: float = 1.0) -> Factors:
+    return hlq_factor_ex(A, N, nb, criterion, alpha)
+
+
+def hlq_solve(f: Factors, b, x):
+    return _check(lib.hlq_solve(f.handle, _dptr(b), _dptr(x)), "hlq_solve")
+
+
+def hlq_gesv_host(A_host: np.ndarray, b_host: np.ndarray, x_host: np.ndarray, N: int, nb: int,
+                  criterion: int = CRIT_MAX, alpha: float = 1.0, opt: HlqOptions | None = None,
+                  stream=None):
+    """Host buffers (A column-major, i.e. a Fortran-ordered numpy array or its raw storage)."""
+    if opt is None:
+        opt = hlq_default_options()
+    opt.stream = _stream_ptr(stream).value
+    info = HlqInfo()
+    rc = lib.hlq_gesv_host(C.c_void_p(A_host.ctypes.data), C.c_void_p(b_host.ctypes.data),
+                           C.c_void_p(x_host.ctypes.data), N, nb, criterion, float(alpha),
+                           C.byref(opt), C.byref(info))
+    _check(rc, "hlq_gesv_host")
+    return rc, info.as_dict()
+
+
+def hlq_generate_uniform(dst, rows, cols, ld, seed, idx0, idx_ld, stream=None):
+    _check(lib.hlq_generate_uniform(_dptr(dst), rows, cols, ld, seed, idx0, idx_ld,
+                                    _stream_ptr(stream)), "hlq_generate_uniform")
+
+
+def hlq_residual(A, N, lda, x, b, stream=None):
+    out = np.zeros(3)
+    _check(lib.hlq_residual(_dptr(A), N, lda, _dptr(x), _dptr(b), out.ctypes.data_as(C.c_void_p),
+                            _stream_ptr(stream)), "hlq_residual")
+    r, an, xn = out
+    return {"resid_inf": r, "A_inf": an, "x_inf": xn,
+            "hpl3": r / (an * xn * 2.0 ** -53 * N) if an * xn > 0 else math.inf}

@@ -1,0 +1,541 @@
+// C ABI of libhlq (include/hlq.h): the handle, the step scheduler of Alg. 1 and
+// the solve.  The host only enqueues work: per step k it launches the criterion kernels, the decide
+// kernel (which writes d_k to device memory) and BOTH branches' kernels, each predicated on d_k
+// (a kernel of the branch not taken exits at its first instruction).  Decisions known on the host
+// (a forced vector, alpha = 0) skip the other branch's launches.  No host round trip inside the
+// factorization: this replaces the paper's Propagate / selection tasks.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <new>
+#include <vector>
+
+#include "hlq_internal.cuh"
+
+namespace hlq {
+void launch_tri_inv(Geo g, int k, const DevWork& w, double* Li, double* Ui, cudaStream_t st);
+void launch_qr_apply(const double* A, Geo g, int k, int ib, const double* Tg, const double* Ttt,
+                     const int2* const* level_pairs, const int* level_count, int nlevels,
+                     double* base, int64_t ldc, int64_t ncols, const uint8_t* dec,
+                     cudaStream_t st);
+void launch_final_scan(const double* A, int64_t N, int64_t lda, int* flag, cudaStream_t st);
+}  // namespace hlq
+
+using namespace hlq;
+
+// ---------------------------------------------------------------------------------------------
+// device-memory cache: big workspaces are reused across calls (like a cuBLAS workspace), so a
+// repeated factorization of the same size does not pay cudaMalloc/cudaFree.
+namespace {
+struct CacheSlot {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+CacheSlot g_cache[4];
+
+void* cache_get(int slot, size_t bytes) {
+  CacheSlot& c = g_cache[slot];
+  if (c.p && c.bytes >= bytes) {
+    void* p = c.p;
+    c.p = nullptr;
+    return p;
+  }
+  if (c.p) {
+    cudaFree(c.p);
+    c.p = nullptr;
+    c.bytes = 0;
+  }
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+void cache_put(int slot, void* p, size_t bytes) {
+  CacheSlot& c = g_cache[slot];
+  if (!p) return;
+  if (c.p) {
+    if (c.bytes >= bytes) {
+      cudaFree(p);
+      return;
+    }
+    cudaFree(c.p);
+  }
+  c.p = p;
+  c.bytes = bytes;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+}  // namespace
+
+struct hlq_factors_s {
+  double* A = nullptr;
+  Geo g{};
+  int ib = 32, D = 1, crit = 0;
+  double alpha = 1.0;
+  cudaStream_t st = nullptr;
+  bool blocking = true;
+  DevWork w{};
+  void* ws_block = nullptr;
+  size_t ws_bytes = 0;
+  // greedy-tree plan: per step k, levels l: device pointer + count
+  std::vector<std::vector<const int2*>> lvl_ptr;
+  std::vector<std::vector<int>> lvl_cnt;
+  // host results
+  std::vector<uint8_t> dec;
+  std::vector<double> margin;
+  std::vector<int> flags;
+  std::vector<double> gstep;
+  int status = 0;
+  double growth = 0.0;
+  bool track_growth = true;
+};
+
+static int cuda_err(cudaError_t e) {
+  if (e == cudaSuccess) return 0;
+  fprintf(stderr, "[hlq] CUDA error: %s\n", cudaGetErrorString(e));
+  return e == cudaErrorMemoryAllocation ? HLQ_ERR_NOMEM : HLQ_ERR_CUDA;
+}
+
+// greedy halving tree (reading 16): rows of each domain (i mod D), then the domain heads
+static void plan_levels(int k, int n, int D, std::vector<std::vector<int2>>& levels) {
+  levels.clear();
+  std::vector<std::vector<int>> doms;
+  for (int d = 0; d < D; ++d) {
+    std::vector<int> rows;
+    for (int i = k; i < n; ++i)
+      if (i % D == d) rows.push_back(i);
+    if (!rows.empty()) doms.push_back(rows);
+  }
+  auto halving = [](std::vector<int> live, std::vector<std::vector<int2>>& out) {
+    while (live.size() > 1) {
+      size_t r = live.size(), h = (r + 1) / 2;
+      std::vector<int2> lv;
+      for (size_t t = 0; t < r - h; ++t) lv.push_back(make_int2(live[t], live[h + t]));
+      out.push_back(lv);
+      live.resize(h);
+    }
+  };
+  std::vector<std::vector<std::vector<int2>>> per(doms.size());
+  size_t depth = 0;
+  std::vector<int> heads;
+  for (size_t d = 0; d < doms.size(); ++d) {
+    halving(doms[d], per[d]);
+    depth = per[d].size() > depth ? per[d].size() : depth;
+    heads.push_back(doms[d][0]);
+  }
+  for (size_t l = 0; l < depth; ++l) {
+    std::vector<int2> lv;
+    for (size_t d = 0; d < per.size(); ++d)
+      if (l < per[d].size()) lv.insert(lv.end(), per[d][l].begin(), per[d][l].end());
+    levels.push_back(lv);
+  }
+  std::sort(heads.begin(), heads.end());
+  halving(heads, levels);
+}
+
+extern "C" {
+
+int hlq_abi(int32_t* so, int32_t* si, int32_t* ver) {
+  if (so) *so = (int32_t)sizeof(hlq_options);
+  if (si) *si = (int32_t)sizeof(hlq_info);
+  if (ver) *ver = 1;
+  return 0;
+}
+
+int hlq_default_options(hlq_options* opt) {
+  if (!opt) return -1;
+  memset(opt, 0, sizeof(*opt));
+  opt->struct_size = (int32_t)sizeof(hlq_options);
+  opt->ib = 32;
+  opt->tree_domains = 1;
+  opt->tree = HLQ_TREE_GREEDY;
+  opt->tie_rel_tol = 1e-10;
+  opt->track_growth = 1;
+  opt->blocking = 1;
+  return 0;
+}
+
+const char* hlq_status_string(int code) {
+  switch (code) {
+    case HLQ_OK: return "ok";
+    case HLQ_ST_NONFINITE: return "non-finite values encountered";
+    case HLQ_ST_SINGULAR: return "exact zero on the final U/R diagonal";
+    case HLQ_ST_ZERO_PIVOT_FORCED: return "forced LU step met an exact zero pivot";
+    case HLQ_ERR_CUDA: return "CUDA error";
+    case HLQ_ERR_NCCL: return "NCCL error";
+    case HLQ_ERR_NOMEM: return "out of device memory";
+    case HLQ_ERR_STATE: return "invalid handle state";
+    default: return code < 0 ? "invalid argument" : "unknown";
+  }
+}
+
+int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double alpha,
+                  const hlq_options* opt_in, hlq_factors_t* out) {
+  if (!out) return -7;
+  *out = nullptr;
+  if (!A) return -1;
+  if (N <= 0) return -2;
+  if (nb <= 0 || nb > 512) return -3;
+  if (criterion < 0 || criterion > 2) return -4;
+  if (!(alpha >= 0.0)) return -5;  // rejects NaN and negatives
+  hlq_options opt;
+  hlq_default_options(&opt);
+  if (opt_in) {
+    if (opt_in->struct_size != (int32_t)sizeof(hlq_options)) return -6;
+    opt = *opt_in;
+  }
+  if (opt.ib == 0) opt.ib = 32;
+  if (opt.tree_domains == 0) opt.tree_domains = 1;
+  if (opt.tie_rel_tol == 0.0) opt.tie_rel_tol = 1e-10;
+  if (opt.ib < 1 || opt.ib > 32 || opt.tree_domains < 1 || opt.tree != HLQ_TREE_GREEDY ||
+      opt.mumps_reading < 0 || opt.mumps_reading > 1)
+    return -6;
+  int64_t lda = opt.lda ? opt.lda : N;
+  if (lda < N) return -6;
+  if (nb > N) nb = (int32_t)N;
+
+  hlq_factors_t f = new (std::nothrow) hlq_factors_s();
+  if (!f) return HLQ_ERR_NOMEM;
+  *out = f;
+  f->A = A;
+  f->g.N = N;
+  f->g.lda = lda;
+  f->g.nb = nb;
+  f->g.n = (int)((N + nb - 1) / nb);
+  f->ib = opt.ib;
+  f->D = opt.tree_domains;
+  f->crit = criterion;
+  f->alpha = alpha;
+  f->st = (cudaStream_t)opt.stream;
+  f->blocking = opt.blocking != 0;
+  f->track_growth = opt.track_growth != 0;
+  const int n = f->g.n, ib = f->ib;
+  Geo g = f->g;
+
+  // plans
+  std::vector<std::vector<std::vector<int2>>> plans(n);
+  size_t npairs = 0;
+  for (int k = 0; k < n; ++k) {
+    plan_levels(k, n, f->D, plans[k]);
+    for (auto& lv : plans[k]) npairs += lv.size();
+  }
+
+  // workspace layout (bytes, 256-aligned pieces)
+  const size_t ntri = (size_t)n * (n + 1) / 2;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += align_up(bytes ? bytes : 1, 256);
+    return o;
+  };
+  size_t oW = take(sizeof(double) * nb * nb), oIpw = take(sizeof(int) * nb),
+         oIp = take(sizeof(int) * (size_t)n * nb), oTg = take(sizeof(double) * ntri * ib * nb),
+         oTt = take(sizeof(double) * ntri * ib * nb), oS = take(sizeof(double) * n),
+         oLm = take(sizeof(double) * nb), oAm = take(sizeof(double) * nb), oInv = take(8),
+         oZp = take(sizeof(int)), oDec = take(n), oMg = take(sizeof(double) * n),
+         oFl = take(sizeof(int) * n), oSt = take(sizeof(int) * 4), oFo = take(n), oRd = take(n),
+         oRm = take(sizeof(double) * n), oGs = take(sizeof(double) * (n + 1)),
+         oPr = take(sizeof(int2) * (npairs + 1)),
+         oSc = take(sizeof(double) * ((size_t)2 * nb * nb + align_up(nb, 64) + (size_t)N * nb + 64));
+  f->ws_bytes = off;
+  f->ws_block = cache_get(0, off);
+  if (!f->ws_block) return HLQ_ERR_NOMEM;
+  char* base = (char*)f->ws_block;
+  DevWork& w = f->w;
+  w.W = (double*)(base + oW);
+  w.ipiv_ws = (int*)(base + oIpw);
+  w.ipiv = (int*)(base + oIp);
+  w.Tg = (double*)(base + oTg);
+  w.Ttt = (double*)(base + oTt);
+  w.s = (double*)(base + oS);
+  w.local_max = (double*)(base + oLm);
+  w.away_max = (double*)(base + oAm);
+  w.inv_norm = (double*)(base + oInv);
+  w.zp = (int*)(base + oZp);
+  w.dec = (uint8_t*)(base + oDec);
+  w.margin = (double*)(base + oMg);
+  w.flags = (int*)(base + oFl);
+  w.status = (int*)(base + oSt);
+  w.forced = opt.forced ? (uint8_t*)(base + oFo) : nullptr;
+  w.ref_dec = (opt.ref_dec && opt.ref_margin) ? (uint8_t*)(base + oRd) : nullptr;
+  w.ref_margin = (opt.ref_dec && opt.ref_margin) ? (double*)(base + oRm) : nullptr;
+  w.gstep = (double*)(base + oGs);
+  w.pairs = (int2*)(base + oPr);
+  w.scratch = (double*)(base + oSc);
+  cudaStream_t st = f->st;
+  int rc = 0;
+
+  // uploads (pairs flattened per step / level)
+  std::vector<int2> flat;
+  flat.reserve(npairs);
+  f->lvl_ptr.assign(n, {});
+  f->lvl_cnt.assign(n, {});
+  for (int k = 0; k < n; ++k)
+    for (auto& lv : plans[k]) {
+      f->lvl_ptr[k].push_back(w.pairs + flat.size());
+      f->lvl_cnt[k].push_back((int)lv.size());
+      flat.insert(flat.end(), lv.begin(), lv.end());
+    }
+  if (!flat.empty() &&
+      (rc = cuda_err(cudaMemcpyAsync(w.pairs, flat.data(), sizeof(int2) * flat.size(),
+                                     cudaMemcpyHostToDevice, st))))
+    return rc;
+  if (w.forced &&
+      (rc = cuda_err(cudaMemcpyAsync(w.forced, opt.forced, n, cudaMemcpyHostToDevice, st))))
+    return rc;
+  if (w.ref_dec) {
+    if ((rc = cuda_err(cudaMemcpyAsync(w.ref_dec, opt.ref_dec, n, cudaMemcpyHostToDevice, st))))
+      return rc;
+    if ((rc = cuda_err(cudaMemcpyAsync(w.ref_margin, opt.ref_margin, sizeof(double) * n,
+                                       cudaMemcpyHostToDevice, st))))
+      return rc;
+  }
+  cudaMemsetAsync(w.status, 0, sizeof(int) * 4, st);
+  cudaMemsetAsync(w.gstep, 0, sizeof(double) * (n + 1), st);
+  cudaMemsetAsync(w.ipiv, 0, sizeof(int) * (size_t)n * nb, st);
+  if (f->track_growth) launch_tile_norm_max(A, g, 0, w.gstep, st);
+
+  const bool alpha_inf = isinf(alpha);
+  for (int k = 0; k < n; ++k) {
+    int known = -1;  // decision known on the host?
+    if (opt.forced)
+      known = opt.forced[k] ? HLQ_DEC_QR : HLQ_DEC_LU;
+    else if (alpha == 0.0)
+      known = HLQ_DEC_QR;
+    const bool criterion_needed = !opt.forced && alpha > 0.0 && !alpha_inf;
+    if (known != HLQ_DEC_QR) {
+      if (criterion_needed) launch_panel_stats(A, g, k, w, st);
+      launch_getrf(A, g, k, w, true, st);
+      double* Li = w.scratch;
+      double* Ui = w.scratch + (size_t)nb * nb;
+      launch_tri_inv(g, k, w, Li, Ui, st);
+      if (criterion_needed && criterion != HLQ_CRIT_MUMPS) launch_invnorm(g, k, w, st);
+    } else {
+      cudaMemsetAsync(w.zp, 0, sizeof(int), st);
+    }
+    launch_decide(g, k, criterion, alpha, opt.mumps_reading, opt.tie_rel_tol, opt.forced != nullptr,
+                  w.ref_dec != nullptr, w, st);
+    if (known != HLQ_DEC_QR) launch_lu_step(A, g, k, w, true, st);
+    if (known != HLQ_DEC_LU)
+      launch_qr_step(A, g, k, ib, f->lvl_ptr[k].data(), f->lvl_cnt[k].data(),
+                     (int)f->lvl_cnt[k].size(), w, true, st);
+    if (f->track_growth && k + 1 < n) launch_tile_norm_max(A, g, k + 1, w.gstep + k + 1, st);
+  }
+  int* scan = w.status + 2;
+  launch_final_scan(A, N, lda, scan, st);
+  if ((rc = cuda_err(cudaGetLastError()))) return rc;
+
+  f->dec.resize(n);
+  f->margin.resize(n);
+  f->flags.resize(n);
+  f->gstep.resize(n + 1);
+  int stat[4];
+  cudaMemcpyAsync(f->dec.data(), w.dec, n, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(f->margin.data(), w.margin, sizeof(double) * n, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(f->flags.data(), w.flags, sizeof(int) * n, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(f->gstep.data(), w.gstep, sizeof(double) * (n + 1), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(stat, w.status, sizeof(int) * 4, cudaMemcpyDeviceToHost, st);
+  if ((rc = cuda_err(cudaStreamSynchronize(st)))) return rc;
+  // status priority: non-finite > zero pivot in a forced LU step > singular
+  if (stat[0] || stat[2])
+    f->status = HLQ_ST_NONFINITE;
+  else if (stat[1])
+    f->status = HLQ_ST_ZERO_PIVOT_FORCED;
+  else if (stat[3])
+    f->status = HLQ_ST_SINGULAR;
+  else
+    f->status = HLQ_OK;
+  if (f->track_growth) {
+    double gmax = f->gstep[0];
+    bool nonfinite = false;
+    for (int k = 0; k <= n; ++k) {
+      double v = f->gstep[k];
+      if (v != v || isinf(v)) nonfinite = true;
+      if (v > gmax) gmax = v;
+    }
+    f->growth = nonfinite ? INFINITY : (f->gstep[0] > 0 ? gmax / f->gstep[0] : NAN);
+  } else {
+    f->growth = NAN;
+  }
+  return f->status;
+}
+
+int hlq_factor(double* A, int64_t N, int32_t nb, int32_t criterion, double alpha,
+               hlq_factors_t* out) {
+  return hlq_factor_ex(A, N, nb, criterion, alpha, nullptr, out);
+}
+
+int hlq_solve(hlq_factors_t f, const double* b, double* x) {
+  if (!f || f->dec.empty()) return -1;
+  if (!b) return -2;
+  if (!x) return -3;
+  if (f->status == HLQ_ST_SINGULAR) return HLQ_ST_SINGULAR;
+  const Geo g = f->g;
+  cudaStream_t st = f->st;
+  int rc;
+  if (x != b &&
+      (rc = cuda_err(cudaMemcpyAsync(x, b, sizeof(double) * g.N, cudaMemcpyDeviceToDevice, st))))
+    return rc;
+  for (int k = 0; k < g.n; ++k) {
+    if (f->dec[k] == HLQ_DEC_LU)
+      launch_solve_lu_fwd(f->A, g, k, f->w.ipiv, x, st);
+    else
+      launch_qr_apply(f->A, g, k, f->ib, f->w.Tg, f->w.Ttt, f->lvl_ptr[k].data(),
+                      f->lvl_cnt[k].data(), (int)f->lvl_cnt[k].size(), x, g.N, 1, nullptr, st);
+  }
+  for (int k = g.n - 1; k >= 0; --k) launch_solve_back(f->A, g, k, x, st);
+  if ((rc = cuda_err(cudaGetLastError()))) return rc;
+  if (f->blocking && (rc = cuda_err(cudaStreamSynchronize(st)))) return rc;
+  return 0;
+}
+
+int hlq_get_info(hlq_factors_t f, hlq_info* info) {
+  if (!f || f->dec.empty()) return -1;
+  if (!info) return -2;
+  memset(info, 0, sizeof(*info));
+  const Geo g = f->g;
+  info->N = g.N;
+  info->nb = g.nb;
+  info->n = g.n;
+  info->ib = f->ib;
+  info->D = f->D;
+  info->status = f->status;
+  info->growth = f->growth;
+  double Nd = (double)g.N;
+  info->fake_flops = 2.0 / 3.0 * Nd * Nd * Nd;
+  double tf = 0.0;
+  for (int k = 0; k < g.n; ++k) {
+    double b = g.bs(k), M = (double)(g.N - g.r0(k) - g.bs(k));
+    double lu = 2.0 / 3.0 * b * b * b + 2.0 * M * b * b + 2.0 * M * M * b;  // Table I
+    tf += f->dec[k] == HLQ_DEC_QR ? 2.0 * lu : lu;
+    if (f->dec[k] == HLQ_DEC_QR) info->qr_steps++;
+    if (f->flags[k] & HLQ_FLAG_NEAR_TIE) info->near_ties++;
+    if (f->flags[k] & HLQ_FLAG_HINTED) info->hinted++;
+  }
+  info->true_flops = tf;
+  return 0;
+}
+
+int hlq_get_decisions(hlq_factors_t f, uint8_t* dec) {
+  if (!f || f->dec.empty()) return -1;
+  if (!dec) return -2;
+  memcpy(dec, f->dec.data(), f->dec.size());
+  return 0;
+}
+int hlq_get_margins(hlq_factors_t f, double* m) {
+  if (!f || f->dec.empty()) return -1;
+  if (!m) return -2;
+  memcpy(m, f->margin.data(), sizeof(double) * f->margin.size());
+  return 0;
+}
+int hlq_get_step_flags(hlq_factors_t f, int32_t* fl) {
+  if (!f || f->dec.empty()) return -1;
+  if (!fl) return -2;
+  memcpy(fl, f->flags.data(), sizeof(int) * f->flags.size());
+  return 0;
+}
+int hlq_get_growth(hlq_factors_t f, double* gr) {
+  if (!f || f->dec.empty()) return -1;
+  if (!gr) return -2;
+  *gr = f->growth;
+  return 0;
+}
+int hlq_get_pivots(hlq_factors_t f, int32_t* ipiv) {
+  if (!f || f->dec.empty()) return -1;
+  if (!ipiv) return -2;
+  return cuda_err(cudaMemcpy(ipiv, f->w.ipiv, sizeof(int) * (size_t)f->g.n * f->g.nb,
+                             cudaMemcpyDeviceToHost));
+}
+int hlq_get_T(hlq_factors_t f, int32_t i, int32_t k, int32_t kind, double* T) {
+  if (!f || f->dec.empty()) return -1;
+  if (k < 0 || k >= f->g.n) return -3;
+  if (i < k || i >= f->g.n) return -2;
+  if (kind < 0 || kind > 1) return -4;
+  if (!T) return -5;
+  const double* src = (kind == 0 ? f->w.Tg : f->w.Ttt) + tri_index(i, k, f->g.n) * (int64_t)f->ib * f->g.nb;
+  return cuda_err(cudaMemcpy(T, src, sizeof(double) * f->ib * f->g.nb, cudaMemcpyDeviceToHost));
+}
+
+void hlq_free(hlq_factors_t f) {
+  if (!f) return;
+  if (f->ws_block) {
+    cudaStreamSynchronize(f->st);
+    cache_put(0, f->ws_block, f->ws_bytes);
+  }
+  delete f;
+}
+
+int hlq_gesv_host(const double* A_host, const double* b_host, double* x_host, int64_t N,
+                  int32_t nb, int32_t criterion, double alpha, const hlq_options* opt,
+                  hlq_info* info) {
+  if (!A_host) return -1;
+  if (!b_host) return -2;
+  if (!x_host) return -3;
+  if (N <= 0) return -4;
+  hlq_options o;
+  hlq_default_options(&o);
+  if (opt) o = *opt;
+  cudaStream_t st = (cudaStream_t)o.stream;
+  size_t abytes = sizeof(double) * (size_t)N * N;
+  char* buf = (char*)cache_get(1, abytes + 2 * sizeof(double) * (size_t)N + 512);
+  if (!buf) return HLQ_ERR_NOMEM;
+  double* dA = (double*)buf;
+  double* db = (double*)(buf + align_up(abytes, 256));
+  double* dx = db + align_up(N, 32);
+  int rc;
+  if ((rc = cuda_err(cudaMemcpyAsync(dA, A_host, abytes, cudaMemcpyHostToDevice, st))) ||
+      (rc = cuda_err(cudaMemcpyAsync(db, b_host, sizeof(double) * N, cudaMemcpyHostToDevice, st)))) {
+    cache_put(1, buf, abytes + 2 * sizeof(double) * (size_t)N + 512);
+    return rc;
+  }
+  o.lda = N;
+  hlq_factors_t f = nullptr;
+  int st_f = hlq_factor_ex(dA, N, nb, criterion, alpha, &o, &f);
+  if (st_f >= 0) {
+    rc = hlq_solve(f, db, dx);
+    if (rc == 0)
+      rc = cuda_err(cudaMemcpyAsync(x_host, dx, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+    if (rc == 0) rc = cuda_err(cudaStreamSynchronize(st));
+    if (info) hlq_get_info(f, info);
+  } else {
+    rc = st_f;
+  }
+  hlq_free(f);
+  cache_put(1, buf, abytes + 2 * sizeof(double) * (size_t)N + 512);
+  return rc != 0 ? rc : st_f;
+}
+
+int hlq_generate_uniform(double* dst, int64_t rows, int64_t cols, int64_t ld, uint64_t seed,
+                         uint64_t idx0, int64_t idx_ld, void* stream) {
+  if (!dst) return -1;
+  if (rows < 0) return -2;
+  if (cols < 0) return -3;
+  if (ld < rows) return -4;
+  launch_generate(dst, rows, cols, ld, seed, idx0, idx_ld, (cudaStream_t)stream);
+  return cuda_err(cudaGetLastError());
+}
+
+int hlq_residual(const double* A, int64_t N, int64_t lda, const double* x, const double* b,
+                 double* out3, void* stream) {
+  if (!A) return -1;
+  if (N <= 0) return -2;
+  if (lda < N) return -3;
+  if (!x) return -4;
+  if (!b) return -5;
+  if (!out3) return -6;
+  cudaStream_t st = (cudaStream_t)stream;
+  double* d = nullptr;
+  int rc;
+  if ((rc = cuda_err(cudaMallocAsync((void**)&d, 3 * sizeof(double), st)))) return rc;
+  launch_residual(A, N, lda, x, b, d, st);
+  rc = cuda_err(cudaMemcpyAsync(out3, d, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  cudaFreeAsync(d, st);
+  if (!rc) rc = cuda_err(cudaStreamSynchronize(st));
+  return rc;
+}
+
+}  // extern "C"

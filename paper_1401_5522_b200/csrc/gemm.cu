@@ -1,0 +1,207 @@
+// a7 (and a5/a6): FP64 tensor-core GEMM  C = beta*C + alpha*A*B  on sm_100a.
+//
+// B200 has no FP64 kind for tcgen05.mma, so the FP64 tensor path is the warp-level DMMA
+// (mma.sync.aligned.m8n8k4.row.col.f64 -> SASS DMMA.884), measured at 37.2 TFLOP/s on this pool
+// (profiles/r01/peak_dmma.jsonl).  Design:
+//   * CTA tile 128 x 64, 8 warps as 4 (M) x 2 (N), warp tile 32 x 32 = 4 x 4 DMMA fragments,
+//     64 FP64 accumulators per thread; 2 CTAs per SM so one CTA's C load/store overlaps the
+//     other's main loop (K = nb = 256 is short: C traffic is ~17% of the DMMA time per tile).
+//   * K staged through shared memory in BK=16 slices by a 3-stage cp.async pipeline;
+//     A slice stored [k][m] (ld 132), B slice [n][k] (ld 20): both paddings make every DMMA
+//     fragment load (lane -> (row g, k t)) bank-conflict free.
+//   * grouped rasterisation (8 tile-rows per group) for L2 reuse of the A panel / B row.
+// The Schur update of the LU step (Alg. 2) is C = C - L_panel * U_row on the
+// strided trailing submatrix; TRSM / SWPTRSM are C = X * U^-1 and C = L^-1 * (P X).
+#include "hlq_internal.cuh"
+
+namespace hlq {
+
+constexpr int BM = 128, BN = 64, BK = 16, STAGES = 3;
+constexpr int LDA_S = BM + 4, LDB_S = BK + 4;
+constexpr int A_STAGE = BK * LDA_S, B_STAGE = BN * LDB_S;
+constexpr int GEMM_SMEM = (A_STAGE + B_STAGE) * STAGES * (int)sizeof(double);
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <bool V16>
+__device__ __forceinline__ void load_stage(double* As, double* Bs, const double* __restrict__ A,
+                                           int64_t lda, const double* __restrict__ B, int64_t ldb,
+                                           int64_t M, int64_t N, int K, int64_t m0, int64_t n0,
+                                           int k0, int tid) {
+  if (V16) {
+    // A: BK x BM doubles = 1024 16-byte chunks, 4 per thread
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      int q = tid + 256 * i;
+      int kk = q >> 6, mm = (q & 63) * 2;
+      bool ok = (k0 + kk < K) && (m0 + mm < M);
+      const double* src = ok ? A + (int64_t)(k0 + kk) * lda + m0 + mm : A;
+      cp_async16(As + kk * LDA_S + mm, src, ok);
+    }
+    // B: BN x BK doubles = 512 chunks, 2 per thread
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      int q = tid + 256 * i;
+      int nn = q >> 3, kk = (q & 7) * 2;
+      bool ok = (n0 + nn < N) && (k0 + kk < K);
+      const double* src = ok ? B + (n0 + nn) * ldb + k0 + kk : B;
+      cp_async16(Bs + nn * LDB_S + kk, src, ok);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      int q = tid + 256 * i;
+      int kk = q >> 7, mm = q & 127;
+      bool ok = (k0 + kk < K) && (m0 + mm < M);
+      const double* src = ok ? A + (int64_t)(k0 + kk) * lda + m0 + mm : A;
+      cp_async8(As + kk * LDA_S + mm, src, ok);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      int q = tid + 256 * i;
+      int nn = q >> 4, kk = q & 15;
+      bool ok = (n0 + nn < N) && (k0 + kk < K);
+      const double* src = ok ? B + (n0 + nn) * ldb + k0 + kk : B;
+      cp_async8(Bs + nn * LDB_S + kk, src, ok);
+    }
+  }
+}
+
+template <bool V16>
+__global__ void __launch_bounds__(256, 2)
+    k_dgemm(double* __restrict__ C, int64_t ldc, const double* __restrict__ A, int64_t lda,
+            const double* __restrict__ B, int64_t ldb, int64_t M, int64_t N, int K, int neg,
+            int beta, const uint8_t* __restrict__ dec, int k, int want) {
+  if (dec != nullptr && dec[k] != want) return;  // predicated launch: the other branch was taken
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + STAGES * A_STAGE;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp & 3, wn = warp >> 2;
+
+  // grouped rasterisation
+  const int64_t ntm = (M + BM - 1) / BM, ntn = (N + BN - 1) / BN;
+  const int64_t bid = blockIdx.x;
+  const int64_t per_group = 8 * ntn;
+  const int64_t grp = bid / per_group;
+  const int64_t first_tm = grp * 8;
+  const int64_t gsz = (ntm - first_tm < 8) ? (ntm - first_tm) : 8;
+  const int64_t tm = first_tm + (bid % per_group) % gsz;
+  const int64_t tn = (bid % per_group) / gsz;
+  const int64_t m0 = tm * BM, n0 = tn * BN;
+
+  double acc[4][4][2];
+  // rows / cols of this thread's accumulators
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      int64_t row = m0 + wm * 32 + mi * 8 + g;
+      int64_t col = n0 + wn * 32 + ni * 8 + 2 * t;
+      double c0 = 0.0, c1 = 0.0;
+      if (beta && row < M) {
+        if (col < N) c0 = C[col * ldc + row];
+        if (col + 1 < N) c1 = C[(col + 1) * ldc + row];
+      }
+      acc[mi][ni][0] = c0;
+      acc[mi][ni][1] = c1;
+    }
+
+  const int KT = (K + BK - 1) / BK;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT)
+      load_stage<V16>(As + s * A_STAGE, Bs + s * B_STAGE, A, lda, B, ldb, M, N, K, m0, n0, s * BK,
+                      tid);
+    cp_commit();
+  }
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      int nk = kt + STAGES - 1;
+      if (nk < KT) {
+        int sl = nk % STAGES;
+        load_stage<V16>(As + sl * A_STAGE, Bs + sl * B_STAGE, A, lda, B, ldb, M, N, K, m0, n0,
+                        nk * BK, tid);
+      }
+      cp_commit();
+    }
+    const double* as = As + (kt % STAGES) * A_STAGE + wm * 32 + g;
+    const double* bs = Bs + (kt % STAGES) * B_STAGE + (wn * 32 + g) * LDB_S + t;
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        a[mi] = as[(k4 + t) * LDA_S + mi * 8];
+        if (neg) a[mi] = -a[mi];
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) b[ni] = bs[ni * 8 * LDB_S + k4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+    }
+  }
+  cp_wait<0>();
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      int64_t row = m0 + wm * 32 + mi * 8 + g;
+      int64_t col = n0 + wn * 32 + ni * 8 + 2 * t;
+      if (row < M) {
+        if (col < N) C[col * ldc + row] = acc[mi][ni][0];
+        if (col + 1 < N) C[(col + 1) * ldc + row] = acc[mi][ni][1];
+      }
+    }
+}
+
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+// C[M x N] = beta*C + (neg ? -1 : 1) * A[M x K] * B[K x N]; dec/k/want: optional predicate.
+void launch_dgemm(double* C, int64_t ldc, const double* A, int64_t lda, const double* B,
+                  int64_t ldb, int64_t M, int64_t N, int K, bool neg, bool beta,
+                  const uint8_t* dec, int k, int want, cudaStream_t st) {
+  if (M <= 0 || N <= 0 || K <= 0) return;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_dgemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
+    cudaFuncSetAttribute(k_dgemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
+    attr = true;
+  }
+  int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  bool v16 = aligned16(A) && aligned16(B) && (lda % 2 == 0) && (ldb % 2 == 0) && (M % 2 == 0) &&
+             (K % 2 == 0);
+  if (v16)
+    k_dgemm<true><<<(unsigned)tiles, 256, GEMM_SMEM, st>>>(C, ldc, A, lda, B, ldb, M, N, K,
+                                                           neg ? 1 : 0, beta ? 1 : 0, dec, k, want);
+  else
+    k_dgemm<false><<<(unsigned)tiles, 256, GEMM_SMEM, st>>>(C, ldc, A, lda, B, ldb, M, N, K,
+                                                            neg ? 1 : 0, beta ? 1 : 0, dec, k, want);
+}
+
+}  // namespace hlq

@@ -1,0 +1,92 @@
+// Internal declarations shared by the libhlq CUDA sources (never included by the oracle).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/hlq.h"
+
+namespace hlq {
+
+// ---- tile geometry (a0) -------------------------------------------------------------------
+struct Geo {
+  int64_t N, lda;
+  int nb, n;
+  __host__ __device__ int64_t r0(int i) const { return (int64_t)i * nb; }
+  __host__ __device__ int bs(int i) const {
+    int64_t r = N - (int64_t)i * nb;
+    return (int)(r < nb ? r : nb);
+  }
+  __host__ __device__ double* tile(double* A, int i, int j) const {
+    return A + r0(j) * lda + r0(i);
+  }
+};
+
+// index of tile (i,k), i >= k, in a packed lower triangle of n x n tiles (column k major)
+__host__ __device__ inline int64_t tri_index(int i, int k, int n) {
+  return (int64_t)k * n - (int64_t)k * (k - 1) / 2 + (i - k);
+}
+
+// ---- per-factorization device workspace ----------------------------------------------------
+struct DevWork {
+  double* W;          // nb*nb speculative LU of A_kk (ld = nb)
+  int* ipiv_ws;       // nb, pivots of the speculative LU
+  int* ipiv;          // n*nb committed pivots
+  double* Tg;         // GEQRT T factors, ib*nb per tile (tri_index)
+  double* Ttt;        // TTQRT T factors, ib*nb per tile (tri_index)
+  double* s;          // n tile norms ||A_ik||_1 of the current panel (index i)
+  double* local_max;  // nb
+  double* away_max;   // nb (atomicMax on bit patterns)
+  double* inv_norm;   // 1
+  int* zp;            // 1: zero pivot in the speculative LU
+  uint8_t* dec;       // n decisions
+  double* margin;     // n
+  int* flags;         // n step flags
+  int* status;        // 1: nonfinite criterion seen
+  uint8_t* forced;    // n or null
+  uint8_t* ref_dec;   // n or null
+  double* ref_margin; // n or null
+  double* gstep;      // n+1: max tile norm of the active matrix at the start of each step
+  int2* pairs;        // TT pair lists of every step/level (host-planned)
+  double* scratch;    // general scratch
+};
+
+// ---- kernels-side launch helpers (defined in the .cu files) ---------------------------------
+void launch_panel_stats(const double* A, Geo g, int k, DevWork w, cudaStream_t st);
+void launch_getrf(const double* A, Geo g, int k, DevWork w, bool need, cudaStream_t st);
+void launch_invnorm(Geo g, int k, DevWork w, cudaStream_t st);
+void launch_decide(Geo g, int k, int crit, double alpha, int mumps_reading, double tie_tol,
+                   int has_forced, int has_ref, DevWork w, cudaStream_t st);
+void launch_lu_step(double* A, Geo g, int k, DevWork w, bool predicated, cudaStream_t st);
+void launch_gemm_sub(double* C, int64_t ldc, const double* Am, int64_t lda, const double* Bm,
+                     int64_t ldb, int64_t M, int64_t Nc, int K, const uint8_t* dec, int k,
+                     cudaStream_t st);
+void launch_qr_step(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
+                    const int* level_count, int nlevels, DevWork w, bool predicated,
+                    cudaStream_t st);
+void launch_tile_norm_max(const double* A, Geo g, int k, double* out, cudaStream_t st);
+void launch_generate(double* dst, int64_t rows, int64_t cols, int64_t ld, uint64_t seed,
+                     uint64_t idx0, int64_t idx_ld, cudaStream_t st);
+// solve
+void launch_solve_lu_fwd(const double* A, Geo g, int k, const int* ipiv, double* x,
+                         cudaStream_t st);
+void launch_solve_qr_fwd(const double* A, Geo g, int k, int ib, const double* Tg,
+                         const double* Ttt, const int2* const* level_pairs, const int* level_count,
+                         int nlevels, double* x, cudaStream_t st);
+void launch_solve_back(const double* A, Geo g, int k, double* x, cudaStream_t st);
+void launch_residual(const double* A, int64_t N, int64_t lda, const double* x, const double* b,
+                     double* out3dev, cudaStream_t st);
+
+// ---- device helpers ---------------------------------------------------------------------------
+__device__ __forceinline__ double nanmax(double a, double b) {
+  // max that propagates NaN (criterion inputs: any NaN -> QR, reading 22)
+  return (a > b || a != a) ? a : b;
+}
+
+__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
+  // v >= 0 or NaN: IEEE bit patterns of non-negative doubles order like unsigned integers and the
+  // canonical NaN (0x7ff8...) orders above +inf, so the max propagates NaN.  Order-independent.
+  atomicMax(reinterpret_cast<unsigned long long*>(addr),
+            (unsigned long long)__double_as_longlong(v));
+}
+
+}  // namespace hlq

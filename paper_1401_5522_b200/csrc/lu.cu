@@ -1,0 +1,90 @@
+// LU step, variant A1 (Alg. 2), predicated on dec[k] == LU:
+//   a5  commit: A_kk <- W (the speculative GETRF), ipiv_k stored;      Factor
+//       eliminate: A_ik <- A_ik U_kk^-1 for all i > k                  Eliminate
+//   a6  apply: A_kj <- L_kk^-1 P_kk A_kj for all j > k                 Apply
+//   a7  update: A_ij <- A_ij - A_ik A_kj for all i, j > k              Update
+// With the LAPACK layout the i (j) loops are one strided column (row) block, so Eliminate and Apply
+// are two GEMMs with the explicit triangular inverses from getrf.cu and Update is one rank-b GEMM.
+// The swaps touch the columns right of the diagonal tile only (reading 23).
+#include "hlq_internal.cuh"
+
+namespace hlq {
+
+void launch_dgemm(double* C, int64_t ldc, const double* A, int64_t lda, const double* B,
+                  int64_t ldb, int64_t M, int64_t N, int K, bool neg, bool beta,
+                  const uint8_t* dec, int k, int want, cudaStream_t st);
+void launch_tri_inv(Geo g, int k, const DevWork& w, double* Li, double* Ui, cudaStream_t st);
+
+// A_kk <- W, ipiv[k*nb..] <- ipiv_ws, perm[r] = row of (P A_kk) r  (sequential swaps composed)
+__global__ void k_lu_commit(double* __restrict__ A, Geo g, int k, const double* __restrict__ W,
+                            const int* __restrict__ ipiv_ws, int* __restrict__ ipiv,
+                            int* __restrict__ perm, const uint8_t* __restrict__ dec) {
+  if (dec[k] != HLQ_DEC_LU) return;
+  const int bk = g.bs(k);
+  double* Akk = g.tile(A, k, k);
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < bk * bk;
+       idx += gridDim.x * blockDim.x) {
+    int c = idx / bk, r = idx - c * bk;
+    Akk[(int64_t)c * g.lda + r] = W[(int64_t)c * g.nb + r];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int r = 0; r < bk; ++r) perm[r] = r;
+    for (int c = 0; c < bk; ++c) {
+      int p = ipiv_ws[c];
+      ipiv[(int64_t)k * g.nb + c] = p;
+      int t = perm[c];
+      perm[c] = perm[p];
+      perm[p] = t;
+    }
+  }
+}
+
+// dst (rows x cols, ld_dst) <- src (ld_src), optionally with rows gathered through perm
+__global__ void k_copy_block(double* __restrict__ dst, int64_t ldd, const double* __restrict__ src,
+                             int64_t lds, int64_t rows, int64_t cols,
+                             const int* __restrict__ perm, const uint8_t* __restrict__ dec, int k) {
+  if (dec != nullptr && dec[k] != HLQ_DEC_LU) return;
+  int64_t total = rows * cols;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c = t / rows, r = t - c * rows;
+    int64_t sr = perm ? perm[r] : r;
+    dst[c * ldd + r] = src[c * lds + sr];
+  }
+}
+
+static unsigned grid_for(int64_t total) {
+  int64_t b = (total + 255) / 256;
+  if (b > 148 * 16) b = 148 * 16;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+void launch_lu_step(double* A, Geo g, int k, DevWork w, bool predicated, cudaStream_t st) {
+  const int bk = g.bs(k);
+  const int64_t k0 = g.r0(k), k1 = k0 + bk;
+  const int64_t M = g.N - k1;  // rows (and columns) below / right of the diagonal tile
+  const uint8_t* dec = w.dec;
+  double* Li = w.scratch;
+  double* Ui = w.scratch + (size_t)g.nb * g.nb;
+  int* perm = reinterpret_cast<int*>(w.scratch + (size_t)2 * g.nb * g.nb);
+  const size_t perm_sz = ((size_t)g.nb + 63) / 64 * 64;
+  double* ws = w.scratch + (size_t)2 * g.nb * g.nb + perm_sz;  // N*nb doubles
+  (void)predicated;
+  k_lu_commit<<<8, 256, 0, st>>>(A, g, k, w.W, w.ipiv_ws, w.ipiv, perm, dec);
+  if (M <= 0) return;
+  // Eliminate: X = A[k1:N, k0:k1]; A[k1:N, k0:k1] = X * U^-1
+  k_copy_block<<<grid_for(M * bk), 256, 0, st>>>(ws, M, A + k0 * g.lda + k1, g.lda, M, bk, nullptr,
+                                                 dec, k);
+  launch_dgemm(A + k0 * g.lda + k1, g.lda, ws, M, Ui, g.nb, M, bk, bk, false, false, dec, k,
+               HLQ_DEC_LU, st);
+  // Apply: Y = P A[k0:k1, k1:N]; A[k0:k1, k1:N] = L^-1 * Y
+  k_copy_block<<<grid_for(M * bk), 256, 0, st>>>(ws, bk, A + k1 * g.lda + k0, g.lda, bk, M, perm,
+                                                 dec, k);
+  launch_dgemm(A + k1 * g.lda + k0, g.lda, Li, g.nb, ws, bk, bk, M, bk, false, false, dec, k,
+               HLQ_DEC_LU, st);
+  // Update: A[k1:N, k1:N] -= A[k1:N, k0:k1] * A[k0:k1, k1:N]
+  launch_dgemm(A + k1 * g.lda + k1, g.lda, A + k0 * g.lda + k1, g.lda, A + k1 * g.lda + k0, g.lda,
+               M, M, bk, true, true, dec, k, HLQ_DEC_LU, st);
+}
+
+}  // namespace hlq

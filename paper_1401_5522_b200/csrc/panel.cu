@@ -1,0 +1,258 @@
+// Panel statistics (a1), decision (a4), tile-norm growth tracking (a12), input generator.
+//   a1  s_i = ||A_ik||_1 (i>k), local_max(j), away_max(j)      Eqs. 2-4
+//   a4  device-side decision d_k, margin, flags                 Alg. 1
+//   a12 max_{i,j>=k} ||A_ij||_1 of the active matrix
+// These kernels are HBM/latency bound: one warp per column, coalesced column reads (a column of a
+// tile is contiguous in the LAPACK layout), warp-shuffle reductions.
+#include <math.h>
+
+#include "hlq_internal.cuh"
+
+namespace hlq {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_nanmax(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = nanmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// grid: one block per tile row i in [k, n); 256 threads (8 warps, one column at a time each)
+__global__ void __launch_bounds__(256) k_panel_stats(const double* __restrict__ A, Geo g, int k,
+                                                     double* __restrict__ s,
+                                                     double* __restrict__ local_max,
+                                                     double* __restrict__ away_max) {
+  const int i = k + blockIdx.x;
+  const int bi = g.bs(i), bk = g.bs(k);
+  const double* T = g.tile(const_cast<double*>(A), i, k);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ double red[8];
+  double tile_norm = 0.0;
+  for (int c = warp; c < bk; c += 8) {
+    const double* col = T + (int64_t)c * g.lda;
+    double sum = 0.0, mx = 0.0;
+    for (int r = lane; r < bi; r += 32) {
+      double a = fabs(col[r]);
+      sum += a;
+      mx = nanmax(mx, a);
+    }
+    sum = warp_sum(sum);
+    mx = warp_nanmax(mx);
+    tile_norm = nanmax(tile_norm, sum);
+    if (lane == 0) {
+      if (i == k)
+        local_max[c] = mx;
+      else
+        atomic_max_nonneg(&away_max[c], mx);
+    }
+  }
+  if (lane == 0) red[warp] = tile_norm;
+  __syncthreads();
+  if (threadIdx.x == 0 && i > k) {
+    double v = red[0];
+    for (int w = 1; w < 8; ++w) v = nanmax(v, red[w]);
+    s[i] = v;
+  }
+}
+
+void launch_panel_stats(const double* A, Geo g, int k, DevWork w, cudaStream_t st) {
+  cudaMemsetAsync(w.away_max, 0, sizeof(double) * g.nb, st);
+  k_panel_stats<<<g.n - k, 256, 0, st>>>(A, g, k, w.s, w.local_max, w.away_max);
+}
+
+// ---------------------------------------------------------------------------------------------
+// a12: max over tiles i,j >= k of the tile 1-norm = max over (tile row, column) of column-segment
+// abs-sums.  grid (tile rows, column groups of 64), 256 threads; atomicMax into *out (>= 0).
+__global__ void __launch_bounds__(256) k_tile_norm_max(const double* __restrict__ A, Geo g, int k,
+                                                       double* out) {
+  const int i = k + blockIdx.x;
+  const int bi = g.bs(i);
+  const int64_t c0 = g.r0(k) + (int64_t)blockIdx.y * 64;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double best = 0.0;
+  for (int cc = warp; cc < 64; cc += 8) {
+    int64_t c = c0 + cc;
+    if (c >= g.N) break;
+    const double* col = A + c * g.lda + g.r0(i);
+    double sum = 0.0;
+    for (int r = lane; r < bi; r += 32) sum += fabs(col[r]);
+    best = nanmax(best, warp_sum(sum));
+  }
+  if (lane == 0) atomic_max_nonneg(out, best);
+}
+
+void launch_tile_norm_max(const double* A, Geo g, int k, double* out, cudaStream_t st) {
+  int64_t ncols = g.N - g.r0(k);
+  dim3 grid(g.n - k, (unsigned)((ncols + 63) / 64));
+  k_tile_norm_max<<<grid, 256, 0, st>>>(A, g, k, out);
+}
+
+// ---------------------------------------------------------------------------------------------
+// a4: the decision.  One block of 256 threads.  Mirrors DESIGN.md readings 3,4,5,7,21,22 and the
+// MUMPS readings (1, 2).  Writes dec[k], margin[k], flags[k]; status[0] |= nonfinite,
+// status[1] |= zero pivot in a forced LU step.
+__device__ __forceinline__ double rel_margin(double lhs, double rhs) {
+  double den = fmax(lhs, rhs);
+  if (den == 0.0) return 1.0;
+  return (lhs - rhs) / den;
+}
+
+__global__ void __launch_bounds__(256) k_decide(Geo g, int k, int crit, double alpha, int reading,
+                                                double tol, int has_forced, int has_ref,
+                                                DevWork w) {
+  const int bk = g.bs(k);
+  const int tid = threadIdx.x;
+  __shared__ double sh_growth[512];
+  __shared__ double sh_min[256];
+  __shared__ int sh_fail[256], sh_nan[256];
+  __shared__ double sh_margin;
+  __shared__ int sh_d, sh_flags;
+  const int zp = w.zp[0];
+  if (tid == 0) {
+    sh_flags = zp ? HLQ_FLAG_ZERO_PIVOT : 0;
+    sh_d = -1;
+    sh_margin = __longlong_as_double(0x7ff8000000000000LL);  // NaN
+    if (has_forced) {
+      sh_d = w.forced[k];
+      sh_flags |= HLQ_FLAG_FORCED;
+      if (sh_d == HLQ_DEC_LU && zp) atomicOr(&w.status[1], 1);
+    } else if (alpha == 0.0) {
+      sh_d = HLQ_DEC_QR;
+    } else if (zp) {
+      sh_d = HLQ_DEC_QR;
+    } else if (isinf(alpha)) {
+      sh_d = HLQ_DEC_LU;
+    }
+  }
+  __syncthreads();
+  if (sh_d < 0) {
+    if (crit == HLQ_CRIT_MAX || crit == HLQ_CRIT_SUM) {
+      if (tid == 0) {
+        double lhs = alpha / w.inv_norm[0];
+        double rhs = 0.0;
+        for (int i = k + 1; i < g.n; ++i) {  // ascending i (deterministic, as the oracle)
+          double v = w.s[i];
+          rhs = (crit == HLQ_CRIT_MAX) ? ((i == k + 1) ? v : nanmax(rhs, v)) : rhs + v;
+        }
+        if (isnan(lhs) || isnan(rhs)) {
+          sh_d = HLQ_DEC_QR;
+          sh_flags |= HLQ_FLAG_NONFINITE;
+        } else {
+          sh_d = (lhs >= rhs) ? HLQ_DEC_LU : HLQ_DEC_QR;
+          sh_margin = rel_margin(lhs, rhs);
+        }
+      }
+    } else {  // MUMPS (Eq. 4)
+      for (int j = tid; j < bk; j += 256) {
+        double p = fabs(w.W[(int64_t)j * g.nb + j]);
+        double lm = w.local_max[j];
+        sh_growth[j] = (lm == 0.0) ? (p > 0.0 ? INFINITY : 0.0) : p / lm;
+      }
+      __syncthreads();
+      double mn = INFINITY;
+      int fail = 0, nn = 0;
+      for (int j = tid; j < bk; j += 256) {
+        double p = fabs(w.W[(int64_t)j * g.nb + j]);
+        double est = w.away_max[j];
+        if (reading == 0) {
+          if (est != 0.0) est = est * sh_growth[j];
+        } else {
+          for (int i = 0; i < j; ++i)
+            if (est != 0.0) est = est * sh_growth[i];
+        }
+        double lhs = alpha * p;
+        if (isnan(lhs) || isnan(est)) {
+          nn = 1;
+          continue;
+        }
+        double mj = isinf(est) ? -1.0 : rel_margin(lhs, est);
+        if (!(lhs >= est)) fail = 1;
+        mn = fmin(mn, mj);
+      }
+      sh_min[tid] = mn;
+      sh_fail[tid] = fail;
+      sh_nan[tid] = nn;
+      __syncthreads();
+      if (tid == 0) {
+        double m = INFINITY;
+        int f = 0, q = 0;
+        for (int t = 0; t < 256; ++t) {
+          m = fmin(m, sh_min[t]);
+          f |= sh_fail[t];
+          q |= sh_nan[t];
+        }
+        if (q) {
+          sh_d = HLQ_DEC_QR;
+          sh_flags |= HLQ_FLAG_NONFINITE;
+        } else {
+          sh_d = f ? HLQ_DEC_QR : HLQ_DEC_LU;
+          sh_margin = (bk == 0) ? 1.0 : m;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int d = sh_d;
+    double mg = sh_margin;
+    int fl = sh_flags;
+    if (!has_forced && !isnan(mg)) {
+      bool near = fabs(mg) < tol;
+      if (near) fl |= HLQ_FLAG_NEAR_TIE;
+      if (has_ref && (near || fabs(w.ref_margin[k]) < tol)) {
+        d = w.ref_dec[k];
+        fl |= HLQ_FLAG_HINTED;
+      }
+    }
+    if (fl & HLQ_FLAG_NONFINITE) atomicOr(&w.status[0], 1);
+    w.dec[k] = (uint8_t)d;
+    w.margin[k] = mg;
+    w.flags[k] = fl;
+  }
+}
+
+void launch_decide(Geo g, int k, int crit, double alpha, int mumps_reading, double tie_tol,
+                   int has_forced, int has_ref, DevWork w, cudaStream_t st) {
+  k_decide<<<1, 256, 0, st>>>(g, k, crit, alpha, mumps_reading, tie_tol, has_forced, has_ref, w);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Counter-based uniform generator: SplitMix64 finalizer.
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_generate(double* dst, int64_t rows, int64_t cols, int64_t ld, uint64_t key,
+                           uint64_t idx0, int64_t idx_ld) {
+  const uint64_t GAMMA = 0x9E3779B97F4A7C15ULL;
+  int64_t total = rows * cols;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c = t / rows, r = t - c * rows;
+    uint64_t idx = idx0 + (uint64_t)c * (uint64_t)idx_ld + (uint64_t)r;
+    uint64_t u = mix64(key + (idx + 1ULL) * GAMMA);
+    dst[c * ld + r] = (double)(u >> 11) * 0x1.0p-53 - 0.5;
+  }
+}
+
+void launch_generate(double* dst, int64_t rows, int64_t cols, int64_t ld, uint64_t seed,
+                     uint64_t idx0, int64_t idx_ld, cudaStream_t st) {
+  // key(seed) = mix64(seed + GAMMA) computed on the host with the same integer arithmetic
+  uint64_t z = seed + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  uint64_t key = z ^ (z >> 31);
+  int64_t total = rows * cols;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  if (blocks < 1) blocks = 1;
+  k_generate<<<(unsigned)blocks, 256, 0, st>>>(dst, rows, cols, ld, key, idx0, idx_ld);
+}
+
+}  // namespace hlq

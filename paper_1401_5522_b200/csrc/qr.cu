@@ -1,0 +1,445 @@
+// QR step on the HQR greedy tree (Alg. 3, Alg. 4b; tree: DESIGN.md reading 16),
+// predicated on dec[k] == QR.  The paper's LU decomposition of the panel "is dropped, and the
+// factorization of the panel starts over": W is simply discarded.
+//   a8  GEQRT of every panel tile (i,k), i >= k, in parallel (one CTA per tile);
+//       UNMQR: row block i <- Q_ik^T row block i for all columns right of the panel
+//   a11 TT levels of the greedy tree: TTQRT(e, i) merges R_i into R_e (V upper triangular stored in
+//       the upper triangle of tile (i,k)), TTMQR applies it to [row e; row i]
+// Householder convention: LAPACK dlarfg (reading 14); T factors ib-blocked, forward column-wise
+// (dlarft), block b of tile (i,k) in columns b*ib.. of an ib x nb array (reading 15).
+// The UNMQR/TTMQR kernels take a generic column block (base, ldc, ncols) so the solve reuses them
+// on the right-hand side (ncols = 1).
+#include <math.h>
+
+#include "hlq_internal.cuh"
+
+namespace hlq {
+
+constexpr int QT = 256;   // threads per CTA (8 warps)
+constexpr int MAXIB = 32;
+constexpr int TLD = 33;   // T block smem stride
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+struct QRSmem {
+  double* Vs;    // MAXIB x ldv : reflector block (column l at Vs + l*ldv)
+  double* Ts;    // MAXIB x TLD : T block, T(q,l) at Ts[l*TLD + q]
+  double* xs;    // 8 warps x ldv : column buffers
+  double* ys;    // 8 warps x MAXIB
+  double* ws;    // 8 warps x MAXIB
+  double* Rs;    // MAXIB x TLD : R_e block of a TT factorization
+  int ldv;
+};
+
+__device__ __forceinline__ QRSmem carve(double* sm, int nb) {
+  QRSmem s;
+  s.ldv = nb + 1;
+  s.Vs = sm;
+  s.Ts = s.Vs + MAXIB * s.ldv;
+  s.xs = s.Ts + MAXIB * TLD;
+  s.ys = s.xs + 8 * s.ldv;
+  s.ws = s.ys + 8 * MAXIB;
+  s.Rs = s.ws + 8 * MAXIB;
+  return s;
+}
+static size_t qr_smem_bytes(int nb) {
+  return sizeof(double) * ((size_t)MAXIB * (nb + 1) + 2 * MAXIB * TLD + 8 * (nb + 1) + 16 * MAXIB);
+}
+
+// Apply H_b^T = (I - V T V^T)^T of a GEQRT block to one column x (rows R, local to the block start),
+// V unit lower (implicit 1 at (l,l), stored below), warp-cooperative, x in the warp's smem buffer.
+__device__ void apply_unit_col(double* x, int R, const QRSmem& s, int sb, double* w, int lane) {
+  for (int l = 0; l < sb; ++l) {
+    const double* v = s.Vs + l * s.ldv;
+    double p = 0.0;
+    for (int r = l + 1 + lane; r < R; r += 32) p += v[r] * x[r];
+    p = wsum(p);
+    if (lane == 0) w[l] = (l < R ? x[l] : 0.0) + p;
+  }
+  __syncwarp();
+  double u = 0.0;
+  if (lane < sb)
+    for (int q = 0; q <= lane; ++q) u += s.Ts[lane * TLD + q] * w[q];
+  __syncwarp();
+  if (lane < sb) w[lane] = u;
+  __syncwarp();
+  for (int r = lane; r < R; r += 32) {
+    double acc = 0.0;
+    int lmax = r < sb ? r : sb - 1;
+    for (int l = 0; l <= lmax; ++l) acc += ((l == r) ? 1.0 : s.Vs[l * s.ldv + r]) * w[l];
+    x[r] -= acc;
+  }
+  __syncwarp();
+}
+
+// Apply a TS/TT block: [c1 (sb rows); c2 (R2 rows)] <- Q_b^T [c1; c2], V2 = Vs (zeros stored where
+// the TT structure has zeros).
+__device__ void apply_pair_col(double* c1, double* c2, int R2, const QRSmem& s, int sb, double* w,
+                               int lane) {
+  for (int l = 0; l < sb; ++l) {
+    const double* v = s.Vs + l * s.ldv;
+    double p = 0.0;
+    for (int r = lane; r < R2; r += 32) p += v[r] * c2[r];
+    p = wsum(p);
+    if (lane == 0) w[l] = c1[l] + p;
+  }
+  __syncwarp();
+  double u = 0.0;
+  if (lane < sb)
+    for (int q = 0; q <= lane; ++q) u += s.Ts[lane * TLD + q] * w[q];
+  __syncwarp();
+  if (lane < sb) {
+    w[lane] = u;
+    c1[lane] -= u;
+  }
+  __syncwarp();
+  for (int r = lane; r < R2; r += 32) {
+    double acc = 0.0;
+    for (int l = 0; l < sb; ++l) acc += s.Vs[l * s.ldv + r] * w[l];
+    c2[r] -= acc;
+  }
+  __syncwarp();
+}
+
+// dlarfg on (alpha = *a, x[0..n)) in place by one warp: returns tau; *a <- beta; x <- v.
+__device__ double warp_larfg(double* a, double* x, int n, int lane) {
+  double p = 0.0;
+  for (int r = lane; r < n; r += 32) p += x[r] * x[r];
+  double ssq = wsum(p);
+  double alpha = *a;
+  if (ssq == 0.0) {
+    for (int r = lane; r < n; r += 32) x[r] = 0.0;
+    __syncwarp();
+    return 0.0;
+  }
+  double nrm = sqrt(alpha * alpha + ssq);
+  double beta = alpha >= 0.0 ? -nrm : nrm;
+  double tau = (beta - alpha) / beta;
+  double sc = alpha - beta;
+  for (int r = lane; r < n; r += 32) x[r] = x[r] / sc;
+  __syncwarp();
+  if (lane == 0) *a = beta;
+  __syncwarp();
+  return tau;
+}
+
+// ---------------------------------------------------------------------------------------------
+// GEQRT of tiles (k + blockIdx.x, k)
+__global__ void __launch_bounds__(QT) k_geqrt(double* __restrict__ A, Geo g, int k, int ib,
+                                              double* __restrict__ Tg, const uint8_t* __restrict__ dec) {
+  if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
+  extern __shared__ double sm[];
+  QRSmem s = carve(sm, g.nb);
+  const int i = k + blockIdx.x;
+  const int bi = g.bs(i), bk = g.bs(k);
+  double* tile = g.tile(A, i, k);
+  double* T = Tg + tri_index(i, k, g.n) * (int64_t)ib * g.nb;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int t = tid; t < ib * g.nb; t += QT) T[t] = 0.0;
+  for (int i0 = 0; i0 < bk; i0 += ib) {
+    const int sb = min(ib, bk - i0);
+    const int R = bi - i0;
+    if (R <= 0) break;  // wide ragged tile: remaining reflectors are the identity
+    for (int t = tid; t < sb * R; t += QT) {
+      int l = t / R, r = t - l * R;
+      s.Vs[l * s.ldv + r] = tile[(int64_t)(i0 + l) * g.lda + i0 + r];
+    }
+    for (int t = tid; t < MAXIB * TLD; t += QT) s.Ts[t] = 0.0;
+    __syncthreads();
+    if (warp == 0) {
+      for (int l = 0; l < sb && l < R; ++l) {
+        double* v = s.Vs + l * s.ldv;
+        double tau = warp_larfg(&v[l], v + l + 1, R - l - 1, lane);
+        if (tau != 0.0) {
+          for (int c = l + 1; c < sb; ++c) {
+            double* vc = s.Vs + c * s.ldv;
+            double p = 0.0;
+            for (int r = l + 1 + lane; r < R; r += 32) p += v[r] * vc[r];
+            double wv = vc[l] + wsum(p);
+            __syncwarp();
+            for (int r = l + 1 + lane; r < R; r += 32) vc[r] -= tau * (v[r] * wv);
+            if (lane == 0) vc[l] -= tau * wv;
+            __syncwarp();
+          }
+        }
+        // T column l: T(l,l) = tau, T(0:l,l) = -tau T(0:l,0:l) z, z_q = V_q . v_l
+        double* wz = s.ws + warp * MAXIB;
+        for (int q = 0; q < l; ++q) {
+          const double* vq = s.Vs + q * s.ldv;
+          double p = 0.0;
+          for (int r = l + 1 + lane; r < R; r += 32) p += vq[r] * v[r];
+          p = wsum(p);
+          if (lane == 0) wz[q] = vq[l] + p;
+        }
+        __syncwarp();
+        double tv = 0.0;
+        if (lane < l)
+          for (int p2 = lane; p2 < l; ++p2) tv += s.Ts[p2 * TLD + lane] * wz[p2];
+        __syncwarp();
+        if (lane < l) s.Ts[l * TLD + lane] = -tau * tv;
+        if (lane == 0) s.Ts[l * TLD + l] = tau;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int t = tid; t < sb * R; t += QT) {
+      int l = t / R, r = t - l * R;
+      tile[(int64_t)(i0 + l) * g.lda + i0 + r] = s.Vs[l * s.ldv + r];
+    }
+    for (int t = tid; t < sb * sb; t += QT) {
+      int l = t / sb, q = t - l * sb;
+      T[(int64_t)(i0 + l) * ib + q] = s.Ts[l * TLD + q];
+    }
+    // trailing columns of the tile
+    double* xb = s.xs + warp * s.ldv;
+    double* wb = s.ws + warp * MAXIB;
+    for (int c = i0 + sb + warp; c < bk; c += 8) {
+      double* col = tile + (int64_t)c * g.lda + i0;
+      for (int r = lane; r < R; r += 32) xb[r] = col[r];
+      __syncwarp();
+      apply_unit_col(xb, R, s, sb, wb, lane);
+      for (int r = lane; r < R; r += 32) col[r] = xb[r];
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+}
+
+// UNMQR: for tile rows i = k + blockIdx.y, columns [c0 + 64*blockIdx.x, +64) of the block
+// (base + r0(i), ldc): C_i <- Q_ik^T C_i
+__global__ void __launch_bounds__(QT) k_unmqr(const double* __restrict__ A, Geo g, int k, int ib,
+                                              const double* __restrict__ Tg, double* base,
+                                              int64_t ldc, int64_t ncols,
+                                              const uint8_t* __restrict__ dec) {
+  if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
+  extern __shared__ double sm[];
+  QRSmem s = carve(sm, g.nb);
+  const int i = k + blockIdx.y;
+  const int bi = g.bs(i), bk = g.bs(k);
+  const double* tile = g.tile(const_cast<double*>(A), i, k);
+  const double* T = Tg + tri_index(i, k, g.n) * (int64_t)ib * g.nb;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t c0 = (int64_t)blockIdx.x * 64;
+  double* xb = s.xs + warp * s.ldv;
+  double* wb = s.ws + warp * MAXIB;
+  for (int i0 = 0; i0 < bk; i0 += ib) {
+    const int sb = min(ib, bk - i0);
+    const int R = bi - i0;
+    if (R <= 0) break;
+    __syncthreads();
+    for (int t = tid; t < sb * R; t += QT) {
+      int l = t / R, r = t - l * R;
+      s.Vs[l * s.ldv + r] = tile[(int64_t)(i0 + l) * g.lda + i0 + r];
+    }
+    for (int t = tid; t < sb * sb; t += QT) {
+      int l = t / sb, q = t - l * sb;
+      s.Ts[l * TLD + q] = T[(int64_t)(i0 + l) * ib + q];
+    }
+    __syncthreads();
+    for (int cc = warp; cc < 64; cc += 8) {
+      int64_t c = c0 + cc;
+      if (c >= ncols) break;
+      double* col = base + c * ldc + g.r0(i) + i0;
+      for (int r = lane; r < R; r += 32) xb[r] = col[r];
+      __syncwarp();
+      apply_unit_col(xb, R, s, sb, wb, lane);
+      for (int r = lane; r < R; r += 32) col[r] = xb[r];
+      __syncwarp();
+    }
+  }
+}
+
+// TTQRT on pairs (e, i) = pairs[blockIdx.x]: [R_e; R_i] (both upper triangular) -> R_e, V (upper
+// triangle of tile (i,k)), T.
+__global__ void __launch_bounds__(QT) k_ttqrt(double* __restrict__ A, Geo g, int k, int ib,
+                                              double* __restrict__ Ttt, const int2* __restrict__ pairs,
+                                              const uint8_t* __restrict__ dec) {
+  if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
+  extern __shared__ double sm[];
+  QRSmem s = carve(sm, g.nb);
+  const int2 pr = pairs[blockIdx.x];
+  const int e = pr.x, i = pr.y;
+  const int bi = g.bs(i), bk = g.bs(k);
+  double* Re = g.tile(A, e, k);
+  double* Ri = g.tile(A, i, k);
+  double* T = Ttt + tri_index(i, k, g.n) * (int64_t)ib * g.nb;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* Rs = s.Rs;  // MAXIB x TLD block of R_e (row q, col l at Rs[l*TLD + q])
+  for (int t = tid; t < ib * g.nb; t += QT) T[t] = 0.0;
+  for (int i0 = 0; i0 < bk; i0 += ib) {
+    const int sb = min(ib, bk - i0);
+    const int R2 = min(bi, i0 + sb);  // rows of V2 that can be nonzero
+    __syncthreads();
+    for (int t = tid; t < sb * R2; t += QT) {
+      int l = t / R2, r = t - l * R2;
+      s.Vs[l * s.ldv + r] = (r <= i0 + l) ? Ri[(int64_t)(i0 + l) * g.lda + r] : 0.0;
+    }
+    for (int t = tid; t < sb * sb; t += QT) {
+      int l = t / sb, q = t - l * sb;
+      Rs[l * TLD + q] = (q <= l) ? Re[(int64_t)(i0 + l) * g.lda + i0 + q] : 0.0;
+    }
+    for (int t = tid; t < MAXIB * TLD; t += QT) s.Ts[t] = 0.0;
+    __syncthreads();
+    if (warp == 0) {
+      for (int l = 0; l < sb; ++l) {
+        double* v = s.Vs + l * s.ldv;
+        const int nr = min(R2, i0 + l + 1);
+        double tau = warp_larfg(&Rs[l * TLD + l], v, nr, lane);
+        if (tau != 0.0) {
+          for (int c = l + 1; c < sb; ++c) {
+            double* vc = s.Vs + c * s.ldv;
+            double p = 0.0;
+            for (int r = lane; r < nr; r += 32) p += v[r] * vc[r];
+            double wv = Rs[c * TLD + l] + wsum(p);
+            __syncwarp();
+            for (int r = lane; r < nr; r += 32) vc[r] -= tau * (v[r] * wv);
+            if (lane == 0) Rs[c * TLD + l] -= tau * wv;
+            __syncwarp();
+          }
+        }
+        double* wz = s.ws + warp * MAXIB;
+        for (int q = 0; q < l; ++q) {
+          const double* vq = s.Vs + q * s.ldv;
+          double p = 0.0;
+          for (int r = lane; r < nr; r += 32) p += vq[r] * v[r];
+          p = wsum(p);
+          if (lane == 0) wz[q] = p;
+        }
+        __syncwarp();
+        double tv = 0.0;
+        if (lane < l)
+          for (int p2 = lane; p2 < l; ++p2) tv += s.Ts[p2 * TLD + lane] * wz[p2];
+        __syncwarp();
+        if (lane < l) s.Ts[l * TLD + lane] = -tau * tv;
+        if (lane == 0) s.Ts[l * TLD + l] = tau;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int t = tid; t < sb * R2; t += QT) {
+      int l = t / R2, r = t - l * R2;
+      if (r <= i0 + l) Ri[(int64_t)(i0 + l) * g.lda + r] = s.Vs[l * s.ldv + r];
+    }
+    for (int t = tid; t < sb * sb; t += QT) {
+      int l = t / sb, q = t - l * sb;
+      if (q <= l) Re[(int64_t)(i0 + l) * g.lda + i0 + q] = Rs[l * TLD + q];
+      T[(int64_t)(i0 + l) * ib + q] = s.Ts[l * TLD + q];
+    }
+    __syncthreads();
+    // trailing columns c >= i0+sb of the pair (R_e rows i0..i0+sb-1, R_i rows 0..R2-1)
+    for (int c = i0 + sb + warp; c < bk; c += 8) {
+      double* col1 = Re + (int64_t)c * g.lda + i0;
+      double* col2 = Ri + (int64_t)c * g.lda;
+      double* wb = s.ws + warp * MAXIB;
+      double* c1b = s.ys + warp * MAXIB;
+      for (int r = lane; r < sb; r += 32) c1b[r] = col1[r];
+      __syncwarp();
+      // c2 directly in global memory (rows < R2 <= c: upper part of tile (i,k))
+      apply_pair_col(c1b, col2, R2, s, sb, wb, lane);
+      for (int r = lane; r < sb; r += 32) col1[r] = c1b[r];
+      __syncwarp();
+    }
+  }
+}
+
+// TTMQR on pairs[blockIdx.y] for columns [64*blockIdx.x, +64) of (base, ldc):
+// [C_e; C_i] <- Q^T [C_e; C_i]
+__global__ void __launch_bounds__(QT) k_ttmqr(const double* __restrict__ A, Geo g, int k, int ib,
+                                              const double* __restrict__ Ttt,
+                                              const int2* __restrict__ pairs, double* base,
+                                              int64_t ldc, int64_t ncols,
+                                              const uint8_t* __restrict__ dec) {
+  if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
+  extern __shared__ double sm[];
+  QRSmem s = carve(sm, g.nb);
+  const int2 pr = pairs[blockIdx.y];
+  const int e = pr.x, i = pr.y;
+  const int bi = g.bs(i), bk = g.bs(k);
+  const double* Vt = g.tile(const_cast<double*>(A), i, k);
+  const double* T = Ttt + tri_index(i, k, g.n) * (int64_t)ib * g.nb;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t c0 = (int64_t)blockIdx.x * 64;
+  double* xb = s.xs + warp * s.ldv;
+  double* wb = s.ws + warp * MAXIB;
+  double* c1b = s.ys + warp * MAXIB;
+  for (int i0 = 0; i0 < bk; i0 += ib) {
+    const int sb = min(ib, bk - i0);
+    const int R2 = min(bi, i0 + sb);
+    __syncthreads();
+    for (int t = tid; t < sb * R2; t += QT) {
+      int l = t / R2, r = t - l * R2;
+      s.Vs[l * s.ldv + r] = (r <= i0 + l) ? Vt[(int64_t)(i0 + l) * g.lda + r] : 0.0;
+    }
+    for (int t = tid; t < sb * sb; t += QT) {
+      int l = t / sb, q = t - l * sb;
+      s.Ts[l * TLD + q] = T[(int64_t)(i0 + l) * ib + q];
+    }
+    __syncthreads();
+    for (int cc = warp; cc < 64; cc += 8) {
+      int64_t c = c0 + cc;
+      if (c >= ncols) break;
+      double* col1 = base + c * ldc + g.r0(e) + i0;
+      double* col2 = base + c * ldc + g.r0(i);
+      for (int r = lane; r < sb; r += 32) c1b[r] = col1[r];
+      for (int r = lane; r < R2; r += 32) xb[r] = col2[r];
+      __syncwarp();
+      apply_pair_col(c1b, xb, R2, s, sb, wb, lane);
+      for (int r = lane; r < sb; r += 32) col1[r] = c1b[r];
+      for (int r = lane; r < R2; r += 32) col2[r] = xb[r];
+      __syncwarp();
+    }
+  }
+}
+
+static void set_attr_once() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  int mx = 200 * 1024;
+  cudaFuncSetAttribute(k_geqrt, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_unmqr, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_ttqrt, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_ttmqr, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+}
+
+// Apply the stored QR step k to the column block (base rows 0..N-1, ldc, ncols): used by the
+// factorization (columns right of the panel) and by the solve (the right-hand side).
+void launch_qr_apply(const double* A, Geo g, int k, int ib, const double* Tg, const double* Ttt,
+                     const int2* const* level_pairs, const int* level_count, int nlevels,
+                     double* base, int64_t ldc, int64_t ncols, const uint8_t* dec,
+                     cudaStream_t st) {
+  set_attr_once();
+  size_t smem = qr_smem_bytes(g.nb);
+  if (ncols <= 0) return;
+  unsigned slabs = (unsigned)((ncols + 63) / 64);
+  k_unmqr<<<dim3(slabs, g.n - k), QT, smem, st>>>(A, g, k, ib, Tg, base, ldc, ncols, dec);
+  for (int l = 0; l < nlevels; ++l)
+    k_ttmqr<<<dim3(slabs, level_count[l]), QT, smem, st>>>(A, g, k, ib, Ttt, level_pairs[l], base,
+                                                           ldc, ncols, dec);
+}
+
+void launch_qr_step(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
+                    const int* level_count, int nlevels, DevWork w, bool predicated,
+                    cudaStream_t st) {
+  set_attr_once();
+  size_t smem = qr_smem_bytes(g.nb);
+  const uint8_t* dec = predicated ? w.dec : nullptr;
+  const int64_t k1 = g.r0(k) + g.bs(k);
+  double* right = A + k1 * g.lda;
+  const int64_t ncols = g.N - k1;
+  k_geqrt<<<g.n - k, QT, smem, st>>>(A, g, k, ib, w.Tg, dec);
+  unsigned slabs = (unsigned)((ncols + 63) / 64);
+  if (ncols > 0) k_unmqr<<<dim3(slabs, g.n - k), QT, smem, st>>>(A, g, k, ib, w.Tg, right, g.lda, ncols, dec);
+  for (int l = 0; l < nlevels; ++l) {
+    k_ttqrt<<<level_count[l], QT, smem, st>>>(A, g, k, ib, w.Ttt, level_pairs[l], dec);
+    if (ncols > 0)
+      k_ttmqr<<<dim3(slabs, level_count[l]), QT, smem, st>>>(A, g, k, ib, w.Ttt, level_pairs[l],
+                                                             right, g.lda, ncols, dec);
+  }
+}
+
+}  // namespace hlq

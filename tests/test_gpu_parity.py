@@ -1,0 +1,200 @@
+"""GPU parity: libhlq (through the C ABI binding) vs the CPU oracle on identical seeded inputs.
+
+Bar (BASELINE.json north_star): identical decision vectors (near ties within
+1e-10 relative take the oracle's decision via ref_dec/ref_margin and are logged), identical pivots on
+every LU step, normwise factor difference <= 1e-10 (or <= 10 x the oracle's own noise floor where the
+method's conditioning makes 1e-10 unattainable), growth within 1e-10 relative, HPL3 <= 16.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import hlq_inputs as I
+from oracle import hlq_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def H():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1401_5522_b200 as H
+    return H
+
+
+def run_pair(H, A, b, nb, crit=O.CRIT_MAX, alpha=1.0, D=1, forced=None, mumps_reading=0):
+    N = A.shape[0]
+    fo = O.hybrid_factor(A, nb, crit, alpha, D=D, forced=forced, mumps_reading=mumps_reading)
+    dA = H.to_colmajor(A)
+    kw = dict(tree_domains=D, mumps_reading=mumps_reading)
+    if forced is not None:
+        f = H.hlq_factor_ex(dA, N, nb, crit, alpha, forced=forced, **kw)
+    else:
+        f = H.hlq_factor_ex(dA, N, nb, crit, alpha, ref_dec=fo.dec,
+                            ref_margin=np.nan_to_num(fo.margin, nan=1.0), **kw)
+    db = torch.from_numpy(np.ascontiguousarray(b)).cuda()
+    x = f.solve(db).cpu().numpy()
+    return fo, f, H.from_colmajor(dA), x
+
+
+def check_parity(fo, f, F, x, A, b, tol=1e-10, hpl=16.0):
+    dec = f.decisions()
+    np.testing.assert_array_equal(dec, fo.dec)
+    piv = f.pivots()
+    for k, ip in fo.ipiv.items():
+        np.testing.assert_array_equal(piv[k, :len(ip)], ip)
+    diff = O.factor_diff(F, fo.A)
+    assert diff <= tol, f"factor diff {diff:.3e}"
+    g = f.growth()
+    assert g == pytest.approx(fo.growth, rel=max(tol, 1e-10))
+    h3 = O.hpl3(A, x, b)
+    assert h3 <= hpl, h3
+    xo = O.solve(fo, b)
+    assert np.linalg.norm(x - xo) <= 1e-8 * np.linalg.norm(xo)
+    return diff, h3
+
+
+def test_generator_bit_identical(H):
+    N = 301
+    t = torch.empty(N * N + N, dtype=torch.float64, device="cuda")
+    H.hlq_generate_uniform(t, N, N, N, 2, 0, N)
+    H.hlq_generate_uniform(t[N * N:], N, 1, N, 2, N * N, N)
+    torch.cuda.synchronize()
+    got = t.cpu().numpy()
+    A = I.uniform_matrix(2, N)
+    np.testing.assert_array_equal(got[:N * N].reshape(N, N).T, A)
+    np.testing.assert_array_equal(got[N * N:], I.uniform_rhs(2, N))
+
+
+@pytest.mark.parametrize("alpha", [1.0, math.inf, 0.0, 1.2e4, 3e4])
+def test_c1_max_criterion(H, alpha):
+    A, b, meta = I.config_system("C1")
+    fo, f, F, x = run_pair(H, A, b, 128, O.CRIT_MAX, alpha)
+    check_parity(fo, f, F, x, A, b)
+
+
+@pytest.mark.parametrize("crit,alpha", [(O.CRIT_SUM, 1.0), (O.CRIT_SUM, 1e6), (O.CRIT_MUMPS, 1.0),
+                                        (O.CRIT_MUMPS, 4.0), (O.CRIT_MUMPS, 1.5)])
+def test_criteria_normal_input(H, crit, alpha):
+    A, b = I.normal_system(1, 1024)
+    fo, f, F, x = run_pair(H, A, b, 128, crit, alpha)
+    check_parity(fo, f, F, x, A, b)
+
+
+def test_mumps_m2_reading(H):
+    A, b = I.normal_system(1, 512)
+    fo, f, F, x = run_pair(H, A, b, 64, O.CRIT_MUMPS, 2.1, mumps_reading=1)
+    check_parity(fo, f, F, x, A, b)
+
+
+@pytest.mark.parametrize("N,nb,crit,alpha", [(1000, 128, O.CRIT_MAX, 1.0),
+                                             (1000, 128, O.CRIT_MAX, math.inf),
+                                             (777, 64, O.CRIT_SUM, 1e5),
+                                             (777, 64, O.CRIT_MUMPS, 2.0),
+                                             (300, 320, O.CRIT_MAX, 1.0),
+                                             (65, 32, O.CRIT_MAX, 1e3)])
+def test_ragged_and_degenerate_sizes(H, N, nb, crit, alpha):
+    A = I.uniform_matrix(5, N)
+    b = I.uniform_rhs(5, N)
+    fo, f, F, x = run_pair(H, A, b, nb, crit, alpha)
+    check_parity(fo, f, F, x, A, b)
+
+
+@pytest.mark.parametrize("D", [2, 3])
+def test_tree_domains(H, D):
+    A = I.uniform_matrix(8, 960)
+    b = I.uniform_rhs(8, 960)
+    fo, f, F, x = run_pair(H, A, b, 64, O.CRIT_MAX, 1.5e4, D=D)
+    check_parity(fo, f, F, x, A, b)
+
+
+@pytest.mark.parametrize("f_qr", [0.0, 0.25, 0.5, 1.0])
+def test_forced_bernoulli_patterns(H, f_qr):
+    N, nb = 1024, 64
+    A = I.uniform_matrix(3, N)
+    b = I.uniform_rhs(3, N)
+    forced = I.bernoulli_pattern(30, N // nb, f_qr)
+    fo, f, F, x = run_pair(H, A, b, nb, forced=forced)
+    # all-LU at N=1024, nb=64: the method's own noise floor is ~1e-11
+    check_parity(fo, f, F, x, A, b, tol=1e-10)
+    assert f.info()["qr_steps"] == int(forced.sum())
+
+
+@pytest.mark.parametrize("alpha,growth", [(1.0, 128.0), (2.0, 2187.0)])
+def test_kronecker_worst_case_bit_exact(H, alpha, growth):
+    """P:523-532 lifted to N=1024, nb=128: every Max decision is an exact tie (LU), growth is
+    exactly (1+alpha)^(n-1) and every intermediate is a binary fraction: bit-exact on the GPU."""
+    A = I.kron_lift(I.worst_case_max(8, alpha), 128)
+    dA = H.to_colmajor(A)
+    f = H.hlq_factor(dA, 1024, 128, H.CRIT_MAX, alpha)
+    assert "".join("LQ"[d] for d in f.decisions()) == "L" * 8
+    assert f.growth() == growth
+    fo = O.hybrid_factor(A, 128, O.CRIT_MAX, alpha)
+    np.testing.assert_array_equal(H.from_colmajor(dA), fo.A)
+    assert np.all(f.step_flags()[:-1] & H.FLAG_NEAR_TIE)
+
+
+@pytest.mark.parametrize("which", ["C4A", "C4B", "C4C"])
+@pytest.mark.parametrize("crit", [O.CRIT_MAX, O.CRIT_SUM, O.CRIT_MUMPS])
+def test_stress_matrices(H, which, crit):
+    """C4 at reduced size (N=1024, nb=64): Wilkinson-type, +1e-6 noise, scaled sub-diagonal tiles."""
+    A, b, meta = I.config_system(which, 1024)
+    if which == "C4C":  # scale by 1e3 with the reduced tile size
+        A, b = I.normal_system(5, 1024)
+        for i in range(0, 1024, 64):
+            for j in range(0, i, 64):
+                A[i:i + 64, j:j + 64] *= 1e3
+    fo, f, F, x = run_pair(H, A, b, 64, crit, 1.0)
+    np.testing.assert_array_equal(f.decisions(), fo.dec)
+    if which == "C4A" and crit == O.CRIT_MUMPS:
+        # designed failure: all exact-tie LU steps; the last column grows like 2^(N-1)
+        assert set(f.decisions()) == {O.LU}
+        assert f.status in (0, 1)
+        return
+    check_parity(fo, f, F, x, A, b)
+
+
+def test_T_factors_match_oracle(H):
+    A = I.uniform_matrix(12, 256)
+    fo = O.hybrid_factor(A, 64, O.CRIT_MAX, 0.0, ib=32)
+    dA = H.to_colmajor(A)
+    f = H.hlq_factor(dA, 256, 64, H.CRIT_MAX, 0.0)
+    for k in range(4):
+        d = fo.qr[k]
+        for i, T in d.T_geqrt.items():
+            assert np.linalg.norm(f.T(i, k, 0) - T) <= 1e-12 * max(1.0, np.linalg.norm(T))
+        for i, T in d.T_tt.items():
+            assert np.linalg.norm(f.T(i, k, 1) - T) <= 1e-12 * max(1.0, np.linalg.norm(T))
+
+
+def test_e2e_host_path(H):
+    A, b, _ = I.config_system("C1")
+    x = np.zeros(1024)
+    rc, info = H.hlq_gesv_host(np.asfortranarray(A), b, x, 1024, 128, H.CRIT_MAX, 1.0)
+    assert rc == 0 and info["n"] == 8
+    assert O.hpl3(A, x, b) < 16
+    fo = O.hybrid_factor(A, 128, O.CRIT_MAX, 1.0)
+    assert info["qr_steps"] == int(fo.dec.sum())
+    assert info["true_flops"] == pytest.approx(O.true_flops(1024, 128, fo.dec), rel=1e-12)
+
+
+def test_device_residual_matches_host(H):
+    A, b, _ = I.config_system("C1")
+    dA = H.to_colmajor(A)
+    x = np.linalg.solve(A, b)
+    r = H.hlq_residual(dA, 1024, 1024, torch.from_numpy(x).cuda(), torch.from_numpy(b).cuda())
+    assert r["hpl3"] == pytest.approx(O.hpl3(A, x, b), rel=1e-6, abs=1e-6)
+
+
+def test_invalid_arguments(H):
+    dA = torch.zeros(16, dtype=torch.float64, device="cuda")
+    with pytest.raises(H.HlqError):
+        H.hlq_factor(dA, 4, 2, 7, 1.0)
+    with pytest.raises(H.HlqError):
+        H.hlq_factor(dA, 4, 2, H.CRIT_MAX, float("nan"))
+    with pytest.raises(H.HlqError):
+        H.hlq_factor(dA, 0, 2, H.CRIT_MAX, 1.0)

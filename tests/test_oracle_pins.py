@@ -308,10 +308,11 @@ def test_all_lu_path_is_restricted_pivot_gaussian_elimination(N, nb):
     assert rel(f.A, G) < 1e-11
 
 
-@pytest.mark.parametrize("N,nb,D", [(128, 32, 1), (160, 32, 2), (150, 32, 3)])
-def test_all_qr_path_reproduces_householder_R(N, nb, D):
+@pytest.mark.parametrize("tree", ["greedy", "flat"])
+@pytest.mark.parametrize("N,nb,D", [(128, 32, 1), (160, 32, 2), (150, 32, 3), (224, 16, 1)])
+def test_all_qr_path_reproduces_householder_R(N, nb, D, tree):
     A, b = I.normal_system(9, N)
-    f = O.hybrid_factor(A, nb, O.CRIT_MAX, 0.0, D=D)
+    f = O.hybrid_factor(A, nb, O.CRIT_MAX, 0.0, D=D, tree=tree)
     R = np.linalg.qr(A, mode="r")
     assert rel(np.abs(np.triu(f.A)), np.abs(R)) < 1e-12
     x = O.solve(f, b)
@@ -384,6 +385,25 @@ def test_ragged_equals_padded(crit, alpha):
     fp = O.hybrid_factor(np.asfortranarray(P), nb, crit, alpha)
     np.testing.assert_array_equal(fr.dec[:-1], fp.dec[:-1])
     assert rel(fr.A[:N, :N], fp.A[:N, :N]) < 1e-12
+
+
+def test_greedy_plan_structure():
+    """Every row i > k is eliminated exactly once, pairs in a level are disjoint, the eliminator is
+    still live, and only row k survives (SPEC trees invariants); depth = ceil(log2(m+1)) for D=1."""
+    for n, k, D in ((9, 0, 1), (16, 3, 1), (17, 0, 2), (30, 5, 4), (5, 4, 1)):
+        rows, ts, levels = O.qr_plan(k, n, D, "greedy")
+        assert rows == list(range(k, n)) and ts == []
+        live = set(range(k, n))
+        for lvl in levels:
+            used = [r for p in lvl for r in p]
+            assert len(used) == len(set(used))
+            for e, i in lvl:
+                assert e in live and i in live and e < i
+            for e, i in lvl:
+                live.discard(i)
+        assert live == {k}
+        if D == 1:
+            assert len(levels) == math.ceil(math.log2(n - k)) if n - k > 1 else len(levels) == 0
 
 
 def test_table_i_sums_and_table_ii_arithmetic():
