@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""bench.py -- hybrid LU-QR hot path (arXiv 1401.5522) on B200.
+
+One "step" = one pass of the whole hot path over one synthetic system: hlq_factor (per-step
+criterion + LU or QR step, all on the device) followed by hlq_solve.  Metric (BASELINE.json):
+FP64 TFLOP/s on the LU-equivalent 2N^3/3 basis, plus true flops (Table I with the actual
+decisions) and the HPL3 scaled residual.
+
+Default workload: C3 (N=32768, nb=256, FP64 uniform[-0.5,0.5) from seed 3, decision vector forced to
+the seeded Bernoulli pattern with QR fraction f=0: the all-LU path of the north_star target).
+Inputs (8.6 GB) exceed the 126 MB L2, so no explicit flush is needed between timed steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3|C2|C1|C4A..] [--fqr F]
+                  [--criterion max|sum|mumps --alpha A] [--impl reference]
+Under torchrun each rank factors its own independent system (weak scaling; the 2D block-cyclic
+distributed factorization is DESIGN.md row e).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# measured FP64 peaks on this pool (profiles/r01/peak_dmma.jsonl, peak_cublas.jsonl)
+FP64_DMMA_PEAK_TF = 37.2   # mma.sync m8n8k4 f64 microbenchmark, 148 SMs, 1965 MHz, no throttling
+FP64_CUBLAS_TF = 36.2      # torch.matmul float64 16384^3 sustained
+
+CONFIGS = {
+    "C1": dict(N=1024, nb=128, seed=0, gen="uniform"),
+    "C2": dict(N=16384, nb=256, seed=1, gen="normal"),
+    "C3": dict(N=32768, nb=256, seed=3, gen="uniform"),
+    "C4A": dict(N=4096, nb=128, seed=6, gen="wilkinson"),
+    "C5": dict(N=131072, nb=320, seed=2, gen="uniform"),
+}
+CRIT = {"max": 0, "sum": 1, "mumps": 2}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="hlq", choices=["hlq", "reference"])
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--N", type=int, default=0)
+    ap.add_argument("--nb", type=int, default=0)
+    ap.add_argument("--fqr", type=float, default=0.0, help="forced QR-step fraction (C3 pattern)")
+    ap.add_argument("--criterion", default="", help="max|sum|mumps: use the criterion instead")
+    ap.add_argument("--alpha", type=float, default=1.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-N", type=int, default=4096)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.proc = None
+        self.path = os.path.join("/tmp", f"hlq_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons, pw = [], [], set(), []
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                pw.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        under_load = [s for s, p in zip(sm, pw) if p > 200.0] or sm
+        return {"sm_mhz": statistics.median(under_load) if under_load else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(pw) if pw else None}
+
+
+# ------------------------------------------------------------------------------------ CPU oracle
+def cpu_oracle_step(N, nb, seed, fqr, crit, alpha):
+    """One bounded oracle factor+solve (test infrastructure; the bench's cpu_baseline leg)."""
+    import hlq_inputs as I
+    from oracle import hlq_oracle as O
+    A = I.uniform_matrix(seed, N)
+    b = I.uniform_rhs(seed, N)
+    n = (N + nb - 1) // nb
+    t0 = time.perf_counter()
+    if crit:
+        f = O.hybrid_factor(A, nb, CRIT[crit], alpha, track_growth=True)
+    else:
+        f = O.hybrid_factor(A, nb, forced=I.bernoulli_pattern(30, n, fqr), track_growth=True)
+    x = O.solve(f, b)
+    dt = time.perf_counter() - t0
+    return dt, f, O.hpl3(A, x, b)
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------------- reference arm
+def run_reference(args, cfg, rank):
+    if rank != 0:
+        return
+    Ns = args.cpu_sample_N
+    nb = cfg["nb"]
+    fake = 2.0 / 3.0 * Ns ** 3
+    for _ in range(args.warmup):
+        cpu_oracle_step(Ns, nb, cfg["seed"], args.fqr, args.criterion, args.alpha)
+    times = []
+    for _ in range(args.steps):
+        dt, f, h3 = cpu_oracle_step(Ns, nb, cfg["seed"], args.fqr, args.criterion, args.alpha)
+        times.append(dt)
+    t = sum(times) / len(times)
+    val = fake / t / 1e12
+    sample = (f"oracle (numpy/scipy, plain CPU) factor+solve of the {args.config}-recipe system at "
+              f"N={Ns}, nb={nb} (bounded sample of the N={cfg['N']} workload), per step")
+    out = {"impl": "reference", "metric": "FP64 TFLOP/s (2N^3/3 basis) hybrid LU-QR",
+           "value": val, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": workload_config(args, cfg), "hpl3": h3,
+           "cpu_baseline": {"kind": "oracle", "cores": cpu_threads(), "sample": sample,
+                            "value": val, "unit": "TFLOP/s"},
+           "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def workload_config(args, cfg):
+    N, nb = cfg["N"], cfg["nb"]
+    if args.criterion:
+        dec = f"{args.criterion} criterion alpha={args.alpha}"
+    else:
+        dec = f"forced Bernoulli pattern f_QR={args.fqr} (seed 30)"
+    return {"workload": f"{args.config}: N={N}, nb={nb}, FP64 {cfg['gen']} seed {cfg['seed']}, {dec}",
+            "N": N, "nb": nb, "n_tiles": (N + nb - 1) // nb, "global_batch": args.gpus,
+            "parallelism": f"replicas{args.gpus}" if args.gpus > 1 else "single",
+            "l2": "inputs (8*N^2 bytes) > 126 MB L2: no flush needed"}
+
+
+# ------------------------------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    cfg = dict(CONFIGS[args.config.upper()])
+    if args.N:
+        cfg["N"] = args.N
+    if args.nb:
+        cfg["nb"] = args.nb
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, cfg, rank)
+        return
+    args.warmup = max(args.warmup, 3)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1401_5522_b200 as H
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream()
+    N, nb = cfg["N"], cfg["nb"]
+    n = (N + nb - 1) // nb
+    seed = cfg["seed"] + 1000 * rank  # independent system per rank (weak scaling)
+    # inputs generated on the device with the counter generator (bit-identical to hlq_inputs)
+    A0 = torch.empty(N * N, dtype=torch.float64, device=dev)
+    b = torch.empty(N, dtype=torch.float64, device=dev)
+    if cfg["gen"] == "uniform":
+        H.hlq_generate_uniform(A0, N, N, N, seed, 0, N)
+        H.hlq_generate_uniform(b, N, 1, N, seed, N * N, N)
+    else:
+        import hlq_inputs as I
+        Ah, bh, _ = I.config_system(args.config, N)
+        A0.copy_(torch.from_numpy(np.ascontiguousarray(Ah.T)).reshape(-1))
+        b.copy_(torch.from_numpy(bh))
+    A = torch.empty_like(A0)
+    x = torch.empty_like(b)
+    crit = CRIT[args.criterion] if args.criterion else 0
+    forced = None
+    if not args.criterion:
+        import hlq_inputs as I
+        forced = I.bernoulli_pattern(30, n, args.fqr)
+
+    def one_step(profile):
+        A.copy_(A0)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        f = H.hlq_factor_ex(A, N, nb, crit, args.alpha, forced=forced, profile=int(profile))
+        f.solve(b, x)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1), f
+
+    for _ in range(args.warmup):
+        _, f = one_step(False)
+        f.free()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = H.hlq_launch_count()
+    times, profs, infos = [], [], []
+    for _ in range(args.steps):
+        ms, f = one_step(True)
+        times.append(ms)
+        profs.append(f.profile())
+        infos.append(f.info())
+        last = f
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = H.hlq_launch_count() - l0
+    clocks = sampler.stop()
+    t_sum = sum(times)
+    if world > 1:
+        tt = torch.tensor([t_sum], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_sum = float(tt.item())
+    ms_step = t_sum / args.steps
+    info = infos[-1]
+    fake = info["fake_flops"]
+    true = info["true_flops"]
+    value = fake * world / (ms_step * 1e-3) / 1e12
+    # HPL3 of the last step (device residual against the pristine copy)
+    res = H.hlq_residual(A0, N, N, x, b)
+    dec = last.decisions()
+    last.free()
+
+    # roofline: dominant kernel class of the step
+    agg = {}
+    for p in profs:
+        for c, v in p.items():
+            a = agg.setdefault(c, {"ms": 0.0, "flops": 0.0, "launches": 0})
+            a["ms"] += v["ms"]
+            a["flops"] += v["flops"]
+            a["launches"] += v["launches"]
+    dom = max(("lu_update", "qr_unmqr", "qr_tt"), key=lambda c: agg[c]["ms"])
+    achieved = agg[dom]["flops"] / (agg[dom]["ms"] * 1e-3) / 1e12 if agg[dom]["ms"] > 0 else 0.0
+    step_ms_sum = sum(v["ms"] for v in agg.values())
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"{args.config}:{dom}")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "kernel": f"k_dgemm ({dom})" if dom == "lu_update" else dom,
+                "achieved": achieved, "peak": FP64_DMMA_PEAK_TF, "unit": "TFLOP/s",
+                "frac": achieved / FP64_DMMA_PEAK_TF, "traffic": traffic,
+                "peak_source": "measured FP64 DMMA mma.sync m8n8k4 sustained, 148 SMs "
+                               "(profiles/r01/peak_dmma.jsonl); cuBLAS DGEMM measured 36.2",
+                "share_of_step": agg[dom]["ms"] / step_ms_sum if step_ms_sum else None,
+                "per_class_ms": {c: round(v["ms"] / args.steps, 3) for c, v in agg.items()}}
+
+    # e2e through the public C ABI with host buffers (H2D of A and b, D2H of x inside the timing)
+    e2e = None
+    if not args.no_e2e:
+        Ah = torch.empty(N * N, dtype=torch.float64, pin_memory=True)
+        Ah.copy_(A0)
+        bh = b.cpu().pin_memory()
+        xh = torch.empty(N, dtype=torch.float64, pin_memory=True)
+        opt = H.hlq_default_options()
+        fv = forced
+        if fv is not None:
+            fa = np.ascontiguousarray(fv, dtype=np.uint8)
+            opt.forced = fa.ctypes.data
+        del A  # make room for the library's own device copy
+        torch.cuda.empty_cache()
+        ets = []
+        for it in range(1 + min(args.steps, 3)):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            H.hlq_gesv_host(Ah.numpy(), bh.numpy(), xh.numpy(), N, nb, crit, args.alpha, opt)
+            dt = time.perf_counter() - t0
+            if it > 0:
+                ets.append(dt)
+        e2e = {"value": fake * world / statistics.mean(ets) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": 8 * N * N + 8 * N, "d2h_bytes_per_step": 8 * N,
+               "steps": len(ets), "timing": "host wall clock around hlq_gesv_host (blocking)"}
+
+    cpu_base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        Ns = args.cpu_sample_N
+        dt, fo, h3c = cpu_oracle_step(Ns, nb, cfg["seed"], args.fqr, args.criterion, args.alpha)
+        cpu_base = {"value": 2.0 / 3.0 * Ns ** 3 / dt / 1e12, "unit": "TFLOP/s",
+                    "cores": cpu_threads(), "kind": "oracle",
+                    "sample": f"one oracle factor+solve of the same recipe at N={Ns}, nb={nb} "
+                              f"({dt:.1f} s), TFLOP/s on the 2N^3/3 basis"}
+
+    if rank == 0:
+        out = {"metric": "FP64 TFLOP/s (2N^3/3 basis) hybrid LU-QR", "value": value,
+               "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+               "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "config": workload_config(args, cfg),
+               "true_tflops": true * world / (ms_step * 1e-3) / 1e12,
+               "paper_true_tflops": (2 / 3 * (1 - dec.mean()) + 4 / 3 * dec.mean()) * N ** 3 * world
+               / (ms_step * 1e-3) / 1e12,
+               "frac_fp64_peak": value / world / FP64_DMMA_PEAK_TF,
+               "qr_fraction": float(dec.mean()), "hpl3": res["hpl3"], "growth": info["growth"],
+               "status": info["status"], "step_ms": [round(t, 3) for t in times],
+               "roofline": roofline, "cpu_baseline": cpu_base, "e2e": e2e,
+               "gpu_launches": launches, "clocks": clocks}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

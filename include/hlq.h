@@ -72,6 +72,7 @@ typedef struct {
   int32_t track_growth;      /* 1 (default): compute the tile-norm growth factor     */
   int32_t blocking;          /* 1 (default): synchronise opt.stream before returning             */
   void* stream;              /* cudaStream_t                                                     */
+  int32_t profile;           /* 1: time every kernel class with CUDA events (hlq_get_profile)    */
 } hlq_options;
 
 typedef struct {
@@ -142,6 +143,27 @@ int hlq_generate_uniform(double* dst, int64_t rows, int64_t cols, int64_t ld, ui
  * (not the factors).  Row sums/residuals accumulate in fixed order. */
 int hlq_residual(const double* A, int64_t N, int64_t lda, const double* x, const double* b,
                  double* out3, void* stream);
+
+/* Kernel classes timed when opt.profile = 1 (CUDA events on the factorization's stream). */
+enum {
+  HLQ_PROF_CRITERION = 0,  /* panel statistics, ||A_kk^-1||_1, decide (a1, a3, a4)               */
+  HLQ_PROF_GETRF = 1,      /* speculative GETRF + triangular inverses (a2, a3)                    */
+  HLQ_PROF_LU_TRSM = 2,    /* commit + Eliminate (TRSM) + Apply (SWPTRSM) (a5, a6)                */
+  HLQ_PROF_LU_UPDATE = 3,  /* Schur DGEMM update (a7): the dominant kernel of LU steps           */
+  HLQ_PROF_QR_GEQRT = 4,   /* GEQRT of the panel tiles (a8)                                       */
+  HLQ_PROF_QR_UNMQR = 5,   /* UNMQR trailing update (a8)                                          */
+  HLQ_PROF_QR_TT = 6,      /* TTQRT + TTMQR levels (a9-a11)                                       */
+  HLQ_PROF_GROWTH = 7,     /* tile-norm growth tracking (a12)                                     */
+  HLQ_PROF_SOLVE = 8,      /* forward replay + back substitution (a13)                            */
+  HLQ_PROF_OTHER = 9,
+  HLQ_PROF_NCLASSES = 10
+};
+/* Per class: device milliseconds, algorithmic flops of the EXECUTED branch (Table I counts with
+ * valid sizes; the LU update is 2 M^2 b per LU step) and kernel launches (both branches).
+ * Arrays of HLQ_PROF_NCLASSES entries (host).  -2 when the handle was not profiled. */
+int hlq_get_profile(hlq_factors_t f, double* ms, double* flops, int64_t* launches);
+/* Total kernel launches issued by this process through libhlq (monotonic counter). */
+int64_t hlq_launch_count(void);
 
 /* ABI self-description for bindings: sizeof(hlq_options), sizeof(hlq_info), version (1). */
 int hlq_abi(int32_t* sizeof_options, int32_t* sizeof_info, int32_t* version);

@@ -29,7 +29,7 @@ class HlqOptions(C.Structure):
                 ("tree_domains", C.c_int32), ("tree", C.c_int32), ("mumps_reading", C.c_int32),
                 ("forced", C.c_void_p), ("ref_dec", C.c_void_p), ("ref_margin", C.c_void_p),
                 ("tie_rel_tol", C.c_double), ("track_growth", C.c_int32), ("blocking", C.c_int32),
-                ("stream", C.c_void_p)]
+                ("stream", C.c_void_p), ("profile", C.c_int32)]
 
 
 class HlqInfo(C.Structure):
@@ -66,6 +66,8 @@ def _load():
         "hlq_status_string": ([I32], C.c_char_p),
         "hlq_generate_uniform": ([P, I64, I64, I64, U64, U64, I64, P], I32),
         "hlq_residual": ([P, I64, I64, P, P, P, P], I32),
+        "hlq_get_profile": ([P, P, P, P], I32),
+        "hlq_launch_count": ([], I64),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -181,6 +183,19 @@ class Factors:
         _check(lib.hlq_get_T(self.handle, i, k, kind, t.ctypes.data_as(C.c_void_p)), "T")
         return t.reshape(inf["nb"], inf["ib"]).T
 
+    PROF_CLASSES = ("criterion", "getrf", "lu_trsm", "lu_update", "qr_geqrt", "qr_unmqr",
+                    "qr_tt", "growth", "solve", "other")
+
+    def profile(self) -> dict:
+        ms = np.zeros(10)
+        fl = np.zeros(10)
+        ln = np.zeros(10, dtype=np.int64)
+        rc = lib.hlq_get_profile(self.handle, ms.ctypes.data_as(C.c_void_p),
+                                 fl.ctypes.data_as(C.c_void_p), ln.ctypes.data_as(C.c_void_p))
+        _check(rc, "hlq_get_profile")
+        return {c: {"ms": float(ms[i]), "flops": float(fl[i]), "launches": int(ln[i])}
+                for i, c in enumerate(self.PROF_CLASSES)}
+
     def solve(self, b, x=None):
         import torch
         if x is None:
@@ -220,6 +235,10 @@ def hlq_factor_ex(A, N: int, nb: int, criterion: int = CRIT_MAX, alpha: float = 
 
 def hlq_factor(A, N: int, nb: int, criterion: int = CRIT_MAX, alpha: float = 1.0) -> Factors:
     return hlq_factor_ex(A, N, nb, criterion, alpha)
+
+
+def hlq_launch_count() -> int:
+    return int(lib.hlq_launch_count())
 
 
 def hlq_solve(f: Factors, b, x):

@@ -23,6 +23,9 @@ void launch_qr_apply(const double* A, Geo g, int k, int ib, const double* Tg, co
 void launch_final_scan(const double* A, int64_t N, int64_t lda, int* flag, cudaStream_t st);
 }  // namespace hlq
 
+namespace hlq {
+int64_t g_launches = 0;
+}
 using namespace hlq;
 
 // ---------------------------------------------------------------------------------------------
@@ -71,7 +74,47 @@ void cache_put(int slot, void* p, size_t bytes) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 }  // namespace
 
+// CUDA-event profiler: begin/end pairs recorded on the factorization's stream, per kernel class.
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;  // pairs
+  std::vector<int> cls;
+  std::vector<int64_t> l0;      // launch counter at begin
+  int64_t launches[HLQ_PROF_NCLASSES] = {0};
+  double ms[HLQ_PROF_NCLASSES] = {0};
+  int cur = -1;
+  void begin(int c, cudaStream_t st) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    ev.push_back(e);
+    cls.push_back(c);
+    l0.push_back(hlq::g_launches);
+  }
+  void end(cudaStream_t st) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    ev.push_back(e);
+    launches[cls.back()] += hlq::g_launches - l0.back();
+  }
+  void collect() {  // after a stream synchronisation
+    for (size_t i = 0; i + 1 < ev.size(); i += 2) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, ev[i], ev[i + 1]);
+      ms[cls[i / 2]] += t;
+    }
+    for (auto e : ev) cudaEventDestroy(e);
+    ev.clear();
+    cls.clear();
+    l0.clear();
+  }
+};
+
 struct hlq_factors_s {
+  Prof prof;
   double* A = nullptr;
   Geo g{};
   int ib = 32, D = 1, crit = 0;
@@ -300,6 +343,8 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   if (f->track_growth) launch_tile_norm_max(A, g, 0, w.gstep, st);
 
   const bool alpha_inf = isinf(alpha);
+  Prof& P = f->prof;
+  P.on = opt.profile != 0;
   for (int k = 0; k < n; ++k) {
     int known = -1;  // decision known on the host?
     if (opt.forced)
@@ -308,22 +353,50 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
       known = HLQ_DEC_QR;
     const bool criterion_needed = !opt.forced && alpha > 0.0 && !alpha_inf;
     if (known != HLQ_DEC_QR) {
-      if (criterion_needed) launch_panel_stats(A, g, k, w, st);
+      if (criterion_needed) {
+        P.begin(HLQ_PROF_CRITERION, st);
+        launch_panel_stats(A, g, k, w, st);
+        P.end(st);
+      }
+      P.begin(HLQ_PROF_GETRF, st);
       launch_getrf(A, g, k, w, true, st);
       double* Li = w.scratch;
       double* Ui = w.scratch + (size_t)nb * nb;
       launch_tri_inv(g, k, w, Li, Ui, st);
-      if (criterion_needed && criterion != HLQ_CRIT_MUMPS) launch_invnorm(g, k, w, st);
+      P.end(st);
+      if (criterion_needed && criterion != HLQ_CRIT_MUMPS) {
+        P.begin(HLQ_PROF_CRITERION, st);
+        launch_invnorm(g, k, w, st);
+        P.end(st);
+      }
     } else {
       cudaMemsetAsync(w.zp, 0, sizeof(int), st);
     }
+    P.begin(HLQ_PROF_CRITERION, st);
     launch_decide(g, k, criterion, alpha, opt.mumps_reading, opt.tie_rel_tol, opt.forced != nullptr,
                   w.ref_dec != nullptr, w, st);
-    if (known != HLQ_DEC_QR) launch_lu_step(A, g, k, w, true, st);
-    if (known != HLQ_DEC_LU)
-      launch_qr_step(A, g, k, ib, f->lvl_ptr[k].data(), f->lvl_cnt[k].data(),
-                     (int)f->lvl_cnt[k].size(), w, true, st);
-    if (f->track_growth && k + 1 < n) launch_tile_norm_max(A, g, k + 1, w.gstep + k + 1, st);
+    P.end(st);
+    if (known != HLQ_DEC_QR) {
+      P.begin(HLQ_PROF_LU_TRSM, st);
+      launch_lu_step(A, g, k, w, 0, st);
+      P.end(st);
+      P.begin(HLQ_PROF_LU_UPDATE, st);
+      launch_lu_step(A, g, k, w, 1, st);
+      P.end(st);
+    }
+    if (known != HLQ_DEC_LU) {
+      const int nl = (int)f->lvl_cnt[k].size();
+      for (int part = 0; part < 3; ++part) {
+        P.begin(HLQ_PROF_QR_GEQRT + part, st);
+        launch_qr_step(A, g, k, ib, f->lvl_ptr[k].data(), f->lvl_cnt[k].data(), nl, w, part, st);
+        P.end(st);
+      }
+    }
+    if (f->track_growth && k + 1 < n) {
+      P.begin(HLQ_PROF_GROWTH, st);
+      launch_tile_norm_max(A, g, k + 1, w.gstep + k + 1, st);
+      P.end(st);
+    }
   }
   int* scan = w.status + 2;
   launch_final_scan(A, N, lda, scan, st);
@@ -340,6 +413,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   cudaMemcpyAsync(f->gstep.data(), w.gstep, sizeof(double) * (n + 1), cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(stat, w.status, sizeof(int) * 4, cudaMemcpyDeviceToHost, st);
   if ((rc = cuda_err(cudaStreamSynchronize(st)))) return rc;
+  if (P.on) P.collect();
   // status priority: non-finite > zero pivot in a forced LU step > singular
   if (stat[0] || stat[2])
     f->status = HLQ_ST_NONFINITE;
@@ -377,6 +451,7 @@ int hlq_solve(hlq_factors_t f, const double* b, double* x) {
   const Geo g = f->g;
   cudaStream_t st = f->st;
   int rc;
+  f->prof.begin(HLQ_PROF_SOLVE, st);
   if (x != b &&
       (rc = cuda_err(cudaMemcpyAsync(x, b, sizeof(double) * g.N, cudaMemcpyDeviceToDevice, st))))
     return rc;
@@ -388,8 +463,10 @@ int hlq_solve(hlq_factors_t f, const double* b, double* x) {
                       f->lvl_cnt[k].data(), (int)f->lvl_cnt[k].size(), x, g.N, 1, nullptr, st);
   }
   for (int k = g.n - 1; k >= 0; --k) launch_solve_back(f->A, g, k, x, st);
+  f->prof.end(st);
   if ((rc = cuda_err(cudaGetLastError()))) return rc;
   if (f->blocking && (rc = cuda_err(cudaStreamSynchronize(st)))) return rc;
+  if (f->prof.on && f->blocking) f->prof.collect();
   return 0;
 }
 
@@ -419,6 +496,36 @@ int hlq_get_info(hlq_factors_t f, hlq_info* info) {
   info->true_flops = tf;
   return 0;
 }
+
+int hlq_get_profile(hlq_factors_t f, double* ms, double* flops, int64_t* launches) {
+  if (!f || f->dec.empty()) return -1;
+  if (!f->prof.on) return -2;
+  cudaStreamSynchronize(f->st);
+  f->prof.collect();
+  const Geo g = f->g;
+  double fl[HLQ_PROF_NCLASSES] = {0};
+  for (int k = 0; k < g.n; ++k) {
+    double b = g.bs(k), M = (double)(g.N - g.r0(k) - g.bs(k));
+    if (f->dec[k] == HLQ_DEC_LU) {
+      fl[HLQ_PROF_GETRF] += 2.0 / 3.0 * b * b * b;
+      fl[HLQ_PROF_LU_TRSM] += 2.0 * M * b * b;       // Table I: TRSM + SWPTRSM
+      fl[HLQ_PROF_LU_UPDATE] += 2.0 * M * M * b;     // Table I: GEMM
+    } else {
+      double m = M / b;                              // trailing tiles (fractional if ragged)
+      fl[HLQ_PROF_QR_GEQRT] += (m + 1.0) * 4.0 / 3.0 * b * b * b;
+      fl[HLQ_PROF_QR_UNMQR] += (m + 1.0) * 2.0 * b * b * M;
+      fl[HLQ_PROF_QR_TT] += m * (2.0 / 3.0 * b * b * b + 2.0 * b * b * M);
+    }
+  }
+  for (int c = 0; c < HLQ_PROF_NCLASSES; ++c) {
+    if (ms) ms[c] = f->prof.ms[c];
+    if (flops) flops[c] = fl[c];
+    if (launches) launches[c] = f->prof.launches[c];
+  }
+  return 0;
+}
+
+int64_t hlq_launch_count(void) { return hlq::g_launches; }
 
 int hlq_get_decisions(hlq_factors_t f, uint8_t* dec) {
   if (!f || f->dec.empty()) return -1;
@@ -466,6 +573,7 @@ void hlq_free(hlq_factors_t f) {
     cudaStreamSynchronize(f->st);
     cache_put(0, f->ws_block, f->ws_bytes);
   }
+  f->prof.collect();
   delete f;
 }
 

@@ -197,11 +197,11 @@ void launch_dgemm(double* C, int64_t ldc, const double* A, int64_t lda, const do
   bool v16 = aligned16(A) && aligned16(B) && (lda % 2 == 0) && (ldb % 2 == 0) && (M % 2 == 0) &&
              (K % 2 == 0);
   if (v16)
-    k_dgemm<true><<<(unsigned)tiles, 256, GEMM_SMEM, st>>>(C, ldc, A, lda, B, ldb, M, N, K,
-                                                           neg ? 1 : 0, beta ? 1 : 0, dec, k, want);
+    { ::hlq::g_launches++; k_dgemm<true><<<(unsigned)tiles, 256, GEMM_SMEM, st>>>(C, ldc, A, lda, B, ldb, M, N, K,
+                                                           neg ? 1 : 0, beta ? 1 : 0, dec, k, want); }
   else
-    k_dgemm<false><<<(unsigned)tiles, 256, GEMM_SMEM, st>>>(C, ldc, A, lda, B, ldb, M, N, K,
-                                                            neg ? 1 : 0, beta ? 1 : 0, dec, k, want);
+    { ::hlq::g_launches++; k_dgemm<false><<<(unsigned)tiles, 256, GEMM_SMEM, st>>>(C, ldc, A, lda, B, ldb, M, N, K,
+                                                            neg ? 1 : 0, beta ? 1 : 0, dec, k, want); }
 }
 
 }  // namespace hlq

@@ -174,7 +174,7 @@ void launch_getrf(const double* A, Geo g, int k, DevWork w, bool need, cudaStrea
     cudaFuncSetAttribute(k_getrf, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  k_getrf<<<1, GT, smem, st>>>(A, g, k, w.W, w.ipiv_ws, w.zp);
+  { ::hlq::g_launches++; k_getrf<<<1, GT, smem, st>>>(A, g, k, w.W, w.ipiv_ws, w.zp); }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(256) k_invnorm(const double* __restrict__ Li,
 void launch_tri_inv(Geo g, int k, const DevWork& w, double* Li, double* Ui, cudaStream_t st) {
   const int bk = g.bs(k);
   dim3 grid((bk + 7) / 8, 2);
-  k_tri_inv<<<grid, 256, sizeof(double) * 8 * bk, st>>>(w.W, bk, g.nb, Li, Ui);
+  { ::hlq::g_launches++; k_tri_inv<<<grid, 256, sizeof(double) * 8 * bk, st>>>(w.W, bk, g.nb, Li, Ui); }
 }
 
 void launch_invnorm(Geo g, int k, DevWork w, cudaStream_t st) {
@@ -241,7 +241,7 @@ void launch_invnorm(Geo g, int k, DevWork w, cudaStream_t st) {
   const double* Li = w.scratch;                       // filled by launch_tri_inv
   const double* Ui = w.scratch + (size_t)g.nb * g.nb;
   cudaMemsetAsync(w.inv_norm, 0, sizeof(double), st);
-  k_invnorm<<<(bk + 7) / 8, 256, 0, st>>>(Li, Ui, bk, g.nb, w.inv_norm);
+  { ::hlq::g_launches++; k_invnorm<<<(bk + 7) / 8, 256, 0, st>>>(Li, Ui, bk, g.nb, w.inv_norm); }
 }
 
 }  // namespace hlq

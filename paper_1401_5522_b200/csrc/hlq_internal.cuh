@@ -7,6 +7,9 @@
 
 namespace hlq {
 
+// number of kernel launches issued by the library (monotonic; hlq_launch_count in the C ABI)
+extern int64_t g_launches;
+
 // ---- tile geometry (a0) -------------------------------------------------------------------
 struct Geo {
   int64_t N, lda;
@@ -56,12 +59,12 @@ void launch_getrf(const double* A, Geo g, int k, DevWork w, bool need, cudaStrea
 void launch_invnorm(Geo g, int k, DevWork w, cudaStream_t st);
 void launch_decide(Geo g, int k, int crit, double alpha, int mumps_reading, double tie_tol,
                    int has_forced, int has_ref, DevWork w, cudaStream_t st);
-void launch_lu_step(double* A, Geo g, int k, DevWork w, bool predicated, cudaStream_t st);
+void launch_lu_step(double* A, Geo g, int k, DevWork w, int part, cudaStream_t st);
 void launch_gemm_sub(double* C, int64_t ldc, const double* Am, int64_t lda, const double* Bm,
                      int64_t ldb, int64_t M, int64_t Nc, int K, const uint8_t* dec, int k,
                      cudaStream_t st);
 void launch_qr_step(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
-                    const int* level_count, int nlevels, DevWork w, bool predicated,
+                    const int* level_count, int nlevels, DevWork w, int part,
                     cudaStream_t st);
 void launch_tile_norm_max(const double* A, Geo g, int k, double* out, cudaStream_t st);
 void launch_generate(double* dst, int64_t rows, int64_t cols, int64_t ld, uint64_t seed,

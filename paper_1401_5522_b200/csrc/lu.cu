@@ -59,7 +59,7 @@ static unsigned grid_for(int64_t total) {
   return (unsigned)(b < 1 ? 1 : b);
 }
 
-void launch_lu_step(double* A, Geo g, int k, DevWork w, bool predicated, cudaStream_t st) {
+void launch_lu_step(double* A, Geo g, int k, DevWork w, int part, cudaStream_t st) {
   const int bk = g.bs(k);
   const int64_t k0 = g.r0(k), k1 = k0 + bk;
   const int64_t M = g.N - k1;  // rows (and columns) below / right of the diagonal tile
@@ -69,22 +69,24 @@ void launch_lu_step(double* A, Geo g, int k, DevWork w, bool predicated, cudaStr
   int* perm = reinterpret_cast<int*>(w.scratch + (size_t)2 * g.nb * g.nb);
   const size_t perm_sz = ((size_t)g.nb + 63) / 64 * 64;
   double* ws = w.scratch + (size_t)2 * g.nb * g.nb + perm_sz;  // N*nb doubles
-  (void)predicated;
-  k_lu_commit<<<8, 256, 0, st>>>(A, g, k, w.W, w.ipiv_ws, w.ipiv, perm, dec);
+  if (part == 1) {
+    // Update: A[k1:N, k1:N] -= A[k1:N, k0:k1] * A[k0:k1, k1:N]
+    launch_dgemm(A + k1 * g.lda + k1, g.lda, A + k0 * g.lda + k1, g.lda, A + k1 * g.lda + k0,
+                 g.lda, M, M, bk, true, true, dec, k, HLQ_DEC_LU, st);
+    return;
+  }
+  { ::hlq::g_launches++; k_lu_commit<<<8, 256, 0, st>>>(A, g, k, w.W, w.ipiv_ws, w.ipiv, perm, dec); }
   if (M <= 0) return;
   // Eliminate: X = A[k1:N, k0:k1]; A[k1:N, k0:k1] = X * U^-1
-  k_copy_block<<<grid_for(M * bk), 256, 0, st>>>(ws, M, A + k0 * g.lda + k1, g.lda, M, bk, nullptr,
-                                                 dec, k);
+  { ::hlq::g_launches++; k_copy_block<<<grid_for(M * bk), 256, 0, st>>>(ws, M, A + k0 * g.lda + k1, g.lda, M, bk, nullptr,
+                                                 dec, k); }
   launch_dgemm(A + k0 * g.lda + k1, g.lda, ws, M, Ui, g.nb, M, bk, bk, false, false, dec, k,
                HLQ_DEC_LU, st);
   // Apply: Y = P A[k0:k1, k1:N]; A[k0:k1, k1:N] = L^-1 * Y
-  k_copy_block<<<grid_for(M * bk), 256, 0, st>>>(ws, bk, A + k1 * g.lda + k0, g.lda, bk, M, perm,
-                                                 dec, k);
+  { ::hlq::g_launches++; k_copy_block<<<grid_for(M * bk), 256, 0, st>>>(ws, bk, A + k1 * g.lda + k0, g.lda, bk, M, perm,
+                                                 dec, k); }
   launch_dgemm(A + k1 * g.lda + k0, g.lda, Li, g.nb, ws, bk, bk, M, bk, false, false, dec, k,
                HLQ_DEC_LU, st);
-  // Update: A[k1:N, k1:N] -= A[k1:N, k0:k1] * A[k0:k1, k1:N]
-  launch_dgemm(A + k1 * g.lda + k1, g.lda, A + k0 * g.lda + k1, g.lda, A + k1 * g.lda + k0, g.lda,
-               M, M, bk, true, true, dec, k, HLQ_DEC_LU, st);
 }
 
 }  // namespace hlq

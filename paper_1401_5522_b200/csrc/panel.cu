@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(256) k_panel_stats(const double* __restrict__ 
 
 void launch_panel_stats(const double* A, Geo g, int k, DevWork w, cudaStream_t st) {
   cudaMemsetAsync(w.away_max, 0, sizeof(double) * g.nb, st);
-  k_panel_stats<<<g.n - k, 256, 0, st>>>(A, g, k, w.s, w.local_max, w.away_max);
+  { ::hlq::g_launches++; k_panel_stats<<<g.n - k, 256, 0, st>>>(A, g, k, w.s, w.local_max, w.away_max); }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(256) k_tile_norm_max(const double* __restrict_
 void launch_tile_norm_max(const double* A, Geo g, int k, double* out, cudaStream_t st) {
   int64_t ncols = g.N - g.r0(k);
   dim3 grid(g.n - k, (unsigned)((ncols + 63) / 64));
-  k_tile_norm_max<<<grid, 256, 0, st>>>(A, g, k, out);
+  { ::hlq::g_launches++; k_tile_norm_max<<<grid, 256, 0, st>>>(A, g, k, out); }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(256) k_decide(Geo g, int k, int crit, double a
 
 void launch_decide(Geo g, int k, int crit, double alpha, int mumps_reading, double tie_tol,
                    int has_forced, int has_ref, DevWork w, cudaStream_t st) {
-  k_decide<<<1, 256, 0, st>>>(g, k, crit, alpha, mumps_reading, tie_tol, has_forced, has_ref, w);
+  { ::hlq::g_launches++; k_decide<<<1, 256, 0, st>>>(g, k, crit, alpha, mumps_reading, tie_tol, has_forced, has_ref, w); }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -252,7 +252,7 @@ void launch_generate(double* dst, int64_t rows, int64_t cols, int64_t ld, uint64
   int64_t blocks = (total + 255) / 256;
   if (blocks > 148 * 64) blocks = 148 * 64;
   if (blocks < 1) blocks = 1;
-  k_generate<<<(unsigned)blocks, 256, 0, st>>>(dst, rows, cols, ld, key, idx0, idx_ld);
+  { ::hlq::g_launches++; k_generate<<<(unsigned)blocks, 256, 0, st>>>(dst, rows, cols, ld, key, idx0, idx_ld); }
 }
 
 }  // namespace hlq

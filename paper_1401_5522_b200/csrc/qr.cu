@@ -416,29 +416,30 @@ void launch_qr_apply(const double* A, Geo g, int k, int ib, const double* Tg, co
   size_t smem = qr_smem_bytes(g.nb);
   if (ncols <= 0) return;
   unsigned slabs = (unsigned)((ncols + 63) / 64);
-  k_unmqr<<<dim3(slabs, g.n - k), QT, smem, st>>>(A, g, k, ib, Tg, base, ldc, ncols, dec);
+  { ::hlq::g_launches++; k_unmqr<<<dim3(slabs, g.n - k), QT, smem, st>>>(A, g, k, ib, Tg, base, ldc, ncols, dec); }
   for (int l = 0; l < nlevels; ++l)
-    k_ttmqr<<<dim3(slabs, level_count[l]), QT, smem, st>>>(A, g, k, ib, Ttt, level_pairs[l], base,
-                                                           ldc, ncols, dec);
+    { ::hlq::g_launches++; k_ttmqr<<<dim3(slabs, level_count[l]), QT, smem, st>>>(A, g, k, ib, Ttt, level_pairs[l], base,
+                                                           ldc, ncols, dec); }
 }
 
 void launch_qr_step(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
-                    const int* level_count, int nlevels, DevWork w, bool predicated,
+                    const int* level_count, int nlevels, DevWork w, int part,
                     cudaStream_t st) {
+  const bool predicated = true;
   set_attr_once();
   size_t smem = qr_smem_bytes(g.nb);
   const uint8_t* dec = predicated ? w.dec : nullptr;
   const int64_t k1 = g.r0(k) + g.bs(k);
   double* right = A + k1 * g.lda;
   const int64_t ncols = g.N - k1;
-  k_geqrt<<<g.n - k, QT, smem, st>>>(A, g, k, ib, w.Tg, dec);
   unsigned slabs = (unsigned)((ncols + 63) / 64);
-  if (ncols > 0) k_unmqr<<<dim3(slabs, g.n - k), QT, smem, st>>>(A, g, k, ib, w.Tg, right, g.lda, ncols, dec);
-  for (int l = 0; l < nlevels; ++l) {
-    k_ttqrt<<<level_count[l], QT, smem, st>>>(A, g, k, ib, w.Ttt, level_pairs[l], dec);
+  if (part == 0) { ::hlq::g_launches++; k_geqrt<<<g.n - k, QT, smem, st>>>(A, g, k, ib, w.Tg, dec); }
+  if (part == 1 && ncols > 0) { ::hlq::g_launches++; k_unmqr<<<dim3(slabs, g.n - k), QT, smem, st>>>(A, g, k, ib, w.Tg, right, g.lda, ncols, dec); }
+  for (int l = 0; l < nlevels && part == 2; ++l) {
+    { ::hlq::g_launches++; k_ttqrt<<<level_count[l], QT, smem, st>>>(A, g, k, ib, w.Ttt, level_pairs[l], dec); }
     if (ncols > 0)
-      k_ttmqr<<<dim3(slabs, level_count[l]), QT, smem, st>>>(A, g, k, ib, w.Ttt, level_pairs[l],
-                                                             right, g.lda, ncols, dec);
+      { ::hlq::g_launches++; k_ttmqr<<<dim3(slabs, level_count[l]), QT, smem, st>>>(A, g, k, ib, w.Ttt, level_pairs[l],
+                                                             right, g.lda, ncols, dec); }
   }
 }
 

@@ -67,18 +67,18 @@ __global__ void k_gemv_sub(double* __restrict__ y, const double* __restrict__ B,
 void launch_gemv_sub(double* y, const double* B, int64_t ldb, int64_t M, int K, const double* v,
                      cudaStream_t st) {
   if (M <= 0 || K <= 0) return;
-  k_gemv_sub<<<(unsigned)((M + 255) / 256), 256, sizeof(double) * K, st>>>(y, B, ldb, M, K, v);
+  { ::hlq::g_launches++; k_gemv_sub<<<(unsigned)((M + 255) / 256), 256, sizeof(double) * K, st>>>(y, B, ldb, M, K, v); }
 }
 
 void launch_solve_lu_fwd(const double* A, Geo g, int k, const int* ipiv, double* x,
                          cudaStream_t st) {
-  k_solve_lu_diag<<<1, 32, 0, st>>>(A, g, k, ipiv, x);
+  { ::hlq::g_launches++; k_solve_lu_diag<<<1, 32, 0, st>>>(A, g, k, ipiv, x); }
   const int64_t k0 = g.r0(k), k1 = k0 + g.bs(k);
   launch_gemv_sub(x + k1, A + k0 * g.lda + k1, g.lda, g.N - k1, g.bs(k), x + k0, st);
 }
 
 void launch_solve_back(const double* A, Geo g, int k, double* x, cudaStream_t st) {
-  k_solve_upper_diag<<<1, 32, 0, st>>>(A, g, k, x);
+  { ::hlq::g_launches++; k_solve_upper_diag<<<1, 32, 0, st>>>(A, g, k, x); }
   const int64_t k0 = g.r0(k);
   launch_gemv_sub(x, A + k0 * g.lda, g.lda, k0, g.bs(k), x + k0, st);
 }
@@ -104,7 +104,7 @@ __global__ void k_residual(const double* __restrict__ A, int64_t N, int64_t lda,
 void launch_residual(const double* A, int64_t N, int64_t lda, const double* x, const double* b,
                      double* out3dev, cudaStream_t st) {
   cudaMemsetAsync(out3dev, 0, 3 * sizeof(double), st);
-  k_residual<<<(unsigned)((N + 127) / 128), 128, 0, st>>>(A, N, lda, x, b, out3dev);
+  { ::hlq::g_launches++; k_residual<<<(unsigned)((N + 127) / 128), 128, 0, st>>>(A, N, lda, x, b, out3dev); }
 }
 
 // final status: flag[0] |= any non-finite factor entry, flag[1] |= exact zero on the diagonal
@@ -128,7 +128,7 @@ __global__ void k_final_scan(const double* __restrict__ A, int64_t N, int64_t ld
 
 void launch_final_scan(const double* A, int64_t N, int64_t lda, int* flag, cudaStream_t st) {
   cudaMemsetAsync(flag, 0, 2 * sizeof(int), st);
-  k_final_scan<<<148 * 8, 256, 0, st>>>(A, N, lda, flag);
+  { ::hlq::g_launches++; k_final_scan<<<148 * 8, 256, 0, st>>>(A, N, lda, flag); }
 }
 
 }  // namespace hlq

@@ -28,7 +28,14 @@ def H():
 
 def run_pair(H, A, b, nb, crit=O.CRIT_MAX, alpha=1.0, D=1, forced=None, mumps_reading=0):
     N = A.shape[0]
-    fo = O.hybrid_factor(A, nb, crit, alpha, D=D, forced=forced, mumps_reading=mumps_reading)
+    pre = {}
+
+    def hook(k, Ab, Aa, d):
+        sl = O.tsl(N, nb, k)
+        pre[k] = Ab[sl, sl].copy()
+    fo = O.hybrid_factor(A, nb, crit, alpha, D=D, forced=forced, mumps_reading=mumps_reading,
+                         on_step=hook)
+    fo.pre_tiles = pre
     dA = H.to_colmajor(A)
     kw = dict(tree_domains=D, mumps_reading=mumps_reading)
     if forced is not None:
@@ -41,14 +48,33 @@ def run_pair(H, A, b, nb, crit=O.CRIT_MAX, alpha=1.0, D=1, forced=None, mumps_re
     return fo, f, H.from_colmajor(dA), x
 
 
-def check_parity(fo, f, F, x, A, b, tol=1e-10, hpl=16.0):
+def check_parity(fo, f, F, x, A, b, tol=1e-10, hpl=16.0, allow_pivot_ties=False):
     dec = f.decisions()
     np.testing.assert_array_equal(dec, fo.dec)
     piv = f.pivots()
+    ties = False
     for k, ip in fo.ipiv.items():
+        if allow_pivot_ties and not np.array_equal(piv[k, :len(ip)], ip):
+            # several pivot sequences are correct when the column maxima tie up to rounding
+            # (structured matrices after QR steps): check the GPU's choice is a valid partial-
+            # pivoting LU of the (oracle's) pre-step tile instead of comparing it to the oracle's.
+            ties = True
+            sl = O.tsl(fo.N, fo.nb, k)
+            Wg = F[sl, sl]
+            bsz = Wg.shape[0]
+            L = np.tril(Wg, -1) + np.eye(bsz)
+            U = np.triu(Wg)
+            PA = fo.pre_tiles[k].copy()
+            for c in range(bsz):
+                p = int(piv[k, c])
+                PA[[c, p], :] = PA[[p, c], :]
+            assert np.abs(np.tril(Wg, -1)).max() <= 1.0 + 1e-12
+            assert np.linalg.norm(PA - L @ U) <= 1e-12 * bsz * np.linalg.norm(PA)
+            continue
         np.testing.assert_array_equal(piv[k, :len(ip)], ip)
     diff = O.factor_diff(F, fo.A)
-    assert diff <= tol, f"factor diff {diff:.3e}"
+    if not ties:
+        assert diff <= tol, f"factor diff {diff:.3e}"
     g = f.growth()
     assert g == pytest.approx(fo.growth, rel=max(tol, 1e-10))
     h3 = O.hpl3(A, x, b)
@@ -138,6 +164,25 @@ def test_kronecker_worst_case_bit_exact(H, alpha, growth):
     assert np.all(f.step_flags()[:-1] & H.FLAG_NEAR_TIE)
 
 
+def check_valid_nonunique(fo, f, A, b, x, H, nrhs=3):
+    """Stress matrices whose tiles are (numerically) rank deficient: the Householder vectors of a
+    rank-deficient tile, hence the complement of Q and the trailing matrix of a QR step, are not
+    unique -- rounding decides them (reading 30).  What is unique is compared
+    (decisions, the solution x), the rest is checked for validity (HPL3 of several right-hand sides
+    solved with the GPU's own factors, growth finite)."""
+    np.testing.assert_array_equal(f.decisions(), fo.dec)
+    xo = O.solve(fo, b)
+    kappa = np.linalg.cond(A, 1)
+    assert np.linalg.norm(x - xo) <= 100 * kappa * 2.2e-16 * np.linalg.norm(xo)
+    assert O.hpl3(A, x, b) <= 16
+    rng = np.random.default_rng(7)
+    for _ in range(nrhs):
+        bb = rng.standard_normal(A.shape[0])
+        xx = f.solve(torch.from_numpy(bb).cuda()).cpu().numpy()
+        assert O.hpl3(A, xx, bb) <= 16
+    assert math.isfinite(f.growth())
+
+
 @pytest.mark.parametrize("which", ["C4A", "C4B", "C4C"])
 @pytest.mark.parametrize("crit", [O.CRIT_MAX, O.CRIT_SUM, O.CRIT_MUMPS])
 def test_stress_matrices(H, which, crit):
@@ -154,8 +199,12 @@ def test_stress_matrices(H, which, crit):
         # designed failure: all exact-tie LU steps; the last column grows like 2^(N-1)
         assert set(f.decisions()) == {O.LU}
         assert f.status in (0, 1)
+        np.testing.assert_array_equal(F, fo.A)  # exact ties + binary-fraction arithmetic
         return
-    check_parity(fo, f, F, x, A, b)
+    if which == "C4C":
+        check_parity(fo, f, F, x, A, b)
+    else:
+        check_valid_nonunique(fo, f, A, b, x, H)
 
 
 def test_T_factors_match_oracle(H):
@@ -187,7 +236,10 @@ def test_device_residual_matches_host(H):
     dA = H.to_colmajor(A)
     x = np.linalg.solve(A, b)
     r = H.hlq_residual(dA, 1024, 1024, torch.from_numpy(x).cuda(), torch.from_numpy(b).cuda())
-    assert r["hpl3"] == pytest.approx(O.hpl3(A, x, b), rel=1e-6, abs=1e-6)
+    assert r["A_inf"] == pytest.approx(np.max(np.sum(np.abs(A), axis=1)), rel=1e-13)
+    assert r["x_inf"] == np.max(np.abs(x))
+    # ||Ax - b|| of a backward-stable solution is rounding noise: summation order changes it
+    assert r["hpl3"] == pytest.approx(O.hpl3(A, x, b), rel=0.25)
 
 
 def test_invalid_arguments(H):
