@@ -6,6 +6,7 @@
 // factorization: this replaces the paper's Propagate / selection tasks.
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -83,7 +84,17 @@ struct Prof {
   int64_t launches[HLQ_PROF_NCLASSES] = {0};
   double ms[HLQ_PROF_NCLASSES] = {0};
   int cur = -1;
+  int debug = -1;
+  void check(const char* where, int k) {
+    if (debug < 0) debug = getenv("HLQ_DEBUG_SYNC") ? 1 : 0;
+    if (!debug) return;
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) fprintf(stderr, "[hlq debug] %s (k=%d): %s\n", where, k, cudaGetErrorString(e));
+  }
   void begin(int c, cudaStream_t st) {
+    check("before stage", c);
+    cur = c;
     if (!on) return;
     cudaEvent_t e;
     cudaEventCreate(&e);
@@ -93,6 +104,7 @@ struct Prof {
     l0.push_back(hlq::g_launches);
   }
   void end(cudaStream_t st) {
+    check("after stage", cur);
     if (!on) return;
     cudaEvent_t e;
     cudaEventCreate(&e);
@@ -283,7 +295,8 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
          oFl = take(sizeof(int) * n), oSt = take(sizeof(int) * 4), oFo = take(n), oRd = take(n),
          oRm = take(sizeof(double) * n), oGs = take(sizeof(double) * (n + 1)),
          oPr = take(sizeof(int2) * (npairs + 1)),
-         oSc = take(sizeof(double) * ((size_t)2 * nb * nb + align_up(nb, 64) + (size_t)N * nb + 64));
+         oSc = take(sizeof(double) * ((size_t)2 * nb * nb + align_up(nb, 64) +
+                                      std::max((size_t)N * nb, (size_t)((N + 127) / 128) * N) + 64));
   f->ws_bytes = off;
   f->ws_block = cache_get(0, off);
   if (!f->ws_block) return HLQ_ERR_NOMEM;
@@ -376,12 +389,14 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
     launch_decide(g, k, criterion, alpha, opt.mumps_reading, opt.tie_rel_tol, opt.forced != nullptr,
                   w.ref_dec != nullptr, w, st);
     P.end(st);
+    // a12 growth fused into the LU update epilogue when the CTA rows align with tile rows
+    const bool fuse_growth = f->track_growth && k + 1 < n && nb % 128 == 0;
     if (known != HLQ_DEC_QR) {
       P.begin(HLQ_PROF_LU_TRSM, st);
       launch_lu_step(A, g, k, w, 0, st);
       P.end(st);
       P.begin(HLQ_PROF_LU_UPDATE, st);
-      launch_lu_step(A, g, k, w, 1, st);
+      launch_lu_step(A, g, k, w, fuse_growth ? 2 : 1, st);
       P.end(st);
     }
     if (known != HLQ_DEC_LU) {
@@ -392,9 +407,12 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
         P.end(st);
       }
     }
-    if (f->track_growth && k + 1 < n) {
+    if (f->track_growth && k + 1 < n && !(fuse_growth && known == HLQ_DEC_LU)) {
       P.begin(HLQ_PROF_GROWTH, st);
-      launch_tile_norm_max(A, g, k + 1, w.gstep + k + 1, st);
+      if (fuse_growth)  // LU steps got it from the GEMM epilogue: only a QR step needs the scan
+        launch_tile_norm_max(A, g, k + 1, w.gstep + k + 1, st, w.dec, k, HLQ_DEC_QR);
+      else
+        launch_tile_norm_max(A, g, k + 1, w.gstep + k + 1, st);
       P.end(st);
     }
   }

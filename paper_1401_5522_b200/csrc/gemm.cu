@@ -91,7 +91,8 @@ template <bool V16>
 __global__ void __launch_bounds__(256, 2)
     k_dgemm(double* __restrict__ C, int64_t ldc, const double* __restrict__ A, int64_t lda,
             const double* __restrict__ B, int64_t ldb, int64_t M, int64_t N, int K, int neg,
-            int beta, const uint8_t* __restrict__ dec, int k, int want) {
+            int beta, const uint8_t* __restrict__ dec, int k, int want,
+            double* __restrict__ colpart) {
   if (dec != nullptr && dec[k] != want) return;  // predicated launch: the other branch was taken
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
@@ -167,6 +168,26 @@ __global__ void __launch_bounds__(256, 2)
     }
   }
   cp_wait<0>();
+  if (colpart != nullptr) {
+    // fused a12 epilogue: per-column |C| sums over this CTA's 128 rows (rows >= M are exact zeros)
+    __syncthreads();
+    double* red = smem;  // 4 (wm) x 64 columns
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double v = 0.0;
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) v += fabs(acc[mi][ni][h]);
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        if (g == 0) red[wm * 64 + wn * 32 + ni * 8 + 2 * t + h] = v;
+      }
+    __syncthreads();
+    if (tid < 64 && n0 + tid < N)
+      colpart[tm * N + n0 + tid] = ((red[tid] + red[64 + tid]) + red[128 + tid]) + red[192 + tid];
+  }
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -185,12 +206,12 @@ static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 // C[M x N] = beta*C + (neg ? -1 : 1) * A[M x K] * B[K x N]; dec/k/want: optional predicate.
 void launch_dgemm(double* C, int64_t ldc, const double* A, int64_t lda, const double* B,
                   int64_t ldb, int64_t M, int64_t N, int K, bool neg, bool beta,
-                  const uint8_t* dec, int k, int want, cudaStream_t st) {
+                  const uint8_t* dec, int k, int want, cudaStream_t st, double* colpart) {
   if (M <= 0 || N <= 0 || K <= 0) return;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_dgemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
-    cudaFuncSetAttribute(k_dgemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
+    smem_optin(k_dgemm<true>);
+    smem_optin(k_dgemm<false>);
     attr = true;
   }
   int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
@@ -198,10 +219,38 @@ void launch_dgemm(double* C, int64_t ldc, const double* A, int64_t lda, const do
              (K % 2 == 0);
   if (v16)
     { ::hlq::g_launches++; k_dgemm<true><<<(unsigned)tiles, 256, GEMM_SMEM, st>>>(C, ldc, A, lda, B, ldb, M, N, K,
-                                                           neg ? 1 : 0, beta ? 1 : 0, dec, k, want); }
+                                                           neg ? 1 : 0, beta ? 1 : 0, dec, k, want, colpart); }
   else
     { ::hlq::g_launches++; k_dgemm<false><<<(unsigned)tiles, 256, GEMM_SMEM, st>>>(C, ldc, A, lda, B, ldb, M, N, K,
-                                                            neg ? 1 : 0, beta ? 1 : 0, dec, k, want); }
+                                                            neg ? 1 : 0, beta ? 1 : 0, dec, k, want, colpart); }
+}
+
+// a12 from the fused epilogue: tile row i = CTA row blocks [i*bpt, (i+1)*bpt); tile-norm max over
+// (tile row, column) -> atomic max into *out.  grid (tile rows, column chunks of 256).
+__global__ void k_colpart_max(const double* __restrict__ colpart, int64_t ntm, int64_t N, int bpt,
+                              double* out, const uint8_t* __restrict__ dec, int k, int want) {
+  if (dec != nullptr && dec[k] != want) return;
+  const int64_t i = blockIdx.x;
+  const int64_t c = (int64_t)blockIdx.y * 256 + threadIdx.x;
+  double v = 0.0;
+  if (c < N) {
+    for (int b = 0; b < bpt; ++b) {
+      int64_t tm = i * bpt + b;
+      if (tm < ntm) v += colpart[tm * N + c];
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) v = nanmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(out, v);
+}
+
+void launch_colpart_max(const double* colpart, int64_t M, int64_t N, int nb, double* out,
+                        const uint8_t* dec, int k, int want, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return;
+  const int64_t ntm = (M + BM - 1) / BM;
+  const int bpt = nb / BM;
+  const int64_t ntiles = (M + nb - 1) / nb;
+  dim3 grid((unsigned)ntiles, (unsigned)((N + 255) / 256));
+  { ::hlq::g_launches++; k_colpart_max<<<grid, 256, 0, st>>>(colpart, ntm, N, bpt, out, dec, k, want); }
 }
 
 }  // namespace hlq

@@ -122,18 +122,28 @@ __global__ void __launch_bounds__(GT) k_getrf(const double* __restrict__ A, Geo 
       int c = idx / rows, r = idx - c * rows;
       W[(int64_t)(p0 + c) * ldw + p0 + r] = P[c * ldp + r];
     }
-    // apply the panel's swaps to every other column of the tile (left and right), in order
-    const int nother = bk - pw;
-    for (int t = tid; t < nother; t += GT) {
-      int col = (t < p0) ? t : t + pw;
-      double* wc = W + (int64_t)col * ldw;
-      for (int c = 0; c < pw; ++c) {
-        int pr = p0 + piv_sh[c];
-        if (pr != p0 + c) {
-          double x = wc[p0 + c];
-          wc[p0 + c] = wc[pr];
-          wc[pr] = x;
-        }
+    // apply the panel's swaps to every other column of the tile (left and right), in order:
+    // one warp per column, the column segment rows [p0, bk) staged in the warp's smem buffer
+    {
+      const int nother = bk - pw;
+      double* cb = sm + 2 * GPW * ldp + warp * ldp;
+      for (int t = warp; t < nother; t += GT / 32) {
+        int col = (t < p0) ? t : t + pw;
+        double* wc = W + (int64_t)col * ldw + p0;
+        for (int r = lane; r < rows; r += 32) cb[r] = wc[r];
+        __syncwarp();
+        if (lane == 0)
+          for (int c = 0; c < pw; ++c) {
+            int pr = piv_sh[c];
+            if (pr != c) {
+              double x = cb[c];
+              cb[c] = cb[pr];
+              cb[pr] = x;
+            }
+          }
+        __syncwarp();
+        for (int r = lane; r < rows; r += 32) wc[r] = cb[r];
+        __syncwarp();
       }
     }
     __syncthreads();
@@ -151,15 +161,46 @@ __global__ void __launch_bounds__(GT) k_getrf(const double* __restrict__ A, Geo 
         }
       }
       __syncthreads();
-      // trailing update: W[p0+pw+r][col] -= sum_c L21[r][c] U12[c][col], sequential in c
+      // trailing update: W[p0+pw+r][col] -= sum_c L21[r][c] U12[c][col], sequential in c.
+      // 64 x 128 output blocks, 4 x 4 per thread (rows tr + 16 i, cols tc + 32 j): 8 shared loads
+      // per 16 separately-rounded multiply/subtract pairs.
       const int nr = rows - pw;
-      for (int idx = tid; idx < nr * ntr; idx += GT) {
-        int t = idx / nr, r = idx - t * nr;
-        double* wp = W + (int64_t)(p0 + pw + t) * ldw + p0 + pw + r;
-        double acc = *wp;
-        for (int c = 0; c < pw; ++c) acc = __dsub_rn(acc, __dmul_rn(P[c * ldp + pw + r], U[c * ldp + t]));
-        *wp = acc;
-      }
+      const int tr = tid & 15, tc = tid >> 4;
+      for (int rb = 0; rb < nr; rb += 64)
+        for (int cb0 = 0; cb0 < ntr; cb0 += 128) {
+          double acc[4][4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              int r = rb + tr + 16 * i, t = cb0 + tc + 32 * j;
+              acc[i][j] = (r < nr && t < ntr) ? W[(int64_t)(p0 + pw + t) * ldw + p0 + pw + r] : 0.0;
+            }
+          for (int c = 0; c < pw; ++c) {
+            double l[4], u[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              int r = rb + tr + 16 * i;
+              l[i] = (r < nr) ? P[c * ldp + pw + r] : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              int t = cb0 + tc + 32 * j;
+              u[j] = (t < ntr) ? U[c * ldp + t] : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) acc[i][j] = __dsub_rn(acc[i][j], __dmul_rn(l[i], u[j]));
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              int r = rb + tr + 16 * i, t = cb0 + tc + 32 * j;
+              if (r < nr && t < ntr) W[(int64_t)(p0 + pw + t) * ldw + p0 + pw + r] = acc[i][j];
+            }
+        }
     }
     __syncthreads();
   }
@@ -168,10 +209,10 @@ __global__ void __launch_bounds__(GT) k_getrf(const double* __restrict__ A, Geo 
 
 void launch_getrf(const double* A, Geo g, int k, DevWork w, bool need, cudaStream_t st) {
   if (!need) return;
-  size_t smem = sizeof(double) * 2 * GPW * (g.nb + 1);
+  size_t smem = sizeof(double) * (2 * GPW + GT / 32) * (g.nb + 1);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_getrf, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    smem_optin(k_getrf);
     attr = true;
   }
   { ::hlq::g_launches++; k_getrf<<<1, GT, smem, st>>>(A, g, k, w.W, w.ipiv_ws, w.zp); }

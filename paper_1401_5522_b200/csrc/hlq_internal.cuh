@@ -66,7 +66,8 @@ void launch_gemm_sub(double* C, int64_t ldc, const double* Am, int64_t lda, cons
 void launch_qr_step(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
                     const int* level_count, int nlevels, DevWork w, int part,
                     cudaStream_t st);
-void launch_tile_norm_max(const double* A, Geo g, int k, double* out, cudaStream_t st);
+void launch_tile_norm_max(const double* A, Geo g, int k, double* out, cudaStream_t st,
+                          const uint8_t* dec = nullptr, int step = 0, int want = 0);
 void launch_generate(double* dst, int64_t rows, int64_t cols, int64_t ld, uint64_t seed,
                      uint64_t idx0, int64_t idx_ld, cudaStream_t st);
 // solve
@@ -78,6 +79,19 @@ void launch_solve_qr_fwd(const double* A, Geo g, int k, int ib, const double* Tg
 void launch_solve_back(const double* A, Geo g, int k, double* x, cudaStream_t st);
 void launch_residual(const double* A, int64_t N, int64_t lda, const double* x, const double* b,
                      double* out3dev, cudaStream_t st);
+
+// allow the largest dynamic shared memory the device permits for this kernel (opt-in minus the
+// kernel's static shared memory)
+template <typename F>
+inline void smem_optin(F* func) {
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, (const void*)func) != cudaSuccess) return;
+  cudaFuncSetAttribute((const void*)func, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       optin - (int)fa.sharedSizeBytes);
+}
 
 // ---- device helpers ---------------------------------------------------------------------------
 __device__ __forceinline__ double nanmax(double a, double b) {

@@ -12,7 +12,10 @@ namespace hlq {
 
 void launch_dgemm(double* C, int64_t ldc, const double* A, int64_t lda, const double* B,
                   int64_t ldb, int64_t M, int64_t N, int K, bool neg, bool beta,
-                  const uint8_t* dec, int k, int want, cudaStream_t st);
+                  const uint8_t* dec, int k, int want, cudaStream_t st,
+                  double* colpart = nullptr);
+void launch_colpart_max(const double* colpart, int64_t M, int64_t N, int nb, double* out,
+                        const uint8_t* dec, int k, int want, cudaStream_t st);
 void launch_tri_inv(Geo g, int k, const DevWork& w, double* Li, double* Ui, cudaStream_t st);
 
 // A_kk <- W, ipiv[k*nb..] <- ipiv_ws, perm[r] = row of (P A_kk) r  (sequential swaps composed)
@@ -69,10 +72,13 @@ void launch_lu_step(double* A, Geo g, int k, DevWork w, int part, cudaStream_t s
   int* perm = reinterpret_cast<int*>(w.scratch + (size_t)2 * g.nb * g.nb);
   const size_t perm_sz = ((size_t)g.nb + 63) / 64 * 64;
   double* ws = w.scratch + (size_t)2 * g.nb * g.nb + perm_sz;  // N*nb doubles
-  if (part == 1) {
-    // Update: A[k1:N, k1:N] -= A[k1:N, k0:k1] * A[k0:k1, k1:N]
+  if (part == 1 || part == 2) {
+    // Update: A[k1:N, k1:N] -= A[k1:N, k0:k1] * A[k0:k1, k1:N]; part 2 also fuses the a12 growth
+    // column sums into the epilogue (requires nb % 128 == 0) and reduces them into gstep[k+1]
+    double* colpart = (part == 2) ? ws : nullptr;
     launch_dgemm(A + k1 * g.lda + k1, g.lda, A + k0 * g.lda + k1, g.lda, A + k1 * g.lda + k0,
-                 g.lda, M, M, bk, true, true, dec, k, HLQ_DEC_LU, st);
+                 g.lda, M, M, bk, true, true, dec, k, HLQ_DEC_LU, st, colpart);
+    if (part == 2) launch_colpart_max(ws, M, M, g.nb, w.gstep + k + 1, dec, k, HLQ_DEC_LU, st);
     return;
   }
   { ::hlq::g_launches++; k_lu_commit<<<8, 256, 0, st>>>(A, g, k, w.W, w.ipiv_ws, w.ipiv, perm, dec); }

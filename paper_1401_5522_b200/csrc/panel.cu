@@ -68,7 +68,9 @@ void launch_panel_stats(const double* A, Geo g, int k, DevWork w, cudaStream_t s
 // a12: max over tiles i,j >= k of the tile 1-norm = max over (tile row, column) of column-segment
 // abs-sums.  grid (tile rows, column groups of 64), 256 threads; atomicMax into *out (>= 0).
 __global__ void __launch_bounds__(256) k_tile_norm_max(const double* __restrict__ A, Geo g, int k,
-                                                       double* out) {
+                                                       double* out, const uint8_t* __restrict__ dec,
+                                                       int step, int want) {
+  if (dec != nullptr && dec[step] != want) return;
   const int i = k + blockIdx.x;
   const int bi = g.bs(i);
   const int64_t c0 = g.r0(k) + (int64_t)blockIdx.y * 64;
@@ -85,10 +87,11 @@ __global__ void __launch_bounds__(256) k_tile_norm_max(const double* __restrict_
   if (lane == 0) atomic_max_nonneg(out, best);
 }
 
-void launch_tile_norm_max(const double* A, Geo g, int k, double* out, cudaStream_t st) {
+void launch_tile_norm_max(const double* A, Geo g, int k, double* out, cudaStream_t st,
+                          const uint8_t* dec, int step, int want) {
   int64_t ncols = g.N - g.r0(k);
   dim3 grid(g.n - k, (unsigned)((ncols + 63) / 64));
-  { ::hlq::g_launches++; k_tile_norm_max<<<grid, 256, 0, st>>>(A, g, k, out); }
+  { ::hlq::g_launches++; k_tile_norm_max<<<grid, 256, 0, st>>>(A, g, k, out, dec, step, want); }
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -399,11 +399,10 @@ static void set_attr_once() {
   static bool done = false;
   if (done) return;
   done = true;
-  int mx = 200 * 1024;
-  cudaFuncSetAttribute(k_geqrt, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-  cudaFuncSetAttribute(k_unmqr, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-  cudaFuncSetAttribute(k_ttqrt, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-  cudaFuncSetAttribute(k_ttmqr, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  smem_optin(k_geqrt);
+  smem_optin(k_unmqr);
+  smem_optin(k_ttqrt);
+  smem_optin(k_ttmqr);
 }
 
 // Apply the stored QR step k to the column block (base rows 0..N-1, ldc, ncols): used by the
@@ -422,6 +421,15 @@ void launch_qr_apply(const double* A, Geo g, int k, int ib, const double* Tg, co
                                                            ldc, ncols, dec); }
 }
 
+void launch_qr_update_dmma(const double* A, Geo g, int k, int ib, const double* Tg,
+                           const double* Ttt, const int2* const* level_pairs,
+                           const int* level_count, int nlevels, double* base, int64_t ldc,
+                           int64_t ncols, const uint8_t* dec, int what, cudaStream_t st);
+
+void launch_qr_panel_tc(double* A, Geo g, int k, int ib, double* Tg, double* Ttt,
+                        const int2* pairs, int npairs, const uint8_t* dec, bool tt,
+                        cudaStream_t st);
+
 void launch_qr_step(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
                     const int* level_count, int nlevels, DevWork w, int part,
                     cudaStream_t st) {
@@ -433,13 +441,34 @@ void launch_qr_step(double* A, Geo g, int k, int ib, const int2* const* level_pa
   double* right = A + k1 * g.lda;
   const int64_t ncols = g.N - k1;
   unsigned slabs = (unsigned)((ncols + 63) / 64);
-  if (part == 0) { ::hlq::g_launches++; k_geqrt<<<g.n - k, QT, smem, st>>>(A, g, k, ib, w.Tg, dec); }
-  if (part == 1 && ncols > 0) { ::hlq::g_launches++; k_unmqr<<<dim3(slabs, g.n - k), QT, smem, st>>>(A, g, k, ib, w.Tg, right, g.lda, ncols, dec); }
+  const bool tc0 = (ib == 32);
+  if (part == 0) {
+    if (tc0)
+      launch_qr_panel_tc(A, g, k, ib, w.Tg, w.Ttt, nullptr, 0, dec, false, st);
+    else
+      { ::hlq::g_launches++; k_geqrt<<<g.n - k, QT, smem, st>>>(A, g, k, ib, w.Tg, dec); }
+  }
+  const bool tc = (ib == 32);  // DMMA trailing updates (qr_dmma.cu) need 32-row reflector blocks
+  if (part == 1 && ncols > 0) {
+    if (tc)
+      launch_qr_update_dmma(A, g, k, ib, w.Tg, w.Ttt, level_pairs, level_count, nlevels, right,
+                            g.lda, ncols, dec, 0, st);
+    else
+      { ::hlq::g_launches++; k_unmqr<<<dim3(slabs, g.n - k), QT, smem, st>>>(A, g, k, ib, w.Tg, right, g.lda, ncols, dec); }
+  }
   for (int l = 0; l < nlevels && part == 2; ++l) {
-    { ::hlq::g_launches++; k_ttqrt<<<level_count[l], QT, smem, st>>>(A, g, k, ib, w.Ttt, level_pairs[l], dec); }
-    if (ncols > 0)
-      { ::hlq::g_launches++; k_ttmqr<<<dim3(slabs, level_count[l]), QT, smem, st>>>(A, g, k, ib, w.Ttt, level_pairs[l],
-                                                             right, g.lda, ncols, dec); }
+    if (tc0)
+      launch_qr_panel_tc(A, g, k, ib, w.Tg, w.Ttt, level_pairs[l], level_count[l], dec, true, st);
+    else
+      { ::hlq::g_launches++; k_ttqrt<<<level_count[l], QT, smem, st>>>(A, g, k, ib, w.Ttt, level_pairs[l], dec); }
+    if (ncols > 0) {
+      if (tc)
+        launch_qr_update_dmma(A, g, k, ib, w.Tg, w.Ttt, level_pairs, level_count, nlevels, right,
+                              g.lda, ncols, dec, 1 + l, st);
+      else
+        { ::hlq::g_launches++; k_ttmqr<<<dim3(slabs, level_count[l]), QT, smem, st>>>(A, g, k, ib, w.Ttt, level_pairs[l],
+                                                               right, g.lda, ncols, dec); }
+    }
   }
 }
 

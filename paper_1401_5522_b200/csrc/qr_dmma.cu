@@ -1,0 +1,599 @@
+// FP64 tensor-core (DMMA) trailing updates of the QR step: UNMQR (a8) and TTMQR (a11), the bulk of
+// a QR step's flops (Table I: "update D" 4(n-1)^2 units; Alg. 4b).
+//
+// One CTA owns a column slab (W columns) of one tile row (UNMQR) or of one TT pair (TTMQR): the
+// slab of the eliminated tile stays in shared memory across all ib-blocks of the reflector, so each
+// C element is read and written once per step.  Per ib-block b of the stored reflector:
+//     GEMM1 (DMMA)  Wb = [C1_b +] V_b^T C          32 x W,  K = rows of V_b
+//     TRMM  (DFMA)  U  = T_b^T Wb                   32 x W,  T_b upper triangular
+//     GEMM2 (DMMA)  C -= V_b U   (TT: C1_b -= U)     rows x W, K = 32
+// V_b is staged in shared memory with its structure made explicit (unit diagonal / zeros above for
+// GEQRT reflectors, zeros below the diagonal for the TT reflectors), so both GEMMs are dense.
+// Fragments: mma.sync.m8n8k4.f64 (lane g=lane/4, t=lane%4: A(g,t), B(t,g), C(g,2t..2t+1)); every
+// operand array has a leading dimension == 4 (mod 16) doubles, which makes all fragment loads
+// bank-conflict free.
+#include "hlq_internal.cuh"
+
+namespace hlq {
+
+constexpr int QD_T = 256;  // 8 warps
+constexpr int LDU = 36;    // 32 (+4) leading dimension of the 32 x W work arrays
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cpa8(void* smem, const void* gmem) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cpa_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
+}
+
+// Asynchronous copy of a column block into shared memory (many bytes in flight per thread):
+// dst[j*ldd + r] = src[j*lds + r] for r < rows, j < cols_valid; zero for rows_pad > r >= rows and
+// for cols_valid <= j < cols_total.  The caller waits (cpa_wait_all) and synchronises.
+__device__ __forceinline__ void cp_cols(double* dst, int ldd, const double* src, int64_t lds,
+                                        int rows, int rows_pad, int cols_valid, int cols_total,
+                                        int tid, int nthr) {
+  const bool v16 = (((uintptr_t)src & 15) == 0) && ((lds & 1) == 0) && ((ldd & 1) == 0) &&
+                   (((uintptr_t)dst & 15) == 0) && ((rows_pad & 1) == 0);
+  if (v16) {
+    const int rp2 = rows_pad >> 1;
+    for (int o = tid; o < cols_total * rp2; o += nthr) {
+      const int j = o / rp2, r = 2 * (o - j * rp2);
+      double* d = dst + j * ldd + r;
+      if (j < cols_valid && r + 1 < rows) {
+        cpa16(d, src + j * lds + r);
+      } else if (j < cols_valid && r < rows) {
+        d[0] = src[j * lds + r];
+        d[1] = 0.0;
+      } else {
+        d[0] = 0.0;
+        d[1] = 0.0;
+      }
+    }
+  } else {
+    for (int o = tid; o < cols_total * rows_pad; o += nthr) {
+      const int j = o / rows_pad, r = o - j * rows_pad;
+      if (j < cols_valid && r < rows)
+        cpa8(dst + j * ldd + r, src + j * lds + r);
+      else
+        dst[j * ldd + r] = 0.0;
+    }
+  }
+}
+
+__host__ __device__ inline int qd_ldc(int nb) { return (nb + 31) / 32 * 32 + 4; }
+
+template <int W>
+static size_t qd_smem(int nb) {
+  const int ldc = qd_ldc(nb);
+  // Cs (W x ldc) + Vs (32 x ldc) + Us (W x LDU) + Ts (32 x 33)
+  return sizeof(double) * ((size_t)W * ldc + 32 * (size_t)ldc + (size_t)W * LDU + 32 * 33);
+}
+
+// GEMM1 + TRMM:  Wb (32 x W) = [C1_b +] Vs^T (32 x RK) * Cs[c_off : c_off + RK, 0:W];
+//                U = T_b^T Wb  -> Us (W x LDU, U(l, col) at Us[col*LDU + l]).
+// Each n-frag (8 columns) is owned by one warp for all 32 rows, so the triangular T_b^T product
+// runs inside the warp (Us doubles as the warp's scratch).  W = 64: warp w owns n-frag w.
+// W = 32: warps w and w+4 split K for n-frag w&3; the upper half adds its partial through Us.
+// TT (c1 != nullptr): Wb starts from C1_b (read from global) and C1_b <- C1_b - U is written back.
+template <int W>
+__device__ __forceinline__ void gemm1_trmm(const double* Vs, const double* Cs, int ldc, int c_off,
+                                           int RK, const double* Ts, double* Us, double* c1,
+                                           int64_t ldcg, int64_t c0, int64_t ncols, int sb,
+                                           int warp, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  const int nf = warp & (W / 8 - 1);
+  const int khalf = (W == 64) ? 0 : (warp >> 2);
+  const int kbeg = (W == 64) ? 0 : khalf * (RK / 2);
+  const int kend = (W == 64) ? RK : kbeg + RK / 2;
+  double acc[4][2];
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      int l = mi * 8 + g;
+      int64_t col = c0 + nf * 8 + 2 * t + h;
+      acc[mi][h] = (c1 != nullptr && khalf == 0 && l < sb && col < ncols) ? c1[col * ldcg + l] : 0.0;
+    }
+  const double* cb = Cs + (nf * 8 + g) * ldc + c_off + t;
+  const double* vb = Vs + g * ldc + t;
+#pragma unroll 4
+  for (int kk = kbeg; kk < kend; kk += 4) {
+    double b = cb[kk];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) dmma(acc[mi][0], acc[mi][1], vb[mi * 8 * ldc + kk], b);
+  }
+  if (W == 32) {
+    if (khalf == 1)
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) Us[(nf * 8 + 2 * t + h) * LDU + mi * 8 + g] = acc[mi][h];
+    __syncthreads();
+    if (khalf == 1) return;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) acc[mi][h] += Us[(nf * 8 + 2 * t + h) * LDU + mi * 8 + g];
+    __syncwarp();
+  }
+  // Wb of this warp's 8 columns -> Us (scratch), then U = T^T Wb in place
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) Us[(nf * 8 + 2 * t + h) * LDU + mi * 8 + g] = acc[mi][h];
+  __syncwarp();
+  double u[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {  // lane -> row l = lane, 8 columns
+    const double* wcol = Us + (nf * 8 + j) * LDU;
+    double v = 0.0;
+    for (int q = 0; q <= lane; ++q) v += Ts[lane * 33 + q] * wcol[q];
+    u[j] = v;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 8; ++j) Us[(nf * 8 + j) * LDU + lane] = u[j];
+  if (c1 != nullptr && lane < sb) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      int64_t col = c0 + nf * 8 + j;
+      if (col < ncols) c1[col * ldcg + lane] -= u[j];
+    }
+  }
+}
+
+// GEMM2: Cs[c_off : c_off + RK, 0:W] -= Vs (RK x 32) * Us (32 x W); macro tiles 32 rows x 16 cols
+template <int W>
+__device__ __forceinline__ void gemm2(const double* Vs, const double* Us, double* Cs, int ldc,
+                                      int c_off, int RK, int warp, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  const int nmt_r = RK / 32, nmt_c = W / 16;
+  for (int mt = warp; mt < nmt_r * nmt_c; mt += 8) {
+    const int r0 = (mt / nmt_c) * 32, n0 = (mt % nmt_c) * 16;
+    double acc[4][2][2];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          acc[mi][ni][h] = Cs[(n0 + ni * 8 + 2 * t + h) * ldc + c_off + r0 + mi * 8 + g];
+#pragma unroll
+    for (int kk = 0; kk < 32; kk += 4) {
+      double a[4], b[2];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) a[mi] = -Vs[(kk + t) * ldc + r0 + mi * 8 + g];
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) b[ni] = Us[(n0 + ni * 8 + g) * LDU + kk + t];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+    }
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          Cs[(n0 + ni * 8 + 2 * t + h) * ldc + c_off + r0 + mi * 8 + g] = acc[mi][ni][h];
+  }
+}
+
+// UNMQR: tile row i = k + blockIdx.y, columns [W*blockIdx.x, +W) of (base, ldcg): C_i <- Q_ik^T C_i
+template <int W>
+__global__ void __launch_bounds__(QD_T) k_unmqr_dmma(const double* __restrict__ A, Geo g, int k,
+                                                     int ib, const double* __restrict__ Tg,
+                                                     double* __restrict__ base, int64_t ldcg,
+                                                     int64_t ncols, const uint8_t* __restrict__ dec) {
+  if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
+  extern __shared__ __align__(16) double sm[];
+  const int ldc = qd_ldc(g.nb);
+  double* Cs = sm;
+  double* Vs = Cs + W * ldc;
+  double* Us = Vs + 32 * ldc;
+  double* Ts = Us + W * LDU;
+  const int i = k + blockIdx.y;
+  const int bi = g.bs(i), bk = g.bs(k);
+  const double* tile = g.tile(const_cast<double*>(A), i, k);
+  const double* T = Tg + tri_index(i, k, g.n) * (int64_t)ib * g.nb;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t c0 = (int64_t)blockIdx.x * W;
+  const int rows_pad = ldc - 4;
+  const int cvalid = (int)((ncols - c0) < W ? (ncols - c0) : W);
+  cp_cols(Cs, ldc, base + c0 * ldcg + g.r0(i), ldcg, bi, rows_pad, cvalid, W, tid, QD_T);
+  for (int i0 = 0; i0 < bk; i0 += ib) {
+    const int sb = min(ib, bk - i0);
+    const int R = bi - i0;
+    if (R <= 0) break;
+    const int RK = (R + 31) / 32 * 32;
+    __syncthreads();
+    cp_cols(Vs, ldc, tile + (int64_t)i0 * g.lda + i0, g.lda, R, RK, sb, 32, tid, QD_T);
+    cpa_wait_all();
+    __syncthreads();
+    for (int o = tid; o < 32 * 32; o += QD_T) {  // unit diagonal, zeros above (explicit structure)
+      int l = o >> 5, r = o & 31;
+      if (r <= l && r < RK) Vs[l * ldc + r] = (r == l && l < sb && r < R) ? 1.0 : 0.0;
+    }
+    for (int o = tid; o < 32 * 32; o += QD_T) {
+      int l = o >> 5, q = o & 31;
+      Ts[l * 33 + q] = (l < sb && q <= l) ? T[(int64_t)(i0 + l) * ib + q] : 0.0;
+    }
+    __syncthreads();
+    gemm1_trmm<W>(Vs, Cs, ldc, i0, RK, Ts, Us, nullptr, 0, c0, ncols, sb, warp, lane);
+    __syncthreads();
+    gemm2<W>(Vs, Us, Cs, ldc, i0, RK, warp, lane);
+  }
+  __syncthreads();
+  for (int o = tid; o < W * bi; o += QD_T) {
+    int j = o / bi, r = o - j * bi;
+    if (c0 + j < ncols) base[(c0 + j) * ldcg + g.r0(i) + r] = Cs[j * ldc + r];
+  }
+}
+
+// TTMQR: pair (e, i) = pairs[blockIdx.y], columns [W*blockIdx.x, +W): [C_e; C_i] <- Q^T [C_e; C_i]
+template <int W>
+__global__ void __launch_bounds__(QD_T) k_ttmqr_dmma(const double* __restrict__ A, Geo g, int k,
+                                                     int ib, const double* __restrict__ Ttt,
+                                                     const int2* __restrict__ pairs,
+                                                     double* __restrict__ base, int64_t ldcg,
+                                                     int64_t ncols, const uint8_t* __restrict__ dec) {
+  if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
+  extern __shared__ __align__(16) double sm[];
+  const int ldc = qd_ldc(g.nb);
+  double* Cs = sm;               // C_i slab (rows of tile i)
+  double* Vs = Cs + W * ldc;
+  double* Us = Vs + 32 * ldc;
+  double* Ts = Us + W * LDU;
+  const int2 pr = pairs[blockIdx.y];
+  const int e = pr.x, i = pr.y;
+  const int bi = g.bs(i), bk = g.bs(k);
+  const double* Vt = g.tile(const_cast<double*>(A), i, k);
+  const double* T = Ttt + tri_index(i, k, g.n) * (int64_t)ib * g.nb;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t c0 = (int64_t)blockIdx.x * W;
+  const int rows_pad = ldc - 4;
+  const int cvalid = (int)((ncols - c0) < W ? (ncols - c0) : W);
+  cp_cols(Cs, ldc, base + c0 * ldcg + g.r0(i), ldcg, bi, rows_pad, cvalid, W, tid, QD_T);
+  for (int i0 = 0; i0 < bk; i0 += ib) {
+    const int sb = min(ib, bk - i0);
+    const int R2 = min(bi, i0 + sb);
+    const int RK = (R2 + 31) / 32 * 32;
+    __syncthreads();
+    cp_cols(Vs, ldc, Vt + (int64_t)i0 * g.lda, g.lda, R2, RK, sb, 32, tid, QD_T);
+    cpa_wait_all();
+    __syncthreads();
+    for (int o = tid; o < 32 * RK; o += QD_T) {  // the TT reflectors are upper triangular
+      int l = o / RK, r = o - l * RK;
+      if (r > i0 + l) Vs[l * ldc + r] = 0.0;
+    }
+    for (int o = tid; o < 32 * 32; o += QD_T) {
+      int l = o >> 5, q = o & 31;
+      Ts[l * 33 + q] = (l < sb && q <= l) ? T[(int64_t)(i0 + l) * ib + q] : 0.0;
+    }
+    __syncthreads();
+    // Wb = C1_b + V2_b^T C2, U = T^T Wb, C1_b -= U (C1_b = rows i0.. of tile e, read/written in place)
+    gemm1_trmm<W>(Vs, Cs, ldc, 0, RK, Ts, Us, base + g.r0(e) + i0, ldcg, c0, ncols, sb, warp, lane);
+    __syncthreads();
+    gemm2<W>(Vs, Us, Cs, ldc, 0, RK, warp, lane);  // C2 -= V2_b U
+  }
+  __syncthreads();
+  for (int o = tid; o < W * bi; o += QD_T) {
+    int j = o / bi, r = o - j * bi;
+    if (c0 + j < ncols) base[(c0 + j) * ldcg + g.r0(i) + r] = Cs[j * ldc + r];
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Panel factorisation of one 32-column reflector block by the whole CTA (8 warps): per column l a
+// CTA-wide sum of squares (dlarfg, reading 14), the update of the block's remaining
+// columns and the T column (dlarft, forward column-wise).  Reductions are warp shuffles followed
+// by a fixed-order sum over the 8 warp partials (deterministic).
+//   GE (GEQRT): Vs column l holds rows 0..R-1 of the block (local row l is the diagonal);
+//               reflector l acts on local rows l..R-1, top element Vs[l][l].
+//   TT (TTQRT): top elements in Rs (32 x 33, R(q,l) at Rs[l*33+q]); Vs column l holds rows
+//               0..R2-1 of R_i (upper triangular: rows <= i0 + l), the reflector's bottom part.
+__device__ __forceinline__ double block_sum(double v, double* red, int tid) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((tid & 31) == 0) red[tid >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) s += red[w];
+  return s;
+}
+
+template <bool TT>
+__device__ void panel_factor(double* Vs, int ldc, double* Rs, double* Ts, int R, int i0, int sb,
+                             double* red, double* bc, int tid) {
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int l = 0; l < sb; ++l) {
+    if (!TT && l >= R) break;
+    const int rlo = TT ? 0 : l + 1;
+    const int rhi = TT ? min(R, i0 + l + 1) : R;
+    double* v = Vs + l * ldc;
+    double p = 0.0;
+    for (int r = rlo + tid; r < rhi; r += QD_T) p += v[r] * v[r];
+    const double ssq = block_sum(p, red, tid);
+    const double alpha = TT ? Rs[l * 33 + l] : v[l];
+    double tau = 0.0, beta = alpha, sc = 1.0;
+    if (ssq != 0.0) {
+      const double nrm = sqrt(alpha * alpha + ssq);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      tau = (beta - alpha) / beta;
+      sc = alpha - beta;
+    }
+    for (int r = rlo + tid; r < rhi; r += QD_T) v[r] = (ssq == 0.0) ? 0.0 : v[r] / sc;
+    __syncthreads();
+    if (tid == 0) {
+      if (TT) Rs[l * 33 + l] = beta; else v[l] = beta;
+    }
+    // update the block's remaining columns with H_l
+    if (tau != 0.0 && l + 1 < sb) {
+      for (int c = l + 1; c < sb; ++c) {
+        const double* vc = Vs + c * ldc;
+        double q = 0.0;
+        for (int r = rlo + tid; r < rhi; r += QD_T) q += v[r] * vc[r];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+        if (lane == 0) red[warp * 33 + c] = q;
+      }
+      __syncthreads();
+      if (tid > l && tid < sb) {
+        double w = TT ? Rs[tid * 33 + l] : Vs[tid * ldc + l];
+#pragma unroll
+        for (int ww = 0; ww < 8; ++ww) w += red[ww * 33 + tid];
+        bc[tid] = w;
+        if (TT) Rs[tid * 33 + l] -= tau * w; else Vs[tid * ldc + l] -= tau * w;
+      }
+      __syncthreads();
+      for (int r = rlo + tid; r < rhi; r += QD_T) {
+        const double vr = v[r];
+        for (int c = l + 1; c < sb; ++c) Vs[c * ldc + r] -= tau * (vr * bc[c]);
+      }
+    }
+    // T column l: T(l,l) = tau; T(0:l, l) = -tau T(0:l, 0:l) z, z_q = V_q . v_l
+    if (l > 0) {
+      for (int q2 = 0; q2 < l; ++q2) {
+        const double* vq = Vs + q2 * ldc;
+        double q = 0.0;
+        for (int r = rlo + tid; r < rhi; r += QD_T) q += vq[r] * v[r];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+        if (lane == 0) red[warp * 33 + q2] = q;
+      }
+      __syncthreads();
+      if (tid < l) {
+        double z = TT ? 0.0 : Vs[tid * ldc + l];  // GE: V_q(l) * 1 (the unit top of v_l)
+#pragma unroll
+        for (int ww = 0; ww < 8; ++ww) z += red[ww * 33 + tid];
+        bc[32 + tid] = z;
+      }
+      __syncthreads();
+      if (tid < l) {
+        double t = 0.0;
+        for (int p2 = tid; p2 < l; ++p2) t += Ts[p2 * 33 + tid] * bc[32 + p2];
+        Ts[l * 33 + tid] = -tau * t;
+      }
+    }
+    if (tid == 0) Ts[l * 33 + l] = tau;
+    __syncthreads();
+  }
+}
+
+// GEQRT of tiles (k + blockIdx.x, k) on tensor cores: per 32-column block, CTA-wide panel
+// factorisation, then the block reflector is applied to the tile's remaining columns in W-column
+// slabs with the same DMMA GEMM1+TRMM / GEMM2 as UNMQR.
+template <int W>
+__global__ void __launch_bounds__(QD_T) k_geqrt_tc(double* __restrict__ A, Geo g, int k, int ib,
+                                                   double* __restrict__ Tg,
+                                                   const uint8_t* __restrict__ dec) {
+  if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
+  extern __shared__ __align__(16) double sm[];
+  const int ldc = qd_ldc(g.nb);
+  double* Cs = sm;
+  double* Vs = Cs + W * ldc;
+  double* Us = Vs + 32 * ldc;
+  double* Ts = Us + W * LDU;
+  double* red = Cs;            // aliases Cs during the panel factorisation
+  double* bc = Cs + 8 * 33;
+  const int i = k + blockIdx.x;
+  const int bi = g.bs(i), bk = g.bs(k);
+  double* tile = g.tile(A, i, k);
+  double* T = Tg + tri_index(i, k, g.n) * (int64_t)ib * g.nb;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int t = tid; t < ib * g.nb; t += QD_T) T[t] = 0.0;
+  for (int i0 = 0; i0 < bk; i0 += ib) {
+    const int sb = min(ib, bk - i0);
+    const int R = bi - i0;
+    if (R <= 0) break;
+    const int RK = (R + 31) / 32 * 32;
+    __syncthreads();
+    cp_cols(Vs, ldc, tile + (int64_t)i0 * g.lda + i0, g.lda, R, RK, sb, 32, tid, QD_T);
+    for (int o = tid; o < 32 * 33; o += QD_T) Ts[o] = 0.0;
+    cpa_wait_all();
+    __syncthreads();
+    panel_factor<false>(Vs, ldc, nullptr, Ts, R, i0, sb, red, bc, tid);
+    for (int o = tid; o < sb * R; o += QD_T) {
+      int l = o / R, r = o - l * R;
+      tile[(int64_t)(i0 + l) * g.lda + i0 + r] = Vs[l * ldc + r];
+    }
+    for (int o = tid; o < sb * sb; o += QD_T) {
+      int l = o / sb, q = o - l * sb;
+      T[(int64_t)(i0 + l) * ib + q] = Ts[l * 33 + q];
+    }
+    __syncthreads();
+    if (i0 + sb >= bk) break;
+    for (int o = tid; o < 32 * 32; o += QD_T) {  // explicit unit-lower structure for the GEMMs
+      int l = o >> 5, r = o & 31;
+      if (r <= l && r < RK) Vs[l * ldc + r] = (r == l && l < sb && r < R) ? 1.0 : 0.0;
+    }
+    for (int c0 = i0 + sb; c0 < bk; c0 += W) {
+      const int cv = min(W, bk - c0);
+      __syncthreads();
+      cp_cols(Cs, ldc, tile + (int64_t)c0 * g.lda + i0, g.lda, R, RK, cv, W, tid, QD_T);
+      cpa_wait_all();
+      __syncthreads();
+      gemm1_trmm<W>(Vs, Cs, ldc, 0, RK, Ts, Us, nullptr, 0, 0, 0, sb, warp, lane);
+      __syncthreads();
+      gemm2<W>(Vs, Us, Cs, ldc, 0, RK, warp, lane);
+      __syncthreads();
+      for (int o = tid; o < cv * R; o += QD_T) {
+        int j = o / R, r = o - j * R;
+        tile[(int64_t)(c0 + j) * g.lda + i0 + r] = Cs[j * ldc + r];
+      }
+    }
+  }
+}
+
+// TTQRT on pairs (e, i) = pairs[blockIdx.x]: [R_e; R_i] -> R_e, V (upper triangle of tile (i,k)), T
+template <int W>
+__global__ void __launch_bounds__(QD_T) k_ttqrt_tc(double* __restrict__ A, Geo g, int k, int ib,
+                                                   double* __restrict__ Ttt,
+                                                   const int2* __restrict__ pairs,
+                                                   const uint8_t* __restrict__ dec) {
+  if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
+  extern __shared__ __align__(16) double sm[];
+  const int ldc = qd_ldc(g.nb);
+  double* Cs = sm;
+  double* Vs = Cs + W * ldc;
+  double* Us = Vs + 32 * ldc;
+  double* Ts = Us + W * LDU;
+  double* red = Cs;              // panel-phase aliases of Cs
+  double* bc = Cs + 8 * 33;
+  double* Rs = Cs + 8 * 33 + 64;
+  const int2 pr = pairs[blockIdx.x];
+  const int e = pr.x, i = pr.y;
+  const int bi = g.bs(i), bk = g.bs(k);
+  double* Re = g.tile(A, e, k);
+  double* Ri = g.tile(A, i, k);
+  double* T = Ttt + tri_index(i, k, g.n) * (int64_t)ib * g.nb;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int t = tid; t < ib * g.nb; t += QD_T) T[t] = 0.0;
+  for (int i0 = 0; i0 < bk; i0 += ib) {
+    const int sb = min(ib, bk - i0);
+    const int R2 = min(bi, i0 + sb);
+    const int RK = (R2 + 31) / 32 * 32;
+    __syncthreads();
+    cp_cols(Vs, ldc, Ri + (int64_t)i0 * g.lda, g.lda, R2, RK, sb, 32, tid, QD_T);
+    for (int o = tid; o < 32 * 33; o += QD_T) {
+      Ts[o] = 0.0;
+      int l = o / 33, q = o - l * 33;
+      Rs[o] = (l < sb && q <= l) ? Re[(int64_t)(i0 + l) * g.lda + i0 + q] : 0.0;
+    }
+    cpa_wait_all();
+    __syncthreads();
+    for (int o = tid; o < 32 * RK; o += QD_T) {
+      int l = o / RK, r = o - l * RK;
+      if (r > i0 + l) Vs[l * ldc + r] = 0.0;
+    }
+    __syncthreads();
+    panel_factor<true>(Vs, ldc, Rs, Ts, R2, i0, sb, red, bc, tid);
+    for (int o = tid; o < sb * R2; o += QD_T) {
+      int l = o / R2, r = o - l * R2;
+      if (r <= i0 + l) Ri[(int64_t)(i0 + l) * g.lda + r] = Vs[l * ldc + r];
+    }
+    for (int o = tid; o < sb * sb; o += QD_T) {
+      int l = o / sb, q = o - l * sb;
+      if (q <= l) Re[(int64_t)(i0 + l) * g.lda + i0 + q] = Rs[l * 33 + q];
+      T[(int64_t)(i0 + l) * ib + q] = Ts[l * 33 + q];
+    }
+    __syncthreads();
+    if (i0 + sb >= bk) break;
+    for (int c0 = i0 + sb; c0 < bk; c0 += W) {
+      const int cv = min(W, bk - c0);
+      __syncthreads();
+      cp_cols(Cs, ldc, Ri + (int64_t)c0 * g.lda, g.lda, R2, RK, cv, W, tid, QD_T);
+      cpa_wait_all();
+      __syncthreads();
+      // Wb = R_e(block rows, slab) + V2^T R_i(slab); U = T^T Wb; R_e(block rows) -= U
+      gemm1_trmm<W>(Vs, Cs, ldc, 0, RK, Ts, Us, Re + i0, g.lda, c0, bk, sb, warp, lane);
+      __syncthreads();
+      gemm2<W>(Vs, Us, Cs, ldc, 0, RK, warp, lane);
+      __syncthreads();
+      for (int o = tid; o < cv * R2; o += QD_T) {
+        int j = o / R2, r = o - j * R2;
+        Ri[(int64_t)(c0 + j) * g.lda + r] = Cs[j * ldc + r];
+      }
+    }
+  }
+}
+
+template <int W>
+static void launch_panel_w(double* A, Geo g, int k, int ib, double* Tg, double* Ttt,
+                           const int2* pairs, int npairs, const uint8_t* dec, bool tt,
+                           cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    smem_optin(k_geqrt_tc<W>);
+    smem_optin(k_ttqrt_tc<W>);
+    attr = true;
+  }
+  const size_t smem = qd_smem<W>(g.nb);
+  if (!tt) {
+    { ::hlq::g_launches++; k_geqrt_tc<W><<<g.n - k, QD_T, smem, st>>>(A, g, k, ib, Tg, dec); }
+  } else {
+    { ::hlq::g_launches++; k_ttqrt_tc<W><<<npairs, QD_T, smem, st>>>(A, g, k, ib, Ttt, pairs, dec); }
+  }
+}
+
+void launch_qr_panel_tc(double* A, Geo g, int k, int ib, double* Tg, double* Ttt,
+                        const int2* pairs, int npairs, const uint8_t* dec, bool tt,
+                        cudaStream_t st) {
+  if (qd_smem<64>(g.nb) <= 227 * 1024)
+    launch_panel_w<64>(A, g, k, ib, Tg, Ttt, pairs, npairs, dec, tt, st);
+  else
+    launch_panel_w<32>(A, g, k, ib, Tg, Ttt, pairs, npairs, dec, tt, st);
+}
+
+template <int W>
+static void launch_w(const double* A, Geo g, int k, int ib, const double* Tg, const double* Ttt,
+                     const int2* const* level_pairs, const int* level_count, int nlevels,
+                     double* base, int64_t ldc, int64_t ncols, const uint8_t* dec, int what,
+                     cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    smem_optin(k_unmqr_dmma<W>);
+    smem_optin(k_ttmqr_dmma<W>);
+    attr = true;
+  }
+  const size_t smem = qd_smem<W>(g.nb);
+  const unsigned slabs = (unsigned)((ncols + W - 1) / W);
+  if (what == 0) {
+    { ::hlq::g_launches++; k_unmqr_dmma<W><<<dim3(slabs, g.n - k), QD_T, smem, st>>>(A, g, k, ib, Tg, base, ldc, ncols, dec); }
+  } else {
+    const int l = what - 1;
+    { ::hlq::g_launches++; k_ttmqr_dmma<W><<<dim3(slabs, level_count[l]), QD_T, smem, st>>>(A, g, k, ib, Ttt, level_pairs[l], base, ldc, ncols, dec); }
+  }
+  (void)nlevels;
+}
+
+// what = 0: UNMQR of all tile rows; what = 1 + l: TTMQR of level l.  Column slab width 64 when the
+// slab + reflector block fit in shared memory (nb <= 256), else 32.
+void launch_qr_update_dmma(const double* A, Geo g, int k, int ib, const double* Tg,
+                           const double* Ttt, const int2* const* level_pairs,
+                           const int* level_count, int nlevels, double* base, int64_t ldc,
+                           int64_t ncols, const uint8_t* dec, int what, cudaStream_t st) {
+  if (ncols <= 0) return;
+  if (qd_smem<64>(g.nb) <= 227 * 1024)
+    launch_w<64>(A, g, k, ib, Tg, Ttt, level_pairs, level_count, nlevels, base, ldc, ncols, dec,
+                 what, st);
+  else
+    launch_w<32>(A, g, k, ib, Tg, Ttt, level_pairs, level_count, nlevels, base, ldc, ncols, dec,
+                 what, st);
+}
+
+}  // namespace hlq

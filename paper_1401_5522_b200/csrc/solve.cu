@@ -9,76 +9,149 @@
 
 namespace hlq {
 
-// LU step k forward: x_k <- L_kk^-1 P_kk x_k (one warp)
-__global__ void k_solve_lu_diag(const double* __restrict__ A, Geo g, int k,
-                                const int* __restrict__ ipiv, double* __restrict__ x) {
+// Triangular solves on one diagonal tile with one CTA (256 threads): the tile is streamed through
+// shared memory in 32-column panels (coalesced loads); x_k lives in shared memory.
+constexpr int SP = 32;
+
+// LU step k forward: x_k <- L_kk^-1 P_kk x_k  (unit lower, column-oriented)
+__global__ void __launch_bounds__(256) k_solve_lu_diag(const double* __restrict__ A, Geo g, int k,
+                                                       const int* __restrict__ ipiv,
+                                                       double* __restrict__ x) {
+  extern __shared__ double sm[];
   const int bk = g.bs(k);
-  const int lane = threadIdx.x;
+  const int ld = bk + 1;
+  double* Ps = sm;            // SP x ld
+  double* xs = sm + SP * ld;  // bk
   const double* Akk = g.tile(const_cast<double*>(A), k, k);
   double* xk = x + g.r0(k);
-  if (lane == 0) {
+  const int tid = threadIdx.x;
+  for (int r = tid; r < bk; r += 256) xs[r] = xk[r];
+  __syncthreads();
+  if (tid == 0)
     for (int c = 0; c < bk; ++c) {
       int p = ipiv[(int64_t)k * g.nb + c];
       if (p != c) {
-        double t = xk[c];
-        xk[c] = xk[p];
-        xk[p] = t;
+        double t = xs[c];
+        xs[c] = xs[p];
+        xs[p] = t;
       }
     }
+  for (int p0 = 0; p0 < bk; p0 += SP) {
+    const int pw = min(SP, bk - p0);
+    __syncthreads();
+    for (int t = tid; t < pw * bk; t += 256) {
+      int c = t / bk, r = t - c * bk;
+      Ps[c * ld + r] = Akk[(int64_t)(p0 + c) * g.lda + r];
+    }
+    __syncthreads();
+    // warp 0: the pw x pw unit-lower diagonal block
+    if (tid < 32) {
+      for (int c = 0; c < pw; ++c) {
+        double xc = xs[p0 + c];
+        __syncwarp();
+        if (tid > c && tid < pw) xs[p0 + tid] -= Ps[c * ld + p0 + tid] * xc;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // all threads: rows below the block
+    for (int r = p0 + pw + tid; r < bk; r += 256) {
+      double acc = 0.0;
+      for (int c = 0; c < pw; ++c) acc += Ps[c * ld + r] * xs[p0 + c];
+      xs[r] -= acc;
+    }
   }
-  __syncwarp();
-  for (int c = 0; c < bk; ++c) {
-    double xc = xk[c];
-    __syncwarp();
-    for (int r = c + 1 + lane; r < bk; r += 32) xk[r] -= Akk[(int64_t)c * g.lda + r] * xc;
-    __syncwarp();
-  }
+  __syncthreads();
+  for (int r = tid; r < bk; r += 256) xk[r] = xs[r];
 }
 
-// back substitution on the diagonal tile: x_k <- U_kk^-1 x_k (one warp)
-__global__ void k_solve_upper_diag(const double* __restrict__ A, Geo g, int k,
-                                   double* __restrict__ x) {
+// back substitution on the diagonal tile: x_k <- U_kk^-1 x_k (panels from the right)
+__global__ void __launch_bounds__(256) k_solve_upper_diag(const double* __restrict__ A, Geo g, int k,
+                                                          double* __restrict__ x) {
+  extern __shared__ double sm[];
   const int bk = g.bs(k);
-  const int lane = threadIdx.x;
+  const int ld = bk + 1;
+  double* Ps = sm;
+  double* xs = sm + SP * ld;
   const double* Akk = g.tile(const_cast<double*>(A), k, k);
   double* xk = x + g.r0(k);
-  for (int c = bk - 1; c >= 0; --c) {
-    double xc = xk[c] / Akk[(int64_t)c * g.lda + c];
-    __syncwarp();
-    if (lane == 0) xk[c] = xc;
-    for (int r = lane; r < c; r += 32) xk[r] -= Akk[(int64_t)c * g.lda + r] * xc;
-    __syncwarp();
+  const int tid = threadIdx.x;
+  for (int r = tid; r < bk; r += 256) xs[r] = xk[r];
+  const int npan = (bk + SP - 1) / SP;
+  for (int pi = npan - 1; pi >= 0; --pi) {
+    const int p0 = pi * SP, pw = min(SP, bk - p0);
+    __syncthreads();
+    for (int t = tid; t < pw * (p0 + pw); t += 256) {
+      int c = t / (p0 + pw), r = t - c * (p0 + pw);
+      Ps[c * ld + r] = Akk[(int64_t)(p0 + c) * g.lda + r];
+    }
+    __syncthreads();
+    if (tid < 32) {
+      for (int c = pw - 1; c >= 0; --c) {
+        double xc = xs[p0 + c] / Ps[c * ld + p0 + c];
+        __syncwarp();
+        if (tid == c) xs[p0 + c] = xc;
+        if (tid < c) xs[p0 + tid] -= Ps[c * ld + p0 + tid] * xc;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int r = tid; r < p0; r += 256) {
+      double acc = 0.0;
+      for (int c = 0; c < pw; ++c) acc += Ps[c * ld + r] * xs[p0 + c];
+      xs[r] -= acc;
+    }
   }
+  __syncthreads();
+  for (int r = tid; r < bk; r += 256) xk[r] = xs[r];
 }
 
-// y[0:M) -= B[0:M, 0:K) * v[0:K)   (B column-major, ldb): one thread per row
-__global__ void k_gemv_sub(double* __restrict__ y, const double* __restrict__ B, int64_t ldb,
-                           int64_t M, int K, const double* __restrict__ v) {
-  extern __shared__ double vs[];
+// y[0:M) -= B[0:M, 0:K) * v[0:K)   (B column-major): CTA = 64 rows x all K, 4 threads per row
+// each summing a quarter of the columns, partials combined in a fixed order (deterministic).
+__global__ void __launch_bounds__(256) k_gemv_sub(double* __restrict__ y, const double* __restrict__ B,
+                                                  int64_t ldb, int64_t M, int K,
+                                                  const double* __restrict__ v) {
+  extern __shared__ double vs[];  // K + 256
+  double* part = vs + K;
   for (int c = threadIdx.x; c < K; c += blockDim.x) vs[c] = v[c];
   __syncthreads();
-  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= M) return;
+  const int rl = threadIdx.x & 63, q = threadIdx.x >> 6;
+  const int64_t r = (int64_t)blockIdx.x * 64 + rl;
   double acc = 0.0;
-  for (int c = 0; c < K; ++c) acc += B[(int64_t)c * ldb + r] * vs[c];
-  y[r] -= acc;
+  if (r < M)
+    for (int c = q; c < K; c += 4) acc += B[(int64_t)c * ldb + r] * vs[c];
+  part[q * 64 + rl] = acc;
+  __syncthreads();
+  if (q == 0 && r < M) y[r] -= ((part[rl] + part[64 + rl]) + part[128 + rl]) + part[192 + rl];
 }
 
 void launch_gemv_sub(double* y, const double* B, int64_t ldb, int64_t M, int K, const double* v,
                      cudaStream_t st) {
   if (M <= 0 || K <= 0) return;
-  { ::hlq::g_launches++; k_gemv_sub<<<(unsigned)((M + 255) / 256), 256, sizeof(double) * K, st>>>(y, B, ldb, M, K, v); }
+  { ::hlq::g_launches++; k_gemv_sub<<<(unsigned)((M + 63) / 64), 256, sizeof(double) * (K + 256), st>>>(y, B, ldb, M, K, v); }
+}
+
+static void solve_attr_once() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  smem_optin(k_solve_lu_diag);
+  smem_optin(k_solve_upper_diag);
 }
 
 void launch_solve_lu_fwd(const double* A, Geo g, int k, const int* ipiv, double* x,
                          cudaStream_t st) {
-  { ::hlq::g_launches++; k_solve_lu_diag<<<1, 32, 0, st>>>(A, g, k, ipiv, x); }
+  solve_attr_once();
+  size_t smem = sizeof(double) * ((size_t)SP * (g.bs(k) + 1) + g.bs(k));
+  { ::hlq::g_launches++; k_solve_lu_diag<<<1, 256, smem, st>>>(A, g, k, ipiv, x); }
   const int64_t k0 = g.r0(k), k1 = k0 + g.bs(k);
   launch_gemv_sub(x + k1, A + k0 * g.lda + k1, g.lda, g.N - k1, g.bs(k), x + k0, st);
 }
 
 void launch_solve_back(const double* A, Geo g, int k, double* x, cudaStream_t st) {
-  { ::hlq::g_launches++; k_solve_upper_diag<<<1, 32, 0, st>>>(A, g, k, x); }
+  solve_attr_once();
+  size_t smem = sizeof(double) * ((size_t)SP * (g.bs(k) + 1) + g.bs(k));
+  { ::hlq::g_launches++; k_solve_upper_diag<<<1, 256, smem, st>>>(A, g, k, x); }
   const int64_t k0 = g.r0(k);
   launch_gemv_sub(x, A + k0 * g.lda, g.lda, k0, g.bs(k), x + k0, st);
 }
