@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi) {
         a[mi] = as[(k4 + t) * LDA_S + mi * 8];
-        if (neg) a[mi] = -a[mi];
+        if (neg) a[mi] = neg_bits(a[mi]);
       }
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) b[ni] = bs[ni * 8 * LDB_S + k4];

@@ -94,6 +94,11 @@ inline void smem_optin(F* func) {
 }
 
 // ---- device helpers ---------------------------------------------------------------------------
+// sign flip on the integer pipe (a DADD negation would occupy the FP64 pipe that DMMA shares)
+__device__ __forceinline__ double neg_bits(double a) {
+  return __longlong_as_double(__double_as_longlong(a) ^ (long long)0x8000000000000000ULL);
+}
+
 __device__ __forceinline__ double nanmax(double a, double b) {
   // max that propagates NaN (criterion inputs: any NaN -> QR, reading 22)
   return (a > b || a != a) ? a : b;

@@ -173,7 +173,7 @@ __device__ __forceinline__ void gemm2(const double* Vs, const double* Us, double
     for (int kk = 0; kk < 32; kk += 4) {
       double a[4], b[2];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) a[mi] = -Vs[(kk + t) * ldc + r0 + mi * 8 + g];
+      for (int mi = 0; mi < 4; ++mi) a[mi] = neg_bits(Vs[(kk + t) * ldc + r0 + mi * 8 + g]);
 #pragma unroll
       for (int ni = 0; ni < 2; ++ni) b[ni] = Us[(n0 + ni * 8 + g) * LDU + kk + t];
 #pragma unroll
@@ -220,15 +220,12 @@ __global__ void __launch_bounds__(QD_T) k_unmqr_dmma(const double* __restrict__ 
     const int RK = (R + 31) / 32 * 32;
     __syncthreads();
     cp_cols(Vs, ldc, tile + (int64_t)i0 * g.lda + i0, g.lda, R, RK, sb, 32, tid, QD_T);
+    cp_cols(Ts, 33, T + (int64_t)i0 * ib, ib, sb, 32, sb, 32, tid, QD_T);  // stored T: zeros below
     cpa_wait_all();
     __syncthreads();
     for (int o = tid; o < 32 * 32; o += QD_T) {  // unit diagonal, zeros above (explicit structure)
       int l = o >> 5, r = o & 31;
       if (r <= l && r < RK) Vs[l * ldc + r] = (r == l && l < sb && r < R) ? 1.0 : 0.0;
-    }
-    for (int o = tid; o < 32 * 32; o += QD_T) {
-      int l = o >> 5, q = o & 31;
-      Ts[l * 33 + q] = (l < sb && q <= l) ? T[(int64_t)(i0 + l) * ib + q] : 0.0;
     }
     __syncthreads();
     gemm1_trmm<W>(Vs, Cs, ldc, i0, RK, Ts, Us, nullptr, 0, c0, ncols, sb, warp, lane);
@@ -272,15 +269,12 @@ __global__ void __launch_bounds__(QD_T) k_ttmqr_dmma(const double* __restrict__ 
     const int RK = (R2 + 31) / 32 * 32;
     __syncthreads();
     cp_cols(Vs, ldc, Vt + (int64_t)i0 * g.lda, g.lda, R2, RK, sb, 32, tid, QD_T);
+    cp_cols(Ts, 33, T + (int64_t)i0 * ib, ib, sb, 32, sb, 32, tid, QD_T);
     cpa_wait_all();
     __syncthreads();
     for (int o = tid; o < 32 * RK; o += QD_T) {  // the TT reflectors are upper triangular
       int l = o / RK, r = o - l * RK;
       if (r > i0 + l) Vs[l * ldc + r] = 0.0;
-    }
-    for (int o = tid; o < 32 * 32; o += QD_T) {
-      int l = o >> 5, q = o & 31;
-      Ts[l * 33 + q] = (l < sb && q <= l) ? T[(int64_t)(i0 + l) * ib + q] : 0.0;
     }
     __syncthreads();
     // Wb = C1_b + V2_b^T C2, U = T^T Wb, C1_b -= U (C1_b = rows i0.. of tile e, read/written in place)
@@ -319,16 +313,47 @@ __device__ __forceinline__ double block_sum(double v, double* red, int tid) {
 template <bool TT>
 __device__ void panel_factor(double* Vs, int ldc, double* Rs, double* Ts, int R, int i0, int sb,
                              double* red, double* bc, int tid) {
+  // Per column l ONE CTA-wide reduction: g[c] = sum_r Vs[c][r] x_r over the rows of reflector l
+  // (x = the raw column l below its top element).  g[l] = ||x||^2 gives dlarfg; for c > l,
+  // w_c = top_c + g[c]/sc updates the remaining columns; for q < l, z_q = [V_q(l)] + g[q]/sc
+  // gives the T column.  The 32 partials of a warp are reduced by a transpose-butterfly
+  // (31 shuffles) and the 8 warp partials are summed in a fixed order (deterministic).
   const int lane = tid & 31, warp = tid >> 5;
   for (int l = 0; l < sb; ++l) {
     if (!TT && l >= R) break;
     const int rlo = TT ? 0 : l + 1;
     const int rhi = TT ? min(R, i0 + l + 1) : R;
-    double* v = Vs + l * ldc;
-    double p = 0.0;
-    for (int r = rlo + tid; r < rhi; r += QD_T) p += v[r] * v[r];
-    const double ssq = block_sum(p, red, tid);
-    const double alpha = TT ? Rs[l * 33 + l] : v[l];
+    double* x = Vs + l * ldc;
+    double p[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) p[c] = 0.0;
+    for (int r = rlo + tid; r < rhi; r += QD_T) {
+      const double xr = x[r];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) p[c] += Vs[c * ldc + r] * xr;
+    }
+    // transpose-butterfly: after the 5 steps lane j holds the warp's sum for column j
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+      const bool upper = (lane & s) != 0;
+#pragma unroll
+      for (int c = 0; c < s; ++c) {
+        double send = upper ? p[c] : p[c + s];
+        double keep = upper ? p[c + s] : p[c];
+        p[c] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+      }
+    }
+    red[warp * 33 + lane] = p[0];
+    __syncthreads();
+    if (tid < 32) {
+      double v = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) v += red[w * 33 + tid];
+      bc[tid] = v;
+    }
+    __syncthreads();
+    const double ssq = bc[l];
+    const double alpha = TT ? Rs[l * 33 + l] : x[l];
     double tau = 0.0, beta = alpha, sc = 1.0;
     if (ssq != 0.0) {
       const double nrm = sqrt(alpha * alpha + ssq);
@@ -336,60 +361,35 @@ __device__ void panel_factor(double* Vs, int ldc, double* Rs, double* Ts, int R,
       tau = (beta - alpha) / beta;
       sc = alpha - beta;
     }
-    for (int r = rlo + tid; r < rhi; r += QD_T) v[r] = (ssq == 0.0) ? 0.0 : v[r] / sc;
+    // w_c (c > l) and z_q (q < l), one division each, into bc[32..63]
+    if (tid < sb && tid != l) {
+      const double gs = (ssq == 0.0) ? 0.0 : bc[tid] / sc;
+      double top = 0.0;
+      if (tid > l) top = TT ? Rs[tid * 33 + l] : Vs[tid * ldc + l];  // w_c = top_c + V_c . v
+      else if (!TT) top = Vs[tid * ldc + l];                          // z_q = V_q(l) + V_q . v
+      bc[32 + tid] = top + gs;
+    }
     __syncthreads();
+    // normalise v and update the remaining columns on the rows of this reflector
+    for (int r = rlo + tid; r < rhi; r += QD_T) {
+      const double vr = (ssq == 0.0) ? 0.0 : x[r] / sc;
+      x[r] = vr;
+      if (tau != 0.0)
+        for (int c = l + 1; c < sb; ++c) Vs[c * ldc + r] -= tau * (vr * bc[32 + c]);
+    }
+    if (tid > l && tid < sb && tau != 0.0) {
+      const double w = bc[32 + tid];
+      if (TT) Rs[tid * 33 + l] -= tau * w; else Vs[tid * ldc + l] -= tau * w;
+    }
+    if (tid < l) {
+      double t = 0.0;
+      for (int p2 = tid; p2 < l; ++p2) t += Ts[p2 * 33 + tid] * bc[32 + p2];
+      Ts[l * 33 + tid] = -tau * t;
+    }
     if (tid == 0) {
-      if (TT) Rs[l * 33 + l] = beta; else v[l] = beta;
+      Ts[l * 33 + l] = tau;
+      if (TT) Rs[l * 33 + l] = beta; else x[l] = beta;
     }
-    // update the block's remaining columns with H_l
-    if (tau != 0.0 && l + 1 < sb) {
-      for (int c = l + 1; c < sb; ++c) {
-        const double* vc = Vs + c * ldc;
-        double q = 0.0;
-        for (int r = rlo + tid; r < rhi; r += QD_T) q += v[r] * vc[r];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-        if (lane == 0) red[warp * 33 + c] = q;
-      }
-      __syncthreads();
-      if (tid > l && tid < sb) {
-        double w = TT ? Rs[tid * 33 + l] : Vs[tid * ldc + l];
-#pragma unroll
-        for (int ww = 0; ww < 8; ++ww) w += red[ww * 33 + tid];
-        bc[tid] = w;
-        if (TT) Rs[tid * 33 + l] -= tau * w; else Vs[tid * ldc + l] -= tau * w;
-      }
-      __syncthreads();
-      for (int r = rlo + tid; r < rhi; r += QD_T) {
-        const double vr = v[r];
-        for (int c = l + 1; c < sb; ++c) Vs[c * ldc + r] -= tau * (vr * bc[c]);
-      }
-    }
-    // T column l: T(l,l) = tau; T(0:l, l) = -tau T(0:l, 0:l) z, z_q = V_q . v_l
-    if (l > 0) {
-      for (int q2 = 0; q2 < l; ++q2) {
-        const double* vq = Vs + q2 * ldc;
-        double q = 0.0;
-        for (int r = rlo + tid; r < rhi; r += QD_T) q += vq[r] * v[r];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-        if (lane == 0) red[warp * 33 + q2] = q;
-      }
-      __syncthreads();
-      if (tid < l) {
-        double z = TT ? 0.0 : Vs[tid * ldc + l];  // GE: V_q(l) * 1 (the unit top of v_l)
-#pragma unroll
-        for (int ww = 0; ww < 8; ++ww) z += red[ww * 33 + tid];
-        bc[32 + tid] = z;
-      }
-      __syncthreads();
-      if (tid < l) {
-        double t = 0.0;
-        for (int p2 = tid; p2 < l; ++p2) t += Ts[p2 * 33 + tid] * bc[32 + p2];
-        Ts[l * 33 + tid] = -tau * t;
-      }
-    }
-    if (tid == 0) Ts[l * 33 + l] = tau;
     __syncthreads();
   }
 }
