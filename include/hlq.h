@@ -148,11 +148,11 @@ int hlq_residual(const double* A, int64_t N, int64_t lda, const double* x, const
 enum {
   HLQ_PROF_CRITERION = 0,  /* panel statistics, ||A_kk^-1||_1, decide (a1, a3, a4)               */
   HLQ_PROF_GETRF = 1,      /* speculative GETRF + triangular inverses (a2, a3)                    */
-  HLQ_PROF_LU_TRSM = 2,    /* commit + Eliminate (TRSM) + Apply (SWPTRSM) (a5, a6)                */
-  HLQ_PROF_LU_UPDATE = 3,  /* Schur DGEMM update (a7): the dominant kernel of LU steps           */
-  HLQ_PROF_QR_GEQRT = 4,   /* GEQRT of the panel tiles (a8)                                       */
-  HLQ_PROF_QR_UNMQR = 5,   /* UNMQR trailing update (a8)                                          */
-  HLQ_PROF_QR_TT = 6,      /* TTQRT + TTMQR levels (a9-a11)                                       */
+  HLQ_PROF_LU_TRSM = 2,    /* LU panel stage: commit + Eliminate (TRSM) (a5)                      */
+  HLQ_PROF_LU_UPDATE = 3,  /* LU update stage: Apply (SWPTRSM) + Schur DGEMM (a6, a7): dominant     */
+  HLQ_PROF_QR_GEQRT = 4,   /* QR panel stage: GEQRT of the panel tiles + TTQRT levels (a8, a9, a11) */
+  HLQ_PROF_QR_UNMQR = 5,   /* QR update stage: UNMQR + TTMQR levels (a8, a10, a11): dominant kernel */
+  HLQ_PROF_QR_TT = 6,      /* (unused since the lookahead split; kept for ABI stability)           */
   HLQ_PROF_GROWTH = 7,     /* tile-norm growth tracking (a12)                                     */
   HLQ_PROF_SOLVE = 8,      /* forward replay + back substitution (a13)                            */
   HLQ_PROF_OTHER = 9,

@@ -125,8 +125,20 @@ struct Prof {
   }
 };
 
+// the library's high-priority panel stream (lookahead), created once per process
+static cudaStream_t panel_stream() {
+  static cudaStream_t sp = nullptr;
+  if (!sp) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&sp, cudaStreamNonBlocking, hi);
+  }
+  return sp;
+}
+
 struct hlq_factors_s {
   Prof prof;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
   double* A = nullptr;
   Geo g{};
   int ib = 32, D = 1, crit = 0;
@@ -256,6 +268,8 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   hlq_factors_t f = new (std::nothrow) hlq_factors_s();
   if (!f) return HLQ_ERR_NOMEM;
   *out = f;
+  cudaEventCreateWithFlags(&f->ev[0], cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&f->ev[1], cudaEventDisableTiming);
   f->A = A;
   f->g.N = N;
   f->g.lda = lda;
@@ -287,23 +301,27 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
     off += align_up(bytes ? bytes : 1, 256);
     return o;
   };
-  size_t oW = take(sizeof(double) * nb * nb), oIpw = take(sizeof(int) * nb),
+  const bool fuse_growth_any = f->track_growth && nb % 128 == 0;
+  const size_t scr = (size_t)2 * nb * nb + align_up(nb, 64);
+  size_t oW0 = take(sizeof(double) * nb * nb), oW1 = take(sizeof(double) * nb * nb),
+         oIpw0 = take(sizeof(int) * nb), oIpw1 = take(sizeof(int) * nb),
          oIp = take(sizeof(int) * (size_t)n * nb), oTg = take(sizeof(double) * ntri * ib * nb),
          oTt = take(sizeof(double) * ntri * ib * nb), oS = take(sizeof(double) * n),
          oLm = take(sizeof(double) * nb), oAm = take(sizeof(double) * nb), oInv = take(8),
          oZp = take(sizeof(int)), oDec = take(n), oMg = take(sizeof(double) * n),
          oFl = take(sizeof(int) * n), oSt = take(sizeof(int) * 4), oFo = take(n), oRd = take(n),
          oRm = take(sizeof(double) * n), oGs = take(sizeof(double) * (n + 1)),
-         oPr = take(sizeof(int2) * (npairs + 1)),
-         oSc = take(sizeof(double) * ((size_t)2 * nb * nb + align_up(nb, 64) +
-                                      std::max((size_t)N * nb, (size_t)((N + 127) / 128) * N) + 64));
+         oPr = take(sizeof(int2) * (npairs + 1)), oSc0 = take(sizeof(double) * scr),
+         oSc1 = take(sizeof(double) * scr), oWp = take(sizeof(double) * (size_t)N * nb),
+         oWr = take(sizeof(double) * (size_t)N * nb),
+         oCp = take(fuse_growth_any ? sizeof(double) * (size_t)((N + 127) / 128) * N : 8);
   f->ws_bytes = off;
   f->ws_block = cache_get(0, off);
   if (!f->ws_block) return HLQ_ERR_NOMEM;
   char* base = (char*)f->ws_block;
   DevWork& w = f->w;
-  w.W = (double*)(base + oW);
-  w.ipiv_ws = (int*)(base + oIpw);
+  w.W = (double*)(base + oW0);
+  w.ipiv_ws = (int*)(base + oIpw0);
   w.ipiv = (int*)(base + oIp);
   w.Tg = (double*)(base + oTg);
   w.Ttt = (double*)(base + oTt);
@@ -321,7 +339,16 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   w.ref_margin = (opt.ref_dec && opt.ref_margin) ? (double*)(base + oRm) : nullptr;
   w.gstep = (double*)(base + oGs);
   w.pairs = (int2*)(base + oPr);
-  w.scratch = (double*)(base + oSc);
+  w.scratch = (double*)(base + oSc0);
+  w.ws_panel = (double*)(base + oWp);
+  w.ws_row = (double*)(base + oWr);
+  w.colpart = fuse_growth_any ? (double*)(base + oCp) : nullptr;
+  // per-parity views (lookahead: step k+1's panel runs while step k's update still reads step k's
+  // W / ipiv / L^-1 / U^-1 / perm)
+  DevWork wpar[2] = {w, w};
+  wpar[1].W = (double*)(base + oW1);
+  wpar[1].ipiv_ws = (int*)(base + oIpw1);
+  wpar[1].scratch = (double*)(base + oSc1);
   cudaStream_t st = f->st;
   int rc = 0;
 
@@ -353,66 +380,96 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   cudaMemsetAsync(w.status, 0, sizeof(int) * 4, st);
   cudaMemsetAsync(w.gstep, 0, sizeof(double) * (n + 1), st);
   cudaMemsetAsync(w.ipiv, 0, sizeof(int) * (size_t)n * nb, st);
+  // Two streams: st (the caller's) runs the trailing updates, sp (high priority) runs the panel
+  // stage of step k+1 as soon as step k has updated column block k+1 (lookahead depth 1).
+  cudaStream_t sp = panel_stream();
+  cudaEvent_t ev_ready = f->ev[0], ev_panel = f->ev[1];
   if (f->track_growth) launch_tile_norm_max(A, g, 0, w.gstep, st);
+  cudaEventRecord(ev_ready, st);
 
   const bool alpha_inf = isinf(alpha);
   Prof& P = f->prof;
   P.on = opt.profile != 0;
+  auto known_of = [&](int k) {
+    if (opt.forced) return opt.forced[k] ? (int)HLQ_DEC_QR : (int)HLQ_DEC_LU;
+    if (alpha == 0.0) return (int)HLQ_DEC_QR;
+    return -1;
+  };
+  const bool criterion_needed = !opt.forced && alpha > 0.0 && !alpha_inf;
   for (int k = 0; k < n; ++k) {
-    int known = -1;  // decision known on the host?
-    if (opt.forced)
-      known = opt.forced[k] ? HLQ_DEC_QR : HLQ_DEC_LU;
-    else if (alpha == 0.0)
-      known = HLQ_DEC_QR;
-    const bool criterion_needed = !opt.forced && alpha > 0.0 && !alpha_inf;
+    const DevWork& wk = wpar[k & 1];
+    const int known = known_of(k);
+    const int nl = (int)f->lvl_cnt[k].size();
+    // ---- panel stage P(k) on sp: criterion, speculative GETRF, decision, the chosen branch's
+    //      panel work (LU: commit + TRSM; QR: GEQRT + all TTQRT levels)
+    cudaStreamWaitEvent(sp, ev_ready, 0);
     if (known != HLQ_DEC_QR) {
       if (criterion_needed) {
-        P.begin(HLQ_PROF_CRITERION, st);
-        launch_panel_stats(A, g, k, w, st);
-        P.end(st);
+        P.begin(HLQ_PROF_CRITERION, sp);
+        launch_panel_stats(A, g, k, wk, sp);
+        P.end(sp);
       }
-      P.begin(HLQ_PROF_GETRF, st);
-      launch_getrf(A, g, k, w, true, st);
-      double* Li = w.scratch;
-      double* Ui = w.scratch + (size_t)nb * nb;
-      launch_tri_inv(g, k, w, Li, Ui, st);
-      P.end(st);
+      P.begin(HLQ_PROF_GETRF, sp);
+      launch_getrf(A, g, k, wk, true, sp);
+      launch_tri_inv(g, k, wk, wk.scratch, wk.scratch + (size_t)nb * nb, sp);
+      P.end(sp);
       if (criterion_needed && criterion != HLQ_CRIT_MUMPS) {
-        P.begin(HLQ_PROF_CRITERION, st);
-        launch_invnorm(g, k, w, st);
-        P.end(st);
+        P.begin(HLQ_PROF_CRITERION, sp);
+        launch_invnorm(g, k, wk, sp);
+        P.end(sp);
       }
     } else {
-      cudaMemsetAsync(w.zp, 0, sizeof(int), st);
+      cudaMemsetAsync(w.zp, 0, sizeof(int), sp);
     }
-    P.begin(HLQ_PROF_CRITERION, st);
+    P.begin(HLQ_PROF_CRITERION, sp);
     launch_decide(g, k, criterion, alpha, opt.mumps_reading, opt.tie_rel_tol, opt.forced != nullptr,
-                  w.ref_dec != nullptr, w, st);
-    P.end(st);
-    // a12 growth fused into the LU update epilogue when the CTA rows align with tile rows
-    const bool fuse_growth = f->track_growth && k + 1 < n && nb % 128 == 0;
+                  w.ref_dec != nullptr, wk, sp);
+    P.end(sp);
     if (known != HLQ_DEC_QR) {
-      P.begin(HLQ_PROF_LU_TRSM, st);
-      launch_lu_step(A, g, k, w, 0, st);
-      P.end(st);
-      P.begin(HLQ_PROF_LU_UPDATE, st);
-      launch_lu_step(A, g, k, w, fuse_growth ? 2 : 1, st);
-      P.end(st);
+      P.begin(HLQ_PROF_LU_TRSM, sp);
+      launch_lu_panel(A, g, k, wk, sp);
+      P.end(sp);
     }
     if (known != HLQ_DEC_LU) {
-      const int nl = (int)f->lvl_cnt[k].size();
-      for (int part = 0; part < 3; ++part) {
-        P.begin(HLQ_PROF_QR_GEQRT + part, st);
-        launch_qr_step(A, g, k, ib, f->lvl_ptr[k].data(), f->lvl_cnt[k].data(), nl, w, part, st);
-        P.end(st);
-      }
+      P.begin(HLQ_PROF_QR_GEQRT, sp);
+      launch_qr_panel(A, g, k, ib, f->lvl_ptr[k].data(), f->lvl_cnt[k].data(), nl, wk, sp);
+      P.end(sp);
     }
-    if (f->track_growth && k + 1 < n && !(fuse_growth && known == HLQ_DEC_LU)) {
+    cudaEventRecord(ev_panel, sp);
+    // ---- update stage U(k) on st: column block k+1 first (then P(k+1) may start), then the rest
+    cudaStreamWaitEvent(st, ev_panel, 0);
+    const int64_t k1 = g.r0(k) + g.bs(k);
+    const bool fuse = f->track_growth && k + 1 < n && nb % 128 == 0;
+    for (int part = 0; part < 2; ++part) {
+      const int64_t c0 = (part == 0) ? k1 : std::min(g.N, k1 + nb);
+      const int64_t c1 = (part == 0) ? std::min(g.N, k1 + nb) : g.N;
+      if (c1 > c0) {
+        if (known != HLQ_DEC_QR) {
+          P.begin(HLQ_PROF_LU_UPDATE, st);
+          launch_lu_update(A, g, k, wk, c0, c1, fuse ? w.colpart : nullptr, st);
+          P.end(st);
+        }
+        if (known != HLQ_DEC_LU) {
+          P.begin(HLQ_PROF_QR_UNMQR, st);
+          launch_qr_update(A, g, k, ib, f->lvl_ptr[k].data(), f->lvl_cnt[k].data(), nl, wk, c0, c1,
+                           st);
+          P.end(st);
+        }
+        // a12: the QR branch (or no fusion) scans the updated columns; the LU GEMM fused it
+        if (f->track_growth && k + 1 < n && !(fuse && known == HLQ_DEC_LU)) {
+          P.begin(HLQ_PROF_GROWTH, st);
+          if (fuse)
+            launch_tile_norm_max(A, g, k + 1, w.gstep + k + 1, st, w.dec, k, HLQ_DEC_QR, c0, c1);
+          else
+            launch_tile_norm_max(A, g, k + 1, w.gstep + k + 1, st, nullptr, 0, 0, c0, c1);
+          P.end(st);
+        }
+      }
+      if (part == 0) cudaEventRecord(ev_ready, st);
+    }
+    if (fuse && known != HLQ_DEC_QR) {
       P.begin(HLQ_PROF_GROWTH, st);
-      if (fuse_growth)  // LU steps got it from the GEMM epilogue: only a QR step needs the scan
-        launch_tile_norm_max(A, g, k + 1, w.gstep + k + 1, st, w.dec, k, HLQ_DEC_QR);
-      else
-        launch_tile_norm_max(A, g, k + 1, w.gstep + k + 1, st);
+      launch_lu_growth(w, g, k, st);
       P.end(st);
     }
   }
@@ -526,13 +583,12 @@ int hlq_get_profile(hlq_factors_t f, double* ms, double* flops, int64_t* launche
     double b = g.bs(k), M = (double)(g.N - g.r0(k) - g.bs(k));
     if (f->dec[k] == HLQ_DEC_LU) {
       fl[HLQ_PROF_GETRF] += 2.0 / 3.0 * b * b * b;
-      fl[HLQ_PROF_LU_TRSM] += 2.0 * M * b * b;       // Table I: TRSM + SWPTRSM
-      fl[HLQ_PROF_LU_UPDATE] += 2.0 * M * M * b;     // Table I: GEMM
+      fl[HLQ_PROF_LU_TRSM] += M * b * b;             // Table I: TRSM
+      fl[HLQ_PROF_LU_UPDATE] += M * b * b + 2.0 * M * M * b;  // Table I: SWPTRSM + GEMM
     } else {
       double m = M / b;                              // trailing tiles (fractional if ragged)
-      fl[HLQ_PROF_QR_GEQRT] += (m + 1.0) * 4.0 / 3.0 * b * b * b;
-      fl[HLQ_PROF_QR_UNMQR] += (m + 1.0) * 2.0 * b * b * M;
-      fl[HLQ_PROF_QR_TT] += m * (2.0 / 3.0 * b * b * b + 2.0 * b * b * M);
+      fl[HLQ_PROF_QR_GEQRT] += (m + 1.0) * 4.0 / 3.0 * b * b * b + m * 2.0 / 3.0 * b * b * b;
+      fl[HLQ_PROF_QR_UNMQR] += (m + 1.0) * 2.0 * b * b * M + m * 2.0 * b * b * M;
     }
   }
   for (int c = 0; c < HLQ_PROF_NCLASSES; ++c) {
@@ -592,6 +648,8 @@ void hlq_free(hlq_factors_t f) {
     cache_put(0, f->ws_block, f->ws_bytes);
   }
   f->prof.collect();
+  for (auto e : f->ev)
+    if (e) cudaEventDestroy(e);
   delete f;
 }
 

@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(256, 2)
     k_dgemm(double* __restrict__ C, int64_t ldc, const double* __restrict__ A, int64_t lda,
             const double* __restrict__ B, int64_t ldb, int64_t M, int64_t N, int K, int neg,
             int beta, const uint8_t* __restrict__ dec, int k, int want,
-            double* __restrict__ colpart) {
+            double* __restrict__ colpart, int64_t ldp) {
   if (dec != nullptr && dec[k] != want) return;  // predicated launch: the other branch was taken
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(256, 2)
       }
     __syncthreads();
     if (tid < 64 && n0 + tid < N)
-      colpart[tm * N + n0 + tid] = ((red[tid] + red[64 + tid]) + red[128 + tid]) + red[192 + tid];
+      colpart[tm * ldp + n0 + tid] = ((red[tid] + red[64 + tid]) + red[128 + tid]) + red[192 + tid];
   }
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
@@ -206,7 +206,9 @@ static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 // C[M x N] = beta*C + (neg ? -1 : 1) * A[M x K] * B[K x N]; dec/k/want: optional predicate.
 void launch_dgemm(double* C, int64_t ldc, const double* A, int64_t lda, const double* B,
                   int64_t ldb, int64_t M, int64_t N, int K, bool neg, bool beta,
-                  const uint8_t* dec, int k, int want, cudaStream_t st, double* colpart) {
+                  const uint8_t* dec, int k, int want, cudaStream_t st, double* colpart,
+                  int64_t ldp) {
+  if (ldp == 0) ldp = N;
   if (M <= 0 || N <= 0 || K <= 0) return;
   static bool attr = false;
   if (!attr) {
@@ -219,10 +221,10 @@ void launch_dgemm(double* C, int64_t ldc, const double* A, int64_t lda, const do
              (K % 2 == 0);
   if (v16)
     { ::hlq::g_launches++; k_dgemm<true><<<(unsigned)tiles, 256, GEMM_SMEM, st>>>(C, ldc, A, lda, B, ldb, M, N, K,
-                                                           neg ? 1 : 0, beta ? 1 : 0, dec, k, want, colpart); }
+                                                           neg ? 1 : 0, beta ? 1 : 0, dec, k, want, colpart, ldp); }
   else
     { ::hlq::g_launches++; k_dgemm<false><<<(unsigned)tiles, 256, GEMM_SMEM, st>>>(C, ldc, A, lda, B, ldb, M, N, K,
-                                                            neg ? 1 : 0, beta ? 1 : 0, dec, k, want, colpart); }
+                                                            neg ? 1 : 0, beta ? 1 : 0, dec, k, want, colpart, ldp); }
 }
 
 // a12 from the fused epilogue: tile row i = CTA row blocks [i*bpt, (i+1)*bpt); tile-norm max over

@@ -50,7 +50,10 @@ struct DevWork {
   double* ref_margin; // n or null
   double* gstep;      // n+1: max tile norm of the active matrix at the start of each step
   int2* pairs;        // TT pair lists of every step/level (host-planned)
-  double* scratch;    // general scratch
+  double* scratch;    // per-parity scratch: Li (nb^2), Ui (nb^2), perm (nb ints)
+  double* ws_panel;   // N*nb: panel copy for the TRSM (panel stream)
+  double* ws_row;     // N*nb: row-block copy for the SWPTRSM (update stream)
+  double* colpart;    // fused growth partials (ceil(N/128) x N) or null
 };
 
 // ---- kernels-side launch helpers (defined in the .cu files) ---------------------------------
@@ -59,15 +62,21 @@ void launch_getrf(const double* A, Geo g, int k, DevWork w, bool need, cudaStrea
 void launch_invnorm(Geo g, int k, DevWork w, cudaStream_t st);
 void launch_decide(Geo g, int k, int crit, double alpha, int mumps_reading, double tie_tol,
                    int has_forced, int has_ref, DevWork w, cudaStream_t st);
-void launch_lu_step(double* A, Geo g, int k, DevWork w, int part, cudaStream_t st);
+void launch_lu_panel(double* A, Geo g, int k, const DevWork& w, cudaStream_t st);
+void launch_lu_update(double* A, Geo g, int k, const DevWork& w, int64_t c0, int64_t c1,
+                      double* colpart, cudaStream_t st);
+void launch_lu_growth(const DevWork& w, Geo g, int k, cudaStream_t st);
 void launch_gemm_sub(double* C, int64_t ldc, const double* Am, int64_t lda, const double* Bm,
                      int64_t ldb, int64_t M, int64_t Nc, int K, const uint8_t* dec, int k,
                      cudaStream_t st);
-void launch_qr_step(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
-                    const int* level_count, int nlevels, DevWork w, int part,
-                    cudaStream_t st);
+void launch_qr_panel(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
+                     const int* level_count, int nlevels, const DevWork& w, cudaStream_t st);
+void launch_qr_update(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
+                      const int* level_count, int nlevels, const DevWork& w, int64_t c0,
+                      int64_t c1, cudaStream_t st);
 void launch_tile_norm_max(const double* A, Geo g, int k, double* out, cudaStream_t st,
-                          const uint8_t* dec = nullptr, int step = 0, int want = 0);
+                          const uint8_t* dec = nullptr, int step = 0, int want = 0,
+                          int64_t cb = -1, int64_t ce = -1);
 void launch_generate(double* dst, int64_t rows, int64_t cols, int64_t ld, uint64_t seed,
                      uint64_t idx0, int64_t idx_ld, cudaStream_t st);
 // solve

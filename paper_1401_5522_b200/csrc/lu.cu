@@ -13,7 +13,7 @@ namespace hlq {
 void launch_dgemm(double* C, int64_t ldc, const double* A, int64_t lda, const double* B,
                   int64_t ldb, int64_t M, int64_t N, int K, bool neg, bool beta,
                   const uint8_t* dec, int k, int want, cudaStream_t st,
-                  double* colpart = nullptr);
+                  double* colpart = nullptr, int64_t ldp = 0);
 void launch_colpart_max(const double* colpart, int64_t M, int64_t N, int nb, double* out,
                         const uint8_t* dec, int k, int want, cudaStream_t st);
 void launch_tri_inv(Geo g, int k, const DevWork& w, double* Li, double* Ui, cudaStream_t st);
@@ -62,37 +62,49 @@ static unsigned grid_for(int64_t total) {
   return (unsigned)(b < 1 ? 1 : b);
 }
 
-void launch_lu_step(double* A, Geo g, int k, DevWork w, int part, cudaStream_t st) {
+// Panel stage of an LU step (column block k only): Factor (commit W, ipiv) + Eliminate (TRSM).
+void launch_lu_panel(double* A, Geo g, int k, const DevWork& w, cudaStream_t st) {
   const int bk = g.bs(k);
   const int64_t k0 = g.r0(k), k1 = k0 + bk;
-  const int64_t M = g.N - k1;  // rows (and columns) below / right of the diagonal tile
+  const int64_t M = g.N - k1;  // rows below the diagonal tile
   const uint8_t* dec = w.dec;
-  double* Li = w.scratch;
-  double* Ui = w.scratch + (size_t)g.nb * g.nb;
+  const double* Ui = w.scratch + (size_t)g.nb * g.nb;
   int* perm = reinterpret_cast<int*>(w.scratch + (size_t)2 * g.nb * g.nb);
-  const size_t perm_sz = ((size_t)g.nb + 63) / 64 * 64;
-  double* ws = w.scratch + (size_t)2 * g.nb * g.nb + perm_sz;  // N*nb doubles
-  if (part == 1 || part == 2) {
-    // Update: A[k1:N, k1:N] -= A[k1:N, k0:k1] * A[k0:k1, k1:N]; part 2 also fuses the a12 growth
-    // column sums into the epilogue (requires nb % 128 == 0) and reduces them into gstep[k+1]
-    double* colpart = (part == 2) ? ws : nullptr;
-    launch_dgemm(A + k1 * g.lda + k1, g.lda, A + k0 * g.lda + k1, g.lda, A + k1 * g.lda + k0,
-                 g.lda, M, M, bk, true, true, dec, k, HLQ_DEC_LU, st, colpart);
-    if (part == 2) launch_colpart_max(ws, M, M, g.nb, w.gstep + k + 1, dec, k, HLQ_DEC_LU, st);
-    return;
-  }
   { ::hlq::g_launches++; k_lu_commit<<<8, 256, 0, st>>>(A, g, k, w.W, w.ipiv_ws, w.ipiv, perm, dec); }
   if (M <= 0) return;
   // Eliminate: X = A[k1:N, k0:k1]; A[k1:N, k0:k1] = X * U^-1
-  { ::hlq::g_launches++; k_copy_block<<<grid_for(M * bk), 256, 0, st>>>(ws, M, A + k0 * g.lda + k1, g.lda, M, bk, nullptr,
-                                                 dec, k); }
-  launch_dgemm(A + k0 * g.lda + k1, g.lda, ws, M, Ui, g.nb, M, bk, bk, false, false, dec, k,
+  { ::hlq::g_launches++; k_copy_block<<<grid_for(M * bk), 256, 0, st>>>(w.ws_panel, M, A + k0 * g.lda + k1, g.lda, M, bk, nullptr, dec, k); }
+  launch_dgemm(A + k0 * g.lda + k1, g.lda, w.ws_panel, M, Ui, g.nb, M, bk, bk, false, false, dec,
+               k, HLQ_DEC_LU, st);
+}
+
+// Update stage of an LU step on the trailing columns [c0, c1) (absolute column indices >= k1):
+// Apply (SWPTRSM on row block k) + Update (DGEMM on all trailing rows).  colpart != nullptr fuses
+// the a12 column sums into the GEMM epilogue (leading dimension ldp = N - k1, column offset c0-k1).
+void launch_lu_update(double* A, Geo g, int k, const DevWork& w, int64_t c0, int64_t c1,
+                      double* colpart, cudaStream_t st) {
+  const int bk = g.bs(k);
+  const int64_t k0 = g.r0(k), k1 = k0 + bk;
+  const int64_t M = g.N - k1;
+  const int64_t nc = c1 - c0;
+  if (M <= 0 || nc <= 0) return;
+  const uint8_t* dec = w.dec;
+  const double* Li = w.scratch;
+  const int* perm = reinterpret_cast<const int*>(w.scratch + (size_t)2 * g.nb * g.nb);
+  double* ws = w.ws_row + (c0 - k1) * bk;  // disjoint per column range
+  // Apply: Y = P A[k0:k1, c0:c1]; A[k0:k1, c0:c1] = L^-1 * Y
+  { ::hlq::g_launches++; k_copy_block<<<grid_for(nc * bk), 256, 0, st>>>(ws, bk, A + c0 * g.lda + k0, g.lda, bk, nc, perm, dec, k); }
+  launch_dgemm(A + c0 * g.lda + k0, g.lda, Li, g.nb, ws, bk, bk, nc, bk, false, false, dec, k,
                HLQ_DEC_LU, st);
-  // Apply: Y = P A[k0:k1, k1:N]; A[k0:k1, k1:N] = L^-1 * Y
-  { ::hlq::g_launches++; k_copy_block<<<grid_for(M * bk), 256, 0, st>>>(ws, bk, A + k1 * g.lda + k0, g.lda, bk, M, perm,
-                                                 dec, k); }
-  launch_dgemm(A + k1 * g.lda + k0, g.lda, Li, g.nb, ws, bk, bk, M, bk, false, false, dec, k,
-               HLQ_DEC_LU, st);
+  // Update: A[k1:N, c0:c1] -= A[k1:N, k0:k1] * A[k0:k1, c0:c1]
+  launch_dgemm(A + c0 * g.lda + k1, g.lda, A + k0 * g.lda + k1, g.lda, A + c0 * g.lda + k0, g.lda,
+               M, nc, bk, true, true, dec, k, HLQ_DEC_LU, st,
+               colpart ? colpart + (c0 - k1) : nullptr, M);
+}
+
+void launch_lu_growth(const DevWork& w, Geo g, int k, cudaStream_t st) {
+  const int64_t M = g.N - (g.r0(k) + g.bs(k));
+  launch_colpart_max(w.colpart, M, M, g.nb, w.gstep + k + 1, w.dec, k, HLQ_DEC_LU, st);
 }
 
 }  // namespace hlq

@@ -69,16 +69,16 @@ void launch_panel_stats(const double* A, Geo g, int k, DevWork w, cudaStream_t s
 // abs-sums.  grid (tile rows, column groups of 64), 256 threads; atomicMax into *out (>= 0).
 __global__ void __launch_bounds__(256) k_tile_norm_max(const double* __restrict__ A, Geo g, int k,
                                                        double* out, const uint8_t* __restrict__ dec,
-                                                       int step, int want) {
+                                                       int step, int want, int64_t cb, int64_t ce) {
   if (dec != nullptr && dec[step] != want) return;
   const int i = k + blockIdx.x;
   const int bi = g.bs(i);
-  const int64_t c0 = g.r0(k) + (int64_t)blockIdx.y * 64;
+  const int64_t c0 = cb + (int64_t)blockIdx.y * 64;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double best = 0.0;
   for (int cc = warp; cc < 64; cc += 8) {
     int64_t c = c0 + cc;
-    if (c >= g.N) break;
+    if (c >= ce) break;
     const double* col = A + c * g.lda + g.r0(i);
     double sum = 0.0;
     for (int r = lane; r < bi; r += 32) sum += fabs(col[r]);
@@ -88,10 +88,13 @@ __global__ void __launch_bounds__(256) k_tile_norm_max(const double* __restrict_
 }
 
 void launch_tile_norm_max(const double* A, Geo g, int k, double* out, cudaStream_t st,
-                          const uint8_t* dec, int step, int want) {
-  int64_t ncols = g.N - g.r0(k);
+                          const uint8_t* dec, int step, int want, int64_t cb, int64_t ce) {
+  if (cb < 0) cb = g.r0(k);
+  if (ce < 0) ce = g.N;
+  int64_t ncols = ce - cb;
+  if (ncols <= 0) return;
   dim3 grid(g.n - k, (unsigned)((ncols + 63) / 64));
-  { ::hlq::g_launches++; k_tile_norm_max<<<grid, 256, 0, st>>>(A, g, k, out, dec, step, want); }
+  { ::hlq::g_launches++; k_tile_norm_max<<<grid, 256, 0, st>>>(A, g, k, out, dec, step, want, cb, ce); }
 }
 
 // ---------------------------------------------------------------------------------------------

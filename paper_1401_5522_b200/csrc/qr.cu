@@ -430,45 +430,51 @@ void launch_qr_panel_tc(double* A, Geo g, int k, int ib, double* Tg, double* Ttt
                         const int2* pairs, int npairs, const uint8_t* dec, bool tt,
                         cudaStream_t st);
 
-void launch_qr_step(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
-                    const int* level_count, int nlevels, DevWork w, int part,
-                    cudaStream_t st) {
-  const bool predicated = true;
+// Panel stage of a QR step (column block k only): GEQRT of every panel tile, then the TTQRT of
+// every level of the greedy tree (a TTQRT only touches panel tiles, so all levels run before any
+// trailing update).  Predicated on dec[k] == QR.
+void launch_qr_panel(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
+                     const int* level_count, int nlevels, const DevWork& w, cudaStream_t st) {
   set_attr_once();
-  size_t smem = qr_smem_bytes(g.nb);
-  const uint8_t* dec = predicated ? w.dec : nullptr;
-  const int64_t k1 = g.r0(k) + g.bs(k);
-  double* right = A + k1 * g.lda;
-  const int64_t ncols = g.N - k1;
-  unsigned slabs = (unsigned)((ncols + 63) / 64);
-  const bool tc0 = (ib == 32);
-  if (part == 0) {
-    if (tc0)
-      launch_qr_panel_tc(A, g, k, ib, w.Tg, w.Ttt, nullptr, 0, dec, false, st);
-    else
-      { ::hlq::g_launches++; k_geqrt<<<g.n - k, QT, smem, st>>>(A, g, k, ib, w.Tg, dec); }
-  }
-  const bool tc = (ib == 32);  // DMMA trailing updates (qr_dmma.cu) need 32-row reflector blocks
-  if (part == 1 && ncols > 0) {
+  const size_t smem = qr_smem_bytes(g.nb);
+  const uint8_t* dec = w.dec;
+  const bool tc = (ib == 32);
+  if (tc)
+    launch_qr_panel_tc(A, g, k, ib, w.Tg, w.Ttt, nullptr, 0, dec, false, st);
+  else
+    { ::hlq::g_launches++; k_geqrt<<<g.n - k, QT, smem, st>>>(A, g, k, ib, w.Tg, dec); }
+  for (int l = 0; l < nlevels; ++l) {
     if (tc)
-      launch_qr_update_dmma(A, g, k, ib, w.Tg, w.Ttt, level_pairs, level_count, nlevels, right,
-                            g.lda, ncols, dec, 0, st);
-    else
-      { ::hlq::g_launches++; k_unmqr<<<dim3(slabs, g.n - k), QT, smem, st>>>(A, g, k, ib, w.Tg, right, g.lda, ncols, dec); }
-  }
-  for (int l = 0; l < nlevels && part == 2; ++l) {
-    if (tc0)
       launch_qr_panel_tc(A, g, k, ib, w.Tg, w.Ttt, level_pairs[l], level_count[l], dec, true, st);
     else
       { ::hlq::g_launches++; k_ttqrt<<<level_count[l], QT, smem, st>>>(A, g, k, ib, w.Ttt, level_pairs[l], dec); }
-    if (ncols > 0) {
-      if (tc)
-        launch_qr_update_dmma(A, g, k, ib, w.Tg, w.Ttt, level_pairs, level_count, nlevels, right,
-                              g.lda, ncols, dec, 1 + l, st);
-      else
-        { ::hlq::g_launches++; k_ttmqr<<<dim3(slabs, level_count[l]), QT, smem, st>>>(A, g, k, ib, w.Ttt, level_pairs[l],
-                                                               right, g.lda, ncols, dec); }
-    }
+  }
+}
+
+// Update stage of a QR step on the trailing columns [c0, c1): UNMQR of every tile row, then the
+// TTMQR of every level in order.  Predicated on dec[k] == QR.
+void launch_qr_update(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
+                      const int* level_count, int nlevels, const DevWork& w, int64_t c0,
+                      int64_t c1, cudaStream_t st) {
+  set_attr_once();
+  const size_t smem = qr_smem_bytes(g.nb);
+  const uint8_t* dec = w.dec;
+  const int64_t ncols = c1 - c0;
+  if (ncols <= 0) return;
+  double* base = A + c0 * g.lda;
+  const unsigned slabs = (unsigned)((ncols + 63) / 64);
+  const bool tc = (ib == 32);  // DMMA trailing updates (qr_dmma.cu) need 32-row reflector blocks
+  if (tc)
+    launch_qr_update_dmma(A, g, k, ib, w.Tg, w.Ttt, level_pairs, level_count, nlevels, base,
+                          g.lda, ncols, dec, 0, st);
+  else
+    { ::hlq::g_launches++; k_unmqr<<<dim3(slabs, g.n - k), QT, smem, st>>>(A, g, k, ib, w.Tg, base, g.lda, ncols, dec); }
+  for (int l = 0; l < nlevels; ++l) {
+    if (tc)
+      launch_qr_update_dmma(A, g, k, ib, w.Tg, w.Ttt, level_pairs, level_count, nlevels, base,
+                            g.lda, ncols, dec, 1 + l, st);
+    else
+      { ::hlq::g_launches++; k_ttmqr<<<dim3(slabs, level_count[l]), QT, smem, st>>>(A, g, k, ib, w.Ttt, level_pairs[l], base, g.lda, ncols, dec); }
   }
 }
 
