@@ -8,7 +8,7 @@ LIB := paper_1401_5522_b200/libhlq.so
 
 all: $(LIB)
 
-build/obj/%.o: paper_1401_5522_b200/csrc/%.cu paper_1401_5522_b200/csrc/hlq_internal.cuh include/hlq.h
+build/obj/%.o: paper_1401_5522_b200/csrc/%.cu $(wildcard paper_1401_5522_b200/csrc/*.cuh) include/hlq.h
 	@mkdir -p build/obj
 	$(NVCC) $(FLAGS) -c $< -o $@
 

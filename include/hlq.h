@@ -168,6 +168,55 @@ int64_t hlq_launch_count(void);
 /* ABI self-description for bindings: sizeof(hlq_options), sizeof(hlq_info), version (1). */
 int hlq_abi(int32_t* sizeof_options, int32_t* sizeof_info, int32_t* version);
 
+/* ---------------------------------------------------------------------------------------------
+ * Multi-GPU: the 2D block-cyclic distribution of P:182-191 ("tile (i,j) is mapped onto process
+ * ((i-1) mod p, (j-1) mod q)"; 0-based here: tile row i -> process row i mod P, tile column j ->
+ * process column j mod Q; world rank r = p*Q + q).  Each rank stores its tiles in a local
+ * column-major array (ScaLAPACK layout, block size nb): local tile row li holds global tile row
+ * li*P + p, local tile column lj holds global tile column lj*Q + q; the ragged last tile stays last.
+ * QR-tree domains are tile rows mod D with P | D (opt.tree_domains, 0 -> D = P), so the intra-domain
+ * eliminations are rank-local and only the domain heads are merged across process rows
+ * (P:187-189).  Decisions and pivots are those of the single-GPU factorization with
+ * the same D; the factors agree with it to rounding (the same kernels run on the same tiles).
+ */
+typedef struct hlq_grid_s* hlq_grid_t; /* opaque; owned by the caller (hlq_grid_free) */
+
+/* 128-byte NCCL unique id into id128 (host).  Rank 0 calls it and shares the bytes with the other
+ * ranks (e.g. over torch.distributed).  HLQ_ERR_NCCL if libnccl.so.2 cannot be loaded. */
+int hlq_nccl_unique_id(void* id128);
+/* NCCL grid: one process per GPU (current device), nranks = P*Q, this process = rank.  Creates the
+ * world communicator and splits it into the row (size Q) and column (size P) communicators.
+ * Collective: every rank must call it.  Errors: -1..-5 arguments, HLQ_ERR_NCCL. */
+int hlq_grid_create_nccl(const void* id128, int32_t nranks, int32_t rank, int32_t P, int32_t Q,
+                         hlq_grid_t* out);
+/* Emulated grid: all P*Q ranks live in this process on the current device and every collective is
+ * a stream-ordered device-to-device copy (testing the distributed path on one GPU). */
+int hlq_grid_create_local(int32_t P, int32_t Q, hlq_grid_t* out);
+void hlq_grid_free(hlq_grid_t g);
+/* P, Q, number of ranks hosted by this process (1 or P*Q) and the world rank of the first one. */
+int hlq_grid_info(hlq_grid_t g, int32_t* P, int32_t* Q, int32_t* nlocal, int32_t* rank0);
+/* Local array shape of rank (p, q): rows mloc, columns nloc (host-only, no GPU needed). */
+int hlq_grid_local_shape(int64_t N, int32_t nb, int32_t P, int32_t Q, int32_t p, int32_t q,
+                         int64_t* mloc, int64_t* nloc);
+/* Host-only description of the step-k plan of process row p (tests): writes
+ * [li0, ms, diag, c, (head_local, head_global) x c, nlev, (cnt, (e,i) x cnt) x nlev,
+ *  ninter, (cnt, (slot_e, slot_i) x cnt) x ninter] into out (cap entries); returns the length.
+ * Intra pairs are local panel indices (local tile row - li0), inter pairs are head slots
+ * s = (d mod P) * (D/P) + d / P of domain d. */
+int hlq_dist_plan(int32_t n, int32_t P, int32_t D, int32_t p, int32_t k, int32_t* out, int32_t cap);
+/* Factor the distributed matrix in place.  A_local: one device pointer per rank hosted by this
+ * process (hlq_grid_info nlocal; rank order), lld: local leading dimensions (NULL or 0 -> mloc).
+ * Same criteria, options (forced / ref_dec / ref_margin are the global host vectors, identical on
+ * every rank), statuses and getters as hlq_factor_ex except hlq_get_pivots / hlq_get_T
+ * (HLQ_ERR_STATE).  ib must be 32.  Collective: every rank calls it with the same arguments.
+ * hlq_solve(f, b, x) on the returned handle: b and x are FULL N-vectors on this process's device
+ * (b replicated on every rank; x returned on every rank).
+ * Errors: -1 grid, -2 A_local, -3 lld, -4 N, -5 nb, -6 criterion, -7 alpha, -8 options,
+ * HLQ_ERR_*. */
+int hlq_factor_dist(hlq_grid_t grid, double* const* A_local, const int64_t* lld, int64_t N,
+                    int32_t nb, int32_t criterion, double alpha, const hlq_options* opt,
+                    hlq_factors_t* out);
+
 #ifdef __cplusplus
 }
 #endif

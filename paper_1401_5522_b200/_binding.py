@@ -68,6 +68,14 @@ def _load():
         "hlq_residual": ([P, I64, I64, P, P, P, P], I32),
         "hlq_get_profile": ([P, P, P, P], I32),
         "hlq_launch_count": ([], I64),
+        "hlq_nccl_unique_id": ([P], I32),
+        "hlq_grid_create_nccl": ([P, I32, I32, I32, I32, P], I32),
+        "hlq_grid_create_local": ([I32, I32, P], I32),
+        "hlq_grid_free": ([P], None),
+        "hlq_grid_info": ([P, P, P, P, P], I32),
+        "hlq_grid_local_shape": ([I64, I32, I32, I32, I32, I32, P, P], I32),
+        "hlq_dist_plan": ([I32, I32, I32, I32, I32, P, I32], I32),
+        "hlq_factor_dist": ([P, P, P, I64, I32, I32, D, P, P], I32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -272,3 +280,139 @@ def hlq_residual(A, N, lda, x, b, stream=None):
     r, an, xn = out
     return {"resid_inf": r, "A_inf": an, "x_inf": xn,
             "hpl3": r / (an * xn * 2.0 ** -53 * N) if an * xn > 0 else math.inf}
+
+
+# ------------------------------------------------------------------ 2D block-cyclic (row e)
+def local_shape(N: int, nb: int, P: int, Q: int, p: int, q: int):
+    """(mloc, nloc) of rank (p, q) (host-only)."""
+    m, n = C.c_int64(), C.c_int64()
+    _check(lib.hlq_grid_local_shape(N, nb, P, Q, p, q, C.byref(m), C.byref(n)), "local_shape")
+    return m.value, n.value
+
+
+def cyclic_rows(N: int, nb: int, P: int, p: int) -> np.ndarray:
+    """global row (or column) indices held by process row p, in local order (plumbing)."""
+    n = -(-N // nb)
+    parts = [np.arange(i * nb, min((i + 1) * nb, N)) for i in range(p, n, P)]
+    return np.concatenate(parts) if parts else np.zeros(0, dtype=np.int64)
+
+
+def scatter_block_cyclic(A: np.ndarray, nb: int, P: int, Q: int, p: int, q: int) -> np.ndarray:
+    N = A.shape[0]
+    return A[np.ix_(cyclic_rows(N, nb, P, p), cyclic_rows(N, nb, Q, q))]
+
+
+def gather_block_cyclic(locs: dict, N: int, nb: int, P: int, Q: int) -> np.ndarray:
+    """locs[(p, q)] = local numpy array -> global N x N."""
+    A = np.zeros((N, N))
+    for (p, q), L in locs.items():
+        if L.size == 0:
+            continue
+        A[np.ix_(cyclic_rows(N, nb, P, p), cyclic_rows(N, nb, Q, q))] = L
+    return A
+
+
+def dist_plan(n: int, P: int, D: int, p: int, k: int) -> dict:
+    """parsed hlq_dist_plan (host-only)."""
+    ln = lib.hlq_dist_plan(n, P, D, p, k, None, 0)
+    _check(ln, "hlq_dist_plan")
+    buf = np.zeros(ln, dtype=np.int32)
+    lib.hlq_dist_plan(n, P, D, p, k, buf.ctypes.data_as(C.c_void_p), ln)
+    v = buf.tolist()
+    out = {"li0": v[0], "ms": v[1], "diag": v[2]}
+    c = v[3]
+    pos = 4
+    out["heads"] = [(v[pos + 2 * t], v[pos + 2 * t + 1]) for t in range(c)]
+    pos += 2 * c
+
+    def levels():
+        nonlocal pos
+        nl = v[pos]
+        pos += 1
+        lv = []
+        for _ in range(nl):
+            cnt = v[pos]
+            pos += 1
+            lv.append([(v[pos + 2 * j], v[pos + 2 * j + 1]) for j in range(cnt)])
+            pos += 2 * cnt
+        return lv
+
+    out["intra"] = levels()
+    out["inter"] = levels()
+    return out
+
+
+class Grid:
+    """Owns an hlq_grid_t: NCCL (one process per GPU) or emulated (all ranks in this process)."""
+
+    def __init__(self, handle):
+        self.handle = C.c_void_p(handle)
+        P, Q, nl, r0 = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+        _check(lib.hlq_grid_info(self.handle, C.byref(P), C.byref(Q), C.byref(nl), C.byref(r0)),
+               "hlq_grid_info")
+        self.P, self.Q, self.nlocal, self.rank0 = P.value, Q.value, nl.value, r0.value
+
+    def ranks(self):
+        """(p, q) of the ranks hosted here, in the order hlq_factor_dist expects."""
+        return [divmod(self.rank0 + t, self.Q) for t in range(self.nlocal)]
+
+    def __del__(self):
+        self.free()
+
+    def free(self):
+        if getattr(self, "handle", None) and self.handle.value:
+            lib.hlq_grid_free(self.handle)
+            self.handle = C.c_void_p(None)
+
+
+def grid_local(P: int, Q: int) -> Grid:
+    h = C.c_void_p()
+    _check(lib.hlq_grid_create_local(P, Q, C.byref(h)), "hlq_grid_create_local")
+    return Grid(h.value)
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    _check(lib.hlq_nccl_unique_id(buf), "hlq_nccl_unique_id")
+    return bytes(buf)
+
+
+def grid_nccl(uid: bytes, nranks: int, rank: int, P: int, Q: int) -> Grid:
+    buf = (C.c_char * 128).from_buffer_copy(uid)
+    h = C.c_void_p()
+    _check(lib.hlq_grid_create_nccl(buf, nranks, rank, P, Q, C.byref(h)), "hlq_grid_create_nccl")
+    return Grid(h.value)
+
+
+def hlq_factor_dist(grid: Grid, A_locals, N: int, nb: int, criterion: int = CRIT_MAX,
+                    alpha: float = 1.0, opt: HlqOptions | None = None, *, lld=None, forced=None,
+                    ref_dec=None, ref_margin=None, stream=None, **fields) -> Factors:
+    """Factor the 2D block-cyclic matrix whose local arrays (torch float64 CUDA tensors with
+    column-major storage, one per rank hosted here) are A_locals, in place."""
+    if opt is None:
+        opt = hlq_default_options()
+        opt.tree_domains = 0
+    for k, v in fields.items():
+        setattr(opt, k, v)
+    keep = []
+    if forced is not None:
+        fa = np.ascontiguousarray(forced, dtype=np.uint8)
+        keep.append(fa)
+        opt.forced = fa.ctypes.data
+    if ref_dec is not None:
+        ra = np.ascontiguousarray(ref_dec, dtype=np.uint8)
+        rm = np.ascontiguousarray(ref_margin, dtype=np.float64)
+        keep += [ra, rm]
+        opt.ref_dec = ra.ctypes.data
+        opt.ref_margin = rm.ctypes.data
+    opt.stream = _stream_ptr(stream).value
+    ptrs = (C.c_void_p * len(A_locals))(*[t.data_ptr() if t.numel() else None for t in A_locals])
+    llds = (C.c_int64 * len(A_locals))(*([0] * len(A_locals) if lld is None else lld))
+    h = C.c_void_p()
+    rc = lib.hlq_factor_dist(grid.handle, ptrs, llds, N, nb, criterion, float(alpha), C.byref(opt),
+                             C.byref(h))
+    if rc < 0:
+        if h.value:
+            lib.hlq_free(h)
+        _check(rc, "hlq_factor_dist")
+    return Factors(h.value, list(A_locals), rc, tuple(keep) + (grid,))

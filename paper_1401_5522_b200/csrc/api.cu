@@ -13,7 +13,7 @@
 #include <new>
 #include <vector>
 
-#include "hlq_internal.cuh"
+#include "handle.cuh"
 
 namespace hlq {
 void launch_tri_inv(Geo g, int k, const DevWork& w, double* Li, double* Ui, cudaStream_t st);
@@ -26,6 +26,8 @@ void launch_final_scan(const double* A, int64_t N, int64_t lda, int* flag, cudaS
 
 namespace hlq {
 int64_t g_launches = 0;
+int dist_solve_entry(hlq_factors_t f, const double* b, double* x);
+void dist_free(DistState* d);
 }
 using namespace hlq;
 
@@ -75,56 +77,6 @@ void cache_put(int slot, void* p, size_t bytes) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 }  // namespace
 
-// CUDA-event profiler: begin/end pairs recorded on the factorization's stream, per kernel class.
-struct Prof {
-  bool on = false;
-  std::vector<cudaEvent_t> ev;  // pairs
-  std::vector<int> cls;
-  std::vector<int64_t> l0;      // launch counter at begin
-  int64_t launches[HLQ_PROF_NCLASSES] = {0};
-  double ms[HLQ_PROF_NCLASSES] = {0};
-  int cur = -1;
-  int debug = -1;
-  void check(const char* where, int k) {
-    if (debug < 0) debug = getenv("HLQ_DEBUG_SYNC") ? 1 : 0;
-    if (!debug) return;
-    cudaError_t e = cudaDeviceSynchronize();
-    if (e == cudaSuccess) e = cudaGetLastError();
-    if (e != cudaSuccess) fprintf(stderr, "[hlq debug] %s (k=%d): %s\n", where, k, cudaGetErrorString(e));
-  }
-  void begin(int c, cudaStream_t st) {
-    check("before stage", c);
-    cur = c;
-    if (!on) return;
-    cudaEvent_t e;
-    cudaEventCreate(&e);
-    cudaEventRecord(e, st);
-    ev.push_back(e);
-    cls.push_back(c);
-    l0.push_back(hlq::g_launches);
-  }
-  void end(cudaStream_t st) {
-    check("after stage", cur);
-    if (!on) return;
-    cudaEvent_t e;
-    cudaEventCreate(&e);
-    cudaEventRecord(e, st);
-    ev.push_back(e);
-    launches[cls.back()] += hlq::g_launches - l0.back();
-  }
-  void collect() {  // after a stream synchronisation
-    for (size_t i = 0; i + 1 < ev.size(); i += 2) {
-      float t = 0.f;
-      cudaEventElapsedTime(&t, ev[i], ev[i + 1]);
-      ms[cls[i / 2]] += t;
-    }
-    for (auto e : ev) cudaEventDestroy(e);
-    ev.clear();
-    cls.clear();
-    l0.clear();
-  }
-};
-
 // the library's high-priority panel stream (lookahead), created once per process
 static cudaStream_t panel_stream() {
   static cudaStream_t sp = nullptr;
@@ -135,31 +87,6 @@ static cudaStream_t panel_stream() {
   }
   return sp;
 }
-
-struct hlq_factors_s {
-  Prof prof;
-  cudaEvent_t ev[2] = {nullptr, nullptr};
-  double* A = nullptr;
-  Geo g{};
-  int ib = 32, D = 1, crit = 0;
-  double alpha = 1.0;
-  cudaStream_t st = nullptr;
-  bool blocking = true;
-  DevWork w{};
-  void* ws_block = nullptr;
-  size_t ws_bytes = 0;
-  // greedy-tree plan: per step k, levels l: device pointer + count
-  std::vector<std::vector<const int2*>> lvl_ptr;
-  std::vector<std::vector<int>> lvl_cnt;
-  // host results
-  std::vector<uint8_t> dec;
-  std::vector<double> margin;
-  std::vector<int> flags;
-  std::vector<double> gstep;
-  int status = 0;
-  double growth = 0.0;
-  bool track_growth = true;
-};
 
 static int cuda_err(cudaError_t e) {
   if (e == cudaSuccess) return 0;
@@ -275,6 +202,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   f->g.lda = lda;
   f->g.nb = nb;
   f->g.n = (int)((N + nb - 1) / nb);
+  f->g.Nc = N;
   f->ib = opt.ib;
   f->D = opt.tree_domains;
   f->crit = criterion;
@@ -523,6 +451,7 @@ int hlq_solve(hlq_factors_t f, const double* b, double* x) {
   if (!b) return -2;
   if (!x) return -3;
   if (f->status == HLQ_ST_SINGULAR) return HLQ_ST_SINGULAR;
+  if (f->dist) return hlq::dist_solve_entry(f, b, x);
   const Geo g = f->g;
   cudaStream_t st = f->st;
   int rc;
@@ -628,6 +557,7 @@ int hlq_get_growth(hlq_factors_t f, double* gr) {
 int hlq_get_pivots(hlq_factors_t f, int32_t* ipiv) {
   if (!f || f->dec.empty()) return -1;
   if (!ipiv) return -2;
+  if (f->dist) return HLQ_ERR_STATE;
   return cuda_err(cudaMemcpy(ipiv, f->w.ipiv, sizeof(int) * (size_t)f->g.n * f->g.nb,
                              cudaMemcpyDeviceToHost));
 }
@@ -637,12 +567,18 @@ int hlq_get_T(hlq_factors_t f, int32_t i, int32_t k, int32_t kind, double* T) {
   if (i < k || i >= f->g.n) return -2;
   if (kind < 0 || kind > 1) return -4;
   if (!T) return -5;
+  if (f->dist) return HLQ_ERR_STATE;
   const double* src = (kind == 0 ? f->w.Tg : f->w.Ttt) + tri_index(i, k, f->g.n) * (int64_t)f->ib * f->g.nb;
   return cuda_err(cudaMemcpy(T, src, sizeof(double) * f->ib * f->g.nb, cudaMemcpyDeviceToHost));
 }
 
 void hlq_free(hlq_factors_t f) {
   if (!f) return;
+  if (f->dist) {
+    cudaStreamSynchronize(f->st);
+    hlq::dist_free(f->dist);
+    f->dist = nullptr;
+  }
   if (f->ws_block) {
     cudaStreamSynchronize(f->st);
     cache_put(0, f->ws_block, f->ws_bytes);

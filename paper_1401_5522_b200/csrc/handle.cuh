@@ -1,0 +1,93 @@
+// The factorization handle behind hlq_factors_t and its CUDA-event profiler (shared by api.cu and
+// the 2D block-cyclic path in dist.cu).
+#pragma once
+#include <stdlib.h>
+#include <stdio.h>
+
+#include <vector>
+
+#include "hlq_internal.cuh"
+
+namespace hlq {
+struct DistState;
+}
+using hlq::DevWork;
+using hlq::Geo;
+
+// CUDA-event profiler: begin/end pairs recorded on the factorization's stream, per kernel class.
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;  // pairs
+  std::vector<int> cls;
+  std::vector<int64_t> l0;      // launch counter at begin
+  int64_t launches[HLQ_PROF_NCLASSES] = {0};
+  double ms[HLQ_PROF_NCLASSES] = {0};
+  int cur = -1;
+  int debug = -1;
+  void check(const char* where, int k) {
+    if (debug < 0) debug = getenv("HLQ_DEBUG_SYNC") ? 1 : 0;
+    if (!debug) return;
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) fprintf(stderr, "[hlq debug] %s (k=%d): %s\n", where, k, cudaGetErrorString(e));
+  }
+  void begin(int c, cudaStream_t st) {
+    check("before stage", c);
+    cur = c;
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    ev.push_back(e);
+    cls.push_back(c);
+    l0.push_back(hlq::g_launches);
+  }
+  void end(cudaStream_t st) {
+    check("after stage", cur);
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    ev.push_back(e);
+    launches[cls.back()] += hlq::g_launches - l0.back();
+  }
+  void collect() {  // after a stream synchronisation
+    for (size_t i = 0; i + 1 < ev.size(); i += 2) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, ev[i], ev[i + 1]);
+      ms[cls[i / 2]] += t;
+    }
+    for (auto e : ev) cudaEventDestroy(e);
+    ev.clear();
+    cls.clear();
+    l0.clear();
+  }
+};
+
+struct hlq_factors_s {
+  Prof prof;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  double* A = nullptr;
+  Geo g{};
+  int ib = 32, D = 1, crit = 0;
+  double alpha = 1.0;
+  cudaStream_t st = nullptr;
+  bool blocking = true;
+  DevWork w{};
+  void* ws_block = nullptr;
+  size_t ws_bytes = 0;
+  // greedy-tree plan: per step k, levels l: device pointer + count
+  std::vector<std::vector<const int2*>> lvl_ptr;
+  std::vector<std::vector<int>> lvl_cnt;
+  // host results
+  std::vector<uint8_t> dec;
+  std::vector<double> margin;
+  std::vector<int> flags;
+  std::vector<double> gstep;
+  int status = 0;
+  double growth = 0.0;
+  bool track_growth = true;
+  // 2D block-cyclic factorization state (dist.cu); nullptr on the single-GPU path
+  hlq::DistState* dist = nullptr;
+};
+

@@ -11,12 +11,19 @@ namespace hlq {
 extern int64_t g_launches;
 
 // ---- tile geometry (a0) -------------------------------------------------------------------
+// N = rows, Nc = columns (square on one GPU; a rank's local panel in the 2D block-cyclic path can
+// end in the ragged last tile row while its panel column is full width).
 struct Geo {
   int64_t N, lda;
   int nb, n;
+  int64_t Nc;
   __host__ __device__ int64_t r0(int i) const { return (int64_t)i * nb; }
   __host__ __device__ int bs(int i) const {
     int64_t r = N - (int64_t)i * nb;
+    return (int)(r < nb ? r : nb);
+  }
+  __host__ __device__ int cbs(int j) const {
+    int64_t r = Nc - (int64_t)j * nb;
     return (int)(r < nb ? r : nb);
   }
   __host__ __device__ double* tile(double* A, int i, int j) const {
@@ -58,6 +65,33 @@ struct DevWork {
 
 // ---- kernels-side launch helpers (defined in the .cu files) ---------------------------------
 void launch_panel_stats(const double* A, Geo g, int k, DevWork w, cudaStream_t st);
+// panel statistics into explicit outputs; diag != 0: tile k is the diagonal tile (local_max),
+// otherwise every tile i >= k is a sub-diagonal tile (s[i], away_max)
+void launch_panel_stats_to(const double* A, Geo g, int k, int diag, double* s, double* local_max,
+                           double* away_max, cudaStream_t st);
+void launch_tri_inv(Geo g, int k, const DevWork& w, double* Li, double* Ui, cudaStream_t st);
+void launch_lu_commit(double* A, Geo g, int k, const double* W, const int* ipiv_ws, int* ipiv,
+                      int* perm, const uint8_t* dec, cudaStream_t st);
+void launch_copy_block(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
+                       int64_t cols, const int* perm, const uint8_t* dec, int k, cudaStream_t st);
+void launch_dgemm(double* C, int64_t ldc, const double* A, int64_t lda, const double* B,
+                  int64_t ldb, int64_t M, int64_t N, int K, bool neg, bool beta,
+                  const uint8_t* dec, int k, int want, cudaStream_t st,
+                  double* colpart = nullptr, int64_t ldp = 0);
+void launch_qr_panel_tc(double* A, Geo g, int k, int ib, double* Tg, double* Ttt,
+                        const int2* pairs, int npairs, const uint8_t* dec, bool tt,
+                        cudaStream_t st);
+void launch_qr_update_dmma(const double* A, Geo g, int k, int ib, const double* Tg,
+                           const double* Ttt, const int2* const* level_pairs,
+                           const int* level_count, int nlevels, double* base, int64_t ldc,
+                           int64_t ncols, const uint8_t* dec, int what, cudaStream_t st);
+// TTMQR levels only (no UNMQR) on a column block: the solve's cross-rank head merges
+void launch_tt_apply(const double* A, Geo g, int k, int ib, const double* Ttt,
+                     const int2* const* level_pairs, const int* level_count, int nlevels,
+                     double* base, int64_t ldc, int64_t ncols, const uint8_t* dec,
+                     cudaStream_t st);
+void launch_gemv_sub(double* y, const double* B, int64_t ldb, int64_t M, int K, const double* v,
+                     cudaStream_t st);
 void launch_getrf(const double* A, Geo g, int k, DevWork w, bool need, cudaStream_t st);
 void launch_invnorm(Geo g, int k, DevWork w, cudaStream_t st);
 void launch_decide(Geo g, int k, int crit, double alpha, int mumps_reading, double tie_tol,

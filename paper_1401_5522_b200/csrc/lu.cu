@@ -10,13 +10,8 @@
 
 namespace hlq {
 
-void launch_dgemm(double* C, int64_t ldc, const double* A, int64_t lda, const double* B,
-                  int64_t ldb, int64_t M, int64_t N, int K, bool neg, bool beta,
-                  const uint8_t* dec, int k, int want, cudaStream_t st,
-                  double* colpart = nullptr, int64_t ldp = 0);
 void launch_colpart_max(const double* colpart, int64_t M, int64_t N, int nb, double* out,
                         const uint8_t* dec, int k, int want, cudaStream_t st);
-void launch_tri_inv(Geo g, int k, const DevWork& w, double* Li, double* Ui, cudaStream_t st);
 
 // A_kk <- W, ipiv[k*nb..] <- ipiv_ws, perm[r] = row of (P A_kk) r  (sequential swaps composed)
 __global__ void k_lu_commit(double* __restrict__ A, Geo g, int k, const double* __restrict__ W,
@@ -60,6 +55,19 @@ static unsigned grid_for(int64_t total) {
   int64_t b = (total + 255) / 256;
   if (b > 148 * 16) b = 148 * 16;
   return (unsigned)(b < 1 ? 1 : b);
+}
+
+void launch_lu_commit(double* A, Geo g, int k, const double* W, const int* ipiv_ws, int* ipiv,
+                      int* perm, const uint8_t* dec, cudaStream_t st) {
+  ::hlq::g_launches++;
+  k_lu_commit<<<8, 256, 0, st>>>(A, g, k, W, ipiv_ws, ipiv, perm, dec);
+}
+
+void launch_copy_block(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
+                       int64_t cols, const int* perm, const uint8_t* dec, int k, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return;
+  ::hlq::g_launches++;
+  k_copy_block<<<grid_for(rows * cols), 256, 0, st>>>(dst, ldd, src, lds, rows, cols, perm, dec, k);
 }
 
 // Panel stage of an LU step (column block k only): Factor (commit W, ipiv) + Eliminate (TRSM).

@@ -23,11 +23,11 @@ __device__ __forceinline__ double warp_nanmax(double v) {
 
 // grid: one block per tile row i in [k, n); 256 threads (8 warps, one column at a time each)
 __global__ void __launch_bounds__(256) k_panel_stats(const double* __restrict__ A, Geo g, int k,
-                                                     double* __restrict__ s,
+                                                     int diag, double* __restrict__ s,
                                                      double* __restrict__ local_max,
                                                      double* __restrict__ away_max) {
   const int i = k + blockIdx.x;
-  const int bi = g.bs(i), bk = g.bs(k);
+  const int bi = g.bs(i), bk = g.cbs(k);
   const double* T = g.tile(const_cast<double*>(A), i, k);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __shared__ double red[8];
@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(256) k_panel_stats(const double* __restrict__ 
     mx = warp_nanmax(mx);
     tile_norm = nanmax(tile_norm, sum);
     if (lane == 0) {
-      if (i == k)
+      if (diag && i == k)
         local_max[c] = mx;
       else
         atomic_max_nonneg(&away_max[c], mx);
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(256) k_panel_stats(const double* __restrict__ 
   }
   if (lane == 0) red[warp] = tile_norm;
   __syncthreads();
-  if (threadIdx.x == 0 && i > k) {
+  if (threadIdx.x == 0 && !(diag && i == k)) {
     double v = red[0];
     for (int w = 1; w < 8; ++w) v = nanmax(v, red[w]);
     s[i] = v;
@@ -60,8 +60,14 @@ __global__ void __launch_bounds__(256) k_panel_stats(const double* __restrict__ 
 }
 
 void launch_panel_stats(const double* A, Geo g, int k, DevWork w, cudaStream_t st) {
-  cudaMemsetAsync(w.away_max, 0, sizeof(double) * g.nb, st);
-  { ::hlq::g_launches++; k_panel_stats<<<g.n - k, 256, 0, st>>>(A, g, k, w.s, w.local_max, w.away_max); }
+  launch_panel_stats_to(A, g, k, 1, w.s, w.local_max, w.away_max, st);
+}
+
+void launch_panel_stats_to(const double* A, Geo g, int k, int diag, double* s, double* local_max,
+                           double* away_max, cudaStream_t st) {
+  cudaMemsetAsync(away_max, 0, sizeof(double) * g.nb, st);
+  if (g.n - k <= 0) return;
+  { ::hlq::g_launches++; k_panel_stats<<<g.n - k, 256, 0, st>>>(A, g, k, diag, s, local_max, away_max); }
 }
 
 // ---------------------------------------------------------------------------------------------

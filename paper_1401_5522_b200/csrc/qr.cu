@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(QT) k_geqrt(double* __restrict__ A, Geo g, int
   extern __shared__ double sm[];
   QRSmem s = carve(sm, g.nb);
   const int i = k + blockIdx.x;
-  const int bi = g.bs(i), bk = g.bs(k);
+  const int bi = g.bs(i), bk = g.cbs(k);
   double* tile = g.tile(A, i, k);
   double* T = Tg + tri_index(i, k, g.n) * (int64_t)ib * g.nb;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(QT) k_unmqr(const double* __restrict__ A, Geo 
   extern __shared__ double sm[];
   QRSmem s = carve(sm, g.nb);
   const int i = k + blockIdx.y;
-  const int bi = g.bs(i), bk = g.bs(k);
+  const int bi = g.bs(i), bk = g.cbs(k);
   const double* tile = g.tile(const_cast<double*>(A), i, k);
   const double* T = Tg + tri_index(i, k, g.n) * (int64_t)ib * g.nb;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(QT) k_ttqrt(double* __restrict__ A, Geo g, int
   QRSmem s = carve(sm, g.nb);
   const int2 pr = pairs[blockIdx.x];
   const int e = pr.x, i = pr.y;
-  const int bi = g.bs(i), bk = g.bs(k);
+  const int bi = g.bs(i), bk = g.cbs(k);
   double* Re = g.tile(A, e, k);
   double* Ri = g.tile(A, i, k);
   double* T = Ttt + tri_index(i, k, g.n) * (int64_t)ib * g.nb;
@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(QT) k_ttmqr(const double* __restrict__ A, Geo 
   QRSmem s = carve(sm, g.nb);
   const int2 pr = pairs[blockIdx.y];
   const int e = pr.x, i = pr.y;
-  const int bi = g.bs(i), bk = g.bs(k);
+  const int bi = g.bs(i), bk = g.cbs(k);
   const double* Vt = g.tile(const_cast<double*>(A), i, k);
   const double* T = Ttt + tri_index(i, k, g.n) * (int64_t)ib * g.nb;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -421,14 +421,18 @@ void launch_qr_apply(const double* A, Geo g, int k, int ib, const double* Tg, co
                                                            ldc, ncols, dec); }
 }
 
-void launch_qr_update_dmma(const double* A, Geo g, int k, int ib, const double* Tg,
-                           const double* Ttt, const int2* const* level_pairs,
-                           const int* level_count, int nlevels, double* base, int64_t ldc,
-                           int64_t ncols, const uint8_t* dec, int what, cudaStream_t st);
-
-void launch_qr_panel_tc(double* A, Geo g, int k, int ib, double* Tg, double* Ttt,
-                        const int2* pairs, int npairs, const uint8_t* dec, bool tt,
-                        cudaStream_t st);
+void launch_tt_apply(const double* A, Geo g, int k, int ib, const double* Ttt,
+                     const int2* const* level_pairs, const int* level_count, int nlevels,
+                     double* base, int64_t ldc, int64_t ncols, const uint8_t* dec,
+                     cudaStream_t st) {
+  set_attr_once();
+  size_t smem = qr_smem_bytes(g.nb);
+  if (ncols <= 0) return;
+  unsigned slabs = (unsigned)((ncols + 63) / 64);
+  for (int l = 0; l < nlevels; ++l)
+    { ::hlq::g_launches++; k_ttmqr<<<dim3(slabs, level_count[l]), QT, smem, st>>>(A, g, k, ib, Ttt, level_pairs[l], base,
+                                                           ldc, ncols, dec); }
+}
 
 // Panel stage of a QR step (column block k only): GEQRT of every panel tile, then the TTQRT of
 // every level of the greedy tree (a TTQRT only touches panel tiles, so all levels run before any

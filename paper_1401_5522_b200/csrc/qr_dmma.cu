@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(QD_T) k_unmqr_dmma(const double* __restrict__ 
   double* Us = Vs + 32 * ldc;
   double* Ts = Us + W * LDU;
   const int i = k + blockIdx.y;
-  const int bi = g.bs(i), bk = g.bs(k);
+  const int bi = g.bs(i), bk = g.cbs(k);
   const double* tile = g.tile(const_cast<double*>(A), i, k);
   const double* T = Tg + tri_index(i, k, g.n) * (int64_t)ib * g.nb;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(QD_T) k_ttmqr_dmma(const double* __restrict__ 
   double* Ts = Us + W * LDU;
   const int2 pr = pairs[blockIdx.y];
   const int e = pr.x, i = pr.y;
-  const int bi = g.bs(i), bk = g.bs(k);
+  const int bi = g.bs(i), bk = g.cbs(k);
   const double* Vt = g.tile(const_cast<double*>(A), i, k);
   const double* T = Ttt + tri_index(i, k, g.n) * (int64_t)ib * g.nb;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(QD_T) k_geqrt_tc(double* __restrict__ A, Geo g
   double* red = Cs;            // aliases Cs during the panel factorisation
   double* bc = Cs + 8 * 33;
   const int i = k + blockIdx.x;
-  const int bi = g.bs(i), bk = g.bs(k);
+  const int bi = g.bs(i), bk = g.cbs(k);
   double* tile = g.tile(A, i, k);
   double* T = Tg + tri_index(i, k, g.n) * (int64_t)ib * g.nb;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(QD_T) k_ttqrt_tc(double* __restrict__ A, Geo g
   double* Rs = Cs + 8 * 33 + 64;
   const int2 pr = pairs[blockIdx.x];
   const int e = pr.x, i = pr.y;
-  const int bi = g.bs(i), bk = g.bs(k);
+  const int bi = g.bs(i), bk = g.cbs(k);
   double* Re = g.tile(A, e, k);
   double* Ri = g.tile(A, i, k);
   double* T = Ttt + tri_index(i, k, g.n) * (int64_t)ib * g.nb;

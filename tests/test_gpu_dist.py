@@ -1,0 +1,128 @@
+"""GPU parity of the 2D block-cyclic path (row e): hlq_factor_dist on an EMULATED P x Q grid (all
+ranks in this process on one B200; the collectives become device copies, the kernels are the
+multi-GPU ones) vs the CPU oracle with the same QR-tree domains D (reading 16).
+
+Bar as in test_gpu_parity.py: identical decision vectors (near ties take the oracle's decision),
+normwise factor difference <= 1e-10, growth within 1e-10 relative, HPL3 <= 16; and the distributed
+factors equal the single-GPU factors with the same D to rounding.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import hlq_inputs as I
+from oracle import hlq_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def H():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1401_5522_b200 as H
+    return H
+
+
+def run_dist(H, A, b, nb, P, Q, crit=O.CRIT_MAX, alpha=1.0, D=None, forced=None, fo=None):
+    N = A.shape[0]
+    D = P if D is None else D
+    if fo is None:
+        fo = O.hybrid_factor(A, nb, crit, alpha, D=D, forced=forced)
+    grid = H.grid_local(P, Q)
+    locs = []
+    for (p, q) in grid.ranks():
+        L = H.scatter_block_cyclic(A, nb, P, Q, p, q)
+        locs.append(H.to_colmajor(L) if L.size else torch.zeros(0, dtype=torch.float64,
+                                                                 device="cuda"))
+    kw = dict(tree_domains=D)
+    if forced is not None:
+        f = H.hlq_factor_dist(grid, locs, N, nb, crit, alpha, forced=forced, **kw)
+    else:
+        f = H.hlq_factor_dist(grid, locs, N, nb, crit, alpha, ref_dec=fo.dec,
+                              ref_margin=np.nan_to_num(fo.margin, nan=1.0), **kw)
+    db = torch.from_numpy(np.ascontiguousarray(b)).cuda()
+    x = f.solve(db).cpu().numpy()
+    F = H.gather_block_cyclic(
+        {pq: (H.from_colmajor(t) if t.numel() else np.zeros((0, 0)))
+         for pq, t in zip(grid.ranks(), locs)}, N, nb, P, Q)
+    return fo, f, F, x
+
+
+def check(fo, f, F, x, A, b, tol=1e-10):
+    np.testing.assert_array_equal(f.decisions(), fo.dec)
+    diff = O.factor_diff(F, fo.A)
+    assert diff <= tol, f"factor diff {diff:.3e}"
+    assert f.growth() == pytest.approx(fo.growth, rel=1e-10)
+    h3 = O.hpl3(A, x, b)
+    assert h3 <= 16.0, h3
+    xo = O.solve(fo, b)
+    assert np.linalg.norm(x - xo) <= 1e-8 * max(1.0, np.linalg.norm(xo))
+    return diff
+
+
+@pytest.mark.parametrize("P,Q", [(1, 2), (2, 1), (2, 2), (2, 3)])
+@pytest.mark.parametrize("alpha", [1.0, math.inf, 1.2e4])
+def test_grid_max_criterion(H, P, Q, alpha):
+    N, nb = 1000, 64                       # 16 tiles, ragged last tile of 40
+    A = I.uniform_matrix(0, N)
+    b = I.uniform_rhs(0, N)
+    fo, f, F, x = run_dist(H, A, b, nb, P, Q, alpha=alpha)
+    check(fo, f, F, x, A, b)
+
+
+@pytest.mark.parametrize("P,Q,D", [(1, 1, 2), (1, 2, 2), (2, 2, 4), (2, 1, 2)])
+def test_grid_domains_match_single_gpu(H, P, Q, D):
+    """C5 fixes D = 2 on every grid so that all grids compute the same factorization."""
+    N, nb = 768, 64
+    A = I.uniform_matrix(2, N)
+    b = I.uniform_rhs(2, N)
+    fo, f, F, x = run_dist(H, A, b, nb, P, Q, alpha=1.0, D=D)
+    check(fo, f, F, x, A, b)
+    dA = H.to_colmajor(A)
+    fs = H.hlq_factor_ex(dA, N, nb, O.CRIT_MAX, 1.0, ref_dec=fo.dec,
+                         ref_margin=np.nan_to_num(fo.margin, nan=1.0), tree_domains=D)
+    np.testing.assert_array_equal(fs.decisions(), f.decisions())
+    assert O.factor_diff(F, H.from_colmajor(dA)) <= 1e-13
+
+
+@pytest.mark.parametrize("f_qr", [0.0, 0.5, 1.0])
+def test_grid_forced_patterns(H, f_qr):
+    N, nb = 1024, 128
+    A = I.uniform_matrix(3, N)
+    b = I.uniform_rhs(3, N)
+    forced = I.bernoulli_pattern(30, N // nb, f_qr)
+    fo, f, F, x = run_dist(H, A, b, nb, 2, 2, forced=forced)
+    check(fo, f, F, x, A, b)
+
+
+@pytest.mark.parametrize("crit,alpha", [(O.CRIT_SUM, 1e6), (O.CRIT_MUMPS, 4.0), (O.CRIT_MUMPS, 1.0)])
+def test_grid_other_criteria(H, crit, alpha):
+    N, nb = 768, 64
+    A, b = I.normal_system(1, N)
+    fo, f, F, x = run_dist(H, A, b, nb, 2, 2, crit=crit, alpha=alpha)
+    check(fo, f, F, x, A, b)
+
+
+@pytest.mark.parametrize("N,nb,P,Q", [(100, 128, 2, 2), (300, 64, 2, 3), (129, 64, 2, 2)])
+def test_grid_degenerate_sizes(H, N, nb, P, Q):
+    """n = 1 (ranks with empty local arrays), fewer tile rows than process rows, ragged 1-row tile."""
+    A = I.uniform_matrix(0, N)
+    b = I.uniform_rhs(0, N)
+    fo, f, F, x = run_dist(H, A, b, nb, P, Q, alpha=1.2e4)
+    check(fo, f, F, x, A, b)
+
+
+def test_grid_kronecker_worst_case(H):
+    """P:525-532 lifted to A_alpha (x) I_nb: every decision an exact tie (LU), growth 128."""
+    nb, n = 64, 8
+    A = np.ascontiguousarray(I.kron_lift(I.worst_case_max(n, 1.0), nb))
+    N = A.shape[0]
+    b = I.uniform_rhs(0, N)
+    fo, f, F, x = run_dist(H, A, b, nb, 2, 2, alpha=1.0, D=2)
+    assert f.growth() == 128.0
+    np.testing.assert_array_equal(f.decisions(), np.zeros(n, dtype=np.uint8))
+    assert O.factor_diff(F, fo.A) == 0.0
