@@ -216,6 +216,16 @@ int hlq_dist_plan(int32_t n, int32_t P, int32_t D, int32_t p, int32_t k, int32_t
 int hlq_factor_dist(hlq_grid_t grid, double* const* A_local, const int64_t* lld, int64_t N,
                     int32_t nb, int32_t criterion, double alpha, const hlq_options* opt,
                     hlq_factors_t* out);
+/* The counter generator of hlq_generate_uniform applied to the block-cyclic local arrays:
+ * local (r, c) of rank (p, q) = G_u(seed, gcol(c) * N + grow(r)) (the global matrix of the input
+ * recipe, each rank generating only its own tiles).  A_local / lld as in hlq_factor_dist. */
+int hlq_generate_uniform_cyclic(hlq_grid_t grid, double* const* A_local, const int64_t* lld,
+                                int64_t N, int32_t nb, uint64_t seed, void* stream);
+/* HPL3 pieces of a distributed ORIGINAL matrix: out3 (host) = ||A x - b||_inf,
+ * ||A||_inf, ||x||_inf; x, b full N-vectors on the device (replicated).  Row sums are reduced over
+ * the process row (NCCL allreduce / ascending q when emulated), maxima over the grid.  Collective. */
+int hlq_residual_dist(hlq_grid_t grid, double* const* A_local, const int64_t* lld, int64_t N,
+                      int32_t nb, const double* x, const double* b, double* out3, void* stream);
 
 #ifdef __cplusplus
 }

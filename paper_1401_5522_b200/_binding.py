@@ -76,6 +76,8 @@ def _load():
         "hlq_grid_local_shape": ([I64, I32, I32, I32, I32, I32, P, P], I32),
         "hlq_dist_plan": ([I32, I32, I32, I32, I32, P, I32], I32),
         "hlq_factor_dist": ([P, P, P, I64, I32, I32, D, P, P], I32),
+        "hlq_generate_uniform_cyclic": ([P, P, P, I64, I32, U64, P], I32),
+        "hlq_residual_dist": ([P, P, P, I64, I32, P, P, P, P], I32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -416,3 +418,22 @@ def hlq_factor_dist(grid: Grid, A_locals, N: int, nb: int, criterion: int = CRIT
             lib.hlq_free(h)
         _check(rc, "hlq_factor_dist")
     return Factors(h.value, list(A_locals), rc, tuple(keep) + (grid,))
+
+
+def _ptr_array(ts):
+    return (C.c_void_p * len(ts))(*[t.data_ptr() if t.numel() else None for t in ts])
+
+
+def hlq_generate_uniform_cyclic(grid: Grid, A_locals, N: int, nb: int, seed: int, stream=None):
+    _check(lib.hlq_generate_uniform_cyclic(grid.handle, _ptr_array(A_locals), None, N, nb, seed,
+                                           _stream_ptr(stream)), "hlq_generate_uniform_cyclic")
+
+
+def hlq_residual_dist(grid: Grid, A_locals, N: int, nb: int, x, b, stream=None):
+    out = np.zeros(3)
+    _check(lib.hlq_residual_dist(grid.handle, _ptr_array(A_locals), None, N, nb, _dptr(x),
+                                 _dptr(b), out.ctypes.data_as(C.c_void_p), _stream_ptr(stream)),
+           "hlq_residual_dist")
+    r, an, xn = out
+    return {"resid_inf": r, "A_inf": an, "x_inf": xn,
+            "hpl3": r / (an * xn * 2.0 ** -53 * N) if an * xn > 0 else math.inf}

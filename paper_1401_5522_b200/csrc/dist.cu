@@ -386,6 +386,71 @@ __global__ void k_scatter_segs(double* __restrict__ x, const double* __restrict_
   }
 }
 
+// counter-based uniform generator on a rank's block-cyclic local array (the same G_u(seed, j*N + i)
+// as hlq_generate_uniform on the global matrix; DESIGN.md input recipe)
+__device__ __forceinline__ uint64_t dmix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+__global__ void k_generate_cyclic(double* __restrict__ A, int64_t lld, int64_t mloc, int64_t nloc,
+                                  int64_t N, int nb, int P, int Q, int p, int q, uint64_t key) {
+  const uint64_t GAMMA = 0x9E3779B97F4A7C15ULL;
+  const int64_t total = mloc * nloc;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = t / mloc, r = t - c * mloc;
+    const int64_t li = r / nb, lj = c / nb;
+    const int64_t gi = (li * P + p) * nb + (r - li * nb);
+    const int64_t gj = (lj * Q + q) * nb + (c - lj * nb);
+    const uint64_t idx = (uint64_t)gj * (uint64_t)N + (uint64_t)gi;
+    const uint64_t u = dmix64(key + (idx + 1ULL) * GAMMA);
+    A[c * lld + r] = (double)(u >> 11) * 0x1.0p-53 - 0.5;
+  }
+}
+
+// HPL3 pieces on a rank: part[r] = sum_{local c} A(r,c) x[gcol(c)], part[mloc + r] = sum |A(r,c)|
+// (columns in ascending local order; the row reduction over process columns follows)
+__global__ void k_residual_part(const double* __restrict__ A, int64_t lld, int64_t mloc,
+                                int64_t nloc, int nb, int Q, int q, const double* __restrict__ x,
+                                double* __restrict__ part) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= mloc) return;
+  double acc = 0.0, rs = 0.0;
+  for (int64_t c = 0; c < nloc; ++c) {
+    const int64_t lj = c / nb;
+    const double a = A[c * lld + r];
+    acc += a * x[(lj * Q + q) * nb + (c - lj * nb)];
+    rs += fabs(a);
+  }
+  part[r] = acc;
+  part[mloc + r] = rs;
+}
+__global__ void k_add_vec(double* __restrict__ dst, const double* __restrict__ src, int64_t n) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    dst[t] += src[t];
+}
+// out[0] = max_r |part[r] - b[grow(r)]|, out[1] = max_r part[mloc + r], out[2] = max |x| (atomic)
+__global__ void k_residual_max(const double* __restrict__ part, int64_t mloc, int nb, int P, int p,
+                               const double* __restrict__ b, const double* __restrict__ x,
+                               int64_t N, double* out) {
+  double r0 = 0.0, r1 = 0.0, r2 = 0.0;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < mloc;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t li = r / nb;
+    const int64_t g = (li * P + p) * nb + (r - li * nb);
+    r0 = nanmax(r0, fabs(part[r] - b[g]));
+    r1 = nanmax(r1, part[mloc + r]);
+  }
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < N;
+       g += (int64_t)gridDim.x * blockDim.x)
+    r2 = nanmax(r2, fabs(x[g]));
+  atomic_max_nonneg(&out[0], r0);
+  atomic_max_nonneg(&out[1], r1);
+  atomic_max_nonneg(&out[2], r2);
+}
+
 static unsigned blocks_for(int64_t total) {
   int64_t b = (total + 255) / 256;
   if (b > 148 * 8) b = 148 * 8;
@@ -664,7 +729,7 @@ static Geo panel_geo(const DistState& ds, const Ctx& c, const StepPlan& sp, int6
   return g;
 }
 
-static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options& opt) {
+static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options& opt, Prof& PR) {
   const int n = ds.n, nb = ds.nb, P = ds.P, Q = ds.Q, S = ds.S, cc = ds.c, ib = ds.ib;
   cudaStream_t st = ds.st;
   const bool has_forced = opt.forced != nullptr;
@@ -705,11 +770,14 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
       double* Apan = c.A + (int64_t)lk * nb * c.lld + (int64_t)sp.li0 * nb;
       Geo gP = panel_geo(ds, c, sp, c.lld);
       gP.Nc = bk;
+      PR.begin(HLQ_PROF_CRITERION, st);
       cudaMemsetAsync(c.rec_send, 0, sizeof(double) * ds.rec_count, st);
       if (sp.ms > 0 && criterion_needed)
         launch_panel_stats_to(Apan, gP, 0, sp.diag, c.rec_send, c.rec_send + ds.ms_max + nb,
                               c.rec_send + ds.ms_max, st);
+      PR.end(st);
       if (sp.diag) {
+        PR.begin(HLQ_PROF_GETRF, st);
         cudaMemsetAsync(c.w.zp, 0, sizeof(int), st);
         cudaMemsetAsync(c.w.inv_norm, 0, sizeof(double), st);
         if (known != HLQ_DEC_QR) {
@@ -720,11 +788,14 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
         ::hlq::g_launches++;
         k_pack_owner<<<16, 256, 0, st>>>(c.rec_send + ds.ms_max + 2 * nb, c.w.inv_norm, c.w.zp,
                                          c.w.W, c.w.ipiv_ws, nb, bk);
+        PR.end(st);
       }
     }
+    PR.begin(HLQ_PROF_OTHER, st);
     if ((rc = col_allgather(ds, qk, [](Ctx& c) { return c.rec_send; },
                             [](Ctx& c) { return c.rec_recv; }, ds.rec_count)))
       return rc;
+    PR.end(st);
     // ---- B: decision, LU panel / QR panel + intra-domain tree
     for (auto& c : ds.ctx) {
       if (c.q != qk) continue;
@@ -733,16 +804,19 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
       Geo gP = panel_geo(ds, c, sp, c.lld);
       gP.Nc = bk;
       const uint8_t* dk = c.w.dec + k;
+      PR.begin(HLQ_PROF_CRITERION, st);
       ::hlq::g_launches++;
       k_unpack_stats<<<16, 256, 0, st>>>(c.rec_recv, ds.rec_count, ds.ms_max, k, n, P, pk, nb, bk,
                                          c.w.s, c.w.away_max, c.w.local_max, c.w.inv_norm, c.w.zp,
                                          c.w.W, c.w.ipiv_ws);
       launch_decide(gglob, k, crit, alpha, opt.mumps_reading, opt.tie_rel_tol, has_forced ? 1 : 0,
                     has_ref ? 1 : 0, c.w, st);
+      PR.end(st);
       double* Li = c.w.scratch;
       double* Ui = c.w.scratch + (size_t)nb * nb;
       int* perm = reinterpret_cast<int*>(c.w.scratch + (size_t)2 * nb * nb);
       if (known != HLQ_DEC_QR) {
+        PR.begin(HLQ_PROF_LU_TRSM, st);
         if (!sp.diag) launch_tri_inv(gglob, k, c.w, Li, Ui, st);
         if (sp.diag) launch_lu_commit(Apan, gP, 0, c.w.W, c.w.ipiv_ws, c.ipiv + (int64_t)k * nb,
                                       perm, dk, st);
@@ -753,22 +827,27 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
           launch_dgemm(Apan + r0, c.lld, c.w.ws_panel, M, Ui, nb, M, bk, bk, false, false, dk, 0,
                        HLQ_DEC_LU, st);
         }
+        PR.end(st);
       }
       if (known != HLQ_DEC_LU && sp.ms > 0) {
+        PR.begin(HLQ_PROF_QR_GEQRT, st);
         double* Tgk = c.Tg + ((int64_t)lk * c.mt + sp.li0) * ib * nb;
         double* Ttk = c.Ttt + ((int64_t)lk * c.mt + sp.li0) * ib * nb;
         launch_qr_panel_tc(Apan, gP, 0, ib, Tgk, Ttk, nullptr, 0, dk, false, st);
         for (size_t l = 0; l < c.intra_ptr[k].size(); ++l)
           launch_qr_panel_tc(Apan, gP, 0, ib, Tgk, Ttk, c.intra_ptr[k][l], c.intra_cnt[k][l], dk,
                              true, st);
+        PR.end(st);
       }
       ::hlq::g_launches++;
       k_pack_rows<<<blocks_for((int64_t)cc * nb * nb), 256, 0, st>>>(
           c.head_send, cc, head_idx(sp), Apan, c.lld, gP.N, nb, nb, bk);
     }
+    PR.begin(HLQ_PROF_OTHER, st);
     if ((rc = col_allgather(ds, qk, [](Ctx& c) { return c.head_send; },
                             [](Ctx& c) { return c.head_recv; }, (int64_t)cc * nb * nb)))
       return rc;
+    PR.end(st);
     // ---- C: inter-domain merges (redundant on the column), package
     for (auto& c : ds.ctx) {
       if (c.q != qk) continue;
@@ -789,6 +868,7 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
       gH.Nc = bk;
       ::hlq::g_launches++;
       k_stack<<<blocks_for((int64_t)S * nb * nb), 256, 0, st>>>(HM, c.head_recv, S, nb, nb);
+      PR.begin(HLQ_PROF_QR_GEQRT, st);
       if (known != HLQ_DEC_LU) {
         for (size_t l = 0; l < c.inter_ptr[k].size(); ++l)
           launch_qr_panel_tc(HM, gH, 0, ib, nullptr, MT, c.inter_ptr[k][l], c.inter_cnt[k][l], dk,
@@ -828,6 +908,7 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
                                      c.w.flags,
                                      reinterpret_cast<int*>(c.w.scratch + (size_t)2 * nb * nb), bk,
                                      k, nb);
+      PR.end(st);
     }
     auto pcount = [&](int p) {
       const int li0 = cyc_below(k, P, p);
@@ -835,7 +916,9 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
       const int64_t prow = std::max<int64_t>(0, cyc_extent(ds.N, nb, P, p) - (int64_t)li0 * nb);
       return ds.pkg_count(prow, ms);
     };
+    PR.begin(HLQ_PROF_OTHER, st);
     if ((rc = row_bcast(ds, qk, [](Ctx& c) { return c.pkg; }, pcount))) return rc;
+    PR.end(st);
     // ---- D: SWPTRSM / UNMQR + intra TTMQR, then pack the head rows
     for (auto& c : ds.ctx) {
       const StepPlan& sp = c.plan[k];
@@ -857,11 +940,14 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
       gK.n = sp.ms;
       gK.Nc = bk;
       if (known != HLQ_DEC_QR && sp.diag) {
+        PR.begin(HLQ_PROF_LU_UPDATE, st);
         launch_copy_block(c.w.ws_row, bk, base, c.lld, bk, ncl, perm, dk, 0, st);
         launch_dgemm(base, c.lld, pk_ + ds.off_Li(prow, sp.ms), nb, c.w.ws_row, bk, bk, ncl, bk,
                      false, false, dk, 0, HLQ_DEC_LU, st);
+        PR.end(st);
       }
       if (known != HLQ_DEC_LU && sp.ms > 0) {
+        PR.begin(HLQ_PROF_QR_UNMQR, st);
         const int nl = (int)c.intra_ptr[k].size();
         launch_qr_update_dmma(pk_, gK, 0, ib, pk_ + ds.off_Tg(prow), pk_ + ds.off_Ttt(prow, sp.ms),
                               c.intra_ptr[k].data(), c.intra_cnt[k].data(), nl, base, c.lld, ncl,
@@ -870,11 +956,13 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
           launch_qr_update_dmma(pk_, gK, 0, ib, pk_ + ds.off_Tg(prow),
                                 pk_ + ds.off_Ttt(prow, sp.ms), c.intra_ptr[k].data(),
                                 c.intra_cnt[k].data(), nl, base, c.lld, ncl, dk, 1 + l, st);
+        PR.end(st);
       }
       ::hlq::g_launches++;
       k_pack_rows<<<blocks_for((int64_t)cc * nb * ncl), 256, 0, st>>>(
           c.hr_send, cc, head_idx(sp), base, c.lld, prow, nb, ncl, ncl);
     }
+    PR.begin(HLQ_PROF_OTHER, st);
     for (int q = 0; q < Q; ++q) {
       const int lc1 = cyc_below(k + 1, Q, q);
       const int64_t ncl = std::max<int64_t>(0, cyc_extent(ds.N, nb, Q, q) - (int64_t)lc1 * nb);
@@ -882,6 +970,7 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
                               [](Ctx& c) { return c.hr_recv; }, (int64_t)cc * nb * ncl)))
         return rc;
     }
+    PR.end(st);
     // ---- E: Schur DGEMM / inter-domain TTMQR; growth
     const int dk_dom = k % ds.D;
     const int slot_k = (dk_dom % P) * cc + dk_dom / P;
@@ -898,10 +987,14 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
       ::hlq::g_launches++;
       k_stack<<<blocks_for(ldh * ncl), 256, 0, st>>>(c.HR, c.hr_recv, S, nb, ncl);
       const int64_t r0 = sp.diag ? bk : 0;
-      if (known != HLQ_DEC_QR && prow - r0 > 0)
+      if (known != HLQ_DEC_QR && prow - r0 > 0) {
+        PR.begin(HLQ_PROF_LU_UPDATE, st);
         launch_dgemm(base + r0, c.lld, pk_ + r0, prow, c.HR + (int64_t)slot_k * nb, ldh,
                      prow - r0, ncl, bk, true, true, dk, 0, HLQ_DEC_LU, st);
+        PR.end(st);
+      }
       if (known != HLQ_DEC_LU) {
+        PR.begin(HLQ_PROF_QR_UNMQR, st);
         Geo gH{};
         gH.N = ldh;
         gH.lda = ldh;
@@ -920,8 +1013,10 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
               base, c.lld, prow, cc, head_idx(sp), c.p * cc, c.HR, ldh, nb, ncl, 0, dk,
               HLQ_DEC_QR);
         }
+        PR.end(st);
       }
       if (opt.track_growth && k + 1 < n && prow - r0 > 0) {
+        PR.begin(HLQ_PROF_GROWTH, st);
         Geo gT{};
         gT.N = prow - r0;
         gT.Nc = c.nloc;
@@ -930,6 +1025,7 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
         gT.n = sp.ms - sp.diag;
         launch_tile_norm_max(c.A + (int64_t)sp.li0 * nb + r0, gT, 0, c.w.gstep + k + 1, st,
                              nullptr, 0, 0, (int64_t)lc1 * nb, c.nloc);
+        PR.end(st);
       }
     }
     if ((rc = cuda_check(cudaGetLastError()))) return rc;
@@ -1210,6 +1306,118 @@ int hlq_dist_plan(int32_t n, int32_t P, int32_t D, int32_t p, int32_t k, int32_t
   return (int)v.size();
 }
 
+int hlq_generate_uniform_cyclic(hlq_grid_t grid, double* const* A_local, const int64_t* lld,
+                                int64_t N, int32_t nb, uint64_t seed, void* stream) {
+  if (!grid) return -1;
+  if (!A_local) return -2;
+  if (N <= 0) return -4;
+  if (nb <= 0) return -5;
+  if (nb > N) nb = (int32_t)N;
+  uint64_t z = seed + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  const uint64_t key = z ^ (z >> 31);
+  const int nlocal = grid->local ? grid->P * grid->Q : 1;
+  for (int t = 0; t < nlocal; ++t) {
+    const int r = grid->local ? t : grid->rank;
+    const int p = r / grid->Q, q = r % grid->Q;
+    const int64_t mloc = cyc_extent(N, nb, grid->P, p), nloc = cyc_extent(N, nb, grid->Q, q);
+    const int64_t ld = (lld && lld[t]) ? lld[t] : std::max<int64_t>(mloc, 1);
+    if (mloc <= 0 || nloc <= 0) continue;
+    if (!A_local[t]) return -2;
+    if (ld < mloc) return -3;
+    ::hlq::g_launches++;
+    k_generate_cyclic<<<blocks_for(mloc * nloc), 256, 0, (cudaStream_t)stream>>>(
+        A_local[t], ld, mloc, nloc, N, nb, grid->P, grid->Q, p, q, key);
+  }
+  return cuda_check(cudaGetLastError());
+}
+
+int hlq_residual_dist(hlq_grid_t grid, double* const* A_local, const int64_t* lld, int64_t N,
+                      int32_t nb, const double* x, const double* b, double* out3, void* stream) {
+  if (!grid) return -1;
+  if (!A_local) return -2;
+  if (N <= 0) return -4;
+  if (nb <= 0) return -5;
+  if (!x) return -6;
+  if (!b) return -7;
+  if (!out3) return -8;
+  if (nb > N) nb = (int32_t)N;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int P = grid->P, Q = grid->Q;
+  const int nlocal = grid->local ? P * Q : 1;
+  const int64_t mmax = cyc_extent(N, nb, P, 0);
+  double* buf = nullptr;
+  int rc;
+  if ((rc = cuda_check(cudaMalloc(&buf, sizeof(double) * (nlocal * 2 * (mmax + 1) + 4 * nlocal)))))
+    return rc;
+  std::vector<int> ps(nlocal), qs(nlocal);
+  std::vector<int64_t> ml(nlocal);
+  for (int t = 0; t < nlocal; ++t) {
+    const int r = grid->local ? t : grid->rank;
+    ps[t] = r / Q;
+    qs[t] = r % Q;
+    ml[t] = cyc_extent(N, nb, P, ps[t]);
+    const int64_t nloc = cyc_extent(N, nb, Q, qs[t]);
+    const int64_t ld = (lld && lld[t]) ? lld[t] : std::max<int64_t>(ml[t], 1);
+    double* part = buf + (int64_t)t * 2 * (mmax + 1);
+    cudaMemsetAsync(part, 0, sizeof(double) * 2 * (mmax + 1), st);
+    if (ml[t] > 0 && nloc > 0) {
+      ::hlq::g_launches++;
+      k_residual_part<<<(unsigned)((ml[t] + 127) / 128), 128, 0, st>>>(A_local[t], ld, ml[t], nloc,
+                                                                       nb, Q, qs[t], x, part);
+    }
+  }
+  // sum the partials over each process row (ascending q), then every rank takes its row's sum
+  if (!grid->local) {
+    if (ml[0] > 0 &&
+        (rc = nccl_err(g_nccl.AllReduce(buf, buf, (size_t)(2 * ml[0]), ncclDouble, ncclSum,
+                                        grid->row, st),
+                       "allreduce(row)"))) {
+      cudaFree(buf);
+      return rc;
+    }
+  } else {
+    // parts are laid out [mloc | mloc]: add q = 1.. into q = 0, then copy back
+    for (int p = 0; p < P; ++p) {
+      const int t0 = p * Q;
+      double* dst = buf + (int64_t)t0 * 2 * (mmax + 1);
+      for (int q = 1; q < Q; ++q) {
+        ::hlq::g_launches++;
+        k_add_vec<<<blocks_for(2 * ml[t0]), 256, 0, st>>>(
+            dst, buf + (int64_t)(t0 + q) * 2 * (mmax + 1), 2 * ml[t0]);
+      }
+      for (int q = 1; q < Q; ++q)
+        cudaMemcpyAsync(buf + (int64_t)(t0 + q) * 2 * (mmax + 1), dst,
+                        sizeof(double) * 2 * ml[t0], cudaMemcpyDeviceToDevice, st);
+    }
+  }
+  double* outs = buf + (int64_t)nlocal * 2 * (mmax + 1);
+  cudaMemsetAsync(outs, 0, sizeof(double) * 4 * nlocal, st);
+  for (int t = 0; t < nlocal; ++t) {
+    ::hlq::g_launches++;
+    k_residual_max<<<64, 256, 0, st>>>(buf + (int64_t)t * 2 * (mmax + 1), ml[t], nb, P, ps[t], b, x,
+                                       N, outs + 4 * t);
+  }
+  if (!grid->local &&
+      (rc = nccl_err(g_nccl.AllReduce(outs, outs, 3, ncclDouble, ncclMax, grid->world, st),
+                     "allreduce(max)"))) {
+    cudaFree(buf);
+    return rc;
+  }
+  std::vector<double> h(4 * nlocal);
+  cudaMemcpyAsync(h.data(), outs, sizeof(double) * 4 * nlocal, cudaMemcpyDeviceToHost, st);
+  rc = cuda_check(cudaStreamSynchronize(st));
+  cudaFree(buf);
+  if (rc) return rc;
+  for (int j = 0; j < 3; ++j) {
+    double m = 0.0;
+    for (int t = 0; t < nlocal; ++t) m = std::max(m, h[4 * t + j]);
+    out3[j] = m;
+  }
+  return 0;
+}
+
 int hlq_factor_dist(hlq_grid_t grid, double* const* A_local, const int64_t* lld, int64_t N,
                     int32_t nb, int32_t criterion, double alpha, const hlq_options* opt_in,
                     hlq_factors_t* out) {
@@ -1295,7 +1503,8 @@ int hlq_factor_dist(hlq_grid_t grid, double* const* A_local, const int64_t* lld,
     int rc = dist_alloc(*ds, c, opt, has_ref);
     if (rc) return rc;
   }
-  int rc = dist_factor(*ds, criterion, alpha, opt);
+  f->prof.on = opt.profile != 0;
+  int rc = dist_factor(*ds, criterion, alpha, opt, f->prof);
   if (rc) return rc;
   Ctx& c0 = ds->ctx[0];
   f->dec.resize(n);

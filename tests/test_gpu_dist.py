@@ -126,3 +126,54 @@ def test_grid_kronecker_worst_case(H):
     assert f.growth() == 128.0
     np.testing.assert_array_equal(f.decisions(), np.zeros(n, dtype=np.uint8))
     assert O.factor_diff(F, fo.A) == 0.0
+
+
+def test_cyclic_generator_bit_identical(H):
+    """Each rank generates only its own tiles of the seeded global matrix (C5 recipe)."""
+    N, nb, P, Q = 1000, 64, 2, 3
+    grid = H.grid_local(P, Q)
+    locs = []
+    for (p, q) in grid.ranks():
+        m, n = H.local_shape(N, nb, P, Q, p, q)
+        locs.append(torch.empty(m * n, dtype=torch.float64, device="cuda"))
+    H.hlq_generate_uniform_cyclic(grid, locs, N, nb, 2)
+    torch.cuda.synchronize()
+    got = H.gather_block_cyclic(
+        {pq: t.cpu().numpy().reshape(H.local_shape(N, nb, P, Q, *pq)[1], -1).T
+         for pq, t in zip(grid.ranks(), locs)}, N, nb, P, Q)
+    np.testing.assert_array_equal(got, I.uniform_matrix(2, N))
+
+
+def test_distributed_residual_matches_host(H):
+    N, nb, P, Q = 700, 64, 2, 2
+    A = I.uniform_matrix(4, N)
+    b = I.uniform_rhs(4, N)
+    x = np.linalg.solve(A, b)
+    grid = H.grid_local(P, Q)
+    locs = [H.to_colmajor(H.scatter_block_cyclic(A, nb, P, Q, p, q)) for (p, q) in grid.ranks()]
+    dx = torch.from_numpy(x).cuda()
+    db = torch.from_numpy(b).cuda()
+    r = H.hlq_residual_dist(grid, locs, N, nb, dx, db)
+    assert r["A_inf"] == pytest.approx(np.abs(A).sum(axis=1).max(), rel=1e-14)
+    assert r["x_inf"] == np.abs(x).max()
+    assert r["resid_inf"] == pytest.approx(np.abs(A @ x - b).max(), rel=0.5, abs=1e-15)
+    assert r["hpl3"] == pytest.approx(O.hpl3(A, x, b), rel=0.5, abs=1e-3)
+
+
+def test_nccl_grid_single_rank(H):
+    """The NCCL plumbing (unique id, CommInitRank, row/column CommSplit, AllGather, Broadcast,
+    AllReduce) on a real 1 x 1 communicator gives the emulated grid's factorization."""
+    N, nb = 768, 64
+    A = I.uniform_matrix(0, N)
+    b = I.uniform_rhs(0, N)
+    fo = O.hybrid_factor(A, nb, O.CRIT_MAX, 1.2e4, D=2)
+    uid = H.nccl_unique_id()
+    grid = H.grid_nccl(uid, 1, 0, 1, 1)
+    dA = H.to_colmajor(A)
+    f = H.hlq_factor_dist(grid, [dA], N, nb, O.CRIT_MAX, 1.2e4, ref_dec=fo.dec,
+                          ref_margin=np.nan_to_num(fo.margin, nan=1.0), tree_domains=2)
+    db = torch.from_numpy(b).cuda()
+    x = f.solve(db).cpu().numpy()
+    check(fo, f, H.from_colmajor(dA), x, A, b)
+    f.free()
+    grid.free()
