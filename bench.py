@@ -12,8 +12,9 @@ Inputs (8.6 GB) exceed the 126 MB L2, so no explicit flush is needed between tim
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3|C2|C1|C4A..] [--fqr F]
                   [--criterion max|sum|mumps --alpha A] [--impl reference]
-Under torchrun each rank factors its own independent system (weak scaling; the 2D block-cyclic
-distributed factorization is DESIGN.md row e).
+Under torchrun (N > 1 GPUs) the SAME global system is factored on a P x Q process grid, 2D
+block-cyclic (DESIGN.md row e; 2 -> 1x2, 4 -> 2x2, 8 -> 2x4; QR-tree domains D = 2 on every grid so
+every grid computes the same factorization), one rank per GPU over NCCL: strong scaling.
 """
 from __future__ import annotations
 
@@ -58,6 +59,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-N", type=int, default=4096)
+    ap.add_argument("--dist", action="store_true",
+                    help="use the 2D block-cyclic NCCL path even on one GPU (1x1 grid)")
     return ap.parse_args()
 
 
@@ -155,7 +158,7 @@ def run_reference(args, cfg, rank):
     out = {"impl": "reference", "metric": "FP64 TFLOP/s (2N^3/3 basis) hybrid LU-QR",
            "value": val, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": workload_config(args, cfg), "hpl3": h3,
            "cpu_baseline": {"kind": "oracle", "cores": cpu_threads(), "sample": sample,
                             "value": val, "unit": "TFLOP/s"},
@@ -164,15 +167,21 @@ def run_reference(args, cfg, rank):
     print(json.dumps(out), flush=True)
 
 
+def grid_shape(world):
+    return {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}.get(world, (1, world))
+
+
 def workload_config(args, cfg):
     N, nb = cfg["N"], cfg["nb"]
     if args.criterion:
         dec = f"{args.criterion} criterion alpha={args.alpha}"
     else:
         dec = f"forced Bernoulli pattern f_QR={args.fqr} (seed 30)"
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    P, Q = grid_shape(world)
     return {"workload": f"{args.config}: N={N}, nb={nb}, FP64 {cfg['gen']} seed {cfg['seed']}, {dec}",
-            "N": N, "nb": nb, "n_tiles": (N + nb - 1) // nb, "global_batch": args.gpus,
-            "parallelism": f"replicas{args.gpus}" if args.gpus > 1 else "single",
+            "N": N, "nb": nb, "n_tiles": (N + nb - 1) // nb, "global_batch": 1,
+            "parallelism": f"2D block-cyclic grid {P}x{Q} (NCCL), D=2" if world > 1 else "single",
             "l2": "inputs (8*N^2 bytes) > 126 MB L2: no flush needed"}
 
 
@@ -200,12 +209,19 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1 or args.dist:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=dev)
+        run_distributed(args, cfg, rank, world, local, dev)
+        dist.destroy_process_group()
+        return
     stream = torch.cuda.current_stream()
     N, nb = cfg["N"], cfg["nb"]
     n = (N + nb - 1) // nb
-    seed = cfg["seed"] + 1000 * rank  # independent system per rank (weak scaling)
+    seed = cfg["seed"]
     # inputs generated on the device with the counter generator (bit-identical to hlq_inputs)
     A0 = torch.empty(N * N, dtype=torch.float64, device=dev)
     b = torch.empty(N, dtype=torch.float64, device=dev)
@@ -339,7 +355,7 @@ def main():
     if rank == 0:
         out = {"metric": "FP64 TFLOP/s (2N^3/3 basis) hybrid LU-QR", "value": value,
                "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-               "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+               "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                "config": workload_config(args, cfg),
                "true_tflops": true * world / (ms_step * 1e-3) / 1e12,
@@ -353,6 +369,150 @@ def main():
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------- multi-GPU arm (row e)
+def run_distributed(args, cfg, rank, world, local, dev):
+    """One system on a P x Q grid: each rank holds its block-cyclic tiles; NCCL carries the
+    statistics allgather, the panel broadcast and the head-row exchange (dist.cu)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import hlq_inputs as I
+    import paper_1401_5522_b200 as H
+
+    P, Q = grid_shape(world)
+    p, q = divmod(rank, Q)
+    obj = [H.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    grid = H.grid_nccl(obj[0], world, rank, P, Q)
+    N, nb = cfg["N"], cfg["nb"]
+    n = (N + nb - 1) // nb
+    D = 2
+    mloc, nloc = H.local_shape(N, nb, P, Q, p, q)
+    stream = torch.cuda.current_stream()
+    # no second copy of A (C5 on one GPU is 137 GB): uniform inputs are regenerated on the device
+    # before every step (outside the timed region), other recipes are re-uploaded from pinned host
+    A = torch.empty(max(mloc * nloc, 1), dtype=torch.float64, device=dev)
+    b = torch.empty(N, dtype=torch.float64, device=dev)
+    Ah_local = None
+    if cfg["gen"] == "uniform":
+        H.hlq_generate_uniform(b, N, 1, N, cfg["seed"], N * N, N)
+    else:
+        Ah, bh, _ = I.config_system(args.config, N)
+        L = H.scatter_block_cyclic(Ah, nb, P, Q, p, q)
+        Ah_local = torch.zeros(max(mloc * nloc, 1), dtype=torch.float64).pin_memory()
+        Ah_local[:L.size].copy_(torch.from_numpy(np.ascontiguousarray(L.T)).reshape(-1))
+        b.copy_(torch.from_numpy(bh))
+        del Ah, L
+
+    def restore():
+        if Ah_local is None:
+            H.hlq_generate_uniform_cyclic(grid, [A], N, nb, cfg["seed"])
+        else:
+            A.copy_(Ah_local, non_blocking=True)
+
+    x = torch.empty_like(b)
+    crit = CRIT[args.criterion] if args.criterion else 0
+    forced = None if args.criterion else I.bernoulli_pattern(30, n, args.fqr)
+
+    def one_step(profile):
+        restore()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        f = H.hlq_factor_dist(grid, [A], N, nb, crit, args.alpha, forced=forced,
+                              tree_domains=D, profile=int(profile))
+        f.solve(b, x)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1), f
+
+    for _ in range(args.warmup):
+        _, f = one_step(False)
+        f.free()
+    sampler = ClockSampler(local)
+    sampler.start()
+    dist.barrier()
+    torch.cuda.synchronize()
+    l0 = H.hlq_launch_count()
+    times, profs = [], []
+    for _ in range(args.steps):
+        ms, f = one_step(True)
+        times.append(ms)
+        profs.append(f.profile())
+        info = f.info()
+        last = f
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches = H.hlq_launch_count() - l0
+    clocks = sampler.stop()
+    tt = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms_step = float(tt.item()) / args.steps
+    dec = last.decisions()
+    last.free()
+    restore()
+    res = H.hlq_residual_dist(grid, [A], N, nb, x, b)
+    fake, true = info["fake_flops"], info["true_flops"]
+    value = fake / (ms_step * 1e-3) / 1e12
+    agg = {}
+    for pr in profs:
+        for c, v in pr.items():
+            a = agg.setdefault(c, {"ms": 0.0, "flops": 0.0})
+            a["ms"] += v["ms"]
+            a["flops"] += v["flops"]
+    dom = max(("lu_update", "qr_unmqr"), key=lambda c: agg[c]["ms"])
+    # this rank's share of the class flops: the trailing update is spread evenly over the grid
+    achieved = agg[dom]["flops"] / world / (agg[dom]["ms"] * 1e-3) / 1e12 if agg[dom]["ms"] else 0.0
+    kname = {"lu_update": "k_dgemm (LU Schur update + SWPTRSM)",
+             "qr_unmqr": "k_unmqr_dmma + k_ttmqr_dmma (QR trailing update)"}[dom]
+    roofline = {"bound": "tensor", "kernel": kname, "achieved": achieved,
+                "peak": FP64_DMMA_PEAK_TF, "unit": "TFLOP/s", "frac": achieved / FP64_DMMA_PEAK_TF,
+                "traffic": None, "rank": rank,
+                "peak_source": "measured FP64 DMMA mma.sync m8n8k4 sustained (per GPU)",
+                "per_class_ms": {c: round(v["ms"] / args.steps, 3) for c, v in agg.items()}}
+    e2e = None
+    if not args.no_e2e:
+        Ah = A.cpu().pin_memory() if Ah_local is None else Ah_local
+        bh = b.cpu().pin_memory()
+        ets = []
+        for it in range(1 + min(args.steps, 2)):
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            A.copy_(Ah, non_blocking=True)
+            b.copy_(bh, non_blocking=True)
+            f = H.hlq_factor_dist(grid, [A], N, nb, crit, args.alpha, forced=forced,
+                                  tree_domains=D)
+            f.solve(b, x)
+            xh = x.cpu()
+            dt = time.perf_counter() - t0
+            f.free()
+            t = torch.tensor([dt], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            if it > 0:
+                ets.append(float(t.item()))
+        e2e = {"value": fake / statistics.mean(ets) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": 8 * N * N + 8 * N * world, "d2h_bytes_per_step": 8 * N * world,
+               "steps": len(ets), "timing": "host wall clock (max over ranks) around H2D of the "
+                                            "local tiles + hlq_factor_dist + hlq_solve + D2H of x"}
+        del xh
+    if rank == 0:
+        out = {"metric": "FP64 TFLOP/s (2N^3/3 basis) hybrid LU-QR", "value": value,
+               "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "config": workload_config(args, cfg),
+               "true_tflops": true / (ms_step * 1e-3) / 1e12,
+               "frac_fp64_peak": value / world / FP64_DMMA_PEAK_TF,
+               "qr_fraction": float(dec.mean()), "hpl3": res["hpl3"], "growth": info["growth"],
+               "status": info["status"], "step_ms": [round(t, 3) for t in times],
+               "roofline": roofline, "cpu_baseline": None, "e2e": e2e,
+               "gpu_launches": launches, "clocks": clocks}
+        print(json.dumps(out), flush=True)
+    grid.free()
 
 
 if __name__ == "__main__":

@@ -12,6 +12,8 @@
 // Fragments: mma.sync.m8n8k4.f64 (lane g=lane/4, t=lane%4: A(g,t), B(t,g), C(g,2t..2t+1)); every
 // operand array has a leading dimension == 4 (mod 16) doubles, which makes all fragment loads
 // bank-conflict free.
+#include <stdlib.h>
+
 #include "hlq_internal.cuh"
 
 namespace hlq {
@@ -583,11 +585,25 @@ static void launch_w(const double* A, Geo g, int k, int ib, const double* Tg, co
 
 // what = 0: UNMQR of all tile rows; what = 1 + l: TTMQR of level l.  Column slab width 64 when the
 // slab + reflector block fit in shared memory (nb <= 256), else 32.
+void launch_qr_update2(const double* A, Geo g, int k, const double* T, const int2* pairs,
+                       int npairs, bool tt, double* base, int64_t ldc, int64_t ncols,
+                       const uint8_t* dec, cudaStream_t st);
+
 void launch_qr_update_dmma(const double* A, Geo g, int k, int ib, const double* Tg,
                            const double* Ttt, const int2* const* level_pairs,
                            const int* level_count, int nlevels, double* base, int64_t ldc,
                            int64_t ncols, const uint8_t* dec, int what, cudaStream_t st) {
   if (ncols <= 0) return;
+  static int v1 = -1;
+  if (v1 < 0) v1 = getenv("HLQ_QR_UPDATE_V1") ? 1 : 0;
+  if (!v1 && ib == 32) {
+    if (what == 0)
+      launch_qr_update2(A, g, k, Tg, nullptr, 0, false, base, ldc, ncols, dec, st);
+    else
+      launch_qr_update2(A, g, k, Ttt, level_pairs[what - 1], level_count[what - 1], true, base,
+                        ldc, ncols, dec, st);
+    return;
+  }
   if (qd_smem<64>(g.nb) <= 227 * 1024)
     launch_w<64>(A, g, k, ib, Tg, Ttt, level_pairs, level_count, nlevels, base, ldc, ncols, dec,
                  what, st);
