@@ -1,27 +1,30 @@
 // QR trailing update, v2 (a8 UNMQR, a10/a11 TTMQR): the bulk of a QR step's flops (Table I
 // "update D" PAPER.md:166; Alg. 4b), on the FP64 tensor cores (DMMA).
 //
-// One CTA owns a slab of W = 8*NW columns of one tile row (UNMQR) or of one TT pair (TTMQR, the
+// One CTA owns a slab of W = 8*NCG columns of one tile row (UNMQR) or of one TT pair (TTMQR, the
 // slab of the eliminated tile i; rows of the surviving tile e are read-modify-written per block).
 // The slab stays in shared memory for the whole step: every C element is read and written once.
-// Warp w owns slab columns [8w, 8w+8) for ALL three products of a reflector block b (32 columns):
-//     GEMM1  W  = [C_e(b) +] V_b^T C        32 x 8 per warp, K = rows of V_b   (DMMA)
-//     TRMM   U  = T_b^T W                   32 x 8 per warp, K = 32            (DMMA)
-//     GEMM2  C -= V_b U   [C_e(b) -= U]     rows x 8 per warp, K = 32          (DMMA)
-// so a warp only ever touches its own columns of C: the only data shared by the CTA is the stream
-// of V_b row chunks (32 x 32, cp.async, DEPTH-deep ring) and T_b.  V_b is streamed twice per block
+// A PAIR of warps (kh = 0, 1) owns slab columns [8cg, 8cg+8) for ALL three products of a reflector
+// block b (32 columns), the two warps taking alternate 32-row chunks of V_b:
+//     GEMM1  W  = [C_e(b) +] V_b^T C        32 x 8, K = rows of V_b; pair-reduced   (DMMA)
+//     TRMM   U  = T_b^T W                   rows 16kh..16kh+15 of 32 x 8, K = 32    (DMMA)
+//     GEMM2  C -= V_b U   [C_e(b) -= U]     chunk rows x 8, K = 32                  (DMMA)
+// so a warp pair only ever touches its own columns of C (named barriers per pair); the data shared
+// by the CTA is the stream of V_b row-chunk pairs (32 x 32 each, cp.async, double-buffered) and
+// T_b.  16 warps per SM (one CTA) hide the shared-memory and DMMA latencies.  V_b is streamed twice per block
 // (GEMM1, GEMM2) from L2; its explicit structure (unit diagonal / zeros above for GEQRT reflectors,
 // zeros below the diagonal for the TT reflectors) is applied when the diagonal chunk's fragments are
 // loaded.  Fragments: mma.sync.m8n8k4.f64 (lane g = lane/4, t = lane%4: A(g,t), B(t,g),
 // C(g, 2t..2t+1)); every shared array has a leading dimension == 4 (mod 16) doubles, which makes the
 // fragment loads bank-conflict free.  Householder convention and T layout: DESIGN.md 14-15.
+#include <stdlib.h>
+
 #include "hlq_internal.cuh"
 
 namespace hlq {
 
 namespace {
 constexpr int LDV = 36;  // V chunk [l][r], T [col][row], W/U [col][l]
-constexpr int DEPTH = 3;
 constexpr int CH = 32 * LDV;  // doubles per ring slot
 
 __device__ __forceinline__ void dmma_(double& c0, double& c1, double a, double b) {
@@ -68,23 +71,26 @@ __device__ __forceinline__ void load_chunk(double* dst, const double* src, int64
   }
 }
 
-template <int NW, bool TT, bool V16>
-__global__ void __launch_bounds__(NW * 32) k_qr_update2(const double* __restrict__ A, Geo g,
-                                                       int k, const double* __restrict__ Tbase,
-                                                       const int2* __restrict__ pairs,
-                                                       double* __restrict__ base, int64_t ldcg,
-                                                       int64_t ncols,
-                                                       const uint8_t* __restrict__ dec) {
+template <int NCG, bool TT>
+__global__ void __launch_bounds__(NCG * 64) k_qr_update2(const double* __restrict__ A, Geo g,
+                                                        int k, const double* __restrict__ Tbase,
+                                                        const int2* __restrict__ pairs,
+                                                        double* __restrict__ base, int64_t ldcg,
+                                                        int64_t ncols,
+                                                        const uint8_t* __restrict__ dec) {
   if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
-  constexpr int W = 8 * NW, NT = 32 * NW;
+  constexpr int W = 8 * NCG, NT = 64 * NCG;
   extern __shared__ __align__(16) double sm[];
   const int ldc = rup32(g.nb) + 4;
   double* Cs = sm;                        // W x ldc   slab of tile i (col-major)
-  double* ring = Cs + W * ldc;            // DEPTH x 32 x LDV
-  double* Ts = ring + DEPTH * CH;         // 2 x 32 x LDV (double-buffered per block)
+  double* ring = Cs + W * ldc;            // 4 x CH: chunk pairs (2 slots each, double-buffered)
+  double* Ts = ring + 4 * CH;             // 2 x CH  (T_b, double-buffered per block)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, tq = lane & 3;
-  double* Ws = Ts + 2 * CH + warp * 8 * LDV;  // per warp 8 x LDV
+  const int cg = warp % NCG, kh = warp / NCG;  // column group, half (chunk parity / TRMM rows)
+  double* Wb = Ts + 2 * CH + cg * 8 * LDV;     // W, then -U, of column group cg ([col][l])
+  double* Rb = Ts + 2 * CH + (NCG + cg) * 8 * LDV;  // partial W of the kh = 1 warp
+  const unsigned pair_bar = 1 + cg;
 
   int e = 0, i;
   if (TT) {
@@ -99,37 +105,34 @@ __global__ void __launch_bounds__(NW * 32) k_qr_update2(const double* __restrict
   const double* T = Tbase + tri_index(i, k, g.n) * (int64_t)32 * g.nb;
   const int64_t c0 = (int64_t)blockIdx.x * W;
   const int cvalid = (int)((ncols - c0) < W ? (ncols - c0) : W);
-  // rows of the slab that any block touches
   const int crows = TT ? (bi < bk ? bi : bk) : bi;
   const int crows_pad = rup32(crows);
   double* Cg = base + c0 * ldcg + g.r0(i);
+  const bool vv16 = ((g.lda & 1) == 0) && ((((uintptr_t)Vt) & 15) == 0);
 
-  // ---- C slab (its own commit group, ahead of the ring prologue)
+  // ---- C slab: 8 threads per column, two rows per thread and step (no divisions)
+  const int sj = tid >> 3, sr = 2 * (tid & 7);
   {
-    const bool v16 = V16 && ((ldcg & 1) == 0) && ((((uintptr_t)Cg) & 15) == 0);
-    if (v16) {
-      const int rp2 = crows_pad >> 1;
-      for (int o = tid; o < W * rp2; o += NT) {
-        const int j = o / rp2, r = 2 * (o - j * rp2);
-        const bool ok = (j < cvalid) && (r + 1 < crows);
-        if (ok) {
-          cp16(Cs + j * ldc + r, Cg + (int64_t)j * ldcg + r, true);
+    const bool c16 = ((ldcg & 1) == 0) && ((((uintptr_t)Cg) & 15) == 0);
+    double* cs = Cs + sj * ldc;
+    const double* cgp = Cg + (int64_t)sj * ldcg;
+    const bool jok = sj < cvalid;
+    for (int r = sr; r < crows_pad; r += 16) {
+      if (jok && r + 1 < crows) {
+        if (c16) {
+          cp16(cs + r, cgp + r, true);
         } else {
-          Cs[j * ldc + r] = (j < cvalid && r < crows) ? Cg[(int64_t)j * ldcg + r] : 0.0;
-          Cs[j * ldc + r + 1] = 0.0;
+          cp8(cs + r, cgp + r, true);
+          cp8(cs + r + 1, cgp + r + 1, true);
         }
-      }
-    } else {
-      for (int o = tid; o < W * crows_pad; o += NT) {
-        const int j = o / crows_pad, r = o - j * crows_pad;
-        const bool ok = (j < cvalid) && (r < crows);
-        cp8(Cs + j * ldc + r, ok ? Cg + (int64_t)j * ldcg + r : Cg, ok);
+      } else {
+        cs[r] = (jok && r < crows) ? cgp[r] : 0.0;
+        cs[r + 1] = 0.0;
       }
     }
     commit_();
   }
 
-  // ---- chunk stream: for every block b: GEMM1 chunks, then GEMM2 chunks (same V_b rows)
   const int nblk = (bk + 31) / 32;
   auto blk_rows = [&](int b, int& rlo, int& rhi) {
     const int i0 = 32 * b;
@@ -141,10 +144,10 @@ __global__ void __launch_bounds__(NW * 32) k_qr_update2(const double* __restrict
       rhi = bi;
     }
   };
-  // producer state
-  int pb = 0, ppass = 0, pc = 0, ps = 0;
+  // producer: chunk pairs within a pass (GEMM1 / GEMM2 of block pb)
+  int pb = 0, ppass = 0, pc = 0, pj = 0;
   bool pdone = false;
-  auto issue = [&]() {
+  auto issue_pair = [&]() {
     if (!pdone) {
       int rlo, rhi;
       blk_rows(pb, rlo, rhi);
@@ -153,16 +156,19 @@ __global__ void __launch_bounds__(NW * 32) k_qr_update2(const double* __restrict
       } else {
         const int i0 = 32 * pb;
         const int cmax = (bk - i0) < 32 ? (bk - i0) : 32;
-        double* slot = ring + (ps % DEPTH) * CH;
-        const bool v16 = V16 && ((g.lda & 1) == 0) && ((((uintptr_t)Vt) & 15) == 0) &&
-                         ((rhi & 1) == 0);
-        if (v16)
-          load_chunk<true>(slot, Vt + (int64_t)i0 * g.lda, g.lda, rlo + 32 * pc, rhi, cmax, tid, NT);
-        else
-          load_chunk<false>(slot, Vt + (int64_t)i0 * g.lda, g.lda, rlo + 32 * pc, rhi, cmax, tid,
-                            NT);
+        const int nch = (rhi - rlo + 31) / 32;
+        const bool v16 = vv16 && ((rhi & 1) == 0);
+        for (int h = 0; h < 2 && pc + h < nch; ++h) {
+          double* slot = ring + (2 * (pj & 1) + h) * CH;
+          if (v16)
+            load_chunk<true>(slot, Vt + (int64_t)i0 * g.lda, g.lda, rlo + 32 * (pc + h), rhi, cmax,
+                             tid, NT);
+          else
+            load_chunk<false>(slot, Vt + (int64_t)i0 * g.lda, g.lda, rlo + 32 * (pc + h), rhi,
+                              cmax, tid, NT);
+        }
         if (ppass == 0 && pc == 0) {
-          // T_b (32 x 32, stored T(q, l) at T[(i0 + l) * 32 + q], zeros below the diagonal)
+          // T_b (32 x 32; T(q, l) at T[(i0 + l) * 32 + q]; zeros below the diagonal)
           double* ts = Ts + (pb & 1) * CH;
           for (int o = tid; o < 32 * 16; o += NT) {
             const int l = o >> 4, q = (o & 15) * 2;
@@ -170,9 +176,9 @@ __global__ void __launch_bounds__(NW * 32) k_qr_update2(const double* __restrict
             cp16(ts + l * LDV + q, ok ? T + (int64_t)(i0 + l) * 32 + q : T, ok);
           }
         }
-        ++ps;
-        const int nch = (rhi - rlo + 31) / 32;
-        if (++pc == nch) {
+        ++pj;
+        pc += 2;
+        if (pc >= nch) {
           pc = 0;
           if (++ppass == 2) {
             ppass = 0;
@@ -183,11 +189,10 @@ __global__ void __launch_bounds__(NW * 32) k_qr_update2(const double* __restrict
     }
     commit_();
   };
-#pragma unroll 1
-  for (int d = 0; d < DEPTH - 1; ++d) issue();
+  issue_pair();
 
-  int s = 0;  // consumer chunk index
-  const int wc = warp * 8;  // first slab column of this warp
+  int j = 0;  // consumer pair index
+  const int wc = cg * 8;
 #pragma unroll 1
   for (int b = 0; b < nblk; ++b) {
     int rlo, rhi;
@@ -196,17 +201,16 @@ __global__ void __launch_bounds__(NW * 32) k_qr_update2(const double* __restrict
     const int i0 = 32 * b;
     const int sb = (bk - i0) < 32 ? (bk - i0) : 32;
     const int nch = (rhi - rlo + 31) / 32;
-    // chunk index (within the block) that holds the diagonal 32 x 32 block of V_b
-    const int cdiag = TT ? (i0 / 32) : 0;
-    double* Ceb = TT ? base + c0 * ldcg + g.r0(e) + i0 : nullptr;  // C_e rows of block b
+    const int cdiag = TT ? (i0 / 32) : 0;  // chunk holding the diagonal 32 x 32 block of V_b
+    double* Ceb = TT ? base + c0 * ldcg + g.r0(e) + i0 : nullptr;
 
-    // ---------------- GEMM1: W = [C_e(b) +] V_b^T C
+    // ---------------- GEMM1 (chunks c = 2j' + kh): W = [C_e(b) +] V_b^T C
     double acc[2][4][2];
 #pragma unroll
     for (int u = 0; u < 2; ++u)
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi) acc[u][mi][0] = acc[u][mi][1] = 0.0;
-    if (TT) {
+    if (TT && kh == 0) {
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -216,17 +220,19 @@ __global__ void __launch_bounds__(NW * 32) k_qr_update2(const double* __restrict
         }
     }
 #pragma unroll 1
-    for (int c = 0; c < nch; ++c, ++s) {
-      wait_<DEPTH - 2>();
+    for (int c = 0; c < nch; c += 2, ++j) {
+      wait_<0>();
       __syncthreads();
-      issue();
-      const double* V = ring + (s % DEPTH) * CH;
-      const double* Cb = Cs + (wc + gq) * ldc + rlo + 32 * c + tq;
-      if (c == cdiag) {
+      issue_pair();
+      const int cc_ = c + kh;
+      if (cc_ >= nch) continue;
+      const double* V = ring + (2 * (j & 1) + kh) * CH;
+      const double* Cb = Cs + (wc + gq) * ldc + rlo + 32 * cc_ + tq;
+      if (cc_ == cdiag) {
 #pragma unroll
         for (int kk = 0; kk < 32; kk += 4) {
           const double bv = Cb[kk];
-          const int r = kk + tq;  // row within the diagonal chunk
+          const int r = kk + tq;
 #pragma unroll
           for (int mi = 0; mi < 4; ++mi) {
             const int l = mi * 8 + gq;
@@ -250,50 +256,65 @@ __global__ void __launch_bounds__(NW * 32) k_qr_update2(const double* __restrict
         }
       }
     }
-    // ---------------- TRMM: U = T_b^T W (this warp's 8 columns), then -U for GEMM2's B operand
+    // ---------------- pair reduction, then TRMM U = T_b^T W split by rows (kh -> mi 2kh, 2kh+1)
+    if (kh == 1) {
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+      for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) Ws[(2 * tq + h) * LDV + mi * 8 + gq] = acc[0][mi][h] + acc[1][mi][h];
-    __syncwarp();
-    {
-      const double* ts = Ts + (b & 1) * CH;
-      double u[4][2];
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi) u[mi][0] = u[mi][1] = 0.0;
-#pragma unroll
-      for (int kk = 0; kk < 32; kk += 4) {
-        const double bv = Ws[gq * LDV + kk + tq];
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
-          dmma_(u[mi][0], u[mi][1], ts[(mi * 8 + gq) * LDV + kk + tq], bv);
-      }
-      __syncwarp();
+        for (int h = 0; h < 2; ++h)
+          Rb[(2 * tq + h) * LDV + mi * 8 + gq] = acc[0][mi][h] + acc[1][mi][h];
+    }
+    asm volatile("bar.sync %0, %1;\n" ::"r"(pair_bar), "n"(64));
+    if (kh == 0) {
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int l = mi * 8 + gq, col = wc + 2 * tq + h;
-          Ws[(2 * tq + h) * LDV + l] = neg_bits(u[mi][h]);
-          if (TT && l < sb && col < cvalid) Ceb[(int64_t)col * ldcg + l] -= u[mi][h];
+          const int o = (2 * tq + h) * LDV + mi * 8 + gq;
+          Wb[o] = (acc[0][mi][h] + acc[1][mi][h]) + Rb[o];
         }
-      __syncwarp();
     }
-    // ---------------- GEMM2: C[rows] -= V_b U
+    asm volatile("bar.sync %0, %1;\n" ::"r"(pair_bar), "n"(64));
+    {
+      const double* ts = Ts + (b & 1) * CH;
+      double u[2][2];
+#pragma unroll
+      for (int m2 = 0; m2 < 2; ++m2) u[m2][0] = u[m2][1] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < 32; kk += 4) {
+        const double bv = Wb[gq * LDV + kk + tq];
+#pragma unroll
+        for (int m2 = 0; m2 < 2; ++m2)
+          dmma_(u[m2][0], u[m2][1], ts[((2 * kh + m2) * 8 + gq) * LDV + kk + tq], bv);
+      }
+      asm volatile("bar.sync %0, %1;\n" ::"r"(pair_bar), "n"(64));
+#pragma unroll
+      for (int m2 = 0; m2 < 2; ++m2)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int l = (2 * kh + m2) * 8 + gq, col = wc + 2 * tq + h;
+          Wb[(2 * tq + h) * LDV + l] = neg_bits(u[m2][h]);
+          if (TT && l < sb && col < cvalid) Ceb[(int64_t)col * ldcg + l] -= u[m2][h];
+        }
+      asm volatile("bar.sync %0, %1;\n" ::"r"(pair_bar), "n"(64));
+    }
+    // ---------------- GEMM2 (chunks c = 2j' + kh): C[rows] -= V_b U
 #pragma unroll 1
-    for (int c = 0; c < nch; ++c, ++s) {
-      wait_<DEPTH - 2>();
+    for (int c = 0; c < nch; c += 2, ++j) {
+      wait_<0>();
       __syncthreads();
-      issue();
-      const double* V = ring + (s % DEPTH) * CH;
-      const int r0 = rlo + 32 * c;
+      issue_pair();
+      const int cc_ = c + kh;
+      if (cc_ >= nch) continue;
+      const double* V = ring + (2 * (j & 1) + kh) * CH;
+      const int r0 = rlo + 32 * cc_;
       double cc[4][2];
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
         for (int h = 0; h < 2; ++h) cc[mi][h] = Cs[(wc + 2 * tq + h) * ldc + r0 + mi * 8 + gq];
-      const double* Ub = Ws + gq * LDV + tq;
-      if (c == cdiag) {
+      const double* Ub = Wb + gq * LDV + tq;
+      if (cc_ == cdiag) {
 #pragma unroll
         for (int kk = 0; kk < 32; kk += 4) {
           const double bv = Ub[kk];
@@ -327,40 +348,44 @@ __global__ void __launch_bounds__(NW * 32) k_qr_update2(const double* __restrict
   }
   wait_<0>();
   __syncthreads();
-  // ---- store the slab
-  for (int o = tid; o < W * crows; o += NT) {
-    const int j = o / crows, r = o - j * crows;
-    if (j < cvalid) Cg[(int64_t)j * ldcg + r] = Cs[j * ldc + r];
+  // ---- store the slab (8 threads per column)
+  if (sj < cvalid) {
+    const double* cs = Cs + sj * ldc;
+    double* cgp = Cg + (int64_t)sj * ldcg;
+    for (int r = sr; r < crows; r += 16) {
+      cgp[r] = cs[r];
+      if (r + 1 < crows) cgp[r + 1] = cs[r + 1];
+    }
   }
 }
 
-template <int NW>
+template <int NCG>
 static size_t upd_smem(int nb) {
-  return sizeof(double) * ((size_t)8 * NW * (rup32(nb) + 4) + (size_t)(DEPTH + 2) * CH +
-                           (size_t)NW * 8 * LDV);
+  return sizeof(double) * ((size_t)8 * NCG * (rup32(nb) + 4) + (size_t)6 * CH +
+                           (size_t)2 * NCG * 8 * LDV);
 }
 
-template <int NW>
+template <int NCG>
 static bool launch_nw(const double* A, Geo g, int k, const double* T, const int2* pairs,
                       int npairs, bool tt, double* base, int64_t ldc, int64_t ncols,
                       const uint8_t* dec, cudaStream_t st) {
-  const size_t smem = upd_smem<NW>(g.nb);
+  const size_t smem = upd_smem<NCG>(g.nb);
   if (smem > 227 * 1024) return false;
   static bool attr = false;
   if (!attr) {
-    smem_optin(k_qr_update2<NW, false, true>);
-    smem_optin(k_qr_update2<NW, true, true>);
+    smem_optin(k_qr_update2<NCG, false>);
+    smem_optin(k_qr_update2<NCG, true>);
     attr = true;
   }
-  const unsigned slabs = (unsigned)((ncols + 8 * NW - 1) / (8 * NW));
+  const unsigned slabs = (unsigned)((ncols + 8 * NCG - 1) / (8 * NCG));
   if (!tt) {
     ::hlq::g_launches++;
-    k_qr_update2<NW, false, true><<<dim3(slabs, g.n - k), NW * 32, smem, st>>>(
+    k_qr_update2<NCG, false><<<dim3(slabs, g.n - k), NCG * 64, smem, st>>>(
         A, g, k, T, nullptr, base, ldc, ncols, dec);
   } else {
     if (npairs <= 0) return true;
     ::hlq::g_launches++;
-    k_qr_update2<NW, true, true><<<dim3(slabs, npairs), NW * 32, smem, st>>>(
+    k_qr_update2<NCG, true><<<dim3(slabs, npairs), NCG * 64, smem, st>>>(
         A, g, k, T, pairs, base, ldc, ncols, dec);
   }
   return true;
@@ -368,14 +393,385 @@ static bool launch_nw(const double* A, Geo g, int k, const double* T, const int2
 
 // UNMQR of every tile row k..n-1 (tt = false, T = GEQRT factors) or TTMQR of one level (tt = true,
 // T = TTQRT factors) on the column block (base, ldc, ncols).  Requires ib = 32 and nb <= 512.
+bool launch_qr_update3(const double* A, Geo g, int k, const double* T, const int2* pairs,
+                       int npairs, bool tt, double* base, int64_t ldc, int64_t ncols,
+                       const uint8_t* dec, cudaStream_t st);
+
 void launch_qr_update2(const double* A, Geo g, int k, const double* T, const int2* pairs,
                        int npairs, bool tt, double* base, int64_t ldc, int64_t ncols,
                        const uint8_t* dec, cudaStream_t st) {
   if (ncols <= 0) return;
+  if (launch_qr_update3(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st)) return;
   if (launch_nw<8>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st)) return;
   if (launch_nw<7>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st)) return;
   if (launch_nw<6>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st)) return;
   launch_nw<4>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st);
+}
+
+// =============================================================================================
+// v3: the slab lives in REGISTERS as C^T accumulator fragments.
+//
+// A DMMA accumulator fragment of an 8x8 block X holds X(g, 2t) and X(g, 2t+1) in lane (g, t); the
+// two registers are exactly the A-operand fragments (lane (g,t) -> A(g,t)) of the 8x4 matrices
+// X[:, even columns] and X[:, odd columns].  Holding C^T (slab columns x tile rows) as accumulators:
+//     GEMM1  W^T  = C^T V_b        A = C^T from registers (even / odd rows), B = V_b from smem
+//     TRMM   U^T  = W^T T_b        A = W^T from registers,                    B = T_b from smem
+//     GEMM2  C^T -= U^T V_b^T      A = U^T from registers,                    B = V_b from smem
+// so the only shared-memory traffic is the B operand (0.5 LDS per DMMA: every B fragment feeds the
+// two 8-column halves of a warp's 16 slab columns) and C never round-trips through shared memory.
+// 8 warps: column group cg = warp & 3 (16 columns), row parity rh = warp >> 2 (the 8-row blocks
+// RB == rh mod 2 of the tile).  GEMM1 partials of the two row parities are pair-reduced (W = P0+P1,
+// commutative, so both warps hold identical W) and both compute the (tiny) TRMM.  V_b row chunks
+// (32 x 32) stream through a cp.async ring in a pass-specific permuted layout that makes every B
+// fragment load bank-conflict free.
+namespace {
+constexpr int LD3 = 40;    // GEMM1 / T chunks: == 8 (mod 16): conflict-free 16-byte fragment pairs
+constexpr int LD3B = 34;   // GEMM2 chunks: == 2 (mod 16): conflict-free 8-byte B fragments
+constexpr int CH3 = 32 * LD3;
+__device__ __forceinline__ double2 lds2(const double* p) {
+  return *reinterpret_cast<const double2*>(p);
+}
+}  // namespace
+
+template <int NB, bool TT, int RQ, int NCG>
+__global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ * NCG) : 1) k_qr_update3(const double* __restrict__ A, Geo g, int k,
+                                                   const double* __restrict__ Tbase,
+                                                   const int2* __restrict__ pairs,
+                                                   double* __restrict__ base, int64_t ldcg,
+                                                   int64_t ncols, const uint8_t* __restrict__ dec) {
+  if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
+  constexpr int NCH = NB / 32;       // 32-row chunks of a tile
+  constexpr int NJ = NB / (8 * RQ);  // 8-row blocks owned by one row group
+  constexpr int QPC = 4 / RQ;        // of those, per 32-row chunk
+  constexpr int NT = 32 * RQ * NCG;
+  constexpr int W = 16 * NCG;        // slab columns
+  constexpr int RING = 6;
+  extern __shared__ __align__(16) double sm[];
+  double* ring = sm;                     // RING x CH3: V chunks [l][r] (ld LD3 / LD3B by pass)
+  double* Ts = ring + RING * CH3;        // 2 x CH3: T_b [l][q]
+  double* Rb = Ts + 2 * CH3;             // RQ*NCG warps x 512: partial W^T
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int cg = warp % NCG, rh = warp / NCG;  // column group, row group (RB == rh mod RQ)
+
+  int e = 0, i;
+  if (TT) {
+    const int2 pr = pairs[blockIdx.y];
+    e = pr.x;
+    i = pr.y;
+  } else {
+    i = k + blockIdx.y;
+  }
+  const int bi = g.bs(i), bk = g.cbs(k);
+  const double* Vt = g.tile(const_cast<double*>(A), i, k);
+  const double* T = Tbase + tri_index(i, k, g.n) * (int64_t)32 * g.nb;
+  const int64_t c0 = (int64_t)blockIdx.x * W;
+  const int cvalid = (int)((ncols - c0) < W ? (ncols - c0) : W);
+  const int crows = TT ? (bi < bk ? bi : bk) : bi;
+  double* Cg = base + c0 * ldcg + g.r0(i);
+  const int wc = cg * 16;  // first slab column of this warp
+  const bool v16 = ((g.lda & 1) == 0) && ((((uintptr_t)Vt) & 15) == 0) && ((crows & 1) == 0);
+
+  // ---- C^T fragments: cT[m][j][h] = C(row 8 RB + 2t + h, col wc + 8m + g), RB = RQ j + rh
+  double cT[2][NJ][2];
+#pragma unroll
+  for (int m = 0; m < 2; ++m) {
+    const int col = wc + 8 * m + gq;
+    const bool cok = col < cvalid;
+    const double* cp = Cg + (int64_t)col * ldcg;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int r = 8 * (RQ * j + rh) + 2 * tq;
+      cT[m][j][0] = (cok && r < crows) ? cp[r] : 0.0;
+      cT[m][j][1] = (cok && r + 1 < crows) ? cp[r + 1] : 0.0;
+    }
+  }
+
+  const int nblk = (bk + 31) / 32;
+  const int nch_i = (crows + 31) / 32;
+  auto chunk_lo = [&](int b) { return TT ? 0 : b; };
+  auto chunk_hi = [&](int b) { return TT ? (b < nch_i - 1 ? b : nch_i - 1) : nch_i - 1; };
+  // producer
+  int pb = 0, ppass = 0, pch = 0;
+  double* pslot = ring;
+  bool pdone = false;
+  auto start_block = [&]() {
+    while (pb < nblk && chunk_hi(pb) < chunk_lo(pb)) ++pb;
+    if (pb >= nblk) pdone = true;
+    pch = chunk_lo(pb);
+  };
+  start_block();
+  // per-thread copy coordinates (16-byte copies: column l, rows r, r+1 of a 32 x 32 chunk)
+  constexpr int CPT = 512 / NT;   // copies per thread per chunk
+  const int cl0 = tid >> 4, cr = (tid & 15) * 2;
+  auto issue = [&]() {
+    if (!pdone) {
+      const int i0 = 32 * pb;
+      const int cmax = (bk - i0) < 32 ? (bk - i0) : 32;
+      const double* src = Vt + (int64_t)i0 * g.lda + 32 * pch;
+      const int rmax = crows - 32 * pch;  // valid rows in this chunk
+      const int ld = ppass == 0 ? LD3 : LD3B;
+      if (v16) {
+        const bool rok = cr < rmax;
+#pragma unroll
+        for (int u = 0; u < CPT; ++u) {
+          const int l = cl0 + (NT / 16) * u;
+          const bool ok = rok && (l < cmax);
+          cp16(pslot + l * ld + cr, ok ? src + (int64_t)l * g.lda + cr : src, ok);
+        }
+      } else {
+        for (int o = tid; o < 1024; o += NT) {
+          const int l = o >> 5, r = o & 31;
+          const bool ok = (r < rmax) && (l < cmax);
+          cp8(pslot + l * ld + r, ok ? src + (int64_t)l * g.lda + r : src, ok);
+        }
+      }
+      if (ppass == 0 && pch == chunk_lo(pb)) {
+        double* ts = Ts + (pb & 1) * CH3;
+#pragma unroll
+        for (int u = 0; u < CPT; ++u) {
+          const int l = cl0 + (NT / 16) * u;
+          const bool ok = l < cmax;
+          cp16(ts + l * LD3 + cr, ok ? T + (int64_t)(i0 + l) * 32 + cr : T, ok);
+        }
+      }
+      pslot = (pslot == ring + (RING - 1) * CH3) ? ring : pslot + CH3;
+      if (++pch > chunk_hi(pb)) {
+        if (++ppass == 2) {
+          ppass = 0;
+          ++pb;
+          start_block();
+        } else {
+          pch = chunk_lo(pb);
+        }
+      }
+    }
+    commit_();
+  };
+#pragma unroll 1
+  for (int d = 0; d < RING - 1; ++d) issue();
+  // explicit structure of the diagonal 32 x 32 block of V_b (GEQRT: unit diagonal, zeros above;
+  // TT: zeros below the diagonal); element (r, l) at V[r * sr + l * sl]
+  auto fix_diag = [&](double* V, int sr, int sl) {
+    for (int o = tid; o < 1024; o += NT) {
+      const int l = o >> 5, r = o & 31;
+      if (TT) {
+        if (r > l) V[r * sr + l * sl] = 0.0;
+      } else {
+        if (r <= l) V[r * sr + l * sl] = (r == l) ? 1.0 : 0.0;
+      }
+    }
+  };
+
+  const double* cslot = ring;
+#pragma unroll 1
+  for (int b = 0; b < nblk; ++b) {
+    const int clo = chunk_lo(b), chi = chunk_hi(b);
+    if (chi < clo) continue;
+    const int i0 = 32 * b;
+    const int sb = (bk - i0) < 32 ? (bk - i0) : 32;
+    double* Ceb = TT ? base + c0 * ldcg + g.r0(e) + i0 : nullptr;
+    // ---------------- GEMM1: W^T[m][nl] (16 cols x 32 refl), K = the warp's rows
+    double wT[2][4][2];
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int nl = 0; nl < 4; ++nl) wT[m][nl][0] = wT[m][nl][1] = 0.0;
+    if (TT && rh == 0) {
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int nl = 0; nl < 4; ++nl)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int col = wc + 8 * m + gq, l = 8 * nl + 2 * tq + h;
+            if (col < cvalid && l < sb) wT[m][nl][h] = Ceb[(int64_t)col * ldcg + l];
+          }
+    }
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+      if (ch < clo || ch > chi) continue;
+      wait_<RING - 2>();
+      __syncthreads();
+      issue();
+      const double* V = cslot;
+      cslot = (cslot == ring + (RING - 1) * CH3) ? ring : cslot + CH3;
+      if (ch == b) {
+        fix_diag(const_cast<double*>(V), 1, LD3);
+        __syncthreads();
+      }
+#pragma unroll
+      for (int q = 0; q < QPC; ++q) {
+        const int rb = rh + RQ * q;  // 8-row block within the chunk
+#pragma unroll
+        for (int nl = 0; nl < 4; ++nl) {
+          const double2 bv = lds2(V + (8 * nl + gq) * LD3 + 8 * rb + 2 * tq);
+#pragma unroll
+          for (int m = 0; m < 2; ++m) {
+            dmma_(wT[m][nl][0], wT[m][nl][1], cT[m][QPC * ch + q][0], bv.x);
+            dmma_(wT[m][nl][0], wT[m][nl][1], cT[m][QPC * ch + q][1], bv.y);
+          }
+        }
+      }
+    }
+    // ---------------- group reduction: W = P_0 + ... + P_{RQ-1} in the same order on every warp
+    {
+      double* mine = Rb + warp * 512;
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int nl = 0; nl < 4; ++nl)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) mine[((m * 4 + nl) * 2 + h) * 32 + lane] = wT[m][nl][h];
+      asm volatile("bar.sync %0, %1;\n" ::"r"(1 + cg), "n"(32 * RQ));
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int nl = 0; nl < 4; ++nl)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int o = ((m * 4 + nl) * 2 + h) * 32 + lane;
+            double v = Rb[cg * 512 + o];
+#pragma unroll
+            for (int r2 = 1; r2 < RQ; ++r2) v += Rb[(cg + NCG * r2) * 512 + o];
+            wT[m][nl][h] = v;
+          }
+      asm volatile("bar.sync %0, %1;\n" ::"r"(1 + cg), "n"(32 * RQ));
+    }
+    // ---------------- TRMM: U^T = W^T T_b (both warps of the pair), then -U^T
+    double uT[2][4][2];
+    {
+      const double* ts = Ts + (b & 1) * CH3;
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int no = 0; no < 4; ++no) uT[m][no][0] = uT[m][no][1] = 0.0;
+#pragma unroll
+      for (int nl = 0; nl < 4; ++nl)
+#pragma unroll
+        for (int no = 0; no < 4; ++no) {
+          const double2 tv = lds2(ts + (8 * no + gq) * LD3 + 8 * nl + 2 * tq);
+#pragma unroll
+          for (int m = 0; m < 2; ++m) {
+            dmma_(uT[m][no][0], uT[m][no][1], wT[m][nl][0], tv.x);
+            dmma_(uT[m][no][0], uT[m][no][1], wT[m][nl][1], tv.y);
+          }
+        }
+    }
+    if (TT && rh == 0) {
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int no = 0; no < 4; ++no)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int col = wc + 8 * m + gq, l = 8 * no + 2 * tq + h;
+            if (col < cvalid && l < sb) Ceb[(int64_t)col * ldcg + l] -= uT[m][no][h];
+          }
+    }
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int no = 0; no < 4; ++no)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) uT[m][no][h] = neg_bits(uT[m][no][h]);
+    // ---------------- GEMM2: C^T[rows of the chunk] -= U^T V_b^T
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+      if (ch < clo || ch > chi) continue;
+      wait_<RING - 2>();
+      __syncthreads();
+      issue();
+      const double* V = cslot;
+      cslot = (cslot == ring + (RING - 1) * CH3) ? ring : cslot + CH3;
+      if (ch == b) {
+        fix_diag(const_cast<double*>(V), 1, LD3B);
+        __syncthreads();
+      }
+#pragma unroll
+      for (int q = 0; q < QPC; ++q) {
+        const int rb = rh + RQ * q;
+#pragma unroll
+        for (int nl = 0; nl < 4; ++nl) {
+          const double bx = V[(8 * nl + 2 * tq) * LD3B + 8 * rb + gq];
+          const double by = V[(8 * nl + 2 * tq + 1) * LD3B + 8 * rb + gq];
+#pragma unroll
+          for (int m = 0; m < 2; ++m) {
+            dmma_(cT[m][QPC * ch + q][0], cT[m][QPC * ch + q][1], uT[m][nl][0], bx);
+            dmma_(cT[m][QPC * ch + q][0], cT[m][QPC * ch + q][1], uT[m][nl][1], by);
+          }
+        }
+      }
+    }
+  }
+  wait_<0>();
+  // ---- store C^T back
+#pragma unroll
+  for (int m = 0; m < 2; ++m) {
+    const int col = wc + 8 * m + gq;
+    if (col >= cvalid) continue;
+    double* cp = Cg + (int64_t)col * ldcg;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int r = 8 * (RQ * j + rh) + 2 * tq;
+      if (r < crows) cp[r] = cT[m][j][0];
+      if (r + 1 < crows) cp[r + 1] = cT[m][j][1];
+    }
+  }
+}
+
+static size_t upd3_smem(int warps) { return sizeof(double) * ((size_t)8 * CH3 + (size_t)warps * 512); }
+
+template <int NB, int RQ = 2, int NCG = 2>
+static void launch3(const double* A, Geo g, int k, const double* T, const int2* pairs, int npairs,
+                    bool tt, double* base, int64_t ldc, int64_t ncols, const uint8_t* dec,
+                    cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    smem_optin(k_qr_update3<NB, false, RQ, NCG>);
+    smem_optin(k_qr_update3<NB, true, RQ, NCG>);
+    attr = true;
+  }
+  const unsigned slabs = (unsigned)((ncols + 16 * NCG - 1) / (16 * NCG));
+  const size_t smem = upd3_smem(RQ * NCG);
+  if (!tt) {
+    ::hlq::g_launches++;
+    k_qr_update3<NB, false, RQ, NCG><<<dim3(slabs, g.n - k), 32 * RQ * NCG, smem, st>>>(
+        A, g, k, T, nullptr, base, ldc, ncols, dec);
+  } else {
+    if (npairs <= 0) return;
+    ::hlq::g_launches++;
+    k_qr_update3<NB, true, RQ, NCG><<<dim3(slabs, npairs), 32 * RQ * NCG, smem, st>>>(
+        A, g, k, T, pairs, base, ldc, ncols, dec);
+  }
+}
+
+// v3 for nb in {64, 128, 192, 256, 320}; false -> the caller falls back to v2
+bool launch_qr_update3(const double* A, Geo g, int k, const double* T, const int2* pairs,
+                       int npairs, bool tt, double* base, int64_t ldc, int64_t ncols,
+                       const uint8_t* dec, cudaStream_t st) {
+  static int off = -1;
+  if (off < 0) off = getenv("HLQ_QR_UPDATE_V2") ? 1 : 0;
+  if (off) return false;
+  if (ncols <= 0) return true;
+  static int ncg = -1;
+  if (ncg < 0) ncg = getenv("HLQ_QR3_NCG") ? atoi(getenv("HLQ_QR3_NCG")) : 2;
+#define HLQ_L3(NBV)                                                                        \
+  case NBV:                                                                                \
+    if (ncg == 4)                                                                          \
+      launch3<NBV, 2, 4>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st);        \
+    else                                                                                   \
+      launch3<NBV, 2, 2>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st);        \
+    return true;
+  switch (g.nb) {
+    HLQ_L3(64)
+    HLQ_L3(128)
+    HLQ_L3(192)
+    HLQ_L3(256)
+    HLQ_L3(320)
+    default: return false;
+  }
+#undef HLQ_L3
 }
 
 }  // namespace hlq
