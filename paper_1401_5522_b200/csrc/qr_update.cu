@@ -433,7 +433,7 @@ __device__ __forceinline__ double2 lds2(const double* p) {
 }
 }  // namespace
 
-template <int NB, bool TT, int RQ, int NCG>
+template <int NB, bool TT, int RQ, int NCG, bool V16>
 __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ * NCG) : 1) k_qr_update3(const double* __restrict__ A, Geo g, int k,
                                                    const double* __restrict__ Tbase,
                                                    const int2* __restrict__ pairs,
@@ -470,7 +470,6 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
   const int crows = TT ? (bi < bk ? bi : bk) : bi;
   double* Cg = base + c0 * ldcg + g.r0(i);
   const int wc = cg * 16;  // first slab column of this warp
-  const bool v16 = ((g.lda & 1) == 0) && ((((uintptr_t)Vt) & 15) == 0) && ((crows & 1) == 0);
 
   // ---- C^T fragments: cT[m][j][h] = C(row 8 RB + 2t + h, col wc + 8m + g), RB = RQ j + rh
   double cT[2][NJ][2];
@@ -491,33 +490,46 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
   const int nch_i = (crows + 31) / 32;
   auto chunk_lo = [&](int b) { return TT ? 0 : b; };
   auto chunk_hi = [&](int b) { return TT ? (b < nch_i - 1 ? b : nch_i - 1) : nch_i - 1; };
-  // producer
-  int pb = 0, ppass = 0, pch = 0;
-  double* pslot = ring;
-  bool pdone = false;
-  auto start_block = [&]() {
-    while (pb < nblk && chunk_hi(pb) < chunk_lo(pb)) ++pb;
-    if (pb >= nblk) pdone = true;
-    pch = chunk_lo(pb);
-  };
-  start_block();
+  // the chunk schedule (block, pass, chunk) of the whole CTA, built once: the producer is a table
+  // lookup per chunk
+  constexpr int MAXS = 2 * NCH * (NCH + 1) / 2 + 2;
+  __shared__ int sched[MAXS];
+  __shared__ int nsched;
+  if (tid == 0) {
+    int n = 0;
+    for (int b = 0; b < nblk; ++b) {
+      const int lo = chunk_lo(b), hi = chunk_hi(b);
+      for (int pass = 0; pass < 2; ++pass)
+        for (int ch = lo; ch <= hi; ++ch) sched[n++] = (b << 16) | (pass << 8) | ch;
+    }
+    nsched = n;
+  }
+  __syncthreads();
+  const int S = nsched;
   // per-thread copy coordinates (16-byte copies: column l, rows r, r+1 of a 32 x 32 chunk)
   constexpr int CPT = 512 / NT;   // copies per thread per chunk
   const int cl0 = tid >> 4, cr = (tid & 15) * 2;
+  int64_t goff[CPT];
+#pragma unroll
+  for (int u = 0; u < CPT; ++u) goff[u] = (int64_t)(cl0 + (NT / 16) * u) * g.lda + cr;
+  int ps = 0;
+  double* pslot = ring;
   auto issue = [&]() {
-    if (!pdone) {
+    if (ps < S) {
+      const int e = sched[ps];
+      const int pb = e >> 16, pass = (e >> 8) & 1, ch = e & 255;
       const int i0 = 32 * pb;
       const int cmax = (bk - i0) < 32 ? (bk - i0) : 32;
-      const double* src = Vt + (int64_t)i0 * g.lda + 32 * pch;
-      const int rmax = crows - 32 * pch;  // valid rows in this chunk
-      const int ld = ppass == 0 ? LD3 : LD3B;
-      if (v16) {
+      const double* src = Vt + (int64_t)i0 * g.lda + 32 * ch;
+      const int rmax = crows - 32 * ch;  // valid rows in this chunk
+      const int ld = pass == 0 ? LD3 : LD3B;
+      if (V16) {
         const bool rok = cr < rmax;
 #pragma unroll
         for (int u = 0; u < CPT; ++u) {
           const int l = cl0 + (NT / 16) * u;
           const bool ok = rok && (l < cmax);
-          cp16(pslot + l * ld + cr, ok ? src + (int64_t)l * g.lda + cr : src, ok);
+          cp16(pslot + l * ld + cr, ok ? src + goff[u] : src, ok);
         }
       } else {
         for (int o = tid; o < 1024; o += NT) {
@@ -526,7 +538,7 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
           cp8(pslot + l * ld + r, ok ? src + (int64_t)l * g.lda + r : src, ok);
         }
       }
-      if (ppass == 0 && pch == chunk_lo(pb)) {
+      if (pass == 0 && ch == chunk_lo(pb)) {
         double* ts = Ts + (pb & 1) * CH3;
 #pragma unroll
         for (int u = 0; u < CPT; ++u) {
@@ -536,15 +548,7 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
         }
       }
       pslot = (pslot == ring + (RING - 1) * CH3) ? ring : pslot + CH3;
-      if (++pch > chunk_hi(pb)) {
-        if (++ppass == 2) {
-          ppass = 0;
-          ++pb;
-          start_block();
-        } else {
-          pch = chunk_lo(pb);
-        }
-      }
+      ++ps;
     }
     commit_();
   };
@@ -722,26 +726,26 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
 
 static size_t upd3_smem(int warps) { return sizeof(double) * ((size_t)8 * CH3 + (size_t)warps * 512); }
 
-template <int NB, int RQ = 2, int NCG = 2>
+template <int NB, int RQ, int NCG, bool V16>
 static void launch3(const double* A, Geo g, int k, const double* T, const int2* pairs, int npairs,
                     bool tt, double* base, int64_t ldc, int64_t ncols, const uint8_t* dec,
                     cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    smem_optin(k_qr_update3<NB, false, RQ, NCG>);
-    smem_optin(k_qr_update3<NB, true, RQ, NCG>);
+    smem_optin(k_qr_update3<NB, false, RQ, NCG, V16>);
+    smem_optin(k_qr_update3<NB, true, RQ, NCG, V16>);
     attr = true;
   }
   const unsigned slabs = (unsigned)((ncols + 16 * NCG - 1) / (16 * NCG));
   const size_t smem = upd3_smem(RQ * NCG);
   if (!tt) {
     ::hlq::g_launches++;
-    k_qr_update3<NB, false, RQ, NCG><<<dim3(slabs, g.n - k), 32 * RQ * NCG, smem, st>>>(
+    k_qr_update3<NB, false, RQ, NCG, V16><<<dim3(slabs, g.n - k), 32 * RQ * NCG, smem, st>>>(
         A, g, k, T, nullptr, base, ldc, ncols, dec);
   } else {
     if (npairs <= 0) return;
     ::hlq::g_launches++;
-    k_qr_update3<NB, true, RQ, NCG><<<dim3(slabs, npairs), 32 * RQ * NCG, smem, st>>>(
+    k_qr_update3<NB, true, RQ, NCG, V16><<<dim3(slabs, npairs), 32 * RQ * NCG, smem, st>>>(
         A, g, k, T, pairs, base, ldc, ncols, dec);
   }
 }
@@ -754,14 +758,19 @@ bool launch_qr_update3(const double* A, Geo g, int k, const double* T, const int
   if (off < 0) off = getenv("HLQ_QR_UPDATE_V2") ? 1 : 0;
   if (off) return false;
   if (ncols <= 0) return true;
+  // 16-byte V copies need an even leading dimension, a 16-byte aligned matrix and even tile heights
+  const bool v16 = ((g.lda & 1) == 0) && ((((uintptr_t)A) & 15) == 0) && ((g.N & 1) == 0) &&
+                   ((g.nb & 1) == 0);
   static int ncg = -1;
   if (ncg < 0) ncg = getenv("HLQ_QR3_NCG") ? atoi(getenv("HLQ_QR3_NCG")) : 2;
 #define HLQ_L3(NBV)                                                                        \
   case NBV:                                                                                \
-    if (ncg == 4)                                                                          \
-      launch3<NBV, 2, 4>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st);        \
+    if (!v16)                                                                              \
+      launch3<NBV, 2, 2, false>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st); \
+    else if (ncg == 4)                                                                     \
+      launch3<NBV, 2, 4, true>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st);  \
     else                                                                                   \
-      launch3<NBV, 2, 2>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st);        \
+      launch3<NBV, 2, 2, true>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st);  \
     return true;
   switch (g.nb) {
     HLQ_L3(64)
