@@ -445,7 +445,10 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
   constexpr int QPC = 4 / RQ;        // of those, per 32-row chunk
   constexpr int NT = 32 * RQ * NCG;
   constexpr int W = 16 * NCG;        // slab columns
-  constexpr int RING = 6;
+  // ring depth: T_b lands in buffer b & 1 up to RING - 1 chunks ahead; safe because block b + 2's
+  // first chunk is issued after every warp finished block b's TRMM (n0(b) + 2 n0(b+1) >= RING - 1
+  // chunks separate them for both chunk schedules)
+  constexpr int RING = 5;
   extern __shared__ __align__(16) double sm[];
   double* ring = sm;                     // RING x CH3: V chunks [l][r] (ld LD3 / LD3B by pass)
   double* Ts = ring + RING * CH3;        // 2 x CH3: T_b [l][q]
@@ -724,7 +727,7 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
   }
 }
 
-static size_t upd3_smem(int warps) { return sizeof(double) * ((size_t)8 * CH3 + (size_t)warps * 512); }
+static size_t upd3_smem(int warps) { return sizeof(double) * ((size_t)7 * CH3 + (size_t)warps * 512); }
 
 template <int NB, int RQ, int NCG, bool V16>
 static void launch3(const double* A, Geo g, int k, const double* T, const int2* pairs, int npairs,
@@ -760,7 +763,7 @@ bool launch_qr_update3(const double* A, Geo g, int k, const double* T, const int
   if (ncols <= 0) return true;
   // 16-byte V copies need an even leading dimension, a 16-byte aligned matrix and even tile heights
   const bool v16 = ((g.lda & 1) == 0) && ((((uintptr_t)A) & 15) == 0) && ((g.N & 1) == 0) &&
-                   ((g.nb & 1) == 0);
+                   ((g.nb & 1) == 0) && ((ldc & 1) == 0) && ((((uintptr_t)base) & 15) == 0);
   static int ncg = -1;
   if (ncg < 0) ncg = getenv("HLQ_QR3_NCG") ? atoi(getenv("HLQ_QR3_NCG")) : 2;
 #define HLQ_L3(NBV)                                                                        \
