@@ -204,6 +204,12 @@ int hlq_grid_local_shape(int64_t N, int32_t nb, int32_t P, int32_t Q, int32_t p,
  * Intra pairs are local panel indices (local tile row - li0), inter pairs are head slots
  * s = (d mod P) * (D/P) + d / P of domain d. */
 int hlq_dist_plan(int32_t n, int32_t P, int32_t D, int32_t p, int32_t k, int32_t* out, int32_t cap);
+/* Host-only element counts (doubles) of the four per-step exchanges of rank (p, q) at step k:
+ * out4[0] statistics record (allgather in process column k mod Q), out4[1] domain-head tiles (same),
+ * out4[2] panel package of process row p (broadcast from process column k mod Q), out4[3] domain-head
+ * rows of process column q (allgather).  All ranks of one communicator get the same value. */
+int hlq_dist_counts(int64_t N, int32_t nb, int32_t P, int32_t Q, int32_t D, int32_t p, int32_t q,
+                    int32_t k, int64_t* out4);
 /* Factor the distributed matrix in place.  A_local: one device pointer per rank hosted by this
  * process (hlq_grid_info nlocal; rank order), lld: local leading dimensions (NULL or 0 -> mloc).
  * Same criteria, options (forced / ref_dec / ref_margin are the global host vectors, identical on

@@ -75,6 +75,7 @@ def _load():
         "hlq_grid_info": ([P, P, P, P, P], I32),
         "hlq_grid_local_shape": ([I64, I32, I32, I32, I32, I32, P, P], I32),
         "hlq_dist_plan": ([I32, I32, I32, I32, I32, P, I32], I32),
+        "hlq_dist_counts": ([I64, I32, I32, I32, I32, I32, I32, I32, P], I32),
         "hlq_factor_dist": ([P, P, P, I64, I32, I32, D, P, P], I32),
         "hlq_generate_uniform_cyclic": ([P, P, P, I64, I32, U64, P], I32),
         "hlq_residual_dist": ([P, P, P, I64, I32, P, P, P, P], I32),
@@ -342,6 +343,14 @@ def dist_plan(n: int, P: int, D: int, p: int, k: int) -> dict:
     out["intra"] = levels()
     out["inter"] = levels()
     return out
+
+
+def dist_counts(N: int, nb: int, P: int, Q: int, D: int, p: int, q: int, k: int):
+    """(stats record, head tiles, panel package, head rows) element counts of step k (host-only)."""
+    out = np.zeros(4, dtype=np.int64)
+    _check(lib.hlq_dist_counts(N, nb, P, Q, D, p, q, k, out.ctypes.data_as(C.c_void_p)),
+           "hlq_dist_counts")
+    return tuple(int(v) for v in out)
 
 
 class Grid:

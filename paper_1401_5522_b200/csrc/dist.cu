@@ -501,6 +501,27 @@ struct DistState {
       if (c.block) cudaFree(c.block);
   }
 };
+// Element counts (doubles) of the four per-step exchanges, as every rank computes them (host):
+// [0] X1 statistics record (column qk allgather, per rank), [1] X2 head tiles (column qk allgather,
+// per rank), [2] X3 panel package of process row p (row broadcast), [3] X4 head rows of process
+// column q (column allgather, per rank).  Ranks of one communicator must agree (NCCL deadlocks
+// otherwise): tests/test_dist_host.py checks it across gloo ranks.
+inline void step_counts(int64_t N, int nb, int P, int Q, int D, int ib, int p, int q, int k,
+                        int64_t out[4]) {
+  const int n = (int)((N + nb - 1) / nb);
+  const int c = D / P, S = D;
+  const int ms_max = cyc_count(n, P, 0);
+  out[0] = ms_max + 3 * (int64_t)nb + 2 + (int64_t)nb * nb;
+  out[1] = (int64_t)c * nb * nb;
+  const int li0 = cyc_below(k, P, p);
+  const int ms = std::max(0, cyc_count(n, P, p) - li0);
+  const int64_t prow = std::max<int64_t>(0, cyc_extent(N, nb, P, p) - (int64_t)li0 * nb);
+  out[2] = prow * nb + 2 * (int64_t)ms * ib * nb + (int64_t)S * nb * nb + (int64_t)S * ib * nb +
+           (int64_t)nb * nb + 4 + nb;
+  const int lc1 = cyc_below(k + 1, Q, q);
+  const int64_t ncl = std::max<int64_t>(0, cyc_extent(N, nb, Q, q) - (int64_t)lc1 * nb);
+  out[3] = (int64_t)c * nb * ncl;
+}
 }  // namespace hlq
 
 // ---------------------------------------------------------------------------------------------
@@ -911,10 +932,9 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
       PR.end(st);
     }
     auto pcount = [&](int p) {
-      const int li0 = cyc_below(k, P, p);
-      const int ms = std::max(0, cyc_count(n, P, p) - li0);
-      const int64_t prow = std::max<int64_t>(0, cyc_extent(ds.N, nb, P, p) - (int64_t)li0 * nb);
-      return ds.pkg_count(prow, ms);
+      int64_t cnt[4];
+      step_counts(ds.N, nb, P, Q, ds.D, ib, p, 0, k, cnt);
+      return cnt[2];
     };
     PR.begin(HLQ_PROF_OTHER, st);
     if ((rc = row_bcast(ds, qk, [](Ctx& c) { return c.pkg; }, pcount))) return rc;
@@ -964,10 +984,10 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
     }
     PR.begin(HLQ_PROF_OTHER, st);
     for (int q = 0; q < Q; ++q) {
-      const int lc1 = cyc_below(k + 1, Q, q);
-      const int64_t ncl = std::max<int64_t>(0, cyc_extent(ds.N, nb, Q, q) - (int64_t)lc1 * nb);
+      int64_t cnt[4];
+      step_counts(ds.N, nb, P, Q, ds.D, ib, 0, q, k, cnt);
       if ((rc = col_allgather(ds, q, [](Ctx& c) { return c.hr_send; },
-                              [](Ctx& c) { return c.hr_recv; }, (int64_t)cc * nb * ncl)))
+                              [](Ctx& c) { return c.hr_recv; }, cnt[3])))
         return rc;
     }
     PR.end(st);
@@ -1415,6 +1435,23 @@ int hlq_residual_dist(hlq_grid_t grid, double* const* A_local, const int64_t* ll
     for (int t = 0; t < nlocal; ++t) m = std::max(m, h[4 * t + j]);
     out3[j] = m;
   }
+  return 0;
+}
+
+int hlq_dist_counts(int64_t N, int32_t nb, int32_t P, int32_t Q, int32_t D, int32_t p, int32_t q,
+                    int32_t k, int64_t* out4) {
+  if (N <= 0) return -1;
+  if (nb <= 0) return -2;
+  if (P < 1) return -3;
+  if (Q < 1) return -4;
+  if (D < P || D % P != 0) return -5;
+  if (p < 0 || p >= P) return -6;
+  if (q < 0 || q >= Q) return -7;
+  if (nb > N) nb = (int32_t)N;
+  const int n = (int)((N + nb - 1) / nb);
+  if (k < 0 || k >= n) return -8;
+  if (!out4) return -9;
+  step_counts(N, nb, P, Q, D, 32, p, q, k, out4);
   return 0;
 }
 
