@@ -300,18 +300,21 @@ def main():
     dom = max(("lu_update", "qr_unmqr"), key=lambda c: agg[c]["ms"])
     achieved = agg[dom]["flops"] / (agg[dom]["ms"] * 1e-3) / 1e12 if agg[dom]["ms"] > 0 else 0.0
     step_ms_sum = sum(v["ms"] for v in agg.values())
-    traffic = None
+    traffic, traffic_note = None, None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(f"{args.config}:{dom}")
+            tj = json.load(open(tpath))
+            traffic = tj.get(f"{args.config}:{dom}")
+            traffic_note = tj.get("_notes", {}).get(f"{args.config}:{dom}")
         except Exception:
             traffic = None
     kname = {"lu_update": "k_dgemm (LU Schur update + SWPTRSM)",
-             "qr_unmqr": "k_unmqr_dmma + k_ttmqr_dmma (QR trailing update)"}[dom]
+             "qr_unmqr": "k_qr_update3 (QR trailing update: UNMQR + TTMQR)"}[dom]
     roofline = {"bound": "tensor", "kernel": kname,
                 "achieved": achieved, "peak": FP64_DMMA_PEAK_TF, "unit": "TFLOP/s",
                 "frac": achieved / FP64_DMMA_PEAK_TF, "traffic": traffic,
+                "traffic_note": traffic_note,
                 "peak_source": "measured FP64 DMMA mma.sync m8n8k4 sustained, 148 SMs "
                                "(profiles/r01/peak_dmma.jsonl); cuBLAS DGEMM measured 36.2",
                 "share_of_step": agg[dom]["ms"] / t_sum if t_sum else None,
@@ -467,7 +470,7 @@ def run_distributed(args, cfg, rank, world, local, dev):
     # this rank's share of the class flops: the trailing update is spread evenly over the grid
     achieved = agg[dom]["flops"] / world / (agg[dom]["ms"] * 1e-3) / 1e12 if agg[dom]["ms"] else 0.0
     kname = {"lu_update": "k_dgemm (LU Schur update + SWPTRSM)",
-             "qr_unmqr": "k_unmqr_dmma + k_ttmqr_dmma (QR trailing update)"}[dom]
+             "qr_unmqr": "k_qr_update3 (QR trailing update: UNMQR + TTMQR)"}[dom]
     roofline = {"bound": "tensor", "kernel": kname, "achieved": achieved,
                 "peak": FP64_DMMA_PEAK_TF, "unit": "TFLOP/s", "frac": achieved / FP64_DMMA_PEAK_TF,
                 "traffic": None, "rank": rank,
