@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
   constexpr int QPC = 4 / RQ;        // of those, per 32-row chunk
   constexpr int NT = 32 * RQ * NCG;
   constexpr int W = 16 * NCG;        // slab columns
-  // ring depth: T_b lands in buffer b & 1 up to RING - 1 chunks ahead; safe because block b + 2's
+  // ring depth: T_b and C_e(b) land in buffer b & 1 up to RING - 1 chunks ahead; safe because block b + 2's
   // first chunk is issued after every warp finished block b's TRMM (n0(b) + 2 n0(b+1) >= RING - 1
   // chunks separate them for both chunk schedules)
   constexpr int RING = 5;
@@ -453,6 +453,7 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
   double* ring = sm;                     // RING x CH3: V chunks [l][r] (ld LD3 / LD3B by pass)
   double* Ts = ring + RING * CH3;        // 2 x CH3: T_b [l][q]
   double* Rb = Ts + 2 * CH3;             // RQ*NCG warps x 512: partial W^T
+  double* CE = Rb + RQ * NCG * 512;      // TT: 2 x (W x LD3) rows i0.. of C_e, [col][row]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, tq = lane & 3;
   const int cg = warp % NCG, rh = warp / NCG;  // column group, row group (RB == rh mod RQ)
@@ -519,8 +520,8 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
   double* pslot = ring;
   auto issue = [&]() {
     if (ps < S) {
-      const int e = sched[ps];
-      const int pb = e >> 16, pass = (e >> 8) & 1, ch = e & 255;
+      const int se = sched[ps];
+      const int pb = se >> 16, pass = (se >> 8) & 1, ch = se & 255;
       const int i0 = 32 * pb;
       const int cmax = (bk - i0) < 32 ? (bk - i0) : 32;
       const double* src = Vt + (int64_t)i0 * g.lda + 32 * ch;
@@ -548,6 +549,24 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
           const int l = cl0 + (NT / 16) * u;
           const bool ok = l < cmax;
           cp16(ts + l * LD3 + cr, ok ? T + (int64_t)(i0 + l) * 32 + cr : T, ok);
+        }
+        if (TT) {
+          // rows i0.. of C_e for this block (W = C_e(b) + V^T C_i; C_e(b) -= U after the TRMM)
+          double* ce = CE + (pb & 1) * W * LD3;
+          const double* cs = base + c0 * ldcg + g.r0(e) + i0;
+          if (V16) {
+            for (int o = tid; o < W * 16; o += NT) {
+              const int j = o >> 4, r = (o & 15) * 2;
+              const bool ok = (j < cvalid) && (r < cmax);
+              cp16(ce + j * LD3 + r, ok ? cs + (int64_t)j * ldcg + r : cs, ok);
+            }
+          } else {
+            for (int o = tid; o < W * 32; o += NT) {
+              const int j = o >> 5, r = o & 31;
+              const bool ok = (j < cvalid) && (r < cmax);
+              cp8(ce + j * LD3 + r, ok ? cs + (int64_t)j * ldcg + r : cs, ok);
+            }
+          }
         }
       }
       pslot = (pslot == ring + (RING - 1) * CH3) ? ring : pslot + CH3;
@@ -584,17 +603,7 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
     for (int m = 0; m < 2; ++m)
 #pragma unroll
       for (int nl = 0; nl < 4; ++nl) wT[m][nl][0] = wT[m][nl][1] = 0.0;
-    if (TT && rh == 0) {
-#pragma unroll
-      for (int m = 0; m < 2; ++m)
-#pragma unroll
-        for (int nl = 0; nl < 4; ++nl)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int col = wc + 8 * m + gq, l = 8 * nl + 2 * tq + h;
-            if (col < cvalid && l < sb) wT[m][nl][h] = Ceb[(int64_t)col * ldcg + l];
-          }
-    }
+    const double* ce = CE + (b & 1) * W * LD3;
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) {
       if (ch < clo || ch > chi) continue;
@@ -606,6 +615,16 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
       if (ch == b) {
         fix_diag(const_cast<double*>(V), 1, LD3);
         __syncthreads();
+      }
+      if (TT && ch == clo && rh == 0) {  // W starts from the C_e block rows (landed with chunk clo)
+#pragma unroll
+        for (int m = 0; m < 2; ++m)
+#pragma unroll
+          for (int nl = 0; nl < 4; ++nl) {
+            const double2 v = lds2(ce + (wc + 8 * m + gq) * LD3 + 8 * nl + 2 * tq);
+            wT[m][nl][0] += v.x;
+            wT[m][nl][1] += v.y;
+          }
       }
 #pragma unroll
       for (int q = 0; q < QPC; ++q) {
@@ -673,7 +692,8 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int col = wc + 8 * m + gq, l = 8 * no + 2 * tq + h;
-            if (col < cvalid && l < sb) Ceb[(int64_t)col * ldcg + l] -= uT[m][no][h];
+            if (col < cvalid && l < sb)
+              Ceb[(int64_t)col * ldcg + l] = ce[col * LD3 + l] - uT[m][no][h];
           }
     }
 #pragma unroll
@@ -727,7 +747,9 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
   }
 }
 
-static size_t upd3_smem(int warps) { return sizeof(double) * ((size_t)7 * CH3 + (size_t)warps * 512); }
+static size_t upd3_smem(int warps, int W) {
+  return sizeof(double) * ((size_t)7 * CH3 + (size_t)warps * 512 + (size_t)2 * W * LD3);
+}
 
 template <int NB, int RQ, int NCG, bool V16>
 static void launch3(const double* A, Geo g, int k, const double* T, const int2* pairs, int npairs,
@@ -740,7 +762,7 @@ static void launch3(const double* A, Geo g, int k, const double* T, const int2* 
     attr = true;
   }
   const unsigned slabs = (unsigned)((ncols + 16 * NCG - 1) / (16 * NCG));
-  const size_t smem = upd3_smem(RQ * NCG);
+  const size_t smem = upd3_smem(RQ * NCG, 16 * NCG);
   if (!tt) {
     ::hlq::g_launches++;
     k_qr_update3<NB, false, RQ, NCG, V16><<<dim3(slabs, g.n - k), 32 * RQ * NCG, smem, st>>>(
