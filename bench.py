@@ -222,18 +222,30 @@ def main():
     N, nb = cfg["N"], cfg["nb"]
     n = (N + nb - 1) // nb
     seed = cfg["seed"]
-    # inputs generated on the device with the counter generator (bit-identical to hlq_inputs)
-    A0 = torch.empty(N * N, dtype=torch.float64, device=dev)
+    # inputs generated on the device with the counter generator (bit-identical to hlq_inputs).
+    # No second copy of A when it would not fit next to the factorization's workspace (C5 on one
+    # GPU is 137 GB): uniform inputs are then regenerated before every step (outside the timing).
+    A = torch.empty(N * N, dtype=torch.float64, device=dev)
     b = torch.empty(N, dtype=torch.float64, device=dev)
+    A0 = None
     if cfg["gen"] == "uniform":
-        H.hlq_generate_uniform(A0, N, N, N, seed, 0, N)
         H.hlq_generate_uniform(b, N, 1, N, seed, N * N, N)
+        if 16.0 * N * N < 0.6 * torch.cuda.get_device_properties(dev).total_memory:
+            A0 = torch.empty_like(A)
+            H.hlq_generate_uniform(A0, N, N, N, seed, 0, N)
     else:
         import hlq_inputs as I
         Ah, bh, _ = I.config_system(args.config, N)
-        A0.copy_(torch.from_numpy(np.ascontiguousarray(Ah.T)).reshape(-1))
+        A0 = torch.from_numpy(np.ascontiguousarray(Ah.T)).reshape(-1).to(dev)
         b.copy_(torch.from_numpy(bh))
-    A = torch.empty_like(A0)
+        del Ah
+
+    def restore():
+        if A0 is not None:
+            A.copy_(A0)
+        else:
+            H.hlq_generate_uniform(A, N, N, N, seed, 0, N)
+
     x = torch.empty_like(b)
     crit = CRIT[args.criterion] if args.criterion else 0
     forced = None
@@ -242,7 +254,7 @@ def main():
         forced = I.bernoulli_pattern(30, n, args.fqr)
 
     def one_step(profile):
-        A.copy_(A0)
+        restore()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -284,10 +296,11 @@ def main():
     fake = info["fake_flops"]
     true = info["true_flops"]
     value = fake * world / (ms_step * 1e-3) / 1e12
-    # HPL3 of the last step (device residual against the pristine copy)
-    res = H.hlq_residual(A0, N, N, x, b)
+    # HPL3 of the last step (device residual against the pristine matrix)
     dec = last.decisions()
     last.free()
+    restore()
+    res = H.hlq_residual(A, N, N, x, b)
 
     # roofline: dominant kernel class of the step
     agg = {}
@@ -322,9 +335,14 @@ def main():
 
     # e2e through the public C ABI with host buffers (H2D of A and b, D2H of x inside the timing)
     e2e = None
-    if not args.no_e2e:
+    if args.no_e2e:
+        pass
+    elif 8.0 * N * N > 64e9:
+        e2e = {"value": None, "unit": "TFLOP/s",
+               "skipped": f"the {8.0 * N * N / 1e9:.0f} GB host copy of A exceeds the 64 GB host budget"}
+    else:
         Ah = torch.empty(N * N, dtype=torch.float64, pin_memory=True)
-        Ah.copy_(A0)
+        Ah.copy_(A)
         bh = b.cpu().pin_memory()
         xh = torch.empty(N, dtype=torch.float64, pin_memory=True)
         opt = H.hlq_default_options()

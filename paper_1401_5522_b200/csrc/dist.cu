@@ -106,7 +106,7 @@ struct hlq_grid_s {
   int P = 1, Q = 1;
   int local = 1;       // 1: all P*Q ranks emulated in this process
   int rank = 0;        // NCCL: this process's world rank (p = rank / Q, q = rank % Q)
-  ncclComm_t world = nullptr, row = nullptr, col = nullptr;
+  ncclComm_t world = nullptr, row = nullptr, col = nullptr, colp = nullptr;  // colp: panel stream
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -470,6 +470,7 @@ struct Ctx {
   double *Tg = nullptr, *Ttt = nullptr, *mstore = nullptr;
   double *rec_send = nullptr, *rec_recv = nullptr, *head_send = nullptr, *head_recv = nullptr;
   double *pkg = nullptr, *hr_send = nullptr, *hr_recv = nullptr, *HR = nullptr;
+  double *pkgs[2] = {nullptr, nullptr}, *scrs[2] = {nullptr, nullptr};  // per step parity
   double *xseg = nullptr, *xk = nullptr, *hx_send = nullptr, *hx_recv = nullptr, *HX = nullptr;
   double *xg = nullptr, *fin = nullptr;
   int2* pairs = nullptr;
@@ -485,6 +486,8 @@ struct DistState {
   int ms_max = 0, mt_max = 0;
   int64_t rec_count = 0, seg_cap = 0;
   cudaStream_t st = nullptr;
+  cudaStream_t sp = nullptr;                    // high-priority panel stream (lookahead)
+  cudaEvent_t ev_part0 = nullptr, ev_panel = nullptr;
   std::vector<Ctx> ctx;
   std::vector<std::vector<std::vector<int2>>> inter;  // per step
   // package layout (offsets in doubles) for a rank with `prow` panel rows and `ms` panel tiles
@@ -499,6 +502,9 @@ struct DistState {
   ~DistState() {
     for (auto& c : ctx)
       if (c.block) cudaFree(c.block);
+    if (ev_part0) cudaEventDestroy(ev_part0);
+    if (ev_panel) cudaEventDestroy(ev_panel);
+    if (sp) cudaStreamDestroy(sp);
   }
 };
 // Element counts (doubles) of the four per-step exchanges, as every rank computes them (host):
@@ -530,13 +536,14 @@ namespace {
 using Buf = std::function<double*(Ctx&)>;
 
 // allgather inside process column q: member p's `count` doubles -> every member's recv at p*count
-int col_allgather(DistState& ds, int q, const Buf& send, const Buf& recv, int64_t count) {
+int col_allgather(DistState& ds, int q, const Buf& send, const Buf& recv, int64_t count,
+                  cudaStream_t st, bool panel_comm) {
   if (count <= 0) return 0;
   if (!ds.gr->local) {
     for (auto& c : ds.ctx)
       if (c.q == q)
-        return nccl_err(g_nccl.AllGather(send(c), recv(c), (size_t)count, ncclDouble, ds.gr->col,
-                                         ds.st),
+        return nccl_err(g_nccl.AllGather(send(c), recv(c), (size_t)count, ncclDouble,
+                                         panel_comm ? ds.gr->colp : ds.gr->col, st),
                         "allgather");
     return 0;
   }
@@ -545,7 +552,7 @@ int col_allgather(DistState& ds, int q, const Buf& send, const Buf& recv, int64_
     for (auto& src : ds.ctx) {
       if (src.q != q) continue;
       int rc = cuda_check(cudaMemcpyAsync(recv(dst) + (int64_t)src.p * count, send(src),
-                                          sizeof(double) * count, cudaMemcpyDeviceToDevice, ds.st));
+                                          sizeof(double) * count, cudaMemcpyDeviceToDevice, st));
       if (rc) return rc;
     }
   }
@@ -553,13 +560,14 @@ int col_allgather(DistState& ds, int q, const Buf& send, const Buf& recv, int64_
 }
 
 // broadcast inside every process row from process column root; count may depend on the row
-int row_bcast(DistState& ds, int root, const Buf& buf, const std::function<int64_t(int)>& count) {
+int row_bcast(DistState& ds, int root, const Buf& buf, const std::function<int64_t(int)>& count,
+              cudaStream_t st) {
   if (!ds.gr->local) {
     for (auto& c : ds.ctx) {
       int64_t n = count(c.p);
       if (n <= 0) return 0;
       return nccl_err(g_nccl.Broadcast(buf(c), buf(c), (size_t)n, ncclDouble, root, ds.gr->row,
-                                       ds.st),
+                                       st),
                       "broadcast(row)");
     }
     return 0;
@@ -571,7 +579,7 @@ int row_bcast(DistState& ds, int root, const Buf& buf, const std::function<int64
       int64_t n = count(src.p);
       if (n <= 0) continue;
       int rc = cuda_check(cudaMemcpyAsync(buf(dst), buf(src), sizeof(double) * n,
-                                          cudaMemcpyDeviceToDevice, ds.st));
+                                          cudaMemcpyDeviceToDevice, st));
       if (rc) return rc;
     }
   }
@@ -637,6 +645,8 @@ static int dist_alloc(DistState& ds, Ctx& c, const hlq_options& opt, bool has_re
          o_ms = take(8 * (size_t)nt * ds.mstore_stride()), o_rs = take(8 * ds.rec_count),
          o_rr = take(8 * (size_t)P * ds.rec_count), o_hs = take(8 * (size_t)cc * nb * nb),
          o_hr = take(8 * (size_t)P * cc * nb * nb), o_pk = take(8 * (size_t)ds.pkg_count(mloc, mt)),
+         o_pk2 = take(8 * (size_t)ds.pkg_count(mloc, mt)),
+         o_scr2 = take(8 * (2 * (size_t)nb * nb + nb)),
          o_rws = take(8 * (size_t)cc * nb * nloc), o_rwr = take(8 * (size_t)P * cc * nb * nloc),
          o_HR = take(8 * (size_t)S * nb * nloc), o_xs = take(8 * (size_t)ds.seg_cap),
          o_xk = take(8 * (size_t)nb), o_hxs = take(8 * (size_t)cc * nb),
@@ -682,6 +692,10 @@ static int dist_alloc(DistState& ds, Ctx& c, const hlq_options& opt, bool has_re
   c.head_send = (double*)(b + o_hs);
   c.head_recv = (double*)(b + o_hr);
   c.pkg = (double*)(b + o_pk);
+  c.pkgs[0] = c.pkg;
+  c.pkgs[1] = (double*)(b + o_pk2);
+  c.scrs[0] = w.scratch;
+  c.scrs[1] = (double*)(b + o_scr2);
   c.hr_send = (double*)(b + o_rws);
   c.hr_recv = (double*)(b + o_rwr);
   c.HR = (double*)(b + o_HR);
@@ -733,6 +747,7 @@ static int dist_alloc(DistState& ds, Ctx& c, const hlq_options& opt, bool has_re
   cudaMemsetAsync(w.dec, 0, n, ds.st);
   cudaMemsetAsync(c.xseg, 0, sizeof(double) * ds.seg_cap, ds.st);
   cudaMemsetAsync(w.scratch, 0, sizeof(double) * (2 * (size_t)nb * nb + nb), ds.st);
+  cudaMemsetAsync(c.scrs[1], 0, sizeof(double) * (2 * (size_t)nb * nb + nb), ds.st);
   return cuda_check(cudaGetLastError());
 }
 
@@ -750,9 +765,15 @@ static Geo panel_geo(const DistState& ds, const Ctx& c, const StepPlan& sp, int6
   return g;
 }
 
+// The factorization schedule: panel stage P(k) (A, X1, B, X2, C, X3) on the high-priority panel
+// stream, update stage U(k) (D, X4, E) on the caller's stream in two parts: part 0 = the local
+// column tile k+1 (process column (k+1) mod Q only), part 1 = the rest.  P(k+1) starts as soon as
+// U(k) part 0 is done and overlaps U(k) part 1 (lookahead depth 1, as on one GPU).  The panel
+// package and the L^-1 / perm scratch are double-buffered by step parity; the panel stream uses its
+// own column communicator (colp) so every NCCL communicator is driven by exactly one stream.
 static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options& opt, Prof& PR) {
   const int n = ds.n, nb = ds.nb, P = ds.P, Q = ds.Q, S = ds.S, cc = ds.c, ib = ds.ib;
-  cudaStream_t st = ds.st;
+  cudaStream_t st = ds.st, sp = ds.sp;
   const bool has_forced = opt.forced != nullptr;
   const bool has_ref = ds.ctx[0].w.ref_dec != nullptr;
   const bool criterion_needed = !has_forced && alpha > 0.0 && !isinf(alpha);
@@ -767,6 +788,313 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
   gglob.lda = ds.N;
   gglob.nb = nb;
   gglob.n = n;
+  // per-parity views of the workspace (scratch = L^-1 | U^-1 | perm)
+  auto wk = [&](Ctx& c, int k) {
+    DevWork w = c.w;
+    w.scratch = c.scrs[k & 1];
+    return w;
+  };
+
+  // ======================================== panel stage P(k) on stream s
+  auto panel = [&](int k, cudaStream_t s) -> int {
+    int rc = 0;
+    const int pk = k % P, qk = k % Q, lk = k / Q;
+    const int bk = (int)std::min<int64_t>(nb, ds.N - (int64_t)k * nb);
+    const int known = known_of(k);
+    // ---- A: statistics, speculative GETRF on the owner
+    for (auto& c : ds.ctx) {
+      if (c.q != qk) continue;
+      const StepPlan& sp_ = c.plan[k];
+      DevWork w = wk(c, k);
+      double* Apan = c.A + (int64_t)lk * nb * c.lld + (int64_t)sp_.li0 * nb;
+      Geo gP = panel_geo(ds, c, sp_, c.lld);
+      gP.Nc = bk;
+      PR.begin(HLQ_PROF_CRITERION, s);
+      cudaMemsetAsync(c.rec_send, 0, sizeof(double) * ds.rec_count, s);
+      if (sp_.ms > 0 && criterion_needed)
+        launch_panel_stats_to(Apan, gP, 0, sp_.diag, c.rec_send, c.rec_send + ds.ms_max + nb,
+                              c.rec_send + ds.ms_max, s);
+      PR.end(s);
+      if (sp_.diag) {
+        PR.begin(HLQ_PROF_GETRF, s);
+        cudaMemsetAsync(w.zp, 0, sizeof(int), s);
+        cudaMemsetAsync(w.inv_norm, 0, sizeof(double), s);
+        if (known != HLQ_DEC_QR) {
+          launch_getrf(Apan, gP, 0, w, true, s);
+          launch_tri_inv(gP, 0, w, w.scratch, w.scratch + (size_t)nb * nb, s);
+          if (criterion_needed && crit != HLQ_CRIT_MUMPS) launch_invnorm(gP, 0, w, s);
+        }
+        ::hlq::g_launches++;
+        k_pack_owner<<<16, 256, 0, s>>>(c.rec_send + ds.ms_max + 2 * nb, w.inv_norm, w.zp, w.W,
+                                        w.ipiv_ws, nb, bk);
+        PR.end(s);
+      }
+    }
+    PR.begin(HLQ_PROF_OTHER, s);
+    if ((rc = col_allgather(ds, qk, [](Ctx& c) { return c.rec_send; },
+                            [](Ctx& c) { return c.rec_recv; }, ds.rec_count, s, true)))
+      return rc;
+    PR.end(s);
+    // ---- B: decision, LU panel / QR panel + intra-domain tree
+    for (auto& c : ds.ctx) {
+      if (c.q != qk) continue;
+      const StepPlan& sp_ = c.plan[k];
+      DevWork w = wk(c, k);
+      double* Apan = c.A + (int64_t)lk * nb * c.lld + (int64_t)sp_.li0 * nb;
+      Geo gP = panel_geo(ds, c, sp_, c.lld);
+      gP.Nc = bk;
+      const uint8_t* dk = w.dec + k;
+      PR.begin(HLQ_PROF_CRITERION, s);
+      ::hlq::g_launches++;
+      k_unpack_stats<<<16, 256, 0, s>>>(c.rec_recv, ds.rec_count, ds.ms_max, k, n, P, pk, nb, bk,
+                                        w.s, w.away_max, w.local_max, w.inv_norm, w.zp, w.W,
+                                        w.ipiv_ws);
+      launch_decide(gglob, k, crit, alpha, opt.mumps_reading, opt.tie_rel_tol, has_forced ? 1 : 0,
+                    has_ref ? 1 : 0, w, s);
+      PR.end(s);
+      double* Li = w.scratch;
+      double* Ui = w.scratch + (size_t)nb * nb;
+      int* perm = reinterpret_cast<int*>(w.scratch + (size_t)2 * nb * nb);
+      if (known != HLQ_DEC_QR) {
+        PR.begin(HLQ_PROF_LU_TRSM, s);
+        if (!sp_.diag) launch_tri_inv(gglob, k, w, Li, Ui, s);
+        if (sp_.diag)
+          launch_lu_commit(Apan, gP, 0, w.W, w.ipiv_ws, c.ipiv + (int64_t)k * nb, perm, dk, s);
+        const int64_t r0 = sp_.diag ? bk : 0;
+        const int64_t M = gP.N - r0;
+        if (M > 0) {
+          launch_copy_block(w.ws_panel, M, Apan + r0, c.lld, M, bk, nullptr, dk, 0, s);
+          launch_dgemm(Apan + r0, c.lld, w.ws_panel, M, Ui, nb, M, bk, bk, false, false, dk, 0,
+                       HLQ_DEC_LU, s);
+        }
+        PR.end(s);
+      }
+      if (known != HLQ_DEC_LU && sp_.ms > 0) {
+        PR.begin(HLQ_PROF_QR_GEQRT, s);
+        double* Tgk = c.Tg + ((int64_t)lk * c.mt + sp_.li0) * ib * nb;
+        double* Ttk = c.Ttt + ((int64_t)lk * c.mt + sp_.li0) * ib * nb;
+        launch_qr_panel_tc(Apan, gP, 0, ib, Tgk, Ttk, nullptr, 0, dk, false, s);
+        for (size_t l = 0; l < c.intra_ptr[k].size(); ++l)
+          launch_qr_panel_tc(Apan, gP, 0, ib, Tgk, Ttk, c.intra_ptr[k][l], c.intra_cnt[k][l], dk,
+                             true, s);
+        PR.end(s);
+      }
+      ::hlq::g_launches++;
+      k_pack_rows<<<blocks_for((int64_t)cc * nb * nb), 256, 0, s>>>(
+          c.head_send, cc, head_idx(sp_), Apan, c.lld, gP.N, nb, nb, bk);
+    }
+    PR.begin(HLQ_PROF_OTHER, s);
+    if ((rc = col_allgather(ds, qk, [](Ctx& c) { return c.head_send; },
+                            [](Ctx& c) { return c.head_recv; }, (int64_t)cc * nb * nb, s, true)))
+      return rc;
+    PR.end(s);
+    // ---- C: inter-domain merges (redundant on the column), package
+    for (auto& c : ds.ctx) {
+      if (c.q != qk) continue;
+      const StepPlan& sp_ = c.plan[k];
+      DevWork w = wk(c, k);
+      double* Apan = c.A + (int64_t)lk * nb * c.lld + (int64_t)sp_.li0 * nb;
+      Geo gP = panel_geo(ds, c, sp_, c.lld);
+      gP.Nc = bk;
+      const uint8_t* dk = w.dec + k;
+      const int64_t prow = gP.N;
+      double* pk_ = c.pkgs[k & 1];
+      double* HM = pk_ + ds.off_HM(prow, sp_.ms);
+      double* MT = pk_ + ds.off_MT(prow, sp_.ms);
+      Geo gH{};
+      gH.N = (int64_t)S * nb;
+      gH.lda = (int64_t)S * nb;
+      gH.nb = nb;
+      gH.n = S;
+      gH.Nc = bk;
+      ::hlq::g_launches++;
+      k_stack<<<blocks_for((int64_t)S * nb * nb), 256, 0, s>>>(HM, c.head_recv, S, nb, nb);
+      PR.begin(HLQ_PROF_QR_GEQRT, s);
+      if (known != HLQ_DEC_LU) {
+        for (size_t l = 0; l < c.inter_ptr[k].size(); ++l)
+          launch_qr_panel_tc(HM, gH, 0, ib, nullptr, MT, c.inter_ptr[k][l], c.inter_cnt[k][l], dk,
+                             true, s);
+        // own heads: R / TT-reflector triangles back into A, merge T factors into the local store
+        ::hlq::g_launches++;
+        k_unstack_rows<<<blocks_for((int64_t)cc * nb * nb), 256, 0, s>>>(
+            Apan, c.lld, prow, cc, head_idx(sp_), c.p * cc, HM, (int64_t)S * nb, nb, bk, 1, dk,
+            HLQ_DEC_QR);
+        for (int t = 0; t < cc; ++t) {
+          const int hl = sp_.head_local[t], hg = sp_.head_global[t];
+          if (hl < 0 || hg == k) continue;
+          ::hlq::g_launches++;
+          k_copy_vec<<<8, 256, 0, s>>>(c.Ttt + ((int64_t)lk * c.mt + sp_.li0 + hl) * ib * nb,
+                                       MT + (int64_t)(c.p * cc + t) * ib * nb, (int64_t)ib * nb, dk,
+                                       HLQ_DEC_QR);
+        }
+        // the solve replays the merges: keep HM + MT of this step
+        double* ms_ = c.mstore + (int64_t)lk * ds.mstore_stride();
+        cudaMemcpyAsync(ms_, HM, sizeof(double) * ds.mstore_stride(), cudaMemcpyDeviceToDevice, s);
+      }
+      // package: panel tiles, T factors, (HM, MT already in place), L^-1, perm, d_k
+      if (prow > 0)
+        cudaMemcpy2DAsync(pk_, sizeof(double) * prow, Apan, sizeof(double) * c.lld,
+                          sizeof(double) * prow, bk, cudaMemcpyDeviceToDevice, s);
+      if (sp_.ms > 0) {
+        cudaMemcpyAsync(pk_ + ds.off_Tg(prow), c.Tg + ((int64_t)lk * c.mt + sp_.li0) * ib * nb,
+                        sizeof(double) * sp_.ms * ib * nb, cudaMemcpyDeviceToDevice, s);
+        cudaMemcpyAsync(pk_ + ds.off_Ttt(prow, sp_.ms),
+                        c.Ttt + ((int64_t)lk * c.mt + sp_.li0) * ib * nb,
+                        sizeof(double) * sp_.ms * ib * nb, cudaMemcpyDeviceToDevice, s);
+      }
+      cudaMemcpyAsync(pk_ + ds.off_Li(prow, sp_.ms), w.scratch, sizeof(double) * nb * nb,
+                      cudaMemcpyDeviceToDevice, s);
+      ::hlq::g_launches++;
+      k_meta_pack<<<1, 256, 0, s>>>(pk_ + ds.off_meta(prow, sp_.ms), w.dec, w.margin, w.flags,
+                                    reinterpret_cast<int*>(w.scratch + (size_t)2 * nb * nb), bk, k,
+                                    nb);
+      PR.end(s);
+    }
+    auto pcount = [&](int p) {
+      int64_t cnt[4];
+      step_counts(ds.N, nb, P, Q, ds.D, ib, p, 0, k, cnt);
+      return cnt[2];
+    };
+    PR.begin(HLQ_PROF_OTHER, s);
+    const int par = k & 1;
+    if ((rc = row_bcast(ds, qk, [par](Ctx& c) { return c.pkgs[par]; }, pcount, s))) return rc;
+    PR.end(s);
+    return cuda_check(cudaGetLastError());
+  };
+
+  // ======================================== update stage U(k), part 0 or 1, on stream s
+  // local trailing columns [lc1*nb, nloc) split at the local column tile of global tile k+1
+  auto part_range = [&](int k, int q, int64_t nloc, int part, int64_t& co, int64_t& w) {
+    const int lc1 = cyc_below(k + 1, Q, q);
+    const int64_t ncl = std::max<int64_t>(0, nloc - (int64_t)lc1 * nb);
+    const int64_t w0 = (k + 1 < n && (k + 1) % Q == q) ? std::min<int64_t>(nb, ncl) : 0;
+    co = part == 0 ? 0 : w0;
+    w = part == 0 ? w0 : ncl - w0;
+    return lc1;
+  };
+  auto update = [&](int k, int part, cudaStream_t s) -> int {
+    int rc = 0;
+    const int bk = (int)std::min<int64_t>(nb, ds.N - (int64_t)k * nb);
+    const int known = known_of(k);
+    const int par = k & 1;
+    // ---- D: SWPTRSM / UNMQR + intra TTMQR, then pack the head rows
+    for (auto& c : ds.ctx) {
+      const StepPlan& sp_ = c.plan[k];
+      DevWork w = wk(c, k);
+      const int64_t prow = std::max<int64_t>(0, c.mloc - (int64_t)sp_.li0 * nb);
+      double* pk_ = c.pkgs[par];
+      const uint8_t* dk = w.dec + k;
+      int* perm = reinterpret_cast<int*>(w.scratch + (size_t)2 * nb * nb);
+      if (part == 0) {
+        ::hlq::g_launches++;
+        k_meta_unpack<<<1, 256, 0, s>>>(pk_ + ds.off_meta(prow, sp_.ms), w.dec, w.margin, w.flags,
+                                        perm, bk, k);
+      }
+      int64_t co, ncl;
+      const int lc1 = part_range(k, c.q, c.nloc, part, co, ncl);
+      if (ncl <= 0 || prow <= 0) continue;
+      double* base = c.A + ((int64_t)lc1 * nb + co) * c.lld + (int64_t)sp_.li0 * nb;
+      Geo gK{};
+      gK.N = prow;
+      gK.lda = prow;
+      gK.nb = nb;
+      gK.n = sp_.ms;
+      gK.Nc = bk;
+      if (known != HLQ_DEC_QR && sp_.diag) {
+        PR.begin(HLQ_PROF_LU_UPDATE, s);
+        launch_copy_block(w.ws_row + co * bk, bk, base, c.lld, bk, ncl, perm, dk, 0, s);
+        launch_dgemm(base, c.lld, pk_ + ds.off_Li(prow, sp_.ms), nb, w.ws_row + co * bk, bk, bk,
+                     ncl, bk, false, false, dk, 0, HLQ_DEC_LU, s);
+        PR.end(s);
+      }
+      if (known != HLQ_DEC_LU && sp_.ms > 0) {
+        PR.begin(HLQ_PROF_QR_UNMQR, s);
+        const int nl = (int)c.intra_ptr[k].size();
+        launch_qr_update_dmma(pk_, gK, 0, ib, pk_ + ds.off_Tg(prow), pk_ + ds.off_Ttt(prow, sp_.ms),
+                              c.intra_ptr[k].data(), c.intra_cnt[k].data(), nl, base, c.lld, ncl,
+                              dk, 0, s);
+        for (int l = 0; l < nl; ++l)
+          launch_qr_update_dmma(pk_, gK, 0, ib, pk_ + ds.off_Tg(prow),
+                                pk_ + ds.off_Ttt(prow, sp_.ms), c.intra_ptr[k].data(),
+                                c.intra_cnt[k].data(), nl, base, c.lld, ncl, dk, 1 + l, s);
+        PR.end(s);
+      }
+      ::hlq::g_launches++;
+      k_pack_rows<<<blocks_for((int64_t)cc * nb * ncl), 256, 0, s>>>(
+          c.hr_send, cc, head_idx(sp_), base, c.lld, prow, nb, ncl, ncl);
+    }
+    // ---- X4: head rows of this part's columns, every process column with a non-empty part
+    PR.begin(HLQ_PROF_OTHER, s);
+    for (int q = 0; q < Q; ++q) {
+      int64_t co, ncl;
+      part_range(k, q, cyc_extent(ds.N, nb, Q, q), part, co, ncl);
+      if ((rc = col_allgather(ds, q, [](Ctx& c) { return c.hr_send; },
+                              [](Ctx& c) { return c.hr_recv; }, (int64_t)cc * nb * ncl, s, false)))
+        return rc;
+    }
+    PR.end(s);
+    // ---- E: Schur DGEMM / inter-domain TTMQR; growth
+    const int dk_dom = k % ds.D;
+    const int slot_k = (dk_dom % P) * cc + dk_dom / P;
+    for (auto& c : ds.ctx) {
+      const StepPlan& sp_ = c.plan[k];
+      DevWork w = wk(c, k);
+      const int64_t prow = std::max<int64_t>(0, c.mloc - (int64_t)sp_.li0 * nb);
+      int64_t co, ncl;
+      const int lc1 = part_range(k, c.q, c.nloc, part, co, ncl);
+      if (ncl <= 0) continue;
+      double* pk_ = c.pkgs[par];
+      const uint8_t* dk = w.dec + k;
+      double* base = c.A + ((int64_t)lc1 * nb + co) * c.lld + (int64_t)sp_.li0 * nb;
+      const int64_t ldh = (int64_t)S * nb;
+      ::hlq::g_launches++;
+      k_stack<<<blocks_for(ldh * ncl), 256, 0, s>>>(c.HR, c.hr_recv, S, nb, ncl);
+      const int64_t r0 = sp_.diag ? bk : 0;
+      if (known != HLQ_DEC_QR && prow - r0 > 0) {
+        PR.begin(HLQ_PROF_LU_UPDATE, s);
+        launch_dgemm(base + r0, c.lld, pk_ + r0, prow, c.HR + (int64_t)slot_k * nb, ldh, prow - r0,
+                     ncl, bk, true, true, dk, 0, HLQ_DEC_LU, s);
+        PR.end(s);
+      }
+      if (known != HLQ_DEC_LU) {
+        PR.begin(HLQ_PROF_QR_UNMQR, s);
+        Geo gH{};
+        gH.N = ldh;
+        gH.lda = ldh;
+        gH.nb = nb;
+        gH.n = S;
+        gH.Nc = bk;
+        const int nl = (int)c.inter_ptr[k].size();
+        double* HM = pk_ + ds.off_HM(prow, sp_.ms);
+        double* MT = pk_ + ds.off_MT(prow, sp_.ms);
+        for (int l = 0; l < nl; ++l)
+          launch_qr_update_dmma(HM, gH, 0, ib, nullptr, MT, c.inter_ptr[k].data(),
+                                c.inter_cnt[k].data(), nl, c.HR, ldh, ncl, dk, 1 + l, s);
+        if (prow > 0 && nl > 0) {
+          ::hlq::g_launches++;
+          k_unstack_rows<<<blocks_for((int64_t)cc * nb * ncl), 256, 0, s>>>(
+              base, c.lld, prow, cc, head_idx(sp_), c.p * cc, c.HR, ldh, nb, ncl, 0, dk, HLQ_DEC_QR);
+        }
+        PR.end(s);
+      }
+      if (opt.track_growth && k + 1 < n && prow - r0 > 0) {
+        PR.begin(HLQ_PROF_GROWTH, s);
+        Geo gT{};
+        gT.N = prow - r0;
+        gT.Nc = c.nloc;
+        gT.lda = c.lld;
+        gT.nb = nb;
+        gT.n = sp_.ms - sp_.diag;
+        const int64_t cb = (int64_t)lc1 * nb + co;
+        launch_tile_norm_max(c.A + (int64_t)sp_.li0 * nb + r0, gT, 0, w.gstep + k + 1, s, nullptr,
+                             0, 0, cb, cb + ncl);
+        PR.end(s);
+      }
+    }
+    return cuda_check(cudaGetLastError());
+  };
+
+  // ======================================== driver
   int rc = 0;
   // a12 at k = 0: max tile norm of every local tile
   if (opt.track_growth)
@@ -780,275 +1108,20 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
       g.n = c.mt;
       launch_tile_norm_max(c.A, g, 0, c.w.gstep, st, nullptr, 0, 0, 0, c.nloc);
     }
+  cudaEventRecord(ds.ev_part0, st);
+  cudaStreamWaitEvent(sp, ds.ev_part0, 0);
+  if ((rc = panel(0, sp))) return rc;
+  cudaEventRecord(ds.ev_panel, sp);
   for (int k = 0; k < n; ++k) {
-    const int pk = k % P, qk = k % Q, lk = k / Q;
-    const int bk = (int)std::min<int64_t>(nb, ds.N - (int64_t)k * nb);
-    const int known = known_of(k);
-    // ---- A: statistics, speculative GETRF on the owner
-    for (auto& c : ds.ctx) {
-      if (c.q != qk) continue;
-      const StepPlan& sp = c.plan[k];
-      double* Apan = c.A + (int64_t)lk * nb * c.lld + (int64_t)sp.li0 * nb;
-      Geo gP = panel_geo(ds, c, sp, c.lld);
-      gP.Nc = bk;
-      PR.begin(HLQ_PROF_CRITERION, st);
-      cudaMemsetAsync(c.rec_send, 0, sizeof(double) * ds.rec_count, st);
-      if (sp.ms > 0 && criterion_needed)
-        launch_panel_stats_to(Apan, gP, 0, sp.diag, c.rec_send, c.rec_send + ds.ms_max + nb,
-                              c.rec_send + ds.ms_max, st);
-      PR.end(st);
-      if (sp.diag) {
-        PR.begin(HLQ_PROF_GETRF, st);
-        cudaMemsetAsync(c.w.zp, 0, sizeof(int), st);
-        cudaMemsetAsync(c.w.inv_norm, 0, sizeof(double), st);
-        if (known != HLQ_DEC_QR) {
-          launch_getrf(Apan, gP, 0, c.w, true, st);
-          launch_tri_inv(gP, 0, c.w, c.w.scratch, c.w.scratch + (size_t)nb * nb, st);
-          if (criterion_needed && crit != HLQ_CRIT_MUMPS) launch_invnorm(gP, 0, c.w, st);
-        }
-        ::hlq::g_launches++;
-        k_pack_owner<<<16, 256, 0, st>>>(c.rec_send + ds.ms_max + 2 * nb, c.w.inv_norm, c.w.zp,
-                                         c.w.W, c.w.ipiv_ws, nb, bk);
-        PR.end(st);
-      }
+    cudaStreamWaitEvent(st, ds.ev_panel, 0);
+    if ((rc = update(k, 0, st))) return rc;
+    if (k + 1 < n) {
+      cudaEventRecord(ds.ev_part0, st);
+      cudaStreamWaitEvent(sp, ds.ev_part0, 0);
+      if ((rc = panel(k + 1, sp))) return rc;
+      cudaEventRecord(ds.ev_panel, sp);
     }
-    PR.begin(HLQ_PROF_OTHER, st);
-    if ((rc = col_allgather(ds, qk, [](Ctx& c) { return c.rec_send; },
-                            [](Ctx& c) { return c.rec_recv; }, ds.rec_count)))
-      return rc;
-    PR.end(st);
-    // ---- B: decision, LU panel / QR panel + intra-domain tree
-    for (auto& c : ds.ctx) {
-      if (c.q != qk) continue;
-      const StepPlan& sp = c.plan[k];
-      double* Apan = c.A + (int64_t)lk * nb * c.lld + (int64_t)sp.li0 * nb;
-      Geo gP = panel_geo(ds, c, sp, c.lld);
-      gP.Nc = bk;
-      const uint8_t* dk = c.w.dec + k;
-      PR.begin(HLQ_PROF_CRITERION, st);
-      ::hlq::g_launches++;
-      k_unpack_stats<<<16, 256, 0, st>>>(c.rec_recv, ds.rec_count, ds.ms_max, k, n, P, pk, nb, bk,
-                                         c.w.s, c.w.away_max, c.w.local_max, c.w.inv_norm, c.w.zp,
-                                         c.w.W, c.w.ipiv_ws);
-      launch_decide(gglob, k, crit, alpha, opt.mumps_reading, opt.tie_rel_tol, has_forced ? 1 : 0,
-                    has_ref ? 1 : 0, c.w, st);
-      PR.end(st);
-      double* Li = c.w.scratch;
-      double* Ui = c.w.scratch + (size_t)nb * nb;
-      int* perm = reinterpret_cast<int*>(c.w.scratch + (size_t)2 * nb * nb);
-      if (known != HLQ_DEC_QR) {
-        PR.begin(HLQ_PROF_LU_TRSM, st);
-        if (!sp.diag) launch_tri_inv(gglob, k, c.w, Li, Ui, st);
-        if (sp.diag) launch_lu_commit(Apan, gP, 0, c.w.W, c.w.ipiv_ws, c.ipiv + (int64_t)k * nb,
-                                      perm, dk, st);
-        const int64_t r0 = sp.diag ? bk : 0;
-        const int64_t M = gP.N - r0;
-        if (M > 0) {
-          launch_copy_block(c.w.ws_panel, M, Apan + r0, c.lld, M, bk, nullptr, dk, 0, st);
-          launch_dgemm(Apan + r0, c.lld, c.w.ws_panel, M, Ui, nb, M, bk, bk, false, false, dk, 0,
-                       HLQ_DEC_LU, st);
-        }
-        PR.end(st);
-      }
-      if (known != HLQ_DEC_LU && sp.ms > 0) {
-        PR.begin(HLQ_PROF_QR_GEQRT, st);
-        double* Tgk = c.Tg + ((int64_t)lk * c.mt + sp.li0) * ib * nb;
-        double* Ttk = c.Ttt + ((int64_t)lk * c.mt + sp.li0) * ib * nb;
-        launch_qr_panel_tc(Apan, gP, 0, ib, Tgk, Ttk, nullptr, 0, dk, false, st);
-        for (size_t l = 0; l < c.intra_ptr[k].size(); ++l)
-          launch_qr_panel_tc(Apan, gP, 0, ib, Tgk, Ttk, c.intra_ptr[k][l], c.intra_cnt[k][l], dk,
-                             true, st);
-        PR.end(st);
-      }
-      ::hlq::g_launches++;
-      k_pack_rows<<<blocks_for((int64_t)cc * nb * nb), 256, 0, st>>>(
-          c.head_send, cc, head_idx(sp), Apan, c.lld, gP.N, nb, nb, bk);
-    }
-    PR.begin(HLQ_PROF_OTHER, st);
-    if ((rc = col_allgather(ds, qk, [](Ctx& c) { return c.head_send; },
-                            [](Ctx& c) { return c.head_recv; }, (int64_t)cc * nb * nb)))
-      return rc;
-    PR.end(st);
-    // ---- C: inter-domain merges (redundant on the column), package
-    for (auto& c : ds.ctx) {
-      if (c.q != qk) continue;
-      const StepPlan& sp = c.plan[k];
-      double* Apan = c.A + (int64_t)lk * nb * c.lld + (int64_t)sp.li0 * nb;
-      Geo gP = panel_geo(ds, c, sp, c.lld);
-      gP.Nc = bk;
-      const uint8_t* dk = c.w.dec + k;
-      const int64_t prow = gP.N;
-      double* pk_ = c.pkg;
-      double* HM = pk_ + ds.off_HM(prow, sp.ms);
-      double* MT = pk_ + ds.off_MT(prow, sp.ms);
-      Geo gH{};
-      gH.N = (int64_t)S * nb;
-      gH.lda = (int64_t)S * nb;
-      gH.nb = nb;
-      gH.n = S;
-      gH.Nc = bk;
-      ::hlq::g_launches++;
-      k_stack<<<blocks_for((int64_t)S * nb * nb), 256, 0, st>>>(HM, c.head_recv, S, nb, nb);
-      PR.begin(HLQ_PROF_QR_GEQRT, st);
-      if (known != HLQ_DEC_LU) {
-        for (size_t l = 0; l < c.inter_ptr[k].size(); ++l)
-          launch_qr_panel_tc(HM, gH, 0, ib, nullptr, MT, c.inter_ptr[k][l], c.inter_cnt[k][l], dk,
-                             true, st);
-        // own heads: R / TT-reflector triangles back into A, merge T factors into the local store
-        ::hlq::g_launches++;
-        k_unstack_rows<<<blocks_for((int64_t)cc * nb * nb), 256, 0, st>>>(
-            Apan, c.lld, prow, cc, head_idx(sp), c.p * cc, HM, (int64_t)S * nb, nb, bk, 1, dk,
-            HLQ_DEC_QR);
-        for (int t = 0; t < cc; ++t) {
-          const int hl = sp.head_local[t], hg = sp.head_global[t];
-          if (hl < 0 || hg == k) continue;
-          ::hlq::g_launches++;
-          k_copy_vec<<<8, 256, 0, st>>>(c.Ttt + ((int64_t)lk * c.mt + sp.li0 + hl) * ib * nb,
-                                        MT + (int64_t)(c.p * cc + t) * ib * nb, (int64_t)ib * nb,
-                                        dk, HLQ_DEC_QR);
-        }
-        // the solve replays the merges: keep HM + MT of this step
-        double* ms_ = c.mstore + (int64_t)lk * ds.mstore_stride();
-        cudaMemcpyAsync(ms_, HM, sizeof(double) * ds.mstore_stride(), cudaMemcpyDeviceToDevice, st);
-      }
-      // package: panel tiles, T factors, (HM, MT already in place), L^-1, perm, d_k
-      if (prow > 0)
-        cudaMemcpy2DAsync(pk_, sizeof(double) * prow, Apan, sizeof(double) * c.lld,
-                          sizeof(double) * prow, bk, cudaMemcpyDeviceToDevice, st);
-      if (sp.ms > 0) {
-        cudaMemcpyAsync(pk_ + ds.off_Tg(prow), c.Tg + ((int64_t)lk * c.mt + sp.li0) * ib * nb,
-                        sizeof(double) * sp.ms * ib * nb, cudaMemcpyDeviceToDevice, st);
-        cudaMemcpyAsync(pk_ + ds.off_Ttt(prow, sp.ms),
-                        c.Ttt + ((int64_t)lk * c.mt + sp.li0) * ib * nb,
-                        sizeof(double) * sp.ms * ib * nb, cudaMemcpyDeviceToDevice, st);
-      }
-      cudaMemcpyAsync(pk_ + ds.off_Li(prow, sp.ms), c.w.scratch, sizeof(double) * nb * nb,
-                      cudaMemcpyDeviceToDevice, st);
-      ::hlq::g_launches++;
-      k_meta_pack<<<1, 256, 0, st>>>(pk_ + ds.off_meta(prow, sp.ms), c.w.dec, c.w.margin,
-                                     c.w.flags,
-                                     reinterpret_cast<int*>(c.w.scratch + (size_t)2 * nb * nb), bk,
-                                     k, nb);
-      PR.end(st);
-    }
-    auto pcount = [&](int p) {
-      int64_t cnt[4];
-      step_counts(ds.N, nb, P, Q, ds.D, ib, p, 0, k, cnt);
-      return cnt[2];
-    };
-    PR.begin(HLQ_PROF_OTHER, st);
-    if ((rc = row_bcast(ds, qk, [](Ctx& c) { return c.pkg; }, pcount))) return rc;
-    PR.end(st);
-    // ---- D: SWPTRSM / UNMQR + intra TTMQR, then pack the head rows
-    for (auto& c : ds.ctx) {
-      const StepPlan& sp = c.plan[k];
-      const int64_t prow = std::max<int64_t>(0, c.mloc - (int64_t)sp.li0 * nb);
-      double* pk_ = c.pkg;
-      const uint8_t* dk = c.w.dec + k;
-      int* perm = reinterpret_cast<int*>(c.w.scratch + (size_t)2 * nb * nb);
-      ::hlq::g_launches++;
-      k_meta_unpack<<<1, 256, 0, st>>>(pk_ + ds.off_meta(prow, sp.ms), c.w.dec, c.w.margin,
-                                       c.w.flags, perm, bk, k);
-      const int lc1 = cyc_below(k + 1, Q, c.q);
-      const int64_t ncl = std::max<int64_t>(0, c.nloc - (int64_t)lc1 * nb);
-      if (ncl <= 0 || prow <= 0) continue;
-      double* base = c.A + (int64_t)lc1 * nb * c.lld + (int64_t)sp.li0 * nb;
-      Geo gK{};
-      gK.N = prow;
-      gK.lda = prow;
-      gK.nb = nb;
-      gK.n = sp.ms;
-      gK.Nc = bk;
-      if (known != HLQ_DEC_QR && sp.diag) {
-        PR.begin(HLQ_PROF_LU_UPDATE, st);
-        launch_copy_block(c.w.ws_row, bk, base, c.lld, bk, ncl, perm, dk, 0, st);
-        launch_dgemm(base, c.lld, pk_ + ds.off_Li(prow, sp.ms), nb, c.w.ws_row, bk, bk, ncl, bk,
-                     false, false, dk, 0, HLQ_DEC_LU, st);
-        PR.end(st);
-      }
-      if (known != HLQ_DEC_LU && sp.ms > 0) {
-        PR.begin(HLQ_PROF_QR_UNMQR, st);
-        const int nl = (int)c.intra_ptr[k].size();
-        launch_qr_update_dmma(pk_, gK, 0, ib, pk_ + ds.off_Tg(prow), pk_ + ds.off_Ttt(prow, sp.ms),
-                              c.intra_ptr[k].data(), c.intra_cnt[k].data(), nl, base, c.lld, ncl,
-                              dk, 0, st);
-        for (int l = 0; l < nl; ++l)
-          launch_qr_update_dmma(pk_, gK, 0, ib, pk_ + ds.off_Tg(prow),
-                                pk_ + ds.off_Ttt(prow, sp.ms), c.intra_ptr[k].data(),
-                                c.intra_cnt[k].data(), nl, base, c.lld, ncl, dk, 1 + l, st);
-        PR.end(st);
-      }
-      ::hlq::g_launches++;
-      k_pack_rows<<<blocks_for((int64_t)cc * nb * ncl), 256, 0, st>>>(
-          c.hr_send, cc, head_idx(sp), base, c.lld, prow, nb, ncl, ncl);
-    }
-    PR.begin(HLQ_PROF_OTHER, st);
-    for (int q = 0; q < Q; ++q) {
-      int64_t cnt[4];
-      step_counts(ds.N, nb, P, Q, ds.D, ib, 0, q, k, cnt);
-      if ((rc = col_allgather(ds, q, [](Ctx& c) { return c.hr_send; },
-                              [](Ctx& c) { return c.hr_recv; }, cnt[3])))
-        return rc;
-    }
-    PR.end(st);
-    // ---- E: Schur DGEMM / inter-domain TTMQR; growth
-    const int dk_dom = k % ds.D;
-    const int slot_k = (dk_dom % P) * cc + dk_dom / P;
-    for (auto& c : ds.ctx) {
-      const StepPlan& sp = c.plan[k];
-      const int64_t prow = std::max<int64_t>(0, c.mloc - (int64_t)sp.li0 * nb);
-      const int lc1 = cyc_below(k + 1, Q, c.q);
-      const int64_t ncl = std::max<int64_t>(0, c.nloc - (int64_t)lc1 * nb);
-      if (ncl <= 0) continue;
-      double* pk_ = c.pkg;
-      const uint8_t* dk = c.w.dec + k;
-      double* base = c.A + (int64_t)lc1 * nb * c.lld + (int64_t)sp.li0 * nb;
-      const int64_t ldh = (int64_t)S * nb;
-      ::hlq::g_launches++;
-      k_stack<<<blocks_for(ldh * ncl), 256, 0, st>>>(c.HR, c.hr_recv, S, nb, ncl);
-      const int64_t r0 = sp.diag ? bk : 0;
-      if (known != HLQ_DEC_QR && prow - r0 > 0) {
-        PR.begin(HLQ_PROF_LU_UPDATE, st);
-        launch_dgemm(base + r0, c.lld, pk_ + r0, prow, c.HR + (int64_t)slot_k * nb, ldh,
-                     prow - r0, ncl, bk, true, true, dk, 0, HLQ_DEC_LU, st);
-        PR.end(st);
-      }
-      if (known != HLQ_DEC_LU) {
-        PR.begin(HLQ_PROF_QR_UNMQR, st);
-        Geo gH{};
-        gH.N = ldh;
-        gH.lda = ldh;
-        gH.nb = nb;
-        gH.n = S;
-        gH.Nc = bk;
-        const int nl = (int)c.inter_ptr[k].size();
-        double* HM = pk_ + ds.off_HM(prow, sp.ms);
-        double* MT = pk_ + ds.off_MT(prow, sp.ms);
-        for (int l = 0; l < nl; ++l)
-          launch_qr_update_dmma(HM, gH, 0, ib, nullptr, MT, c.inter_ptr[k].data(),
-                                c.inter_cnt[k].data(), nl, c.HR, ldh, ncl, dk, 1 + l, st);
-        if (prow > 0 && nl > 0) {
-          ::hlq::g_launches++;
-          k_unstack_rows<<<blocks_for((int64_t)cc * nb * ncl), 256, 0, st>>>(
-              base, c.lld, prow, cc, head_idx(sp), c.p * cc, c.HR, ldh, nb, ncl, 0, dk,
-              HLQ_DEC_QR);
-        }
-        PR.end(st);
-      }
-      if (opt.track_growth && k + 1 < n && prow - r0 > 0) {
-        PR.begin(HLQ_PROF_GROWTH, st);
-        Geo gT{};
-        gT.N = prow - r0;
-        gT.Nc = c.nloc;
-        gT.lda = c.lld;
-        gT.nb = nb;
-        gT.n = sp.ms - sp.diag;
-        launch_tile_norm_max(c.A + (int64_t)sp.li0 * nb + r0, gT, 0, c.w.gstep + k + 1, st,
-                             nullptr, 0, 0, (int64_t)lc1 * nb, c.nloc);
-        PR.end(st);
-      }
-    }
-    if ((rc = cuda_check(cudaGetLastError()))) return rc;
+    if ((rc = update(k, 1, st))) return rc;
   }
   // final scan + reductions
   for (auto& c : ds.ctx) {
@@ -1131,7 +1204,7 @@ static int dist_solve(DistState& ds, const std::vector<uint8_t>& dec, const doub
                                                                   nb, 1, 1);
       }
       if ((rc = col_allgather(ds, qk, [](Ctx& c) { return c.hx_send; },
-                              [](Ctx& c) { return c.hx_recv; }, (int64_t)cc * nb)))
+                              [](Ctx& c) { return c.hx_recv; }, (int64_t)cc * nb, st, false)))
         return rc;
       for (auto& c : ds.ctx) {
         if (c.q != qk) continue;
@@ -1154,7 +1227,7 @@ static int dist_solve(DistState& ds, const std::vector<uint8_t>& dec, const doub
         }
       }
     }
-    if ((rc = row_bcast(ds, qk, [](Ctx& c) { return c.xseg; }, seg_count))) return rc;
+    if ((rc = row_bcast(ds, qk, [](Ctx& c) { return c.xseg; }, seg_count, st))) return rc;
   }
   for (int k = n - 1; k >= 0; --k) {
     const int pk = k % P, qk = k % Q, lk = k / Q;
@@ -1176,12 +1249,12 @@ static int dist_solve(DistState& ds, const std::vector<uint8_t>& dec, const doub
       launch_gemv_sub(c.xseg, c.A + (int64_t)lk * nb * c.lld, c.lld, (int64_t)sp.li0 * nb, bk,
                       c.xk, st);
     }
-    if ((rc = row_bcast(ds, qk, [](Ctx& c) { return c.xseg; }, seg_count))) return rc;
+    if ((rc = row_bcast(ds, qk, [](Ctx& c) { return c.xseg; }, seg_count, st))) return rc;
   }
   // full x on every rank: allgather of the segments in each process column
   for (int q = 0; q < Q; ++q)
     if ((rc = col_allgather(ds, q, [](Ctx& c) { return c.xseg; }, [](Ctx& c) { return c.xg; },
-                            ds.seg_cap)))
+                            ds.seg_cap, st, false)))
       return rc;
   Ctx& c0 = ds.ctx[0];
   ::hlq::g_launches++;
@@ -1236,6 +1309,7 @@ int hlq_grid_create_nccl(const void* id128, int32_t nranks, int32_t rank, int32_
   const int p = rank / Q, q = rank % Q;
   if (!rc) rc = nccl_err(g_nccl.CommSplit(g->world, p, q, &g->row, nullptr), "CommSplit(row)");
   if (!rc) rc = nccl_err(g_nccl.CommSplit(g->world, q, p, &g->col, nullptr), "CommSplit(col)");
+  if (!rc) rc = nccl_err(g_nccl.CommSplit(g->world, q, p, &g->colp, nullptr), "CommSplit(colp)");
   if (rc) {
     hlq_grid_free(g);
     return rc;
@@ -1262,6 +1336,7 @@ void hlq_grid_free(hlq_grid_t g) {
   if (!g) return;
   if (g->row) g_nccl.CommDestroy(g->row);
   if (g->col) g_nccl.CommDestroy(g->col);
+  if (g->colp) g_nccl.CommDestroy(g->colp);
   if (g->world) g_nccl.CommDestroy(g->world);
   delete g;
 }
@@ -1513,6 +1588,13 @@ int hlq_factor_dist(hlq_grid_t grid, double* const* A_local, const int64_t* lld,
   ds->n = n;
   ds->N = N;
   ds->st = f->st;
+  {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&ds->sp, cudaStreamNonBlocking, hi);
+    cudaEventCreateWithFlags(&ds->ev_part0, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ds->ev_panel, cudaEventDisableTiming);
+  }
   ds->ms_max = cyc_count(n, P, 0);
   ds->mt_max = ds->ms_max;
   ds->rec_count = ds->ms_max + 3 * (int64_t)nb + 2 + (int64_t)nb * nb;
