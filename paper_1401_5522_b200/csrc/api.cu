@@ -242,7 +242,9 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
          oPr = take(sizeof(int2) * (npairs + 1)), oSc0 = take(sizeof(double) * scr),
          oSc1 = take(sizeof(double) * scr), oWp = take(sizeof(double) * (size_t)N * nb),
          oWr = take(sizeof(double) * (size_t)N * nb),
-         oCp = take(fuse_growth_any ? sizeof(double) * (size_t)((N + 127) / 128) * N : 8);
+         oCp = take(fuse_growth_any ? sizeof(double) * (size_t)((N + 127) / 128) * N : 8),
+         oLi = take(sizeof(double) * (size_t)n * 2 * nb * nb),
+         oLp = take(sizeof(int) * (size_t)n * nb), oSt2 = take(sizeof(double) * (size_t)nb);
   f->ws_bytes = off;
   f->ws_block = cache_get(0, off);
   if (!f->ws_block) return HLQ_ERR_NOMEM;
@@ -271,6 +273,9 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   w.ws_panel = (double*)(base + oWp);
   w.ws_row = (double*)(base + oWr);
   w.colpart = fuse_growth_any ? (double*)(base + oCp) : nullptr;
+  w.luinv = (double*)(base + oLi);
+  w.luperm = (int*)(base + oLp);
+  w.solve_t = (double*)(base + oSt2);
   // per-parity views (lookahead: step k+1's panel runs while step k's update still reads step k's
   // W / ipiv / L^-1 / U^-1 / perm)
   DevWork wpar[2] = {w, w};
@@ -356,6 +361,12 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
     if (known != HLQ_DEC_QR) {
       P.begin(HLQ_PROF_LU_TRSM, sp);
       launch_lu_panel(A, g, k, wk, sp);
+      // keep L_kk^-1, U_kk^-1 and the composed permutation for the solve (LU steps only)
+      launch_copy_block(w.luinv + (size_t)k * 2 * nb * nb, nb, wk.scratch, nb, nb, 2 * nb, nullptr,
+                        w.dec, k, sp);
+      launch_copy_ints(w.luperm + (size_t)k * nb,
+                       reinterpret_cast<const int*>(wk.scratch + (size_t)2 * nb * nb), nb, w.dec, k,
+                       sp);
       P.end(sp);
     }
     if (known != HLQ_DEC_LU) {
@@ -461,12 +472,19 @@ int hlq_solve(hlq_factors_t f, const double* b, double* x) {
     return rc;
   for (int k = 0; k < g.n; ++k) {
     if (f->dec[k] == HLQ_DEC_LU)
-      launch_solve_lu_fwd(f->A, g, k, f->w.ipiv, x, st);
+      launch_solve_lu_fwd_inv(f->A, g, k, f->w.luinv + (size_t)k * 2 * g.nb * g.nb,
+                              f->w.luperm + (size_t)k * g.nb, x, f->w.solve_t, st);
     else
       launch_qr_apply(f->A, g, k, f->ib, f->w.Tg, f->w.Ttt, f->lvl_ptr[k].data(),
                       f->lvl_cnt[k].data(), (int)f->lvl_cnt[k].size(), x, g.N, 1, nullptr, st);
   }
-  for (int k = g.n - 1; k >= 0; --k) launch_solve_back(f->A, g, k, x, st);
+  for (int k = g.n - 1; k >= 0; --k) {
+    if (f->dec[k] == HLQ_DEC_LU)
+      launch_solve_back_inv(f->A, g, k, f->w.luinv + ((size_t)k * 2 + 1) * g.nb * g.nb, x,
+                            f->w.solve_t, st);
+    else
+      launch_solve_back(f->A, g, k, x, st);
+  }
   f->prof.end(st);
   if ((rc = cuda_err(cudaGetLastError()))) return rc;
   if (f->blocking && (rc = cuda_err(cudaStreamSynchronize(st)))) return rc;

@@ -61,6 +61,9 @@ struct DevWork {
   double* ws_panel;   // N*nb: panel copy for the TRSM (panel stream)
   double* ws_row;     // N*nb: row-block copy for the SWPTRSM (update stream)
   double* colpart;    // fused growth partials (ceil(N/128) x N) or null
+  double* luinv;      // per LU step k: L_kk^-1 | U_kk^-1 (2 nb*nb, ld nb) for the solve, or null
+  int* luperm;        // per LU step k: composed row permutation of P_kk (nb ints), or null
+  double* solve_t;    // nb scratch doubles for the solve
 };
 
 // ---- kernels-side launch helpers (defined in the .cu files) ---------------------------------
@@ -74,6 +77,8 @@ void launch_lu_commit(double* A, Geo g, int k, const double* W, const int* ipiv_
                       int* perm, const uint8_t* dec, cudaStream_t st);
 void launch_copy_block(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
                        int64_t cols, const int* perm, const uint8_t* dec, int k, cudaStream_t st);
+// dst[0:n) = src[0:n) (ints) when dec[k] == LU
+void launch_copy_ints(int* dst, const int* src, int n, const uint8_t* dec, int k, cudaStream_t st);
 void launch_dgemm(double* C, int64_t ldc, const double* A, int64_t lda, const double* B,
                   int64_t ldb, int64_t M, int64_t N, int K, bool neg, bool beta,
                   const uint8_t* dec, int k, int want, cudaStream_t st,
@@ -120,6 +125,12 @@ void launch_solve_qr_fwd(const double* A, Geo g, int k, int ib, const double* Tg
                          const double* Ttt, const int2* const* level_pairs, const int* level_count,
                          int nlevels, double* x, cudaStream_t st);
 void launch_solve_back(const double* A, Geo g, int k, double* x, cudaStream_t st);
+// LU steps with the stored explicit inverses: x_k <- L_kk^-1 P x_k, rows below -= L_ik x_k
+void launch_solve_lu_fwd_inv(const double* A, Geo g, int k, const double* Li, const int* perm,
+                             double* x, double* t, cudaStream_t st);
+// back substitution of an LU step: x_k <- U_kk^-1 x_k, rows above -= A_ik x_k
+void launch_solve_back_inv(const double* A, Geo g, int k, const double* Ui, double* x, double* t,
+                           cudaStream_t st);
 void launch_residual(const double* A, int64_t N, int64_t lda, const double* x, const double* b,
                      double* out3dev, cudaStream_t st);
 

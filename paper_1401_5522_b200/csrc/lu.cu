@@ -70,6 +70,18 @@ void launch_copy_block(double* dst, int64_t ldd, const double* src, int64_t lds,
   k_copy_block<<<grid_for(rows * cols), 256, 0, st>>>(dst, ldd, src, lds, rows, cols, perm, dec, k);
 }
 
+__global__ void k_copy_ints(int* __restrict__ dst, const int* __restrict__ src, int n,
+                            const uint8_t* __restrict__ dec, int k) {
+  if (dec != nullptr && dec[k] != HLQ_DEC_LU) return;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) dst[t] = src[t];
+}
+
+void launch_copy_ints(int* dst, const int* src, int n, const uint8_t* dec, int k, cudaStream_t st) {
+  if (n <= 0) return;
+  ::hlq::g_launches++;
+  k_copy_ints<<<1, 256, 0, st>>>(dst, src, n, dec, k);
+}
+
 // Panel stage of an LU step (column block k only): Factor (commit W, ipiv) + Eliminate (TRSM).
 void launch_lu_panel(double* A, Geo g, int k, const DevWork& w, cudaStream_t st) {
   const int bk = g.bs(k);

@@ -395,6 +395,86 @@ __global__ void __launch_bounds__(QT) k_ttmqr(const double* __restrict__ A, Geo 
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// The solve's Q^T x (one column): every reflector block read once straight from global memory
+// (coalesced down the columns), the vector segment in shared memory; one CTA per tile row (UNMQR)
+// or per TT pair.  Per block b: W = [x_e(b) +] V_b^T x, U = T_b^T W, x -= V_b U [x_e(b) -= U].
+// Dot products: warp w takes reflectors 4w..4w+3, lanes stride the rows, warp-shuffle reduction.
+template <bool TT>
+__global__ void __launch_bounds__(256) k_qr_apply_vec(const double* __restrict__ A, Geo g, int k,
+                                                      int ib, const double* __restrict__ Tb,
+                                                      const int2* __restrict__ pairs,
+                                                      double* __restrict__ x) {
+  __shared__ double xs[512];
+  __shared__ double xe[32];
+  __shared__ double Wv[32], Uv[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int e = 0, i;
+  if (TT) {
+    const int2 pr = pairs[blockIdx.x];
+    e = pr.x;
+    i = pr.y;
+  } else {
+    i = k + blockIdx.x;
+  }
+  const int bi = g.bs(i), bk = g.cbs(k);
+  const double* V = g.tile(const_cast<double*>(A), i, k);
+  const double* T = Tb + tri_index(i, k, g.n) * (int64_t)ib * g.nb;
+  double* xi = x + g.r0(i);
+  for (int r = tid; r < bi; r += 256) xs[r] = xi[r];
+  __syncthreads();
+  for (int i0 = 0; i0 < bk; i0 += ib) {
+    const int sb = min(ib, bk - i0);
+    if (!TT && i0 >= bi) break;
+    if (TT && tid < sb) xe[tid] = x[g.r0(e) + i0 + tid];
+    // W
+    for (int l = warp; l < sb; l += 8) {
+      const double* v = V + (int64_t)(i0 + l) * g.lda;
+      double p = 0.0;
+      if (TT) {
+        const int rhi = min(bi, i0 + l + 1);
+        for (int r = lane; r < rhi; r += 32) p += v[r] * xs[r];
+      } else {
+        for (int r = i0 + l + 1 + lane; r < bi; r += 32) p += v[r] * xs[r];
+      }
+      p = wsum(p);
+      if (lane == 0) Wv[l] = p;
+    }
+    __syncthreads();
+    if (tid < sb) {
+      const double w0 = TT ? xe[tid] : (i0 + tid < bi ? xs[i0 + tid] : 0.0);
+      Wv[tid] += w0;
+    }
+    __syncthreads();
+    // U = T^T W (T(q, l) at T[(i0 + l) * ib + q], upper triangular)
+    if (tid < sb) {
+      double u = 0.0;
+      for (int q = 0; q <= tid; ++q) u += T[(int64_t)(i0 + tid) * ib + q] * Wv[q];
+      Uv[tid] = u;
+    }
+    __syncthreads();
+    // x -= V U
+    if (TT) {
+      for (int r = tid; r < min(bi, i0 + sb); r += 256) {
+        double acc = 0.0;
+        for (int l = (r > i0 ? r - i0 : 0); l < sb; ++l) acc += V[(int64_t)(i0 + l) * g.lda + r] * Uv[l];
+        xs[r] -= acc;
+      }
+      if (tid < sb) x[g.r0(e) + i0 + tid] = xe[tid] - Uv[tid];
+    } else {
+      for (int r = i0 + tid; r < bi; r += 256) {
+        const int lmax = min(r - i0, sb - 1);
+        double acc = 0.0;
+        for (int l = 0; l <= lmax; ++l)
+          acc += ((i0 + l == r) ? 1.0 : V[(int64_t)(i0 + l) * g.lda + r]) * Uv[l];
+        xs[r] -= acc;
+      }
+    }
+    __syncthreads();
+  }
+  for (int r = tid; r < bi; r += 256) xi[r] = xs[r];
+}
+
 static void set_attr_once() {
   static bool done = false;
   if (done) return;
@@ -414,6 +494,12 @@ void launch_qr_apply(const double* A, Geo g, int k, int ib, const double* Tg, co
   set_attr_once();
   size_t smem = qr_smem_bytes(g.nb);
   if (ncols <= 0) return;
+  if (ncols == 1 && dec == nullptr && g.nb <= 512) {
+    { ::hlq::g_launches++; k_qr_apply_vec<false><<<g.n - k, 256, 0, st>>>(A, g, k, ib, Tg, nullptr, base); }
+    for (int l = 0; l < nlevels; ++l)
+      { ::hlq::g_launches++; k_qr_apply_vec<true><<<level_count[l], 256, 0, st>>>(A, g, k, ib, Ttt, level_pairs[l], base); }
+    return;
+  }
   unsigned slabs = (unsigned)((ncols + 63) / 64);
   { ::hlq::g_launches++; k_unmqr<<<dim3(slabs, g.n - k), QT, smem, st>>>(A, g, k, ib, Tg, base, ldc, ncols, dec); }
   for (int l = 0; l < nlevels; ++l)
@@ -428,6 +514,11 @@ void launch_tt_apply(const double* A, Geo g, int k, int ib, const double* Ttt,
   set_attr_once();
   size_t smem = qr_smem_bytes(g.nb);
   if (ncols <= 0) return;
+  if (ncols == 1 && dec == nullptr && g.nb <= 512) {
+    for (int l = 0; l < nlevels; ++l)
+      { ::hlq::g_launches++; k_qr_apply_vec<true><<<level_count[l], 256, 0, st>>>(A, g, k, ib, Ttt, level_pairs[l], base); }
+    return;
+  }
   unsigned slabs = (unsigned)((ncols + 63) / 64);
   for (int l = 0; l < nlevels; ++l)
     { ::hlq::g_launches++; k_ttmqr<<<dim3(slabs, level_count[l]), QT, smem, st>>>(A, g, k, ib, Ttt, level_pairs[l], base,

@@ -157,6 +157,55 @@ void launch_solve_back(const double* A, Geo g, int k, double* x, cudaStream_t st
 }
 
 // ---------------------------------------------------------------------------------------------
+// LU steps with the explicit triangular inverses kept by the factorization (L_kk^-1, U_kk^-1 are
+// what Eliminate / Apply multiply by, Alg. 2): the diagonal solves become parallel GEMVs.
+// t[r] = sum_c M[c*ld + r] * v(c) over the triangle (lower: c <= r, upper: c >= r), v(c) = x_k[perm[c]]
+// or x_k[c]; one CTA per 32 rows, 8 warps splitting c, partials summed in a fixed order.
+template <bool LOWER>
+__global__ void __launch_bounds__(256) k_tri_gemv(const double* __restrict__ M, int ld, int bk,
+                                                  const int* __restrict__ perm,
+                                                  const double* __restrict__ xk,
+                                                  double* __restrict__ t) {
+  __shared__ double v[512];
+  __shared__ double part[8][33];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c = threadIdx.x; c < bk; c += 256) v[c] = xk[perm ? perm[c] : c];
+  __syncthreads();
+  const int r = blockIdx.x * 32 + lane;
+  double acc = 0.0;
+  if (r < bk) {
+    const int c0 = LOWER ? 0 : r, c1 = LOWER ? r + 1 : bk;
+    for (int c = c0 + ((warp - c0) % 8 + 8) % 8; c < c1; c += 8) acc += M[(int64_t)c * ld + r] * v[c];
+  }
+  part[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && r < bk) {
+    double s2 = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s2 += part[w][lane];
+    t[r] = s2;
+  }
+}
+
+void launch_solve_lu_fwd_inv(const double* A, Geo g, int k, const double* Li, const int* perm,
+                             double* x, double* t, cudaStream_t st) {
+  const int bk = g.bs(k);
+  const int64_t k0 = g.r0(k), k1 = k0 + bk;
+  { ::hlq::g_launches++; k_tri_gemv<true><<<(bk + 31) / 32, 256, 0, st>>>(Li, g.nb, bk, perm, x + k0, t); }
+  cudaMemcpyAsync(x + k0, t, sizeof(double) * bk, cudaMemcpyDeviceToDevice, st);
+  launch_gemv_sub(x + k1, A + k0 * g.lda + k1, g.lda, g.N - k1, bk, x + k0, st);
+}
+
+void launch_solve_back_inv(const double* A, Geo g, int k, const double* Ui, double* x, double* t,
+                           cudaStream_t st) {
+  const int bk = g.bs(k);
+  const int64_t k0 = g.r0(k);
+  { ::hlq::g_launches++; k_tri_gemv<false><<<(bk + 31) / 32, 256, 0, st>>>(Ui, g.nb, bk, nullptr, x + k0, t); }
+  cudaMemcpyAsync(x + k0, t, sizeof(double) * bk, cudaMemcpyDeviceToDevice, st);
+  launch_gemv_sub(x, A + k0 * g.lda, g.lda, k0, bk, x + k0, st);
+}
+
+// ---------------------------------------------------------------------------------------------
 // HPL3 pieces: out[0] = ||A x - b||_inf, out[1] = ||A||_inf, out[2] = ||x||_inf (atomic max >= 0)
 __global__ void k_residual(const double* __restrict__ A, int64_t N, int64_t lda,
                            const double* __restrict__ x, const double* __restrict__ b,
