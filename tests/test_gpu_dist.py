@@ -107,7 +107,8 @@ def test_grid_other_criteria(H, crit, alpha):
     check(fo, f, F, x, A, b)
 
 
-@pytest.mark.parametrize("N,nb,P,Q", [(100, 128, 2, 2), (300, 64, 2, 3), (129, 64, 2, 2)])
+@pytest.mark.parametrize("N,nb,P,Q", [(100, 128, 2, 2), (300, 64, 2, 3), (129, 64, 2, 2),
+                                      (1000, 320, 2, 2), (1000, 320, 1, 2)])
 def test_grid_degenerate_sizes(H, N, nb, P, Q):
     """n = 1 (ranks with empty local arrays), fewer tile rows than process rows, ragged 1-row tile."""
     A = I.uniform_matrix(0, N)

@@ -122,7 +122,15 @@ def test_mumps_m2_reading(H):
                                              (777, 64, O.CRIT_SUM, 1e5),
                                              (777, 64, O.CRIT_MUMPS, 2.0),
                                              (300, 320, O.CRIT_MAX, 1.0),
-                                             (65, 32, O.CRIT_MAX, 1e3)])
+                                             (65, 32, O.CRIT_MAX, 1e3),
+                                             # C5's nb = 320 with a ragged last tile (QR update
+                                             # kernel instantiation for nb = 320, 32-column tail)
+                                             (1000, 320, O.CRIT_MAX, 1.0),
+                                             (1000, 320, O.CRIT_MAX, 1.6e4),
+                                             # nb outside the register-slab instantiations (96):
+                                             # the shared-memory QR update path
+                                             (800, 96, O.CRIT_MAX, 1.0),
+                                             (1001, 192, O.CRIT_MAX, 1.0)])
 def test_ragged_and_degenerate_sizes(H, N, nb, crit, alpha):
     A = I.uniform_matrix(5, N)
     b = I.uniform_rhs(5, N)
