@@ -485,8 +485,14 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
       const int r = 8 * (RQ * j + rh) + 2 * tq;
-      cT[m][j][0] = (cok && r < crows) ? cp[r] : 0.0;
-      cT[m][j][1] = (cok && r + 1 < crows) ? cp[r + 1] : 0.0;
+      if (V16 && cok && r + 1 < crows) {  // 16-byte aligned pair (even ld, even row)
+        const double2 v = *reinterpret_cast<const double2*>(cp + r);
+        cT[m][j][0] = v.x;
+        cT[m][j][1] = v.y;
+      } else {
+        cT[m][j][0] = (cok && r < crows) ? cp[r] : 0.0;
+        cT[m][j][1] = (cok && r + 1 < crows) ? cp[r + 1] : 0.0;
+      }
     }
   }
 
@@ -741,8 +747,12 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
       const int r = 8 * (RQ * j + rh) + 2 * tq;
-      if (r < crows) cp[r] = cT[m][j][0];
-      if (r + 1 < crows) cp[r + 1] = cT[m][j][1];
+      if (V16 && r + 1 < crows) {
+        *reinterpret_cast<double2*>(cp + r) = make_double2(cT[m][j][0], cT[m][j][1]);
+      } else {
+        if (r < crows) cp[r] = cT[m][j][0];
+        if (r + 1 < crows) cp[r + 1] = cT[m][j][1];
+      }
     }
   }
 }
