@@ -118,6 +118,66 @@ def inv_norm1_from_lu(W: np.ndarray) -> float:
     return norm1(X)
 
 
+def inv_norm1_estimate(W: np.ndarray, itmax: int = 5) -> float:
+    """NEXT f3: ||A_kk^-1||_1 "approximated ... by an iterative method" -- the Hager /
+    Higham 1-norm estimator in the order of LAPACK dlacn2 (the estimator dgecon runs on the LU
+    factors), applied to B = U^-1 L^-1 (the column permutation P does not change a 1-norm).
+    A lower bound of the exact norm; usually equal.  Steps (dlacn2 labels):
+      x = e/n; y = B x; est = ||y||_1; xi = sign(y) (sign(0) = +1); z = B^T xi; j = first argmax|z|
+      loop (iter = 2..itmax): x = e_j; y = B x; est_old = est; est = ||y||_1
+        if sign(y) == xi: stop (repeated sign vector); if est <= est_old: stop (cycling)
+        xi = sign(y); z = B^T xi; j_last = j; j = first argmax |z|
+        continue while z[j_last] != |z[j]| and iter < itmax
+      final: x_i = (-1)^i (1 + i/(n-1)); t = 2 ||B x||_1 / (3n); est = max(est, t)
+    """
+    b = W.shape[0]
+    L = np.tril(W, -1) + np.eye(b)
+    U = np.triu(W)
+
+    def Bx(v):
+        with np.errstate(all="ignore"):
+            t = solve_triangular(L, v, lower=True, unit_diagonal=True, check_finite=False)
+            return solve_triangular(U, t, lower=False, check_finite=False)
+
+    def BTx(v):
+        with np.errstate(all="ignore"):
+            t = solve_triangular(U, v, lower=False, trans="T", check_finite=False)
+            return solve_triangular(L, t, lower=True, unit_diagonal=True, trans="T",
+                                    check_finite=False)
+
+    def sgn(v):
+        return np.where(v >= 0.0, 1.0, -1.0)
+
+    y = Bx(np.full(b, 1.0 / b))
+    if b == 1:
+        return float(abs(y[0]))
+    est = float(np.sum(np.abs(y)))
+    xi = sgn(y)
+    z = BTx(xi)
+    j = int(np.argmax(np.abs(z)))
+    it = 2
+    while True:
+        x = np.zeros(b)
+        x[j] = 1.0
+        y = Bx(x)
+        est_old = est
+        est = float(np.sum(np.abs(y)))
+        xs = sgn(y)
+        if np.array_equal(xs, xi) or est <= est_old:
+            break
+        xi = xs
+        z = BTx(xi)
+        j_last = j
+        j = int(np.argmax(np.abs(z)))
+        if z[j_last] != abs(z[j]) and it < itmax:
+            it += 1
+            continue
+        break
+    x = np.array([(1.0 if i % 2 == 0 else -1.0) * (1.0 + i / (b - 1)) for i in range(b)])
+    t = 2.0 * (float(np.sum(np.abs(Bx(x)))) / (3 * b))
+    return max(est, t)
+
+
 # ----------------------------------------------------------------------------------------------
 # a4: the criteria (Eq. 2 Max P:495, Eq. 3 Sum P:537, Eq. 4 MUMPS P:576-579) and the decision
 # ----------------------------------------------------------------------------------------------
@@ -514,9 +574,10 @@ class Factors:
 def hybrid_factor(A_in: np.ndarray, nb: int, crit: int = CRIT_MAX, alpha: float = 1.0, D: int = 1,
                   ib: int = 32, mumps_reading: int = 0, forced=None, track_growth: bool = True,
                   tie_tol: float = 1e-10, variant: int = 0, on_step=None,
-                  tree: str = "greedy") -> Factors:
+                  tree: str = "greedy", invnorm: str = "exact") -> Factors:
     """Alg. 1: for each step, speculative tile LU, criterion, LU or QR step.
 
+    invnorm: "exact" (ledger 3, default) or "estimate" (NEXT f3: inv_norm1_estimate).
     forced: decision vector used verbatim (C3); variant=1 uses the reversed-chunk GEMM (noise floor).
     on_step(k, A_before, A_after, d): optional test hook called after each step with copies.
     """
@@ -551,7 +612,7 @@ def hybrid_factor(A_in: np.ndarray, nb: int, crit: int = CRIT_MAX, alpha: float 
             d = LU  # ledger 4
         else:
             if crit in (CRIT_MAX, CRIT_SUM):
-                inv = inv_norm1_from_lu(W)
+                inv = inv_norm1_from_lu(W) if invnorm == "exact" else inv_norm1_estimate(W)
                 lu, mg = criterion_max_sum(crit, alpha, inv, s)
             else:
                 lu, mg = criterion_mumps(alpha, W, lmax, amax, mumps_reading)

@@ -60,6 +60,38 @@ def test_inv_norm_matches_dense_inverse(b):
     assert O.inv_norm1_from_lu(W) == 2.0
 
 
+@pytest.mark.parametrize("b", [2, 3, 17, 64, 128, 256])
+def test_inv_norm_estimate_matches_lapack_dgecon(b):
+    """NEXT f3: the oracle's Hager/Higham iteration is LAPACK's: dgecon on the same LU
+    factors returns rcond = 1 / (||A||_1 * est), and est is a lower bound of the exact norm."""
+    from scipy.linalg import lapack, lu_factor
+    rng = np.random.default_rng(100 + b)
+    for trial in range(6):
+        T = rng.standard_normal((b, b)) if trial % 2 else rng.uniform(-0.5, 0.5, (b, b))
+        W, _, _ = O.getrf(T)
+        lu, _ = lu_factor(T)
+        anorm = float(np.abs(T).sum(axis=0).max())
+        rcond, info = lapack.dgecon(lu, anorm, norm="1")
+        assert info == 0
+        est = O.inv_norm1_estimate(W)
+        assert est == pytest.approx(1.0 / (rcond * anorm), rel=1e-11)
+        assert est <= O.inv_norm1_from_lu(W) * (1 + 1e-12)
+
+
+def test_inv_norm_estimate_special_cases():
+    W, _, _ = O.getrf(np.array([[4.0]]))
+    assert O.inv_norm1_estimate(W) == 0.25                      # n = 1: |A^-1 x|
+    W, _, _ = O.getrf(np.diag([2.0, 0.5, 8.0, 1.0]))
+    assert O.inv_norm1_estimate(W) == 2.0                       # diagonal: exact (= max 1/|d|)
+    from scipy.linalg import lapack, lu_factor
+    T = np.triu(np.ones((6, 6)))          # ||T^-1||_1 = 2; the estimator stops at 17/9 (< 2)
+    W, _, _ = O.getrf(T)
+    rcond, _ = lapack.dgecon(lu_factor(T)[0], 6.0, norm="1")
+    assert O.inv_norm1_estimate(W) == pytest.approx(1.0 / (6.0 * rcond), rel=1e-14)
+    assert O.inv_norm1_estimate(W) == pytest.approx(17.0 / 9.0, rel=1e-14)
+    assert O.inv_norm1_from_lu(W) == 2.0
+
+
 @pytest.mark.parametrize("b,ib", [(8, 4), (32, 32), (64, 16), (50, 16), (128, 32)])
 def test_geqrt_matches_lapack_dgeqrt(b, ib):
     T0 = RNG.standard_normal((b, b))
