@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--fqr", type=float, default=0.0, help="forced QR-step fraction (C3 pattern)")
     ap.add_argument("--criterion", default="", help="max|sum|mumps: use the criterion instead")
     ap.add_argument("--alpha", type=float, default=1.0)
+    ap.add_argument("--invnorm", default="exact", choices=["exact", "estimate"],
+                    help="||A_kk^-1||_1 exact (default) or the Hager/Higham estimate (NEXT f3)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-N", type=int, default=4096)
@@ -175,6 +177,8 @@ def workload_config(args, cfg):
     N, nb = cfg["N"], cfg["nb"]
     if args.criterion:
         dec = f"{args.criterion} criterion alpha={args.alpha}"
+        if args.invnorm == "estimate":
+            dec += " (||A_kk^-1||_1 estimated)"
     else:
         dec = f"forced Bernoulli pattern f_QR={args.fqr} (seed 30)"
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -258,7 +262,8 @@ def main():
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        f = H.hlq_factor_ex(A, N, nb, crit, args.alpha, forced=forced, profile=int(profile))
+        f = H.hlq_factor_ex(A, N, nb, crit, args.alpha, forced=forced, profile=int(profile),
+                            invnorm_estimate=int(args.invnorm == "estimate"))
         f.solve(b, x)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -444,7 +449,8 @@ def run_distributed(args, cfg, rank, world, local, dev):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         f = H.hlq_factor_dist(grid, [A], N, nb, crit, args.alpha, forced=forced,
-                              tree_domains=D, profile=int(profile))
+                              tree_domains=D, profile=int(profile),
+                              invnorm_estimate=int(args.invnorm == "estimate"))
         f.solve(b, x)
         e1.record(stream)
         torch.cuda.synchronize()

@@ -73,6 +73,8 @@ typedef struct {
   int32_t blocking;          /* 1 (default): synchronise opt.stream before returning             */
   void* stream;              /* cudaStream_t                                                     */
   int32_t profile;           /* 1: time every kernel class with CUDA events (hlq_get_profile)    */
+  int32_t invnorm_estimate;  /* 0 (default): ||A_kk^-1||_1 exact (reading 3); 1: the
+                                Hager/Higham estimate in LAPACK dlacn2 order (NEXT f3) */
 } hlq_options;
 
 typedef struct {

@@ -29,7 +29,7 @@ class HlqOptions(C.Structure):
                 ("tree_domains", C.c_int32), ("tree", C.c_int32), ("mumps_reading", C.c_int32),
                 ("forced", C.c_void_p), ("ref_dec", C.c_void_p), ("ref_margin", C.c_void_p),
                 ("tie_rel_tol", C.c_double), ("track_growth", C.c_int32), ("blocking", C.c_int32),
-                ("stream", C.c_void_p), ("profile", C.c_int32)]
+                ("stream", C.c_void_p), ("profile", C.c_int32), ("invnorm_estimate", C.c_int32)]
 
 
 class HlqInfo(C.Structure):

@@ -88,6 +88,9 @@ static cudaStream_t panel_stream() {
   return sp;
 }
 
+// the estimator keeps its vectors in shared memory (nb <= 512 is the library limit anyway)
+static bool g_nb_too_big_for_estimate(int nb, int est) { return est && nb > 512; }
+
 static int cuda_err(cudaError_t e) {
   if (e == cudaSuccess) return 0;
   fprintf(stderr, "[hlq] CUDA error: %s\n", cudaGetErrorString(e));
@@ -186,7 +189,8 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   if (opt.tree_domains == 0) opt.tree_domains = 1;
   if (opt.tie_rel_tol == 0.0) opt.tie_rel_tol = 1e-10;
   if (opt.ib < 1 || opt.ib > 32 || opt.tree_domains < 1 || opt.tree != HLQ_TREE_GREEDY ||
-      opt.mumps_reading < 0 || opt.mumps_reading > 1)
+      opt.mumps_reading < 0 || opt.mumps_reading > 1 || opt.invnorm_estimate < 0 ||
+      opt.invnorm_estimate > 1 || g_nb_too_big_for_estimate(nb, opt.invnorm_estimate))
     return -6;
   int64_t lda = opt.lda ? opt.lda : N;
   if (lda < N) return -6;
@@ -348,7 +352,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
       P.end(sp);
       if (criterion_needed && criterion != HLQ_CRIT_MUMPS) {
         P.begin(HLQ_PROF_CRITERION, sp);
-        launch_invnorm(g, k, wk, sp);
+        launch_invnorm(g, k, wk, sp, opt.invnorm_estimate);
         P.end(sp);
       }
     } else {

@@ -271,16 +271,156 @@ __global__ void __launch_bounds__(256) k_invnorm(const double* __restrict__ Li,
   if (lane == 0) atomic_max_nonneg(inv_norm, colsum);
 }
 
+// NEXT f3: the Hager / Higham estimate of ||U^-1 L^-1||_1 in the order of LAPACK
+// dlacn2 (the oracle's inv_norm1_estimate), one CTA.  B x = Ui (Li x) and B^T v = Li^T (Ui^T v) are
+// triangular GEMVs with the explicit inverses of k_tri_inv; sums and the first-max argmax are CTA
+// reductions in a fixed order.
+__device__ double est_asum(const double* y, int n, double* red) {
+  const int tid = threadIdx.x;
+  double s = 0.0;
+  for (int r = tid; r < n; r += 256) s += fabs(y[r]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  __syncthreads();
+  if ((tid & 31) == 0) red[tid >> 5] = s;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) t += red[w];
+  __syncthreads();
+  return t;
+}
+__device__ int est_argmax(const double* z, int n, double* redv, int* redi) {
+  const int tid = threadIdx.x;
+  double bv = -1.0;
+  int bi = 0x7fffffff;
+  for (int r = tid; r < n; r += 256) {
+    const double v = fabs(z[r]);
+    if (v > bv) {
+      bv = v;
+      bi = r;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  __syncthreads();
+  if ((tid & 31) == 0) {
+    redv[tid >> 5] = bv;
+    redi[tid >> 5] = bi;
+  }
+  __syncthreads();
+  double v = redv[0];
+  int i = redi[0];
+  for (int w = 1; w < 8; ++w)
+    if (redv[w] > v || (redv[w] == v && redi[w] < i)) {
+      v = redv[w];
+      i = redi[w];
+    }
+  __syncthreads();
+  return i;
+}
+
+__global__ void __launch_bounds__(256) k_invnorm_est(const double* __restrict__ Li,
+                                                     const double* __restrict__ Ui, int n, int ld,
+                                                     double* out) {
+  __shared__ double x[512], t[512], y[512], xi[512];
+  __shared__ double red[8];
+  __shared__ int redi[8];
+  __shared__ int s_diff;
+  const int tid = threadIdx.x;
+  auto Bx = [&](const double* v, double* o) {  // o = Ui (Li v)
+    for (int r = tid; r < n; r += 256) {
+      double a = 0.0;
+      for (int c = 0; c <= r; ++c) a += Li[(int64_t)c * ld + r] * v[c];
+      t[r] = a;
+    }
+    __syncthreads();
+    for (int r = tid; r < n; r += 256) {
+      double a = 0.0;
+      for (int c = r; c < n; ++c) a += Ui[(int64_t)c * ld + r] * t[c];
+      o[r] = a;
+    }
+    __syncthreads();
+  };
+  auto BTx = [&](const double* v, double* o) {  // o = Li^T (Ui^T v)
+    for (int r = tid; r < n; r += 256) {
+      double a = 0.0;
+      for (int c = 0; c <= r; ++c) a += Ui[(int64_t)r * ld + c] * v[c];
+      t[r] = a;
+    }
+    __syncthreads();
+    for (int r = tid; r < n; r += 256) {
+      double a = 0.0;
+      for (int c = r; c < n; ++c) a += Li[(int64_t)r * ld + c] * t[c];
+      o[r] = a;
+    }
+    __syncthreads();
+  };
+  for (int r = tid; r < n; r += 256) x[r] = 1.0 / (double)n;
+  __syncthreads();
+  Bx(x, y);
+  if (n == 1) {
+    if (tid == 0) out[0] = fabs(y[0]);
+    return;
+  }
+  double est = est_asum(y, n, red);
+  for (int r = tid; r < n; r += 256) xi[r] = y[r] >= 0.0 ? 1.0 : -1.0;
+  __syncthreads();
+  BTx(xi, x);  // z in x
+  int j = est_argmax(x, n, red, redi);
+  for (int it = 2;; ) {
+    for (int r = tid; r < n; r += 256) x[r] = (r == j) ? 1.0 : 0.0;
+    __syncthreads();
+    Bx(x, y);
+    const double est_old = est;
+    est = est_asum(y, n, red);
+    if (tid == 0) s_diff = 0;
+    __syncthreads();
+    for (int r = tid; r < n; r += 256)
+      if ((y[r] >= 0.0 ? 1.0 : -1.0) != xi[r]) s_diff = 1;
+    __syncthreads();
+    if (!s_diff || est <= est_old) break;
+    for (int r = tid; r < n; r += 256) xi[r] = y[r] >= 0.0 ? 1.0 : -1.0;
+    __syncthreads();
+    BTx(xi, x);
+    const int jl = j;
+    j = est_argmax(x, n, red, redi);
+    if (x[jl] != fabs(x[j]) && it < 5) {
+      ++it;
+      continue;
+    }
+    break;
+  }
+  for (int r = tid; r < n; r += 256)
+    x[r] = ((r & 1) ? -1.0 : 1.0) * (1.0 + (double)r / (double)(n - 1));
+  __syncthreads();
+  Bx(x, y);
+  const double tt = 2.0 * (est_asum(y, n, red) / (double)(3 * n));
+  if (tid == 0) out[0] = tt > est ? tt : est;
+}
+
 void launch_tri_inv(Geo g, int k, const DevWork& w, double* Li, double* Ui, cudaStream_t st) {
   const int bk = g.bs(k);
   dim3 grid((bk + 7) / 8, 2);
   { ::hlq::g_launches++; k_tri_inv<<<grid, 256, sizeof(double) * 8 * bk, st>>>(w.W, bk, g.nb, Li, Ui); }
 }
 
-void launch_invnorm(Geo g, int k, DevWork w, cudaStream_t st) {
+void launch_invnorm(Geo g, int k, DevWork w, cudaStream_t st, int estimate) {
   const int bk = g.bs(k);
   const double* Li = w.scratch;                       // filled by launch_tri_inv
   const double* Ui = w.scratch + (size_t)g.nb * g.nb;
+  if (estimate) {
+    ::hlq::g_launches++;
+    k_invnorm_est<<<1, 256, 0, st>>>(Li, Ui, bk, g.nb, w.inv_norm);
+    return;
+  }
   cudaMemsetAsync(w.inv_norm, 0, sizeof(double), st);
   { ::hlq::g_launches++; k_invnorm<<<(bk + 7) / 8, 256, 0, st>>>(Li, Ui, bk, g.nb, w.inv_norm); }
 }

@@ -98,7 +98,8 @@ void launch_tt_apply(const double* A, Geo g, int k, int ib, const double* Ttt,
 void launch_gemv_sub(double* y, const double* B, int64_t ldb, int64_t M, int K, const double* v,
                      cudaStream_t st);
 void launch_getrf(const double* A, Geo g, int k, DevWork w, bool need, cudaStream_t st);
-void launch_invnorm(Geo g, int k, DevWork w, cudaStream_t st);
+// estimate != 0: the Hager / Higham estimate (NEXT f3) instead of the exact norm
+void launch_invnorm(Geo g, int k, DevWork w, cudaStream_t st, int estimate = 0);
 void launch_decide(Geo g, int k, int crit, double alpha, int mumps_reading, double tie_tol,
                    int has_forced, int has_ref, DevWork w, cudaStream_t st);
 void launch_lu_panel(double* A, Geo g, int k, const DevWork& w, cudaStream_t st);

@@ -26,7 +26,8 @@ def H():
     return H
 
 
-def run_pair(H, A, b, nb, crit=O.CRIT_MAX, alpha=1.0, D=1, forced=None, mumps_reading=0):
+def run_pair(H, A, b, nb, crit=O.CRIT_MAX, alpha=1.0, D=1, forced=None, mumps_reading=0,
+             invnorm="exact"):
     N = A.shape[0]
     pre = {}
 
@@ -34,10 +35,11 @@ def run_pair(H, A, b, nb, crit=O.CRIT_MAX, alpha=1.0, D=1, forced=None, mumps_re
         sl = O.tsl(N, nb, k)
         pre[k] = Ab[sl, sl].copy()
     fo = O.hybrid_factor(A, nb, crit, alpha, D=D, forced=forced, mumps_reading=mumps_reading,
-                         on_step=hook)
+                         on_step=hook, invnorm=invnorm)
     fo.pre_tiles = pre
     dA = H.to_colmajor(A)
-    kw = dict(tree_domains=D, mumps_reading=mumps_reading)
+    kw = dict(tree_domains=D, mumps_reading=mumps_reading,
+              invnorm_estimate=1 if invnorm == "estimate" else 0)
     if forced is not None:
         f = H.hlq_factor_ex(dA, N, nb, crit, alpha, forced=forced, **kw)
     else:
@@ -258,3 +260,20 @@ def test_invalid_arguments(H):
         H.hlq_factor(dA, 4, 2, H.CRIT_MAX, float("nan"))
     with pytest.raises(H.HlqError):
         H.hlq_factor(dA, 0, 2, H.CRIT_MAX, 1.0)
+
+
+@pytest.mark.parametrize("crit,alpha,seed", [(O.CRIT_MAX, 1.2e4, 0), (O.CRIT_MAX, 3e4, 0),
+                                             (O.CRIT_SUM, 1e5, 5), (O.CRIT_MAX, 1.0, 1)])
+def test_invnorm_estimator_option(H, crit, alpha, seed):
+    """NEXT f3: the criterion with the Hager/Higham estimate of ||A_kk^-1||_1 takes the
+    oracle's decisions (same estimator, LAPACK dlacn2 order) and keeps the factor parity bar."""
+    N, nb = 1024, 128
+    A = I.uniform_matrix(seed, N)
+    b = I.uniform_rhs(seed, N)
+    fo, f, F, x = run_pair(H, A, b, nb, crit, alpha, invnorm="estimate")
+    check_parity(fo, f, F, x, A, b)
+    # the estimate never exceeds the exact norm, so alpha / ||A_kk^-1|| can only grow: LU steps of
+    # the exact run's first step are LU here too
+    fe = O.hybrid_factor(A, nb, crit, alpha)
+    if fe.dec[0] == O.LU:
+        assert fo.dec[0] == O.LU
