@@ -95,6 +95,51 @@ def bernoulli_pattern(seed: int, n: int, f: float) -> np.ndarray:
     return (u < f).astype(np.uint8)
 
 
+# Special matrices of the paper's stability study (Table III) -- ONLY those the paper
+# itself defines by a formula (the rest of Higham's toolbox is not reproduced).  1-based i, j as in
+# the paper; random ingredients drawn from numpy default_rng(seed).  NEXT f3.
+SPECIAL_BY_FORMULA = ("house", "parter", "ris", "hankel", "compan", "lehmer", "demmel", "hilb",
+                      "lotkin", "orthogo")
+
+
+def special_matrix(name: str, n: int, seed: int = 7) -> np.ndarray:
+    i = np.arange(1, n + 1, dtype=np.float64)[:, None]
+    j = np.arange(1, n + 1, dtype=np.float64)[None, :]
+    rng = np.random.default_rng(seed)
+    if name == "house":      # A = eye(n) - beta*v*v'; v ~ randn, beta = 2/(v'v) (reading 31)
+        v = rng.standard_normal(n)
+        A = np.eye(n) - (2.0 / float(v @ v)) * np.outer(v, v)
+    elif name == "parter":   # A(i,j) = 1/(i - j + 0.5)
+        A = 1.0 / (i - j + 0.5)
+    elif name == "ris":      # A(i,j) = 0.5/(n - i - j + 1.5)
+        A = 0.5 / (n - i - j + 1.5)
+    elif name == "hankel":   # hankel(c, r), c, r = randn(n,1), c(n) = r(1)
+        c = rng.standard_normal(n)
+        r = rng.standard_normal(n)
+        c[-1] = r[0]
+        s_ = (i + j - 1).astype(np.int64)   # A(i,j) = c(i+j-1) if i+j-1 <= n else r(i+j-n)
+        A = np.where(s_ <= n, c[np.minimum(s_, n) - 1], r[np.clip(s_ - n, 1, n) - 1])
+    elif name == "compan":   # compan(randn(n+1,1)): first row -p(2:)/p(1), ones below the diagonal
+        p = rng.standard_normal(n + 1)
+        A = np.diag(np.ones(n - 1), -1)
+        A[0, :] = -p[1:] / p[0]
+    elif name == "lehmer":   # A(i,j) = i/j for j >= i, symmetric
+        A = np.minimum(i, j) / np.maximum(i, j)
+    elif name == "demmel":   # D*(eye(n) + 1e-7*rand(n)), D = diag(10^(14*(0:n-1)/n)) (ledger 29)
+        D = 10.0 ** (14.0 * np.arange(n) / n)
+        A = D[:, None] * (np.eye(n) + 1e-7 * rng.random((n, n)))
+    elif name == "hilb":     # 1/(i + j - 1)
+        A = 1.0 / (i + j - 1)
+    elif name == "lotkin":   # the Hilbert matrix with its first row all ones
+        A = 1.0 / (i + j - 1)
+        A[0, :] = 1.0
+    elif name == "orthogo":  # sqrt(2/(n+1)) sin(i j pi/(n+1))
+        A = np.sqrt(2.0 / (n + 1)) * np.sin(i * j * np.pi / (n + 1))
+    else:
+        raise ValueError(f"special matrix {name!r} is not defined by a formula in the paper")
+    return np.asfortranarray(A)
+
+
 def config_system(name: str, N: int | None = None):
     """Return (A, b, meta) for a named BASELINE config at its size (or an override N).
 
