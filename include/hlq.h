@@ -21,6 +21,10 @@
 #ifndef HLQ_H
 #define HLQ_H
 
+/* largest tile size: the diagonal-tile kernels (GETRF, GEQRT/TTQRT panels) keep a 32-column
+ * panel plus the U12 block of one tile in shared memory */
+#define HLQ_MAX_NB 320
+
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -98,7 +102,8 @@ int hlq_default_options(hlq_options* opt);
  *          below: L_ik (LU step) or the GEQRT reflectors V (strictly lower part of tile
  *          (i,k)) plus the TT reflectors (upper triangle of tile (i,k), i>k).  The handle BORROWS A:
  *          keep it alive and unmodified until hlq_free if hlq_solve is to be called.
- *   N >= 1, 1 <= nb;  N need not be a multiple of nb (ragged last tile).
+ *   N >= 1, 1 <= nb <= HLQ_MAX_NB;  N need not be a multiple of nb (ragged last tile);
+ *          nb > N is clamped to N.
  *   criterion HLQ_CRIT_*;  alpha >= 0 (0 -> every step QR, +inf -> every step LU; NaN invalid).
  *   out    receives a new handle (free with hlq_free) even when the status is positive.
  * Errors: -1 A NULL, -2 N, -3 nb, -4 criterion, -5 alpha, -6 options, HLQ_ERR_*. */

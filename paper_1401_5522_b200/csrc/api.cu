@@ -88,8 +88,6 @@ static cudaStream_t panel_stream() {
   return sp;
 }
 
-// the estimator keeps its vectors in shared memory (nb <= 512 is the library limit anyway)
-static bool g_nb_too_big_for_estimate(int nb, int est) { return est && nb > 512; }
 
 static int cuda_err(cudaError_t e) {
   if (e == cudaSuccess) return 0;
@@ -176,7 +174,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   *out = nullptr;
   if (!A) return -1;
   if (N <= 0) return -2;
-  if (nb <= 0 || nb > 512) return -3;
+  if (nb <= 0 || nb > HLQ_MAX_NB) return -3;
   if (criterion < 0 || criterion > 2) return -4;
   if (!(alpha >= 0.0)) return -5;  // rejects NaN and negatives
   hlq_options opt;
@@ -190,7 +188,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   if (opt.tie_rel_tol == 0.0) opt.tie_rel_tol = 1e-10;
   if (opt.ib < 1 || opt.ib > 32 || opt.tree_domains < 1 || opt.tree != HLQ_TREE_GREEDY ||
       opt.mumps_reading < 0 || opt.mumps_reading > 1 || opt.invnorm_estimate < 0 ||
-      opt.invnorm_estimate > 1 || g_nb_too_big_for_estimate(nb, opt.invnorm_estimate))
+      opt.invnorm_estimate > 1)
     return -6;
   int64_t lda = opt.lda ? opt.lda : N;
   if (lda < N) return -6;

@@ -1539,7 +1539,7 @@ int hlq_factor_dist(hlq_grid_t grid, double* const* A_local, const int64_t* lld,
   if (!grid) return -1;
   if (!A_local) return -2;
   if (N <= 0) return -4;
-  if (nb <= 0 || nb > 512) return -5;
+  if (nb <= 0 || nb > HLQ_MAX_NB) return -5;
   if (criterion < 0 || criterion > 2) return -6;
   if (!(alpha >= 0.0)) return -7;
   hlq_options opt;

@@ -5,7 +5,11 @@
 //     (reading 3).  The inverses are reused by the LU step: TRSM and SWPTRSM
 //     become DMMA GEMMs with U^-1 and L^-1 (gemm.cu).
 //
-// GETRF is blocked right-looking with 32-column panels held in shared memory, ONE CTA.  Every
+// GETRF is blocked right-looking with 32-column panels, ONE CTA of 512 threads.  Inside a panel
+// every thread holds one row in registers (two barriers per column, pivot search by redux.sync);
+// the panel's 32 row swaps are applied to the rest of the tile as one gathered permutation, U12
+// is a register-blocked forward substitution and the trailing update a 4x4-per-thread blocked
+// product from shared memory.  Every
 // element update is a separately rounded multiply and subtract applied in column order (the
 // __dmul_rn/__dsub_rn intrinsics forbid FMA contraction), and the pivot is the first maximum of
 // |column|, so W and ipiv are bit-identical to the unblocked elimination order of the oracle.
@@ -26,6 +30,69 @@ __device__ __forceinline__ bool piv_better(double v, int i, double bv, int bi) {
 }
 constexpr int GT = 512;       // threads
 
+// The same order as a 64-bit key: for |v| >= 0 the IEEE bits are monotone, every NaN maps to one
+// key above +inf, and the "no candidate" sentinel (-1) maps to 0 with index INT_MAX, which loses
+// every tie to a real zero.  A warp reduces (key desc, index asc) with three redux.sync.
+__device__ __forceinline__ unsigned long long piv_key(double v) {
+  if (v != v) return 0x7ff8000000000000ull;
+  return v < 0.0 ? 0ull : (unsigned long long)__double_as_longlong(v);
+}
+__device__ __forceinline__ void warp_piv_reduce(unsigned long long& key, int& idx) {
+  const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  const unsigned mi =
+      __reduce_min_sync(0xffffffffu, (hi == mhi && lo == mlo) ? (unsigned)idx : 0x7fffffffu);
+  key = ((unsigned long long)mhi << 32) | mlo;
+  idx = (int)mi;
+}
+
+
+// W[r][t] -= sum_c L[c][r] * U[c][t] (c sequential, separately rounded), r < nr, t < ntr.
+// Blocks of 16 RI x 32 CJ outputs, RI x CJ per thread (rows tr + 16 i, cols tc + 32 j): RI + CJ
+// shared loads per RI CJ multiply/subtract pairs.
+template <int RI, int CJ>
+__device__ __forceinline__ void trail_update(double* __restrict__ Wt, int ldw, const double* L,
+                                             const double* U, int ldp, int nr, int ntr, int kc,
+                                             int tid) {
+  const int tr = tid & 15, tc = tid >> 4;
+  for (int rb = 0; rb < nr; rb += 16 * RI)
+    for (int cb0 = 0; cb0 < ntr; cb0 += 32 * CJ) {
+      double acc[RI][CJ];
+#pragma unroll
+      for (int i = 0; i < RI; ++i)
+#pragma unroll
+        for (int j = 0; j < CJ; ++j) {
+          const int r = rb + tr + 16 * i, t = cb0 + tc + 32 * j;
+          acc[i][j] = (r < nr && t < ntr) ? Wt[(int64_t)t * ldw + r] : 0.0;
+        }
+      for (int c = 0; c < kc; ++c) {
+        double l[RI], u[CJ];
+#pragma unroll
+        for (int i = 0; i < RI; ++i) {
+          const int r = rb + tr + 16 * i;
+          l[i] = (r < nr) ? L[c * ldp + r] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < CJ; ++j) {
+          const int t = cb0 + tc + 32 * j;
+          u[j] = (t < ntr) ? U[c * ldp + t] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < RI; ++i)
+#pragma unroll
+          for (int j = 0; j < CJ; ++j) acc[i][j] = __dsub_rn(acc[i][j], __dmul_rn(l[i], u[j]));
+      }
+#pragma unroll
+      for (int i = 0; i < RI; ++i)
+#pragma unroll
+        for (int j = 0; j < CJ; ++j) {
+          const int r = rb + tr + 16 * i, t = cb0 + tc + 32 * j;
+          if (r < nr && t < ntr) Wt[(int64_t)t * ldw + r] = acc[i][j];
+        }
+    }
+}
+
 // smem: panel P[GPW][ldp] + U12 block U[GPW][ldu]
 __global__ void __launch_bounds__(GT) k_getrf(const double* __restrict__ A, Geo g, int k,
                                               double* __restrict__ W, int* __restrict__ ipiv,
@@ -36,171 +103,205 @@ __global__ void __launch_bounds__(GT) k_getrf(const double* __restrict__ A, Geo 
   const int ldp = g.nb + 1;  // odd stride: conflict-free column-per-thread access
   double* P = sm;                    // GPW x ldp
   double* U = sm + GPW * ldp;        // GPW x ldp  (row c of U12 for trailing column j at U[c*ldp + j])
-  __shared__ double rv[GT / 32];
+  __shared__ unsigned long long rv[GT / 32];
   __shared__ int ri[GT / 32];
   __shared__ int piv_sh[GPW];
   __shared__ int zp_sh;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double* Akk = g.tile(const_cast<double*>(A), k, k);
-  for (int idx = tid; idx < bk * bk; idx += GT) {
-    int c = idx / bk, r = idx - c * bk;
-    W[(int64_t)c * ldw + r] = Akk[(int64_t)c * g.lda + r];
+  for (int c0 = warp; c0 < bk; c0 += 4 * (GT / 32)) {  // one warp per column, 4 columns in flight
+    double v[4][(HLQ_MAX_NB + 31) / 32];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int i = 0; i < (HLQ_MAX_NB + 31) / 32; ++i) {
+        const int c = c0 + q * (GT / 32), r = lane + 32 * i;
+        if (c < bk && r < bk) v[q][i] = Akk[(int64_t)c * g.lda + r];
+      }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int i = 0; i < (HLQ_MAX_NB + 31) / 32; ++i) {
+        const int c = c0 + q * (GT / 32), r = lane + 32 * i;
+        if (c < bk && r < bk) W[(int64_t)c * ldw + r] = v[q][i];
+      }
   }
   if (tid == 0) zp_sh = 0;
   __syncthreads();
   for (int p0 = 0; p0 < bk; p0 += GPW) {
     const int pw = min(GPW, bk - p0);
     const int rows = bk - p0;
-    for (int idx = tid; idx < pw * rows; idx += GT) {
-      int c = idx / rows, r = idx - c * rows;
-      P[c * ldp + r] = W[(int64_t)(p0 + c) * ldw + p0 + r];
-    }
-    __syncthreads();
-    for (int c = 0; c < pw; ++c) {
-      // first maximum of |P[c][r]|, r in [c, rows)
-      double best = -1.0;
-      int bidx = 0x7fffffff;
-      for (int r = c + tid; r < rows; r += GT) {
-        double v = fabs(P[c * ldp + r]);
-        if (piv_better(v, r, best, bidx)) {
-          best = v;
-          bidx = r;
-        }
-      }
+    // The panel lives in registers: thread r owns panel row r (rows <= nb <= GT) for the whole
+    // panel.  Per column two barriers: (B) every warp reduces the partial maxima (redundantly),
+    // the pivot row's owner publishes it to X and the owner of row c its row to Y; (A) the two
+    // exchange rows, every row below c is scaled by the pivot and updated with the pivot row
+    // (broadcast from X), and each warp takes its partial first maximum of the NEXT column.
+    double* X = U;             // pivot row (GPW doubles)
+    double* Y = U + GPW;       // row c on its way to the pivot's position
+    double pr_[GPW];
+    const bool own = tid < rows;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        double ov = __shfl_xor_sync(0xffffffffu, best, o);
-        int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
-        if (piv_better(ov, oi, best, bidx)) {
-          best = ov;
-          bidx = oi;
-        }
-      }
+    for (int j = 0; j < GPW; ++j)
+      pr_[j] = (own && j < pw) ? W[(int64_t)(p0 + j) * ldw + p0 + tid] : 0.0;
+    const int nwarp_rows = GT / 32;
+    {
+      unsigned long long key = own ? piv_key(fabs(pr_[0])) : 0ull;
+      int bidx = own ? tid : 0x7fffffff;
+      warp_piv_reduce(key, bidx);
       if (lane == 0) {
-        rv[warp] = best;
+        rv[warp] = key;
         ri[warp] = bidx;
       }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < GPW; ++c) {
+      if (c < pw) {
+        unsigned long long bk_ = lane < nwarp_rows ? rv[lane] : 0ull;
+        int bi = lane < nwarp_rows ? ri[lane] : 0x7fffffff;
+        warp_piv_reduce(bk_, bi);
+        if (bi == 0x7fffffff || bi >= rows) bi = c;
+        if (tid == 0) {
+          piv_sh[c] = bi;
+          ipiv[p0 + c] = p0 + bi;
+        }
+        if (tid == bi) {
+#pragma unroll
+          for (int j = 0; j < GPW; ++j) X[j] = pr_[j];
+        }
+        if (tid == c && bi != c) {
+#pragma unroll
+          for (int j = 0; j < GPW; ++j) Y[j] = pr_[j];
+        }
+        __syncthreads();
+        if (bi != c) {
+          if (tid == c) {
+#pragma unroll
+            for (int j = 0; j < GPW; ++j) pr_[j] = X[j];
+          } else if (tid == bi) {
+#pragma unroll
+            for (int j = 0; j < GPW; ++j) pr_[j] = Y[j];
+          }
+        }
+        const double d = X[c];
+        if (d == 0.0 && tid == 0) zp_sh = 1;  // ledger 7: column left unscaled, no update
+        const bool act = own && tid > c;
+        if (act && d != 0.0) {
+          const double l = pr_[c] / d;
+          pr_[c] = l;
+#pragma unroll
+          for (int j = c + 1; j < GPW; ++j) pr_[j] = __dsub_rn(pr_[j], __dmul_rn(l, X[j]));
+        }
+        if (c + 1 < pw) {
+          unsigned long long key = act ? piv_key(fabs(pr_[c + 1])) : 0ull;
+          int bidx = act ? tid : 0x7fffffff;
+          warp_piv_reduce(key, bidx);
+          if (lane == 0) {
+            rv[warp] = key;
+            ri[warp] = bidx;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    if (own) {  // the factored panel: to shared memory (L11, L21 below) and back to W
+#pragma unroll
+      for (int j = 0; j < GPW; ++j)
+        if (j < pw) {
+          P[j * ldp + tid] = pr_[j];
+          W[(int64_t)(p0 + j) * ldw + p0 + tid] = pr_[j];
+        }
+    }
+    // apply the panel's swaps to every other column of the tile (left and right): the 32 sequential
+    // swaps compose into a permutation that moves at most 64 rows; gather those rows column by
+    // column, one warp per column.
+    {
+      int* perm = reinterpret_cast<int*>(sm + 2 * GPW * ldp);      // rows ints
+      int* mv = perm + ((rows + 1) & ~1);                           // <= 2*GPW moved rows
+      __shared__ int nmv_sh;
+      for (int r = tid; r < rows; r += GT) perm[r] = r;
       __syncthreads();
       if (tid == 0) {
-        double b = rv[0];
-        int bi = ri[0];
-        for (int w = 1; w < GT / 32; ++w)
-          if (piv_better(rv[w], ri[w], b, bi)) {
-            b = rv[w];
-            bi = ri[w];
+        for (int c = 0; c < pw; ++c) {
+          const int pr = piv_sh[c];
+          if (pr != c) {
+            const int t = perm[c];
+            perm[c] = perm[pr];
+            perm[pr] = t;
           }
-        if (bi == 0x7fffffff || bi >= rows) bi = c;
-        piv_sh[c] = bi;
-        ipiv[p0 + c] = p0 + bi;
+        }
+        nmv_sh = 0;
       }
       __syncthreads();
-      const int pr = piv_sh[c];
-      if (pr != c && tid < pw) {
-        double t = P[tid * ldp + c];
-        P[tid * ldp + c] = P[tid * ldp + pr];
-        P[tid * ldp + pr] = t;
-      }
+      // moved rows (order irrelevant: every one has its own destination)
+      for (int r = tid; r < rows; r += GT)
+        if (perm[r] != r) mv[atomicAdd(&nmv_sh, 1)] = r;
       __syncthreads();
-      const double d = P[c * ldp + c];
-      if (d == 0.0) {
-        if (tid == 0) zp_sh = 1;
-        __syncthreads();
-        continue;  // ledger 7: column left unscaled, no update
-      }
-      for (int r = c + 1 + tid; r < rows; r += GT) P[c * ldp + r] = P[c * ldp + r] / d;
-      __syncthreads();
-      // rank-1 update inside the panel: P[j][r] -= P[c][r] * P[j][c]
-      const int nr = rows - c - 1, nj = pw - c - 1;
-      for (int idx = tid; idx < nr * nj; idx += GT) {
-        int j = c + 1 + idx / nr, r = c + 1 + idx % nr;
-        P[j * ldp + r] = __dsub_rn(P[j * ldp + r], __dmul_rn(P[c * ldp + r], P[j * ldp + c]));
-      }
-      __syncthreads();
-    }
-    // write the panel back
-    for (int idx = tid; idx < pw * rows; idx += GT) {
-      int c = idx / rows, r = idx - c * rows;
-      W[(int64_t)(p0 + c) * ldw + p0 + r] = P[c * ldp + r];
-    }
-    // apply the panel's swaps to every other column of the tile (left and right), in order:
-    // one warp per column, the column segment rows [p0, bk) staged in the warp's smem buffer
-    {
+      const int nmv = nmv_sh;
       const int nother = bk - pw;
-      double* cb = sm + 2 * GPW * ldp + warp * ldp;
-      for (int t = warp; t < nother; t += GT / 32) {
-        int col = (t < p0) ? t : t + pw;
-        double* wc = W + (int64_t)col * ldw + p0;
-        for (int r = lane; r < rows; r += 32) cb[r] = wc[r];
-        __syncwarp();
-        if (lane == 0)
-          for (int c = 0; c < pw; ++c) {
-            int pr = piv_sh[c];
-            if (pr != c) {
-              double x = cb[c];
-              cb[c] = cb[pr];
-              cb[pr] = x;
-            }
+      // one warp per column: lane owns moved rows lane and lane + 32 (nmv <= 64); all loads of a
+      // column precede its stores (__syncwarp), four columns in flight per warp
+      int du0 = -1, su0 = 0, du1 = -1, su1 = 0;
+      if (lane < nmv) { du0 = mv[lane]; su0 = perm[du0]; }
+      if (lane + 32 < nmv) { du1 = mv[lane + 32]; su1 = perm[du1]; }
+      if (nmv > 0) {
+        constexpr int NW = GT / 32, CF = 4;
+        for (int t0 = warp; t0 < nother; t0 += NW * CF) {
+          double v0[CF], v1[CF];
+#pragma unroll
+          for (int q = 0; q < CF; ++q) {
+            const int t = t0 + NW * q;
+            const int col = (t < p0) ? t : t + pw;
+            const double* wc = W + (int64_t)col * ldw + p0;
+            if (t < nother && du0 >= 0) v0[q] = wc[su0];
+            if (t < nother && du1 >= 0) v1[q] = wc[su1];
           }
-        __syncwarp();
-        for (int r = lane; r < rows; r += 32) wc[r] = cb[r];
-        __syncwarp();
+          __syncwarp();
+#pragma unroll
+          for (int q = 0; q < CF; ++q) {
+            const int t = t0 + NW * q;
+            const int col = (t < p0) ? t : t + pw;
+            double* wc = W + (int64_t)col * ldw + p0;
+            if (t < nother && du0 >= 0) wc[du0] = v0[q];
+            if (t < nother && du1 >= 0) wc[du1] = v1[q];
+          }
+        }
       }
     }
     __syncthreads();
     const int ntr = bk - p0 - pw;  // trailing columns
     if (ntr > 0) {
       // U12 = L11^-1 A12: forward substitution per column in elimination order
+      // (same rounding order per element as the column-by-column substitution, l increasing; the
+      // 32 running sums of a column are independent chains held in registers)
       for (int t = tid; t < ntr; t += GT) {
         int col = p0 + pw + t;
         double* wc = W + (int64_t)col * ldw + p0;
-        for (int c = 0; c < pw; ++c) {
-          double x = wc[c];
-          for (int l = 0; l < c; ++l) x = __dsub_rn(x, __dmul_rn(P[l * ldp + c], U[l * ldp + t]));
-          U[c * ldp + t] = x;
-          wc[c] = x;
+        double acc[GPW];
+#pragma unroll
+        for (int c = 0; c < GPW; ++c) acc[c] = c < pw ? wc[c] : 0.0;
+#pragma unroll
+        for (int l = 0; l < GPW; ++l) {
+          if (l < pw) {
+            const double u = acc[l];
+            U[l * ldp + t] = u;
+            wc[l] = u;
+#pragma unroll
+            for (int c = l + 1; c < GPW; ++c) acc[c] = __dsub_rn(acc[c], __dmul_rn(P[l * ldp + c], u));
+          }
         }
       }
       __syncthreads();
-      // trailing update: W[p0+pw+r][col] -= sum_c L21[r][c] U12[c][col], sequential in c.
-      // 64 x 128 output blocks, 4 x 4 per thread (rows tr + 16 i, cols tc + 32 j): 8 shared loads
-      // per 16 separately-rounded multiply/subtract pairs.
+      // trailing update: W[p0+pw+r][col] -= sum_c L21[r][c] U12[c][col], sequential in c; the
+      // per-thread block shrinks with the trailing matrix so that idle lanes stay few
       const int nr = rows - pw;
-      const int tr = tid & 15, tc = tid >> 4;
-      for (int rb = 0; rb < nr; rb += 64)
-        for (int cb0 = 0; cb0 < ntr; cb0 += 128) {
-          double acc[4][4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              int r = rb + tr + 16 * i, t = cb0 + tc + 32 * j;
-              acc[i][j] = (r < nr && t < ntr) ? W[(int64_t)(p0 + pw + t) * ldw + p0 + pw + r] : 0.0;
-            }
-          for (int c = 0; c < pw; ++c) {
-            double l[4], u[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              int r = rb + tr + 16 * i;
-              l[i] = (r < nr) ? P[c * ldp + pw + r] : 0.0;
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              int t = cb0 + tc + 32 * j;
-              u[j] = (t < ntr) ? U[c * ldp + t] : 0.0;
-            }
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-              for (int j = 0; j < 4; ++j) acc[i][j] = __dsub_rn(acc[i][j], __dmul_rn(l[i], u[j]));
-          }
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              int r = rb + tr + 16 * i, t = cb0 + tc + 32 * j;
-              if (r < nr && t < ntr) W[(int64_t)(p0 + pw + t) * ldw + p0 + pw + r] = acc[i][j];
-            }
-        }
+      double* Wt = W + (int64_t)(p0 + pw) * ldw + p0 + pw;
+      if (ntr > 64 && nr > 32)
+        trail_update<4, 4>(Wt, ldw, P + pw, U, ldp, nr, ntr, pw, tid);
+      else if (nr > 32)
+        trail_update<4, 2>(Wt, ldw, P + pw, U, ldp, nr, ntr, pw, tid);
+      else
+        trail_update<2, 2>(Wt, ldw, P + pw, U, ldp, nr, ntr, pw, tid);
     }
     __syncthreads();
   }

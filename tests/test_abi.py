@@ -48,6 +48,7 @@ def test_argument_errors_without_gpu(built):
     dummy = ctypes.c_void_p(0x1000)
     assert lib.hlq_factor(dummy, 0, 2, 0, 1.0, ctypes.byref(h)) == -2
     assert lib.hlq_factor(dummy, 8, 0, 0, 1.0, ctypes.byref(h)) == -3
+    assert lib.hlq_factor(dummy, 4096, 321, 0, 1.0, ctypes.byref(h)) == -3  # HLQ_MAX_NB = 320
     assert lib.hlq_factor(dummy, 8, 2, 5, 1.0, ctypes.byref(h)) == -4
     assert lib.hlq_factor(dummy, 8, 2, 0, float("nan"), ctypes.byref(h)) == -5
     assert lib.hlq_factor(dummy, 8, 2, 0, -1.0, ctypes.byref(h)) == -5
