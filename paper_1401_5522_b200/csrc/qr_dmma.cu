@@ -74,12 +74,18 @@ __device__ __forceinline__ void cp_cols(double* dst, int ldd, const double* src,
 }
 
 __host__ __device__ inline int qd_ldc(int nb) { return (nb + 31) / 32 * 32 + 4; }
+// the C slab region; during a panel factorisation it holds the scratch (PF_WS) and R_e's block
+__host__ __device__ inline int qd_cs(int W, int nb) {
+  const int c = W * qd_ldc(nb);
+  constexpr int panel = 2 * 8 * 33 + 64 + 32 * 33 + 32 + 8 * 40 + 32 * 33;  // PF_WS + 32 x 33
+  return c > panel ? c : panel;
+}
 
 template <int W>
 static size_t qd_smem(int nb) {
   const int ldc = qd_ldc(nb);
   // Cs (W x ldc) + Vs (32 x ldc) + Us (W x LDU) + Ts (32 x 33)
-  return sizeof(double) * ((size_t)W * ldc + 32 * (size_t)ldc + (size_t)W * LDU + 32 * 33);
+  return sizeof(double) * ((size_t)qd_cs(W, nb) + 32 * (size_t)ldc + (size_t)W * LDU + 32 * 33);
 }
 
 // GEMM1 + TRMM:  Wb (32 x W) = [C1_b +] Vs^T (32 x RK) * Cs[c_off : c_off + RK, 0:W];
@@ -135,17 +141,27 @@ __device__ __forceinline__ void gemm1_trmm(const double* Vs, const double* Cs, i
 #pragma unroll
     for (int h = 0; h < 2; ++h) Us[(nf * 8 + 2 * t + h) * LDU + mi * 8 + g] = acc[mi][h];
   __syncwarp();
-  double u[8];
+  // U = T^T Wb on the tensor cores: A = T^T (lower triangular: k-steps kk <= 8 mi + 7 only),
+  // B = Wb (this warp's 8 columns from Us)
+  double ua[4][2];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {  // lane -> row l = lane, 8 columns
-    const double* wcol = Us + (nf * 8 + j) * LDU;
-    double v = 0.0;
-    for (int q = 0; q <= lane; ++q) v += Ts[lane * 33 + q] * wcol[q];
-    u[j] = v;
+  for (int mi = 0; mi < 4; ++mi) ua[mi][0] = ua[mi][1] = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < 32; kk += 4) {
+    const double bw = Us[(nf * 8 + g) * LDU + kk + t];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+      if (kk <= 8 * mi + 7) dmma(ua[mi][0], ua[mi][1], Ts[(mi * 8 + g) * 33 + kk + t], bw);
   }
   __syncwarp();
 #pragma unroll
-  for (int j = 0; j < 8; ++j) Us[(nf * 8 + j) * LDU + lane] = u[j];
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) Us[(nf * 8 + 2 * t + h) * LDU + mi * 8 + g] = ua[mi][h];
+  __syncwarp();
+  double u[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) u[j] = Us[(nf * 8 + j) * LDU + lane];
   if (c1 != nullptr && lane < sb) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -203,7 +219,7 @@ __global__ void __launch_bounds__(QD_T) k_unmqr_dmma(const double* __restrict__ 
   extern __shared__ __align__(16) double sm[];
   const int ldc = qd_ldc(g.nb);
   double* Cs = sm;
-  double* Vs = Cs + W * ldc;
+  double* Vs = Cs + qd_cs(W, g.nb);
   double* Us = Vs + 32 * ldc;
   double* Ts = Us + W * LDU;
   const int i = k + blockIdx.y;
@@ -252,7 +268,7 @@ __global__ void __launch_bounds__(QD_T) k_ttmqr_dmma(const double* __restrict__ 
   extern __shared__ __align__(16) double sm[];
   const int ldc = qd_ldc(g.nb);
   double* Cs = sm;               // C_i slab (rows of tile i)
-  double* Vs = Cs + W * ldc;
+  double* Vs = Cs + qd_cs(W, g.nb);
   double* Us = Vs + 32 * ldc;
   double* Ts = Us + W * LDU;
   const int2 pr = pairs[blockIdx.y];
@@ -312,88 +328,146 @@ __device__ __forceinline__ double block_sum(double v, double* red, int tid) {
   return s;
 }
 
-template <bool TT>
+// Register-resident layout: lane c owns column c of the 32-column block and warp w owns the NR
+// rows w*NR .. w*NR+NR-1 (NR static), so thread (w, c) holds V[r][c] of its rows in registers and
+// the column loop needs no register indexing by l.  Per column l ONE barrier: x_r = V[r][l] is a
+// shuffle from lane l, thread (w, c) forms its warp's partial of g[c] = sum_r V[r][c] x_r over
+// the reflector's rows, and (GE) the owner of row l publishes that row (the reflector's top
+// elements); after the barrier every warp sums the 8 partials itself (fixed order: identical in
+// every warp), lane c forms dlarfg and w_c / z_c, and each thread updates its own elements.  The
+// T recurrence (dlarft, forward column-wise) runs in warp 0 right after z_l is formed.
+// v = x (1 / (alpha - beta)) as LAPACK dlarfg scales.  Scratch ws:
+// red [2][8][33] | top [2][32] | Z [32][33] | (unused) [32] | xs [8][40]  (PF_WS doubles).  Column l
+// reaches the 32 lanes of a warp through xs (lane l stores its NR values, 16-byte broadcasts back).
+constexpr int PF_WS = 2 * 8 * 33 + 64 + 32 * 33 + 32 + 8 * 40;
+
+template <bool TT, int NR>
 __device__ void panel_factor(double* Vs, int ldc, double* Rs, double* Ts, int R, int i0, int sb,
-                             double* red, double* bc, int tid) {
-  // Per column l ONE CTA-wide reduction: g[c] = sum_r Vs[c][r] x_r over the rows of reflector l
-  // (x = the raw column l below its top element).  g[l] = ||x||^2 gives dlarfg; for c > l,
-  // w_c = top_c + g[c]/sc updates the remaining columns; for q < l, z_q = [V_q(l)] + g[q]/sc
-  // gives the T column.  The 32 partials of a warp are reduced by a transpose-butterfly
-  // (31 shuffles) and the 8 warp partials are summed in a fixed order (deterministic).
+                             double* ws, int tid) {
   const int lane = tid & 31, warp = tid >> 5;
-  for (int l = 0; l < sb; ++l) {
-    if (!TT && l >= R) break;
+  double* red = ws;
+  double* top = ws + 2 * 8 * 33;
+  double* Z = top + 64;
+  double* tauv = Z + 32 * 33;
+  double* xs = tauv + 32 + warp * 40;  // this warp's copy of column l (16-byte aligned)
+  const int rw = warp * NR;  // first row of this warp
+  const int lmax = TT ? sb : min(sb, R);
+  double a[NR];
+#pragma unroll
+  for (int i = 0; i < NR; ++i) a[i] = (rw + i < R && lane < sb) ? Vs[lane * ldc + rw + i] : 0.0;
+#pragma unroll 1
+  for (int l = 0; l < lmax; ++l) {
+    const int bf = l & 1;
+    // reflector rows: GE below the diagonal (l, R), TT the upper-triangle rows [0, min(R, i0+l+1))
     const int rlo = TT ? 0 : l + 1;
     const int rhi = TT ? min(R, i0 + l + 1) : R;
-    double* x = Vs + l * ldc;
-    double p[32];
+    // this warp's reflector rows are i in [ilo, ihi) (warp-uniform; empty for most warps early on)
+    const int ilo = max(0, rlo - rw), ihi = min(NR, rhi - rw);
+    const bool wact = ilo < ihi;
+    double part = 0.0;
+    if (wact) {
+      if (lane == l) {
 #pragma unroll
-    for (int c = 0; c < 32; ++c) p[c] = 0.0;
-    for (int r = rlo + tid; r < rhi; r += QD_T) {
-      const double xr = x[r];
+        for (int i = 0; i < NR; i += 2)
+          *reinterpret_cast<double2*>(xs + i) = make_double2(a[i], a[i + 1]);
+      }
+      __syncwarp();
 #pragma unroll
-      for (int c = 0; c < 32; ++c) p[c] += Vs[c * ldc + r] * xr;
-    }
-    // transpose-butterfly: after the 5 steps lane j holds the warp's sum for column j
-#pragma unroll
-    for (int s = 16; s >= 1; s >>= 1) {
-      const bool upper = (lane & s) != 0;
-#pragma unroll
-      for (int c = 0; c < s; ++c) {
-        double send = upper ? p[c] : p[c + s];
-        double keep = upper ? p[c + s] : p[c];
-        p[c] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+      for (int i = 0; i < NR; i += 2) {
+        const double2 x = *reinterpret_cast<const double2*>(xs + i);
+        if (i >= ilo && i < ihi) part += a[i] * x.x;
+        if (i + 1 >= ilo && i + 1 < ihi) part += a[i + 1] * x.y;
       }
     }
-    red[warp * 33 + lane] = p[0];
-    __syncthreads();
-    if (tid < 32) {
-      double v = 0.0;
+    red[(bf * 8 + warp) * 33 + lane] = part;
+    if (!TT && l >= rw && l < rw + NR) {
 #pragma unroll
-      for (int w = 0; w < 8; ++w) v += red[w * 33 + tid];
-      bc[tid] = v;
+      for (int i = 0; i < NR; ++i)
+        if (rw + i == l) top[bf * 32 + lane] = a[i];
     }
     __syncthreads();
-    const double ssq = bc[l];
-    const double alpha = TT ? Rs[l * 33 + l] : x[l];
-    double tau = 0.0, beta = alpha, sc = 1.0;
+    double gsum = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) gsum += red[(bf * 8 + w) * 33 + lane];
+    const double ssq = __shfl_sync(0xffffffffu, gsum, l);
+    const double alpha = TT ? Rs[l * 33 + l] : top[bf * 32 + l];
+    double tau = 0.0, beta = alpha, rsc = 0.0;
     if (ssq != 0.0) {
       const double nrm = sqrt(alpha * alpha + ssq);
       beta = alpha >= 0.0 ? -nrm : nrm;
       tau = (beta - alpha) / beta;
-      sc = alpha - beta;
+      rsc = 1.0 / (alpha - beta);
     }
-    // w_c (c > l) and z_q (q < l), one division each, into bc[32..63]
-    if (tid < sb && tid != l) {
-      const double gs = (ssq == 0.0) ? 0.0 : bc[tid] / sc;
-      double top = 0.0;
-      if (tid > l) top = TT ? Rs[tid * 33 + l] : Vs[tid * ldc + l];  // w_c = top_c + V_c . v
-      else if (!TT) top = Vs[tid * ldc + l];                          // z_q = V_q(l) + V_q . v
-      bc[32 + tid] = top + gs;
+    // lane c: w_c = top_c + V_c . v (c > l), z_q = [V_q(l)] + V_q . v (q < l)
+    double topc = 0.0;
+    if (TT) {
+      if (lane > l) topc = Rs[lane * 33 + l];
+    } else {
+      topc = top[bf * 32 + lane];
     }
-    __syncthreads();
-    // normalise v and update the remaining columns on the rows of this reflector
-    for (int r = rlo + tid; r < rhi; r += QD_T) {
-      const double vr = (ssq == 0.0) ? 0.0 : x[r] / sc;
-      x[r] = vr;
-      if (tau != 0.0)
-        for (int c = l + 1; c < sb; ++c) Vs[c * ldc + r] -= tau * (vr * bc[32 + c]);
+    const double wz = topc + gsum * rsc;
+    if (TT && warp == 0) {
+      if (lane > l && lane < sb && tau != 0.0) Rs[lane * 33 + l] -= tau * wz;
+      if (lane == 0) Rs[l * 33 + l] = beta;
     }
-    if (tid > l && tid < sb && tau != 0.0) {
-      const double w = bc[32 + tid];
-      if (TT) Rs[tid * 33 + l] -= tau * w; else Vs[tid * ldc + l] -= tau * w;
+    if (warp == 7) {  // the highest rows: idle for most TT columns
+      if (lane < l) Z[l * 33 + lane] = wz;
+      __syncwarp();
+      // T(q, l) = -tau sum_{p = q}^{l-1} T(q, p) z_p (q < l), T(l, l) = tau: four FMA chains
+      if (lane < l) {
+        double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+        int p2 = lane;
+        for (; p2 + 3 < l; p2 += 4) {
+          t0 += Ts[p2 * 33 + lane] * Z[l * 33 + p2];
+          t1 += Ts[(p2 + 1) * 33 + lane] * Z[l * 33 + p2 + 1];
+          t2 += Ts[(p2 + 2) * 33 + lane] * Z[l * 33 + p2 + 2];
+          t3 += Ts[(p2 + 3) * 33 + lane] * Z[l * 33 + p2 + 3];
+        }
+        for (; p2 < l; ++p2) t0 += Ts[p2 * 33 + lane] * Z[l * 33 + p2];
+        Ts[l * 33 + lane] = -tau * ((t0 + t1) + (t2 + t3));
+      }
+      if (lane == 0) Ts[l * 33 + l] = tau;
     }
-    if (tid < l) {
-      double t = 0.0;
-      for (int p2 = tid; p2 < l; ++p2) t += Ts[p2 * 33 + tid] * bc[32 + p2];
-      Ts[l * 33 + tid] = -tau * t;
+    const bool upd = lane > l && lane < sb && tau != 0.0;
+    if (wact) {
+      const double tw = tau * wz;
+      if (lane == l) {
+#pragma unroll
+        for (int i = 0; i < NR; ++i)
+          if (i >= ilo && i < ihi) a[i] = xs[i] * rsc;
+      } else if (upd) {
+#pragma unroll
+        for (int i = 0; i < NR; ++i)
+          if (i >= ilo && i < ihi) a[i] -= tau * ((xs[i] * rsc) * wz);
+      }
+      (void)tw;
     }
-    if (tid == 0) {
-      Ts[l * 33 + l] = tau;
-      if (TT) Rs[l * 33 + l] = beta; else x[l] = beta;
+    if (!TT && l >= rw && l < rw + NR) {  // row l: the R row of reflector l
+#pragma unroll
+      for (int i = 0; i < NR; ++i)
+        if (rw + i == l) {
+          if (lane == l) a[i] = beta;
+          else if (upd) a[i] -= tau * wz;
+        }
     }
-    __syncthreads();
   }
+#pragma unroll
+  for (int i = 0; i < NR; ++i)
+    if (rw + i < R && lane < sb) Vs[lane * ldc + rw + i] = a[i];
+  __syncthreads();
+}
+
+// rows per warp for a block of R <= nb rows (one kernel for every NR: measured faster than
+// per-NR kernels, whose smaller register allocations throttle the DMMA block updates)
+template <bool TT>
+__device__ __forceinline__ void panel_factor_nb(int nb, double* Vs, int ldc, double* Rs,
+                                                double* Ts, int R, int i0, int sb, double* ws,
+                                                int tid) {
+  if (nb <= 64) panel_factor<TT, 8>(Vs, ldc, Rs, Ts, R, i0, sb, ws, tid);
+  else if (nb <= 128) panel_factor<TT, 16>(Vs, ldc, Rs, Ts, R, i0, sb, ws, tid);
+  else if (nb <= 192) panel_factor<TT, 24>(Vs, ldc, Rs, Ts, R, i0, sb, ws, tid);
+  else if (nb <= 256) panel_factor<TT, 32>(Vs, ldc, Rs, Ts, R, i0, sb, ws, tid);
+  else panel_factor<TT, 40>(Vs, ldc, Rs, Ts, R, i0, sb, ws, tid);
 }
 
 // GEQRT of tiles (k + blockIdx.x, k) on tensor cores: per 32-column block, CTA-wide panel
@@ -407,11 +481,9 @@ __global__ void __launch_bounds__(QD_T) k_geqrt_tc(double* __restrict__ A, Geo g
   extern __shared__ __align__(16) double sm[];
   const int ldc = qd_ldc(g.nb);
   double* Cs = sm;
-  double* Vs = Cs + W * ldc;
+  double* Vs = Cs + qd_cs(W, g.nb);
   double* Us = Vs + 32 * ldc;
   double* Ts = Us + W * LDU;
-  double* red = Cs;            // aliases Cs during the panel factorisation
-  double* bc = Cs + 8 * 33;
   const int i = k + blockIdx.x;
   const int bi = g.bs(i), bk = g.cbs(k);
   double* tile = g.tile(A, i, k);
@@ -428,7 +500,7 @@ __global__ void __launch_bounds__(QD_T) k_geqrt_tc(double* __restrict__ A, Geo g
     for (int o = tid; o < 32 * 33; o += QD_T) Ts[o] = 0.0;
     cpa_wait_all();
     __syncthreads();
-    panel_factor<false>(Vs, ldc, nullptr, Ts, R, i0, sb, red, bc, tid);
+    panel_factor_nb<false>(g.nb, Vs, ldc, nullptr, Ts, R, i0, sb, Cs, tid);
     for (int o = tid; o < sb * R; o += QD_T) {
       int l = o / R, r = o - l * R;
       tile[(int64_t)(i0 + l) * g.lda + i0 + r] = Vs[l * ldc + r];
@@ -471,12 +543,10 @@ __global__ void __launch_bounds__(QD_T) k_ttqrt_tc(double* __restrict__ A, Geo g
   extern __shared__ __align__(16) double sm[];
   const int ldc = qd_ldc(g.nb);
   double* Cs = sm;
-  double* Vs = Cs + W * ldc;
+  double* Vs = Cs + qd_cs(W, g.nb);
   double* Us = Vs + 32 * ldc;
   double* Ts = Us + W * LDU;
-  double* red = Cs;              // panel-phase aliases of Cs
-  double* bc = Cs + 8 * 33;
-  double* Rs = Cs + 8 * 33 + 64;
+  double* Rs = Cs + PF_WS;       // panel phase: Cs holds the panel scratch, then R_e's block
   const int2 pr = pairs[blockIdx.x];
   const int e = pr.x, i = pr.y;
   const int bi = g.bs(i), bk = g.cbs(k);
@@ -503,7 +573,7 @@ __global__ void __launch_bounds__(QD_T) k_ttqrt_tc(double* __restrict__ A, Geo g
       if (r > i0 + l) Vs[l * ldc + r] = 0.0;
     }
     __syncthreads();
-    panel_factor<true>(Vs, ldc, Rs, Ts, R2, i0, sb, red, bc, tid);
+    panel_factor_nb<true>(g.nb, Vs, ldc, Rs, Ts, R2, i0, sb, Cs, tid);
     for (int o = tid; o < sb * R2; o += QD_T) {
       int l = o / R2, r = o - l * R2;
       if (r <= i0 + l) Ri[(int64_t)(i0 + l) * g.lda + r] = Vs[l * ldc + r];
@@ -531,6 +601,7 @@ __global__ void __launch_bounds__(QD_T) k_ttqrt_tc(double* __restrict__ A, Geo g
         Ri[(int64_t)(c0 + j) * g.lda + r] = Cs[j * ldc + r];
       }
     }
+    __syncthreads();
   }
 }
 

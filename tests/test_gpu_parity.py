@@ -289,8 +289,9 @@ def test_special_matrices_by_formula(H, name, crit, alpha):
     complements): the Householder vectors of such a panel, hence the trailing matrix after a QR
     step and every later criterion input, are decided by rounding (reading 30), so the
     decision vectors of two correct implementations may part after such a step.  What is compared:
-    the first decision (identical inputs), the stability verdict of the GPU's own run (HPL3 <= 16 or
-    not; MUMPS is expected to fail on some), and -- with the oracle's decision vector forced --
+    the first decision (identical inputs), the stability verdict of the GPU's own run when it took the
+    oracle's decisions (HPL3 <= 16 or not; MUMPS is expected to fail on some), and -- with the
+    oracle's decision vector forced --
     that the GPU factors solve the system as well as the oracle's (HPL3 <= 16 for several
     right-hand sides whenever the oracle's is)."""
     N, nb = 512, 64
@@ -300,7 +301,8 @@ def test_special_matrices_by_formula(H, name, crit, alpha):
     assert f.decisions()[0] == fo.dec[0]
     h3_o = O.hpl3(A, O.solve(fo, b), b)
     h3_g = O.hpl3(A, x, b)
-    assert (h3_g <= 16.0) == (h3_o <= 16.0), (h3_g, h3_o)
+    if np.array_equal(f.decisions(), fo.dec):  # same path: the same stability verdict
+        assert (h3_g <= 16.0) == (h3_o <= 16.0), (h3_g, h3_o)
     dA = H.to_colmajor(A)
     ff = H.hlq_factor_ex(dA, N, nb, crit, alpha, forced=fo.dec)
     np.testing.assert_array_equal(ff.decisions(), fo.dec)
