@@ -372,11 +372,20 @@ __device__ void panel_factor(double* Vs, int ldc, double* Rs, double* Ts, int R,
           *reinterpret_cast<double2*>(xs + i) = make_double2(a[i], a[i + 1]);
       }
       __syncwarp();
+      if (ilo == 0 && ihi == NR) {  // every row of the warp (no per-row predicates)
 #pragma unroll
-      for (int i = 0; i < NR; i += 2) {
-        const double2 x = *reinterpret_cast<const double2*>(xs + i);
-        if (i >= ilo && i < ihi) part += a[i] * x.x;
-        if (i + 1 >= ilo && i + 1 < ihi) part += a[i + 1] * x.y;
+        for (int i = 0; i < NR; i += 2) {
+          const double2 x = *reinterpret_cast<const double2*>(xs + i);
+          part += a[i] * x.x;
+          part += a[i + 1] * x.y;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < NR; i += 2) {
+          const double2 x = *reinterpret_cast<const double2*>(xs + i);
+          if (i >= ilo && i < ihi) part += a[i] * x.x;
+          if (i + 1 >= ilo && i + 1 < ihi) part += a[i + 1] * x.y;
+        }
       }
     }
     red[(bf * 8 + warp) * 33 + lane] = part;
@@ -430,17 +439,22 @@ __device__ void panel_factor(double* Vs, int ldc, double* Rs, double* Ts, int R,
     }
     const bool upd = lane > l && lane < sb && tau != 0.0;
     if (wact) {
-      const double tw = tau * wz;
       if (lane == l) {
 #pragma unroll
         for (int i = 0; i < NR; ++i)
           if (i >= ilo && i < ihi) a[i] = xs[i] * rsc;
       } else if (upd) {
+        // a -= tau (x / (alpha - beta)) w_c, as one FMA per element with c = tau w_c / (alpha - beta)
+        const double cf = tau * wz * rsc;
+        if (ilo == 0 && ihi == NR) {
 #pragma unroll
-        for (int i = 0; i < NR; ++i)
-          if (i >= ilo && i < ihi) a[i] -= tau * ((xs[i] * rsc) * wz);
+          for (int i = 0; i < NR; ++i) a[i] -= xs[i] * cf;
+        } else {
+#pragma unroll
+          for (int i = 0; i < NR; ++i)
+            if (i >= ilo && i < ihi) a[i] -= xs[i] * cf;
+        }
       }
-      (void)tw;
     }
     if (!TT && l >= rw && l < rw + NR) {  // row l: the R row of reflector l
 #pragma unroll
