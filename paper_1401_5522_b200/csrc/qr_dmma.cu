@@ -352,6 +352,8 @@ __device__ void panel_factor(double* Vs, int ldc, double* Rs, double* Ts, int R,
   double* xs = tauv + 32 + warp * 40;  // this warp's copy of column l (16-byte aligned)
   const int rw = warp * NR;  // first row of this warp
   const int lmax = TT ? sb : min(sb, R);
+  int pl = -1;  // TT, warp 0: the pending R_e row update
+  double ptau = 0.0, pwz = 0.0, pbeta = 0.0;
   double a[NR];
 #pragma unroll
   for (int i = 0; i < NR; ++i) a[i] = (rw + i < R && lane < sb) ? Vs[lane * ldc + rw + i] : 0.0;
@@ -366,6 +368,7 @@ __device__ void panel_factor(double* Vs, int ldc, double* Rs, double* Ts, int R,
     const bool wact = ilo < ihi;
     double part = 0.0;
     if (wact) {
+      __syncwarp();  // the previous column's reads of xs are done
       if (lane == l) {
 #pragma unroll
         for (int i = 0; i < NR; i += 2)
@@ -416,8 +419,16 @@ __device__ void panel_factor(double* Vs, int ldc, double* Rs, double* Ts, int R,
     }
     const double wz = topc + gsum * rsc;
     if (TT && warp == 0) {
-      if (lane > l && lane < sb && tau != 0.0) Rs[lane * 33 + l] -= tau * wz;
-      if (lane == 0) Rs[l * 33 + l] = beta;
+      // R_e row l (Rs[c*33 + l], c >= l) is written one column late: every warp reads it in this
+      // column (alpha, top_c) and the next barrier orders the write after those reads
+      if (pl >= 0) {
+        if (lane > pl && lane < sb && ptau != 0.0) Rs[lane * 33 + pl] -= ptau * pwz;
+        if (lane == 0) Rs[pl * 33 + pl] = pbeta;
+      }
+      pl = l;
+      ptau = tau;
+      pwz = wz;
+      pbeta = beta;
     }
     if (warp == 7) {  // the highest rows: idle for most TT columns
       if (lane < l) Z[l * 33 + lane] = wz;
@@ -469,6 +480,11 @@ __device__ void panel_factor(double* Vs, int ldc, double* Rs, double* Ts, int R,
   for (int i = 0; i < NR; ++i)
     if (rw + i < R && lane < sb) Vs[lane * ldc + rw + i] = a[i];
   __syncthreads();
+  if (TT && warp == 0 && pl >= 0) {
+    if (lane > pl && lane < sb && ptau != 0.0) Rs[lane * 33 + pl] -= ptau * pwz;
+    if (lane == 0) Rs[pl * 33 + pl] = pbeta;
+  }
+  if (TT) __syncthreads();
 }
 
 // rows per warp for a block of R <= nb rows (one kernel for every NR: measured faster than
