@@ -436,6 +436,47 @@ def tsmqr(V2: np.ndarray, T: np.ndarray, ib: int, C1: np.ndarray, C2: np.ndarray
 # ----------------------------------------------------------------------------------------------
 # a8-a11: QR step = HQR elimination list (Alg. 3, Alg. 4), plan(k, n, D)
 # ----------------------------------------------------------------------------------------------
+def a2_factor(A: np.ndarray, N: int, nb: int, k: int, ib: int):
+    """NEXT f4, variant A2 Factor: A_kk <- GEQRT(A_kk) in place (V strictly below the
+    diagonal, U_kk = R on and above it).  Returns (T_kk, R, zero_pivot): the criterion reads
+    |U_jj| = |R_jj| (MUMPS pivots) and an exact zero on R's diagonal is a zero pivot (ledger 7)."""
+    rk = tsl(N, nb, k)
+    T = geqrt(A[rk, rk], ib)
+    R = np.triu(A[rk, rk])
+    return T, R, bool(np.any(np.diag(R) == 0.0))
+
+
+def a2_inv_norm1(A: np.ndarray, N: int, nb: int, k: int, T: np.ndarray, ib: int) -> float:
+    """||A_kk^-1||_1 = ||U_kk^-1 Q_kk^T||_1 exactly (ledger 3) from the A2 factors: Q^T formed by
+    applying the stored reflectors to the identity (UNMQR), then a triangular solve with U_kk."""
+    rk = tsl(N, nb, k)
+    b = rk.stop - rk.start
+    QT = np.eye(b)
+    unmqr(A[rk, rk], T, ib, QT)
+    with np.errstate(all="ignore"):
+        X = solve_triangular(np.triu(A[rk, rk]), QT, lower=False, check_finite=False)
+    return float(np.max(np.sum(np.abs(X), axis=0)))
+
+
+def lu_step_a2(A: np.ndarray, N: int, nb: int, k: int, T: np.ndarray, ib: int):
+    """Variant A2 Eliminate / Apply / Update on the in-place GEQRT factors of A_kk."""
+    n = ntiles(N, nb)
+    rk = tsl(N, nb, k)
+    k0, k1 = rk.start, rk.stop
+    if k + 1 == n:
+        return
+    U = np.triu(A[rk, rk])
+    # Eliminate: A_ik <- A_ik U_kk^-1 for i > k (P:383-385)
+    with np.errstate(all="ignore"):
+        A[k1:N, k0:k1] = solve_triangular(U, A[k1:N, k0:k1].T, trans="T", lower=False,
+                                          check_finite=False).T
+    # Apply: A_kj <- Q_kk^T A_kj for j > k (P:387-389), with the reflectors V_kk of A_kk
+    unmqr(A[rk, rk], T, ib, A[k0:k1, k1:N])
+    # Update: A_ij <- A_ij - A_ik A_kj (P:391-392, "the exact same as in (A1)")
+    with np.errstate(all="ignore"):
+        A[k1:N, k1:N] -= A[k1:N, k0:k1] @ A[k0:k1, k1:N]
+
+
 def _domains(k: int, n: int, D: int):
     """Rows k..n-1 split into domains by (i mod D) (2D block-cyclic rows), each ascending,
     domains ordered by their first row."""
@@ -499,7 +540,9 @@ class QRStepData:
 
 
 def qr_step(A: np.ndarray, N: int, nb: int, k: int, D: int, ib: int,
-            tree: str = "greedy") -> QRStepData:
+            tree: str = "greedy", T_kk=None) -> QRStepData:
+    """T_kk: the diagonal tile was already factored in place by GEQRT (LU variant A2: "the
+    factorization of A_kk is not discarded but rather used to continue the QR step")."""
     n = ntiles(N, nb)
     ck = tsl(N, nb, k)
     right = slice(ck.stop, N)
@@ -509,7 +552,7 @@ def qr_step(A: np.ndarray, N: int, nb: int, k: int, D: int, ib: int,
     for h in geqrt_rows:
         rh = tsl(N, nb, h)
         tile = A[rh, ck]
-        data.T_geqrt[h] = geqrt(tile, ib)
+        data.T_geqrt[h] = T_kk if (h == k and T_kk is not None) else geqrt(tile, ib)
         if right.start < N:
             unmqr(tile, data.T_geqrt[h], ib, A[rh, right])
     # TS eliminations in plan order (Alg. 4a lines 2, 5)
@@ -569,15 +612,19 @@ class Factors:
     growth: float
     status: int
     stats: list
+    lu_variant: str = "A1"
 
 
 def hybrid_factor(A_in: np.ndarray, nb: int, crit: int = CRIT_MAX, alpha: float = 1.0, D: int = 1,
                   ib: int = 32, mumps_reading: int = 0, forced=None, track_growth: bool = True,
                   tie_tol: float = 1e-10, variant: int = 0, on_step=None,
-                  tree: str = "greedy", invnorm: str = "exact") -> Factors:
+                  tree: str = "greedy", invnorm: str = "exact", lu_variant: str = "A1") -> Factors:
     """Alg. 1: for each step, speculative tile LU, criterion, LU or QR step.
 
     invnorm: "exact" (ledger 3, default) or "estimate" (NEXT f3: inv_norm1_estimate).
+    lu_variant: "A1" (Alg. 2, default) or "A2" (NEXT f4: the diagonal tile is
+    QR-factored in place before the criterion; an LU step eliminates with U_kk = R and applies
+    Q_kk^T, a QR step continues from that factorization).
     forced: decision vector used verbatim (C3); variant=1 uses the reversed-chunk GEMM (noise floor).
     on_step(k, A_before, A_after, d): optional test hook called after each step with copies.
     """
@@ -589,14 +636,26 @@ def hybrid_factor(A_in: np.ndarray, nb: int, crit: int = CRIT_MAX, alpha: float 
     near_tie = np.zeros(n, dtype=bool)
     ipivs, qrs, stats = {}, {}, []
     status = 0
+    if lu_variant not in ("A1", "A2"):
+        raise ValueError("lu_variant must be 'A1' or 'A2'")
+    if lu_variant == "A2" and invnorm != "exact":
+        raise ValueError("the A2 variant computes the exact ||A_kk^-1||_1 only")
+    a2 = lu_variant == "A2"
     g0 = max_tile_norm(A, N, nb, 0) if track_growth else 1.0
     g = g0
     for k in range(n):
         rk = tsl(N, nb, k)
         A_before = A.copy() if on_step is not None else None
         s, lmax, amax = panel_stats(A, N, nb, k)
-        # Factor (speculative, out of place: the paper's Backup Panel P:634-640 becomes a copy)
-        W, ipiv, zp = getrf(A[rk, rk])
+        T_kk = None
+        if a2 and not (forced is None and alpha == 0.0) and not (forced is not None
+                                                                  and int(forced[k]) == QR):
+            # A2 Factor: in place; a QR decision continues from it
+            T_kk, W, zp = a2_factor(A, N, nb, k, ib)
+            ipiv = np.arange(rk.stop - rk.start, dtype=np.int32)
+        else:
+            # Factor (speculative, out of place: the paper's Backup Panel P:634-640 becomes a copy)
+            W, ipiv, zp = getrf(A[rk, rk])
         inv = float("nan")
         mg = float("nan")
         if forced is not None:
@@ -612,7 +671,10 @@ def hybrid_factor(A_in: np.ndarray, nb: int, crit: int = CRIT_MAX, alpha: float 
             d = LU  # ledger 4
         else:
             if crit in (CRIT_MAX, CRIT_SUM):
-                inv = inv_norm1_from_lu(W) if invnorm == "exact" else inv_norm1_estimate(W)
+                if a2:
+                    inv = a2_inv_norm1(A, N, nb, k, T_kk, ib)
+                else:
+                    inv = inv_norm1_from_lu(W) if invnorm == "exact" else inv_norm1_estimate(W)
                 lu, mg = criterion_max_sum(crit, alpha, inv, s)
             else:
                 lu, mg = criterion_mumps(alpha, W, lmax, amax, mumps_reading)
@@ -626,7 +688,10 @@ def hybrid_factor(A_in: np.ndarray, nb: int, crit: int = CRIT_MAX, alpha: float 
         margin[k] = mg
         stats.append({"k": k, "s": s, "local_max": lmax, "away_max": amax, "inv_norm": inv,
                       "zero_pivot": zp})
-        if d == LU:
+        if d == LU and T_kk is not None:
+            lu_step_a2(A, N, nb, k, T_kk, ib)
+            qrs[k] = QRStepData(T_geqrt={k: T_kk})  # Q_kk for the solve's forward pass
+        elif d == LU:
             lu_step(A, N, nb, k, W, ipiv)
             if variant == 1 and k + 1 < n:
                 # undo the standard update and redo it with the reversed-chunk order
@@ -635,7 +700,7 @@ def hybrid_factor(A_in: np.ndarray, nb: int, crit: int = CRIT_MAX, alpha: float 
                 lu_step_update_variant(A, N, nb, k)
             ipivs[k] = ipiv
         else:
-            qrs[k] = qr_step(A, N, nb, k, D, ib, tree)
+            qrs[k] = qr_step(A, N, nb, k, D, ib, tree, T_kk=T_kk)
         if track_growth and k + 1 < n:
             g = max(g, max_tile_norm(A, N, nb, k + 1))
         if on_step is not None:
@@ -652,7 +717,8 @@ def hybrid_factor(A_in: np.ndarray, nb: int, crit: int = CRIT_MAX, alpha: float 
     growth = (g / g0) if (track_growth and g0 > 0) else float("nan")
     if track_growth and not np.isfinite(g):
         growth = math.inf
-    return Factors(A, N, nb, n, ib, D, tree, dec, margin, near_tie, ipivs, qrs, growth, status, stats)
+    return Factors(A, N, nb, n, ib, D, tree, dec, margin, near_tie, ipivs, qrs, growth, status, stats,
+                   lu_variant)
 
 
 # ----------------------------------------------------------------------------------------------
@@ -668,7 +734,12 @@ def apply_transforms(f: Factors, x: np.ndarray) -> np.ndarray:
     for k in range(n):
         rk = tsl(N, nb, k)
         k0, k1 = rk.start, rk.stop
-        if f.dec[k] == LU:
+        if f.dec[k] == LU and f.lu_variant == "A2":
+            # A2: x_k <- Q_kk^T x_k, then x_i -= L_ik x_k
+            unmqr(A[rk, rk], f.qr[k].T_geqrt[k], ib, x[rk, :])
+            if k1 < N:
+                x[k1:N, :] -= A[k1:N, k0:k1] @ x[rk, :]
+        elif f.dec[k] == LU:
             ipiv = f.ipiv[k]
             for c in range(k1 - k0):
                 p = int(ipiv[c])

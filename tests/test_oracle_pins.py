@@ -474,3 +474,100 @@ def test_counter_generator_matches_plain_int_reference():
     assert A.flags["F_CONTIGUOUS"]
     u = I.uniform_matrix(0, 256).ravel()
     assert -0.5 <= u.min() and u.max() < 0.5 and abs(u.mean()) < 0.01
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT f4: LU step variant A2
+# ---------------------------------------------------------------------------------------------
+def _a2_reconstruct(f):
+    """A from the A2 all-LU factors by block elimination algebra: with A_kk = Q_k R_k,
+    L~_ik = (stored L_ik) Q_k^T, U~_kk = Q_k R_k, U~_kj = Q_k (stored A_kj), A = sum_k L~_:k U~_k:."""
+    N, nb, ib = f.N, f.nb, f.ib
+    F = f.A
+    A = np.zeros((N, N))
+    for k in range(f.n):
+        rk = O.tsl(N, nb, k)
+        k0, k1 = rk.start, rk.stop
+        Qt = np.eye(k1 - k0)
+        O.unmqr(F[rk, rk], f.qr[k].T_geqrt[k], ib, Qt)  # Q_k^T, independent of the step code
+        Q = Qt.T
+        Lt = np.vstack([np.eye(k1 - k0), F[k1:N, k0:k1] @ Qt])
+        Ut = np.hstack([Q @ np.triu(F[rk, rk]), Q @ F[k0:k1, k1:N]])
+        A[k0:N, k0:N] += Lt @ Ut
+    return A
+
+
+@pytest.mark.parametrize("N,nb", [(384, 64), (300, 64)])
+def test_a2_all_lu_is_block_elimination(N, nb):
+    """alpha = inf under A2: the packed factors reassemble A (block LU with QR-factored pivots).
+    Block elimination has no pivoting across tiles, so the input is made diagonally dominant
+    (stable: the reassembly error is then at rounding level)."""
+    A = I.uniform_matrix(0, N) + (N / 2.0) * np.eye(N)
+    f = O.hybrid_factor(A, nb, O.CRIT_MAX, math.inf, lu_variant="A2")
+    assert np.all(f.dec == O.LU)
+    Ar = _a2_reconstruct(f)
+    assert np.linalg.norm(Ar - A) / np.linalg.norm(A) < 1e-13
+    b = I.uniform_rhs(0, N)
+    x = O.solve(f, b)
+    assert np.allclose(x, np.linalg.solve(A, b), rtol=0, atol=1e-9 * np.abs(x).max())
+
+
+def test_a2_schur_complement_equals_a1():
+    """The Schur complement A22 - A21 A11^-1 A12 does not depend on how A11 is factored: after an LU
+    step, the A1 (GETRF) and A2 (GEQRT) trailing matrices agree to rounding."""
+    A = I.normal_system(1, 512)[0]
+    trail = {}
+
+    def hook(tag):
+        def on_step(k, before, after, d):
+            if k == 0:
+                trail[tag] = after[128:, 128:].copy()
+        return on_step
+    O.hybrid_factor(A, 128, O.CRIT_MAX, math.inf, on_step=hook("A1"))
+    O.hybrid_factor(A, 128, O.CRIT_MAX, math.inf, lu_variant="A2", on_step=hook("A2"))
+    d = np.linalg.norm(trail["A1"] - trail["A2"]) / np.linalg.norm(trail["A1"])
+    assert d < 1e-12, d
+
+
+@pytest.mark.parametrize("dist", ["uniform", "normal"])
+def test_a2_criterion_inverse_norm_is_exact(dist):
+    """||R^-1 Q^T||_1 from the in-place GEQRT factors equals ||A_kk^-1||_1 of the dense inverse."""
+    A = I.uniform_matrix(5, 256) if dist == "uniform" else I.normal_system(5, 256)[0]
+    W = np.array(A, order="F", copy=True)
+    T, R, zp = O.a2_factor(W, 256, 128, 0, 32)
+    v = O.a2_inv_norm1(W, 256, 128, 0, T, 32)
+    ref = np.linalg.norm(np.linalg.inv(A[:128, :128]), 1)
+    assert not zp
+    assert abs(v - ref) <= 1e-11 * ref
+    # MUMPS pivots |U_jj| = |R_jj| are the absolute diagonal of Householder R (numpy, up to signs)
+    Rn = np.linalg.qr(A[:128, :128], mode="r")
+    assert np.allclose(np.abs(np.diag(R)), np.abs(np.diag(Rn)), rtol=1e-12, atol=0)
+
+
+def test_a2_qr_steps_reuse_the_diagonal_factorization():
+    """A QR decision continues from the A2 GEQRT: with Max alpha = 1 (QR at every step
+    but the last) the A2 factors equal A1's bit for bit except the last diagonal tile, which A2
+    QR-factors (|R| = numpy's) where A1 LU-factors it."""
+    N, nb = 512, 64
+    A = I.uniform_matrix(0, N)
+    f1 = O.hybrid_factor(A, nb, O.CRIT_MAX, 1.0)
+    f2 = O.hybrid_factor(A, nb, O.CRIT_MAX, 1.0, lu_variant="A2")
+    assert np.array_equal(f1.dec, f2.dec) and f1.dec[-1] == O.LU and np.all(f1.dec[:-1] == O.QR)
+    last = slice(N - nb, N)
+    F1, F2 = f1.A.copy(), f2.A.copy()
+    F1[last, last] = 0.0
+    F2[last, last] = 0.0
+    assert np.array_equal(F1, F2)
+    # the last tile before its factorization is the same in both runs: A1 holds its LU, A2 its QR
+    Lw = np.tril(f1.A[last, last], -1) + np.eye(nb)
+    S = Lw @ np.triu(f1.A[last, last])
+    S = S[np.argsort(_perm_of(f1.ipiv[f1.n - 1]))]
+    assert np.allclose(np.abs(np.diag(np.triu(f2.A[last, last]))),
+                       np.abs(np.diag(np.linalg.qr(S, mode="r"))), rtol=1e-10, atol=0)
+
+
+def _perm_of(ipiv):
+    p = np.arange(len(ipiv))
+    for c, r in enumerate(ipiv):
+        p[[c, r]] = p[[r, c]]
+    return p
