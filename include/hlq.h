@@ -79,7 +79,15 @@ typedef struct {
   int32_t profile;           /* 1: time every kernel class with CUDA events (hlq_get_profile)    */
   int32_t invnorm_estimate;  /* 0 (default): ||A_kk^-1||_1 exact (reading 3); 1: the
                                 Hager/Higham estimate in LAPACK dlacn2 order (NEXT f3) */
+  int32_t lu_variant;        /* HLQ_LU_A1 (default, Alg. 2) or HLQ_LU_A2 (NEXT f4): the
+                                diagonal tile is QR-factored in place (GEQRT) before the criterion,
+                                which reads ||U_kk^-1 Q_kk^T||_1 / |U_jj| from it; an LU step then
+                                eliminates with U_kk^-1 and applies Q_kk^T to row k, a QR step
+                                continues from that factorization.  A2 needs ib = 32, the exact
+                                inverse norm and one GPU (hlq_factor_dist rejects it: -8). */
 } hlq_options;
+
+enum { HLQ_LU_A1 = 0, HLQ_LU_A2 = 1 };
 
 typedef struct {
   int64_t N;

@@ -188,7 +188,8 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   if (opt.tie_rel_tol == 0.0) opt.tie_rel_tol = 1e-10;
   if (opt.ib < 1 || opt.ib > 32 || opt.tree_domains < 1 || opt.tree != HLQ_TREE_GREEDY ||
       opt.mumps_reading < 0 || opt.mumps_reading > 1 || opt.invnorm_estimate < 0 ||
-      opt.invnorm_estimate > 1)
+      opt.invnorm_estimate > 1 || opt.lu_variant < HLQ_LU_A1 || opt.lu_variant > HLQ_LU_A2 ||
+      (opt.lu_variant == HLQ_LU_A2 && (opt.ib != 32 || opt.invnorm_estimate != 0)))
     return -6;
   int64_t lda = opt.lda ? opt.lda : N;
   if (lda < N) return -6;
@@ -208,6 +209,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   f->ib = opt.ib;
   f->D = opt.tree_domains;
   f->crit = criterion;
+  f->lu_variant = opt.lu_variant;
   f->alpha = alpha;
   f->st = (cudaStream_t)opt.stream;
   f->blocking = opt.blocking != 0;
@@ -331,6 +333,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
     return -1;
   };
   const bool criterion_needed = !opt.forced && alpha > 0.0 && !alpha_inf;
+  const bool a2 = opt.lu_variant == HLQ_LU_A2;
   for (int k = 0; k < n; ++k) {
     const DevWork& wk = wpar[k & 1];
     const int known = known_of(k);
@@ -345,12 +348,29 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
         P.end(sp);
       }
       P.begin(HLQ_PROF_GETRF, sp);
-      launch_getrf(A, g, k, wk, true, sp);
-      launch_tri_inv(g, k, wk, wk.scratch, wk.scratch + (size_t)nb * nb, sp);
+      if (a2) {
+        // A2 Factor: GEQRT of the diagonal tile in place (a one-tile view of A), then
+        // W <- the tile, Li <- Q_kk^T (UNMQR applied to I), Ui <- U_kk^-1 (L^-1 is not needed)
+        const int bk = g.bs(k);
+        Geo gk = g;
+        gk.N = bk;
+        gk.Nc = bk;
+        gk.n = 1;
+        double* Akk = g.tile(A, k, k);
+        const double* Tkk = w.Tg + tri_index(k, k, n) * (int64_t)ib * nb;
+        launch_qr_panel_tc(Akk, gk, 0, ib, const_cast<double*>(Tkk), nullptr, nullptr, 0, nullptr,
+                           false, sp);
+        launch_a2_prep(A, g, k, wk, sp);
+        launch_tri_inv(g, k, wk, wk.ws_panel, wk.scratch + (size_t)nb * nb, sp);
+        launch_qr_update2(Akk, gk, 0, Tkk, nullptr, 0, false, wk.scratch, nb, bk, nullptr, sp);
+      } else {
+        launch_getrf(A, g, k, wk, true, sp);
+        launch_tri_inv(g, k, wk, wk.scratch, wk.scratch + (size_t)nb * nb, sp);
+      }
       P.end(sp);
       if (criterion_needed && criterion != HLQ_CRIT_MUMPS) {
         P.begin(HLQ_PROF_CRITERION, sp);
-        launch_invnorm(g, k, wk, sp, opt.invnorm_estimate);
+        launch_invnorm(g, k, wk, sp, opt.invnorm_estimate, a2 ? 1 : 0);
         P.end(sp);
       }
     } else {
@@ -362,7 +382,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
     P.end(sp);
     if (known != HLQ_DEC_QR) {
       P.begin(HLQ_PROF_LU_TRSM, sp);
-      launch_lu_panel(A, g, k, wk, sp);
+      launch_lu_panel(A, g, k, wk, sp, /*commit=*/!a2);
       // keep L_kk^-1, U_kk^-1 and the composed permutation for the solve (LU steps only)
       launch_copy_block(w.luinv + (size_t)k * 2 * nb * nb, nb, wk.scratch, nb, nb, 2 * nb, nullptr,
                         w.dec, k, sp);
@@ -373,7 +393,8 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
     }
     if (known != HLQ_DEC_LU) {
       P.begin(HLQ_PROF_QR_GEQRT, sp);
-      launch_qr_panel(A, g, k, ib, f->lvl_ptr[k].data(), f->lvl_cnt[k].data(), nl, wk, sp);
+      launch_qr_panel(A, g, k, ib, f->lvl_ptr[k].data(), f->lvl_cnt[k].data(), nl, wk, sp,
+                      /*diag_done=*/a2 && known != HLQ_DEC_QR);
       P.end(sp);
     }
     cudaEventRecord(ev_panel, sp);
@@ -475,7 +496,8 @@ int hlq_solve(hlq_factors_t f, const double* b, double* x) {
   for (int k = 0; k < g.n; ++k) {
     if (f->dec[k] == HLQ_DEC_LU)
       launch_solve_lu_fwd_inv(f->A, g, k, f->w.luinv + (size_t)k * 2 * g.nb * g.nb,
-                              f->w.luperm + (size_t)k * g.nb, x, f->w.solve_t, st);
+                              f->w.luperm + (size_t)k * g.nb, x, f->w.solve_t, st,
+                              /*dense=*/f->lu_variant == HLQ_LU_A2);
     else
       launch_qr_apply(f->A, g, k, f->ib, f->w.Tg, f->w.Ttt, f->lvl_ptr[k].data(),
                       f->lvl_cnt[k].data(), (int)f->lvl_cnt[k].size(), x, g.N, 1, nullptr, st);
@@ -512,7 +534,9 @@ int hlq_get_info(hlq_factors_t f, hlq_info* info) {
   for (int k = 0; k < g.n; ++k) {
     double b = g.bs(k), M = (double)(g.N - g.r0(k) - g.bs(k));
     double lu = 2.0 / 3.0 * b * b * b + 2.0 * M * b * b + 2.0 * M * M * b;  // Table I
-    tf += f->dec[k] == HLQ_DEC_QR ? 2.0 * lu : lu;
+    // A2: Factor and Apply cost twice A1's: 4/3 b^3 + M b^2 + 2 M b^2 + 2 M^2 b
+    const double lu2 = 4.0 / 3.0 * b * b * b + 3.0 * M * b * b + 2.0 * M * M * b;
+    tf += f->dec[k] == HLQ_DEC_QR ? 2.0 * lu : (f->lu_variant == HLQ_LU_A2 ? lu2 : lu);
     if (f->dec[k] == HLQ_DEC_QR) info->qr_steps++;
     if (f->flags[k] & HLQ_FLAG_NEAR_TIE) info->near_ties++;
     if (f->flags[k] & HLQ_FLAG_HINTED) info->hinted++;
@@ -531,9 +555,10 @@ int hlq_get_profile(hlq_factors_t f, double* ms, double* flops, int64_t* launche
   for (int k = 0; k < g.n; ++k) {
     double b = g.bs(k), M = (double)(g.N - g.r0(k) - g.bs(k));
     if (f->dec[k] == HLQ_DEC_LU) {
-      fl[HLQ_PROF_GETRF] += 2.0 / 3.0 * b * b * b;
+      const bool a2 = f->lu_variant == HLQ_LU_A2;  // Factor and Apply cost twice
+      fl[HLQ_PROF_GETRF] += (a2 ? 4.0 : 2.0) / 3.0 * b * b * b;
       fl[HLQ_PROF_LU_TRSM] += M * b * b;             // Table I: TRSM
-      fl[HLQ_PROF_LU_UPDATE] += M * b * b + 2.0 * M * M * b;  // Table I: SWPTRSM + GEMM
+      fl[HLQ_PROF_LU_UPDATE] += (a2 ? 2.0 : 1.0) * M * b * b + 2.0 * M * M * b;  // SWPTRSM + GEMM
     } else {
       double m = M / b;                              // trailing tiles (fractional if ragged)
       fl[HLQ_PROF_QR_GEQRT] += (m + 1.0) * 4.0 / 3.0 * b * b * b + m * 2.0 / 3.0 * b * b * b;

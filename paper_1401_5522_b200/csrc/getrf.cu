@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(256) k_tri_inv(const double* __restrict__ W, i
 // ||U^-1 L^-1||_1: warp per column j of X = Ui * Li; column abs-sum; atomic max.
 __global__ void __launch_bounds__(256) k_invnorm(const double* __restrict__ Li,
                                                  const double* __restrict__ Ui, int bk, int ldw,
-                                                 double* inv_norm) {
+                                                 double* inv_norm, int dense) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j = blockIdx.x * 8 + warp;
   if (j >= bk) return;
@@ -364,7 +364,8 @@ __global__ void __launch_bounds__(256) k_invnorm(const double* __restrict__ Li,
   double colsum = 0.0;
   for (int r = lane; r < bk; r += 32) {
     double x = 0.0;
-    for (int c = (r > j ? r : j); c < bk; ++c) x += Ui[(int64_t)c * ldw + r] * lj[c];
+    const int cb = dense ? r : (r > j ? r : j);  // dense Li (A2: Q^T) has no zero upper part
+    for (int c = cb; c < bk; ++c) x += Ui[(int64_t)c * ldw + r] * lj[c];
     colsum += fabs(x);
   }
 #pragma unroll
@@ -513,7 +514,42 @@ void launch_tri_inv(Geo g, int k, const DevWork& w, double* Li, double* Ui, cuda
   { ::hlq::g_launches++; k_tri_inv<<<grid, 256, sizeof(double) * 8 * bk, st>>>(w.W, bk, g.nb, Li, Ui); }
 }
 
-void launch_invnorm(Geo g, int k, DevWork w, cudaStream_t st, int estimate) {
+// NEXT f4, variant A2: the diagonal tile is QR-factored in place; W <- the tile, zero
+// pivot = an exact zero on R's diagonal, no row interchanges (identity ipiv / permutation), Li <- I.
+__global__ void k_a2_prep(const double* __restrict__ A, Geo g, int k, double* __restrict__ W,
+                          int* __restrict__ zp, int* __restrict__ ipiv_step, int* __restrict__ perm,
+                          double* __restrict__ Li) {
+  const int bk = g.bs(k);
+  const double* Akk = g.tile(const_cast<double*>(A), k, k);
+  __shared__ int zero;
+  if (threadIdx.x == 0) zero = 0;
+  __syncthreads();
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < bk * bk;
+       idx += gridDim.x * blockDim.x) {
+    const int c = idx / bk, r = idx - c * bk;
+    const double v = Akk[(int64_t)c * g.lda + r];
+    W[(int64_t)c * g.nb + r] = v;
+    Li[(int64_t)c * g.nb + r] = (r == c) ? 1.0 : 0.0;
+    if (r == c && v == 0.0) zero = 1;
+  }
+  __syncthreads();
+  if (blockIdx.x == 0) {
+    for (int c = threadIdx.x; c < bk; c += blockDim.x) {
+      ipiv_step[c] = c;
+      perm[c] = c;
+    }
+  }
+  if (threadIdx.x == 0 && zero) atomicOr(zp, 1);
+}
+
+void launch_a2_prep(const double* A, Geo g, int k, DevWork w, cudaStream_t st) {
+  cudaMemsetAsync(w.zp, 0, sizeof(int), st);
+  int* perm = reinterpret_cast<int*>(w.scratch + (size_t)2 * g.nb * g.nb);
+  ::hlq::g_launches++;
+  k_a2_prep<<<8, 256, 0, st>>>(A, g, k, w.W, w.zp, w.ipiv + (size_t)k * g.nb, perm, w.scratch);
+}
+
+void launch_invnorm(Geo g, int k, DevWork w, cudaStream_t st, int estimate, int dense) {
   const int bk = g.bs(k);
   const double* Li = w.scratch;                       // filled by launch_tri_inv
   const double* Ui = w.scratch + (size_t)g.nb * g.nb;
@@ -523,7 +559,7 @@ void launch_invnorm(Geo g, int k, DevWork w, cudaStream_t st, int estimate) {
     return;
   }
   cudaMemsetAsync(w.inv_norm, 0, sizeof(double), st);
-  { ::hlq::g_launches++; k_invnorm<<<(bk + 7) / 8, 256, 0, st>>>(Li, Ui, bk, g.nb, w.inv_norm); }
+  { ::hlq::g_launches++; k_invnorm<<<(bk + 7) / 8, 256, 0, st>>>(Li, Ui, bk, g.nb, w.inv_norm, dense); }
 }
 
 }  // namespace hlq

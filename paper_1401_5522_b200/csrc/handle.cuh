@@ -70,6 +70,7 @@ struct hlq_factors_s {
   double* A = nullptr;
   Geo g{};
   int ib = 32, D = 1, crit = 0;
+  int lu_variant = 0;  // HLQ_LU_A1 / HLQ_LU_A2
   double alpha = 1.0;
   cudaStream_t st = nullptr;
   bool blocking = true;

@@ -83,9 +83,14 @@ void launch_dgemm(double* C, int64_t ldc, const double* A, int64_t lda, const do
                   int64_t ldb, int64_t M, int64_t N, int K, bool neg, bool beta,
                   const uint8_t* dec, int k, int want, cudaStream_t st,
                   double* colpart = nullptr, int64_t ldp = 0);
+// tt = false: GEQRT of tiles i_first.. (i_first < 0: k..n-1); tt = true: TTQRT of the pairs
 void launch_qr_panel_tc(double* A, Geo g, int k, int ib, double* Tg, double* Ttt,
                         const int2* pairs, int npairs, const uint8_t* dec, bool tt,
-                        cudaStream_t st);
+                        cudaStream_t st, int i_first = -1);
+// UNMQR (tt = false) / one TTMQR level (tt = true) on the column block (base, ldc, ncols)
+void launch_qr_update2(const double* A, Geo g, int k, const double* T, const int2* pairs,
+                       int npairs, bool tt, double* base, int64_t ldc, int64_t ncols,
+                       const uint8_t* dec, cudaStream_t st);
 void launch_qr_update_dmma(const double* A, Geo g, int k, int ib, const double* Tg,
                            const double* Ttt, const int2* const* level_pairs,
                            const int* level_count, int nlevels, double* base, int64_t ldc,
@@ -98,19 +103,28 @@ void launch_tt_apply(const double* A, Geo g, int k, int ib, const double* Ttt,
 void launch_gemv_sub(double* y, const double* B, int64_t ldb, int64_t M, int K, const double* v,
                      cudaStream_t st);
 void launch_getrf(const double* A, Geo g, int k, DevWork w, bool need, cudaStream_t st);
-// estimate != 0: the Hager / Higham estimate (NEXT f3) instead of the exact norm
-void launch_invnorm(Geo g, int k, DevWork w, cudaStream_t st, int estimate = 0);
+// estimate != 0: the Hager / Higham estimate (NEXT f3) instead of the exact norm;
+// dense != 0: the Li slot holds a dense matrix (A2: Q_kk^T) instead of unit-lower L^-1
+void launch_invnorm(Geo g, int k, DevWork w, cudaStream_t st, int estimate = 0, int dense = 0);
+// NEXT f4 (A2): after the in-place GEQRT of tile k: W <- the tile (R on/above the diagonal, for the
+// MUMPS pivots and the triangular inverse), zero-pivot flag = any R_jj == 0, the step's ipiv and
+// the scratch permutation = identity, and the scratch Li slot = I (Q^T is formed on it)
+void launch_a2_prep(const double* A, Geo g, int k, DevWork w, cudaStream_t st);
 void launch_decide(Geo g, int k, int crit, double alpha, int mumps_reading, double tie_tol,
                    int has_forced, int has_ref, DevWork w, cudaStream_t st);
-void launch_lu_panel(double* A, Geo g, int k, const DevWork& w, cudaStream_t st);
+// commit = false (A2): A_kk already holds its factors in place; only the Eliminate GEMM runs
+void launch_lu_panel(double* A, Geo g, int k, const DevWork& w, cudaStream_t st,
+                     bool commit = true);
 void launch_lu_update(double* A, Geo g, int k, const DevWork& w, int64_t c0, int64_t c1,
                       double* colpart, cudaStream_t st);
 void launch_lu_growth(const DevWork& w, Geo g, int k, cudaStream_t st);
 void launch_gemm_sub(double* C, int64_t ldc, const double* Am, int64_t lda, const double* Bm,
                      int64_t ldb, int64_t M, int64_t Nc, int K, const uint8_t* dec, int k,
                      cudaStream_t st);
+// diag_done (A2): tile k was already GEQRT-factored in place by the Factor stage
 void launch_qr_panel(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
-                     const int* level_count, int nlevels, const DevWork& w, cudaStream_t st);
+                     const int* level_count, int nlevels, const DevWork& w, cudaStream_t st,
+                     bool diag_done = false);
 void launch_qr_update(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
                       const int* level_count, int nlevels, const DevWork& w, int64_t c0,
                       int64_t c1, cudaStream_t st);
@@ -127,8 +141,9 @@ void launch_solve_qr_fwd(const double* A, Geo g, int k, int ib, const double* Tg
                          int nlevels, double* x, cudaStream_t st);
 void launch_solve_back(const double* A, Geo g, int k, double* x, cudaStream_t st);
 // LU steps with the stored explicit inverses: x_k <- L_kk^-1 P x_k, rows below -= L_ik x_k
+// (dense: x_k <- Li x_k with a full Li, the A2 variant's Q_kk^T)
 void launch_solve_lu_fwd_inv(const double* A, Geo g, int k, const double* Li, const int* perm,
-                             double* x, double* t, cudaStream_t st);
+                             double* x, double* t, cudaStream_t st, bool dense = false);
 // back substitution of an LU step: x_k <- U_kk^-1 x_k, rows above -= A_ik x_k
 void launch_solve_back_inv(const double* A, Geo g, int k, const double* Ui, double* x, double* t,
                            cudaStream_t st);

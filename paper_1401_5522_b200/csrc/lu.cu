@@ -83,14 +83,14 @@ void launch_copy_ints(int* dst, const int* src, int n, const uint8_t* dec, int k
 }
 
 // Panel stage of an LU step (column block k only): Factor (commit W, ipiv) + Eliminate (TRSM).
-void launch_lu_panel(double* A, Geo g, int k, const DevWork& w, cudaStream_t st) {
+void launch_lu_panel(double* A, Geo g, int k, const DevWork& w, cudaStream_t st, bool commit) {
   const int bk = g.bs(k);
   const int64_t k0 = g.r0(k), k1 = k0 + bk;
   const int64_t M = g.N - k1;  // rows below the diagonal tile
   const uint8_t* dec = w.dec;
   const double* Ui = w.scratch + (size_t)g.nb * g.nb;
   int* perm = reinterpret_cast<int*>(w.scratch + (size_t)2 * g.nb * g.nb);
-  { ::hlq::g_launches++; k_lu_commit<<<8, 256, 0, st>>>(A, g, k, w.W, w.ipiv_ws, w.ipiv, perm, dec); }
+  if (commit) { ::hlq::g_launches++; k_lu_commit<<<8, 256, 0, st>>>(A, g, k, w.W, w.ipiv_ws, w.ipiv, perm, dec); }
   if (M <= 0) return;
   // Eliminate: X = A[k1:N, k0:k1]; A[k1:N, k0:k1] = X * U^-1
   { ::hlq::g_launches++; k_copy_block<<<grid_for(M * bk), 256, 0, st>>>(w.ws_panel, M, A + k0 * g.lda + k1, g.lda, M, bk, nullptr, dec, k); }

@@ -529,13 +529,15 @@ void launch_tt_apply(const double* A, Geo g, int k, int ib, const double* Ttt,
 // every level of the greedy tree (a TTQRT only touches panel tiles, so all levels run before any
 // trailing update).  Predicated on dec[k] == QR.
 void launch_qr_panel(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
-                     const int* level_count, int nlevels, const DevWork& w, cudaStream_t st) {
+                     const int* level_count, int nlevels, const DevWork& w, cudaStream_t st,
+                     bool diag_done) {
   set_attr_once();
   const size_t smem = qr_smem_bytes(g.nb);
   const uint8_t* dec = w.dec;
   const bool tc = (ib == 32);
   if (tc)
-    launch_qr_panel_tc(A, g, k, ib, w.Tg, w.Ttt, nullptr, 0, dec, false, st);
+    launch_qr_panel_tc(A, g, k, ib, w.Tg, w.Ttt, nullptr, 0, dec, false, st,
+                       diag_done ? k + 1 : k);
   else
     { ::hlq::g_launches++; k_geqrt<<<g.n - k, QT, smem, st>>>(A, g, k, ib, w.Tg, dec); }
   for (int l = 0; l < nlevels; ++l) {

@@ -506,7 +506,7 @@ __device__ __forceinline__ void panel_factor_nb(int nb, double* Vs, int ldc, dou
 template <int W>
 __global__ void __launch_bounds__(QD_T) k_geqrt_tc(double* __restrict__ A, Geo g, int k, int ib,
                                                    double* __restrict__ Tg,
-                                                   const uint8_t* __restrict__ dec) {
+                                                   const uint8_t* __restrict__ dec, int i_first) {
   if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
   extern __shared__ __align__(16) double sm[];
   const int ldc = qd_ldc(g.nb);
@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(QD_T) k_geqrt_tc(double* __restrict__ A, Geo g
   double* Vs = Cs + qd_cs(W, g.nb);
   double* Us = Vs + 32 * ldc;
   double* Ts = Us + W * LDU;
-  const int i = k + blockIdx.x;
+  const int i = i_first + blockIdx.x;
   const int bi = g.bs(i), bk = g.cbs(k);
   double* tile = g.tile(A, i, k);
   double* T = Tg + tri_index(i, k, g.n) * (int64_t)ib * g.nb;
@@ -638,7 +638,7 @@ __global__ void __launch_bounds__(QD_T) k_ttqrt_tc(double* __restrict__ A, Geo g
 template <int W>
 static void launch_panel_w(double* A, Geo g, int k, int ib, double* Tg, double* Ttt,
                            const int2* pairs, int npairs, const uint8_t* dec, bool tt,
-                           cudaStream_t st) {
+                           cudaStream_t st, int i_first) {
   static bool attr = false;
   if (!attr) {
     smem_optin(k_geqrt_tc<W>);
@@ -647,7 +647,8 @@ static void launch_panel_w(double* A, Geo g, int k, int ib, double* Tg, double* 
   }
   const size_t smem = qd_smem<W>(g.nb);
   if (!tt) {
-    { ::hlq::g_launches++; k_geqrt_tc<W><<<g.n - k, QD_T, smem, st>>>(A, g, k, ib, Tg, dec); }
+    if (g.n - i_first <= 0) return;
+    { ::hlq::g_launches++; k_geqrt_tc<W><<<g.n - i_first, QD_T, smem, st>>>(A, g, k, ib, Tg, dec, i_first); }
   } else {
     { ::hlq::g_launches++; k_ttqrt_tc<W><<<npairs, QD_T, smem, st>>>(A, g, k, ib, Ttt, pairs, dec); }
   }
@@ -655,11 +656,12 @@ static void launch_panel_w(double* A, Geo g, int k, int ib, double* Tg, double* 
 
 void launch_qr_panel_tc(double* A, Geo g, int k, int ib, double* Tg, double* Ttt,
                         const int2* pairs, int npairs, const uint8_t* dec, bool tt,
-                        cudaStream_t st) {
+                        cudaStream_t st, int i_first) {
+  if (i_first < 0) i_first = k;
   if (qd_smem<64>(g.nb) <= 227 * 1024)
-    launch_panel_w<64>(A, g, k, ib, Tg, Ttt, pairs, npairs, dec, tt, st);
+    launch_panel_w<64>(A, g, k, ib, Tg, Ttt, pairs, npairs, dec, tt, st, i_first);
   else
-    launch_panel_w<32>(A, g, k, ib, Tg, Ttt, pairs, npairs, dec, tt, st);
+    launch_panel_w<32>(A, g, k, ib, Tg, Ttt, pairs, npairs, dec, tt, st, i_first);
 }
 
 template <int W>

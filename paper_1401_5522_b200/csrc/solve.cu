@@ -159,9 +159,10 @@ void launch_solve_back(const double* A, Geo g, int k, double* x, cudaStream_t st
 // ---------------------------------------------------------------------------------------------
 // LU steps with the explicit triangular inverses kept by the factorization (L_kk^-1, U_kk^-1 are
 // what Eliminate / Apply multiply by, Alg. 2): the diagonal solves become parallel GEMVs.
-// t[r] = sum_c M[c*ld + r] * v(c) over the triangle (lower: c <= r, upper: c >= r), v(c) = x_k[perm[c]]
-// or x_k[c]; one CTA per 32 rows, 8 warps splitting c, partials summed in a fixed order.
-template <bool LOWER>
+// t[r] = sum_c M[c*ld + r] * v(c) over the triangle (lower: c <= r, upper: c >= r) or the whole
+// row (dense: the A2 variant's Q_kk^T), v(c) = x_k[perm[c]] or x_k[c]; one CTA per 32 rows, 8 warps
+// splitting c, partials summed in a fixed order.
+template <bool LOWER, bool DENSE = false>
 __global__ void __launch_bounds__(256) k_tri_gemv(const double* __restrict__ M, int ld, int bk,
                                                   const int* __restrict__ perm,
                                                   const double* __restrict__ xk,
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(256) k_tri_gemv(const double* __restrict__ M, 
   const int r = blockIdx.x * 32 + lane;
   double acc = 0.0;
   if (r < bk) {
-    const int c0 = LOWER ? 0 : r, c1 = LOWER ? r + 1 : bk;
+    const int c0 = (LOWER || DENSE) ? 0 : r, c1 = DENSE ? bk : (LOWER ? r + 1 : bk);
     for (int c = c0 + ((warp - c0) % 8 + 8) % 8; c < c1; c += 8) acc += M[(int64_t)c * ld + r] * v[c];
   }
   part[warp][lane] = acc;
@@ -188,10 +189,14 @@ __global__ void __launch_bounds__(256) k_tri_gemv(const double* __restrict__ M, 
 }
 
 void launch_solve_lu_fwd_inv(const double* A, Geo g, int k, const double* Li, const int* perm,
-                             double* x, double* t, cudaStream_t st) {
+                             double* x, double* t, cudaStream_t st, bool dense) {
   const int bk = g.bs(k);
   const int64_t k0 = g.r0(k), k1 = k0 + bk;
-  { ::hlq::g_launches++; k_tri_gemv<true><<<(bk + 31) / 32, 256, 0, st>>>(Li, g.nb, bk, perm, x + k0, t); }
+  ::hlq::g_launches++;
+  if (dense)
+    k_tri_gemv<true, true><<<(bk + 31) / 32, 256, 0, st>>>(Li, g.nb, bk, perm, x + k0, t);
+  else
+    k_tri_gemv<true><<<(bk + 31) / 32, 256, 0, st>>>(Li, g.nb, bk, perm, x + k0, t);
   cudaMemcpyAsync(x + k0, t, sizeof(double) * bk, cudaMemcpyDeviceToDevice, st);
   launch_gemv_sub(x + k1, A + k0 * g.lda + k1, g.lda, g.N - k1, bk, x + k0, st);
 }

@@ -49,6 +49,13 @@ def test_argument_errors_without_gpu(built):
     assert lib.hlq_factor(dummy, 0, 2, 0, 1.0, ctypes.byref(h)) == -2
     assert lib.hlq_factor(dummy, 8, 0, 0, 1.0, ctypes.byref(h)) == -3
     assert lib.hlq_factor(dummy, 4096, 321, 0, 1.0, ctypes.byref(h)) == -3  # HLQ_MAX_NB = 320
+    # options: unknown LU variant; A2 needs ib = 32 and the exact inverse norm
+    for fields in ({"lu_variant": 2}, {"lu_variant": 1, "ib": 16},
+                   {"lu_variant": 1, "invnorm_estimate": 1}):
+        opt = H.hlq_default_options()
+        for k, v in fields.items():
+            setattr(opt, k, v)
+        assert lib.hlq_factor_ex(dummy, 8, 2, 0, 1.0, ctypes.byref(opt), ctypes.byref(h)) == -6
     assert lib.hlq_factor(dummy, 8, 2, 5, 1.0, ctypes.byref(h)) == -4
     assert lib.hlq_factor(dummy, 8, 2, 0, float("nan"), ctypes.byref(h)) == -5
     assert lib.hlq_factor(dummy, 8, 2, 0, -1.0, ctypes.byref(h)) == -5

@@ -27,7 +27,7 @@ def H():
 
 
 def run_pair(H, A, b, nb, crit=O.CRIT_MAX, alpha=1.0, D=1, forced=None, mumps_reading=0,
-             invnorm="exact", tie_rel_tol=1e-10):
+             invnorm="exact", tie_rel_tol=1e-10, lu_variant="A1"):
     N = A.shape[0]
     pre = {}
 
@@ -35,11 +35,12 @@ def run_pair(H, A, b, nb, crit=O.CRIT_MAX, alpha=1.0, D=1, forced=None, mumps_re
         sl = O.tsl(N, nb, k)
         pre[k] = Ab[sl, sl].copy()
     fo = O.hybrid_factor(A, nb, crit, alpha, D=D, forced=forced, mumps_reading=mumps_reading,
-                         on_step=hook, invnorm=invnorm)
+                         on_step=hook, invnorm=invnorm, lu_variant=lu_variant)
     fo.pre_tiles = pre
     dA = H.to_colmajor(A)
     kw = dict(tree_domains=D, mumps_reading=mumps_reading,
-              invnorm_estimate=1 if invnorm == "estimate" else 0, tie_rel_tol=tie_rel_tol)
+              invnorm_estimate=1 if invnorm == "estimate" else 0, tie_rel_tol=tie_rel_tol,
+              lu_variant=H.LU_A2 if lu_variant == "A2" else H.LU_A1)
     if forced is not None:
         f = H.hlq_factor_ex(dA, N, nb, crit, alpha, forced=forced, **kw)
     else:
@@ -313,3 +314,49 @@ def test_special_matrices_by_formula(H, name, crit, alpha):
         h_o = O.hpl3(A, O.solve(fo, bb), bb)
         if h_o <= 16.0:
             assert h_g <= 16.0, (h_g, h_o)
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT f4: LU step variant A2 against the oracle's A2
+# ---------------------------------------------------------------------------------------------
+def _a2_input(gen, N):
+    if gen == "dominant":  # block elimination without pivoting across tiles needs a stable input
+        return I.uniform_matrix(0, N) + (N / 2.0) * np.eye(N), I.uniform_rhs(0, N)
+    if gen == "normal":
+        return I.normal_system(1, N)
+    return I.uniform_matrix(0, N), I.uniform_rhs(0, N)
+
+
+@pytest.mark.parametrize("N,nb,crit,alpha,gen,forced_f", [
+    (1024, 128, O.CRIT_MAX, math.inf, "dominant", None),   # every step an A2 LU step
+    (1000, 128, O.CRIT_MAX, math.inf, "dominant", None),   # ragged last tile (104)
+    (1024, 128, O.CRIT_MAX, 1.0, "uniform", None),         # QR steps continue from the A2 GEQRT
+    (1000, 128, O.CRIT_MAX, 1.2e4, "uniform", None),       # genuine LU/QR mix, ragged
+    (1024, 128, O.CRIT_SUM, 1.0e3, "dominant", None),      # Sum on the A2 inverse norm
+    (1024, 128, O.CRIT_MUMPS, 2.1, "normal", None),        # MUMPS pivots |R_jj|
+    (960, 64, O.CRIT_MAX, 1.0, "dominant", 0.5),           # forced Bernoulli pattern
+    (320, 320, O.CRIT_MAX, math.inf, "dominant", None),    # n = 1, nb = 320
+])
+def test_a2_variant_parity(H, N, nb, crit, alpha, gen, forced_f):
+    A, b = _a2_input(gen, N)
+    n = (N + nb - 1) // nb
+    forced = I.bernoulli_pattern(30, n, forced_f) if forced_f is not None else None
+    fo, f, F, x = run_pair(H, A, b, nb, crit, alpha, forced=forced, lu_variant="A2")
+    np.testing.assert_array_equal(f.decisions(), fo.dec)
+    assert O.factor_diff(F, fo.A) <= 1e-10, O.factor_diff(F, fo.A)
+    h_o = O.hpl3(A, O.solve(fo, b), b)
+    h_g = O.hpl3(A, x, b)
+    if h_o <= 16.0:
+        assert h_g <= 16.0, (h_g, h_o)
+    if gen == "dominant" and forced is None:
+        assert np.allclose(x, np.linalg.solve(A, b), rtol=0, atol=1e-10 * np.abs(x).max())
+    assert f.info()["true_flops"] == pytest.approx(
+        sum(O.step_flops(N, nb, k, O.QR) if d == O.QR else _a2_lu_flops(N, nb, k)
+            for k, d in enumerate(fo.dec)), rel=1e-12)
+
+
+def _a2_lu_flops(N, nb, k):
+    """P:397: A2's Factor (QR of the tile, 4/3 b^3) and Apply (ORMQR, 2 M b^2) cost twice A1's."""
+    sl = O.tsl(N, nb, k)
+    bb, M = sl.stop - sl.start, N - sl.stop
+    return 4.0 / 3.0 * bb ** 3 + M * bb * bb + 2.0 * M * bb * bb + 2.0 * M * M * bb
