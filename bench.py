@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--alpha", type=float, default=1.0)
     ap.add_argument("--invnorm", default="exact", choices=["exact", "estimate"],
                     help="||A_kk^-1||_1 exact (default) or the Hager/Higham estimate (NEXT f3)")
+    ap.add_argument("--lu-variant", default="A1", choices=["A1", "A2"],
+                    help="LU step variant (A2: QR-factored diagonal tile, NEXT f4, P:373-397)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-N", type=int, default=4096)
@@ -181,6 +183,8 @@ def workload_config(args, cfg):
             dec += " (||A_kk^-1||_1 estimated)"
     else:
         dec = f"forced Bernoulli pattern f_QR={args.fqr} (seed 30)"
+    if args.lu_variant == "A2":
+        dec += ", LU variant A2"
     world = int(os.environ.get("WORLD_SIZE", "1"))
     P, Q = grid_shape(world)
     return {"workload": f"{args.config}: N={N}, nb={nb}, FP64 {cfg['gen']} seed {cfg['seed']}, {dec}",
@@ -213,6 +217,8 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if (world > 1 or args.dist) and args.lu_variant != "A1":
+        raise SystemExit("the multi-GPU path implements LU variant A1 only")
     if world > 1 or args.dist:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
@@ -263,7 +269,8 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         f = H.hlq_factor_ex(A, N, nb, crit, args.alpha, forced=forced, profile=int(profile),
-                            invnorm_estimate=int(args.invnorm == "estimate"))
+                            invnorm_estimate=int(args.invnorm == "estimate"),
+                            lu_variant=H.LU_A2 if args.lu_variant == "A2" else H.LU_A1)
         f.solve(b, x)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -351,6 +358,8 @@ def main():
         bh = b.cpu().pin_memory()
         xh = torch.empty(N, dtype=torch.float64, pin_memory=True)
         opt = H.hlq_default_options()
+        opt.invnorm_estimate = int(args.invnorm == "estimate")
+        opt.lu_variant = H.LU_A2 if args.lu_variant == "A2" else H.LU_A1
         fv = forced
         if fv is not None:
             fa = np.ascontiguousarray(fv, dtype=np.uint8)
