@@ -13,3 +13,6 @@ timeout 600 python bench.py --dist --steps 3 --warmup 3 --no-e2e > $O/bench_dist
 timeout 900 python bench.py --config C5 --N 32768 --criterion max --alpha 1 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $O/bench_c5r.log 2>&1
 timeout 900 python bench.py --config C2 --criterion max --alpha 1 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $O/bench_c2_max1.log 2>&1
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_reference.log 2>&1
+timeout 900 python bench.py --config C2 --criterion max --alpha 1 --lu-variant A2 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $O/bench_c2_max1_a2.log 2>&1
+timeout 900 python bench.py --lu-variant A2 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > $O/bench_c3_f0_a2.log 2>&1
+timeout 900 python bench.py --fqr 1.0 --lu-variant A2 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $O/bench_c3_f1_a2.log 2>&1
