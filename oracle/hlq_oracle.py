@@ -76,6 +76,34 @@ def panel_stats(A: np.ndarray, N: int, nb: int, k: int):
     return s, local_max, away_max
 
 
+def domain_tiles(k: int, n: int, D: int):
+    """NEXT f1: the diagonal domain of step k = the panel tiles i >= k of the diagonal tile's domain,
+    i = k (mod D) (domains = tile rows mod D, the QR tree's domains and the 2D grid's process rows;
+    "all tiles in the diagonal domain are local to a single node").  D = 1: every tile."""
+    return [i for i in range(k, n) if (i - k) % D == 0]
+
+
+def panel_stats_domain(A: np.ndarray, N: int, nb: int, k: int, D: int):
+    """Criterion inputs under diagonal-domain pivoting (DESIGN reading 33):
+    s_i = ||A_ik||_1 over the tiles OFF the domain (ascending i; the domain tiles are eliminated by
+    the pivoted LU itself), local_max(j) over the domain tiles, away_max(j) over the other tiles."""
+    n = ntiles(N, nb)
+    ck = tsl(N, nb, k)
+    dom = set(domain_tiles(k, n, D))
+    s = np.array([norm1(A[tsl(N, nb, i), ck]) for i in range(k + 1, n) if i not in dom],
+                 dtype=np.float64)
+    b = ck.stop - ck.start
+    local_max = np.zeros(b)
+    away_max = np.zeros(b)
+    for i in range(k, n):
+        m = np.max(np.abs(A[tsl(N, nb, i), ck]), axis=0)
+        if i in dom:
+            local_max = np.maximum(local_max, m)
+        else:
+            away_max = np.maximum(away_max, m)
+    return s, local_max, away_max
+
+
 # ----------------------------------------------------------------------------------------------
 # a2: GETRF with partial pivoting local to the tile (Alg. 2 P:227, P:247-249)
 # ----------------------------------------------------------------------------------------------
@@ -102,6 +130,72 @@ def getrf(T: np.ndarray):
         W[c + 1:, c] = W[c + 1:, c] / W[c, c]
         W[c + 1:, c + 1:] -= np.outer(W[c + 1:, c], W[c, c + 1:])
     return W, ipiv, zero_pivot
+
+
+def getrf_stack(S: np.ndarray):
+    """NEXT f1: partial pivoting over the stacked diagonal domain (R x b, R >= b, the domain tiles in
+    ascending order): the same unblocked elimination as getrf, the pivot search running over all R
+    rows (first maximum, ledger 6).  ipiv[c] in stack coordinates (LAPACK sequential swaps); an
+    exact zero pivot leaves the column unscaled (ledger 7).  Returns (S factored, ipiv, zero_pivot)."""
+    W = np.array(S, dtype=np.float64, copy=True)
+    R, b = W.shape
+    ipiv = np.zeros(b, dtype=np.int32)
+    zero_pivot = False
+    for c in range(b):
+        p = c + int(np.argmax(np.abs(W[c:, c])))
+        ipiv[c] = p
+        if p != c:
+            W[[c, p], :] = W[[p, c], :]
+        if W[c, c] == 0.0:
+            zero_pivot = True
+            continue
+        W[c + 1:, c] = W[c + 1:, c] / W[c, c]
+        W[c + 1:, c + 1:] -= np.outer(W[c + 1:, c], W[c, c + 1:])
+    return W, ipiv, zero_pivot
+
+
+def domain_rows(N: int, nb: int, k: int, D: int) -> np.ndarray:
+    """Global row indices of the stacked diagonal domain (tile k first)."""
+    n = ntiles(N, nb)
+    return np.concatenate([np.arange(tsl(N, nb, i).start, tsl(N, nb, i).stop)
+                           for i in domain_tiles(k, n, D)])
+
+
+def lu_step_domain(A: np.ndarray, N: int, nb: int, k: int, D: int, Wst: np.ndarray,
+                   ipiv: np.ndarray):
+    """LU step with diagonal-domain pivoting ("a swap is performed with all
+    tiles of the local panel, and then a triangular solve is applied to the first row.  On all other
+    nodes ... the panel is updated with TRSM tasks, and the trailing sub-matrix ... with GEMM")."""
+    n = ntiles(N, nb)
+    rk = tsl(N, nb, k)
+    k0, k1 = rk.start, rk.stop
+    b = k1 - k0
+    G = domain_rows(N, nb, k, D)
+    # Factor: the pivoted domain LU replaces the domain's panel (U11/L11 in tile k, L in the others)
+    A[G, k0:k1] = Wst
+    if k + 1 == n:
+        return
+    dom = set(domain_tiles(k, n, D))
+    U = np.triu(Wst[:b, :])
+    L = np.tril(Wst[:b, :], -1) + np.eye(b)
+    # Eliminate the tiles off the domain: A_ik <- A_ik U_11^-1
+    with np.errstate(all="ignore"):
+        for i in range(k + 1, n):
+            if i not in dom:
+                ri = tsl(N, nb, i)
+                A[ri, k0:k1] = solve_triangular(U, A[ri, k0:k1].T, trans="T", lower=False,
+                                                check_finite=False).T
+    # Swap: the domain's row interchanges on the trailing columns (columns > k only, reading 23)
+    for c in range(b):
+        p = int(ipiv[c])
+        if p != c:
+            A[[G[c], G[p]], k1:N] = A[[G[p], G[c]], k1:N]
+    # Apply: A_kj <- L_11^-1 A_kj
+    with np.errstate(all="ignore"):
+        A[k0:k1, k1:N] = solve_triangular(L, A[k0:k1, k1:N], lower=True, unit_diagonal=True,
+                                          check_finite=False)
+        # Update: A_ij <- A_ij - A_ik A_kj for every i, j > k
+        A[k1:N, k1:N] -= A[k1:N, k0:k1] @ A[k0:k1, k1:N]
 
 
 # ----------------------------------------------------------------------------------------------
@@ -613,18 +707,22 @@ class Factors:
     status: int
     stats: list
     lu_variant: str = "A1"
+    pivot_scope: str = "tile"
 
 
 def hybrid_factor(A_in: np.ndarray, nb: int, crit: int = CRIT_MAX, alpha: float = 1.0, D: int = 1,
                   ib: int = 32, mumps_reading: int = 0, forced=None, track_growth: bool = True,
                   tie_tol: float = 1e-10, variant: int = 0, on_step=None,
-                  tree: str = "greedy", invnorm: str = "exact", lu_variant: str = "A1") -> Factors:
+                  tree: str = "greedy", invnorm: str = "exact", lu_variant: str = "A1",
+                  pivot_scope: str = "tile") -> Factors:
     """Alg. 1: for each step, speculative tile LU, criterion, LU or QR step.
 
     invnorm: "exact" (ledger 3, default) or "estimate" (NEXT f3: inv_norm1_estimate).
     lu_variant: "A1" (Alg. 2, default) or "A2" (NEXT f4: the diagonal tile is
     QR-factored in place before the criterion; an LU step eliminates with U_kk = R and applies
     Q_kk^T, a QR step continues from that factorization).
+    pivot_scope: "tile" (north_star, ledger 8) or "domain" (NEXT f1: the pivot search runs
+    over the diagonal domain, the D-domain of the QR tree; DESIGN reading 33).
     forced: decision vector used verbatim (C3); variant=1 uses the reversed-chunk GEMM (noise floor).
     on_step(k, A_before, A_after, d): optional test hook called after each step with copies.
     """
@@ -641,18 +739,32 @@ def hybrid_factor(A_in: np.ndarray, nb: int, crit: int = CRIT_MAX, alpha: float 
     if lu_variant == "A2" and invnorm != "exact":
         raise ValueError("the A2 variant computes the exact ||A_kk^-1||_1 only")
     a2 = lu_variant == "A2"
+    if pivot_scope not in ("tile", "domain"):
+        raise ValueError("pivot_scope must be 'tile' or 'domain'")
+    dp = pivot_scope == "domain"
+    if dp and a2:
+        raise ValueError("diagonal-domain pivoting is defined for the A1 LU step")
     g0 = max_tile_norm(A, N, nb, 0) if track_growth else 1.0
     g = g0
     for k in range(n):
         rk = tsl(N, nb, k)
         A_before = A.copy() if on_step is not None else None
-        s, lmax, amax = panel_stats(A, N, nb, k)
+        if dp:
+            s, lmax, amax = panel_stats_domain(A, N, nb, k, D)
+        else:
+            s, lmax, amax = panel_stats(A, N, nb, k)
         T_kk = None
+        Wst = None
         if a2 and not (forced is None and alpha == 0.0) and not (forced is not None
                                                                   and int(forced[k]) == QR):
             # A2 Factor: in place; a QR decision continues from it
             T_kk, W, zp = a2_factor(A, N, nb, k, ib)
             ipiv = np.arange(rk.stop - rk.start, dtype=np.int32)
+        elif dp:
+            # Factor over the diagonal domain (speculative, out of place); the criterion reads the
+            # pivoted diagonal tile's LU, the top b x b of the stack
+            Wst, ipiv, zp = getrf_stack(A[domain_rows(N, nb, k, D), rk])
+            W = Wst[:rk.stop - rk.start, :]
         else:
             # Factor (speculative, out of place: the paper's Backup Panel P:634-640 becomes a copy)
             W, ipiv, zp = getrf(A[rk, rk])
@@ -691,6 +803,9 @@ def hybrid_factor(A_in: np.ndarray, nb: int, crit: int = CRIT_MAX, alpha: float 
         if d == LU and T_kk is not None:
             lu_step_a2(A, N, nb, k, T_kk, ib)
             qrs[k] = QRStepData(T_geqrt={k: T_kk})  # Q_kk for the solve's forward pass
+        elif d == LU and Wst is not None:
+            lu_step_domain(A, N, nb, k, D, Wst, ipiv)
+            ipivs[k] = ipiv  # stack coordinates (Factors.pivot_scope says so)
         elif d == LU:
             lu_step(A, N, nb, k, W, ipiv)
             if variant == 1 and k + 1 < n:
@@ -718,7 +833,7 @@ def hybrid_factor(A_in: np.ndarray, nb: int, crit: int = CRIT_MAX, alpha: float 
     if track_growth and not np.isfinite(g):
         growth = math.inf
     return Factors(A, N, nb, n, ib, D, tree, dec, margin, near_tie, ipivs, qrs, growth, status, stats,
-                   lu_variant)
+                   lu_variant, pivot_scope)
 
 
 # ----------------------------------------------------------------------------------------------
@@ -741,10 +856,12 @@ def apply_transforms(f: Factors, x: np.ndarray) -> np.ndarray:
                 x[k1:N, :] -= A[k1:N, k0:k1] @ x[rk, :]
         elif f.dec[k] == LU:
             ipiv = f.ipiv[k]
+            G = (domain_rows(N, nb, k, f.D) if f.pivot_scope == "domain"
+                 else np.arange(k0, k1))
             for c in range(k1 - k0):
                 p = int(ipiv[c])
                 if p != c:
-                    x[[k0 + c, k0 + p], :] = x[[k0 + p, k0 + c], :]
+                    x[[G[c], G[p]], :] = x[[G[p], G[c]], :]
             Lkk = np.tril(A[rk, rk], -1) + np.eye(k1 - k0)
             x[rk, :] = solve_triangular(Lkk, x[rk, :], lower=True, unit_diagonal=True,
                                         check_finite=False)

@@ -571,3 +571,75 @@ def _perm_of(ipiv):
     for c, r in enumerate(ipiv):
         p[[c, r]] = p[[r, c]]
     return p
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT f1: diagonal-domain pivoting
+# ---------------------------------------------------------------------------------------------
+def test_domain_pivoting_d1_is_lapack_lupp():
+    """D = 1: the diagonal domain is the whole panel, every step is LU (no tile off the domain), and
+    the factorization is right-looking LU with partial pivoting: pivots identical to LAPACK dgetrf
+    (scipy lu_factor) and U equal to LAPACK's."""
+    N, nb = 512, 64
+    A = I.uniform_matrix(3, N)
+    f = O.hybrid_factor(A, nb, O.CRIT_MAX, 1.0, D=1, pivot_scope="domain")
+    assert np.all(f.dec == O.LU)
+    lu, piv = sl.lu_factor(A)
+    gpiv = np.concatenate([k * nb + f.ipiv[k] for k in range(f.n)])
+    assert np.array_equal(gpiv, piv)
+    U = np.triu(f.A)
+    assert np.linalg.norm(U - np.triu(lu)) / np.linalg.norm(np.triu(lu)) < 1e-13
+    b = I.uniform_rhs(3, N)
+    assert np.allclose(O.solve(f, b), sl.lu_solve((lu, piv), b), rtol=0, atol=1e-10)
+
+
+@pytest.mark.parametrize("crit,alpha", [(O.CRIT_MAX, 1.0), (O.CRIT_MAX, 1e4),
+                                        (O.CRIT_SUM, 1e5), (O.CRIT_MUMPS, 2.1)])
+def test_domain_pivoting_with_singleton_domains_is_tile_pivoting(crit, alpha):
+    """D >= n: every domain is one tile, so diagonal-domain pivoting is tile-local pivoting."""
+    N, nb = 768, 128
+    A = I.normal_system(2, N)[0]
+    f1 = O.hybrid_factor(A, nb, crit, alpha, D=6, pivot_scope="tile")
+    f2 = O.hybrid_factor(A, nb, crit, alpha, D=6, pivot_scope="domain")
+    assert np.array_equal(f1.dec, f2.dec)
+    assert np.allclose(f1.margin, f2.margin, rtol=1e-13, atol=0, equal_nan=True)
+    assert O.factor_diff(f2.A, f1.A) < 1e-14
+    for k in f1.ipiv:
+        assert np.array_equal(f1.ipiv[k], f2.ipiv[k])
+
+
+def test_domain_statistics_and_pivoted_tile_by_hand():
+    """3 x 3 tiles, D = 2, step 0: the domain is tiles {0, 2}; s = [||A_10||_1] (off the domain),
+    local_max over tiles 0 and 2, away_max over tile 1, and the criterion's ||A_kk^-1|| is that of
+    the diagonal tile after the domain's row interchanges."""
+    nb, N = 8, 24
+    A = I.normal_system(4, N)[0]
+    s, lm, am = O.panel_stats_domain(A, N, nb, 0, 2)
+    assert np.array_equal(s, [np.max(np.sum(np.abs(A[8:16, :8]), axis=0))])
+    assert np.array_equal(lm, np.maximum(np.abs(A[:8, :8]).max(0), np.abs(A[16:24, :8]).max(0)))
+    assert np.array_equal(am, np.abs(A[8:16, :8]).max(0))
+    rows = np.r_[0:8, 16:24]
+    assert np.array_equal(O.domain_rows(N, nb, 0, 2), rows)
+    Wst, ipiv, zp = O.getrf_stack(A[rows, :8])
+    P = np.arange(16)
+    for c, p in enumerate(ipiv):
+        P[[c, p]] = P[[p, c]]
+    top = A[rows[P[:8]], :8]  # the diagonal tile after pivoting among the domain's tiles
+    assert abs(O.inv_norm1_from_lu(Wst[:8]) - np.linalg.norm(np.linalg.inv(top), 1)) \
+        <= 1e-12 * np.linalg.norm(np.linalg.inv(top), 1)
+    # the stack LU is LAPACK's partial pivoting of the stacked domain
+    lu, piv = sl.lu_factor(A[rows, :8])
+    assert np.array_equal(ipiv, piv)
+
+
+def test_domain_pivoting_mixed_run_solves_and_raises_lu_likelihood():
+    """pivoting over the domain 'increases the likelihood of an LU step'.  Normal input,
+    N = 1024, nb = 128, D = 2, Max alpha in the mixing range: at least as many LU steps as tile
+    pivoting, and the solve is accurate."""
+    N, nb = 1024, 128
+    A, b = I.normal_system(1, N)
+    for alpha in (3e3, 1e4, 3e4):
+        ft = O.hybrid_factor(A, nb, O.CRIT_MAX, alpha, D=2, pivot_scope="tile")
+        fd = O.hybrid_factor(A, nb, O.CRIT_MAX, alpha, D=2, pivot_scope="domain")
+        assert np.sum(fd.dec == O.LU) >= np.sum(ft.dec == O.LU)
+        assert O.hpl3(A, O.solve(fd, b), b) <= 16.0
