@@ -85,9 +85,18 @@ typedef struct {
                                 eliminates with U_kk^-1 and applies Q_kk^T to row k, a QR step
                                 continues from that factorization.  A2 needs ib = 32, the exact
                                 inverse norm and one GPU (hlq_factor_dist rejects it: -8). */
+  int32_t pivot_scope;       /* HLQ_PIVOT_TILE (default, north_star) or HLQ_PIVOT_DOMAIN (NEXT f1,
+                                P:271-285): the speculative LU pivots over the diagonal domain, the
+                                panel tiles i >= k with i = k (mod tree_domains), stacked tile k
+                                first; the criterion reads the pivoted diagonal tile and the tiles
+                                off the domain (reading 33); an LU step swaps the domain's
+                                rows of the trailing columns, keeps the domain's L from the stacked
+                                LU and eliminates the other tiles with U_kk.  tree_domains = 1 makes
+                                every step LU with partial pivoting (LUPP).  A1 variant, one GPU. */
 } hlq_options;
 
 enum { HLQ_LU_A1 = 0, HLQ_LU_A2 = 1 };
+enum { HLQ_PIVOT_TILE = 0, HLQ_PIVOT_DOMAIN = 1 };
 
 typedef struct {
   int64_t N;

@@ -189,7 +189,9 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   if (opt.ib < 1 || opt.ib > 32 || opt.tree_domains < 1 || opt.tree != HLQ_TREE_GREEDY ||
       opt.mumps_reading < 0 || opt.mumps_reading > 1 || opt.invnorm_estimate < 0 ||
       opt.invnorm_estimate > 1 || opt.lu_variant < HLQ_LU_A1 || opt.lu_variant > HLQ_LU_A2 ||
-      (opt.lu_variant == HLQ_LU_A2 && (opt.ib != 32 || opt.invnorm_estimate != 0)))
+      (opt.lu_variant == HLQ_LU_A2 && (opt.ib != 32 || opt.invnorm_estimate != 0)) ||
+      opt.pivot_scope < HLQ_PIVOT_TILE || opt.pivot_scope > HLQ_PIVOT_DOMAIN ||
+      (opt.pivot_scope == HLQ_PIVOT_DOMAIN && opt.lu_variant != HLQ_LU_A1))
     return -6;
   int64_t lda = opt.lda ? opt.lda : N;
   if (lda < N) return -6;
@@ -210,6 +212,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   f->D = opt.tree_domains;
   f->crit = criterion;
   f->lu_variant = opt.lu_variant;
+  f->pivot_scope = opt.pivot_scope;
   f->alpha = alpha;
   f->st = (cudaStream_t)opt.stream;
   f->blocking = opt.blocking != 0;
@@ -249,6 +252,11 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
          oCp = take(fuse_growth_any ? sizeof(double) * (size_t)((N + 127) / 128) * N : 8),
          oLi = take(sizeof(double) * (size_t)n * 2 * nb * nb),
          oLp = take(sizeof(int) * (size_t)n * nb), oSt2 = take(sizeof(double) * (size_t)nb);
+  const bool dpiv = opt.pivot_scope == HLQ_PIVOT_DOMAIN;
+  size_t oWd = take(dpiv ? sizeof(double) * (size_t)N * nb : 8),
+         oDp = take(dpiv ? sizeof(int) * (size_t)n * nb : 8),
+         oDk = take(sizeof(unsigned long long) * 2 * 148), oDi = take(sizeof(int) * 2 * 148),
+         oDc = take(sizeof(unsigned int));
   f->ws_bytes = off;
   f->ws_block = cache_get(0, off);
   if (!f->ws_block) return HLQ_ERR_NOMEM;
@@ -280,6 +288,11 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   w.luinv = (double*)(base + oLi);
   w.luperm = (int*)(base + oLp);
   w.solve_t = (double*)(base + oSt2);
+  w.wdom = dpiv ? (double*)(base + oWd) : nullptr;
+  w.dipiv = dpiv ? (int*)(base + oDp) : nullptr;
+  w.dom_key = (unsigned long long*)(base + oDk);
+  w.dom_idx = (int*)(base + oDi);
+  w.dom_counter = (unsigned int*)(base + oDc);
   // per-parity views (lookahead: step k+1's panel runs while step k's update still reads step k's
   // W / ipiv / L^-1 / U^-1 / perm)
   DevWork wpar[2] = {w, w};
@@ -315,6 +328,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
       return rc;
   }
   cudaMemsetAsync(w.status, 0, sizeof(int) * 4, st);
+  cudaMemsetAsync(w.dom_counter, 0, sizeof(unsigned int), st);
   cudaMemsetAsync(w.gstep, 0, sizeof(double) * (n + 1), st);
   cudaMemsetAsync(w.ipiv, 0, sizeof(int) * (size_t)n * nb, st);
   // Two streams: st (the caller's) runs the trailing updates, sp (high priority) runs the panel
@@ -334,6 +348,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   };
   const bool criterion_needed = !opt.forced && alpha > 0.0 && !alpha_inf;
   const bool a2 = opt.lu_variant == HLQ_LU_A2;
+  const int Dp = f->D;  // diagonal-domain pivoting: the QR tree's domains
   for (int k = 0; k < n; ++k) {
     const DevWork& wk = wpar[k & 1];
     const int known = known_of(k);
@@ -344,7 +359,10 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
     if (known != HLQ_DEC_QR) {
       if (criterion_needed) {
         P.begin(HLQ_PROF_CRITERION, sp);
-        launch_panel_stats(A, g, k, wk, sp);
+        if (dpiv)
+          launch_panel_stats_domain(A, g, k, Dp, wk, sp);
+        else
+          launch_panel_stats(A, g, k, wk, sp);
         P.end(sp);
       }
       P.begin(HLQ_PROF_GETRF, sp);
@@ -363,6 +381,10 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
         launch_a2_prep(A, g, k, wk, sp);
         launch_tri_inv(g, k, wk, wk.ws_panel, wk.scratch + (size_t)nb * nb, sp);
         launch_qr_update2(Akk, gk, 0, Tkk, nullptr, 0, false, wk.scratch, nb, bk, nullptr, sp);
+      } else if (dpiv) {
+        // NEXT f1: partial pivoting over the stacked diagonal domain; W <- its pivoted top tile
+        launch_dom_factor(A, g, k, Dp, wk, sp);
+        launch_tri_inv(g, k, wk, wk.scratch, wk.scratch + (size_t)nb * nb, sp);
       } else {
         launch_getrf(A, g, k, wk, true, sp);
         launch_tri_inv(g, k, wk, wk.scratch, wk.scratch + (size_t)nb * nb, sp);
@@ -382,7 +404,10 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
     P.end(sp);
     if (known != HLQ_DEC_QR) {
       P.begin(HLQ_PROF_LU_TRSM, sp);
-      launch_lu_panel(A, g, k, wk, sp, /*commit=*/!a2);
+      launch_lu_panel(A, g, k, wk, sp, /*commit=*/!a2 && !dpiv);
+      // the domain's stacked LU replaces its panel tiles (after the Eliminate GEMM, which also
+      // wrote them: U_kk^-1 applies to the tiles off the domain only)
+      if (dpiv) launch_dom_commit(A, g, k, Dp, wk, sp);
       // keep L_kk^-1, U_kk^-1 and the composed permutation for the solve (LU steps only)
       launch_copy_block(w.luinv + (size_t)k * 2 * nb * nb, nb, wk.scratch, nb, nb, 2 * nb, nullptr,
                         w.dec, k, sp);
@@ -408,6 +433,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
       if (c1 > c0) {
         if (known != HLQ_DEC_QR) {
           P.begin(HLQ_PROF_LU_UPDATE, st);
+          if (dpiv) launch_dom_swap_cols(A, g, k, Dp, w.dipiv + (size_t)k * nb, c0, c1, w.dec, st);
           launch_lu_update(A, g, k, wk, c0, c1, fuse ? w.colpart : nullptr, st);
           P.end(st);
         }
@@ -494,6 +520,8 @@ int hlq_solve(hlq_factors_t f, const double* b, double* x) {
       (rc = cuda_err(cudaMemcpyAsync(x, b, sizeof(double) * g.N, cudaMemcpyDeviceToDevice, st))))
     return rc;
   for (int k = 0; k < g.n; ++k) {
+    if (f->dec[k] == HLQ_DEC_LU && f->pivot_scope == HLQ_PIVOT_DOMAIN)
+      launch_dom_swap_vec(x, g, k, f->D, f->w.dipiv + (size_t)k * g.nb, st);
     if (f->dec[k] == HLQ_DEC_LU)
       launch_solve_lu_fwd_inv(f->A, g, k, f->w.luinv + (size_t)k * 2 * g.nb * g.nb,
                               f->w.luperm + (size_t)k * g.nb, x, f->w.solve_t, st,

@@ -1554,7 +1554,8 @@ int hlq_factor_dist(hlq_grid_t grid, double* const* A_local, const int64_t* lld,
   if (opt.ib == 0) opt.ib = 32;
   if (opt.tie_rel_tol == 0.0) opt.tie_rel_tol = 1e-10;
   if (opt.ib != 32 || D < P || D % P != 0 || D / P > 16 || opt.tree != HLQ_TREE_GREEDY ||
-      opt.mumps_reading < 0 || opt.mumps_reading > 1 || opt.lu_variant != HLQ_LU_A1)
+      opt.mumps_reading < 0 || opt.mumps_reading > 1 || opt.lu_variant != HLQ_LU_A1 ||
+      opt.pivot_scope != HLQ_PIVOT_TILE)
     return -8;
   hlq_factors_t f = new (std::nothrow) hlq_factors_s();
   if (!f) return HLQ_ERR_NOMEM;

@@ -71,6 +71,7 @@ struct hlq_factors_s {
   Geo g{};
   int ib = 32, D = 1, crit = 0;
   int lu_variant = 0;  // HLQ_LU_A1 / HLQ_LU_A2
+  int pivot_scope = 0;  // HLQ_PIVOT_TILE / HLQ_PIVOT_DOMAIN
   double alpha = 1.0;
   cudaStream_t st = nullptr;
   bool blocking = true;

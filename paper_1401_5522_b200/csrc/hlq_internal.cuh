@@ -64,6 +64,12 @@ struct DevWork {
   double* luinv;      // per LU step k: L_kk^-1 | U_kk^-1 (2 nb*nb, ld nb) for the solve, or null
   int* luperm;        // per LU step k: composed row permutation of P_kk (nb ints), or null
   double* solve_t;    // nb scratch doubles for the solve
+  // NEXT f1 (diagonal-domain pivoting), null otherwise
+  double* wdom;       // N*nb: the stacked domain panel (ld = its row count)
+  int* dipiv;         // n*nb: per step, the domain's pivots in stack coordinates
+  unsigned long long* dom_key;  // 2*148 partial pivot keys
+  int* dom_idx;                 // 2*148 partial pivot rows
+  unsigned int* dom_counter;    // arrivals of the last-CTA reduction
 };
 
 // ---- kernels-side launch helpers (defined in the .cu files) ---------------------------------
@@ -72,6 +78,18 @@ void launch_panel_stats(const double* A, Geo g, int k, DevWork w, cudaStream_t s
 // otherwise every tile i >= k is a sub-diagonal tile (s[i], away_max)
 void launch_panel_stats_to(const double* A, Geo g, int k, int diag, double* s, double* local_max,
                            double* away_max, cudaStream_t st);
+// NEXT f1: statistics split by the diagonal domain (tiles i = k mod D): local_max over the domain,
+// away_max and s_i over the other tiles (s_i = 0 inside the domain)
+void launch_panel_stats_domain(const double* A, Geo g, int k, int D, DevWork w, cudaStream_t st);
+// NEXT f1 (domain.cu): speculative stack factorization into w.wdom / w.dipiv + top tile into W;
+// commit (dec == LU) of the stack over the domain tiles; the domain's interchanges on columns
+// [c0, c1) (dec == LU) and on the solve's vector
+int64_t dom_rows(Geo g, int k, int D);
+void launch_dom_factor(double* A, Geo g, int k, int D, DevWork w, cudaStream_t st);
+void launch_dom_commit(double* A, Geo g, int k, int D, DevWork w, cudaStream_t st);
+void launch_dom_swap_cols(double* A, Geo g, int k, int D, const int* ipiv_stack, int64_t c0,
+                          int64_t c1, const uint8_t* dec, cudaStream_t st);
+void launch_dom_swap_vec(double* x, Geo g, int k, int D, const int* ipiv_stack, cudaStream_t st);
 void launch_tri_inv(Geo g, int k, const DevWork& w, double* Li, double* Ui, cudaStream_t st);
 void launch_lu_commit(double* A, Geo g, int k, const double* W, const int* ipiv_ws, int* ipiv,
                       int* perm, const uint8_t* dec, cudaStream_t st);

@@ -25,7 +25,7 @@ __device__ __forceinline__ double warp_nanmax(double v) {
 __global__ void __launch_bounds__(256) k_panel_stats(const double* __restrict__ A, Geo g, int k,
                                                      int diag, double* __restrict__ s,
                                                      double* __restrict__ local_max,
-                                                     double* __restrict__ away_max) {
+                                                     double* __restrict__ away_max, int D) {
   const int i = k + blockIdx.x;
   const int bi = g.bs(i), bk = g.cbs(k);
   const double* T = g.tile(const_cast<double*>(A), i, k);
@@ -44,7 +44,9 @@ __global__ void __launch_bounds__(256) k_panel_stats(const double* __restrict__ 
     mx = warp_nanmax(mx);
     tile_norm = nanmax(tile_norm, sum);
     if (lane == 0) {
-      if (diag && i == k)
+      if (D > 0)  // diagonal-domain statistics (local_max zeroed by the launcher)
+        atomic_max_nonneg((i - k) % D == 0 ? &local_max[c] : &away_max[c], mx);
+      else if (diag && i == k)
         local_max[c] = mx;
       else
         atomic_max_nonneg(&away_max[c], mx);
@@ -55,7 +57,7 @@ __global__ void __launch_bounds__(256) k_panel_stats(const double* __restrict__ 
   if (threadIdx.x == 0 && !(diag && i == k)) {
     double v = red[0];
     for (int w = 1; w < 8; ++w) v = nanmax(v, red[w]);
-    s[i] = v;
+    s[i] = (D > 0 && (i - k) % D == 0) ? 0.0 : v;  // the domain's tiles are not in the rhs
   }
 }
 
@@ -67,7 +69,15 @@ void launch_panel_stats_to(const double* A, Geo g, int k, int diag, double* s, d
                            double* away_max, cudaStream_t st) {
   cudaMemsetAsync(away_max, 0, sizeof(double) * g.nb, st);
   if (g.n - k <= 0) return;
-  { ::hlq::g_launches++; k_panel_stats<<<g.n - k, 256, 0, st>>>(A, g, k, diag, s, local_max, away_max); }
+  { ::hlq::g_launches++; k_panel_stats<<<g.n - k, 256, 0, st>>>(A, g, k, diag, s, local_max, away_max, 0); }
+}
+
+void launch_panel_stats_domain(const double* A, Geo g, int k, int D, DevWork w, cudaStream_t st) {
+  cudaMemsetAsync(w.away_max, 0, sizeof(double) * g.nb, st);
+  cudaMemsetAsync(w.local_max, 0, sizeof(double) * g.nb, st);
+  if (g.n - k <= 0) return;
+  ::hlq::g_launches++;
+  k_panel_stats<<<g.n - k, 256, 0, st>>>(A, g, k, 1, w.s, w.local_max, w.away_max, D);
 }
 
 // ---------------------------------------------------------------------------------------------

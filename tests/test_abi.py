@@ -51,7 +51,8 @@ def test_argument_errors_without_gpu(built):
     assert lib.hlq_factor(dummy, 4096, 321, 0, 1.0, ctypes.byref(h)) == -3  # HLQ_MAX_NB = 320
     # options: unknown LU variant; A2 needs ib = 32 and the exact inverse norm
     for fields in ({"lu_variant": 2}, {"lu_variant": 1, "ib": 16},
-                   {"lu_variant": 1, "invnorm_estimate": 1}):
+                   {"lu_variant": 1, "invnorm_estimate": 1}, {"pivot_scope": 2},
+                   {"pivot_scope": 1, "lu_variant": 1}):
         opt = H.hlq_default_options()
         for k, v in fields.items():
             setattr(opt, k, v)

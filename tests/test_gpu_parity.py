@@ -27,7 +27,7 @@ def H():
 
 
 def run_pair(H, A, b, nb, crit=O.CRIT_MAX, alpha=1.0, D=1, forced=None, mumps_reading=0,
-             invnorm="exact", tie_rel_tol=1e-10, lu_variant="A1"):
+             invnorm="exact", tie_rel_tol=1e-10, lu_variant="A1", pivot_scope="tile"):
     N = A.shape[0]
     pre = {}
 
@@ -35,12 +35,14 @@ def run_pair(H, A, b, nb, crit=O.CRIT_MAX, alpha=1.0, D=1, forced=None, mumps_re
         sl = O.tsl(N, nb, k)
         pre[k] = Ab[sl, sl].copy()
     fo = O.hybrid_factor(A, nb, crit, alpha, D=D, forced=forced, mumps_reading=mumps_reading,
-                         on_step=hook, invnorm=invnorm, lu_variant=lu_variant)
+                         on_step=hook, invnorm=invnorm, lu_variant=lu_variant,
+                         pivot_scope=pivot_scope)
     fo.pre_tiles = pre
     dA = H.to_colmajor(A)
     kw = dict(tree_domains=D, mumps_reading=mumps_reading,
               invnorm_estimate=1 if invnorm == "estimate" else 0, tie_rel_tol=tie_rel_tol,
-              lu_variant=H.LU_A2 if lu_variant == "A2" else H.LU_A1)
+              lu_variant=H.LU_A2 if lu_variant == "A2" else H.LU_A1,
+              pivot_scope=H.PIVOT_DOMAIN if pivot_scope == "domain" else H.PIVOT_TILE)
     if forced is not None:
         f = H.hlq_factor_ex(dA, N, nb, crit, alpha, forced=forced, **kw)
     else:
@@ -360,3 +362,35 @@ def _a2_lu_flops(N, nb, k):
     sl = O.tsl(N, nb, k)
     bb, M = sl.stop - sl.start, N - sl.stop
     return 4.0 / 3.0 * bb ** 3 + M * bb * bb + 2.0 * M * bb * bb + 2.0 * M * M * bb
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT f1: diagonal-domain pivoting against the oracle's
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("N,nb,D,crit,alpha,gen,forced_f", [
+    (1024, 128, 1, O.CRIT_MAX, 1.0, "uniform", None),     # one domain: LU with partial pivoting
+    (1024, 128, 2, O.CRIT_MAX, 1.0, "uniform", None),     # QR until the last step
+    (1024, 128, 2, O.CRIT_MAX, 3e4, "normal", None),      # genuine LU / QR mix
+    (1000, 128, 2, O.CRIT_MAX, 1.2e4, "uniform", None),   # ragged last tile (104 rows)
+    (1024, 128, 3, O.CRIT_SUM, 1e5, "normal", None),
+    (1024, 128, 2, O.CRIT_MUMPS, 2.1, "normal", None),    # domain-split local / away maxima
+    (960, 64, 2, O.CRIT_MAX, 1.0, "uniform", 0.5),        # forced pattern: domain LU steps
+    (777, 64, 4, O.CRIT_MAX, math.inf, "uniform", None),  # all LU, ragged, D = 4
+])
+def test_domain_pivoting_parity(H, N, nb, D, crit, alpha, gen, forced_f):
+    A, b = (I.normal_system(1, N) if gen == "normal"
+            else (I.uniform_matrix(0, N), I.uniform_rhs(0, N)))
+    n = (N + nb - 1) // nb
+    forced = I.bernoulli_pattern(30, n, forced_f) if forced_f is not None else None
+    fo, f, F, x = run_pair(H, A, b, nb, crit, alpha, D=D, forced=forced, pivot_scope="domain")
+    np.testing.assert_array_equal(f.decisions(), fo.dec)
+    piv = f.pivots()
+    for k, ip in fo.ipiv.items():  # the stacked domain's pivots (stack coordinates)
+        np.testing.assert_array_equal(piv[k, :len(ip)], ip)
+    assert O.factor_diff(F, fo.A) <= 1e-10, O.factor_diff(F, fo.A)
+    h_o = O.hpl3(A, O.solve(fo, b), b)
+    h_g = O.hpl3(A, x, b)
+    assert h_g <= 16.0 or h_o > 16.0, (h_g, h_o)
+    if D == 1:  # LUPP: the solution of LAPACK's dgesv
+        assert np.all(fo.dec == O.LU)
+        assert np.allclose(x, np.linalg.solve(A, b), rtol=0, atol=1e-9 * np.abs(x).max())
