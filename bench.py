@@ -60,6 +60,10 @@ def parse():
                     help="||A_kk^-1||_1 exact (default) or the Hager/Higham estimate (NEXT f3)")
     ap.add_argument("--lu-variant", default="A1", choices=["A1", "A2"],
                     help="LU step variant (A2: QR-factored diagonal tile, NEXT f4, P:373-397)")
+    ap.add_argument("--pivot-scope", default="tile", choices=["tile", "domain"],
+                    help="domain: diagonal-domain pivoting over the D domains (NEXT f1, P:271-285)")
+    ap.add_argument("--domains", type=int, default=1,
+                    help="single GPU: QR-tree / pivoting domains D (tile rows mod D)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-N", type=int, default=4096)
@@ -185,6 +189,10 @@ def workload_config(args, cfg):
         dec = f"forced Bernoulli pattern f_QR={args.fqr} (seed 30)"
     if args.lu_variant == "A2":
         dec += ", LU variant A2"
+    if args.pivot_scope == "domain":
+        dec += f", diagonal-domain pivoting D={args.domains}"
+    elif args.domains != 1:
+        dec += f", D={args.domains}"
     world = int(os.environ.get("WORLD_SIZE", "1"))
     P, Q = grid_shape(world)
     return {"workload": f"{args.config}: N={N}, nb={nb}, FP64 {cfg['gen']} seed {cfg['seed']}, {dec}",
@@ -217,8 +225,8 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if (world > 1 or args.dist) and args.lu_variant != "A1":
-        raise SystemExit("the multi-GPU path implements LU variant A1 only")
+    if (world > 1 or args.dist) and (args.lu_variant != "A1" or args.pivot_scope != "tile"):
+        raise SystemExit("the multi-GPU path implements LU variant A1 with tile pivoting only")
     if world > 1 or args.dist:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
@@ -270,7 +278,10 @@ def main():
         e0.record(stream)
         f = H.hlq_factor_ex(A, N, nb, crit, args.alpha, forced=forced, profile=int(profile),
                             invnorm_estimate=int(args.invnorm == "estimate"),
-                            lu_variant=H.LU_A2 if args.lu_variant == "A2" else H.LU_A1)
+                            lu_variant=H.LU_A2 if args.lu_variant == "A2" else H.LU_A1,
+                            tree_domains=args.domains,
+                            pivot_scope=H.PIVOT_DOMAIN if args.pivot_scope == "domain"
+                            else H.PIVOT_TILE)
         f.solve(b, x)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -360,6 +371,8 @@ def main():
         opt = H.hlq_default_options()
         opt.invnorm_estimate = int(args.invnorm == "estimate")
         opt.lu_variant = H.LU_A2 if args.lu_variant == "A2" else H.LU_A1
+        opt.tree_domains = args.domains
+        opt.pivot_scope = H.PIVOT_DOMAIN if args.pivot_scope == "domain" else H.PIVOT_TILE
         fv = forced
         if fv is not None:
             fa = np.ascontiguousarray(fv, dtype=np.uint8)

@@ -64,10 +64,13 @@ __device__ __forceinline__ bool dbetter(unsigned long long ka, int ia, unsigned 
 
 constexpr int DT = 256;
 
-// Column c of the stack elimination (c = -1: only the pivot search of column 0).  grid = G CTAs
-// owning contiguous row ranges; part_key / part_idx hold the G partial maxima, *counter the arrivals.
+// Column c of the stack elimination (c = -1: none), updating the columns (c, cend) of its 32-column
+// sub-panel, then the pivot search of column cn (-1: none) with the swap of the whole row.  grid
+// = G CTAs owning contiguous row ranges; part_key / part_idx hold the G partial maxima, *counter the
+// arrivals.
 __global__ void __launch_bounds__(DT) k_dom_step(double* __restrict__ Wd, int64_t R, int bk, int c,
-                                                 int* __restrict__ ipiv, int* __restrict__ zp,
+                                                 int cend, int cn, int* __restrict__ ipiv,
+                                                 int* __restrict__ zp,
                                                  unsigned long long* __restrict__ part_key,
                                                  int* __restrict__ part_idx,
                                                  unsigned int* __restrict__ counter) {
@@ -79,20 +82,19 @@ __global__ void __launch_bounds__(DT) k_dom_step(double* __restrict__ Wd, int64_
   const int64_t rpb = (R + gridDim.x - 1) / gridDim.x;
   const int64_t rb = (int64_t)blockIdx.x * rpb, re = min(R, rb + rpb);
   if (c >= 0) {
-    for (int j = c + tid; j < bk; j += DT) urow[j] = __ldcg(Wd + (int64_t)j * R + c);
+    for (int j = c + tid; j < cend; j += DT) urow[j] = __ldcg(Wd + (int64_t)j * R + c);
     __syncthreads();
     const double d = urow[c];
     if (d != 0.0) {  // exact zero pivot: the column stays unscaled, no update (ledger 7)
       for (int64_t r = max(rb, (int64_t)c + 1) + tid; r < re; r += DT) {
         const double l = Wd[(int64_t)c * R + r] / d;
         Wd[(int64_t)c * R + r] = l;
-        for (int j = c + 1; j < bk; ++j)
+        for (int j = c + 1; j < cend; ++j)  // the sub-panel's columns (the rest: k_dom_trail)
           Wd[(int64_t)j * R + r] = __dsub_rn(Wd[(int64_t)j * R + r], __dmul_rn(l, urow[j]));
       }
     }
   }
-  const int cn = c + 1;
-  if (cn >= bk) return;
+  if (cn < 0 || cn >= bk) return;
   // partial first maximum of column cn over this CTA's rows >= cn
   unsigned long long bkey = 0ull;
   int bidx = 0x7fffffff;
@@ -162,6 +164,83 @@ __global__ void __launch_bounds__(DT) k_dom_step(double* __restrict__ Wd, int64_
   if (tid == 0 && __ldcg(Wd + (int64_t)cn * R + cn) == 0.0) atomicOr(zp, 1);
 }
 
+// After a 32-column sub-panel [c0, c0 + pw): U12 = L11^-1 A12 on the sub-panel's rows (one thread per
+// column, right-looking with the running sums in registers: per element the same sequence of
+// separately rounded multiply / subtract as the unblocked elimination, c ascending).
+__global__ void __launch_bounds__(128) k_dom_u12(double* __restrict__ Wd, int64_t R, int bk, int c0,
+                                                 int pw) {
+  __shared__ double L11[32][33];
+  for (int o = threadIdx.x; o < 32 * 32; o += blockDim.x) {
+    const int c = o >> 5, r = o & 31;
+    L11[c][r] = (c < pw && r < pw) ? Wd[(int64_t)(c0 + c) * R + c0 + r] : 0.0;
+  }
+  __syncthreads();
+  const int j = c0 + pw + blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= bk) return;
+  double* col = Wd + (int64_t)j * R + c0;
+  double acc[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) acc[c] = c < pw ? col[c] : 0.0;
+#pragma unroll
+  for (int l = 0; l < 32; ++l) {
+    if (l < pw) {
+      const double u = acc[l];
+      col[l] = u;
+#pragma unroll
+      for (int c = l + 1; c < 32; ++c) acc[c] = __dsub_rn(acc[c], __dmul_rn(L11[l][c], u));
+    }
+  }
+}
+
+// Trailing update of the stack after a sub-panel: rows [c0 + pw, R) x columns [c0 + pw, bk):
+// W[r][j] -= sum_{c = c0}^{c0+pw-1} L[r][c] U[c][j], c ascending, separately rounded (bit-identical
+// to the unblocked order).  64 x 64 output tiles, 4 x 4 per thread, L21 / U12 blocks in shared memory.
+__global__ void __launch_bounds__(256) k_dom_trail(double* __restrict__ Wd, int64_t R, int bk,
+                                                   int c0, int pw) {
+  __shared__ double Ls[32][65];
+  __shared__ double Us[32][65];
+  const int64_t rbase = c0 + pw + (int64_t)blockIdx.x * 64;
+  const int jbase = c0 + pw + blockIdx.y * 64;
+  const int tid = threadIdx.x;
+  for (int o = tid; o < 32 * 64; o += 256) {
+    const int c = o >> 6, x = o & 63;
+    const int64_t r = rbase + x;
+    const int j = jbase + x;
+    Ls[c][x] = (c < pw && r < R) ? Wd[(int64_t)(c0 + c) * R + r] : 0.0;
+    Us[c][x] = (c < pw && j < bk) ? Wd[(int64_t)j * R + c0 + c] : 0.0;
+  }
+  __syncthreads();
+  const int tr = tid & 15, tc = tid >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t r = rbase + tr + 16 * i;
+      const int j = jbase + tc + 16 * q;
+      acc[i][q] = (r < R && j < bk) ? Wd[(int64_t)j * R + r] : 0.0;
+    }
+  for (int c = 0; c < pw; ++c) {
+    double l[4], u[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) l[i] = Ls[c][tr + 16 * i];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) u[q] = Us[c][tc + 16 * q];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[i][q] = __dsub_rn(acc[i][q], __dmul_rn(l[i], u[q]));
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t r = rbase + tr + 16 * i;
+      const int j = jbase + tc + 16 * q;
+      if (r < R && j < bk) Wd[(int64_t)j * R + r] = acc[i][q];
+    }
+}
+
 // top b x b of the stack -> W (ld nb) for the inverse / criterion kernels; identity permutations
 __global__ void k_dom_top(const double* __restrict__ Wd, int64_t R, int bk, int ldw,
                           double* __restrict__ W, int* __restrict__ perm,
@@ -186,10 +265,26 @@ void launch_dom_factor(double* A, Geo g, int k, int D, DevWork w, cudaStream_t s
   ::hlq::g_launches++;
   k_dom_copy<<<grid_for(R * bk), 256, 0, st>>>(A, g, k, D, w.wdom, R, 0, nullptr);
   int* ipiv_stack = w.dipiv + (size_t)k * g.nb;
-  for (int c = -1; c < bk; ++c) {
+  // blocked right-looking over 32-column sub-panels: per column one k_dom_step inside the
+  // sub-panel, then U12 and the trailing update of the sub-panel's remaining columns
+  auto step = [&](int c, int cend, int cn) {
     ::hlq::g_launches++;
-    k_dom_step<<<G, DT, 0, st>>>(w.wdom, R, bk, c, ipiv_stack, w.zp, w.dom_key, w.dom_idx,
-                                  w.dom_counter);
+    k_dom_step<<<G, DT, 0, st>>>(w.wdom, R, bk, c, cend, cn, ipiv_stack, w.zp, w.dom_key,
+                                  w.dom_idx, w.dom_counter);
+  };
+  step(-1, 0, 0);
+  for (int c0 = 0; c0 < bk; c0 += 32) {
+    const int pw = std::min(32, bk - c0);
+    const int nrest = bk - c0 - pw;
+    // the sub-panel's last column defers the next search until U12 / the trailing update are done
+    for (int c = c0; c < c0 + pw; ++c) step(c, c0 + pw, c + 1 < c0 + pw ? c + 1 : -1);
+    if (nrest > 0) {
+      ::hlq::g_launches += 2;
+      k_dom_u12<<<(nrest + 127) / 128, 128, 0, st>>>(w.wdom, R, bk, c0, pw);
+      dim3 tg((unsigned)((R - c0 - pw + 63) / 64), (unsigned)((nrest + 63) / 64));
+      k_dom_trail<<<tg, 256, 0, st>>>(w.wdom, R, bk, c0, pw);
+      step(-1, 0, c0 + pw);
+    }
   }
   int* perm = reinterpret_cast<int*>(w.scratch + (size_t)2 * g.nb * g.nb);
   ::hlq::g_launches++;
