@@ -670,7 +670,9 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
           }
       asm volatile("bar.sync %0, %1;\n" ::"r"(1 + cg), "n"(32 * RQ));
     }
-    // ---------------- TRMM: U^T = W^T T_b (both warps of the pair), then -U^T
+    // ---------------- TRMM: U^T = W^T T_b (both warps of the pair; T_b is upper triangular, its
+    // 8 x 8 blocks below the diagonal are zero and skipped), then -U^T.  (Splitting the blocks
+    // between the two warps and exchanging them through shared memory measured slower.)
     double uT[2][4][2];
     {
       const double* ts = Ts + (b & 1) * CH3;
@@ -682,6 +684,7 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
       for (int nl = 0; nl < 4; ++nl)
 #pragma unroll
         for (int no = 0; no < 4; ++no) {
+          if (nl > no) continue;
           const double2 tv = lds2(ts + (8 * no + gq) * LD3 + 8 * nl + 2 * tq);
 #pragma unroll
           for (int m = 0; m < 2; ++m) {
