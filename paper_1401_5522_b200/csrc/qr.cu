@@ -400,6 +400,96 @@ __global__ void __launch_bounds__(QT) k_ttmqr(const double* __restrict__ A, Geo 
 // (coalesced down the columns), the vector segment in shared memory; one CTA per tile row (UNMQR)
 // or per TT pair.  Per block b: W = [x_e(b) +] V_b^T x, U = T_b^T W, x -= V_b U [x_e(b) -= U].
 // Dot products: warp w takes reflectors 4w..4w+3, lanes stride the rows, warp-shuffle reduction.
+// The solve's Q^T x, register form: thread t owns rows t and t + 256 of the tile (nb <= 320) and,
+// per reflector block, its rows of V_b (32 registers per row), so V is read once; W = V_b^T x is a
+// transpose-butterfly reduction (31 shuffles per warp) plus a fixed-order sum of the 8 warp
+// partials, U = T_b^T W by 32 threads, and x -= V_b U stays in registers.
+template <bool TT>
+__global__ void __launch_bounds__(256) k_qr_apply_vec2(const double* __restrict__ A, Geo g, int k,
+                                                       int ib, const double* __restrict__ Tb,
+                                                       const int2* __restrict__ pairs,
+                                                       double* __restrict__ x) {
+  __shared__ double red[8][33];
+  __shared__ double Uv[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int e = 0, i;
+  if (TT) {
+    const int2 pr = pairs[blockIdx.x];
+    e = pr.x;
+    i = pr.y;
+  } else {
+    i = k + blockIdx.x;
+  }
+  const int bi = g.bs(i), bk = g.cbs(k);
+  const double* V = g.tile(const_cast<double*>(A), i, k);
+  const double* T = Tb + tri_index(i, k, g.n) * (int64_t)ib * g.nb;
+  double* xi = x + g.r0(i);
+  double* xe = x + g.r0(e);
+  const int r0 = tid, r1 = tid + 256;
+  double x0 = r0 < bi ? xi[r0] : 0.0, x1 = r1 < bi ? xi[r1] : 0.0;
+  for (int i0 = 0; i0 < bk; i0 += 32) {
+    const int sb = min(32, bk - i0);
+    if (!TT && i0 >= bi) break;
+    // this thread's rows of V_b with the reflector structure made explicit
+    double v0[32], v1[32];
+#pragma unroll
+    for (int l = 0; l < 32; ++l) {
+      const int c = i0 + l;
+      const double* col = V + (int64_t)c * g.lda;
+      if (TT) {
+        v0[l] = (l < sb && r0 < bi && r0 <= c) ? col[r0] : 0.0;
+        v1[l] = (l < sb && r1 < bi && r1 <= c) ? col[r1] : 0.0;
+      } else {
+        v0[l] = (l < sb && r0 < bi && r0 >= c) ? (r0 == c ? 1.0 : col[r0]) : 0.0;
+        v1[l] = (l < sb && r1 < bi && r1 >= c) ? (r1 == c ? 1.0 : col[r1]) : 0.0;
+      }
+    }
+    // W = [x_e(b) +] V_b^T x
+    double p[32];
+#pragma unroll
+    for (int l = 0; l < 32; ++l) p[l] = v0[l] * x0 + v1[l] * x1;
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+      const bool upper = (lane & s) != 0;
+#pragma unroll
+      for (int c = 0; c < s; ++c) {
+        const double send = upper ? p[c] : p[c + s];
+        const double keep = upper ? p[c + s] : p[c];
+        p[c] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+      }
+    }
+    red[warp][lane] = p[0];
+    __syncthreads();
+    if (warp == 0) {
+      double w = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) w += red[q][lane];
+      const double xo = (TT && lane < sb) ? xe[i0 + lane] : 0.0;  // x_e(b) before the block
+      if (TT) w += xo;
+      // U = T_b^T W: u_l = sum_{q <= l} T(q, l) W_q (T(q, l) at T[(i0 + l) * ib + q])
+      double u = 0.0;
+      for (int q = 0; q < 32; ++q) {
+        const double wq = __shfl_sync(0xffffffffu, w, q);
+        if (q <= lane && lane < sb) u += T[(int64_t)(i0 + lane) * ib + q] * wq;
+      }
+      Uv[lane] = u;
+      if (TT && lane < sb) xe[i0 + lane] = xo - u;  // x_e(b) -= U
+    }
+    __syncthreads();
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int l = 0; l < 32; ++l) {
+      a0 += v0[l] * Uv[l];
+      a1 += v1[l] * Uv[l];
+    }
+    x0 -= a0;
+    x1 -= a1;
+    __syncthreads();
+  }
+  if (r0 < bi) xi[r0] = x0;
+  if (r1 < bi) xi[r1] = x1;
+}
+
 template <bool TT>
 __global__ void __launch_bounds__(256) k_qr_apply_vec(const double* __restrict__ A, Geo g, int k,
                                                       int ib, const double* __restrict__ Tb,
@@ -494,6 +584,12 @@ void launch_qr_apply(const double* A, Geo g, int k, int ib, const double* Tg, co
   set_attr_once();
   size_t smem = qr_smem_bytes(g.nb);
   if (ncols <= 0) return;
+  if (ncols == 1 && dec == nullptr && ib == 32) {
+    { ::hlq::g_launches++; k_qr_apply_vec2<false><<<g.n - k, 256, 0, st>>>(A, g, k, ib, Tg, nullptr, base); }
+    for (int l = 0; l < nlevels; ++l)
+      { ::hlq::g_launches++; k_qr_apply_vec2<true><<<level_count[l], 256, 0, st>>>(A, g, k, ib, Ttt, level_pairs[l], base); }
+    return;
+  }
   if (ncols == 1 && dec == nullptr && g.nb <= 512) {
     { ::hlq::g_launches++; k_qr_apply_vec<false><<<g.n - k, 256, 0, st>>>(A, g, k, ib, Tg, nullptr, base); }
     for (int l = 0; l < nlevels; ++l)
@@ -514,6 +610,11 @@ void launch_tt_apply(const double* A, Geo g, int k, int ib, const double* Ttt,
   set_attr_once();
   size_t smem = qr_smem_bytes(g.nb);
   if (ncols <= 0) return;
+  if (ncols == 1 && dec == nullptr && ib == 32) {
+    for (int l = 0; l < nlevels; ++l)
+      { ::hlq::g_launches++; k_qr_apply_vec2<true><<<level_count[l], 256, 0, st>>>(A, g, k, ib, Ttt, level_pairs[l], base); }
+    return;
+  }
   if (ncols == 1 && dec == nullptr && g.nb <= 512) {
     for (int l = 0; l < nlevels; ++l)
       { ::hlq::g_launches++; k_qr_apply_vec<true><<<level_count[l], 256, 0, st>>>(A, g, k, ib, Ttt, level_pairs[l], base); }
