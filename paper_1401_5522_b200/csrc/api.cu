@@ -437,17 +437,25 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
           launch_lu_update(A, g, k, wk, c0, c1, fuse ? w.colpart : nullptr, st);
           P.end(st);
         }
+        bool qr_fused = false;
         if (known != HLQ_DEC_LU) {
           P.begin(HLQ_PROF_QR_UNMQR, st);
-          launch_qr_update(A, g, k, ib, f->lvl_ptr[k].data(), f->lvl_cnt[k].data(), nl, wk, c0, c1,
-                           st);
+          // a12 fused into the TTMQR epilogues: every row i > k is final after its merge
+          qr_fused = launch_qr_update(A, g, k, ib, f->lvl_ptr[k].data(), f->lvl_cnt[k].data(), nl,
+                                      wk, c0, c1, st,
+                                      (f->track_growth && k + 1 < n) ? w.gstep + k + 1 : nullptr);
           P.end(st);
         }
-        // a12: the QR branch (or no fusion) scans the updated columns; the LU GEMM fused it
-        if (f->track_growth && k + 1 < n && !(fuse && known == HLQ_DEC_LU)) {
+        // a12 for whatever branch did not fuse it: the LU GEMM epilogue (fuse) and the TTMQR
+        // epilogues (qr_fused) cover their own branch; the rest is scanned, predicated on d_k
+        const bool lu_done = fuse || known == HLQ_DEC_QR;
+        const bool qr_done = qr_fused || known == HLQ_DEC_LU;
+        if (f->track_growth && k + 1 < n && !(lu_done && qr_done)) {
           P.begin(HLQ_PROF_GROWTH, st);
-          if (fuse)
+          if (lu_done)
             launch_tile_norm_max(A, g, k + 1, w.gstep + k + 1, st, w.dec, k, HLQ_DEC_QR, c0, c1);
+          else if (qr_done)
+            launch_tile_norm_max(A, g, k + 1, w.gstep + k + 1, st, w.dec, k, HLQ_DEC_LU, c0, c1);
           else
             launch_tile_norm_max(A, g, k + 1, w.gstep + k + 1, st, nullptr, 0, 0, c0, c1);
           P.end(st);

@@ -106,13 +106,16 @@ void launch_qr_panel_tc(double* A, Geo g, int k, int ib, double* Tg, double* Ttt
                         const int2* pairs, int npairs, const uint8_t* dec, bool tt,
                         cudaStream_t st, int i_first = -1);
 // UNMQR (tt = false) / one TTMQR level (tt = true) on the column block (base, ldc, ncols)
-void launch_qr_update2(const double* A, Geo g, int k, const double* T, const int2* pairs,
+// gmax (TT only): fuse the eliminated tiles' column abs-sum maxima into *gmax (a12); returns
+// whether the fused kernel ran (false: the caller scans the columns itself)
+bool launch_qr_update2(const double* A, Geo g, int k, const double* T, const int2* pairs,
                        int npairs, bool tt, double* base, int64_t ldc, int64_t ncols,
-                       const uint8_t* dec, cudaStream_t st);
-void launch_qr_update_dmma(const double* A, Geo g, int k, int ib, const double* Tg,
+                       const uint8_t* dec, cudaStream_t st, double* gmax = nullptr);
+bool launch_qr_update_dmma(const double* A, Geo g, int k, int ib, const double* Tg,
                            const double* Ttt, const int2* const* level_pairs,
                            const int* level_count, int nlevels, double* base, int64_t ldc,
-                           int64_t ncols, const uint8_t* dec, int what, cudaStream_t st);
+                           int64_t ncols, const uint8_t* dec, int what, cudaStream_t st,
+                           double* gmax = nullptr);
 // TTMQR levels only (no UNMQR) on a column block: the solve's cross-rank head merges
 void launch_tt_apply(const double* A, Geo g, int k, int ib, const double* Ttt,
                      const int2* const* level_pairs, const int* level_count, int nlevels,
@@ -143,9 +146,10 @@ void launch_gemm_sub(double* C, int64_t ldc, const double* Am, int64_t lda, cons
 void launch_qr_panel(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
                      const int* level_count, int nlevels, const DevWork& w, cudaStream_t st,
                      bool diag_done = false);
-void launch_qr_update(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
+// returns whether every TTMQR level fused the a12 scan into gmax (gmax != nullptr)
+bool launch_qr_update(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
                       const int* level_count, int nlevels, const DevWork& w, int64_t c0,
-                      int64_t c1, cudaStream_t st);
+                      int64_t c1, cudaStream_t st, double* gmax = nullptr);
 void launch_tile_norm_max(const double* A, Geo g, int k, double* out, cudaStream_t st,
                           const uint8_t* dec = nullptr, int step = 0, int want = 0,
                           int64_t cb = -1, int64_t ce = -1);

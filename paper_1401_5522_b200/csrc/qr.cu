@@ -651,14 +651,15 @@ void launch_qr_panel(double* A, Geo g, int k, int ib, const int2* const* level_p
 
 // Update stage of a QR step on the trailing columns [c0, c1): UNMQR of every tile row, then the
 // TTMQR of every level in order.  Predicated on dec[k] == QR.
-void launch_qr_update(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
+bool launch_qr_update(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
                       const int* level_count, int nlevels, const DevWork& w, int64_t c0,
-                      int64_t c1, cudaStream_t st) {
+                      int64_t c1, cudaStream_t st, double* gmax) {
   set_attr_once();
   const size_t smem = qr_smem_bytes(g.nb);
   const uint8_t* dec = w.dec;
   const int64_t ncols = c1 - c0;
-  if (ncols <= 0) return;
+  if (ncols <= 0) return true;
+  bool fused = gmax != nullptr && nlevels > 0;
   double* base = A + c0 * g.lda;
   const unsigned slabs = (unsigned)((ncols + 63) / 64);
   const bool tc = (ib == 32);  // DMMA trailing updates (qr_dmma.cu) need 32-row reflector blocks
@@ -668,12 +669,15 @@ void launch_qr_update(double* A, Geo g, int k, int ib, const int2* const* level_
   else
     { ::hlq::g_launches++; k_unmqr<<<dim3(slabs, g.n - k), QT, smem, st>>>(A, g, k, ib, w.Tg, base, g.lda, ncols, dec); }
   for (int l = 0; l < nlevels; ++l) {
-    if (tc)
-      launch_qr_update_dmma(A, g, k, ib, w.Tg, w.Ttt, level_pairs, level_count, nlevels, base,
-                            g.lda, ncols, dec, 1 + l, st);
-    else
+    if (tc) {
+      fused &= launch_qr_update_dmma(A, g, k, ib, w.Tg, w.Ttt, level_pairs, level_count, nlevels,
+                                     base, g.lda, ncols, dec, 1 + l, st, gmax);
+    } else {
+      fused = false;
       { ::hlq::g_launches++; k_ttmqr<<<dim3(slabs, level_count[l]), QT, smem, st>>>(A, g, k, ib, w.Ttt, level_pairs[l], base, g.lda, ncols, dec); }
+    }
   }
+  return fused;
 }
 
 }  // namespace hlq

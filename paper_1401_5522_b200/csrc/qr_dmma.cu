@@ -688,24 +688,19 @@ static void launch_w(const double* A, Geo g, int k, int ib, const double* Tg, co
 
 // what = 0: UNMQR of all tile rows; what = 1 + l: TTMQR of level l.  Column slab width 64 when the
 // slab + reflector block fit in shared memory (nb <= 256), else 32.
-void launch_qr_update2(const double* A, Geo g, int k, const double* T, const int2* pairs,
-                       int npairs, bool tt, double* base, int64_t ldc, int64_t ncols,
-                       const uint8_t* dec, cudaStream_t st);
-
-void launch_qr_update_dmma(const double* A, Geo g, int k, int ib, const double* Tg,
+bool launch_qr_update_dmma(const double* A, Geo g, int k, int ib, const double* Tg,
                            const double* Ttt, const int2* const* level_pairs,
                            const int* level_count, int nlevels, double* base, int64_t ldc,
-                           int64_t ncols, const uint8_t* dec, int what, cudaStream_t st) {
-  if (ncols <= 0) return;
+                           int64_t ncols, const uint8_t* dec, int what, cudaStream_t st,
+                           double* gmax) {
+  if (ncols <= 0) return true;
   static int v1 = -1;
   if (v1 < 0) v1 = getenv("HLQ_QR_UPDATE_V1") ? 1 : 0;
   if (!v1 && ib == 32) {
     if (what == 0)
-      launch_qr_update2(A, g, k, Tg, nullptr, 0, false, base, ldc, ncols, dec, st);
-    else
-      launch_qr_update2(A, g, k, Ttt, level_pairs[what - 1], level_count[what - 1], true, base,
-                        ldc, ncols, dec, st);
-    return;
+      return launch_qr_update2(A, g, k, Tg, nullptr, 0, false, base, ldc, ncols, dec, st);
+    return launch_qr_update2(A, g, k, Ttt, level_pairs[what - 1], level_count[what - 1], true,
+                             base, ldc, ncols, dec, st, gmax);
   }
   if (qd_smem<64>(g.nb) <= 227 * 1024)
     launch_w<64>(A, g, k, ib, Tg, Ttt, level_pairs, level_count, nlevels, base, ldc, ncols, dec,
@@ -713,6 +708,7 @@ void launch_qr_update_dmma(const double* A, Geo g, int k, int ib, const double* 
   else
     launch_w<32>(A, g, k, ib, Tg, Ttt, level_pairs, level_count, nlevels, base, ldc, ncols, dec,
                  what, st);
+  return false;
 }
 
 }  // namespace hlq

@@ -395,17 +395,19 @@ static bool launch_nw(const double* A, Geo g, int k, const double* T, const int2
 // T = TTQRT factors) on the column block (base, ldc, ncols).  Requires ib = 32 and nb <= 512.
 bool launch_qr_update3(const double* A, Geo g, int k, const double* T, const int2* pairs,
                        int npairs, bool tt, double* base, int64_t ldc, int64_t ncols,
-                       const uint8_t* dec, cudaStream_t st);
+                       const uint8_t* dec, cudaStream_t st, double* gmax);
 
-void launch_qr_update2(const double* A, Geo g, int k, const double* T, const int2* pairs,
+bool launch_qr_update2(const double* A, Geo g, int k, const double* T, const int2* pairs,
                        int npairs, bool tt, double* base, int64_t ldc, int64_t ncols,
-                       const uint8_t* dec, cudaStream_t st) {
-  if (ncols <= 0) return;
-  if (launch_qr_update3(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st)) return;
-  if (launch_nw<8>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st)) return;
-  if (launch_nw<7>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st)) return;
-  if (launch_nw<6>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st)) return;
+                       const uint8_t* dec, cudaStream_t st, double* gmax) {
+  if (ncols <= 0) return true;
+  if (launch_qr_update3(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st, gmax))
+    return true;
+  if (launch_nw<8>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st)) return false;
+  if (launch_nw<7>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st)) return false;
+  if (launch_nw<6>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st)) return false;
   launch_nw<4>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st);
+  return false;
 }
 
 // =============================================================================================
@@ -438,7 +440,8 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
                                                    const double* __restrict__ Tbase,
                                                    const int2* __restrict__ pairs,
                                                    double* __restrict__ base, int64_t ldcg,
-                                                   int64_t ncols, const uint8_t* __restrict__ dec) {
+                                                   int64_t ncols, const uint8_t* __restrict__ dec,
+                                                   double* __restrict__ gmax) {
   if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
   constexpr int NCH = NB / 32;       // 32-row chunks of a tile
   constexpr int NJ = NB / (8 * RQ);  // 8-row blocks owned by one row group
@@ -758,6 +761,33 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
       }
     }
   }
+  // a12 fused (TT): the eliminated tile's rows are final after its merge, so the slab's column
+  // abs-sums over the tile give its share of max_{i,j>k} ||A_ij||_1 for the next step
+  if (TT && gmax != nullptr) {
+    double cs[2];
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      double a = 0.0;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) a += fabs(cT[m][j][0]) + fabs(cT[m][j][1]);
+      a += __shfl_xor_sync(0xffffffffu, a, 1);
+      a += __shfl_xor_sync(0xffffffffu, a, 2);
+      cs[m] = a;
+    }
+    double* xr = Rb + cg * 512;  // the row groups' partial column sums (Rb is free here)
+    __syncthreads();
+    if (tq == 0) {
+      xr[rh * 16 + gq] = cs[0];
+      xr[rh * 16 + 8 + gq] = cs[1];
+    }
+    __syncthreads();
+    if (rh == 0 && lane < 16) {
+      double v = 0.0;
+#pragma unroll
+      for (int r2 = 0; r2 < RQ; ++r2) v += xr[r2 * 16 + lane];
+      if (wc + lane < cvalid) atomic_max_nonneg(gmax, fabs(v));
+    }
+  }
 }
 
 static size_t upd3_smem(int warps, int W) {
@@ -767,7 +797,7 @@ static size_t upd3_smem(int warps, int W) {
 template <int NB, int RQ, int NCG, bool V16>
 static void launch3(const double* A, Geo g, int k, const double* T, const int2* pairs, int npairs,
                     bool tt, double* base, int64_t ldc, int64_t ncols, const uint8_t* dec,
-                    cudaStream_t st) {
+                    cudaStream_t st, double* gmax) {
   static bool attr = false;
   if (!attr) {
     smem_optin(k_qr_update3<NB, false, RQ, NCG, V16>);
@@ -779,19 +809,19 @@ static void launch3(const double* A, Geo g, int k, const double* T, const int2* 
   if (!tt) {
     ::hlq::g_launches++;
     k_qr_update3<NB, false, RQ, NCG, V16><<<dim3(slabs, g.n - k), 32 * RQ * NCG, smem, st>>>(
-        A, g, k, T, nullptr, base, ldc, ncols, dec);
+        A, g, k, T, nullptr, base, ldc, ncols, dec, nullptr);
   } else {
     if (npairs <= 0) return;
     ::hlq::g_launches++;
     k_qr_update3<NB, true, RQ, NCG, V16><<<dim3(slabs, npairs), 32 * RQ * NCG, smem, st>>>(
-        A, g, k, T, pairs, base, ldc, ncols, dec);
+        A, g, k, T, pairs, base, ldc, ncols, dec, gmax);
   }
 }
 
 // v3 for nb in {64, 128, 192, 256, 320}; false -> the caller falls back to v2
 bool launch_qr_update3(const double* A, Geo g, int k, const double* T, const int2* pairs,
                        int npairs, bool tt, double* base, int64_t ldc, int64_t ncols,
-                       const uint8_t* dec, cudaStream_t st) {
+                       const uint8_t* dec, cudaStream_t st, double* gmax) {
   static int off = -1;
   if (off < 0) off = getenv("HLQ_QR_UPDATE_V2") ? 1 : 0;
   if (off) return false;
@@ -804,11 +834,11 @@ bool launch_qr_update3(const double* A, Geo g, int k, const double* T, const int
 #define HLQ_L3(NBV)                                                                        \
   case NBV:                                                                                \
     if (!v16)                                                                              \
-      launch3<NBV, 2, 2, false>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st); \
+      launch3<NBV, 2, 2, false>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st, gmax); \
     else if (ncg == 4)                                                                     \
-      launch3<NBV, 2, 4, true>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st);  \
+      launch3<NBV, 2, 4, true>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st, gmax);  \
     else                                                                                   \
-      launch3<NBV, 2, 2, true>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st);  \
+      launch3<NBV, 2, 2, true>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st, gmax);  \
     return true;
   switch (g.nb) {
     HLQ_L3(64)
