@@ -75,17 +75,25 @@ void cache_put(int slot, void* p, size_t bytes) {
 }
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// a DevWork view whose kernels are not predicated on d_k (speculative work)
+hlq::DevWork wk_nodec(const hlq::DevWork& w) {
+  hlq::DevWork v = w;
+  v.dec = nullptr;
+  return v;
+}
 }  // namespace
 
-// the library's high-priority panel stream (lookahead), created once per process
-static cudaStream_t panel_stream() {
-  static cudaStream_t sp = nullptr;
-  if (!sp) {
+// the library's high-priority panel streams (lookahead), created once per process: sp runs the
+// criterion (speculative LU) and the chosen branch, sq the speculative QR panel beside it
+static cudaStream_t panel_stream(int which = 0) {
+  static cudaStream_t s[2] = {nullptr, nullptr};
+  if (!s[which]) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    cudaStreamCreateWithPriority(&sp, cudaStreamNonBlocking, hi);
+    cudaStreamCreateWithPriority(&s[which], cudaStreamNonBlocking, hi);
   }
-  return sp;
+  return s[which];
 }
 
 
@@ -200,8 +208,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   hlq_factors_t f = new (std::nothrow) hlq_factors_s();
   if (!f) return HLQ_ERR_NOMEM;
   *out = f;
-  cudaEventCreateWithFlags(&f->ev[0], cudaEventDisableTiming);
-  cudaEventCreateWithFlags(&f->ev[1], cudaEventDisableTiming);
+  for (int e = 0; e < 4; ++e) cudaEventCreateWithFlags(&f->ev[e], cudaEventDisableTiming);
   f->A = A;
   f->g.N = N;
   f->g.lda = lda;
@@ -253,10 +260,18 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
          oLi = take(sizeof(double) * (size_t)n * 2 * nb * nb),
          oLp = take(sizeof(int) * (size_t)n * nb), oSt2 = take(sizeof(double) * (size_t)nb);
   const bool dpiv = opt.pivot_scope == HLQ_PIVOT_DOMAIN;
+  // speculative QR panel: with a criterion to evaluate, the QR branch's panel (GEQRT of every tile +
+  // every TTQRT level) runs on a copy of the panel beside the speculative LU and the criterion, and
+  // is copied back if the step is QR (A1, ib = 32; HLQ_SPEC_QR=0 disables it)
+  static int spec_env = -1;
+  if (spec_env < 0) spec_env = getenv("HLQ_SPEC_QR") ? atoi(getenv("HLQ_SPEC_QR")) : 1;
+  const bool spec_qr = spec_env != 0 && !opt.forced && alpha > 0.0 && !isinf(alpha) &&
+                       opt.lu_variant == HLQ_LU_A1 && opt.ib == 32;
   size_t oWd = take(dpiv ? sizeof(double) * (size_t)N * nb : 8),
          oDp = take(dpiv ? sizeof(int) * (size_t)n * nb : 8),
          oDk = take(sizeof(unsigned long long) * 2 * 148), oDi = take(sizeof(int) * 2 * 148),
-         oDc = take(sizeof(unsigned int));
+         oDc = take(sizeof(unsigned int)),
+         oQp = take(spec_qr ? sizeof(double) * (size_t)N * nb : 8);
   f->ws_bytes = off;
   f->ws_block = cache_get(0, off);
   if (!f->ws_block) return HLQ_ERR_NOMEM;
@@ -289,6 +304,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   w.luperm = (int*)(base + oLp);
   w.solve_t = (double*)(base + oSt2);
   w.wdom = dpiv ? (double*)(base + oWd) : nullptr;
+  w.qpan = spec_qr ? (double*)(base + oQp) : nullptr;
   w.dipiv = dpiv ? (int*)(base + oDp) : nullptr;
   w.dom_key = (unsigned long long*)(base + oDk);
   w.dom_idx = (int*)(base + oDi);
@@ -333,8 +349,8 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   cudaMemsetAsync(w.ipiv, 0, sizeof(int) * (size_t)n * nb, st);
   // Two streams: st (the caller's) runs the trailing updates, sp (high priority) runs the panel
   // stage of step k+1 as soon as step k has updated column block k+1 (lookahead depth 1).
-  cudaStream_t sp = panel_stream();
-  cudaEvent_t ev_ready = f->ev[0], ev_panel = f->ev[1];
+  cudaStream_t sp = panel_stream(0), sq = panel_stream(1);
+  cudaEvent_t ev_ready = f->ev[0], ev_panel = f->ev[1], ev_qsrc = f->ev[2], ev_qdone = f->ev[3];
   if (f->track_growth) launch_tile_norm_max(A, g, 0, w.gstep, st);
   cudaEventRecord(ev_ready, st);
 
@@ -356,6 +372,23 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
     // ---- panel stage P(k) on sp: criterion, speculative GETRF, decision, the chosen branch's
     //      panel work (LU: commit + TRSM; QR: GEQRT + all TTQRT levels)
     cudaStreamWaitEvent(sp, ev_ready, 0);
+    const bool spec = spec_qr && known == -1 && k + 1 < n;
+    if (spec) {
+      // the QR branch's panel on a copy of column block k (rows >= k0, global row indices, ld N)
+      const int64_t k0 = g.r0(k);
+      const int bk = g.cbs(k);
+      cudaStreamWaitEvent(sq, ev_ready, 0);
+      launch_copy_block(w.qpan + k0, N, A + k0 * lda + k0, lda, N - k0, bk, nullptr, nullptr, 0,
+                        sq);
+      cudaEventRecord(ev_qsrc, sq);  // (the LU branch may overwrite A's panel only after this)
+      Geo gq = g;
+      gq.lda = N;
+      P.begin(HLQ_PROF_QR_GEQRT, sq);
+      launch_qr_panel(w.qpan - k0 * N, gq, k, ib, f->lvl_ptr[k].data(), f->lvl_cnt[k].data(), nl,
+                      wk_nodec(wk), sq);
+      P.end(sq);
+      cudaEventRecord(ev_qdone, sq);
+    }
     if (known != HLQ_DEC_QR) {
       if (criterion_needed) {
         P.begin(HLQ_PROF_CRITERION, sp);
@@ -402,6 +435,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
     launch_decide(g, k, criterion, alpha, opt.mumps_reading, opt.tie_rel_tol, opt.forced != nullptr,
                   w.ref_dec != nullptr, wk, sp);
     P.end(sp);
+    if (spec) cudaStreamWaitEvent(sp, ev_qsrc, 0);
     if (known != HLQ_DEC_QR) {
       P.begin(HLQ_PROF_LU_TRSM, sp);
       launch_lu_panel(A, g, k, wk, sp, /*commit=*/!a2 && !dpiv);
@@ -416,7 +450,13 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
                        sp);
       P.end(sp);
     }
-    if (known != HLQ_DEC_LU) {
+    if (spec) {
+      // QR decision: the speculative panel replaces A's column block k (rows >= k0)
+      cudaStreamWaitEvent(sp, ev_qdone, 0);
+      const int64_t k0 = g.r0(k);
+      launch_copy_block_if(A + k0 * lda + k0, lda, w.qpan + k0, N, N - k0, g.cbs(k), w.dec, k,
+                           HLQ_DEC_QR, sp);
+    } else if (known != HLQ_DEC_LU) {
       P.begin(HLQ_PROF_QR_GEQRT, sp);
       launch_qr_panel(A, g, k, ib, f->lvl_ptr[k].data(), f->lvl_cnt[k].data(), nl, wk, sp,
                       /*diag_done=*/a2 && known != HLQ_DEC_QR);

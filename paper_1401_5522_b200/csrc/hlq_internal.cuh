@@ -65,6 +65,7 @@ struct DevWork {
   int* luperm;        // per LU step k: composed row permutation of P_kk (nb ints), or null
   double* solve_t;    // nb scratch doubles for the solve
   // NEXT f1 (diagonal-domain pivoting), null otherwise
+  double* qpan;       // N*nb: the speculative QR panel (rows indexed globally, ld N), or null
   double* wdom;       // N*nb: the stacked domain panel (ld = its row count)
   int* dipiv;         // n*nb: per step, the domain's pivots in stack coordinates
   unsigned long long* dom_key;  // 2*148 partial pivot keys
@@ -95,6 +96,10 @@ void launch_lu_commit(double* A, Geo g, int k, const double* W, const int* ipiv_
                       int* perm, const uint8_t* dec, cudaStream_t st);
 void launch_copy_block(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
                        int64_t cols, const int* perm, const uint8_t* dec, int k, cudaStream_t st);
+// dst <- src (rows x cols) when dec[k] == want; unconditional copy when dec == nullptr is not
+// supported (use launch_copy_block)
+void launch_copy_block_if(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
+                          int64_t cols, const uint8_t* dec, int k, int want, cudaStream_t st);
 // dst[0:n) = src[0:n) (ints) when dec[k] == LU
 void launch_copy_ints(int* dst, const int* src, int n, const uint8_t* dec, int k, cudaStream_t st);
 void launch_dgemm(double* C, int64_t ldc, const double* A, int64_t lda, const double* B,

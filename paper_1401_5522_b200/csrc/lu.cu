@@ -37,6 +37,19 @@ __global__ void k_lu_commit(double* __restrict__ A, Geo g, int k, const double* 
   }
 }
 
+// dst <- src (rows x cols) when dec[k] == want (the speculative QR panel's copy-back)
+__global__ void k_copy_block_if(double* __restrict__ dst, int64_t ldd, const double* __restrict__ src,
+                                int64_t lds, int64_t rows, int64_t cols,
+                                const uint8_t* __restrict__ dec, int k, int want) {
+  if (dec[k] != want) return;
+  const int64_t total = rows * cols;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = t / rows, r = t - c * rows;
+    dst[c * ldd + r] = src[c * lds + r];
+  }
+}
+
 // dst (rows x cols, ld_dst) <- src (ld_src), optionally with rows gathered through perm
 __global__ void k_copy_block(double* __restrict__ dst, int64_t ldd, const double* __restrict__ src,
                              int64_t lds, int64_t rows, int64_t cols,
@@ -61,6 +74,14 @@ void launch_lu_commit(double* A, Geo g, int k, const double* W, const int* ipiv_
                       int* perm, const uint8_t* dec, cudaStream_t st) {
   ::hlq::g_launches++;
   k_lu_commit<<<8, 256, 0, st>>>(A, g, k, W, ipiv_ws, ipiv, perm, dec);
+}
+
+void launch_copy_block_if(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
+                          int64_t cols, const uint8_t* dec, int k, int want, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return;
+  ::hlq::g_launches++;
+  k_copy_block_if<<<grid_for(rows * cols), 256, 0, st>>>(dst, ldd, src, lds, rows, cols, dec, k,
+                                                         want);
 }
 
 void launch_copy_block(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
