@@ -208,7 +208,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   hlq_factors_t f = new (std::nothrow) hlq_factors_s();
   if (!f) return HLQ_ERR_NOMEM;
   *out = f;
-  for (int e = 0; e < 4; ++e) cudaEventCreateWithFlags(&f->ev[e], cudaEventDisableTiming);
+  for (int e = 0; e < 5; ++e) cudaEventCreateWithFlags(&f->ev[e], cudaEventDisableTiming);
   f->A = A;
   f->g.N = N;
   f->g.lda = lda;
@@ -266,7 +266,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   static int spec_env = -1;
   if (spec_env < 0) spec_env = getenv("HLQ_SPEC_QR") ? atoi(getenv("HLQ_SPEC_QR")) : 1;
   const bool spec_qr = spec_env != 0 && !opt.forced && alpha > 0.0 && !isinf(alpha) &&
-                       opt.lu_variant == HLQ_LU_A1 && opt.ib == 32;
+                       opt.ib == 32;
   size_t oWd = take(dpiv ? sizeof(double) * (size_t)N * nb : 8),
          oDp = take(dpiv ? sizeof(int) * (size_t)n * nb : 8),
          oDk = take(sizeof(unsigned long long) * 2 * 148), oDi = take(sizeof(int) * 2 * 148),
@@ -350,7 +350,8 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   // Two streams: st (the caller's) runs the trailing updates, sp (high priority) runs the panel
   // stage of step k+1 as soon as step k has updated column block k+1 (lookahead depth 1).
   cudaStream_t sp = panel_stream(0), sq = panel_stream(1);
-  cudaEvent_t ev_ready = f->ev[0], ev_panel = f->ev[1], ev_qsrc = f->ev[2], ev_qdone = f->ev[3];
+  cudaEvent_t ev_ready = f->ev[0], ev_panel = f->ev[1], ev_qsrc = f->ev[2], ev_qdone = f->ev[3],
+              ev_a2 = f->ev[4];
   if (f->track_growth) launch_tile_norm_max(A, g, 0, w.gstep, st);
   cudaEventRecord(ev_ready, st);
 
@@ -373,11 +374,12 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
     //      panel work (LU: commit + TRSM; QR: GEQRT + all TTQRT levels)
     cudaStreamWaitEvent(sp, ev_ready, 0);
     const bool spec = spec_qr && known == -1 && k + 1 < n;
-    if (spec) {
-      // the QR branch's panel on a copy of column block k (rows >= k0, global row indices, ld N)
+    // the QR branch's panel on a copy of column block k (rows >= k0, global row indices, ld N),
+    // started once the panel is in its pre-branch state (A2: after the diagonal GEQRT)
+    auto start_spec = [&](cudaEvent_t after) {
       const int64_t k0 = g.r0(k);
       const int bk = g.cbs(k);
-      cudaStreamWaitEvent(sq, ev_ready, 0);
+      cudaStreamWaitEvent(sq, after, 0);
       launch_copy_block(w.qpan + k0, N, A + k0 * lda + k0, lda, N - k0, bk, nullptr, nullptr, 0,
                         sq);
       cudaEventRecord(ev_qsrc, sq);  // (the LU branch may overwrite A's panel only after this)
@@ -385,10 +387,11 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
       gq.lda = N;
       P.begin(HLQ_PROF_QR_GEQRT, sq);
       launch_qr_panel(w.qpan - k0 * N, gq, k, ib, f->lvl_ptr[k].data(), f->lvl_cnt[k].data(), nl,
-                      wk_nodec(wk), sq);
+                      wk_nodec(wk), sq, /*diag_done=*/a2);
       P.end(sq);
       cudaEventRecord(ev_qdone, sq);
-    }
+    };
+    if (spec && !a2) start_spec(ev_ready);
     if (known != HLQ_DEC_QR) {
       if (criterion_needed) {
         P.begin(HLQ_PROF_CRITERION, sp);
@@ -411,6 +414,10 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
         const double* Tkk = w.Tg + tri_index(k, k, n) * (int64_t)ib * nb;
         launch_qr_panel_tc(Akk, gk, 0, ib, const_cast<double*>(Tkk), nullptr, nullptr, 0, nullptr,
                            false, sp);
+        if (spec) {
+          cudaEventRecord(ev_a2, sp);
+          start_spec(ev_a2);
+        }
         launch_a2_prep(A, g, k, wk, sp);
         launch_tri_inv(g, k, wk, wk.ws_panel, wk.scratch + (size_t)nb * nb, sp);
         launch_qr_update2(Akk, gk, 0, Tkk, nullptr, 0, false, wk.scratch, nb, bk, nullptr, sp);

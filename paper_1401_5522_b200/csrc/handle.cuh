@@ -66,7 +66,7 @@ struct Prof {
 
 struct hlq_factors_s {
   Prof prof;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   double* A = nullptr;
   Geo g{};
   int ib = 32, D = 1, crit = 0;
