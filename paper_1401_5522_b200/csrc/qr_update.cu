@@ -448,9 +448,11 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
   constexpr int QPC = 4 / RQ;        // of those, per 32-row chunk
   constexpr int NT = 32 * RQ * NCG;
   constexpr int W = 16 * NCG;        // slab columns
-  // ring depth: T_b and C_e(b) land in buffer b & 1 up to RING - 1 chunks ahead; safe because block b + 2's
-  // first chunk is issued after every warp finished block b's TRMM (n0(b) + 2 n0(b+1) >= RING - 1
-  // chunks separate them for both chunk schedules)
+  // ring depth: T_b and C_e(b) land in buffer b & 1 with block b's first chunk, issued up to
+  // `ahead` chunks before it is consumed; safe when block b + 2's first chunk is issued after every
+  // warp finished block b's TRMM, i.e. n0(b) + 2 n0(b+1) >= ahead (n0 = chunks per pass).  That holds
+  // for ahead = RING - 1 = 4 except in a TT merge whose eliminated tile has <= 32 rows (every
+  // block one chunk: 1 + 2 = 3), where the distance drops to 3 (see short3 below).
   constexpr int RING = 5;
   extern __shared__ __align__(16) double sm[];
   double* ring = sm;                     // RING x CH3: V chunks [l][r] (ld LD3 / LD3B by pass)
@@ -583,8 +585,11 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
     }
     commit_();
   };
+  // a TT merge of a tile with <= 32 rows has one chunk per pass in every block: prefetch 3 chunks
+  // ahead instead of 4 so block b + 2's T / C_e never overwrite block b's before its TRMM
+  const bool short3 = TT && nch_i == 1;
 #pragma unroll 1
-  for (int d = 0; d < RING - 1; ++d) issue();
+  for (int d = 0; d < (short3 ? RING - 2 : RING - 1); ++d) issue();
   // explicit structure of the diagonal 32 x 32 block of V_b (GEQRT: unit diagonal, zeros above;
   // TT: zeros below the diagonal); element (r, l) at V[r * sr + l * sl]
   auto fix_diag = [&](double* V, int sr, int sl) {
@@ -616,7 +621,10 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) {
       if (ch < clo || ch > chi) continue;
-      wait_<RING - 2>();
+      if (short3)
+        wait_<RING - 3>();
+      else
+        wait_<RING - 2>();
       __syncthreads();
       issue();
       const double* V = cslot;
@@ -718,7 +726,10 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) {
       if (ch < clo || ch > chi) continue;
-      wait_<RING - 2>();
+      if (short3)
+        wait_<RING - 3>();
+      else
+        wait_<RING - 2>();
       __syncthreads();
       issue();
       const double* V = cslot;
@@ -818,7 +829,7 @@ static void launch3(const double* A, Geo g, int k, const double* T, const int2* 
   }
 }
 
-// v3 for nb in {64, 128, 192, 256, 320}; false -> the caller falls back to v2
+// v3 for every nb <= 320 (instantiated at 64, 128, 192, 256, 320); false -> the caller falls back to v2
 bool launch_qr_update3(const double* A, Geo g, int k, const double* T, const int2* pairs,
                        int npairs, bool tt, double* base, int64_t ldc, int64_t ncols,
                        const uint8_t* dec, cudaStream_t st, double* gmax) {
@@ -840,7 +851,10 @@ bool launch_qr_update3(const double* A, Geo g, int k, const double* T, const int
     else                                                                                   \
       launch3<NBV, 2, 2, true>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st, gmax);  \
     return true;
-  switch (g.nb) {
+  // the instantiation with the next tile size up: smaller tiles are its ragged case (every row,
+  // column and reflector bound is a runtime mask), e.g. the paper's nb = 240 runs on NB = 256
+  const int nbi = g.nb <= 64 ? 64 : g.nb <= 128 ? 128 : g.nb <= 192 ? 192 : g.nb <= 256 ? 256 : 320;
+  switch (nbi) {
     HLQ_L3(64)
     HLQ_L3(128)
     HLQ_L3(192)

@@ -132,10 +132,20 @@ def test_mumps_m2_reading(H):
                                              # kernel instantiation for nb = 320, 32-column tail)
                                              (1000, 320, O.CRIT_MAX, 1.0),
                                              (1000, 320, O.CRIT_MAX, 1.6e4),
-                                             # nb outside the register-slab instantiations (96):
-                                             # the shared-memory QR update path
+                                             # nb between the register-slab instantiations (96,
+                                             # 160, the paper's 240): the next instantiation up
+                                             # runs them as its ragged case
                                              (800, 96, O.CRIT_MAX, 1.0),
-                                             (1001, 192, O.CRIT_MAX, 1.0)])
+                                             (900, 160, O.CRIT_MAX, 1.0),
+                                             (1200, 240, O.CRIT_MAX, 1.0),
+                                             (1000, 240, O.CRIT_MAX, 1.2e4),
+                                             (1001, 192, O.CRIT_MAX, 1.0),
+                                             # last tile of <= 32 rows with >= 3 reflector blocks:
+                                             # every TT block of that merge is one chunk (the
+                                             # QR update's short prefetch distance)
+                                             (928, 128, O.CRIT_MAX, 1.0),
+                                             (700, 96, O.CRIT_MAX, 1.0),
+                                             (1824, 256, O.CRIT_MAX, 0.0)])
 def test_ragged_and_degenerate_sizes(H, N, nb, crit, alpha):
     A = I.uniform_matrix(5, N)
     b = I.uniform_rhs(5, N)
