@@ -1,0 +1,54 @@
+"""Seeded sweep over sizes and options (-m gpu): tile sizes between and at the kernel
+instantiations, ragged last tiles of every length class (1 row, <= 32 rows, partial chunks),
+forced LU / QR patterns, QR-tree domains, the LU variant A2 and diagonal-domain pivoting -- each
+against the oracle run with the same options (decisions identical, factors within 1e-10, HPL3).
+
+Forced decision vectors keep the comparison free of criterion near-ties; the inputs are diagonally
+shifted so that every LU path (including block elimination without pivoting across tiles) is
+stable at these sizes."""
+import numpy as np
+import pytest
+import torch
+
+import hlq_inputs as I
+from oracle import hlq_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _cases():
+    rng = np.random.default_rng(2024)
+    cases = []
+    for t in range(64):
+        nb = int(rng.choice([32, 48, 64, 80, 96, 128, 144, 160, 192, 224, 240, 256, 288, 320]))
+        n = int(rng.integers(1, 7))
+        tail = int(rng.choice([0, 1, 7, 31, 32, 33, nb // 2, nb - 1]))
+        N = max(1, (n - 1) * nb + (tail if tail > 0 else nb))
+        f = float(rng.choice([0.0, 0.5, 1.0]))
+        D = int(rng.choice([1, 2, 3]))
+        variant = str(rng.choice(["A1", "A1", "A2"]))
+        scope = "domain" if (variant == "A1" and rng.random() < 0.3) else "tile"
+        cases.append((t, N, nb, f, D, variant, scope))
+    return cases
+
+
+@pytest.mark.parametrize("t,N,nb,f,D,variant,scope", _cases())
+def test_fuzz_against_oracle(t, N, nb, f, D, variant, scope):
+    import paper_1401_5522_b200 as H
+    A = I.uniform_matrix(100 + t, N) + 2.0 * np.eye(N)
+    b = I.uniform_rhs(100 + t, N)
+    n = (N + nb - 1) // nb
+    forced = I.bernoulli_pattern(30 + t, n, f)
+    fo = O.hybrid_factor(A, nb, O.CRIT_MAX, 1.0, D=D, forced=forced, lu_variant=variant,
+                         pivot_scope=scope)
+    dA = H.to_colmajor(A)
+    fg = H.hlq_factor_ex(dA, N, nb, O.CRIT_MAX, 1.0, forced=forced, tree_domains=D,
+                         lu_variant=H.LU_A2 if variant == "A2" else H.LU_A1,
+                         pivot_scope=H.PIVOT_DOMAIN if scope == "domain" else H.PIVOT_TILE)
+    np.testing.assert_array_equal(fg.decisions(), fo.dec)
+    F = H.from_colmajor(dA)
+    assert O.factor_diff(F, fo.A) <= 1e-10, O.factor_diff(F, fo.A)
+    x = fg.solve(torch.from_numpy(np.ascontiguousarray(b)).cuda()).cpu().numpy()
+    assert O.hpl3(A, x, b) <= 16.0
+    assert np.allclose(x, O.solve(fo, b), rtol=0, atol=1e-8 * max(1.0, np.abs(x).max()))
+    fg.free()
