@@ -52,3 +52,34 @@ def test_fuzz_against_oracle(t, N, nb, f, D, variant, scope):
     assert O.hpl3(A, x, b) <= 16.0
     assert np.allclose(x, O.solve(fo, b), rtol=0, atol=1e-8 * max(1.0, np.abs(x).max()))
     fg.free()
+
+
+def _dist_cases():
+    rng = np.random.default_rng(77)
+    cases = []
+    for t in range(24):
+        P, Q = [(1, 2), (2, 1), (2, 2), (2, 3), (1, 3), (3, 1)][int(rng.integers(0, 6))]
+        nb = int(rng.choice([32, 64, 96, 128, 160, 256]))
+        n = int(rng.integers(1, 8))
+        tail = int(rng.choice([0, 1, 31, 32, 33, nb // 2]))
+        N = max(1, (n - 1) * nb + (tail if tail > 0 else nb))
+        f = float(rng.choice([0.0, 0.5, 1.0]))
+        D = P * int(rng.choice([1, 2]))
+        cases.append((t, N, nb, P, Q, D, f))
+    return cases
+
+
+@pytest.mark.parametrize("t,N,nb,P,Q,D,f", _dist_cases())
+def test_fuzz_block_cyclic_against_oracle(t, N, nb, P, Q, D, f):
+    """The 2D block-cyclic path on emulated grids (all ranks in this process, collectives as
+    device copies), forced patterns, D = P or 2P domains, ragged tails, empty ranks."""
+    from test_gpu_dist import run_dist
+    import paper_1401_5522_b200 as H
+    A = I.uniform_matrix(200 + t, N) + 2.0 * np.eye(N)
+    b = I.uniform_rhs(200 + t, N)
+    n = (N + nb - 1) // nb
+    forced = I.bernoulli_pattern(60 + t, n, f)
+    fo, fg, F, x = run_dist(H, A, b, nb, P, Q, D=D, forced=forced)
+    np.testing.assert_array_equal(fg.decisions(), fo.dec)
+    assert O.factor_diff(F, fo.A) <= 1e-10, O.factor_diff(F, fo.A)
+    assert O.hpl3(A, x, b) <= 16.0
