@@ -449,22 +449,19 @@ __device__ void panel_factor(double* Vs, int ldc, double* Rs, double* Ts, int R,
       if (lane == 0) Ts[l * 33 + l] = tau;
     }
     const bool upd = lane > l && lane < sb && tau != 0.0;
-    if (wact) {
-      if (lane == l) {
+    if (wact && (lane == l || upd)) {
+      // lane l stores v = x / (alpha - beta) = fma(x, rsc, 0); lanes c > l apply
+      // a -= tau (x / (alpha - beta)) w_c = fma(x, -c, a), c = tau w_c / (alpha - beta): one code path
+      // for both (no divergent passes), a select feeding the addend
+      const bool own = lane == l;
+      const double co = own ? rsc : -(tau * wz * rsc);
+      if (ilo == 0 && ihi == NR) {
+#pragma unroll
+        for (int i = 0; i < NR; ++i) a[i] = fma(xs[i], co, own ? 0.0 : a[i]);
+      } else {
 #pragma unroll
         for (int i = 0; i < NR; ++i)
-          if (i >= ilo && i < ihi) a[i] = xs[i] * rsc;
-      } else if (upd) {
-        // a -= tau (x / (alpha - beta)) w_c, as one FMA per element with c = tau w_c / (alpha - beta)
-        const double cf = tau * wz * rsc;
-        if (ilo == 0 && ihi == NR) {
-#pragma unroll
-          for (int i = 0; i < NR; ++i) a[i] -= xs[i] * cf;
-        } else {
-#pragma unroll
-          for (int i = 0; i < NR; ++i)
-            if (i >= ilo && i < ihi) a[i] -= xs[i] * cf;
-        }
+          if (i >= ilo && i < ihi) a[i] = fma(xs[i], co, own ? 0.0 : a[i]);
       }
     }
     if (!TT && l >= rw && l < rw + NR) {  // row l: the R row of reflector l
