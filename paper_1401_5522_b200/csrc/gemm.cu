@@ -49,27 +49,27 @@ __device__ __forceinline__ void load_stage(double* As, double* Bs, const double*
                                            int64_t M, int64_t N, int K, int64_t m0, int64_t n0,
                                            int k0, int tid) {
   if (V16) {
-    // A: BK x BM doubles = 1024 16-byte chunks, 4 per thread
+    // A: BK x BM doubles = BK * 64 16-byte chunks, BK / 4 per thread
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < BK / 4; ++i) {
       int q = tid + 256 * i;
       int kk = q >> 6, mm = (q & 63) * 2;
       bool ok = (k0 + kk < K) && (m0 + mm < M);
       const double* src = ok ? A + (int64_t)(k0 + kk) * lda + m0 + mm : A;
       cp_async16(As + kk * LDA_S + mm, src, ok);
     }
-    // B: BN x BK doubles = 512 chunks, 2 per thread
+    // B: BN x BK doubles = BK * 32 chunks, BK / 8 per thread
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < BK / 8; ++i) {
       int q = tid + 256 * i;
-      int nn = q >> 3, kk = (q & 7) * 2;
+      int nn = q / (BK / 2), kk = (q % (BK / 2)) * 2;
       bool ok = (n0 + nn < N) && (k0 + kk < K);
       const double* src = ok ? B + (n0 + nn) * ldb + k0 + kk : B;
       cp_async16(Bs + nn * LDB_S + kk, src, ok);
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < BK / 2; ++i) {
       int q = tid + 256 * i;
       int kk = q >> 7, mm = q & 127;
       bool ok = (k0 + kk < K) && (m0 + mm < M);
@@ -77,9 +77,9 @@ __device__ __forceinline__ void load_stage(double* As, double* Bs, const double*
       cp_async8(As + kk * LDA_S + mm, src, ok);
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < BK / 4; ++i) {
       int q = tid + 256 * i;
-      int nn = q >> 4, kk = q & 15;
+      int nn = q / BK, kk = q % BK;
       bool ok = (n0 + nn < N) && (k0 + kk < K);
       const double* src = ok ? B + (n0 + nn) * ldb + k0 + kk : B;
       cp_async8(Bs + nn * LDB_S + kk, src, ok);
