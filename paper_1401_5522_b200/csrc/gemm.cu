@@ -12,14 +12,22 @@
 //   * grouped rasterisation (8 tile-rows per group) for L2 reuse of the A panel / B row.
 // The Schur update of the LU step (Alg. 2) is C = C - L_panel * U_row on the
 // strided trailing submatrix; TRSM / SWPTRSM are C = X * U^-1 and C = L^-1 * (P X).
+#include <stdlib.h>
+
 #include "hlq_internal.cuh"
 
 namespace hlq {
 
-constexpr int BM = 128, BN = 64, BK = 16, STAGES = 3;
+// WN = warps along N: 2 -> CTA tile 128 x 64, 256 threads, 2 CTAs/SM (default);
+//                     4 -> CTA tile 128 x 128, 512 threads, 1 CTA/SM (HLQ_DGEMM_WN=4)
+constexpr int BM = 128, BK = 16, STAGES = 3;
 constexpr int LDA_S = BM + 4, LDB_S = BK + 4;
-constexpr int A_STAGE = BK * LDA_S, B_STAGE = BN * LDB_S;
-constexpr int GEMM_SMEM = (A_STAGE + B_STAGE) * STAGES * (int)sizeof(double);
+constexpr int A_STAGE = BK * LDA_S;
+template <int WN> __host__ __device__ constexpr int gemm_bn() { return 32 * WN; }
+template <int WN> __host__ __device__ constexpr int gemm_b_stage() { return gemm_bn<WN>() * LDB_S; }
+template <int WN> __host__ __device__ constexpr int gemm_smem() {
+  return (A_STAGE + gemm_b_stage<WN>()) * STAGES * (int)sizeof(double);
+}
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -43,25 +51,26 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
                : "d"(a), "d"(b));
 }
 
-template <bool V16>
+template <bool V16, int WN>
 __device__ __forceinline__ void load_stage(double* As, double* Bs, const double* __restrict__ A,
                                            int64_t lda, const double* __restrict__ B, int64_t ldb,
                                            int64_t M, int64_t N, int K, int64_t m0, int64_t n0,
                                            int k0, int tid) {
+  constexpr int NT = 128 * WN;
   if (V16) {
-    // A: BK x BM doubles = BK * 64 16-byte chunks, BK / 4 per thread
+    // A: BK x BM doubles = BK * 64 16-byte chunks
 #pragma unroll
-    for (int i = 0; i < BK / 4; ++i) {
-      int q = tid + 256 * i;
+    for (int i = 0; i < BK * 64 / NT; ++i) {
+      int q = tid + NT * i;
       int kk = q >> 6, mm = (q & 63) * 2;
       bool ok = (k0 + kk < K) && (m0 + mm < M);
       const double* src = ok ? A + (int64_t)(k0 + kk) * lda + m0 + mm : A;
       cp_async16(As + kk * LDA_S + mm, src, ok);
     }
-    // B: BN x BK doubles = BK * 32 chunks, BK / 8 per thread
+    // B: BN x BK doubles = BN * BK / 2 chunks
 #pragma unroll
-    for (int i = 0; i < BK / 8; ++i) {
-      int q = tid + 256 * i;
+    for (int i = 0; i < gemm_bn<WN>() * BK / 2 / NT; ++i) {
+      int q = tid + NT * i;
       int nn = q / (BK / 2), kk = (q % (BK / 2)) * 2;
       bool ok = (n0 + nn < N) && (k0 + kk < K);
       const double* src = ok ? B + (n0 + nn) * ldb + k0 + kk : B;
@@ -69,16 +78,16 @@ __device__ __forceinline__ void load_stage(double* As, double* Bs, const double*
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < BK / 2; ++i) {
-      int q = tid + 256 * i;
+    for (int i = 0; i < BK * BM / NT; ++i) {
+      int q = tid + NT * i;
       int kk = q >> 7, mm = q & 127;
       bool ok = (k0 + kk < K) && (m0 + mm < M);
       const double* src = ok ? A + (int64_t)(k0 + kk) * lda + m0 + mm : A;
       cp_async8(As + kk * LDA_S + mm, src, ok);
     }
 #pragma unroll
-    for (int i = 0; i < BK / 4; ++i) {
-      int q = tid + 256 * i;
+    for (int i = 0; i < gemm_bn<WN>() * BK / NT; ++i) {
+      int q = tid + NT * i;
       int nn = q / BK, kk = q % BK;
       bool ok = (n0 + nn < N) && (k0 + kk < K);
       const double* src = ok ? B + (n0 + nn) * ldb + k0 + kk : B;
@@ -87,8 +96,8 @@ __device__ __forceinline__ void load_stage(double* As, double* Bs, const double*
   }
 }
 
-template <bool V16>
-__global__ void __launch_bounds__(256, 2)
+template <bool V16, int WN>
+__global__ void __launch_bounds__(128 * WN, WN == 2 ? 2 : 1)
     k_dgemm(double* __restrict__ C, int64_t ldc, const double* __restrict__ A, int64_t lda,
             const double* __restrict__ B, int64_t ldb, int64_t M, int64_t N, int K, int neg,
             int beta, const uint8_t* __restrict__ dec, int k, int want,
@@ -96,6 +105,7 @@ __global__ void __launch_bounds__(256, 2)
   if (dec != nullptr && dec[k] != want) return;  // predicated launch: the other branch was taken
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
+  constexpr int BN = gemm_bn<WN>(), B_STAGE = gemm_b_stage<WN>();
   double* Bs = smem + STAGES * A_STAGE;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -133,7 +143,7 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < KT)
-      load_stage<V16>(As + s * A_STAGE, Bs + s * B_STAGE, A, lda, B, ldb, M, N, K, m0, n0, s * BK,
+      load_stage<V16, WN>(As + s * A_STAGE, Bs + s * B_STAGE, A, lda, B, ldb, M, N, K, m0, n0, s * BK,
                       tid);
     cp_commit();
   }
@@ -144,7 +154,7 @@ __global__ void __launch_bounds__(256, 2)
       int nk = kt + STAGES - 1;
       if (nk < KT) {
         int sl = nk % STAGES;
-        load_stage<V16>(As + sl * A_STAGE, Bs + sl * B_STAGE, A, lda, B, ldb, M, N, K, m0, n0,
+        load_stage<V16, WN>(As + sl * A_STAGE, Bs + sl * B_STAGE, A, lda, B, ldb, M, N, K, m0, n0,
                         nk * BK, tid);
       }
       cp_commit();
@@ -182,11 +192,12 @@ __global__ void __launch_bounds__(256, 2)
         v += __shfl_xor_sync(0xffffffffu, v, 4);
         v += __shfl_xor_sync(0xffffffffu, v, 8);
         v += __shfl_xor_sync(0xffffffffu, v, 16);
-        if (g == 0) red[wm * 64 + wn * 32 + ni * 8 + 2 * t + h] = v;
+        if (g == 0) red[wm * BN + wn * 32 + ni * 8 + 2 * t + h] = v;
       }
     __syncthreads();
-    if (tid < 64 && n0 + tid < N)
-      colpart[tm * ldp + n0 + tid] = ((red[tid] + red[64 + tid]) + red[128 + tid]) + red[192 + tid];
+    if (tid < BN && n0 + tid < N)
+      colpart[tm * ldp + n0 + tid] =
+          ((red[tid] + red[BN + tid]) + red[2 * BN + tid]) + red[3 * BN + tid];
   }
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
@@ -203,6 +214,30 @@ __global__ void __launch_bounds__(256, 2)
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
+template <int WN>
+static void launch_dgemm_wn(double* C, int64_t ldc, const double* A, int64_t lda, const double* B,
+                            int64_t ldb, int64_t M, int64_t N, int K, bool neg, bool beta,
+                            const uint8_t* dec, int k, int want, cudaStream_t st, double* colpart,
+                            int64_t ldp) {
+  static bool attr = false;
+  if (!attr) {
+    smem_optin(k_dgemm<true, WN>);
+    smem_optin(k_dgemm<false, WN>);
+    attr = true;
+  }
+  constexpr int BN = gemm_bn<WN>();
+  const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const bool v16 = aligned16(A) && aligned16(B) && (lda % 2 == 0) && (ldb % 2 == 0) &&
+                   (M % 2 == 0) && (K % 2 == 0);
+  ::hlq::g_launches++;
+  if (v16)
+    k_dgemm<true, WN><<<(unsigned)tiles, 128 * WN, gemm_smem<WN>(), st>>>(
+        C, ldc, A, lda, B, ldb, M, N, K, neg ? 1 : 0, beta ? 1 : 0, dec, k, want, colpart, ldp);
+  else
+    k_dgemm<false, WN><<<(unsigned)tiles, 128 * WN, gemm_smem<WN>(), st>>>(
+        C, ldc, A, lda, B, ldb, M, N, K, neg ? 1 : 0, beta ? 1 : 0, dec, k, want, colpart, ldp);
+}
+
 // C[M x N] = beta*C + (neg ? -1 : 1) * A[M x K] * B[K x N]; dec/k/want: optional predicate.
 void launch_dgemm(double* C, int64_t ldc, const double* A, int64_t lda, const double* B,
                   int64_t ldb, int64_t M, int64_t N, int K, bool neg, bool beta,
@@ -210,21 +245,12 @@ void launch_dgemm(double* C, int64_t ldc, const double* A, int64_t lda, const do
                   int64_t ldp) {
   if (ldp == 0) ldp = N;
   if (M <= 0 || N <= 0 || K <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    smem_optin(k_dgemm<true>);
-    smem_optin(k_dgemm<false>);
-    attr = true;
-  }
-  int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  bool v16 = aligned16(A) && aligned16(B) && (lda % 2 == 0) && (ldb % 2 == 0) && (M % 2 == 0) &&
-             (K % 2 == 0);
-  if (v16)
-    { ::hlq::g_launches++; k_dgemm<true><<<(unsigned)tiles, 256, GEMM_SMEM, st>>>(C, ldc, A, lda, B, ldb, M, N, K,
-                                                           neg ? 1 : 0, beta ? 1 : 0, dec, k, want, colpart, ldp); }
+  static int wn = -1;
+  if (wn < 0) wn = getenv("HLQ_DGEMM_WN") ? atoi(getenv("HLQ_DGEMM_WN")) : 2;
+  if (wn == 4)
+    launch_dgemm_wn<4>(C, ldc, A, lda, B, ldb, M, N, K, neg, beta, dec, k, want, st, colpart, ldp);
   else
-    { ::hlq::g_launches++; k_dgemm<false><<<(unsigned)tiles, 256, GEMM_SMEM, st>>>(C, ldc, A, lda, B, ldb, M, N, K,
-                                                            neg ? 1 : 0, beta ? 1 : 0, dec, k, want, colpart, ldp); }
+    launch_dgemm_wn<2>(C, ldc, A, lda, B, ldb, M, N, K, neg, beta, dec, k, want, st, colpart, ldp);
 }
 
 // a12 from the fused epilogue: tile row i = CTA row blocks [i*bpt, (i+1)*bpt); tile-norm max over
