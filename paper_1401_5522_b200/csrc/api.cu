@@ -243,7 +243,8 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
     off += align_up(bytes ? bytes : 1, 256);
     return o;
   };
-  const bool fuse_growth_any = f->track_growth && nb % 128 == 0;
+  const int cpr = gemm_colpart_rows();  // row granularity of the DGEMM's fused column partials
+  const bool fuse_growth_any = f->track_growth && nb % cpr == 0;
   const size_t scr = (size_t)2 * nb * nb + align_up(nb, 64);
   size_t oW0 = take(sizeof(double) * nb * nb), oW1 = take(sizeof(double) * nb * nb),
          oIpw0 = take(sizeof(int) * nb), oIpw1 = take(sizeof(int) * nb),
@@ -256,7 +257,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
          oPr = take(sizeof(int2) * (npairs + 1)), oSc0 = take(sizeof(double) * scr),
          oSc1 = take(sizeof(double) * scr), oWp = take(sizeof(double) * (size_t)N * nb),
          oWr = take(sizeof(double) * (size_t)N * nb),
-         oCp = take(fuse_growth_any ? sizeof(double) * (size_t)((N + 127) / 128) * N : 8),
+         oCp = take(fuse_growth_any ? sizeof(double) * (size_t)((N + cpr - 1) / cpr) * N : 8),
          oLi = take(sizeof(double) * (size_t)n * 2 * nb * nb),
          oLp = take(sizeof(int) * (size_t)n * nb), oSt2 = take(sizeof(double) * (size_t)nb);
   const bool dpiv = opt.pivot_scope == HLQ_PIVOT_DOMAIN;
@@ -473,7 +474,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
     // ---- update stage U(k) on st: column block k+1 first (then P(k+1) may start), then the rest
     cudaStreamWaitEvent(st, ev_panel, 0);
     const int64_t k1 = g.r0(k) + g.bs(k);
-    const bool fuse = f->track_growth && k + 1 < n && nb % 128 == 0;
+    const bool fuse = f->track_growth && k + 1 < n && nb % cpr == 0;
     for (int part = 0; part < 2; ++part) {
       const int64_t c0 = (part == 0) ? k1 : std::min(g.N, k1 + nb);
       const int64_t c1 = (part == 0) ? std::min(g.N, k1 + nb) : g.N;

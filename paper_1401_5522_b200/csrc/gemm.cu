@@ -3,9 +3,9 @@
 // B200 has no FP64 kind for tcgen05.mma, so the FP64 tensor path is the warp-level DMMA
 // (mma.sync.aligned.m8n8k4.row.col.f64 -> SASS DMMA.884), measured at 37.2 TFLOP/s on this pool
 // (profiles/r01/peak_dmma.jsonl).  Design:
-//   * CTA tile 128 x 64, 8 warps as 4 (M) x 2 (N), warp tile 32 x 32 = 4 x 4 DMMA fragments,
-//     64 FP64 accumulators per thread; 2 CTAs per SM so one CTA's C load/store overlaps the
-//     other's main loop (K = nb = 256 is short: C traffic is ~17% of the DMMA time per tile).
+//   * CTA tile 64 x 64, 4 warps as 2 (M) x 2 (N), warp tile 32 x 32 = 4 x 4 DMMA fragments,
+//     64 FP64 accumulators per thread; 4 CTAs per SM so one CTA's C load/store and barriers
+//     overlap the others' main loops (K = nb = 256 is short).  Other warp grids by template.
 //   * K staged through shared memory in BK=16 slices by a 3-stage cp.async pipeline;
 //     A slice stored [k][m] (ld 132), B slice [n][k] (ld 20): both paddings make every DMMA
 //     fragment load (lane -> (row g, k t)) bank-conflict free.
@@ -13,6 +13,7 @@
 // The Schur update of the LU step (Alg. 2) is C = C - L_panel * U_row on the
 // strided trailing submatrix; TRSM / SWPTRSM are C = X * U^-1 and C = L^-1 * (P X).
 #include <stdlib.h>
+#include <string.h>
 
 #include "hlq_internal.cuh"
 
@@ -20,14 +21,19 @@ namespace hlq {
 
 // WN = warps along N: 2 -> CTA tile 128 x 64, 256 threads, 2 CTAs/SM (default);
 //                     4 -> CTA tile 128 x 128, 512 threads, 1 CTA/SM (HLQ_DGEMM_WN=4)
-constexpr int BM = 128, BK = 16, STAGES = 3;
-constexpr int LDA_S = BM + 4, LDB_S = BK + 4;
-constexpr int A_STAGE = BK * LDA_S;
+constexpr int BK = 16, STAGES = 3;
+constexpr int LDB_S = BK + 4;
+// warp grid WM x WN of 32 x 32 warp tiles: CTA tile (32 WM) x (32 WN)
+template <int WM> __host__ __device__ constexpr int gemm_bm() { return 32 * WM; }
+template <int WM> __host__ __device__ constexpr int gemm_lda_s() { return 32 * WM + 4; }
+template <int WM> __host__ __device__ constexpr int gemm_a_stage() { return BK * gemm_lda_s<WM>(); }
 template <int WN> __host__ __device__ constexpr int gemm_bn() { return 32 * WN; }
 template <int WN> __host__ __device__ constexpr int gemm_b_stage() { return gemm_bn<WN>() * LDB_S; }
-template <int WN> __host__ __device__ constexpr int gemm_smem() {
-  return (A_STAGE + gemm_b_stage<WN>()) * STAGES * (int)sizeof(double);
+template <int WM, int WN> __host__ __device__ constexpr int gemm_smem() {
+  return (gemm_a_stage<WM>() + gemm_b_stage<WN>()) * STAGES * (int)sizeof(double);
 }
+// the row granularity of the fused a12 column partials (colpart): the CTA tile height
+static int g_gemm_bm = 128;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -51,18 +57,18 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
                : "d"(a), "d"(b));
 }
 
-template <bool V16, int WN>
+template <bool V16, int WM, int WN>
 __device__ __forceinline__ void load_stage(double* As, double* Bs, const double* __restrict__ A,
                                            int64_t lda, const double* __restrict__ B, int64_t ldb,
                                            int64_t M, int64_t N, int K, int64_t m0, int64_t n0,
                                            int k0, int tid) {
-  constexpr int NT = 128 * WN;
+  constexpr int NT = 32 * WM * WN, BM = gemm_bm<WM>(), LDA_S = gemm_lda_s<WM>();
   if (V16) {
-    // A: BK x BM doubles = BK * 64 16-byte chunks
+    // A: BK x BM doubles = BK * BM / 2 16-byte chunks
 #pragma unroll
-    for (int i = 0; i < BK * 64 / NT; ++i) {
+    for (int i = 0; i < BK * BM / 2 / NT; ++i) {
       int q = tid + NT * i;
-      int kk = q >> 6, mm = (q & 63) * 2;
+      int kk = q / (BM / 2), mm = (q % (BM / 2)) * 2;
       bool ok = (k0 + kk < K) && (m0 + mm < M);
       const double* src = ok ? A + (int64_t)(k0 + kk) * lda + m0 + mm : A;
       cp_async16(As + kk * LDA_S + mm, src, ok);
@@ -80,7 +86,7 @@ __device__ __forceinline__ void load_stage(double* As, double* Bs, const double*
 #pragma unroll
     for (int i = 0; i < BK * BM / NT; ++i) {
       int q = tid + NT * i;
-      int kk = q >> 7, mm = q & 127;
+      int kk = q / BM, mm = q % BM;
       bool ok = (k0 + kk < K) && (m0 + mm < M);
       const double* src = ok ? A + (int64_t)(k0 + kk) * lda + m0 + mm : A;
       cp_async8(As + kk * LDA_S + mm, src, ok);
@@ -96,8 +102,8 @@ __device__ __forceinline__ void load_stage(double* As, double* Bs, const double*
   }
 }
 
-template <bool V16, int WN>
-__global__ void __launch_bounds__(128 * WN, WN == 2 ? 2 : 1)
+template <bool V16, int WM, int WN>
+__global__ void __launch_bounds__(32 * WM * WN, 16 / (WM * WN) > 0 ? 16 / (WM * WN) : 1)
     k_dgemm(double* __restrict__ C, int64_t ldc, const double* __restrict__ A, int64_t lda,
             const double* __restrict__ B, int64_t ldb, int64_t M, int64_t N, int K, int neg,
             int beta, const uint8_t* __restrict__ dec, int k, int want,
@@ -105,11 +111,12 @@ __global__ void __launch_bounds__(128 * WN, WN == 2 ? 2 : 1)
   if (dec != nullptr && dec[k] != want) return;  // predicated launch: the other branch was taken
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
-  constexpr int BN = gemm_bn<WN>(), B_STAGE = gemm_b_stage<WN>();
+  constexpr int BM = gemm_bm<WM>(), BN = gemm_bn<WN>(), B_STAGE = gemm_b_stage<WN>();
+  constexpr int LDA_S = gemm_lda_s<WM>(), A_STAGE = gemm_a_stage<WM>();
   double* Bs = smem + STAGES * A_STAGE;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = warp & 3, wn = warp >> 2;
+  const int wm = warp % WM, wn = warp / WM;
 
   // grouped rasterisation
   const int64_t ntm = (M + BM - 1) / BM, ntn = (N + BN - 1) / BN;
@@ -143,7 +150,7 @@ __global__ void __launch_bounds__(128 * WN, WN == 2 ? 2 : 1)
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < KT)
-      load_stage<V16, WN>(As + s * A_STAGE, Bs + s * B_STAGE, A, lda, B, ldb, M, N, K, m0, n0, s * BK,
+      load_stage<V16, WM, WN>(As + s * A_STAGE, Bs + s * B_STAGE, A, lda, B, ldb, M, N, K, m0, n0, s * BK,
                       tid);
     cp_commit();
   }
@@ -154,7 +161,7 @@ __global__ void __launch_bounds__(128 * WN, WN == 2 ? 2 : 1)
       int nk = kt + STAGES - 1;
       if (nk < KT) {
         int sl = nk % STAGES;
-        load_stage<V16, WN>(As + sl * A_STAGE, Bs + sl * B_STAGE, A, lda, B, ldb, M, N, K, m0, n0,
+        load_stage<V16, WM, WN>(As + sl * A_STAGE, Bs + sl * B_STAGE, A, lda, B, ldb, M, N, K, m0, n0,
                         nk * BK, tid);
       }
       cp_commit();
@@ -181,7 +188,7 @@ __global__ void __launch_bounds__(128 * WN, WN == 2 ? 2 : 1)
   if (colpart != nullptr) {
     // fused a12 epilogue: per-column |C| sums over this CTA's 128 rows (rows >= M are exact zeros)
     __syncthreads();
-    double* red = smem;  // 4 (wm) x 64 columns
+    double* red = smem;  // WM (wm) x BN columns
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
@@ -195,9 +202,12 @@ __global__ void __launch_bounds__(128 * WN, WN == 2 ? 2 : 1)
         if (g == 0) red[wm * BN + wn * 32 + ni * 8 + 2 * t + h] = v;
       }
     __syncthreads();
-    if (tid < BN && n0 + tid < N)
-      colpart[tm * ldp + n0 + tid] =
-          ((red[tid] + red[BN + tid]) + red[2 * BN + tid]) + red[3 * BN + tid];
+    if (tid < BN && n0 + tid < N) {
+      double v = red[tid];
+#pragma unroll
+      for (int q = 1; q < WM; ++q) v += red[q * BN + tid];
+      colpart[tm * ldp + n0 + tid] = v;
+    }
   }
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
@@ -214,28 +224,50 @@ __global__ void __launch_bounds__(128 * WN, WN == 2 ? 2 : 1)
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
-template <int WN>
-static void launch_dgemm_wn(double* C, int64_t ldc, const double* A, int64_t lda, const double* B,
-                            int64_t ldb, int64_t M, int64_t N, int K, bool neg, bool beta,
-                            const uint8_t* dec, int k, int want, cudaStream_t st, double* colpart,
-                            int64_t ldp) {
+template <int WM, int WN>
+static void launch_dgemm_w(double* C, int64_t ldc, const double* A, int64_t lda, const double* B,
+                           int64_t ldb, int64_t M, int64_t N, int K, bool neg, bool beta,
+                           const uint8_t* dec, int k, int want, cudaStream_t st, double* colpart,
+                           int64_t ldp) {
   static bool attr = false;
   if (!attr) {
-    smem_optin(k_dgemm<true, WN>);
-    smem_optin(k_dgemm<false, WN>);
+    smem_optin(k_dgemm<true, WM, WN>);
+    smem_optin(k_dgemm<false, WM, WN>);
     attr = true;
   }
-  constexpr int BN = gemm_bn<WN>();
+  constexpr int BM = gemm_bm<WM>(), BN = gemm_bn<WN>();
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const bool v16 = aligned16(A) && aligned16(B) && (lda % 2 == 0) && (ldb % 2 == 0) &&
                    (M % 2 == 0) && (K % 2 == 0);
   ::hlq::g_launches++;
   if (v16)
-    k_dgemm<true, WN><<<(unsigned)tiles, 128 * WN, gemm_smem<WN>(), st>>>(
+    k_dgemm<true, WM, WN><<<(unsigned)tiles, 32 * WM * WN, gemm_smem<WM, WN>(), st>>>(
         C, ldc, A, lda, B, ldb, M, N, K, neg ? 1 : 0, beta ? 1 : 0, dec, k, want, colpart, ldp);
   else
-    k_dgemm<false, WN><<<(unsigned)tiles, 128 * WN, gemm_smem<WN>(), st>>>(
+    k_dgemm<false, WM, WN><<<(unsigned)tiles, 32 * WM * WN, gemm_smem<WM, WN>(), st>>>(
         C, ldc, A, lda, B, ldb, M, N, K, neg ? 1 : 0, beta ? 1 : 0, dec, k, want, colpart, ldp);
+}
+
+// CTA tile = (32 WM) x (32 WN): default WM x WN = 2 x 2 (64 x 64, 4 warps, 4 CTAs/SM: C3 LU update
+// 27.5 TF vs 27.3 for 4 x 2 = 128 x 64 with 2 CTAs/SM, 26.3 for 2 x 4, 25.0 for 4 x 1, 23.8 for
+// 4 x 4); HLQ_DGEMM_TILE=4x2|4x4|2x4|4x1 selects the alternatives
+static int dgemm_tile() {
+  static int t = -1;
+  if (t < 0) {
+    const char* e = getenv("HLQ_DGEMM_TILE");
+    t = 2;
+    if (e && !strcmp(e, "4x2")) t = 0;
+    if (e && !strcmp(e, "4x4")) t = 1;
+    if (e && !strcmp(e, "2x4")) t = 3;
+    if (e && !strcmp(e, "4x1")) t = 4;
+    g_gemm_bm = (t == 2 || t == 3) ? 64 : 128;
+  }
+  return t;
+}
+
+int gemm_colpart_rows() {
+  dgemm_tile();
+  return g_gemm_bm;
 }
 
 // C[M x N] = beta*C + (neg ? -1 : 1) * A[M x K] * B[K x N]; dec/k/want: optional predicate.
@@ -245,12 +277,27 @@ void launch_dgemm(double* C, int64_t ldc, const double* A, int64_t lda, const do
                   int64_t ldp) {
   if (ldp == 0) ldp = N;
   if (M <= 0 || N <= 0 || K <= 0) return;
-  static int wn = -1;
-  if (wn < 0) wn = getenv("HLQ_DGEMM_WN") ? atoi(getenv("HLQ_DGEMM_WN")) : 2;
-  if (wn == 4)
-    launch_dgemm_wn<4>(C, ldc, A, lda, B, ldb, M, N, K, neg, beta, dec, k, want, st, colpart, ldp);
-  else
-    launch_dgemm_wn<2>(C, ldc, A, lda, B, ldb, M, N, K, neg, beta, dec, k, want, st, colpart, ldp);
+  switch (dgemm_tile()) {
+    case 1:
+      launch_dgemm_w<4, 4>(C, ldc, A, lda, B, ldb, M, N, K, neg, beta, dec, k, want, st, colpart,
+                           ldp);
+      break;
+    case 2:
+      launch_dgemm_w<2, 2>(C, ldc, A, lda, B, ldb, M, N, K, neg, beta, dec, k, want, st, colpart,
+                           ldp);
+      break;
+    case 3:
+      launch_dgemm_w<2, 4>(C, ldc, A, lda, B, ldb, M, N, K, neg, beta, dec, k, want, st, colpart,
+                           ldp);
+      break;
+    case 4:
+      launch_dgemm_w<4, 1>(C, ldc, A, lda, B, ldb, M, N, K, neg, beta, dec, k, want, st, colpart,
+                           ldp);
+      break;
+    default:
+      launch_dgemm_w<4, 2>(C, ldc, A, lda, B, ldb, M, N, K, neg, beta, dec, k, want, st, colpart,
+                           ldp);
+  }
 }
 
 // a12 from the fused epilogue: tile row i = CTA row blocks [i*bpt, (i+1)*bpt); tile-norm max over
@@ -274,6 +321,7 @@ __global__ void k_colpart_max(const double* __restrict__ colpart, int64_t ntm, i
 void launch_colpart_max(const double* colpart, int64_t M, int64_t N, int nb, double* out,
                         const uint8_t* dec, int k, int want, cudaStream_t st) {
   if (M <= 0 || N <= 0) return;
+  const int BM = gemm_colpart_rows();
   const int64_t ntm = (M + BM - 1) / BM;
   const int bpt = nb / BM;
   const int64_t ntiles = (M + nb - 1) / nb;

@@ -102,6 +102,8 @@ void launch_copy_block_if(double* dst, int64_t ldd, const double* src, int64_t l
                           int64_t cols, const uint8_t* dec, int k, int want, cudaStream_t st);
 // dst[0:n) = src[0:n) (ints) when dec[k] == LU
 void launch_copy_ints(int* dst, const int* src, int n, const uint8_t* dec, int k, cudaStream_t st);
+// rows per block of the DGEMM's fused a12 column partials (its CTA tile height)
+int gemm_colpart_rows();
 void launch_dgemm(double* C, int64_t ldc, const double* A, int64_t lda, const double* B,
                   int64_t ldb, int64_t M, int64_t N, int K, bool neg, bool beta,
                   const uint8_t* dec, int k, int want, cudaStream_t st,
