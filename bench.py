@@ -298,7 +298,10 @@ def main():
     torch.cuda.synchronize()
     l0 = H.hlq_launch_count()
     times, profs, infos = [], [], []
+    last = None
     for _ in range(args.steps):
+        if last is not None:
+            last.free()  # its workspace goes back to the library's cache before the next step
         ms, f = one_step(True)
         times.append(ms)
         profs.append(f.profile())
@@ -487,7 +490,10 @@ def run_distributed(args, cfg, rank, world, local, dev):
     torch.cuda.synchronize()
     l0 = H.hlq_launch_count()
     times, profs = [], []
+    last = None
     for _ in range(args.steps):
+        if last is not None:
+            last.free()
         ms, f = one_step(True)
         times.append(ms)
         profs.append(f.profile())
