@@ -118,7 +118,9 @@ int hlq_default_options(hlq_options* opt);
  *          every diagonal tile U_kk (LU) or R_kk (QR); tiles right of the diagonal the final rows;
  *          below: L_ik (LU step) or the GEQRT reflectors V (strictly lower part of tile
  *          (i,k)) plus the TT reflectors (upper triangle of tile (i,k), i>k).  The handle BORROWS A:
- *          keep it alive and unmodified until hlq_free if hlq_solve is to be called.
+ *          keep it alive and unmodified until hlq_free if hlq_solve is to be called.  The handle
+ *          owns a device workspace taken from a one-entry cache that hlq_free refills: a
+ *          factorization started while another handle is alive allocates its own (cudaMalloc).
  *   N >= 1, 1 <= nb <= HLQ_MAX_NB;  N need not be a multiple of nb (ragged last tile);
  *          nb > N is clamped to N.
  *   criterion HLQ_CRIT_*;  alpha >= 0 (0 -> every step QR, +inf -> every step LU; NaN invalid).
