@@ -76,12 +76,6 @@ void cache_put(int slot, void* p, size_t bytes) {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-// a DevWork view whose kernels are not predicated on d_k (speculative work)
-hlq::DevWork wk_nodec(const hlq::DevWork& w) {
-  hlq::DevWork v = w;
-  v.dec = nullptr;
-  return v;
-}
 }  // namespace
 
 // the library's high-priority panel streams (lookahead), created once per process: sp runs the
@@ -387,12 +381,20 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
       Geo gq = g;
       gq.lda = N;
       P.begin(HLQ_PROF_QR_GEQRT, sq);
+      // predicated on d_k with "undecided" = run: once the criterion decides LU, the remaining
+      // speculative launches exit at their first instruction
       launch_qr_panel(w.qpan - k0 * N, gq, k, ib, f->lvl_ptr[k].data(), f->lvl_cnt[k].data(), nl,
-                      wk_nodec(wk), sq, /*diag_done=*/a2);
+                      wk, sq, /*diag_done=*/a2);
       P.end(sq);
       cudaEventRecord(ev_qdone, sq);
     };
-    if (spec && !a2) start_spec(ev_ready);
+    if (spec) {
+      cudaMemsetAsync(w.dec + k, 0xff, 1, sp);  // d_k undecided until k_decide
+      if (!a2) {
+        cudaEventRecord(ev_a2, sp);
+        start_spec(ev_a2);
+      }
+    }
     if (known != HLQ_DEC_QR) {
       if (criterion_needed) {
         P.begin(HLQ_PROF_CRITERION, sp);

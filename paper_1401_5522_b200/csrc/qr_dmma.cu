@@ -504,7 +504,7 @@ template <int W>
 __global__ void __launch_bounds__(QD_T) k_geqrt_tc(double* __restrict__ A, Geo g, int k, int ib,
                                                    double* __restrict__ Tg,
                                                    const uint8_t* __restrict__ dec, int i_first) {
-  if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
+  if (dec != nullptr && dec[k] == HLQ_DEC_LU) return;  // (undecided: speculative run)
   extern __shared__ __align__(16) double sm[];
   const int ldc = qd_ldc(g.nb);
   double* Cs = sm;
@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(QD_T) k_ttqrt_tc(double* __restrict__ A, Geo g
                                                    double* __restrict__ Ttt,
                                                    const int2* __restrict__ pairs,
                                                    const uint8_t* __restrict__ dec) {
-  if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
+  if (dec != nullptr && dec[k] == HLQ_DEC_LU) return;  // (undecided: speculative run)
   extern __shared__ __align__(16) double sm[];
   const int ldc = qd_ldc(g.nb);
   double* Cs = sm;
