@@ -122,18 +122,20 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------ CPU oracle
-def cpu_oracle_step(N, nb, seed, fqr, crit, alpha):
-    """One bounded oracle factor+solve (test infrastructure; the bench's cpu_baseline leg)."""
+def cpu_oracle_step(config, N, nb, fqr, crit, alpha, domains=1):
+    """One bounded oracle factor+solve of the config's own input recipe (hlq_inputs.config_system:
+    the same generator as the GPU arm) at size N (test infrastructure; the bench's cpu_baseline
+    leg and the reference arm)."""
     import hlq_inputs as I
     from oracle import hlq_oracle as O
-    A = I.uniform_matrix(seed, N)
-    b = I.uniform_rhs(seed, N)
+    A, b, _ = I.config_system(config, N)
     n = (N + nb - 1) // nb
     t0 = time.perf_counter()
     if crit:
-        f = O.hybrid_factor(A, nb, CRIT[crit], alpha, track_growth=True)
+        f = O.hybrid_factor(A, nb, CRIT[crit], alpha, D=domains, track_growth=True)
     else:
-        f = O.hybrid_factor(A, nb, forced=I.bernoulli_pattern(30, n, fqr), track_growth=True)
+        f = O.hybrid_factor(A, nb, forced=I.bernoulli_pattern(30, n, fqr), D=domains,
+                            track_growth=True)
     x = O.solve(f, b)
     dt = time.perf_counter() - t0
     return dt, f, O.hpl3(A, x, b)
@@ -154,20 +156,27 @@ def run_reference(args, cfg, rank):
     nb = cfg["nb"]
     fake = 2.0 / 3.0 * Ns ** 3
     for _ in range(args.warmup):
-        cpu_oracle_step(Ns, nb, cfg["seed"], args.fqr, args.criterion, args.alpha)
+        cpu_oracle_step(args.config, Ns, nb, args.fqr, args.criterion, args.alpha, args.domains)
     times = []
     for _ in range(args.steps):
-        dt, f, h3 = cpu_oracle_step(Ns, nb, cfg["seed"], args.fqr, args.criterion, args.alpha)
+        dt, f, h3 = cpu_oracle_step(args.config, Ns, nb, args.fqr, args.criterion, args.alpha,
+                                    args.domains)
         times.append(dt)
     t = sum(times) / len(times)
     val = fake / t / 1e12
-    sample = (f"oracle (numpy/scipy, plain CPU) factor+solve of the {args.config}-recipe system at "
-              f"N={Ns}, nb={nb} (bounded sample of the N={cfg['N']} workload), per step")
+    sample = (f"oracle (numpy/scipy, plain CPU) factor+solve of the {args.config} recipe (same "
+              f"generator) at N={Ns}, nb={nb}: a bounded sample of the N={cfg['N']} workload, per "
+              f"step; TFLOP/s on the sample's own 2N^3/3")
+    conf = workload_config(args, cfg)
+    conf["workload"] = f"[bounded sample, N={Ns}] " + conf["workload"]
+    conf["N"] = Ns
+    conf["n_tiles"] = (Ns + nb - 1) // nb
+    conf["sample_of_N"] = cfg["N"]
     out = {"impl": "reference", "metric": "FP64 TFLOP/s (2N^3/3 basis) hybrid LU-QR",
            "value": val, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": workload_config(args, cfg), "hpl3": h3,
+           "config": conf, "hpl3": h3,
            "cpu_baseline": {"kind": "oracle", "cores": cpu_threads(), "sample": sample,
                             "value": val, "unit": "TFLOP/s"},
            "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
@@ -397,11 +406,23 @@ def main():
     cpu_base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         Ns = args.cpu_sample_N
-        dt, fo, h3c = cpu_oracle_step(Ns, nb, cfg["seed"], args.fqr, args.criterion, args.alpha)
+        dt, fo, h3c = cpu_oracle_step(args.config, Ns, nb, args.fqr, args.criterion, args.alpha,
+                                      args.domains)
         cpu_base = {"value": 2.0 / 3.0 * Ns ** 3 / dt / 1e12, "unit": "TFLOP/s",
-                    "cores": cpu_threads(), "kind": "oracle",
-                    "sample": f"one oracle factor+solve of the same recipe at N={Ns}, nb={nb} "
-                              f"({dt:.1f} s), TFLOP/s on the 2N^3/3 basis"}
+                    "cores": cpu_threads(), "kind": "oracle", "N_sample": Ns,
+                    "sample": f"one oracle factor+solve of the {args.config} recipe (same "
+                              f"generator) at N={Ns}, nb={nb} ({dt:.1f} s), TFLOP/s on the "
+                              f"sample's 2N^3/3; the GPU line is at N={N}"}
+        full = os.path.join(ROOT, "profiles", "r02", "parity_full.json")
+        if os.path.exists(full):
+            try:  # the full-size oracle run of this workload, from the committed parity record
+                rec = json.load(open(full)).get("runs", {}).get(args.config + (
+                    f"_f{args.fqr}" if not args.criterion else f"_{args.criterion}{args.alpha:g}"))
+                if rec:
+                    cpu_base["full_size_oracle"] = {k: rec[k] for k in (
+                        "N", "oracle_s", "oracle_cores", "oracle_tflops") if k in rec}
+            except Exception:
+                pass
 
     if rank == 0:
         out = {"metric": "FP64 TFLOP/s (2N^3/3 basis) hybrid LU-QR", "value": value,

@@ -16,7 +16,9 @@
  *     BLOCKING by default (they return after completion so the hlq_get_* getters are valid).
  *   - Return value: 0 = OK; -i = argument i invalid (LAPACK style); HLQ_ERR_* (< -99) = CUDA /
  *     out-of-memory errors; positive HLQ_ST_* = informational, the factorization completed.
- *   - Thread-compatible: one handle per host thread.  No exceptions cross the ABI.
+ *   - Thread-safe for distinct handles: the workspace cache and the panel streams are kept per
+ *     device under a lock, so handles on different host threads (or devices) never share memory;
+ *     one handle must not be used from two threads at once.  No exceptions cross the ABI.
  */
 #ifndef HLQ_H
 #define HLQ_H
@@ -64,7 +66,8 @@ typedef struct hlq_factors_s* hlq_factors_t; /* opaque; owned by the library */
 typedef struct {
   int32_t struct_size;       /* = sizeof(hlq_options) (ABI versioning)                          */
   int64_t lda;               /* leading dimension of A (0 -> N)                                  */
-  int32_t ib;                /* inner block of the stored Householder T factors (0 -> 32)        */
+  int32_t ib;                /* inner block of the stored Householder T factors: 32 (0 -> 32;
+                                any other value is rejected with -6)                              */
   int32_t tree_domains;      /* D: QR-tree domains = tile rows mod D (0 -> 1 on one GPU)         */
   int32_t tree;              /* HLQ_TREE_GREEDY                                                  */
   int32_t mumps_reading;     /* 0 = M1 (default, reading 1), 1 = M2                    */

@@ -162,7 +162,7 @@ def domain_rows(N: int, nb: int, k: int, D: int) -> np.ndarray:
 
 
 def lu_step_domain(A: np.ndarray, N: int, nb: int, k: int, D: int, Wst: np.ndarray,
-                   ipiv: np.ndarray):
+                   ipiv: np.ndarray, variant: int = 0):
     """LU step with diagonal-domain pivoting ("a swap is performed with all
     tiles of the local panel, and then a triangular solve is applied to the first row.  On all other
     nodes ... the panel is updated with TRSM tasks, and the trailing sub-matrix ... with GEMM")."""
@@ -194,8 +194,8 @@ def lu_step_domain(A: np.ndarray, N: int, nb: int, k: int, D: int, Wst: np.ndarr
     with np.errstate(all="ignore"):
         A[k0:k1, k1:N] = solve_triangular(L, A[k0:k1, k1:N], lower=True, unit_diagonal=True,
                                           check_finite=False)
-        # Update: A_ij <- A_ij - A_ik A_kj for every i, j > k
-        A[k1:N, k1:N] -= A[k1:N, k0:k1] @ A[k0:k1, k1:N]
+    # Update: A_ij <- A_ij - A_ik A_kj for every i, j > k
+    schur_update(A, N, k0, k1, variant)
 
 
 # ----------------------------------------------------------------------------------------------
@@ -356,7 +356,24 @@ def criterion_mumps(alpha: float, W: np.ndarray, local_max: np.ndarray, away_max
 # ----------------------------------------------------------------------------------------------
 # a5/a6/a7: LU step, variant A1 (Alg. 2)
 # ----------------------------------------------------------------------------------------------
-def lu_step(A: np.ndarray, N: int, nb: int, k: int, W: np.ndarray, ipiv: np.ndarray):
+def schur_update(A: np.ndarray, N: int, k0: int, k1: int, variant: int = 0):
+    """Update: A_ij <- A_ij - A_ik A_kj for all i, j > k, as one rank-b product.
+    variant = 1 is the noise-floor variant (BASELINE "reversed inner-product order"): the same
+    product summed over 4 K-chunks in reverse order -- same mathematics, different rounding."""
+    with np.errstate(all="ignore"):
+        if variant == 0:
+            A[k1:N, k1:N] -= A[k1:N, k0:k1] @ A[k0:k1, k1:N]
+            return
+        edges = np.linspace(k0, k1, 5).astype(int)
+        acc = np.zeros((N - k1, N - k1))
+        for c in reversed(range(4)):
+            lo, hi = edges[c], edges[c + 1]
+            acc += A[k1:N, lo:hi] @ A[lo:hi, k1:N]
+        A[k1:N, k1:N] -= acc
+
+
+def lu_step(A: np.ndarray, N: int, nb: int, k: int, W: np.ndarray, ipiv: np.ndarray,
+            variant: int = 0):
     n = ntiles(N, nb)
     rk = tsl(N, nb, k)
     k0, k1 = rk.start, rk.stop
@@ -380,22 +397,7 @@ def lu_step(A: np.ndarray, N: int, nb: int, k: int, W: np.ndarray, ipiv: np.ndar
     with np.errstate(all="ignore"):
         A[k0:k1, k1:N] = solve_triangular(L, C, lower=True, unit_diagonal=True, check_finite=False)
     # Update: A_ij <- A_ij - A_ik A_kj for i, j > k
-    with np.errstate(all="ignore"):
-        A[k1:N, k1:N] -= A[k1:N, k0:k1] @ A[k0:k1, k1:N]
-
-
-def lu_step_update_variant(A, N, nb, k, chunks=4):
-    """Noise-floor variant of the Update (BASELINE "reversed inner-product order"): the rank-b
-    product is summed over K chunks in reverse order.  Same mathematics, different rounding."""
-    rk = tsl(N, nb, k)
-    k0, k1 = rk.start, rk.stop
-    b = k1 - k0
-    edges = np.linspace(0, b, chunks + 1).astype(int)
-    acc = np.zeros((N - k1, N - k1))
-    for c in reversed(range(chunks)):
-        lo, hi = k0 + edges[c], k0 + edges[c + 1]
-        acc += A[k1:N, lo:hi] @ A[lo:hi, k1:N]
-    A[k1:N, k1:N] -= acc
+    schur_update(A, N, k0, k1, variant)
 
 
 # ----------------------------------------------------------------------------------------------
@@ -552,7 +554,8 @@ def a2_inv_norm1(A: np.ndarray, N: int, nb: int, k: int, T: np.ndarray, ib: int)
     return float(np.max(np.sum(np.abs(X), axis=0)))
 
 
-def lu_step_a2(A: np.ndarray, N: int, nb: int, k: int, T: np.ndarray, ib: int):
+def lu_step_a2(A: np.ndarray, N: int, nb: int, k: int, T: np.ndarray, ib: int,
+               variant: int = 0):
     """Variant A2 Eliminate / Apply / Update on the in-place GEQRT factors of A_kk."""
     n = ntiles(N, nb)
     rk = tsl(N, nb, k)
@@ -567,8 +570,7 @@ def lu_step_a2(A: np.ndarray, N: int, nb: int, k: int, T: np.ndarray, ib: int):
     # Apply: A_kj <- Q_kk^T A_kj for j > k, with the reflectors V_kk of A_kk
     unmqr(A[rk, rk], T, ib, A[k0:k1, k1:N])
     # Update: A_ij <- A_ij - A_ik A_kj ("the exact same as in (A1)")
-    with np.errstate(all="ignore"):
-        A[k1:N, k1:N] -= A[k1:N, k0:k1] @ A[k0:k1, k1:N]
+    schur_update(A, N, k0, k1, variant)
 
 
 def _domains(k: int, n: int, D: int):
@@ -723,7 +725,9 @@ def hybrid_factor(A_in: np.ndarray, nb: int, crit: int = CRIT_MAX, alpha: float 
     Q_kk^T, a QR step continues from that factorization).
     pivot_scope: "tile" (north_star, ledger 8) or "domain" (NEXT f1: the pivot search runs
     over the diagonal domain, the D-domain of the QR tree; DESIGN reading 33).
-    forced: decision vector used verbatim (C3); variant=1 uses the reversed-chunk GEMM (noise floor).
+    forced: decision vector used verbatim (C3); variant=1 sums every LU Schur update (A1, A2 and
+    domain steps) in reversed K-chunk order (schur_update): the noise-floor run, delta_floor =
+    factor_diff(variant 1, variant 0) with the decisions forced equal.
     on_step(k, A_before, A_after, d): optional test hook called after each step with copies.
     """
     A = np.array(A_in, dtype=np.float64, order="F", copy=True)
@@ -801,18 +805,13 @@ def hybrid_factor(A_in: np.ndarray, nb: int, crit: int = CRIT_MAX, alpha: float 
         stats.append({"k": k, "s": s, "local_max": lmax, "away_max": amax, "inv_norm": inv,
                       "zero_pivot": zp})
         if d == LU and T_kk is not None:
-            lu_step_a2(A, N, nb, k, T_kk, ib)
+            lu_step_a2(A, N, nb, k, T_kk, ib, variant)
             qrs[k] = QRStepData(T_geqrt={k: T_kk})  # Q_kk for the solve's forward pass
         elif d == LU and Wst is not None:
-            lu_step_domain(A, N, nb, k, D, Wst, ipiv)
+            lu_step_domain(A, N, nb, k, D, Wst, ipiv, variant)
             ipivs[k] = ipiv  # stack coordinates (Factors.pivot_scope says so)
         elif d == LU:
-            lu_step(A, N, nb, k, W, ipiv)
-            if variant == 1 and k + 1 < n:
-                # undo the standard update and redo it with the reversed-chunk order
-                k0, k1 = rk.start, rk.stop
-                A[k1:N, k1:N] += A[k1:N, k0:k1] @ A[k0:k1, k1:N]
-                lu_step_update_variant(A, N, nb, k)
+            lu_step(A, N, nb, k, W, ipiv, variant)
             ipivs[k] = ipiv
         else:
             qrs[k] = qr_step(A, N, nb, k, D, ib, tree, T_kk=T_kk)

@@ -11,4 +11,4 @@ from ._binding import (  # noqa: F401
     hlq_launch_count, hlq_residual, hlq_solve, lib, lib_path, to_colmajor,
     Grid, cyclic_rows, dist_counts, dist_plan, gather_block_cyclic, grid_local, grid_nccl, hlq_factor_dist,
     local_shape, nccl_unique_id, scatter_block_cyclic, hlq_generate_uniform_cyclic,
-    hlq_residual_dist)
+    hlq_residual_dist, _step_vectors)

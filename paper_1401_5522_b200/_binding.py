@@ -218,6 +218,39 @@ class Factors:
         return x
 
 
+def _check_device_matrix(A, rows: int, cols: int, ld: int, what: str):
+    """A must be a contiguous float64 CUDA tensor holding at least ld*(cols-1)+rows elements."""
+    import torch
+    if not isinstance(A, torch.Tensor):
+        raise HlqError(f"{what}: expected a torch tensor, got {type(A).__name__}")
+    if A.dtype != torch.float64 or not A.is_cuda or not A.is_contiguous():
+        raise HlqError(f"{what}: needs a contiguous float64 CUDA tensor "
+                       f"(got {A.dtype}, device {A.device}, contiguous={A.is_contiguous()})")
+    need = ld * (cols - 1) + rows if rows > 0 and cols > 0 else 0
+    if A.numel() < need:
+        raise HlqError(f"{what}: {A.numel()} elements < ld*(N-1)+N = {need}")
+
+
+def _step_vectors(opt: HlqOptions, n: int, forced, ref_dec, ref_margin, keep: list):
+    """Marshal the per-step host vectors (n entries each) into opt."""
+    if forced is not None:
+        fa = np.ascontiguousarray(forced, dtype=np.uint8)
+        if fa.shape != (n,):
+            raise HlqError(f"forced has shape {fa.shape}, needs ({n},) = ceil(N/nb)")
+        keep.append(fa)
+        opt.forced = fa.ctypes.data
+    if (ref_dec is None) != (ref_margin is None):
+        raise HlqError("ref_dec and ref_margin must be given together")
+    if ref_dec is not None:
+        ra = np.ascontiguousarray(ref_dec, dtype=np.uint8)
+        rm = np.ascontiguousarray(ref_margin, dtype=np.float64)
+        if ra.shape != (n,) or rm.shape != (n,):
+            raise HlqError(f"ref_dec / ref_margin have shapes {ra.shape} / {rm.shape}, need ({n},)")
+        keep += [ra, rm]
+        opt.ref_dec = ra.ctypes.data
+        opt.ref_margin = rm.ctypes.data
+
+
 def hlq_factor_ex(A, N: int, nb: int, criterion: int = CRIT_MAX, alpha: float = 1.0,
                   opt: HlqOptions | None = None, *, forced=None, ref_dec=None, ref_margin=None,
                   stream=None, **fields) -> Factors:
@@ -226,17 +259,11 @@ def hlq_factor_ex(A, N: int, nb: int, criterion: int = CRIT_MAX, alpha: float = 
         opt = hlq_default_options()
     for k, v in fields.items():
         setattr(opt, k, v)
+    if N >= 1 and nb >= 1:
+        _check_device_matrix(A, N, N, opt.lda if opt.lda else N, "hlq_factor_ex: A")
     keep = []
-    if forced is not None:
-        fa = np.ascontiguousarray(forced, dtype=np.uint8)
-        keep.append(fa)
-        opt.forced = fa.ctypes.data
-    if ref_dec is not None:
-        ra = np.ascontiguousarray(ref_dec, dtype=np.uint8)
-        rm = np.ascontiguousarray(ref_margin, dtype=np.float64)
-        keep += [ra, rm]
-        opt.ref_dec = ra.ctypes.data
-        opt.ref_margin = rm.ctypes.data
+    n = -(-N // min(nb, N)) if N >= 1 and nb >= 1 else 0
+    _step_vectors(opt, n, forced, ref_dec, ref_margin, keep)
     opt.stream = _stream_ptr(stream).value
     h = C.c_void_p()
     rc = lib.hlq_factor_ex(_dptr(A), N, nb, criterion, float(alpha), C.byref(opt), C.byref(h))
@@ -256,6 +283,9 @@ def hlq_launch_count() -> int:
 
 
 def hlq_solve(f: Factors, b, x):
+    N = f.info()["N"]
+    _check_device_matrix(b, N, 1, N, "hlq_solve: b")
+    _check_device_matrix(x, N, 1, N, "hlq_solve: x")
     return _check(lib.hlq_solve(f.handle, _dptr(b), _dptr(x)), "hlq_solve")
 
 
@@ -409,16 +439,8 @@ def hlq_factor_dist(grid: Grid, A_locals, N: int, nb: int, criterion: int = CRIT
     for k, v in fields.items():
         setattr(opt, k, v)
     keep = []
-    if forced is not None:
-        fa = np.ascontiguousarray(forced, dtype=np.uint8)
-        keep.append(fa)
-        opt.forced = fa.ctypes.data
-    if ref_dec is not None:
-        ra = np.ascontiguousarray(ref_dec, dtype=np.uint8)
-        rm = np.ascontiguousarray(ref_margin, dtype=np.float64)
-        keep += [ra, rm]
-        opt.ref_dec = ra.ctypes.data
-        opt.ref_margin = rm.ctypes.data
+    n = -(-N // min(nb, N)) if N >= 1 and nb >= 1 else 0
+    _step_vectors(opt, n, forced, ref_dec, ref_margin, keep)
     opt.stream = _stream_ptr(stream).value
     ptrs = (C.c_void_p * len(A_locals))(*[t.data_ptr() if t.numel() else None for t in A_locals])
     llds = (C.c_int64 * len(A_locals))(*([0] * len(A_locals) if lld is None else lld))

@@ -10,6 +10,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 #include <new>
 #include <vector>
 
@@ -33,26 +34,41 @@ using namespace hlq;
 
 // ---------------------------------------------------------------------------------------------
 // device-memory cache: big workspaces are reused across calls (like a cuBLAS workspace), so a
-// repeated factorization of the same size does not pay cudaMalloc/cudaFree.
+// repeated factorization of the same size does not pay cudaMalloc/cudaFree.  One entry per
+// (device, slot); a taken block belongs to exactly one handle until it is put back.  Guarded by a
+// mutex, so handles on different host threads (and devices) never share a block.
 namespace {
 struct CacheSlot {
   void* p = nullptr;
   size_t bytes = 0;
 };
-CacheSlot g_cache[4];
+constexpr int kMaxDev = 64;
+std::mutex g_cache_mu;
+CacheSlot g_cache[kMaxDev][2];
+
+int cur_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < 0 ? 0 : (d >= kMaxDev ? kMaxDev - 1 : d);
+}
 
 void* cache_get(int slot, size_t bytes) {
-  CacheSlot& c = g_cache[slot];
-  if (c.p && c.bytes >= bytes) {
-    void* p = c.p;
-    c.p = nullptr;
-    return p;
-  }
-  if (c.p) {
-    cudaFree(c.p);
+  const int dev = cur_device();
+  void* stale = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    CacheSlot& c = g_cache[dev][slot];
+    if (c.p && c.bytes >= bytes) {
+      void* p = c.p;
+      c.p = nullptr;
+      c.bytes = 0;
+      return p;
+    }
+    stale = c.p;
     c.p = nullptr;
     c.bytes = 0;
   }
+  if (stale) cudaFree(stale);
   void* p = nullptr;
   if (cudaMalloc(&p, bytes) != cudaSuccess) {
     cudaGetLastError();
@@ -60,34 +76,48 @@ void* cache_get(int slot, size_t bytes) {
   }
   return p;
 }
-void cache_put(int slot, void* p, size_t bytes) {
-  CacheSlot& c = g_cache[slot];
+// p was taken on device dev
+void cache_put(int dev, int slot, void* p, size_t bytes) {
   if (!p) return;
-  if (c.p) {
-    if (c.bytes >= bytes) {
-      cudaFree(p);
-      return;
+  void* drop = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    CacheSlot& c = g_cache[dev][slot];
+    if (c.p && c.bytes >= bytes) {
+      drop = p;
+    } else {
+      drop = c.p;
+      c.p = p;
+      c.bytes = bytes;
     }
-    cudaFree(c.p);
   }
-  c.p = p;
-  c.bytes = bytes;
+  if (drop) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+    cudaFree(drop);
+    if (prev != dev) cudaSetDevice(prev);
+  }
 }
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 }  // namespace
 
-// the library's high-priority panel streams (lookahead), created once per process: sp runs the
-// criterion (speculative LU) and the chosen branch, sq the speculative QR panel beside it
+// the library's high-priority panel streams (lookahead), created once per device: sp runs the
+// criterion (speculative LU) and the chosen branch, sq the speculative QR panel beside it.
+// Concurrent factorizations on one device share them (their panel stages then serialise; every
+// cross-stream dependency is an event of the handle itself, so correctness does not depend on it).
 static cudaStream_t panel_stream(int which = 0) {
-  static cudaStream_t s[2] = {nullptr, nullptr};
-  if (!s[which]) {
+  static cudaStream_t s[kMaxDev][2] = {};
+  const int dev = cur_device();
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  if (!s[dev][which]) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    cudaStreamCreateWithPriority(&s[which], cudaStreamNonBlocking, hi);
+    cudaStreamCreateWithPriority(&s[dev][which], cudaStreamNonBlocking, hi);
   }
-  return s[which];
+  return s[dev][which];
 }
 
 
@@ -188,10 +218,10 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   if (opt.ib == 0) opt.ib = 32;
   if (opt.tree_domains == 0) opt.tree_domains = 1;
   if (opt.tie_rel_tol == 0.0) opt.tie_rel_tol = 1e-10;
-  if (opt.ib < 1 || opt.ib > 32 || opt.tree_domains < 1 || opt.tree != HLQ_TREE_GREEDY ||
+  if (opt.ib != 32 || opt.tree_domains < 1 || opt.tree != HLQ_TREE_GREEDY ||
       opt.mumps_reading < 0 || opt.mumps_reading > 1 || opt.invnorm_estimate < 0 ||
       opt.invnorm_estimate > 1 || opt.lu_variant < HLQ_LU_A1 || opt.lu_variant > HLQ_LU_A2 ||
-      (opt.lu_variant == HLQ_LU_A2 && (opt.ib != 32 || opt.invnorm_estimate != 0)) ||
+      (opt.lu_variant == HLQ_LU_A2 && opt.invnorm_estimate != 0) ||
       opt.pivot_scope < HLQ_PIVOT_TILE || opt.pivot_scope > HLQ_PIVOT_DOMAIN ||
       (opt.pivot_scope == HLQ_PIVOT_DOMAIN && opt.lu_variant != HLQ_LU_A1))
     return -6;
@@ -260,14 +290,14 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   // is copied back if the step is QR (A1, ib = 32; HLQ_SPEC_QR=0 disables it)
   static int spec_env = -1;
   if (spec_env < 0) spec_env = getenv("HLQ_SPEC_QR") ? atoi(getenv("HLQ_SPEC_QR")) : 1;
-  const bool spec_qr = spec_env != 0 && !opt.forced && alpha > 0.0 && !isinf(alpha) &&
-                       opt.ib == 32;
+  const bool spec_qr = spec_env != 0 && !opt.forced && alpha > 0.0 && !isinf(alpha);
   size_t oWd = take(dpiv ? sizeof(double) * (size_t)N * nb : 8),
          oDp = take(dpiv ? sizeof(int) * (size_t)n * nb : 8),
          oDk = take(sizeof(unsigned long long) * 2 * 148), oDi = take(sizeof(int) * 2 * 148),
          oDc = take(sizeof(unsigned int)),
          oQp = take(spec_qr ? sizeof(double) * (size_t)N * nb : 8);
   f->ws_bytes = off;
+  f->dev = cur_device();
   f->ws_block = cache_get(0, off);
   if (!f->ws_block) return HLQ_ERR_NOMEM;
   char* base = (char*)f->ws_block;
@@ -384,7 +414,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
       // predicated on d_k with "undecided" = run: once the criterion decides LU, the remaining
       // speculative launches exit at their first instruction
       launch_qr_panel(w.qpan - k0 * N, gq, k, ib, f->lvl_ptr[k].data(), f->lvl_cnt[k].data(), nl,
-                      wk, sq, /*diag_done=*/a2);
+                      wk, sq, /*diag_done=*/a2, /*spec=*/true);
       P.end(sq);
       cudaEventRecord(ev_qdone, sq);
     };
@@ -712,7 +742,7 @@ void hlq_free(hlq_factors_t f) {
   }
   if (f->ws_block) {
     cudaStreamSynchronize(f->st);
-    cache_put(0, f->ws_block, f->ws_bytes);
+    cache_put(f->dev, 0, f->ws_block, f->ws_bytes);
   }
   f->prof.collect();
   for (auto e : f->ev)
@@ -732,6 +762,7 @@ int hlq_gesv_host(const double* A_host, const double* b_host, double* x_host, in
   if (opt) o = *opt;
   cudaStream_t st = (cudaStream_t)o.stream;
   size_t abytes = sizeof(double) * (size_t)N * N;
+  const int dev = cur_device();
   char* buf = (char*)cache_get(1, abytes + 2 * sizeof(double) * (size_t)N + 512);
   if (!buf) return HLQ_ERR_NOMEM;
   double* dA = (double*)buf;
@@ -740,7 +771,7 @@ int hlq_gesv_host(const double* A_host, const double* b_host, double* x_host, in
   int rc;
   if ((rc = cuda_err(cudaMemcpyAsync(dA, A_host, abytes, cudaMemcpyHostToDevice, st))) ||
       (rc = cuda_err(cudaMemcpyAsync(db, b_host, sizeof(double) * N, cudaMemcpyHostToDevice, st)))) {
-    cache_put(1, buf, abytes + 2 * sizeof(double) * (size_t)N + 512);
+    cache_put(dev, 1, buf, abytes + 2 * sizeof(double) * (size_t)N + 512);
     return rc;
   }
   o.lda = N;
@@ -756,7 +787,7 @@ int hlq_gesv_host(const double* A_host, const double* b_host, double* x_host, in
     rc = st_f;
   }
   hlq_free(f);
-  cache_put(1, buf, abytes + 2 * sizeof(double) * (size_t)N + 512);
+  cache_put(dev, 1, buf, abytes + 2 * sizeof(double) * (size_t)N + 512);
   return rc != 0 ? rc : st_f;
 }
 

@@ -229,11 +229,10 @@ static void launch_dgemm_w(double* C, int64_t ldc, const double* A, int64_t lda,
                            int64_t ldb, int64_t M, int64_t N, int K, bool neg, bool beta,
                            const uint8_t* dec, int k, int want, cudaStream_t st, double* colpart,
                            int64_t ldp) {
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;
+  if (first_on_device(attr)) {
     smem_optin(k_dgemm<true, WM, WN>);
     smem_optin(k_dgemm<false, WM, WN>);
-    attr = true;
   }
   constexpr int BM = gemm_bm<WM>(), BN = gemm_bn<WN>();
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);

@@ -311,10 +311,9 @@ __global__ void __launch_bounds__(GT) k_getrf(const double* __restrict__ A, Geo 
 void launch_getrf(const double* A, Geo g, int k, DevWork w, bool need, cudaStream_t st) {
   if (!need) return;
   size_t smem = sizeof(double) * (2 * GPW + GT / 32) * (g.nb + 1);
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;
+  if (first_on_device(attr)) {
     smem_optin(k_getrf);
-    attr = true;
   }
   { ::hlq::g_launches++; k_getrf<<<1, GT, smem, st>>>(A, g, k, w.W, w.ipiv_ws, w.zp); }
 }

@@ -77,6 +77,7 @@ struct hlq_factors_s {
   bool blocking = true;
   DevWork w{};
   void* ws_block = nullptr;
+  int dev = 0;  // device of the workspace block
   size_t ws_bytes = 0;
   // greedy-tree plan: per step k, levels l: device pointer + count
   std::vector<std::vector<const int2*>> lvl_ptr;

@@ -108,10 +108,12 @@ void launch_dgemm(double* C, int64_t ldc, const double* A, int64_t lda, const do
                   int64_t ldb, int64_t M, int64_t N, int K, bool neg, bool beta,
                   const uint8_t* dec, int k, int want, cudaStream_t st,
                   double* colpart = nullptr, int64_t ldp = 0);
-// tt = false: GEQRT of tiles i_first.. (i_first < 0: k..n-1); tt = true: TTQRT of the pairs
+// tt = false: GEQRT of tiles i_first.. (i_first < 0: k..n-1); tt = true: TTQRT of the pairs.
+// Predicated on dec[k] == QR (dec != nullptr); spec: a speculative launch, which also runs while
+// dec[k] is undecided (0xff) and exits once it is LU
 void launch_qr_panel_tc(double* A, Geo g, int k, int ib, double* Tg, double* Ttt,
                         const int2* pairs, int npairs, const uint8_t* dec, bool tt,
-                        cudaStream_t st, int i_first = -1);
+                        cudaStream_t st, int i_first = -1, bool spec = false);
 // UNMQR (tt = false) / one TTMQR level (tt = true) on the column block (base, ldc, ncols)
 // gmax (TT only): fuse the eliminated tiles' column abs-sum maxima into *gmax (a12); returns
 // whether the fused kernel ran (false: the caller scans the columns itself)
@@ -149,10 +151,11 @@ void launch_lu_growth(const DevWork& w, Geo g, int k, cudaStream_t st);
 void launch_gemm_sub(double* C, int64_t ldc, const double* Am, int64_t lda, const double* Bm,
                      int64_t ldb, int64_t M, int64_t Nc, int K, const uint8_t* dec, int k,
                      cudaStream_t st);
-// diag_done (A2): tile k was already GEQRT-factored in place by the Factor stage
+// diag_done (A2): tile k was already GEQRT-factored in place by the Factor stage;
+// spec: the speculative QR panel (runs while d_k is undecided, see launch_qr_panel_tc)
 void launch_qr_panel(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
                      const int* level_count, int nlevels, const DevWork& w, cudaStream_t st,
-                     bool diag_done = false);
+                     bool diag_done = false, bool spec = false);
 // returns whether every TTMQR level fused the a12 scan into gmax (gmax != nullptr)
 bool launch_qr_update(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
                       const int* level_count, int nlevels, const DevWork& w, int64_t c0,
@@ -190,6 +193,17 @@ inline void smem_optin(F* func) {
   if (cudaFuncGetAttributes(&fa, (const void*)func) != cudaSuccess) return;
   cudaFuncSetAttribute((const void*)func, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        optin - (int)fa.sharedSizeBytes);
+}
+
+// true the first time it is called on the current device for this flag word (per-device one-time
+// kernel attribute setup; a concurrent duplicate call only repeats an idempotent attribute set)
+inline bool first_on_device(unsigned long long& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ULL << (dev & 63);
+  if (__atomic_load_n(&mask, __ATOMIC_ACQUIRE) & bit) return false;
+  __atomic_fetch_or(&mask, bit, __ATOMIC_ACQ_REL);
+  return true;
 }
 
 // ---- device helpers ---------------------------------------------------------------------------

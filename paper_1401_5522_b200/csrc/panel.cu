@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(256) k_decide(Geo g, int k, int crit, double a
     sh_d = -1;
     sh_margin = __longlong_as_double(0x7ff8000000000000LL);  // NaN
     if (has_forced) {
-      sh_d = w.forced[k];
+      sh_d = w.forced[k] ? HLQ_DEC_QR : HLQ_DEC_LU;  // any nonzero entry = QR
       sh_flags |= HLQ_FLAG_FORCED;
       if (sh_d == HLQ_DEC_LU && zp) atomicOr(&w.status[1], 1);
     } else if (alpha == 0.0) {
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(256) k_decide(Geo g, int k, int crit, double a
       bool near = fabs(mg) < tol;
       if (near) fl |= HLQ_FLAG_NEAR_TIE;
       if (has_ref && (near || fabs(w.ref_margin[k]) < tol)) {
-        d = w.ref_dec[k];
+        d = w.ref_dec[k] ? HLQ_DEC_QR : HLQ_DEC_LU;
         fl |= HLQ_FLAG_HINTED;
       }
     }

@@ -1,9 +1,7 @@
-// FP64 tensor-core (DMMA) trailing updates of the QR step: UNMQR (a8) and TTMQR (a11), the bulk of
-// a QR step's flops (Table I: "update D" 4(n-1)^2 units; Alg. 4b).
-//
-// One CTA owns a column slab (W columns) of one tile row (UNMQR) or of one TT pair (TTMQR): the
-// slab of the eliminated tile stays in shared memory across all ib-blocks of the reflector, so each
-// C element is read and written once per step.  Per ib-block b of the stored reflector:
+// FP64 tensor-core (DMMA) QR panel kernels: GEQRT (a8) and TTQRT (a11) of the panel tiles, one CTA
+// per tile / TT pair (Alg. 4, Alg. 4b).  Per 32-column reflector block the CTA
+// factors the block (panel_factor, registers + warp shuffles) and applies the block reflector to
+// the tile's remaining columns in W-column slabs:
 //     GEMM1 (DMMA)  Wb = [C1_b +] V_b^T C          32 x W,  K = rows of V_b
 //     TRMM  (DFMA)  U  = T_b^T Wb                   32 x W,  T_b upper triangular
 //     GEMM2 (DMMA)  C -= V_b U   (TT: C1_b -= U)     rows x W, K = 32
@@ -209,104 +207,6 @@ __device__ __forceinline__ void gemm2(const double* Vs, const double* Us, double
   }
 }
 
-// UNMQR: tile row i = k + blockIdx.y, columns [W*blockIdx.x, +W) of (base, ldcg): C_i <- Q_ik^T C_i
-template <int W>
-__global__ void __launch_bounds__(QD_T) k_unmqr_dmma(const double* __restrict__ A, Geo g, int k,
-                                                     int ib, const double* __restrict__ Tg,
-                                                     double* __restrict__ base, int64_t ldcg,
-                                                     int64_t ncols, const uint8_t* __restrict__ dec) {
-  if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
-  extern __shared__ __align__(16) double sm[];
-  const int ldc = qd_ldc(g.nb);
-  double* Cs = sm;
-  double* Vs = Cs + qd_cs(W, g.nb);
-  double* Us = Vs + 32 * ldc;
-  double* Ts = Us + W * LDU;
-  const int i = k + blockIdx.y;
-  const int bi = g.bs(i), bk = g.cbs(k);
-  const double* tile = g.tile(const_cast<double*>(A), i, k);
-  const double* T = Tg + tri_index(i, k, g.n) * (int64_t)ib * g.nb;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t c0 = (int64_t)blockIdx.x * W;
-  const int rows_pad = ldc - 4;
-  const int cvalid = (int)((ncols - c0) < W ? (ncols - c0) : W);
-  cp_cols(Cs, ldc, base + c0 * ldcg + g.r0(i), ldcg, bi, rows_pad, cvalid, W, tid, QD_T);
-  for (int i0 = 0; i0 < bk; i0 += ib) {
-    const int sb = min(ib, bk - i0);
-    const int R = bi - i0;
-    if (R <= 0) break;
-    const int RK = (R + 31) / 32 * 32;
-    __syncthreads();
-    cp_cols(Vs, ldc, tile + (int64_t)i0 * g.lda + i0, g.lda, R, RK, sb, 32, tid, QD_T);
-    cp_cols(Ts, 33, T + (int64_t)i0 * ib, ib, sb, 32, sb, 32, tid, QD_T);  // stored T: zeros below
-    cpa_wait_all();
-    __syncthreads();
-    for (int o = tid; o < 32 * 32; o += QD_T) {  // unit diagonal, zeros above (explicit structure)
-      int l = o >> 5, r = o & 31;
-      if (r <= l && r < RK) Vs[l * ldc + r] = (r == l && l < sb && r < R) ? 1.0 : 0.0;
-    }
-    __syncthreads();
-    gemm1_trmm<W>(Vs, Cs, ldc, i0, RK, Ts, Us, nullptr, 0, c0, ncols, sb, warp, lane);
-    __syncthreads();
-    gemm2<W>(Vs, Us, Cs, ldc, i0, RK, warp, lane);
-  }
-  __syncthreads();
-  for (int o = tid; o < W * bi; o += QD_T) {
-    int j = o / bi, r = o - j * bi;
-    if (c0 + j < ncols) base[(c0 + j) * ldcg + g.r0(i) + r] = Cs[j * ldc + r];
-  }
-}
-
-// TTMQR: pair (e, i) = pairs[blockIdx.y], columns [W*blockIdx.x, +W): [C_e; C_i] <- Q^T [C_e; C_i]
-template <int W>
-__global__ void __launch_bounds__(QD_T) k_ttmqr_dmma(const double* __restrict__ A, Geo g, int k,
-                                                     int ib, const double* __restrict__ Ttt,
-                                                     const int2* __restrict__ pairs,
-                                                     double* __restrict__ base, int64_t ldcg,
-                                                     int64_t ncols, const uint8_t* __restrict__ dec) {
-  if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
-  extern __shared__ __align__(16) double sm[];
-  const int ldc = qd_ldc(g.nb);
-  double* Cs = sm;               // C_i slab (rows of tile i)
-  double* Vs = Cs + qd_cs(W, g.nb);
-  double* Us = Vs + 32 * ldc;
-  double* Ts = Us + W * LDU;
-  const int2 pr = pairs[blockIdx.y];
-  const int e = pr.x, i = pr.y;
-  const int bi = g.bs(i), bk = g.cbs(k);
-  const double* Vt = g.tile(const_cast<double*>(A), i, k);
-  const double* T = Ttt + tri_index(i, k, g.n) * (int64_t)ib * g.nb;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t c0 = (int64_t)blockIdx.x * W;
-  const int rows_pad = ldc - 4;
-  const int cvalid = (int)((ncols - c0) < W ? (ncols - c0) : W);
-  cp_cols(Cs, ldc, base + c0 * ldcg + g.r0(i), ldcg, bi, rows_pad, cvalid, W, tid, QD_T);
-  for (int i0 = 0; i0 < bk; i0 += ib) {
-    const int sb = min(ib, bk - i0);
-    const int R2 = min(bi, i0 + sb);
-    const int RK = (R2 + 31) / 32 * 32;
-    __syncthreads();
-    cp_cols(Vs, ldc, Vt + (int64_t)i0 * g.lda, g.lda, R2, RK, sb, 32, tid, QD_T);
-    cp_cols(Ts, 33, T + (int64_t)i0 * ib, ib, sb, 32, sb, 32, tid, QD_T);
-    cpa_wait_all();
-    __syncthreads();
-    for (int o = tid; o < 32 * RK; o += QD_T) {  // the TT reflectors are upper triangular
-      int l = o / RK, r = o - l * RK;
-      if (r > i0 + l) Vs[l * ldc + r] = 0.0;
-    }
-    __syncthreads();
-    // Wb = C1_b + V2_b^T C2, U = T^T Wb, C1_b -= U (C1_b = rows i0.. of tile e, read/written in place)
-    gemm1_trmm<W>(Vs, Cs, ldc, 0, RK, Ts, Us, base + g.r0(e) + i0, ldcg, c0, ncols, sb, warp, lane);
-    __syncthreads();
-    gemm2<W>(Vs, Us, Cs, ldc, 0, RK, warp, lane);  // C2 -= V2_b U
-  }
-  __syncthreads();
-  for (int o = tid; o < W * bi; o += QD_T) {
-    int j = o / bi, r = o - j * bi;
-    if (c0 + j < ncols) base[(c0 + j) * ldcg + g.r0(i) + r] = Cs[j * ldc + r];
-  }
-}
-
 // ---------------------------------------------------------------------------------------------
 // Panel factorisation of one 32-column reflector block by the whole CTA (8 warps): per column l a
 // CTA-wide sum of squares (dlarfg, reading 14), the update of the block's remaining
@@ -503,8 +403,10 @@ __device__ __forceinline__ void panel_factor_nb(int nb, double* Vs, int ldc, dou
 template <int W>
 __global__ void __launch_bounds__(QD_T) k_geqrt_tc(double* __restrict__ A, Geo g, int k, int ib,
                                                    double* __restrict__ Tg,
-                                                   const uint8_t* __restrict__ dec, int i_first) {
-  if (dec != nullptr && dec[k] == HLQ_DEC_LU) return;  // (undecided: speculative run)
+                                                   const uint8_t* __restrict__ dec, int i_first,
+                                                   int spec) {
+  // predicated on d_k == QR; a speculative launch (spec) also runs while d_k is undecided
+  if (dec != nullptr && (spec ? dec[k] == HLQ_DEC_LU : dec[k] != HLQ_DEC_QR)) return;
   extern __shared__ __align__(16) double sm[];
   const int ldc = qd_ldc(g.nb);
   double* Cs = sm;
@@ -565,8 +467,8 @@ template <int W>
 __global__ void __launch_bounds__(QD_T) k_ttqrt_tc(double* __restrict__ A, Geo g, int k, int ib,
                                                    double* __restrict__ Ttt,
                                                    const int2* __restrict__ pairs,
-                                                   const uint8_t* __restrict__ dec) {
-  if (dec != nullptr && dec[k] == HLQ_DEC_LU) return;  // (undecided: speculative run)
+                                                   const uint8_t* __restrict__ dec, int spec) {
+  if (dec != nullptr && (spec ? dec[k] == HLQ_DEC_LU : dec[k] != HLQ_DEC_QR)) return;
   extern __shared__ __align__(16) double sm[];
   const int ldc = qd_ldc(g.nb);
   double* Cs = sm;
@@ -635,77 +537,45 @@ __global__ void __launch_bounds__(QD_T) k_ttqrt_tc(double* __restrict__ A, Geo g
 template <int W>
 static void launch_panel_w(double* A, Geo g, int k, int ib, double* Tg, double* Ttt,
                            const int2* pairs, int npairs, const uint8_t* dec, bool tt,
-                           cudaStream_t st, int i_first) {
-  static bool attr = false;
-  if (!attr) {
+                           cudaStream_t st, int i_first, bool spec) {
+  static unsigned long long attr = 0;
+  if (first_on_device(attr)) {
     smem_optin(k_geqrt_tc<W>);
     smem_optin(k_ttqrt_tc<W>);
-    attr = true;
   }
   const size_t smem = qd_smem<W>(g.nb);
   if (!tt) {
     if (g.n - i_first <= 0) return;
-    { ::hlq::g_launches++; k_geqrt_tc<W><<<g.n - i_first, QD_T, smem, st>>>(A, g, k, ib, Tg, dec, i_first); }
+    { ::hlq::g_launches++; k_geqrt_tc<W><<<g.n - i_first, QD_T, smem, st>>>(A, g, k, ib, Tg, dec, i_first, spec ? 1 : 0); }
   } else {
-    { ::hlq::g_launches++; k_ttqrt_tc<W><<<npairs, QD_T, smem, st>>>(A, g, k, ib, Ttt, pairs, dec); }
+    { ::hlq::g_launches++; k_ttqrt_tc<W><<<npairs, QD_T, smem, st>>>(A, g, k, ib, Ttt, pairs, dec, spec ? 1 : 0); }
   }
 }
 
 void launch_qr_panel_tc(double* A, Geo g, int k, int ib, double* Tg, double* Ttt,
                         const int2* pairs, int npairs, const uint8_t* dec, bool tt,
-                        cudaStream_t st, int i_first) {
+                        cudaStream_t st, int i_first, bool spec) {
   if (i_first < 0) i_first = k;
   if (qd_smem<64>(g.nb) <= 227 * 1024)
-    launch_panel_w<64>(A, g, k, ib, Tg, Ttt, pairs, npairs, dec, tt, st, i_first);
+    launch_panel_w<64>(A, g, k, ib, Tg, Ttt, pairs, npairs, dec, tt, st, i_first, spec);
   else
-    launch_panel_w<32>(A, g, k, ib, Tg, Ttt, pairs, npairs, dec, tt, st, i_first);
+    launch_panel_w<32>(A, g, k, ib, Tg, Ttt, pairs, npairs, dec, tt, st, i_first, spec);
 }
 
-template <int W>
-static void launch_w(const double* A, Geo g, int k, int ib, const double* Tg, const double* Ttt,
-                     const int2* const* level_pairs, const int* level_count, int nlevels,
-                     double* base, int64_t ldc, int64_t ncols, const uint8_t* dec, int what,
-                     cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    smem_optin(k_unmqr_dmma<W>);
-    smem_optin(k_ttmqr_dmma<W>);
-    attr = true;
-  }
-  const size_t smem = qd_smem<W>(g.nb);
-  const unsigned slabs = (unsigned)((ncols + W - 1) / W);
-  if (what == 0) {
-    { ::hlq::g_launches++; k_unmqr_dmma<W><<<dim3(slabs, g.n - k), QD_T, smem, st>>>(A, g, k, ib, Tg, base, ldc, ncols, dec); }
-  } else {
-    const int l = what - 1;
-    { ::hlq::g_launches++; k_ttmqr_dmma<W><<<dim3(slabs, level_count[l]), QD_T, smem, st>>>(A, g, k, ib, Ttt, level_pairs[l], base, ldc, ncols, dec); }
-  }
-  (void)nlevels;
-}
-
-// what = 0: UNMQR of all tile rows; what = 1 + l: TTMQR of level l.  Column slab width 64 when the
-// slab + reflector block fit in shared memory (nb <= 256), else 32.
+// what = 0: UNMQR of all tile rows; what = 1 + l: TTMQR of level l (qr_update.cu, register-slab
+// DMMA kernel; ib = 32).  Returns whether the a12 scan was fused (TTMQR levels with gmax).
 bool launch_qr_update_dmma(const double* A, Geo g, int k, int ib, const double* Tg,
                            const double* Ttt, const int2* const* level_pairs,
                            const int* level_count, int nlevels, double* base, int64_t ldc,
                            int64_t ncols, const uint8_t* dec, int what, cudaStream_t st,
                            double* gmax) {
+  (void)ib;
+  (void)nlevels;
   if (ncols <= 0) return true;
-  static int v1 = -1;
-  if (v1 < 0) v1 = getenv("HLQ_QR_UPDATE_V1") ? 1 : 0;
-  if (!v1 && ib == 32) {
-    if (what == 0)
-      return launch_qr_update2(A, g, k, Tg, nullptr, 0, false, base, ldc, ncols, dec, st);
-    return launch_qr_update2(A, g, k, Ttt, level_pairs[what - 1], level_count[what - 1], true,
-                             base, ldc, ncols, dec, st, gmax);
-  }
-  if (qd_smem<64>(g.nb) <= 227 * 1024)
-    launch_w<64>(A, g, k, ib, Tg, Ttt, level_pairs, level_count, nlevels, base, ldc, ncols, dec,
-                 what, st);
-  else
-    launch_w<32>(A, g, k, ib, Tg, Ttt, level_pairs, level_count, nlevels, base, ldc, ncols, dec,
-                 what, st);
-  return false;
+  if (what == 0)
+    return launch_qr_update2(A, g, k, Tg, nullptr, 0, false, base, ldc, ncols, dec, st);
+  return launch_qr_update2(A, g, k, Ttt, level_pairs[what - 1], level_count[what - 1], true, base,
+                           ldc, ncols, dec, st, gmax);
 }
 
 }  // namespace hlq

@@ -1,22 +1,9 @@
-// QR trailing update, v2 (a8 UNMQR, a10/a11 TTMQR): the bulk of a QR step's flops (Table I
-// "update D" PAPER.md:166; Alg. 4b), on the FP64 tensor cores (DMMA).
-//
-// One CTA owns a slab of W = 8*NCG columns of one tile row (UNMQR) or of one TT pair (TTMQR, the
-// slab of the eliminated tile i; rows of the surviving tile e are read-modify-written per block).
-// The slab stays in shared memory for the whole step: every C element is read and written once.
-// A PAIR of warps (kh = 0, 1) owns slab columns [8cg, 8cg+8) for ALL three products of a reflector
-// block b (32 columns), the two warps taking alternate 32-row chunks of V_b:
-//     GEMM1  W  = [C_e(b) +] V_b^T C        32 x 8, K = rows of V_b; pair-reduced   (DMMA)
-//     TRMM   U  = T_b^T W                   rows 16kh..16kh+15 of 32 x 8, K = 32    (DMMA)
-//     GEMM2  C -= V_b U   [C_e(b) -= U]     chunk rows x 8, K = 32                  (DMMA)
-// so a warp pair only ever touches its own columns of C (named barriers per pair); the data shared
-// by the CTA is the stream of V_b row-chunk pairs (32 x 32 each, cp.async, double-buffered) and
-// T_b.  16 warps per SM (one CTA) hide the shared-memory and DMMA latencies.  V_b is streamed twice per block
-// (GEMM1, GEMM2) from L2; its explicit structure (unit diagonal / zeros above for GEQRT reflectors,
-// zeros below the diagonal for the TT reflectors) is applied when the diagonal chunk's fragments are
-// loaded.  Fragments: mma.sync.m8n8k4.f64 (lane g = lane/4, t = lane%4: A(g,t), B(t,g),
-// C(g, 2t..2t+1)); every shared array has a leading dimension == 4 (mod 16) doubles, which makes the
-// fragment loads bank-conflict free.  Householder convention and T layout: DESIGN.md 14-15.
+// QR trailing update (a8 UNMQR, a10/a11 TTMQR): the bulk of a QR step's flops (Table I "update D"
+// PAPER.md:166; Alg. 4b), on the FP64 tensor cores (DMMA).  One CTA owns a column slab of
+// one tile row (UNMQR) or of the eliminated tile of one TT pair (TTMQR) for the whole step and
+// keeps it in REGISTERS as C^T accumulator fragments (design below, "v3"); every C element is read
+// and written once per launch.  Householder convention and T layout: DESIGN.md readings 14-15.
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "hlq_internal.cuh"
@@ -24,8 +11,6 @@
 namespace hlq {
 
 namespace {
-constexpr int LDV = 36;  // V chunk [l][r], T [col][row], W/U [col][l]
-constexpr int CH = 32 * LDV;  // doubles per ring slot
 
 __device__ __forceinline__ void dmma_(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -48,348 +33,7 @@ __device__ __forceinline__ void wait_() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-__host__ __device__ inline int rup32(int x) { return (x + 31) / 32 * 32; }
 }  // namespace
-
-// rows [r0, r0+32) x cols [c0, c0+32) of a column-major source (ld) -> dst[l*LDV + r]; zero-fill rows
-// >= rmax and columns >= cmax
-template <bool V16>
-__device__ __forceinline__ void load_chunk(double* dst, const double* src, int64_t ld, int r0,
-                                           int rmax, int cmax, int tid, int nthr) {
-  if (V16) {
-    for (int o = tid; o < 32 * 16; o += nthr) {
-      const int l = o >> 4, r = (o & 15) * 2;
-      const bool ok = (r0 + r < rmax) && (l < cmax);  // rmax even on this path
-      cp16(dst + l * LDV + r, ok ? src + (int64_t)l * ld + r0 + r : src, ok);
-    }
-  } else {
-    for (int o = tid; o < 32 * 32; o += nthr) {
-      const int l = o >> 5, r = o & 31;
-      const bool ok = (r0 + r < rmax) && (l < cmax);
-      cp8(dst + l * LDV + r, ok ? src + (int64_t)l * ld + r0 + r : src, ok);
-    }
-  }
-}
-
-template <int NCG, bool TT>
-__global__ void __launch_bounds__(NCG * 64) k_qr_update2(const double* __restrict__ A, Geo g,
-                                                        int k, const double* __restrict__ Tbase,
-                                                        const int2* __restrict__ pairs,
-                                                        double* __restrict__ base, int64_t ldcg,
-                                                        int64_t ncols,
-                                                        const uint8_t* __restrict__ dec) {
-  if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
-  constexpr int W = 8 * NCG, NT = 64 * NCG;
-  extern __shared__ __align__(16) double sm[];
-  const int ldc = rup32(g.nb) + 4;
-  double* Cs = sm;                        // W x ldc   slab of tile i (col-major)
-  double* ring = Cs + W * ldc;            // 4 x CH: chunk pairs (2 slots each, double-buffered)
-  double* Ts = ring + 4 * CH;             // 2 x CH  (T_b, double-buffered per block)
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int gq = lane >> 2, tq = lane & 3;
-  const int cg = warp % NCG, kh = warp / NCG;  // column group, half (chunk parity / TRMM rows)
-  double* Wb = Ts + 2 * CH + cg * 8 * LDV;     // W, then -U, of column group cg ([col][l])
-  double* Rb = Ts + 2 * CH + (NCG + cg) * 8 * LDV;  // partial W of the kh = 1 warp
-  const unsigned pair_bar = 1 + cg;
-
-  int e = 0, i;
-  if (TT) {
-    const int2 pr = pairs[blockIdx.y];
-    e = pr.x;
-    i = pr.y;
-  } else {
-    i = k + blockIdx.y;
-  }
-  const int bi = g.bs(i), bk = g.cbs(k);
-  const double* Vt = g.tile(const_cast<double*>(A), i, k);
-  const double* T = Tbase + tri_index(i, k, g.n) * (int64_t)32 * g.nb;
-  const int64_t c0 = (int64_t)blockIdx.x * W;
-  const int cvalid = (int)((ncols - c0) < W ? (ncols - c0) : W);
-  const int crows = TT ? (bi < bk ? bi : bk) : bi;
-  const int crows_pad = rup32(crows);
-  double* Cg = base + c0 * ldcg + g.r0(i);
-  const bool vv16 = ((g.lda & 1) == 0) && ((((uintptr_t)Vt) & 15) == 0);
-
-  // ---- C slab: 8 threads per column, two rows per thread and step (no divisions)
-  const int sj = tid >> 3, sr = 2 * (tid & 7);
-  {
-    const bool c16 = ((ldcg & 1) == 0) && ((((uintptr_t)Cg) & 15) == 0);
-    double* cs = Cs + sj * ldc;
-    const double* cgp = Cg + (int64_t)sj * ldcg;
-    const bool jok = sj < cvalid;
-    for (int r = sr; r < crows_pad; r += 16) {
-      if (jok && r + 1 < crows) {
-        if (c16) {
-          cp16(cs + r, cgp + r, true);
-        } else {
-          cp8(cs + r, cgp + r, true);
-          cp8(cs + r + 1, cgp + r + 1, true);
-        }
-      } else {
-        cs[r] = (jok && r < crows) ? cgp[r] : 0.0;
-        cs[r + 1] = 0.0;
-      }
-    }
-    commit_();
-  }
-
-  const int nblk = (bk + 31) / 32;
-  auto blk_rows = [&](int b, int& rlo, int& rhi) {
-    const int i0 = 32 * b;
-    if (TT) {
-      rlo = 0;
-      rhi = bi < i0 + 32 ? bi : i0 + 32;
-    } else {
-      rlo = i0;
-      rhi = bi;
-    }
-  };
-  // producer: chunk pairs within a pass (GEMM1 / GEMM2 of block pb)
-  int pb = 0, ppass = 0, pc = 0, pj = 0;
-  bool pdone = false;
-  auto issue_pair = [&]() {
-    if (!pdone) {
-      int rlo, rhi;
-      blk_rows(pb, rlo, rhi);
-      if (rhi <= rlo) {
-        pdone = true;
-      } else {
-        const int i0 = 32 * pb;
-        const int cmax = (bk - i0) < 32 ? (bk - i0) : 32;
-        const int nch = (rhi - rlo + 31) / 32;
-        const bool v16 = vv16 && ((rhi & 1) == 0);
-        for (int h = 0; h < 2 && pc + h < nch; ++h) {
-          double* slot = ring + (2 * (pj & 1) + h) * CH;
-          if (v16)
-            load_chunk<true>(slot, Vt + (int64_t)i0 * g.lda, g.lda, rlo + 32 * (pc + h), rhi, cmax,
-                             tid, NT);
-          else
-            load_chunk<false>(slot, Vt + (int64_t)i0 * g.lda, g.lda, rlo + 32 * (pc + h), rhi,
-                              cmax, tid, NT);
-        }
-        if (ppass == 0 && pc == 0) {
-          // T_b (32 x 32; T(q, l) at T[(i0 + l) * 32 + q]; zeros below the diagonal)
-          double* ts = Ts + (pb & 1) * CH;
-          for (int o = tid; o < 32 * 16; o += NT) {
-            const int l = o >> 4, q = (o & 15) * 2;
-            const bool ok = l < cmax;
-            cp16(ts + l * LDV + q, ok ? T + (int64_t)(i0 + l) * 32 + q : T, ok);
-          }
-        }
-        ++pj;
-        pc += 2;
-        if (pc >= nch) {
-          pc = 0;
-          if (++ppass == 2) {
-            ppass = 0;
-            if (++pb == nblk) pdone = true;
-          }
-        }
-      }
-    }
-    commit_();
-  };
-  issue_pair();
-
-  int j = 0;  // consumer pair index
-  const int wc = cg * 8;
-#pragma unroll 1
-  for (int b = 0; b < nblk; ++b) {
-    int rlo, rhi;
-    blk_rows(b, rlo, rhi);
-    if (rhi <= rlo) break;
-    const int i0 = 32 * b;
-    const int sb = (bk - i0) < 32 ? (bk - i0) : 32;
-    const int nch = (rhi - rlo + 31) / 32;
-    const int cdiag = TT ? (i0 / 32) : 0;  // chunk holding the diagonal 32 x 32 block of V_b
-    double* Ceb = TT ? base + c0 * ldcg + g.r0(e) + i0 : nullptr;
-
-    // ---------------- GEMM1 (chunks c = 2j' + kh): W = [C_e(b) +] V_b^T C
-    double acc[2][4][2];
-#pragma unroll
-    for (int u = 0; u < 2; ++u)
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi) acc[u][mi][0] = acc[u][mi][1] = 0.0;
-    if (TT && kh == 0) {
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int l = mi * 8 + gq, col = wc + 2 * tq + h;
-          if (l < sb && col < cvalid) acc[0][mi][h] = Ceb[(int64_t)col * ldcg + l];
-        }
-    }
-#pragma unroll 1
-    for (int c = 0; c < nch; c += 2, ++j) {
-      wait_<0>();
-      __syncthreads();
-      issue_pair();
-      const int cc_ = c + kh;
-      if (cc_ >= nch) continue;
-      const double* V = ring + (2 * (j & 1) + kh) * CH;
-      const double* Cb = Cs + (wc + gq) * ldc + rlo + 32 * cc_ + tq;
-      if (cc_ == cdiag) {
-#pragma unroll
-        for (int kk = 0; kk < 32; kk += 4) {
-          const double bv = Cb[kk];
-          const int r = kk + tq;
-#pragma unroll
-          for (int mi = 0; mi < 4; ++mi) {
-            const int l = mi * 8 + gq;
-            double a = V[l * LDV + r];
-            if (TT) {
-              if (r > l) a = 0.0;
-            } else {
-              a = (r < l) ? 0.0 : ((r == l) ? 1.0 : a);
-            }
-            dmma_(acc[(kk >> 2) & 1][mi][0], acc[(kk >> 2) & 1][mi][1], a, bv);
-          }
-        }
-      } else {
-#pragma unroll
-        for (int kk = 0; kk < 32; kk += 4) {
-          const double bv = Cb[kk];
-#pragma unroll
-          for (int mi = 0; mi < 4; ++mi)
-            dmma_(acc[(kk >> 2) & 1][mi][0], acc[(kk >> 2) & 1][mi][1],
-                  V[(mi * 8 + gq) * LDV + kk + tq], bv);
-        }
-      }
-    }
-    // ---------------- pair reduction, then TRMM U = T_b^T W split by rows (kh -> mi 2kh, 2kh+1)
-    if (kh == 1) {
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-          Rb[(2 * tq + h) * LDV + mi * 8 + gq] = acc[0][mi][h] + acc[1][mi][h];
-    }
-    asm volatile("bar.sync %0, %1;\n" ::"r"(pair_bar), "n"(64));
-    if (kh == 0) {
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int o = (2 * tq + h) * LDV + mi * 8 + gq;
-          Wb[o] = (acc[0][mi][h] + acc[1][mi][h]) + Rb[o];
-        }
-    }
-    asm volatile("bar.sync %0, %1;\n" ::"r"(pair_bar), "n"(64));
-    {
-      const double* ts = Ts + (b & 1) * CH;
-      double u[2][2];
-#pragma unroll
-      for (int m2 = 0; m2 < 2; ++m2) u[m2][0] = u[m2][1] = 0.0;
-#pragma unroll
-      for (int kk = 0; kk < 32; kk += 4) {
-        const double bv = Wb[gq * LDV + kk + tq];
-#pragma unroll
-        for (int m2 = 0; m2 < 2; ++m2)
-          dmma_(u[m2][0], u[m2][1], ts[((2 * kh + m2) * 8 + gq) * LDV + kk + tq], bv);
-      }
-      asm volatile("bar.sync %0, %1;\n" ::"r"(pair_bar), "n"(64));
-#pragma unroll
-      for (int m2 = 0; m2 < 2; ++m2)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int l = (2 * kh + m2) * 8 + gq, col = wc + 2 * tq + h;
-          Wb[(2 * tq + h) * LDV + l] = neg_bits(u[m2][h]);
-          if (TT && l < sb && col < cvalid) Ceb[(int64_t)col * ldcg + l] -= u[m2][h];
-        }
-      asm volatile("bar.sync %0, %1;\n" ::"r"(pair_bar), "n"(64));
-    }
-    // ---------------- GEMM2 (chunks c = 2j' + kh): C[rows] -= V_b U
-#pragma unroll 1
-    for (int c = 0; c < nch; c += 2, ++j) {
-      wait_<0>();
-      __syncthreads();
-      issue_pair();
-      const int cc_ = c + kh;
-      if (cc_ >= nch) continue;
-      const double* V = ring + (2 * (j & 1) + kh) * CH;
-      const int r0 = rlo + 32 * cc_;
-      double cc[4][2];
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) cc[mi][h] = Cs[(wc + 2 * tq + h) * ldc + r0 + mi * 8 + gq];
-      const double* Ub = Wb + gq * LDV + tq;
-      if (cc_ == cdiag) {
-#pragma unroll
-        for (int kk = 0; kk < 32; kk += 4) {
-          const double bv = Ub[kk];
-          const int l = kk + tq;
-#pragma unroll
-          for (int mi = 0; mi < 4; ++mi) {
-            const int r = mi * 8 + gq;
-            double a = V[l * LDV + r];
-            if (TT) {
-              if (r > l) a = 0.0;
-            } else {
-              a = (r < l) ? 0.0 : ((r == l) ? 1.0 : a);
-            }
-            dmma_(cc[mi][0], cc[mi][1], a, bv);
-          }
-        }
-      } else {
-#pragma unroll
-        for (int kk = 0; kk < 32; kk += 4) {
-          const double bv = Ub[kk];
-#pragma unroll
-          for (int mi = 0; mi < 4; ++mi)
-            dmma_(cc[mi][0], cc[mi][1], V[(kk + tq) * LDV + mi * 8 + gq], bv);
-        }
-      }
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) Cs[(wc + 2 * tq + h) * ldc + r0 + mi * 8 + gq] = cc[mi][h];
-    }
-  }
-  wait_<0>();
-  __syncthreads();
-  // ---- store the slab (8 threads per column)
-  if (sj < cvalid) {
-    const double* cs = Cs + sj * ldc;
-    double* cgp = Cg + (int64_t)sj * ldcg;
-    for (int r = sr; r < crows; r += 16) {
-      cgp[r] = cs[r];
-      if (r + 1 < crows) cgp[r + 1] = cs[r + 1];
-    }
-  }
-}
-
-template <int NCG>
-static size_t upd_smem(int nb) {
-  return sizeof(double) * ((size_t)8 * NCG * (rup32(nb) + 4) + (size_t)6 * CH +
-                           (size_t)2 * NCG * 8 * LDV);
-}
-
-template <int NCG>
-static bool launch_nw(const double* A, Geo g, int k, const double* T, const int2* pairs,
-                      int npairs, bool tt, double* base, int64_t ldc, int64_t ncols,
-                      const uint8_t* dec, cudaStream_t st) {
-  const size_t smem = upd_smem<NCG>(g.nb);
-  if (smem > 227 * 1024) return false;
-  static bool attr = false;
-  if (!attr) {
-    smem_optin(k_qr_update2<NCG, false>);
-    smem_optin(k_qr_update2<NCG, true>);
-    attr = true;
-  }
-  const unsigned slabs = (unsigned)((ncols + 8 * NCG - 1) / (8 * NCG));
-  if (!tt) {
-    ::hlq::g_launches++;
-    k_qr_update2<NCG, false><<<dim3(slabs, g.n - k), NCG * 64, smem, st>>>(
-        A, g, k, T, nullptr, base, ldc, ncols, dec);
-  } else {
-    if (npairs <= 0) return true;
-    ::hlq::g_launches++;
-    k_qr_update2<NCG, true><<<dim3(slabs, npairs), NCG * 64, smem, st>>>(
-        A, g, k, T, pairs, base, ldc, ncols, dec);
-  }
-  return true;
-}
 
 // UNMQR of every tile row k..n-1 (tt = false, T = GEQRT factors) or TTMQR of one level (tt = true,
 // T = TTQRT factors) on the column block (base, ldc, ncols).  Requires ib = 32 and nb <= 512.
@@ -401,13 +45,11 @@ bool launch_qr_update2(const double* A, Geo g, int k, const double* T, const int
                        int npairs, bool tt, double* base, int64_t ldc, int64_t ncols,
                        const uint8_t* dec, cudaStream_t st, double* gmax) {
   if (ncols <= 0) return true;
-  if (launch_qr_update3(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st, gmax))
-    return true;
-  if (launch_nw<8>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st)) return false;
-  if (launch_nw<7>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st)) return false;
-  if (launch_nw<6>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st)) return false;
-  launch_nw<4>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st);
-  return false;
+  if (!launch_qr_update3(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st, gmax)) {
+    fprintf(stderr, "[hlq] QR update: nb = %d has no register-slab instantiation\n", g.nb);
+    abort();
+  }
+  return tt && gmax != nullptr;
 }
 
 // =============================================================================================
@@ -809,11 +451,10 @@ template <int NB, int RQ, int NCG, bool V16>
 static void launch3(const double* A, Geo g, int k, const double* T, const int2* pairs, int npairs,
                     bool tt, double* base, int64_t ldc, int64_t ncols, const uint8_t* dec,
                     cudaStream_t st, double* gmax) {
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;
+  if (first_on_device(attr)) {
     smem_optin(k_qr_update3<NB, false, RQ, NCG, V16>);
     smem_optin(k_qr_update3<NB, true, RQ, NCG, V16>);
-    attr = true;
   }
   const unsigned slabs = (unsigned)((ncols + 16 * NCG - 1) / (16 * NCG));
   const size_t smem = upd3_smem(RQ * NCG, 16 * NCG);
@@ -833,9 +474,6 @@ static void launch3(const double* A, Geo g, int k, const double* T, const int2* 
 bool launch_qr_update3(const double* A, Geo g, int k, const double* T, const int2* pairs,
                        int npairs, bool tt, double* base, int64_t ldc, int64_t ncols,
                        const uint8_t* dec, cudaStream_t st, double* gmax) {
-  static int off = -1;
-  if (off < 0) off = getenv("HLQ_QR_UPDATE_V2") ? 1 : 0;
-  if (off) return false;
   if (ncols <= 0) return true;
   // 16-byte V copies need an even leading dimension, a 16-byte aligned matrix and even tile heights
   const bool v16 = ((g.lda & 1) == 0) && ((((uintptr_t)A) & 15) == 0) && ((g.N & 1) == 0) &&

@@ -132,9 +132,8 @@ void launch_gemv_sub(double* y, const double* B, int64_t ldb, int64_t M, int K, 
 }
 
 static void solve_attr_once() {
-  static bool done = false;
-  if (done) return;
-  done = true;
+  static unsigned long long done = 0;
+  if (!first_on_device(done)) return;
   smem_optin(k_solve_lu_diag);
   smem_optin(k_solve_upper_diag);
 }

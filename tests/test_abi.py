@@ -52,7 +52,7 @@ def test_argument_errors_without_gpu(built):
     # options: unknown LU variant; A2 needs ib = 32 and the exact inverse norm
     for fields in ({"lu_variant": 2}, {"lu_variant": 1, "ib": 16},
                    {"lu_variant": 1, "invnorm_estimate": 1}, {"pivot_scope": 2},
-                   {"pivot_scope": 1, "lu_variant": 1}):
+                   {"pivot_scope": 1, "lu_variant": 1}, {"ib": 16}, {"ib": 8}, {"ib": 33}):
         opt = H.hlq_default_options()
         for k, v in fields.items():
             setattr(opt, k, v)
@@ -72,3 +72,26 @@ def test_product_path_has_no_oracle_or_cpu_fallback():
                 txt = open(os.path.join(dirpath, fn)).read()
                 assert not re.search(r"(import|from)\s+oracle|hlq_oracle|hlqo_", txt), fn
                 assert "numpy.linalg" not in txt and "scipy" not in txt, fn
+
+
+def test_binding_validates_arguments_before_the_call(built):
+    """The binding refuses what the C side cannot check (host-side, no GPU needed): a non-CUDA or
+    wrong-dtype matrix, a matrix smaller than lda*(N-1)+N, per-step vectors of the wrong length,
+    ref_dec without ref_margin."""
+    import numpy as np
+    import torch
+    import paper_1401_5522_b200 as H
+    with pytest.raises(H.HlqError, match="float64 CUDA"):
+        H.hlq_factor_ex(torch.zeros(64, dtype=torch.float64), 8, 4)
+    with pytest.raises(H.HlqError, match="float64 CUDA"):
+        H.hlq_factor_ex(torch.zeros(64, dtype=torch.float32), 8, 4)
+    opt = H.hlq_default_options()
+    with pytest.raises(H.HlqError):
+        H._step_vectors(opt, 2, np.zeros(3), None, None, [])
+    with pytest.raises(H.HlqError, match="together"):
+        H._step_vectors(opt, 2, None, np.zeros(2), None, [])
+    with pytest.raises(H.HlqError):
+        H._step_vectors(opt, 2, None, np.zeros(2), np.zeros(1), [])
+    keep = []
+    H._step_vectors(opt, 2, np.array([0, 1]), np.array([1, 0]), np.array([0.5, -0.5]), keep)
+    assert len(keep) == 3 and opt.forced and opt.ref_dec and opt.ref_margin

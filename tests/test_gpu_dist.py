@@ -13,6 +13,7 @@ import pytest
 
 import hlq_inputs as I
 from oracle import hlq_oracle as O
+from test_gpu_parity import check_decision_record, hint_kwargs
 
 pytestmark = pytest.mark.gpu
 
@@ -41,9 +42,11 @@ def run_dist(H, A, b, nb, P, Q, crit=O.CRIT_MAX, alpha=1.0, D=None, forced=None,
     kw = dict(tree_domains=D)
     if forced is not None:
         f = H.hlq_factor_dist(grid, locs, N, nb, crit, alpha, forced=forced, **kw)
+        fo.hinted_run, fo.forced_run = False, True
     else:
-        f = H.hlq_factor_dist(grid, locs, N, nb, crit, alpha, ref_dec=fo.dec,
-                              ref_margin=np.nan_to_num(fo.margin, nan=1.0), **kw)
+        hk = hint_kwargs(fo)  # the oracle's decisions only where it has a near tie
+        f = H.hlq_factor_dist(grid, locs, N, nb, crit, alpha, **hk, **kw)
+        fo.hinted_run, fo.forced_run = bool(hk), False
     db = torch.from_numpy(np.ascontiguousarray(b)).cuda()
     x = f.solve(db).cpu().numpy()
     F = H.gather_block_cyclic(
@@ -54,6 +57,8 @@ def run_dist(H, A, b, nb, P, Q, crit=O.CRIT_MAX, alpha=1.0, D=None, forced=None,
 
 def check(fo, f, F, x, A, b, tol=1e-10):
     np.testing.assert_array_equal(f.decisions(), fo.dec)
+    check_decision_record(fo, f, getattr(fo, "hinted_run", False),
+                          forced=getattr(fo, "forced_run", False))
     diff = O.factor_diff(F, fo.A)
     assert diff <= tol, f"factor diff {diff:.3e}"
     assert f.growth() == pytest.approx(fo.growth, rel=1e-10)
@@ -83,8 +88,7 @@ def test_grid_domains_match_single_gpu(H, P, Q, D):
     fo, f, F, x = run_dist(H, A, b, nb, P, Q, alpha=1.0, D=D)
     check(fo, f, F, x, A, b)
     dA = H.to_colmajor(A)
-    fs = H.hlq_factor_ex(dA, N, nb, O.CRIT_MAX, 1.0, ref_dec=fo.dec,
-                         ref_margin=np.nan_to_num(fo.margin, nan=1.0), tree_domains=D)
+    fs = H.hlq_factor_ex(dA, N, nb, O.CRIT_MAX, 1.0, tree_domains=D, **hint_kwargs(fo))
     np.testing.assert_array_equal(fs.decisions(), f.decisions())
     assert O.factor_diff(F, H.from_colmajor(dA)) <= 1e-13
 
@@ -171,8 +175,8 @@ def test_nccl_grid_single_rank(H):
     uid = H.nccl_unique_id()
     grid = H.grid_nccl(uid, 1, 0, 1, 1)
     dA = H.to_colmajor(A)
-    f = H.hlq_factor_dist(grid, [dA], N, nb, O.CRIT_MAX, 1.2e4, ref_dec=fo.dec,
-                          ref_margin=np.nan_to_num(fo.margin, nan=1.0), tree_domains=2)
+    f = H.hlq_factor_dist(grid, [dA], N, nb, O.CRIT_MAX, 1.2e4, tree_domains=2,
+                          **hint_kwargs(fo))
     db = torch.from_numpy(b).cuda()
     x = f.solve(db).cpu().numpy()
     check(fo, f, H.from_colmajor(dA), x, A, b)

@@ -643,3 +643,59 @@ def test_domain_pivoting_mixed_run_solves_and_raises_lu_likelihood():
         fd = O.hybrid_factor(A, nb, O.CRIT_MAX, alpha, D=2, pivot_scope="domain")
         assert np.sum(fd.dec == O.LU) >= np.sum(ft.dec == O.LU)
         assert O.hpl3(A, O.solve(fd, b), b) <= 16.0
+
+
+def test_margin_hand_values():
+    """ledger 21: margin = (lhs - rhs) / max(lhs, rhs).  Hand cases at nb = 1 (no rounding in the
+    tile LU): lhs / rhs = 3 / 2 -> +1/3 (a /min or /(lhs+rhs) denominator would give 1/2 or 1/5),
+    2 / 3 -> -1/3; MUMPS pivot 4, away 3, alpha 2.1 -> (8.4 - 3) / 8.4."""
+    f = O.hybrid_factor(np.asfortranarray([[3.0, 0.0], [2.0, 1.0]]), 1, O.CRIT_MAX, 1.0)
+    assert f.dec[0] == O.LU and f.margin[0] == pytest.approx(1.0 / 3.0, abs=1e-15)
+    f = O.hybrid_factor(np.asfortranarray([[2.0, 0.0], [3.0, 1.0]]), 1, O.CRIT_MAX, 1.0)
+    assert f.dec[0] == O.QR and f.margin[0] == pytest.approx(-1.0 / 3.0, abs=1e-15)
+    # Sum: below {2, 2} against 3 -> rhs 4: (3 - 4) / 4
+    A = np.asfortranarray([[3.0, 0.0, 0.0], [2.0, 1.0, 0.0], [2.0, 0.0, 1.0]])
+    f = O.hybrid_factor(A, 1, O.CRIT_SUM, 1.0)
+    assert f.dec[0] == O.QR and f.margin[0] == pytest.approx(-0.25, abs=1e-15)
+    A = np.asfortranarray([[4.0, 0.0, 0.0], [1.0, 1.0, 0.0], [3.0, 0.0, 1.0]])
+    f = O.hybrid_factor(A, 1, O.CRIT_MUMPS, 2.1)
+    assert f.dec[0] == O.LU and f.margin[0] == pytest.approx((8.4 - 3.0) / 8.4, abs=1e-15)
+
+
+def test_mumps_m1_m2_hand_case_nb2():
+    """MUMPS readings on a 2 x 2 diagonal tile (worked by hand).  A_kk = [[2, 1], [1, 3]]: no swap,
+    U = [[2, 1], [0, 2.5]], pivots (2, 2.5); local_max = (2, 3); growth_factor = (1, 2.5/3).
+    Below: [[1, 4], [0.5, 1]] -> away_max = (1, 4).  alpha = 1.5 -> alpha*pivot = (3, 3.75).
+    M1: estimate = away * own growth = (1, 4*2.5/3 = 10/3): 3 >= 1, 3.75 >= 10/3 -> LU,
+        margin = min(2/3, (3.75 - 10/3)/3.75 = 1/9).
+    M2: estimate(j) = away(j) * prod_{i<j} growth(i) = (1, 4*1 = 4): 3.75 < 4 -> QR,
+        margin = min(2/3, (3.75 - 4)/4 = -1/16)."""
+    A = np.zeros((4, 4))
+    A[0:2, 0:2] = [[2.0, 1.0], [1.0, 3.0]]
+    A[2:4, 0:2] = [[1.0, 4.0], [0.5, 1.0]]
+    A[2:4, 2:4] = np.eye(2)
+    A = np.asfortranarray(A)
+    f1 = O.hybrid_factor(A, 2, O.CRIT_MUMPS, 1.5, mumps_reading=0)
+    assert f1.dec[0] == O.LU and f1.margin[0] == pytest.approx(1.0 / 9.0, abs=1e-14)
+    f2 = O.hybrid_factor(A, 2, O.CRIT_MUMPS, 1.5, mumps_reading=1)
+    assert f2.dec[0] == O.QR and f2.margin[0] == pytest.approx(-1.0 / 16.0, abs=1e-14)
+
+
+def test_noise_floor_variant_same_mathematics():
+    """variant = 1 (reversed K-chunk Schur sums, the delta_floor run) computes the same
+    factorization up to rounding: decisions and pivots identical, factors within a few ulps of
+    growth-scaled noise, and not bit-identical (the summation order really differs)."""
+    A = I.uniform_matrix(3, 512)
+    forced = np.zeros(8, dtype=np.uint8)
+    f0 = O.hybrid_factor(A, 64, forced=forced)
+    f1 = O.hybrid_factor(A, 64, forced=forced, variant=1)
+    for k in f0.ipiv:
+        np.testing.assert_array_equal(f0.ipiv[k], f1.ipiv[k])
+    d = O.factor_diff(f1.A, f0.A)
+    assert 0.0 < d < 1e-9
+    for scope, lu in (("domain", "A1"), ("tile", "A2")):
+        g0 = O.hybrid_factor(A + 2 * np.eye(512), 64, forced=forced, D=2, pivot_scope=scope,
+                             lu_variant=lu)
+        g1 = O.hybrid_factor(A + 2 * np.eye(512), 64, forced=forced, D=2, pivot_scope=scope,
+                             lu_variant=lu, variant=1)
+        assert 0.0 < O.factor_diff(g1.A, g0.A) < 1e-11
