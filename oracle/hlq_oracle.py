@@ -185,11 +185,14 @@ def lu_step_domain(A: np.ndarray, N: int, nb: int, k: int, D: int, Wst: np.ndarr
                 ri = tsl(N, nb, i)
                 A[ri, k0:k1] = solve_triangular(U, A[ri, k0:k1].T, trans="T", lower=False,
                                                 check_finite=False).T
-    # Swap: the domain's row interchanges on the trailing columns (columns > k only, reading 23)
+    # Swap: the domain's row interchanges on the trailing columns (columns > k only, reading 23),
+    # the sequential swaps applied to an index vector, then one gather of the rows
+    src = np.arange(len(G))
     for c in range(b):
         p = int(ipiv[c])
         if p != c:
-            A[[G[c], G[p]], k1:N] = A[[G[p], G[c]], k1:N]
+            src[[c, p]] = src[[p, c]]
+    A[G, k1:N] = A[G[src], k1:N]
     # Apply: A_kj <- L_11^-1 A_kj
     with np.errstate(all="ignore"):
         A[k0:k1, k1:N] = solve_triangular(L, A[k0:k1, k1:N], lower=True, unit_diagonal=True,
@@ -359,16 +362,20 @@ def criterion_mumps(alpha: float, W: np.ndarray, local_max: np.ndarray, away_max
 def schur_update(A: np.ndarray, N: int, k0: int, k1: int, variant: int = 0):
     """Update: A_ij <- A_ij - A_ik A_kj for all i, j > k, as one rank-b product.
     variant = 1 is the noise-floor variant (BASELINE "reversed inner-product order"): the same
-    product summed over 4 K-chunks in reverse order -- same mathematics, different rounding."""
+    product summed over 4 K-chunks in reverse order -- same mathematics, different rounding.
+    The product is formed as (A_kj^T A_ik^T)^T so that it comes out in A's column-major order
+    (a layout choice only: subtracting a row-major temporary from a column-major view of a large
+    matrix is memory-order bound)."""
+    def prod(lo, hi):
+        return (A[lo:hi, k1:N].T @ A[k1:N, lo:hi].T).T
     with np.errstate(all="ignore"):
         if variant == 0:
-            A[k1:N, k1:N] -= A[k1:N, k0:k1] @ A[k0:k1, k1:N]
+            A[k1:N, k1:N] -= prod(k0, k1)
             return
         edges = np.linspace(k0, k1, 5).astype(int)
-        acc = np.zeros((N - k1, N - k1))
+        acc = np.zeros((N - k1, N - k1), order="F")
         for c in reversed(range(4)):
-            lo, hi = edges[c], edges[c + 1]
-            acc += A[k1:N, lo:hi] @ A[lo:hi, k1:N]
+            acc += prod(edges[c], edges[c + 1])
         A[k1:N, k1:N] -= acc
 
 
@@ -389,11 +396,13 @@ def lu_step(A: np.ndarray, N: int, nb: int, k: int, W: np.ndarray, ipiv: np.ndar
         A[k1:N, k0:k1] = solve_triangular(U, A[k1:N, k0:k1].T, trans="T", lower=False,
                                           check_finite=False).T
     # Apply: A_kj <- L_kk^-1 P_kk A_kj for j > k  (ledger 12, ledger 23: columns > k only)
-    C = A[k0:k1, k1:N]
+    # (the sequential swaps applied to an index vector, then one gather of the rows)
+    src = np.arange(b)
     for c in range(b):
         p = int(ipiv[c])
         if p != c:
-            C[[c, p], :] = C[[p, c], :]
+            src[[c, p]] = src[[p, c]]
+    C = A[k0:k1, k1:N][src, :]
     with np.errstate(all="ignore"):
         A[k0:k1, k1:N] = solve_triangular(L, C, lower=True, unit_diagonal=True, check_finite=False)
     # Update: A_ij <- A_ij - A_ik A_kj for i, j > k

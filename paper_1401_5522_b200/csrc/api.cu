@@ -282,8 +282,8 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
          oSc1 = take(sizeof(double) * scr), oWp = take(sizeof(double) * (size_t)N * nb),
          oWr = take(sizeof(double) * (size_t)N * nb),
          oCp = take(fuse_growth_any ? sizeof(double) * (size_t)((N + cpr - 1) / cpr) * N : 8),
-         oLi = take(sizeof(double) * (size_t)n * 2 * nb * nb),
-         oLp = take(sizeof(int) * (size_t)n * nb), oSt2 = take(sizeof(double) * (size_t)nb);
+         oLi = take(opt.lu_variant == HLQ_LU_A2 ? sizeof(double) * (size_t)n * 2 * nb * nb : 8),
+         oLp = take(opt.lu_variant == HLQ_LU_A2 ? sizeof(int) * (size_t)n * nb : 8), oSt2 = take(sizeof(double) * (size_t)nb);
   const bool dpiv = opt.pivot_scope == HLQ_PIVOT_DOMAIN;
   // speculative QR panel: with a criterion to evaluate, the QR branch's panel (GEQRT of every tile +
   // every TTQRT level) runs on a copy of the panel beside the speculative LU and the criterion, and
@@ -482,12 +482,14 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
       // the domain's stacked LU replaces its panel tiles (after the Eliminate GEMM, which also
       // wrote them: U_kk^-1 applies to the tiles off the domain only)
       if (dpiv) launch_dom_commit(A, g, k, Dp, wk, sp);
-      // keep L_kk^-1, U_kk^-1 and the composed permutation for the solve (LU steps only)
-      launch_copy_block(w.luinv + (size_t)k * 2 * nb * nb, nb, wk.scratch, nb, nb, 2 * nb, nullptr,
-                        w.dec, k, sp);
-      launch_copy_ints(w.luperm + (size_t)k * nb,
-                       reinterpret_cast<const int*>(wk.scratch + (size_t)2 * nb * nb), nb, w.dec, k,
-                       sp);
+      if (a2) {
+        // A2: keep Q_kk^T (and the identity permutation) for the solve's forward pass
+        launch_copy_block(w.luinv + (size_t)k * 2 * nb * nb, nb, wk.scratch, nb, nb, nb, nullptr,
+                          w.dec, k, sp);
+        launch_copy_ints(w.luperm + (size_t)k * nb,
+                         reinterpret_cast<const int*>(wk.scratch + (size_t)2 * nb * nb), nb, w.dec,
+                         k, sp);
+      }
       P.end(sp);
     }
     if (spec) {
@@ -514,7 +516,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
         if (known != HLQ_DEC_QR) {
           P.begin(HLQ_PROF_LU_UPDATE, st);
           if (dpiv) launch_dom_swap_cols(A, g, k, Dp, w.dipiv + (size_t)k * nb, c0, c1, w.dec, st);
-          launch_lu_update(A, g, k, wk, c0, c1, fuse ? w.colpart : nullptr, st);
+          launch_lu_update(A, g, k, wk, c0, c1, fuse ? w.colpart : nullptr, st, a2);
           P.end(st);
         }
         bool qr_fused = false;
@@ -607,24 +609,24 @@ int hlq_solve(hlq_factors_t f, const double* b, double* x) {
   if (x != b &&
       (rc = cuda_err(cudaMemcpyAsync(x, b, sizeof(double) * g.N, cudaMemcpyDeviceToDevice, st))))
     return rc;
+  // forward pass: replay every step on x (LU: P_kk, L_kk^-1 by substitution, x_i -= L_ik x_k;
+  // A2: Q_kk^T; QR: the stored reflectors of the tree), then block back substitution with U_kk /
+  // R_kk (substitution inside the tile, GEMV with the row tiles)
   for (int k = 0; k < g.n; ++k) {
     if (f->dec[k] == HLQ_DEC_LU && f->pivot_scope == HLQ_PIVOT_DOMAIN)
       launch_dom_swap_vec(x, g, k, f->D, f->w.dipiv + (size_t)k * g.nb, st);
-    if (f->dec[k] == HLQ_DEC_LU)
+    if (f->dec[k] == HLQ_DEC_LU && f->lu_variant == HLQ_LU_A2)
       launch_solve_lu_fwd_inv(f->A, g, k, f->w.luinv + (size_t)k * 2 * g.nb * g.nb,
                               f->w.luperm + (size_t)k * g.nb, x, f->w.solve_t, st,
-                              /*dense=*/f->lu_variant == HLQ_LU_A2);
+                              /*dense=*/true);
+    else if (f->dec[k] == HLQ_DEC_LU)
+      launch_solve_lu_fwd(f->A, g, k,
+                          f->pivot_scope == HLQ_PIVOT_DOMAIN ? nullptr : f->w.ipiv, x, st);
     else
       launch_qr_apply(f->A, g, k, f->ib, f->w.Tg, f->w.Ttt, f->lvl_ptr[k].data(),
                       f->lvl_cnt[k].data(), (int)f->lvl_cnt[k].size(), x, g.N, 1, nullptr, st);
   }
-  for (int k = g.n - 1; k >= 0; --k) {
-    if (f->dec[k] == HLQ_DEC_LU)
-      launch_solve_back_inv(f->A, g, k, f->w.luinv + ((size_t)k * 2 + 1) * g.nb * g.nb, x,
-                            f->w.solve_t, st);
-    else
-      launch_solve_back(f->A, g, k, x, st);
-  }
+  for (int k = g.n - 1; k >= 0; --k) launch_solve_back(f->A, g, k, x, st);
   f->prof.end(st);
   if ((rc = cuda_err(cudaGetLastError()))) return rc;
   if (f->blocking && (rc = cuda_err(cudaStreamSynchronize(st)))) return rc;

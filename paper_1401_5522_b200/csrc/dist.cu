@@ -853,21 +853,16 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
       launch_decide(gglob, k, crit, alpha, opt.mumps_reading, opt.tie_rel_tol, has_forced ? 1 : 0,
                     has_ref ? 1 : 0, w, s);
       PR.end(s);
-      double* Li = w.scratch;
-      double* Ui = w.scratch + (size_t)nb * nb;
       int* perm = reinterpret_cast<int*>(w.scratch + (size_t)2 * nb * nb);
       if (known != HLQ_DEC_QR) {
         PR.begin(HLQ_PROF_LU_TRSM, s);
-        if (!sp_.diag) launch_tri_inv(gglob, k, w, Li, Ui, s);
         if (sp_.diag)
           launch_lu_commit(Apan, gP, 0, w.W, w.ipiv_ws, c.ipiv + (int64_t)k * nb, perm, dk, s);
         const int64_t r0 = sp_.diag ? bk : 0;
         const int64_t M = gP.N - r0;
-        if (M > 0) {
-          launch_copy_block(w.ws_panel, M, Apan + r0, c.lld, M, bk, nullptr, dk, 0, s);
-          launch_dgemm(Apan + r0, c.lld, w.ws_panel, M, Ui, nb, M, bk, bk, false, false, dk, 0,
-                       HLQ_DEC_LU, s);
-        }
+        // Eliminate with U_kk from the gathered speculative LU W (blocked substitution, trsm.cu)
+        if (M > 0)
+          launch_trsm_eliminate(Apan, c.lld, r0, 0, M, bk, w.W, nb, dk, 0, HLQ_DEC_LU, s);
         PR.end(s);
       }
       if (known != HLQ_DEC_LU && sp_.ms > 0) {
@@ -943,7 +938,8 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
                         c.Ttt + ((int64_t)lk * c.mt + sp_.li0) * ib * nb,
                         sizeof(double) * sp_.ms * ib * nb, cudaMemcpyDeviceToDevice, s);
       }
-      cudaMemcpyAsync(pk_ + ds.off_Li(prow, sp_.ms), w.scratch, sizeof(double) * nb * nb,
+      // the package's L slot carries W (L_kk \\ U_kk): the row ranks' Apply solves with L_kk
+      cudaMemcpyAsync(pk_ + ds.off_Li(prow, sp_.ms), w.W, sizeof(double) * nb * nb,
                       cudaMemcpyDeviceToDevice, s);
       ::hlq::g_launches++;
       k_meta_pack<<<1, 256, 0, s>>>(pk_ + ds.off_meta(prow, sp_.ms), w.dec, w.margin, w.flags,
@@ -1003,9 +999,8 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
       gK.Nc = bk;
       if (known != HLQ_DEC_QR && sp_.diag) {
         PR.begin(HLQ_PROF_LU_UPDATE, s);
-        launch_copy_block(w.ws_row + co * bk, bk, base, c.lld, bk, ncl, perm, dk, 0, s);
-        launch_dgemm(base, c.lld, pk_ + ds.off_Li(prow, sp_.ms), nb, w.ws_row + co * bk, bk, bk,
-                     ncl, bk, false, false, dk, 0, HLQ_DEC_LU, s);
+        launch_trsm_apply(base, c.lld, 0, 0, ncl, bk, pk_ + ds.off_Li(prow, sp_.ms), nb, perm, dk,
+                          0, HLQ_DEC_LU, s);
         PR.end(s);
       }
       if (known != HLQ_DEC_LU && sp_.ms > 0) {

@@ -145,8 +145,19 @@ void launch_decide(Geo g, int k, int crit, double alpha, int mumps_reading, doub
 // commit = false (A2): A_kk already holds its factors in place; only the Eliminate GEMM runs
 void launch_lu_panel(double* A, Geo g, int k, const DevWork& w, cudaStream_t st,
                      bool commit = true);
+// a2: LU variant A2 (Apply = Q_kk^T GEMM); otherwise the unit-lower triangular solve
 void launch_lu_update(double* A, Geo g, int k, const DevWork& w, int64_t c0, int64_t c1,
-                      double* colpart, cudaStream_t st);
+                      double* colpart, cudaStream_t st, bool a2 = false);
+// trsm.cu: blocked triangular solves (DMMA off-diagonal blocks, substitution on 32 x 32 diagonal
+// blocks), in place, predicated on dec[k] == want.  Eliminate: A[r0:r0+M, c0:c0+bk] <- X U^-1,
+// U = upper triangle of W (ld ldw).  Apply: A[r0:r0+bk, c0:c0+nc] <- L^-1 P X, L = unit lower
+// triangle of W, row r of P X = row perm[r] of X.
+void launch_trsm_eliminate(double* A, int64_t lda, int64_t r0, int64_t c0, int64_t M, int bk,
+                           const double* W, int ldw, const uint8_t* dec, int k, int want,
+                           cudaStream_t st);
+void launch_trsm_apply(double* A, int64_t lda, int64_t r0, int64_t c0, int64_t nc, int bk,
+                       const double* W, int ldw, const int* perm, const uint8_t* dec, int k,
+                       int want, cudaStream_t st);
 void launch_lu_growth(const DevWork& w, Geo g, int k, cudaStream_t st);
 void launch_gemm_sub(double* C, int64_t ldc, const double* Am, int64_t lda, const double* Bm,
                      int64_t ldb, int64_t M, int64_t Nc, int K, const uint8_t* dec, int k,

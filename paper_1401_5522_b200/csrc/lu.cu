@@ -4,8 +4,10 @@
 //   a6  apply: A_kj <- L_kk^-1 P_kk A_kj for all j > k                 Apply
 //   a7  update: A_ij <- A_ij - A_ik A_kj for all i, j > k              Update
 // With the LAPACK layout the i (j) loops are one strided column (row) block, so Eliminate and Apply
-// are two GEMMs with the explicit triangular inverses from getrf.cu and Update is one rank-b GEMM.
-// The swaps touch the columns right of the diagonal tile only (reading 23).
+// are two blocked triangular solves (trsm.cu: DMMA off-diagonal updates + substitution in 32 x 32
+// diagonal blocks) and Update is one rank-b GEMM.  The swaps touch the columns right of the
+// diagonal tile only (reading 23).  LU variant A2 applies Q_kk^T (an orthogonal matrix,
+// formed explicitly by getrf.cu) with a GEMM.
 #include "hlq_internal.cuh"
 
 namespace hlq {
@@ -109,21 +111,18 @@ void launch_lu_panel(double* A, Geo g, int k, const DevWork& w, cudaStream_t st,
   const int64_t k0 = g.r0(k), k1 = k0 + bk;
   const int64_t M = g.N - k1;  // rows below the diagonal tile
   const uint8_t* dec = w.dec;
-  const double* Ui = w.scratch + (size_t)g.nb * g.nb;
   int* perm = reinterpret_cast<int*>(w.scratch + (size_t)2 * g.nb * g.nb);
   if (commit) { ::hlq::g_launches++; k_lu_commit<<<8, 256, 0, st>>>(A, g, k, w.W, w.ipiv_ws, w.ipiv, perm, dec); }
   if (M <= 0) return;
-  // Eliminate: X = A[k1:N, k0:k1]; A[k1:N, k0:k1] = X * U^-1
-  { ::hlq::g_launches++; k_copy_block<<<grid_for(M * bk), 256, 0, st>>>(w.ws_panel, M, A + k0 * g.lda + k1, g.lda, M, bk, nullptr, dec, k); }
-  launch_dgemm(A + k0 * g.lda + k1, g.lda, w.ws_panel, M, Ui, g.nb, M, bk, bk, false, false, dec,
-               k, HLQ_DEC_LU, st);
+  // Eliminate: A[k1:N, k0:k1] <- A[k1:N, k0:k1] U^-1 (U: upper triangle of W; A2: R), in place
+  launch_trsm_eliminate(A, g.lda, k1, k0, M, bk, w.W, g.nb, dec, k, HLQ_DEC_LU, st);
 }
 
 // Update stage of an LU step on the trailing columns [c0, c1) (absolute column indices >= k1):
 // Apply (SWPTRSM on row block k) + Update (DGEMM on all trailing rows).  colpart != nullptr fuses
 // the a12 column sums into the GEMM epilogue (leading dimension ldp = N - k1, column offset c0-k1).
 void launch_lu_update(double* A, Geo g, int k, const DevWork& w, int64_t c0, int64_t c1,
-                      double* colpart, cudaStream_t st) {
+                      double* colpart, cudaStream_t st, bool a2) {
   const int bk = g.bs(k);
   const int64_t k0 = g.r0(k), k1 = k0 + bk;
   const int64_t M = g.N - k1;
@@ -132,11 +131,16 @@ void launch_lu_update(double* A, Geo g, int k, const DevWork& w, int64_t c0, int
   const uint8_t* dec = w.dec;
   const double* Li = w.scratch;
   const int* perm = reinterpret_cast<const int*>(w.scratch + (size_t)2 * g.nb * g.nb);
-  double* ws = w.ws_row + (c0 - k1) * bk;  // disjoint per column range
-  // Apply: Y = P A[k0:k1, c0:c1]; A[k0:k1, c0:c1] = L^-1 * Y
-  { ::hlq::g_launches++; k_copy_block<<<grid_for(nc * bk), 256, 0, st>>>(ws, bk, A + c0 * g.lda + k0, g.lda, bk, nc, perm, dec, k); }
-  launch_dgemm(A + c0 * g.lda + k0, g.lda, Li, g.nb, ws, bk, bk, nc, bk, false, false, dec, k,
-               HLQ_DEC_LU, st);
+  if (a2) {
+    // A2 Apply: A[k0:k1, c0:c1] <- Q_kk^T A[k0:k1, c0:c1] (Li slot = Q^T, perm = identity)
+    double* ws = w.ws_row + (c0 - k1) * bk;  // disjoint per column range
+    { ::hlq::g_launches++; k_copy_block<<<grid_for(nc * bk), 256, 0, st>>>(ws, bk, A + c0 * g.lda + k0, g.lda, bk, nc, perm, dec, k); }
+    launch_dgemm(A + c0 * g.lda + k0, g.lda, Li, g.nb, ws, bk, bk, nc, bk, false, false, dec, k,
+                 HLQ_DEC_LU, st);
+  } else {
+    // Apply: A[k0:k1, c0:c1] <- L^-1 P A[k0:k1, c0:c1] (L: unit lower triangle of W), in place
+    launch_trsm_apply(A, g.lda, k0, c0, nc, bk, w.W, g.nb, perm, dec, k, HLQ_DEC_LU, st);
+  }
   // Update: A[k1:N, c0:c1] -= A[k1:N, k0:k1] * A[k0:k1, c0:c1]
   launch_dgemm(A + c0 * g.lda + k1, g.lda, A + k0 * g.lda + k1, g.lda, A + c0 * g.lda + k0, g.lda,
                M, nc, bk, true, true, dec, k, HLQ_DEC_LU, st,

@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(256) k_solve_lu_diag(const double* __restrict_
   const int tid = threadIdx.x;
   for (int r = tid; r < bk; r += 256) xs[r] = xk[r];
   __syncthreads();
-  if (tid == 0)
+  if (tid == 0 && ipiv != nullptr)
     for (int c = 0; c < bk; ++c) {
       int p = ipiv[(int64_t)k * g.nb + c];
       if (p != c) {

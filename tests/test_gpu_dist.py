@@ -32,7 +32,13 @@ def run_dist(H, A, b, nb, P, Q, crit=O.CRIT_MAX, alpha=1.0, D=None, forced=None,
     N = A.shape[0]
     D = P if D is None else D
     if fo is None:
-        fo = O.hybrid_factor(A, nb, crit, alpha, D=D, forced=forced)
+        pre = {}
+
+        def hook(k, Ab, Aa, d):
+            sl = O.tsl(N, nb, k)
+            pre[k] = Ab[sl, sl].copy()
+        fo = O.hybrid_factor(A, nb, crit, alpha, D=D, forced=forced, on_step=hook)
+        fo.pre_tiles = pre
     grid = H.grid_local(P, Q)
     locs = []
     for (p, q) in grid.ranks():
@@ -57,9 +63,9 @@ def run_dist(H, A, b, nb, P, Q, crit=O.CRIT_MAX, alpha=1.0, D=None, forced=None,
 
 def check(fo, f, F, x, A, b, tol=1e-10):
     np.testing.assert_array_equal(f.decisions(), fo.dec)
-    check_decision_record(fo, f, getattr(fo, "hinted_run", False),
-                          forced=getattr(fo, "forced_run", False))
     diff = O.factor_diff(F, fo.A)
+    check_decision_record(fo, f, getattr(fo, "hinted_run", False),
+                          forced=getattr(fo, "forced_run", False), diff=diff)
     assert diff <= tol, f"factor diff {diff:.3e}"
     assert f.growth() == pytest.approx(fo.growth, rel=1e-10)
     h3 = O.hpl3(A, x, b)

@@ -117,7 +117,7 @@ def test_fuzz_criteria_against_oracle(t, N, nb, crit, alpha, gen, variant, scope
         A, b = I.uniform_matrix(300 + t, N), I.uniform_rhs(300 + t, N)
     fo, fg, F, x = run_pair(H, A, b, nb, crit, alpha, D=D, lu_variant=variant, pivot_scope=scope)
     np.testing.assert_array_equal(fg.decisions(), fo.dec)
-    check_decision_record(fo, fg, fo.hinted_run)
+    check_decision_record(fo, fg, fo.hinted_run, diff=O.factor_diff(F, fo.A))
     h_o = O.hpl3(A, O.solve(fo, b), b)
     h_g = O.hpl3(A, x, b)
     if h_o <= 16.0:
