@@ -18,8 +18,8 @@ in DESIGN.md "Readings" and cited at its use below as "ledger <n>".
 
 Pins (tests/test_oracle_pins.py, -m "not gpu"): every public function is pinned to something other
 than itself -- scipy/numpy library routines, closed forms, the paper's worked example
-and bounds, brute force on 2x2/3x3-tile matrices.  parity unpinned: the MUMPS M2
-reading (`mumps_reading=1`) beyond its nb=1 hand values, see DESIGN.md.
+and bounds, brute force on 2x2/3x3-tile matrices.  The MUMPS M2 reading
+(`mumps_reading=1`) is pinned only by hand values (nb=1; nb=2), see DESIGN.md.
 """
 from __future__ import annotations
 
@@ -473,6 +473,12 @@ def _unit_lower(Tile, i0, j1):
     return V
 
 
+def _fmm(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """The product a @ b, returned in column-major (Fortran) order: formed as (b^T a^T)^T, so that
+    updates of column-major row blocks of A are not memory-order bound (a layout choice only)."""
+    return (b.T @ a.T).T
+
+
 def unmqr(Vtile: np.ndarray, T: np.ndarray, ib: int, C: np.ndarray):
     """UNMQR: C <- Q^T C with Q from a GEQRT tile; blocks applied in order 0,1,..."""
     mrow, b = Vtile.shape
@@ -481,7 +487,7 @@ def unmqr(Vtile: np.ndarray, T: np.ndarray, ib: int, C: np.ndarray):
         V = _unit_lower(Vtile, i0, i0 + sb)
         Tb = np.triu(T[0:sb, i0:i0 + sb])
         Cb = C[i0:, :]
-        C[i0:, :] = Cb - V @ (Tb.T @ (V.T @ Cb))
+        C[i0:, :] = Cb - _fmm(V, _fmm(Tb.T, _fmm(V.T, Cb)))
 
 
 def tsqrt(R: np.ndarray, A2: np.ndarray, ib: int, tt: bool = False):
@@ -533,9 +539,9 @@ def tsmqr(V2: np.ndarray, T: np.ndarray, ib: int, C1: np.ndarray, C2: np.ndarray
         sb = min(ib, b - i0)
         Vb = Vfull[:, i0:i0 + sb]
         Tb = np.triu(T[0:sb, i0:i0 + sb])
-        Wm = Tb.T @ (C1[i0:i0 + sb, :] + Vb.T @ C2)
+        Wm = _fmm(Tb.T, C1[i0:i0 + sb, :] + _fmm(Vb.T, C2))
         C1[i0:i0 + sb, :] -= Wm
-        C2 -= Vb @ Wm
+        C2 -= _fmm(Vb, Wm)
 
 
 # ----------------------------------------------------------------------------------------------
@@ -644,23 +650,54 @@ class QRStepData:
     T_tt: dict = field(default_factory=dict)     # row i -> T of TTQRT(A_e,k ; A_ik)
 
 
+QR_COLS = 1024
+_POOL = None
+
+
+def _pmap(fn, items):
+    """Run fn over INDEPENDENT work items (disjoint tiles / column chunks) on the host's cores:
+    every item is computed exactly as in a sequential loop, only concurrently (numpy releases the
+    GIL in its array operations); BLAS runs single-threaded inside the items."""
+    global _POOL
+    items = list(items)
+    if len(items) <= 1:
+        return [fn(it) for it in items]
+    if _POOL is None:
+        import os
+        from concurrent.futures import ThreadPoolExecutor
+        try:
+            nthr = len(os.sched_getaffinity(0))
+        except Exception:
+            nthr = os.cpu_count() or 1
+        _POOL = ThreadPoolExecutor(max_workers=int(os.environ.get("HLQ_ORACLE_THREADS", nthr)))
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):
+        return list(_POOL.map(fn, items))
+
+
 def qr_step(A: np.ndarray, N: int, nb: int, k: int, D: int, ib: int,
             tree: str = "greedy", T_kk=None) -> QRStepData:
     """T_kk: the diagonal tile was already factored in place by GEQRT (LU variant A2: "the
-    factorization of A_kk is not discarded but rather used to continue the QR step")."""
+    factorization of A_kk is not discarded but rather used to continue the QR step").
+
+    Independent work runs concurrently (_pmap): the GEQRTs of the tiles, the pairs of one TT level
+    (disjoint rows), and the column chunks of one trailing update -- Q^T acts on every column
+    independently, so applying it chunk by chunk is the same computation."""
     n = ntiles(N, nb)
     ck = tsl(N, nb, k)
-    right = slice(ck.stop, N)
+    chunks = [slice(c, min(c + QR_COLS, N)) for c in range(ck.stop, N, QR_COLS)]
     data = QRStepData()
     geqrt_rows, ts_list, tt_levels = qr_plan(k, n, D, tree)
     # GEQRT + UNMQR (Alg. 4a lines 1, 4; Alg. 4b lines 1-2, 4-5); rows are independent
-    for h in geqrt_rows:
+    def factor_row(h):
         rh = tsl(N, nb, h)
-        tile = A[rh, ck]
-        data.T_geqrt[h] = T_kk if (h == k and T_kk is not None) else geqrt(tile, ib)
-        if right.start < N:
-            unmqr(tile, data.T_geqrt[h], ib, A[rh, right])
-    # TS eliminations in plan order (Alg. 4a lines 2, 5)
+        return T_kk if (h == k and T_kk is not None) else geqrt(A[rh, ck], ib)
+    for h, T in zip(geqrt_rows, _pmap(factor_row, geqrt_rows)):
+        data.T_geqrt[h] = T
+    _pmap(lambda hc: unmqr(A[tsl(N, nb, hc[0]), ck], data.T_geqrt[hc[0]], ib,
+                           A[tsl(N, nb, hc[0]), hc[1]]),
+          [(h, cs) for h in geqrt_rows for cs in chunks])
+    # TS eliminations in plan order (Alg. 4a lines 2, 5): sequential along the chain
     for e, i in ts_list:
         re_, ri = tsl(N, nb, e), tsl(N, nb, i)
         R = A[re_, ck]
@@ -669,20 +706,23 @@ def qr_step(A: np.ndarray, N: int, nb: int, k: int, D: int, ib: int,
         data.T_ts[i] = tsqrt(Rv, A2, ib)
         iu = np.triu_indices(R.shape[0], m=R.shape[1])
         R[iu] = Rv[iu]
-        if right.start < N:
-            tsmqr(A2, data.T_ts[i], ib, A[re_, right], A[ri, right])
+        _pmap(lambda cs: tsmqr(A2, data.T_ts[i], ib, A[re_, cs], A[ri, cs]), chunks)
     # TT eliminations level by level (Alg. 4b lines 6-9); pairs inside a level are disjoint
+    def tt_factor(pair):
+        e, i = pair
+        re_, ri = tsl(N, nb, e), tsl(N, nb, i)
+        R = A[re_, ck]
+        Rv = np.triu(R)
+        T = tsqrt(Rv, A[ri, ck], ib, tt=True)
+        iu = np.triu_indices(R.shape[0], m=R.shape[1])
+        R[iu] = Rv[iu]
+        return T
     for level in tt_levels:
-        for e, i in level:
-            re_, ri = tsl(N, nb, e), tsl(N, nb, i)
-            R = A[re_, ck]
-            Rv = np.triu(R)
-            Ht = A[ri, ck]
-            data.T_tt[i] = tsqrt(Rv, Ht, ib, tt=True)
-            iu = np.triu_indices(R.shape[0], m=R.shape[1])
-            R[iu] = Rv[iu]
-            if right.start < N:
-                tsmqr(Ht, data.T_tt[i], ib, A[re_, right], A[ri, right], tt=True)
+        for (e, i), T in zip(level, _pmap(tt_factor, level)):
+            data.T_tt[i] = T
+        _pmap(lambda pc: tsmqr(A[tsl(N, nb, pc[1]), ck], data.T_tt[pc[1]], ib,
+                               A[tsl(N, nb, pc[0]), pc[2]], A[tsl(N, nb, pc[1]), pc[2]], tt=True),
+              [(e, i, cs) for e, i in level for cs in chunks])
     return data
 
 
