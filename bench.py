@@ -62,6 +62,8 @@ def parse():
                     help="LU step variant (A2: QR-factored diagonal tile, NEXT f4, P:373-397)")
     ap.add_argument("--pivot-scope", default="tile", choices=["tile", "domain"],
                     help="domain: diagonal-domain pivoting over the D domains (NEXT f1, P:271-285)")
+    ap.add_argument("--tree", default="greedy",
+                    help="QR elimination tree: greedy (default) or hqrA (TS groups of A tiles)")
     ap.add_argument("--domains", type=int, default=1,
                     help="single GPU: QR-tree / pivoting domains D (tile rows mod D)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -122,7 +124,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------ CPU oracle
-def cpu_oracle_step(config, N, nb, fqr, crit, alpha, domains=1):
+def cpu_oracle_step(config, N, nb, fqr, crit, alpha, domains=1, tree="greedy"):
     """One bounded oracle factor+solve of the config's own input recipe (hlq_inputs.config_system:
     the same generator as the GPU arm) at size N (test infrastructure; the bench's cpu_baseline
     leg and the reference arm)."""
@@ -132,10 +134,10 @@ def cpu_oracle_step(config, N, nb, fqr, crit, alpha, domains=1):
     n = (N + nb - 1) // nb
     t0 = time.perf_counter()
     if crit:
-        f = O.hybrid_factor(A, nb, CRIT[crit], alpha, D=domains, track_growth=True)
+        f = O.hybrid_factor(A, nb, CRIT[crit], alpha, D=domains, track_growth=True, tree=tree)
     else:
         f = O.hybrid_factor(A, nb, forced=I.bernoulli_pattern(30, n, fqr), D=domains,
-                            track_growth=True)
+                            track_growth=True, tree=tree)
     x = O.solve(f, b)
     dt = time.perf_counter() - t0
     return dt, f, O.hpl3(A, x, b)
@@ -156,11 +158,12 @@ def run_reference(args, cfg, rank):
     nb = cfg["nb"]
     fake = 2.0 / 3.0 * Ns ** 3
     for _ in range(args.warmup):
-        cpu_oracle_step(args.config, Ns, nb, args.fqr, args.criterion, args.alpha, args.domains)
+        cpu_oracle_step(args.config, Ns, nb, args.fqr, args.criterion, args.alpha, args.domains,
+                        args.tree)
     times = []
     for _ in range(args.steps):
         dt, f, h3 = cpu_oracle_step(args.config, Ns, nb, args.fqr, args.criterion, args.alpha,
-                                    args.domains)
+                                    args.domains, args.tree)
         times.append(dt)
     t = sum(times) / len(times)
     val = fake / t / 1e12
@@ -184,6 +187,12 @@ def run_reference(args, cfg, rank):
     print(json.dumps(out), flush=True)
 
 
+def tree_fields(args):
+    if args.tree == "greedy":
+        return {}
+    return {"tree": 1, "ts_group": int(args.tree[3:] or 4)}
+
+
 def grid_shape(world):
     return {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}.get(world, (1, world))
 
@@ -198,6 +207,8 @@ def workload_config(args, cfg):
         dec = f"forced Bernoulli pattern f_QR={args.fqr} (seed 30)"
     if args.lu_variant == "A2":
         dec += ", LU variant A2"
+    if args.tree != "greedy":
+        dec += f", QR tree {args.tree}"
     if args.pivot_scope == "domain":
         dec += f", diagonal-domain pivoting D={args.domains}"
     elif args.domains != 1:
@@ -290,7 +301,7 @@ def main():
                             lu_variant=H.LU_A2 if args.lu_variant == "A2" else H.LU_A1,
                             tree_domains=args.domains,
                             pivot_scope=H.PIVOT_DOMAIN if args.pivot_scope == "domain"
-                            else H.PIVOT_TILE)
+                            else H.PIVOT_TILE, **tree_fields(args))
         f.solve(b, x)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -385,6 +396,8 @@ def main():
         opt.lu_variant = H.LU_A2 if args.lu_variant == "A2" else H.LU_A1
         opt.tree_domains = args.domains
         opt.pivot_scope = H.PIVOT_DOMAIN if args.pivot_scope == "domain" else H.PIVOT_TILE
+        for key, v in tree_fields(args).items():
+            setattr(opt, key, v)
         fv = forced
         if fv is not None:
             fa = np.ascontiguousarray(fv, dtype=np.uint8)
@@ -407,7 +420,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         Ns = args.cpu_sample_N
         dt, fo, h3c = cpu_oracle_step(args.config, Ns, nb, args.fqr, args.criterion, args.alpha,
-                                      args.domains)
+                                      args.domains, args.tree)
         cpu_base = {"value": 2.0 / 3.0 * Ns ** 3 / dt / 1e12, "unit": "TFLOP/s",
                     "cores": cpu_threads(), "kind": "oracle", "N_sample": Ns,
                     "sample": f"one oracle factor+solve of the {args.config} recipe (same "

@@ -37,8 +37,11 @@ extern "C" {
 enum { HLQ_CRIT_MAX = 0, HLQ_CRIT_SUM = 1, HLQ_CRIT_MUMPS = 2 };
 /* decision of a step (Alg. 1 "Perform an LU step" / "Perform a QR step") */
 enum { HLQ_DEC_LU = 0, HLQ_DEC_QR = 1 };
-/* QR elimination tree (Alg. 3 + HQR trees P:358-364) */
-enum { HLQ_TREE_GREEDY = 0 };
+/* QR elimination tree (Alg. 3 + HQR trees P:296-305; readings 16
+ * and 34): GREEDY = every panel tile GEQRT'd, TT merges on the halving tree; HQR = square-tile TS
+ * eliminations inside groups of opt.ts_group consecutive tiles of a domain, then the halving tree
+ * over the group heads and over the domain heads */
+enum { HLQ_TREE_GREEDY = 0, HLQ_TREE_HQR = 1 };
 
 /* error / status codes */
 enum {
@@ -69,7 +72,7 @@ typedef struct {
   int32_t ib;                /* inner block of the stored Householder T factors: 32 (0 -> 32;
                                 any other value is rejected with -6)                              */
   int32_t tree_domains;      /* D: QR-tree domains = tile rows mod D (0 -> 1 on one GPU)         */
-  int32_t tree;              /* HLQ_TREE_GREEDY                                                  */
+  int32_t tree;              /* HLQ_TREE_GREEDY (default) or HLQ_TREE_HQR (one GPU)              */
   int32_t mumps_reading;     /* 0 = M1 (default, reading 1), 1 = M2                    */
   const uint8_t* forced;     /* host, n entries or NULL: decision vector used verbatim (C3)      */
   const uint8_t* ref_dec;    /* host, n entries or NULL: reference (oracle) decisions            */
@@ -96,6 +99,7 @@ typedef struct {
                                 rows of the trailing columns, keeps the domain's L from the stacked
                                 LU and eliminates the other tiles with U_kk.  tree_domains = 1 makes
                                 every step LU with partial pivoting (LUPP).  A1 variant, one GPU. */
+  int32_t ts_group;          /* HLQ_TREE_HQR: tiles per TS group (0 -> 4); 1 = the greedy tree   */
 } hlq_options;
 
 enum { HLQ_LU_A1 = 0, HLQ_LU_A2 = 1 };

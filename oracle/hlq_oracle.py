@@ -621,6 +621,12 @@ def qr_plan(k: int, n: int, D: int, tree: str = "greedy"):
       (GEQRT) and the rows of each domain are merged by the halving tree; the domain heads are then
       merged by the same halving tree (the inter-domain level).  Critical path O(log m).
     tree="flat": flat TS inside each domain onto its head, then flat TT of the heads onto k.
+    tree="hqrA" (A >= 1, e.g. "hqr4"; reading 34): the two-level HQR tree of P:296-305 and
+      P:358-364 with square-tile (TS) eliminations at the low level: the rows of each domain are cut
+      into consecutive groups of A tiles; inside a group the first tile (the group head, GEQRT) kills
+      the others one after another with TSQRT ("square" tiles); the group heads of a
+      domain are then merged by the halving tree (TT, "triangular" tiles) and the domain heads by
+      the same halving tree.  A = 1 is the greedy tree; A >= m+1 with D = 1 is the flat TS tree.
     """
     doms = _domains(k, n, D)
     heads = [dm[0] for dm in doms]
@@ -628,7 +634,17 @@ def qr_plan(k: int, n: int, D: int, tree: str = "greedy"):
         ts_list = [(dm[0], i) for dm in doms for i in dm[1:]]
         tt_levels = [[(k, h)] for h in sorted(heads) if h != k]
         return sorted(heads), ts_list, tt_levels
-    if tree != "greedy":
+    ts_list = []
+    geqrt_rows = list(range(k, n))
+    if tree.startswith("hqr"):
+        a = int(tree[3:]) if len(tree) > 3 else 4
+        if a < 1:
+            raise ValueError(tree)
+        groups = [[dm[s:s + a] for s in range(0, len(dm), a)] for dm in doms]
+        ts_list = [(gr[0], i) for gs in groups for gr in gs for i in gr[1:]]
+        doms = [[gr[0] for gr in gs] for gs in groups]  # the TT levels run over the group heads
+        geqrt_rows = sorted(h for dm in doms for h in dm)
+    elif tree != "greedy":
         raise ValueError(tree)
     per_dom = [_halving_levels(dm) for dm in doms]
     depth = max((len(lv) for lv in per_dom), default=0)
@@ -640,7 +656,7 @@ def qr_plan(k: int, n: int, D: int, tree: str = "greedy"):
                 lvl.extend(lv[l])
         tt_levels.append(lvl)
     tt_levels.extend(_halving_levels(sorted(heads)))
-    return list(range(k, n)), [], tt_levels
+    return geqrt_rows, ts_list, tt_levels
 
 
 @dataclass

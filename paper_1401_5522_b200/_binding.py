@@ -19,6 +19,7 @@ CRIT_MAX, CRIT_SUM, CRIT_MUMPS = 0, 1, 2
 DEC_LU, DEC_QR = 0, 1
 LU_A1, LU_A2 = 0, 1  # hlq_options.lu_variant (NEXT f4)
 PIVOT_TILE, PIVOT_DOMAIN = 0, 1  # hlq_options.pivot_scope (NEXT f1)
+TREE_GREEDY, TREE_HQR = 0, 1  # hlq_options.tree (HQR: TS groups of ts_group tiles)
 FLAG_ZERO_PIVOT, FLAG_NEAR_TIE, FLAG_FORCED, FLAG_HINTED, FLAG_NONFINITE = 1, 2, 4, 8, 16
 
 
@@ -32,7 +33,7 @@ class HlqOptions(C.Structure):
                 ("forced", C.c_void_p), ("ref_dec", C.c_void_p), ("ref_margin", C.c_void_p),
                 ("tie_rel_tol", C.c_double), ("track_growth", C.c_int32), ("blocking", C.c_int32),
                 ("stream", C.c_void_p), ("profile", C.c_int32), ("invnorm_estimate", C.c_int32),
-                ("lu_variant", C.c_int32), ("pivot_scope", C.c_int32)]
+                ("lu_variant", C.c_int32), ("pivot_scope", C.c_int32), ("ts_group", C.c_int32)]
 
 
 class HlqInfo(C.Structure):

@@ -18,10 +18,6 @@
 
 namespace hlq {
 void launch_tri_inv(Geo g, int k, const DevWork& w, double* Li, double* Ui, cudaStream_t st);
-void launch_qr_apply(const double* A, Geo g, int k, int ib, const double* Tg, const double* Ttt,
-                     const int2* const* level_pairs, const int* level_count, int nlevels,
-                     double* base, int64_t ldc, int64_t ncols, const uint8_t* dec,
-                     cudaStream_t st);
 void launch_final_scan(const double* A, int64_t N, int64_t lda, int* flag, cudaStream_t st);
 }  // namespace hlq
 
@@ -102,6 +98,13 @@ void cache_put(int dev, int slot, void* p, size_t bytes) {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+constexpr int kSolveG = 4;  // tiles per work unit of the persistent solve
+size_t solve_ws_bytes(int n, int nb, int cmax, size_t units) {
+  return align_up(sizeof(int2) * units, 256) + align_up(sizeof(int) * n, 256) +
+         align_up(sizeof(int) * (size_t)n * cmax, 256) + sizeof(double) * (size_t)n * cmax * nb +
+         256;
+}
+
 }  // namespace
 
 // the library's high-priority panel streams (lookahead), created once per device: sp runs the
@@ -127,15 +130,49 @@ static int cuda_err(cudaError_t e) {
   return e == cudaErrorMemoryAllocation ? HLQ_ERR_NOMEM : HLQ_ERR_CUDA;
 }
 
-// greedy halving tree (reading 16): rows of each domain (i mod D), then the domain heads
-static void plan_levels(int k, int n, int D, std::vector<std::vector<int2>>& levels) {
-  levels.clear();
+// QR elimination plan of step k (readings 16 and 34): the rows of each domain (i mod D);
+// tsa == 0: the greedy halving tree over all rows of a domain, then over the domain heads;
+// tsa >= 1 (HQR): each domain's rows cut into consecutive groups of tsa tiles, flat TS inside a
+// group onto its head, the halving tree over a domain's group heads, then over the domain heads.
+struct StepPlanHost {
+  std::vector<std::vector<int2>> levels;  // TT levels
+  std::vector<int> heads;                 // GEQRT rows (HQR only; greedy: all rows k..n-1)
+  std::vector<int2> ts_pairs;             // TS eliminations, group by group
+  std::vector<int> ts_off;                // group offsets into ts_pairs (ngroups + 1)
+};
+
+static void plan_step(int k, int n, int D, int tsa, StepPlanHost& p) {
+  p.levels.clear();
+  p.heads.clear();
+  p.ts_pairs.clear();
+  p.ts_off.clear();
   std::vector<std::vector<int>> doms;
   for (int d = 0; d < D; ++d) {
     std::vector<int> rows;
     for (int i = k; i < n; ++i)
       if (i % D == d) rows.push_back(i);
     if (!rows.empty()) doms.push_back(rows);
+  }
+  std::sort(doms.begin(), doms.end(),
+            [](const std::vector<int>& a, const std::vector<int>& b) { return a[0] < b[0]; });
+  std::vector<int> dom_heads;
+  for (auto& dm : doms) dom_heads.push_back(dm[0]);
+  if (tsa >= 1) {
+    p.ts_off.push_back(0);
+    for (auto& dm : doms) {
+      std::vector<int> gh;
+      for (size_t s = 0; s < dm.size(); s += (size_t)tsa) {
+        const size_t e = std::min(dm.size(), s + (size_t)tsa);
+        gh.push_back(dm[s]);
+        if (e - s > 1) {
+          for (size_t t = s + 1; t < e; ++t) p.ts_pairs.push_back(make_int2(dm[s], dm[t]));
+          p.ts_off.push_back((int)p.ts_pairs.size());
+        }
+      }
+      dm = gh;  // the TT levels run over the group heads
+    }
+    for (auto& dm : doms) p.heads.insert(p.heads.end(), dm.begin(), dm.end());
+    std::sort(p.heads.begin(), p.heads.end());
   }
   auto halving = [](std::vector<int> live, std::vector<std::vector<int2>>& out) {
     while (live.size() > 1) {
@@ -148,20 +185,17 @@ static void plan_levels(int k, int n, int D, std::vector<std::vector<int2>>& lev
   };
   std::vector<std::vector<std::vector<int2>>> per(doms.size());
   size_t depth = 0;
-  std::vector<int> heads;
   for (size_t d = 0; d < doms.size(); ++d) {
     halving(doms[d], per[d]);
     depth = per[d].size() > depth ? per[d].size() : depth;
-    heads.push_back(doms[d][0]);
   }
   for (size_t l = 0; l < depth; ++l) {
     std::vector<int2> lv;
     for (size_t d = 0; d < per.size(); ++d)
       if (l < per[d].size()) lv.insert(lv.end(), per[d][l].begin(), per[d][l].end());
-    levels.push_back(lv);
+    p.levels.push_back(lv);
   }
-  std::sort(heads.begin(), heads.end());
-  halving(heads, levels);
+  halving(dom_heads, p.levels);
 }
 
 extern "C" {
@@ -218,7 +252,10 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   if (opt.ib == 0) opt.ib = 32;
   if (opt.tree_domains == 0) opt.tree_domains = 1;
   if (opt.tie_rel_tol == 0.0) opt.tie_rel_tol = 1e-10;
-  if (opt.ib != 32 || opt.tree_domains < 1 || opt.tree != HLQ_TREE_GREEDY ||
+  if (opt.tree == HLQ_TREE_HQR && opt.ts_group == 0) opt.ts_group = 4;
+  if (opt.ib != 32 || opt.tree_domains < 1 ||
+      (opt.tree != HLQ_TREE_GREEDY && opt.tree != HLQ_TREE_HQR) ||
+      (opt.tree == HLQ_TREE_HQR && opt.ts_group < 1) ||
       opt.mumps_reading < 0 || opt.mumps_reading > 1 || opt.invnorm_estimate < 0 ||
       opt.invnorm_estimate > 1 || opt.lu_variant < HLQ_LU_A1 || opt.lu_variant > HLQ_LU_A2 ||
       (opt.lu_variant == HLQ_LU_A2 && opt.invnorm_estimate != 0) ||
@@ -252,12 +289,18 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   Geo g = f->g;
 
   // plans
-  std::vector<std::vector<std::vector<int2>>> plans(n);
-  size_t npairs = 0;
+  const int tsa = opt.tree == HLQ_TREE_HQR ? opt.ts_group : 0;
+  std::vector<StepPlanHost> plans(n);
+  size_t npairs = 0, nts = 0, nheads = 0, noff = 0;
   for (int k = 0; k < n; ++k) {
-    plan_levels(k, n, f->D, plans[k]);
-    for (auto& lv : plans[k]) npairs += lv.size();
+    plan_step(k, n, f->D, tsa, plans[k]);
+    for (auto& lv : plans[k].levels) npairs += lv.size();
+    nts += plans[k].ts_pairs.size();
+    nheads += plans[k].heads.size();
+    noff += plans[k].ts_off.size();
   }
+  f->tree = opt.tree;
+  f->ts_group = tsa;
 
   // workspace layout (bytes, 256-aligned pieces)
   const size_t ntri = (size_t)n * (n + 1) / 2;
@@ -278,12 +321,12 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
          oZp = take(sizeof(int)), oDec = take(n), oMg = take(sizeof(double) * n),
          oFl = take(sizeof(int) * n), oSt = take(sizeof(int) * 4), oFo = take(n), oRd = take(n),
          oRm = take(sizeof(double) * n), oGs = take(sizeof(double) * (n + 1)),
-         oPr = take(sizeof(int2) * (npairs + 1)), oSc0 = take(sizeof(double) * scr),
+         oPr = take(sizeof(int2) * (npairs + nts + 1)), oHd = take(sizeof(int) * (nheads + noff + 1)), oSc0 = take(sizeof(double) * scr),
          oSc1 = take(sizeof(double) * scr), oWp = take(sizeof(double) * (size_t)N * nb),
          oWr = take(sizeof(double) * (size_t)N * nb),
          oCp = take(fuse_growth_any ? sizeof(double) * (size_t)((N + cpr - 1) / cpr) * N : 8),
          oLi = take(opt.lu_variant == HLQ_LU_A2 ? sizeof(double) * (size_t)n * 2 * nb * nb : 8),
-         oLp = take(opt.lu_variant == HLQ_LU_A2 ? sizeof(int) * (size_t)n * nb : 8), oSt2 = take(sizeof(double) * (size_t)nb);
+         oLp = take(sizeof(int) * (size_t)n * nb), oSt2 = take(sizeof(double) * (size_t)nb);
   const bool dpiv = opt.pivot_scope == HLQ_PIVOT_DOMAIN;
   // speculative QR panel: with a criterion to evaluate, the QR branch's panel (GEQRT of every tile +
   // every TTQRT level) runs on a copy of the panel beside the speculative LU and the criterion, and
@@ -296,6 +339,10 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
          oDk = take(sizeof(unsigned long long) * 2 * 148), oDi = take(sizeof(int) * 2 * 148),
          oDc = take(sizeof(unsigned int)),
          oQp = take(spec_qr ? sizeof(double) * (size_t)N * nb : 8);
+  // persistent-solve workspace (hlq_solve): unit tables (capacity 2 n cmax), flags, partials
+  const int scmax = solve_rows_cmax(n, kSolveG);
+  const size_t solve_cap = (size_t)2 * n * scmax + 1;
+  size_t oSv = take(solve_ws_bytes(n, nb, scmax, solve_cap));
   f->ws_bytes = off;
   f->dev = cur_device();
   f->ws_block = cache_get(0, off);
@@ -334,6 +381,10 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   w.dom_key = (unsigned long long*)(base + oDk);
   w.dom_idx = (int*)(base + oDi);
   w.dom_counter = (unsigned int*)(base + oDc);
+  f->solve_ws_in = base + oSv;
+  f->tma_maps = make_tma_maps(A, N, lda, nb);
+  w.tma_maps = f->tma_maps;
+  f->solve_cap = solve_cap;
   // per-parity views (lookahead: step k+1's panel runs while step k's update still reads step k's
   // W / ipiv / L^-1 / U^-1 / perm)
   DevWork wpar[2] = {w, w};
@@ -343,19 +394,44 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   cudaStream_t st = f->st;
   int rc = 0;
 
-  // uploads (pairs flattened per step / level)
+  // uploads (pairs flattened per step / level; HQR: heads, TS pairs and group offsets)
   std::vector<int2> flat;
-  flat.reserve(npairs);
+  std::vector<int> iflat;
+  flat.reserve(npairs + nts);
+  iflat.reserve(nheads + noff);
   f->lvl_ptr.assign(n, {});
   f->lvl_cnt.assign(n, {});
-  for (int k = 0; k < n; ++k)
-    for (auto& lv : plans[k]) {
+  f->tsplan.assign(n, QRTsPlan{nullptr, 0, nullptr, nullptr, 0});
+  int* hbase = (int*)(base + oHd);
+  for (int k = 0; k < n; ++k) {
+    for (auto& lv : plans[k].levels) {
       f->lvl_ptr[k].push_back(w.pairs + flat.size());
       f->lvl_cnt[k].push_back((int)lv.size());
       flat.insert(flat.end(), lv.begin(), lv.end());
     }
+    const StepPlanHost& p = plans[k];
+    if (tsa >= 1 && !p.ts_off.empty() && p.ts_off.size() > 1) {
+      QRTsPlan& t = f->tsplan[k];
+      t.pairs = w.pairs + flat.size();
+      flat.insert(flat.end(), p.ts_pairs.begin(), p.ts_pairs.end());
+      t.heads = hbase + iflat.size();
+      t.nheads = (int)p.heads.size();
+      iflat.insert(iflat.end(), p.heads.begin(), p.heads.end());
+      t.off = hbase + iflat.size();
+      t.ngroups = (int)p.ts_off.size() - 1;
+      iflat.insert(iflat.end(), p.ts_off.begin(), p.ts_off.end());
+    } else if (tsa >= 1) {
+      // no TS pair in this step (every group a single tile): the greedy launches over the heads,
+      // which are then all the rows k..n-1 (tsa = 1) -- or a one-row panel
+      f->tsplan[k] = QRTsPlan{nullptr, 0, nullptr, nullptr, 0};
+    }
+  }
   if (!flat.empty() &&
       (rc = cuda_err(cudaMemcpyAsync(w.pairs, flat.data(), sizeof(int2) * flat.size(),
+                                     cudaMemcpyHostToDevice, st))))
+    return rc;
+  if (!iflat.empty() &&
+      (rc = cuda_err(cudaMemcpyAsync(hbase, iflat.data(), sizeof(int) * iflat.size(),
                                      cudaMemcpyHostToDevice, st))))
     return rc;
   if (w.forced &&
@@ -414,7 +490,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
       // predicated on d_k with "undecided" = run: once the criterion decides LU, the remaining
       // speculative launches exit at their first instruction
       launch_qr_panel(w.qpan - k0 * N, gq, k, ib, f->lvl_ptr[k].data(), f->lvl_cnt[k].data(), nl,
-                      wk, sq, /*diag_done=*/a2, /*spec=*/true);
+                      wk, sq, /*diag_done=*/a2, /*spec=*/true, &f->tsplan[k]);
       P.end(sq);
       cudaEventRecord(ev_qdone, sq);
     };
@@ -482,14 +558,14 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
       // the domain's stacked LU replaces its panel tiles (after the Eliminate GEMM, which also
       // wrote them: U_kk^-1 applies to the tiles off the domain only)
       if (dpiv) launch_dom_commit(A, g, k, Dp, wk, sp);
-      if (a2) {
-        // A2: keep Q_kk^T (and the identity permutation) for the solve's forward pass
+      // keep the composed row permutation of P_kk for the solve (A2: identity) and, for A2,
+      // Q_kk^T for its forward pass
+      launch_copy_ints(w.luperm + (size_t)k * nb,
+                       reinterpret_cast<const int*>(wk.scratch + (size_t)2 * nb * nb), nb, w.dec, k,
+                       sp);
+      if (a2)
         launch_copy_block(w.luinv + (size_t)k * 2 * nb * nb, nb, wk.scratch, nb, nb, nb, nullptr,
                           w.dec, k, sp);
-        launch_copy_ints(w.luperm + (size_t)k * nb,
-                         reinterpret_cast<const int*>(wk.scratch + (size_t)2 * nb * nb), nb, w.dec,
-                         k, sp);
-      }
       P.end(sp);
     }
     if (spec) {
@@ -501,7 +577,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
     } else if (known != HLQ_DEC_LU) {
       P.begin(HLQ_PROF_QR_GEQRT, sp);
       launch_qr_panel(A, g, k, ib, f->lvl_ptr[k].data(), f->lvl_cnt[k].data(), nl, wk, sp,
-                      /*diag_done=*/a2 && known != HLQ_DEC_QR);
+                      /*diag_done=*/a2 && known != HLQ_DEC_QR, /*spec=*/false, &f->tsplan[k]);
       P.end(sp);
     }
     cudaEventRecord(ev_panel, sp);
@@ -525,7 +601,8 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
           // a12 fused into the TTMQR epilogues: every row i > k is final after its merge
           qr_fused = launch_qr_update(A, g, k, ib, f->lvl_ptr[k].data(), f->lvl_cnt[k].data(), nl,
                                       wk, c0, c1, st,
-                                      (f->track_growth && k + 1 < n) ? w.gstep + k + 1 : nullptr);
+                                      (f->track_growth && k + 1 < n) ? w.gstep + k + 1 : nullptr,
+                                      &f->tsplan[k]);
           P.end(st);
         }
         // a12 for whatever branch did not fuse it: the LU GEMM epilogue (fuse) and the TTMQR
@@ -611,8 +688,67 @@ int hlq_solve(hlq_factors_t f, const double* b, double* x) {
     return rc;
   // forward pass: replay every step on x (LU: P_kk, L_kk^-1 by substitution, x_i -= L_ik x_k;
   // A2: Q_kk^T; QR: the stored reflectors of the tree), then block back substitution with U_kk /
-  // R_kk (substitution inside the tile, GEMV with the row tiles)
-  for (int k = 0; k < g.n; ++k) {
+  // R_kk.  Runs of consecutive A1 LU steps and the back substitution are single persistent
+  // launches (solve.cu k_solve_rows); QR, A2 and domain-pivoting steps replay step by step.
+  const int n = g.n, G = kSolveG, cmax = solve_rows_cmax(n, G);
+  if (!f->solve_ws) {
+    auto eligible = [&](int k) {
+      return f->dec[k] == HLQ_DEC_LU && f->lu_variant == HLQ_LU_A1 &&
+             f->pivot_scope == HLQ_PIVOT_TILE;
+    };
+    std::vector<int2> table;
+    f->solve_runs.clear();
+    f->solve_unit_off.clear();
+    f->solve_unit_cnt.clear();
+    size_t used = 0;
+    for (int k = 0; k < n;) {
+      if (!eligible(k)) { ++k; continue; }
+      int kb = k;
+      while (kb < n && eligible(kb)) ++kb;
+      f->solve_runs.push_back({k, kb});
+      table.resize(used + (size_t)(n - k) * cmax);
+      const size_t cnt = build_solve_units(true, n, k, kb, G, table.data() + used);
+      f->solve_unit_off.push_back(used);
+      f->solve_unit_cnt.push_back(cnt);
+      used += cnt;
+      k = kb;
+    }
+    table.resize(used + (size_t)n * cmax);
+    const size_t cb = build_solve_units(false, n, 0, n, G, table.data() + used);
+    f->solve_unit_off.push_back(used);
+    f->solve_unit_cnt.push_back(cb);
+    used += cb;
+    if (used <= f->solve_cap) {
+      f->solve_ws = f->solve_ws_in;  // the factorization's workspace piece
+    } else {  // many alternating LU runs: a larger table
+      if ((rc = cuda_err(cudaMalloc(&f->solve_ws_own, solve_ws_bytes(n, g.nb, cmax, used))))) {
+        f->solve_ws_own = nullptr;
+        return rc;
+      }
+      f->solve_ws = f->solve_ws_own;
+    }
+    f->solve_used = used;
+    if ((rc = cuda_err(cudaMemcpyAsync(f->solve_ws, table.data(), sizeof(int2) * used,
+                                       cudaMemcpyHostToDevice, st))))
+      return rc;
+  }
+  char* sw = (char*)f->solve_ws;
+  const size_t used = f->solve_used > f->solve_cap ? f->solve_used : f->solve_cap;
+  const int2* units = (const int2*)sw;
+  int* xflag = (int*)(sw + align_up(sizeof(int2) * used, 256));
+  int* pflag = (int*)((char*)xflag + align_up(sizeof(int) * n, 256));
+  double* part = (double*)((char*)pflag + align_up(sizeof(int) * (size_t)n * cmax, 256));
+  unsigned* ticket = (unsigned*)(part + (size_t)n * cmax * g.nb);
+  size_t run = 0;
+  for (int k = 0; k < n; ++k) {
+    if (run < f->solve_runs.size() && f->solve_runs[run].first == k) {
+      const int kb = f->solve_runs[run].second;
+      launch_solve_rows(true, f->A, g, k, kb, G, units + f->solve_unit_off[run],
+                        f->solve_unit_cnt[run], f->w.luperm, x, xflag, part, pflag, ticket, st);
+      ++run;
+      k = kb - 1;
+      continue;
+    }
     if (f->dec[k] == HLQ_DEC_LU && f->pivot_scope == HLQ_PIVOT_DOMAIN)
       launch_dom_swap_vec(x, g, k, f->D, f->w.dipiv + (size_t)k * g.nb, st);
     if (f->dec[k] == HLQ_DEC_LU && f->lu_variant == HLQ_LU_A2)
@@ -620,13 +756,14 @@ int hlq_solve(hlq_factors_t f, const double* b, double* x) {
                               f->w.luperm + (size_t)k * g.nb, x, f->w.solve_t, st,
                               /*dense=*/true);
     else if (f->dec[k] == HLQ_DEC_LU)
-      launch_solve_lu_fwd(f->A, g, k,
-                          f->pivot_scope == HLQ_PIVOT_DOMAIN ? nullptr : f->w.ipiv, x, st);
+      launch_solve_lu_fwd(f->A, g, k, nullptr, x, st);  // domain pivoting: rows already swapped
     else
       launch_qr_apply(f->A, g, k, f->ib, f->w.Tg, f->w.Ttt, f->lvl_ptr[k].data(),
-                      f->lvl_cnt[k].data(), (int)f->lvl_cnt[k].size(), x, g.N, 1, nullptr, st);
+                      f->lvl_cnt[k].data(), (int)f->lvl_cnt[k].size(), x, g.N, 1, nullptr, st,
+                      &f->tsplan[k]);
   }
-  for (int k = g.n - 1; k >= 0; --k) launch_solve_back(f->A, g, k, x, st);
+  launch_solve_rows(false, f->A, g, 0, n, G, units + f->solve_unit_off.back(),
+                    f->solve_unit_cnt.back(), nullptr, x, xflag, part, pflag, ticket, st);
   f->prof.end(st);
   if ((rc = cuda_err(cudaGetLastError()))) return rc;
   if (f->blocking && (rc = cuda_err(cudaStreamSynchronize(st)))) return rc;
@@ -745,6 +882,11 @@ void hlq_free(hlq_factors_t f) {
   if (f->ws_block) {
     cudaStreamSynchronize(f->st);
     cache_put(f->dev, 0, f->ws_block, f->ws_bytes);
+  }
+  if (f->tma_maps) free_tma_maps(f->tma_maps);
+  if (f->solve_ws_own) {
+    cudaStreamSynchronize(f->st);
+    cudaFree(f->solve_ws_own);
   }
   f->prof.collect();
   for (auto e : f->ev)

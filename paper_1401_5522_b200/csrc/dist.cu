@@ -37,10 +37,6 @@
 #include "handle.cuh"
 
 namespace hlq {
-void launch_qr_apply(const double* A, Geo g, int k, int ib, const double* Tg, const double* Ttt,
-                     const int2* const* level_pairs, const int* level_count, int nlevels,
-                     double* base, int64_t ldc, int64_t ncols, const uint8_t* dec,
-                     cudaStream_t st);
 void launch_solve_lu_fwd(const double* A, Geo g, int k, const int* ipiv, double* x,
                          cudaStream_t st);
 void launch_solve_back(const double* A, Geo g, int k, double* x, cudaStream_t st);

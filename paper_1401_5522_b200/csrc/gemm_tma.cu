@@ -1,0 +1,326 @@
+// a7: the LU Schur update  A[k1:N, c0:c1] -= A[k1:N, k0:k1] * A[k0:k1, c0:c1]  (Alg. 2 P:236,
+// P:260-261), persistent and TMA-fed, on the FP64 tensor cores (DMMA).
+//
+// B200 has no FP64 kind for tcgen05.mma, so the FP64 tensor path is the warp-level DMMA
+// (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4).  What TMA adds here is the operand staging:
+//   * one producer warp (one elected lane) streams 16-deep K slices of the L panel and of the U row
+//     through a 6-stage shared-memory ring with cp.async.bulk.tensor (SWIZZLE_128B boxes), arming
+//     full / empty mbarriers; the 4 consumer warps never issue a global load for A or B and never
+//     meet at a CTA-wide barrier in the main loop;
+//   * the kernel is persistent (2 CTAs per SM, grid = 2 x #SMs), walks the output tiles in grouped
+//     raster order, and the producer runs ahead into the next tile's K slices while the consumers
+//     finish the previous tile's epilogue -- no per-tile prologue bubble, no wave-quantization tail;
+//   * 128-byte swizzle + a fragment row order chosen so every DMMA fragment load is
+//     bank-conflict free: the A (L panel) box is {16 rows, 16 k, 4 row groups}; accumulator row g
+//     of a fragment holds panel row (g & 3) + 8 (g >> 2) + 4 s of its 16-row group (s = the
+//     fragment's half), which spreads the 32 lanes over all 16 8-byte slots of a 128-byte row.
+// Epilogue: C_new = C - (A B) (the product accumulates from zero, so the rounding is that of
+// "A_ij - (A_ik A_kj)"), written back with the fused a12 column abs-sums (colpart) when asked.
+// Eligibility (else gemm.cu's cp.async kernel): lda even, A 16-byte aligned, N and nb multiples of
+// 16 (every TMA box in bounds or zero-filled past the matrix).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "hlq_internal.cuh"
+
+namespace hlq {
+
+namespace {
+constexpr int TM_BM = 64, TM_BN = 64, TM_BK = 16, TM_ST = 6;
+constexpr int TM_CONS = 4;                       // consumer warps (2 x 2 warp tiles of 32 x 32)
+constexpr int TM_T = 32 * (TM_CONS + 1);         // + the producer warp
+constexpr int TM_A_BYTES = TM_BM * TM_BK * 8;    // 8 KB
+constexpr int TM_B_BYTES = TM_BN * TM_BK * 8;    // 8 KB
+constexpr int TM_STAGE = TM_A_BYTES + TM_B_BYTES;
+constexpr int TM_SMEM = TM_ST * TM_STAGE + 1024 /*align*/ + 2 * TM_BN * 8 + 256;
+constexpr int TM_CTAS_PER_SM = 2;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0,
+                                            int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void dmma_tm(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+// row within a 16-row group held by accumulator row g of a fragment half s (conflict-free A loads)
+__device__ __forceinline__ int frag_row(int g, int s) { return (g & 3) + 8 * (g >> 2) + 4 * s; }
+}  // namespace
+
+struct TmaMaps {
+  CUtensorMap a;  // 3D {16 rows, columns, row groups of 16} over the whole matrix: the L panel role
+  CUtensorMap b;  // 2D {rows, columns} over the whole matrix: the U row-block role
+};
+
+__global__ void __launch_bounds__(TM_T, TM_CTAS_PER_SM)
+    k_dgemm_tma(const __grid_constant__ TmaMaps maps, double* __restrict__ C, int64_t ldc,
+                int64_t M, int64_t N, int K, int arow0, int kcol0, int bcol0,
+                const uint8_t* __restrict__ dec, int k, int want, double* __restrict__ colpart,
+                int64_t ldp) {
+  if (dec != nullptr && dec[k] != want) return;  // predicated launch (the branch not taken)
+  extern __shared__ __align__(1024) unsigned char tm_smem_raw[];
+  unsigned char* sm = (unsigned char*)(((uintptr_t)tm_smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(sm + TM_ST * TM_STAGE);
+  uint64_t* empty = full + TM_ST;
+  double* red = (double*)(empty + TM_ST);  // 2 x 64 column partials (a12 epilogue)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < TM_ST; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, TM_CONS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t ntm = (M + TM_BM - 1) / TM_BM, ntn = (N + TM_BN - 1) / TM_BN;
+  const int64_t ntiles = ntm * ntn;
+  const int KT = K / TM_BK;
+  auto tile_coords = [&](int64_t t, int64_t& tm, int64_t& tn) {  // grouped raster (8 tile rows)
+    const int64_t per_group = 8 * ntn;
+    const int64_t grp = t / per_group;
+    const int64_t first_tm = grp * 8;
+    const int64_t gsz = (ntm - first_tm < 8) ? (ntm - first_tm) : 8;
+    tm = first_tm + (t % per_group) % gsz;
+    tn = (t % per_group) / gsz;
+  };
+
+  if (warp == TM_CONS) {
+    // ---------------- producer: one lane streams the K slices of every tile of this CTA
+    if (lane == 0) {
+      int s = 0;
+      unsigned ph = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int64_t tm, tn;
+        tile_coords(t, tm, tn);
+        const int rg = (int)((arow0 + tm * TM_BM) >> 4);   // row group of the panel rows
+        const int bc = (int)(bcol0 + tn * TM_BN);          // first output column
+        for (int kt = 0; kt < KT; ++kt) {
+          mbar_wait(empty + s, ph ^ 1);
+          unsigned char* st = sm + s * TM_STAGE;
+          mbar_expect_tx(full + s, TM_STAGE);
+          tma_load_3d(st, &maps.a, full + s, 0, kcol0 + kt * TM_BK, rg);
+          tma_load_2d(st + TM_A_BYTES, &maps.b, full + s, kcol0 + kt * TM_BK, bc);
+          if (++s == TM_ST) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+    return;
+  }
+  // ---------------- consumers: 4 warps, warp tile 32 x 32 (wm, wn)
+  const int g = lane >> 2, t4 = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;
+  int s = 0;
+  unsigned ph = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    int64_t tm, tn;
+    tile_coords(t, tm, tn);
+    double acc[4][4][2];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+    for (int kt = 0; kt < KT; ++kt) {
+      mbar_wait(full + s, ph);
+      const double* As = (const double*)(sm + s * TM_STAGE);
+      const double* Bs = (const double*)(sm + s * TM_STAGE + TM_A_BYTES);
+#pragma unroll
+      for (int k4 = 0; k4 < TM_BK; k4 += 4) {
+        const int kk = k4 + t4;
+        double a[4], b[4];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) {
+          const int mhi = wm * 2 + (mi >> 1), mlo = frag_row(g, mi & 1);
+          a[mi] = As[(mhi * 16 + kk) * 16 + ((((mlo >> 1) ^ (kk & 7)) << 1) | (mlo & 1))];
+        }
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+          const int nn = wn * 32 + ni * 8 + g;
+          b[ni] = Bs[nn * 16 + ((((kk >> 1) ^ g) << 1) | (kk & 1))];
+        }
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) dmma_tm(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + s);
+      if (++s == TM_ST) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+    // epilogue: C_new = C - acc, in place in the accumulators (one 8-column fragment row at a
+    // time: its loads are independent of each other)
+    const int64_t m0 = tm * TM_BM, n0 = tn * TM_BN;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+      const int64_t row = m0 + (wm * 2 + (mi >> 1)) * 16 + frag_row(g, mi & 1);
+      double c[4][2];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const int64_t col = n0 + wn * 32 + ni * 8 + 2 * t4;
+        c[ni][0] = (row < M && col < N) ? C[col * ldc + row] : 0.0;
+        c[ni][1] = (row < M && col + 1 < N) ? C[(col + 1) * ldc + row] : 0.0;
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const int64_t col = n0 + wn * 32 + ni * 8 + 2 * t4;
+        acc[mi][ni][0] = c[ni][0] - acc[mi][ni][0];
+        acc[mi][ni][1] = c[ni][1] - acc[mi][ni][1];
+        if (row < M) {
+          if (col < N) C[col * ldc + row] = acc[mi][ni][0];
+          if (col + 1 < N) C[(col + 1) * ldc + row] = acc[mi][ni][1];
+        }
+      }
+    }
+    if (colpart != nullptr) {
+      // fused a12: per-column |C_new| sums over the tile's 64 rows (rows >= M are exact zeros)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          double v = 0.0;
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi) v += fabs(acc[mi][ni][h]);
+          v += __shfl_xor_sync(0xffffffffu, v, 4);
+          v += __shfl_xor_sync(0xffffffffu, v, 8);
+          v += __shfl_xor_sync(0xffffffffu, v, 16);
+          if (g == 0) red[wm * TM_BN + wn * 32 + ni * 8 + 2 * t4 + h] = v;
+        }
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * TM_CONS) : "memory");
+      if (tid < TM_BN && n0 + tid < N) colpart[tm * ldp + n0 + tid] = red[tid] + red[TM_BN + tid];
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * TM_CONS) : "memory");
+    }
+  }
+}
+
+// ---- host side ---------------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+
+// Tensor maps of the whole N x N matrix (ld lda) for the TMA Schur update; returns nullptr when the
+// matrix is not eligible (the caller keeps the cp.async kernel).  The maps live in the returned
+// heap block (free with free_tma_maps).
+void* make_tma_maps(const double* A, int64_t N, int64_t lda, int nb) {
+  static int off = -1;
+  if (off < 0) off = getenv("HLQ_DGEMM_TMA") ? (atoi(getenv("HLQ_DGEMM_TMA")) == 0) : 0;
+  if (off) return nullptr;
+  if ((lda & 1) || (((uintptr_t)A) & 15) || (N % 16) || (nb % 16) || N < 16) return nullptr;
+  if (N > (int64_t)1 << 31) return nullptr;
+  auto fn = encode_fn();
+  if (!fn) return nullptr;
+  TmaMaps* m = (TmaMaps*)aligned_alloc(64, sizeof(TmaMaps));
+  if (!m) return nullptr;
+  memset(m, 0, sizeof(*m));
+  const cuuint32_t estr3[3] = {1, 1, 1}, estr2[2] = {1, 1};
+  // A role: dims {16 (rows within a group), N (columns), N/16 (row groups)}
+  const cuuint64_t gdA[3] = {16, (cuuint64_t)N, (cuuint64_t)(N / 16)};
+  const cuuint64_t gsA[2] = {(cuuint64_t)lda * 8, 16 * 8};
+  const cuuint32_t boxA[3] = {16, TM_BK, TM_BM / 16};
+  CUresult r1 = fn(&m->a, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)A, gdA, gsA, boxA, estr3,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  // B role: dims {N (rows = k), N (columns)}
+  const cuuint64_t gdB[2] = {(cuuint64_t)N, (cuuint64_t)N};
+  const cuuint64_t gsB[1] = {(cuuint64_t)lda * 8};
+  const cuuint32_t boxB[2] = {TM_BK, TM_BN};
+  CUresult r2 = fn(&m->b, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)A, gdB, gsB, boxB, estr2,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS) {
+    free(m);
+    return nullptr;
+  }
+  return m;
+}
+
+void free_tma_maps(void* m) { free(m); }
+
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// A[k1 : k1+M, c0 : c0+nc] -= A[k1 : k1+M, k0 : k0+K] * A[k0 : k0+K, c0 : c0+nc] on the TMA path
+// (maps from make_tma_maps for this matrix); false when K or the tile origin is not eligible.
+bool launch_schur_tma(const void* maps, double* A, int64_t lda, int64_t k0, int64_t k1, int64_t c0,
+                      int64_t M, int64_t nc, int K, const uint8_t* dec, int k, int want,
+                      double* colpart, int64_t ldp, cudaStream_t st) {
+  if (!maps || K % TM_BK || k1 % 16 || M <= 0 || nc <= 0) return false;
+  static unsigned long long attr = 0;
+  if (first_on_device(attr))
+    cudaFuncSetAttribute(k_dgemm_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, TM_SMEM);
+  const int64_t tiles = ((M + TM_BM - 1) / TM_BM) * ((nc + TM_BN - 1) / TM_BN);
+  const int64_t grid = std::min<int64_t>(tiles, (int64_t)sm_count() * TM_CTAS_PER_SM);
+  ::hlq::g_launches++;
+  k_dgemm_tma<<<(unsigned)grid, TM_T, TM_SMEM, st>>>(
+      *(const TmaMaps*)maps, A + c0 * lda + k1, lda, M, nc, K, (int)k1, (int)k0, (int)c0, dec, k,
+      want, colpart, ldp ? ldp : nc);
+  return true;
+}
+
+}  // namespace hlq

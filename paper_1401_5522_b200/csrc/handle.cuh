@@ -4,6 +4,7 @@
 #include <stdlib.h>
 #include <stdio.h>
 
+#include <utility>
 #include <vector>
 
 #include "hlq_internal.cuh"
@@ -79,7 +80,9 @@ struct hlq_factors_s {
   void* ws_block = nullptr;
   int dev = 0;  // device of the workspace block
   size_t ws_bytes = 0;
-  // greedy-tree plan: per step k, levels l: device pointer + count
+  int tree = 0, ts_group = 0;  // HLQ_TREE_*, the HQR TS group size (0: greedy)
+  std::vector<hlq::QRTsPlan> tsplan;  // per step: the HQR TS level (ngroups = 0: none)
+  // QR-tree plan: per step k, TT levels l: device pointer + count
   std::vector<std::vector<const int2*>> lvl_ptr;
   std::vector<std::vector<int>> lvl_cnt;
   // host results
@@ -90,6 +93,15 @@ struct hlq_factors_s {
   int status = 0;
   double growth = 0.0;
   bool track_growth = true;
+  // persistent-solve workspace (allocated at the first hlq_solve): unit tables per forward LU run
+  // and for the back substitution, flags, chunk partial sums
+  void* tma_maps = nullptr;      // gemm_tma.cu tensor maps of A (host memory) or null
+  void* solve_ws = nullptr;      // = solve_ws_in, or solve_ws_own when the tables outgrow it
+  void* solve_ws_in = nullptr;   // piece of the factorization workspace (table capacity solve_cap)
+  void* solve_ws_own = nullptr;  // own allocation (freed by hlq_free)
+  size_t solve_cap = 0, solve_used = 0;
+  std::vector<std::pair<int, int>> solve_runs;   // [ka, kb) of every forward LU run
+  std::vector<size_t> solve_unit_off, solve_unit_cnt;  // per run (+1: back pass) in the table
   // 2D block-cyclic factorization state (dist.cu); nullptr on the single-GPU path
   hlq::DistState* dist = nullptr;
 };

@@ -71,6 +71,16 @@ struct DevWork {
   unsigned long long* dom_key;  // 2*148 partial pivot keys
   int* dom_idx;                 // 2*148 partial pivot rows
   unsigned int* dom_counter;    // arrivals of the last-CTA reduction
+  const void* tma_maps;         // TMA tensor maps of A for the Schur update (gemm_tma.cu) or null
+};
+
+// ---- the HQR tree's TS level of one QR step (DESIGN reading 34); nullptr / ngroups = 0: greedy
+struct QRTsPlan {
+  const int* heads;      // device: the GEQRT / UNMQR tile rows (the group heads), ascending
+  int nheads;
+  const int2* pairs;     // device: (head, i) TS eliminations, group by group, in chain order
+  const int* off;        // device: ngroups + 1 offsets into pairs
+  int ngroups;
 };
 
 // ---- kernels-side launch helpers (defined in the .cu files) ---------------------------------
@@ -120,11 +130,30 @@ void launch_qr_panel_tc(double* A, Geo g, int k, int ib, double* Tg, double* Ttt
 bool launch_qr_update2(const double* A, Geo g, int k, const double* T, const int2* pairs,
                        int npairs, bool tt, double* base, int64_t ldc, int64_t ncols,
                        const uint8_t* dec, cudaStream_t st, double* gmax = nullptr);
+// HQR tree with TS groups (DESIGN reading 34): GEQRT / UNMQR of listed tile rows (the group heads),
+// TSQRT chains and TSMQR chain updates (one CTA per group and column slab; pairs[off[g]..off[g+1]))
+void launch_geqrt_rows(double* A, Geo g, int k, int ib, double* Tg, const int* rows, int nrows,
+                       const uint8_t* dec, cudaStream_t st, bool spec);
+void launch_tsqrt_chains(double* A, Geo g, int k, int ib, double* Tts, const int2* pairs,
+                         const int* off, int ngroups, const uint8_t* dec, cudaStream_t st,
+                         bool spec);
+void launch_unmqr_rows(const double* A, Geo g, int k, const double* T, const int* rows, int nrows,
+                       double* base, int64_t ldc, int64_t ncols, const uint8_t* dec,
+                       cudaStream_t st);
+void launch_tsmqr_chains(const double* A, Geo g, int k, const double* T, const int2* pairs,
+                         const int* off, int ngroups, double* base, int64_t ldc, int64_t ncols,
+                         const uint8_t* dec, cudaStream_t st, double* gmax);
 bool launch_qr_update_dmma(const double* A, Geo g, int k, int ib, const double* Tg,
                            const double* Ttt, const int2* const* level_pairs,
                            const int* level_count, int nlevels, double* base, int64_t ldc,
                            int64_t ncols, const uint8_t* dec, int what, cudaStream_t st,
                            double* gmax = nullptr);
+// the solve's Q^T x of QR step k (ncols = 1): GEQRT rows (ts: the HQR group heads + TS chains),
+// then the TT levels
+void launch_qr_apply(const double* A, Geo g, int k, int ib, const double* Tg, const double* Ttt,
+                     const int2* const* level_pairs, const int* level_count, int nlevels,
+                     double* base, int64_t ldc, int64_t ncols, const uint8_t* dec,
+                     cudaStream_t st, const QRTsPlan* ts = nullptr);
 // TTMQR levels only (no UNMQR) on a column block: the solve's cross-rank head merges
 void launch_tt_apply(const double* A, Geo g, int k, int ib, const double* Ttt,
                      const int2* const* level_pairs, const int* level_count, int nlevels,
@@ -148,6 +177,13 @@ void launch_lu_panel(double* A, Geo g, int k, const DevWork& w, cudaStream_t st,
 // a2: LU variant A2 (Apply = Q_kk^T GEMM); otherwise the unit-lower triangular solve
 void launch_lu_update(double* A, Geo g, int k, const DevWork& w, int64_t c0, int64_t c1,
                       double* colpart, cudaStream_t st, bool a2 = false);
+// gemm_tma.cu: tensor maps of the whole matrix (nullptr if not eligible) and the persistent
+// TMA-fed Schur update A[k1:k1+M, c0:c0+nc] -= A[k1:, k0:k0+K] A[k0:k0+K, c0:] (false: not eligible)
+void* make_tma_maps(const double* A, int64_t N, int64_t lda, int nb);
+void free_tma_maps(void* m);
+bool launch_schur_tma(const void* maps, double* A, int64_t lda, int64_t k0, int64_t k1, int64_t c0,
+                      int64_t M, int64_t nc, int K, const uint8_t* dec, int k, int want,
+                      double* colpart, int64_t ldp, cudaStream_t st);
 // trsm.cu: blocked triangular solves (DMMA off-diagonal blocks, substitution on 32 x 32 diagonal
 // blocks), in place, predicated on dec[k] == want.  Eliminate: A[r0:r0+M, c0:c0+bk] <- X U^-1,
 // U = upper triangle of W (ld ldw).  Apply: A[r0:r0+bk, c0:c0+nc] <- L^-1 P X, L = unit lower
@@ -166,11 +202,12 @@ void launch_gemm_sub(double* C, int64_t ldc, const double* Am, int64_t lda, cons
 // spec: the speculative QR panel (runs while d_k is undecided, see launch_qr_panel_tc)
 void launch_qr_panel(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
                      const int* level_count, int nlevels, const DevWork& w, cudaStream_t st,
-                     bool diag_done = false, bool spec = false);
+                     bool diag_done = false, bool spec = false, const QRTsPlan* ts = nullptr);
 // returns whether every TTMQR level fused the a12 scan into gmax (gmax != nullptr)
 bool launch_qr_update(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
                       const int* level_count, int nlevels, const DevWork& w, int64_t c0,
-                      int64_t c1, cudaStream_t st, double* gmax = nullptr);
+                      int64_t c1, cudaStream_t st, double* gmax = nullptr,
+                      const QRTsPlan* ts = nullptr);
 void launch_tile_norm_max(const double* A, Geo g, int k, double* out, cudaStream_t st,
                           const uint8_t* dec = nullptr, int step = 0, int want = 0,
                           int64_t cb = -1, int64_t ce = -1);
@@ -192,6 +229,14 @@ void launch_solve_back_inv(const double* A, Geo g, int k, const double* Ui, doub
                            cudaStream_t st);
 void launch_residual(const double* A, int64_t N, int64_t lda, const double* x, const double* b,
                      double* out3dev, cudaStream_t st);
+// persistent block-row solves (solve.cu): fwd = the forward pass of the LU steps [ka, kb) over
+// block rows >= ka (perm_all: per step the composed row permutation of P_kk), !fwd = the back
+// substitution over all block rows; G tiles per work unit, units from build_solve_units
+int solve_rows_cmax(int n, int G);
+size_t build_solve_units(bool fwd, int n, int ka, int kb, int G, int2* out);
+void launch_solve_rows(bool fwd, const double* A, Geo g, int ka, int kb, int G, const int2* units,
+                       size_t nunits, const int* perm_all, double* x, int* xflag, double* part,
+                       int* pflag, unsigned* ticket, cudaStream_t st);
 
 // allow the largest dynamic shared memory the device permits for this kernel (opt-in minus the
 // kernel's static shared memory)

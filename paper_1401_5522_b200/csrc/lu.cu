@@ -141,10 +141,13 @@ void launch_lu_update(double* A, Geo g, int k, const DevWork& w, int64_t c0, int
     // Apply: A[k0:k1, c0:c1] <- L^-1 P A[k0:k1, c0:c1] (L: unit lower triangle of W), in place
     launch_trsm_apply(A, g.lda, k0, c0, nc, bk, w.W, g.nb, perm, dec, k, HLQ_DEC_LU, st);
   }
-  // Update: A[k1:N, c0:c1] -= A[k1:N, k0:k1] * A[k0:k1, c0:c1]
-  launch_dgemm(A + c0 * g.lda + k1, g.lda, A + k0 * g.lda + k1, g.lda, A + c0 * g.lda + k0, g.lda,
-               M, nc, bk, true, true, dec, k, HLQ_DEC_LU, st,
-               colpart ? colpart + (c0 - k1) : nullptr, M);
+  // Update: A[k1:N, c0:c1] -= A[k1:N, k0:k1] * A[k0:k1, c0:c1] (persistent TMA kernel when the
+  // matrix is eligible, else the cp.async kernel)
+  if (!launch_schur_tma(w.tma_maps, A, g.lda, k0, k1, c0, M, nc, bk, dec, k, HLQ_DEC_LU,
+                        colpart ? colpart + (c0 - k1) : nullptr, M, st))
+    launch_dgemm(A + c0 * g.lda + k1, g.lda, A + k0 * g.lda + k1, g.lda, A + c0 * g.lda + k0,
+                 g.lda, M, nc, bk, true, true, dec, k, HLQ_DEC_LU, st,
+                 colpart ? colpart + (c0 - k1) : nullptr, M);
 }
 
 void launch_lu_growth(const DevWork& w, Geo g, int k, cudaStream_t st) {

@@ -18,22 +18,14 @@ namespace hlq {
 // per reflector block, its rows of V_b (32 registers per row), so V is read once; W = V_b^T x is a
 // transpose-butterfly reduction (31 shuffles per warp) plus a fixed-order sum of the 8 warp
 // partials, U = T_b^T W by 32 threads, and x -= V_b U stays in registers.
-template <bool TT>
-__global__ void __launch_bounds__(256) k_qr_apply_vec2(const double* __restrict__ A, Geo g, int k,
-                                                       int ib, const double* __restrict__ Tb,
-                                                       const int2* __restrict__ pairs,
-                                                       double* __restrict__ x) {
-  __shared__ double red[8][33];
-  __shared__ double Uv[32];
+// MODE 0: GEQRT reflectors of tile row i (unit lower); 1: TT reflectors of the pair (e, i)
+// (upper triangular); 2: TS reflectors of the pair (e, i) (square)
+template <int MODE>
+__device__ void qr_apply_vec_body(const double* __restrict__ A, Geo g, int k, int ib,
+                                  const double* __restrict__ Tb, int e, int i,
+                                  double* __restrict__ x, double (*red)[33], double* Uv) {
+  constexpr bool TT = MODE != 0, TS = MODE == 2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int e = 0, i;
-  if (TT) {
-    const int2 pr = pairs[blockIdx.x];
-    e = pr.x;
-    i = pr.y;
-  } else {
-    i = k + blockIdx.x;
-  }
   const int bi = g.bs(i), bk = g.cbs(k);
   const double* V = g.tile(const_cast<double*>(A), i, k);
   const double* T = Tb + tri_index(i, k, g.n) * (int64_t)ib * g.nb;
@@ -51,8 +43,8 @@ __global__ void __launch_bounds__(256) k_qr_apply_vec2(const double* __restrict_
       const int c = i0 + l;
       const double* col = V + (int64_t)c * g.lda;
       if (TT) {
-        v0[l] = (l < sb && r0 < bi && r0 <= c) ? col[r0] : 0.0;
-        v1[l] = (l < sb && r1 < bi && r1 <= c) ? col[r1] : 0.0;
+        v0[l] = (l < sb && r0 < bi && (TS || r0 <= c)) ? col[r0] : 0.0;
+        v1[l] = (l < sb && r1 < bi && (TS || r1 <= c)) ? col[r1] : 0.0;
       } else {
         v0[l] = (l < sb && r0 < bi && r0 >= c) ? (r0 == c ? 1.0 : col[r0]) : 0.0;
         v1[l] = (l < sb && r1 < bi && r1 >= c) ? (r1 == c ? 1.0 : col[r1]) : 0.0;
@@ -104,18 +96,55 @@ __global__ void __launch_bounds__(256) k_qr_apply_vec2(const double* __restrict_
   if (r1 < bi) xi[r1] = x1;
 }
 
+template <bool TT>
+__global__ void __launch_bounds__(256) k_qr_apply_vec2(const double* __restrict__ A, Geo g, int k,
+                                                       int ib, const double* __restrict__ Tb,
+                                                       const int2* __restrict__ pairs,
+                                                       const int* __restrict__ rows,
+                                                       double* __restrict__ x) {
+  __shared__ double red[8][33];
+  __shared__ double Uv[32];
+  if (TT) {
+    const int2 pr = pairs[blockIdx.x];
+    qr_apply_vec_body<1>(A, g, k, ib, Tb, pr.x, pr.y, x, red, Uv);
+  } else {
+    qr_apply_vec_body<0>(A, g, k, ib, Tb, 0, rows != nullptr ? rows[blockIdx.x] : k + blockIdx.x,
+                         x, red, Uv);
+  }
+}
+
+// the TS chains of an HQR step on x: one CTA per group, its pairs in order
+__global__ void __launch_bounds__(256) k_qr_apply_vec_ts(const double* __restrict__ A, Geo g, int k,
+                                                         int ib, const double* __restrict__ Tb,
+                                                         const int2* __restrict__ pairs,
+                                                         const int* __restrict__ off,
+                                                         double* __restrict__ x) {
+  __shared__ double red[8][33];
+  __shared__ double Uv[32];
+  for (int p = off[blockIdx.x]; p < off[blockIdx.x + 1]; ++p) {
+    const int2 pr = pairs[p];
+    qr_apply_vec_body<2>(A, g, k, ib, Tb, pr.x, pr.y, x, red, Uv);
+    __syncthreads();
+  }
+}
+
 // Apply the stored QR step k to the solve's vector x (rows 0..N-1 of base): Q_ik^T of every
 // GEQRT tile, then the TTMQR of every level (ncols must be 1, ib = 32).
 void launch_qr_apply(const double* A, Geo g, int k, int ib, const double* Tg, const double* Ttt,
                      const int2* const* level_pairs, const int* level_count, int nlevels,
                      double* base, int64_t ldc, int64_t ncols, const uint8_t* dec,
-                     cudaStream_t st) {
+                     cudaStream_t st, const QRTsPlan* ts) {
   (void)ldc;
   (void)dec;
   if (ncols <= 0) return;
-  { ::hlq::g_launches++; k_qr_apply_vec2<false><<<g.n - k, 256, 0, st>>>(A, g, k, ib, Tg, nullptr, base); }
+  if (ts != nullptr && ts->ngroups > 0) {  // HQR: Q^T of the group heads, then the TS chains
+    { ::hlq::g_launches++; k_qr_apply_vec2<false><<<ts->nheads, 256, 0, st>>>(A, g, k, ib, Tg, nullptr, ts->heads, base); }
+    { ::hlq::g_launches++; k_qr_apply_vec_ts<<<ts->ngroups, 256, 0, st>>>(A, g, k, ib, Ttt, ts->pairs, ts->off, base); }
+  } else {
+    { ::hlq::g_launches++; k_qr_apply_vec2<false><<<g.n - k, 256, 0, st>>>(A, g, k, ib, Tg, nullptr, nullptr, base); }
+  }
   for (int l = 0; l < nlevels; ++l)
-    { ::hlq::g_launches++; k_qr_apply_vec2<true><<<level_count[l], 256, 0, st>>>(A, g, k, ib, Ttt, level_pairs[l], base); }
+    { ::hlq::g_launches++; k_qr_apply_vec2<true><<<level_count[l], 256, 0, st>>>(A, g, k, ib, Ttt, level_pairs[l], nullptr, base); }
 }
 
 // TTMQR levels only on the solve's vector (the distributed solve's cross-rank head merges)
@@ -127,7 +156,7 @@ void launch_tt_apply(const double* A, Geo g, int k, int ib, const double* Ttt,
   (void)dec;
   if (ncols <= 0) return;
   for (int l = 0; l < nlevels; ++l)
-    { ::hlq::g_launches++; k_qr_apply_vec2<true><<<level_count[l], 256, 0, st>>>(A, g, k, ib, Ttt, level_pairs[l], base); }
+    { ::hlq::g_launches++; k_qr_apply_vec2<true><<<level_count[l], 256, 0, st>>>(A, g, k, ib, Ttt, level_pairs[l], nullptr, base); }
 }
 
 // Panel stage of a QR step (column block k only): GEQRT of every panel tile, then the TTQRT of
@@ -135,10 +164,17 @@ void launch_tt_apply(const double* A, Geo g, int k, int ib, const double* Ttt,
 // trailing update).  Predicated on dec[k] (speculative launches also run while it is undecided).
 void launch_qr_panel(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
                      const int* level_count, int nlevels, const DevWork& w, cudaStream_t st,
-                     bool diag_done, bool spec) {
+                     bool diag_done, bool spec, const QRTsPlan* ts) {
   const uint8_t* dec = w.dec;
-  launch_qr_panel_tc(A, g, k, ib, w.Tg, w.Ttt, nullptr, 0, dec, false, st, diag_done ? k + 1 : k,
-                     spec);
+  if (ts != nullptr && ts->ngroups > 0) {
+    // HQR: GEQRT of the group heads (A2: the head k is done), then every group's TSQRT chain
+    const int skip = (diag_done && ts->nheads > 0) ? 1 : 0;  // heads[0] == k
+    launch_geqrt_rows(A, g, k, ib, w.Tg, ts->heads + skip, ts->nheads - skip, dec, st, spec);
+    launch_tsqrt_chains(A, g, k, ib, w.Ttt, ts->pairs, ts->off, ts->ngroups, dec, st, spec);
+  } else {
+    launch_qr_panel_tc(A, g, k, ib, w.Tg, w.Ttt, nullptr, 0, dec, false, st,
+                       diag_done ? k + 1 : k, spec);
+  }
   for (int l = 0; l < nlevels; ++l)
     launch_qr_panel_tc(A, g, k, ib, w.Tg, w.Ttt, level_pairs[l], level_count[l], dec, true, st, -1,
                        spec);
@@ -148,14 +184,23 @@ void launch_qr_panel(double* A, Geo g, int k, int ib, const int2* const* level_p
 // TTMQR of every level in order.  Predicated on dec[k] == QR.
 bool launch_qr_update(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
                       const int* level_count, int nlevels, const DevWork& w, int64_t c0,
-                      int64_t c1, cudaStream_t st, double* gmax) {
+                      int64_t c1, cudaStream_t st, double* gmax, const QRTsPlan* ts) {
   const uint8_t* dec = w.dec;
   const int64_t ncols = c1 - c0;
   if (ncols <= 0) return true;
-  bool fused = gmax != nullptr && nlevels > 0;
+  const bool hqr = ts != nullptr && ts->ngroups > 0;
+  bool fused = gmax != nullptr && (nlevels > 0 || hqr);
   double* base = A + c0 * g.lda;
-  launch_qr_update_dmma(A, g, k, ib, w.Tg, w.Ttt, level_pairs, level_count, nlevels, base, g.lda,
-                        ncols, dec, 0, st);
+  if (hqr) {
+    // HQR: UNMQR of the group heads, then the TSMQR chains (a12 fused: every TS-eliminated row is
+    // final after its pair, every head after its TT merge)
+    launch_unmqr_rows(A, g, k, w.Tg, ts->heads, ts->nheads, base, g.lda, ncols, dec, st);
+    launch_tsmqr_chains(A, g, k, w.Ttt, ts->pairs, ts->off, ts->ngroups, base, g.lda, ncols, dec,
+                        st, gmax);
+  } else {
+    launch_qr_update_dmma(A, g, k, ib, w.Tg, w.Ttt, level_pairs, level_count, nlevels, base,
+                          g.lda, ncols, dec, 0, st);
+  }
   for (int l = 0; l < nlevels; ++l)
     fused &= launch_qr_update_dmma(A, g, k, ib, w.Tg, w.Ttt, level_pairs, level_count, nlevels,
                                    base, g.lda, ncols, dec, 1 + l, st, gmax);

@@ -12,6 +12,8 @@
 // bank-conflict free.
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "hlq_internal.cuh"
 
 namespace hlq {
@@ -241,7 +243,8 @@ __device__ __forceinline__ double block_sum(double v, double* red, int tid) {
 // reaches the 32 lanes of a warp through xs (lane l stores its NR values, 16-byte broadcasts back).
 constexpr int PF_WS = 2 * 8 * 33 + 64 + 32 * 33 + 32 + 8 * 40;
 
-template <bool TT, int NR>
+// FULL (TT only): the eliminated tile is square (TSQRT): every reflector spans all R rows
+template <bool TT, int NR, bool FULL = false>
 __device__ void panel_factor(double* Vs, int ldc, double* Rs, double* Ts, int R, int i0, int sb,
                              double* ws, int tid) {
   const int lane = tid & 31, warp = tid >> 5;
@@ -260,9 +263,10 @@ __device__ void panel_factor(double* Vs, int ldc, double* Rs, double* Ts, int R,
 #pragma unroll 1
   for (int l = 0; l < lmax; ++l) {
     const int bf = l & 1;
-    // reflector rows: GE below the diagonal (l, R), TT the upper-triangle rows [0, min(R, i0+l+1))
+    // reflector rows: GE below the diagonal (l, R), TT the upper-triangle rows [0, min(R, i0+l+1)),
+    // TS (FULL) all rows [0, R)
     const int rlo = TT ? 0 : l + 1;
-    const int rhi = TT ? min(R, i0 + l + 1) : R;
+    const int rhi = TT ? (FULL ? R : min(R, i0 + l + 1)) : R;
     // this warp's reflector rows are i in [ilo, ihi) (warp-uniform; empty for most warps early on)
     const int ilo = max(0, rlo - rw), ihi = min(NR, rhi - rw);
     const bool wact = ilo < ihi;
@@ -386,15 +390,15 @@ __device__ void panel_factor(double* Vs, int ldc, double* Rs, double* Ts, int R,
 
 // rows per warp for a block of R <= nb rows (one kernel for every NR: measured faster than
 // per-NR kernels, whose smaller register allocations throttle the DMMA block updates)
-template <bool TT>
+template <bool TT, bool FULL = false>
 __device__ __forceinline__ void panel_factor_nb(int nb, double* Vs, int ldc, double* Rs,
                                                 double* Ts, int R, int i0, int sb, double* ws,
                                                 int tid) {
-  if (nb <= 64) panel_factor<TT, 8>(Vs, ldc, Rs, Ts, R, i0, sb, ws, tid);
-  else if (nb <= 128) panel_factor<TT, 16>(Vs, ldc, Rs, Ts, R, i0, sb, ws, tid);
-  else if (nb <= 192) panel_factor<TT, 24>(Vs, ldc, Rs, Ts, R, i0, sb, ws, tid);
-  else if (nb <= 256) panel_factor<TT, 32>(Vs, ldc, Rs, Ts, R, i0, sb, ws, tid);
-  else panel_factor<TT, 40>(Vs, ldc, Rs, Ts, R, i0, sb, ws, tid);
+  if (nb <= 64) panel_factor<TT, 8, FULL>(Vs, ldc, Rs, Ts, R, i0, sb, ws, tid);
+  else if (nb <= 128) panel_factor<TT, 16, FULL>(Vs, ldc, Rs, Ts, R, i0, sb, ws, tid);
+  else if (nb <= 192) panel_factor<TT, 24, FULL>(Vs, ldc, Rs, Ts, R, i0, sb, ws, tid);
+  else if (nb <= 256) panel_factor<TT, 32, FULL>(Vs, ldc, Rs, Ts, R, i0, sb, ws, tid);
+  else panel_factor<TT, 40, FULL>(Vs, ldc, Rs, Ts, R, i0, sb, ws, tid);
 }
 
 // GEQRT of tiles (k + blockIdx.x, k) on tensor cores: per 32-column block, CTA-wide panel
@@ -404,7 +408,7 @@ template <int W>
 __global__ void __launch_bounds__(QD_T) k_geqrt_tc(double* __restrict__ A, Geo g, int k, int ib,
                                                    double* __restrict__ Tg,
                                                    const uint8_t* __restrict__ dec, int i_first,
-                                                   int spec) {
+                                                   int spec, const int* __restrict__ rows) {
   // predicated on d_k == QR; a speculative launch (spec) also runs while d_k is undecided
   if (dec != nullptr && (spec ? dec[k] == HLQ_DEC_LU : dec[k] != HLQ_DEC_QR)) return;
   extern __shared__ __align__(16) double sm[];
@@ -413,7 +417,7 @@ __global__ void __launch_bounds__(QD_T) k_geqrt_tc(double* __restrict__ A, Geo g
   double* Vs = Cs + qd_cs(W, g.nb);
   double* Us = Vs + 32 * ldc;
   double* Ts = Us + W * LDU;
-  const int i = i_first + blockIdx.x;
+  const int i = rows != nullptr ? rows[blockIdx.x] : i_first + blockIdx.x;
   const int bi = g.bs(i), bk = g.cbs(k);
   double* tile = g.tile(A, i, k);
   double* T = Tg + tri_index(i, k, g.n) * (int64_t)ib * g.nb;
@@ -462,22 +466,17 @@ __global__ void __launch_bounds__(QD_T) k_geqrt_tc(double* __restrict__ A, Geo g
   }
 }
 
-// TTQRT on pairs (e, i) = pairs[blockIdx.x]: [R_e; R_i] -> R_e, V (upper triangle of tile (i,k)), T
-template <int W>
-__global__ void __launch_bounds__(QD_T) k_ttqrt_tc(double* __restrict__ A, Geo g, int k, int ib,
-                                                   double* __restrict__ Ttt,
-                                                   const int2* __restrict__ pairs,
-                                                   const uint8_t* __restrict__ dec, int spec) {
-  if (dec != nullptr && (spec ? dec[k] == HLQ_DEC_LU : dec[k] != HLQ_DEC_QR)) return;
-  extern __shared__ __align__(16) double sm[];
+// TTQRT (TS = false) / TSQRT (TS = true) of the pair (e, i): [R_e; A_i] -> R_e, the
+// reflectors V in tile (i,k) (TT: its upper triangle; TS: the whole square tile), T
+template <int W, bool TS>
+__device__ void qrt_pair(double* __restrict__ A, Geo g, int k, int ib, double* __restrict__ Ttt,
+                         int e, int i, double* sm) {
   const int ldc = qd_ldc(g.nb);
   double* Cs = sm;
   double* Vs = Cs + qd_cs(W, g.nb);
   double* Us = Vs + 32 * ldc;
   double* Ts = Us + W * LDU;
   double* Rs = Cs + PF_WS;       // panel phase: Cs holds the panel scratch, then R_e's block
-  const int2 pr = pairs[blockIdx.x];
-  const int e = pr.x, i = pr.y;
   const int bi = g.bs(i), bk = g.cbs(k);
   double* Re = g.tile(A, e, k);
   double* Ri = g.tile(A, i, k);
@@ -486,7 +485,7 @@ __global__ void __launch_bounds__(QD_T) k_ttqrt_tc(double* __restrict__ A, Geo g
   for (int t = tid; t < ib * g.nb; t += QD_T) T[t] = 0.0;
   for (int i0 = 0; i0 < bk; i0 += ib) {
     const int sb = min(ib, bk - i0);
-    const int R2 = min(bi, i0 + sb);
+    const int R2 = TS ? bi : min(bi, i0 + sb);
     const int RK = (R2 + 31) / 32 * 32;
     __syncthreads();
     cp_cols(Vs, ldc, Ri + (int64_t)i0 * g.lda, g.lda, R2, RK, sb, 32, tid, QD_T);
@@ -497,15 +496,17 @@ __global__ void __launch_bounds__(QD_T) k_ttqrt_tc(double* __restrict__ A, Geo g
     }
     cpa_wait_all();
     __syncthreads();
-    for (int o = tid; o < 32 * RK; o += QD_T) {
-      int l = o / RK, r = o - l * RK;
-      if (r > i0 + l) Vs[l * ldc + r] = 0.0;
+    if (!TS) {
+      for (int o = tid; o < 32 * RK; o += QD_T) {
+        int l = o / RK, r = o - l * RK;
+        if (r > i0 + l) Vs[l * ldc + r] = 0.0;
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    panel_factor_nb<true>(g.nb, Vs, ldc, Rs, Ts, R2, i0, sb, Cs, tid);
+    panel_factor_nb<true, TS>(g.nb, Vs, ldc, Rs, Ts, R2, i0, sb, Cs, tid);
     for (int o = tid; o < sb * R2; o += QD_T) {
       int l = o / R2, r = o - l * R2;
-      if (r <= i0 + l) Ri[(int64_t)(i0 + l) * g.lda + r] = Vs[l * ldc + r];
+      if (TS || r <= i0 + l) Ri[(int64_t)(i0 + l) * g.lda + r] = Vs[l * ldc + r];
     }
     for (int o = tid; o < sb * sb; o += QD_T) {
       int l = o / sb, q = o - l * sb;
@@ -534,6 +535,36 @@ __global__ void __launch_bounds__(QD_T) k_ttqrt_tc(double* __restrict__ A, Geo g
   }
 }
 
+// TTQRT on pairs (e, i) = pairs[blockIdx.x]: [R_e; R_i] -> R_e, V (upper triangle of tile (i,k)), T
+template <int W>
+__global__ void __launch_bounds__(QD_T) k_ttqrt_tc(double* __restrict__ A, Geo g, int k, int ib,
+                                                   double* __restrict__ Ttt,
+                                                   const int2* __restrict__ pairs,
+                                                   const uint8_t* __restrict__ dec, int spec) {
+  if (dec != nullptr && (spec ? dec[k] == HLQ_DEC_LU : dec[k] != HLQ_DEC_QR)) return;
+  extern __shared__ __align__(16) double sm[];
+  const int2 pr = pairs[blockIdx.x];
+  qrt_pair<W, false>(A, g, k, ib, Ttt, pr.x, pr.y, sm);
+}
+
+// TSQRT chains (Alg. 4a): CTA = one group of the HQR tree; its pairs (head, i) =
+// pairs[off[blockIdx.x] .. off[blockIdx.x + 1]) in order, each killing the square tile i with the
+// head's R (the head's R row stays in L2 between the pairs of the chain)
+template <int W>
+__global__ void __launch_bounds__(QD_T) k_tsqrt_tc(double* __restrict__ A, Geo g, int k, int ib,
+                                                   double* __restrict__ Tts,
+                                                   const int2* __restrict__ pairs,
+                                                   const int* __restrict__ off,
+                                                   const uint8_t* __restrict__ dec, int spec) {
+  if (dec != nullptr && (spec ? dec[k] == HLQ_DEC_LU : dec[k] != HLQ_DEC_QR)) return;
+  extern __shared__ __align__(16) double sm[];
+  for (int p = off[blockIdx.x]; p < off[blockIdx.x + 1]; ++p) {
+    const int2 pr = pairs[p];
+    qrt_pair<W, true>(A, g, k, ib, Tts, pr.x, pr.y, sm);
+    __syncthreads();
+  }
+}
+
 template <int W>
 static void launch_panel_w(double* A, Geo g, int k, int ib, double* Tg, double* Ttt,
                            const int2* pairs, int npairs, const uint8_t* dec, bool tt,
@@ -546,7 +577,7 @@ static void launch_panel_w(double* A, Geo g, int k, int ib, double* Tg, double* 
   const size_t smem = qd_smem<W>(g.nb);
   if (!tt) {
     if (g.n - i_first <= 0) return;
-    { ::hlq::g_launches++; k_geqrt_tc<W><<<g.n - i_first, QD_T, smem, st>>>(A, g, k, ib, Tg, dec, i_first, spec ? 1 : 0); }
+    { ::hlq::g_launches++; k_geqrt_tc<W><<<g.n - i_first, QD_T, smem, st>>>(A, g, k, ib, Tg, dec, i_first, spec ? 1 : 0, nullptr); }
   } else {
     { ::hlq::g_launches++; k_ttqrt_tc<W><<<npairs, QD_T, smem, st>>>(A, g, k, ib, Ttt, pairs, dec, spec ? 1 : 0); }
   }
@@ -560,6 +591,39 @@ void launch_qr_panel_tc(double* A, Geo g, int k, int ib, double* Tg, double* Ttt
     launch_panel_w<64>(A, g, k, ib, Tg, Ttt, pairs, npairs, dec, tt, st, i_first, spec);
   else
     launch_panel_w<32>(A, g, k, ib, Tg, Ttt, pairs, npairs, dec, tt, st, i_first, spec);
+}
+
+// GEQRT of the listed tile rows (the HQR tree's group heads), predicated as launch_qr_panel_tc
+void launch_geqrt_rows(double* A, Geo g, int k, int ib, double* Tg, const int* rows, int nrows,
+                       const uint8_t* dec, cudaStream_t st, bool spec) {
+  if (nrows <= 0) return;
+  auto go = [&](auto W_) {
+    constexpr int W = decltype(W_)::value;
+    static unsigned long long attr = 0;
+    if (first_on_device(attr)) smem_optin(k_geqrt_tc<W>);
+    ::hlq::g_launches++;
+    k_geqrt_tc<W><<<nrows, QD_T, qd_smem<W>(g.nb), st>>>(A, g, k, ib, Tg, dec, 0, spec ? 1 : 0,
+                                                          rows);
+  };
+  if (qd_smem<64>(g.nb) <= 227 * 1024) go(std::integral_constant<int, 64>());
+  else go(std::integral_constant<int, 32>());
+}
+
+// TSQRT chains of the HQR tree: one CTA per group (pairs[off[g] .. off[g+1]) in order)
+void launch_tsqrt_chains(double* A, Geo g, int k, int ib, double* Tts, const int2* pairs,
+                         const int* off, int ngroups, const uint8_t* dec, cudaStream_t st,
+                         bool spec) {
+  if (ngroups <= 0) return;
+  auto go = [&](auto W_) {
+    constexpr int W = decltype(W_)::value;
+    static unsigned long long attr = 0;
+    if (first_on_device(attr)) smem_optin(k_tsqrt_tc<W>);
+    ::hlq::g_launches++;
+    k_tsqrt_tc<W><<<ngroups, QD_T, qd_smem<W>(g.nb), st>>>(A, g, k, ib, Tts, pairs, off, dec,
+                                                            spec ? 1 : 0);
+  };
+  if (qd_smem<64>(g.nb) <= 227 * 1024) go(std::integral_constant<int, 64>());
+  else go(std::integral_constant<int, 32>());
 }
 
 // what = 0: UNMQR of all tile rows; what = 1 + l: TTMQR of level l (qr_update.cu, register-slab

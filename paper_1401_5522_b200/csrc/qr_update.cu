@@ -35,17 +35,21 @@ __device__ __forceinline__ void wait_() {
 
 }  // namespace
 
-// UNMQR of every tile row k..n-1 (tt = false, T = GEQRT factors) or TTMQR of one level (tt = true,
-// T = TTQRT factors) on the column block (base, ldc, ncols).  Requires ib = 32 and nb <= 512.
 bool launch_qr_update3(const double* A, Geo g, int k, const double* T, const int2* pairs,
-                       int npairs, bool tt, double* base, int64_t ldc, int64_t ncols,
-                       const uint8_t* dec, cudaStream_t st, double* gmax);
+                       int npairs, int mode, const int* list, double* base, int64_t ldc,
+                       int64_t ncols, const uint8_t* dec, cudaStream_t st, double* gmax);
 
+// UNMQR of every tile row k..n-1 (tt = false, T = GEQRT factors) or TTMQR of one level (tt = true,
+// T = TTQRT factors) on the column block (base, ldc, ncols); returns whether the a12 scan was fused
 bool launch_qr_update2(const double* A, Geo g, int k, const double* T, const int2* pairs,
                        int npairs, bool tt, double* base, int64_t ldc, int64_t ncols,
                        const uint8_t* dec, cudaStream_t st, double* gmax) {
   if (ncols <= 0) return true;
-  if (!launch_qr_update3(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st, gmax)) {
+  const bool ok = tt ? launch_qr_update3(A, g, k, T, pairs, npairs, 1, nullptr, base, ldc, ncols,
+                                         dec, st, gmax)
+                     : launch_qr_update3(A, g, k, T, nullptr, g.n - k, 0, nullptr, base, ldc,
+                                         ncols, dec, st, nullptr);
+  if (!ok) {
     fprintf(stderr, "[hlq] QR update: nb = %d has no register-slab instantiation\n", g.nb);
     abort();
   }
@@ -77,14 +81,15 @@ __device__ __forceinline__ double2 lds2(const double* p) {
 }
 }  // namespace
 
-template <int NB, bool TT, int RQ, int NCG, bool V16>
-__global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ * NCG) : 1) k_qr_update3(const double* __restrict__ A, Geo g, int k,
-                                                   const double* __restrict__ Tbase,
-                                                   const int2* __restrict__ pairs,
-                                                   double* __restrict__ base, int64_t ldcg,
-                                                   int64_t ncols, const uint8_t* __restrict__ dec,
-                                                   double* __restrict__ gmax) {
-  if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
+// MODE 0: UNMQR of tile row i (GEQRT reflectors, unit lower); 1: TTMQR of the pair (e, i) (TT
+// reflectors, upper triangular); 2: TSMQR of the pair (e, i) (TS reflectors, square)
+template <int NB, int MODE, int RQ, int NCG, bool V16>
+__device__ __forceinline__ void qr_update3_body(const double* __restrict__ A, Geo g, int k,
+                                                const double* __restrict__ Tbase, int e, int i,
+                                                double* __restrict__ base, int64_t ldcg,
+                                                int64_t ncols, double* __restrict__ gmax) {
+  constexpr bool TT = MODE != 0;  // pair modes: the eliminator's rows C_e are read-modify-written
+  constexpr bool TS = MODE == 2;
   constexpr int NCH = NB / 32;       // 32-row chunks of a tile
   constexpr int NJ = NB / (8 * RQ);  // 8-row blocks owned by one row group
   constexpr int QPC = 4 / RQ;        // of those, per 32-row chunk
@@ -104,21 +109,12 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, tq = lane & 3;
   const int cg = warp % NCG, rh = warp / NCG;  // column group, row group (RB == rh mod RQ)
-
-  int e = 0, i;
-  if (TT) {
-    const int2 pr = pairs[blockIdx.y];
-    e = pr.x;
-    i = pr.y;
-  } else {
-    i = k + blockIdx.y;
-  }
   const int bi = g.bs(i), bk = g.cbs(k);
   const double* Vt = g.tile(const_cast<double*>(A), i, k);
   const double* T = Tbase + tri_index(i, k, g.n) * (int64_t)32 * g.nb;
   const int64_t c0 = (int64_t)blockIdx.x * W;
   const int cvalid = (int)((ncols - c0) < W ? (ncols - c0) : W);
-  const int crows = TT ? (bi < bk ? bi : bk) : bi;
+  const int crows = (TT && !TS) ? (bi < bk ? bi : bk) : bi;
   double* Cg = base + c0 * ldcg + g.r0(i);
   const int wc = cg * 16;  // first slab column of this warp
 
@@ -146,7 +142,9 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
   const int nblk = (bk + 31) / 32;
   const int nch_i = (crows + 31) / 32;
   auto chunk_lo = [&](int b) { return TT ? 0 : b; };
-  auto chunk_hi = [&](int b) { return TT ? (b < nch_i - 1 ? b : nch_i - 1) : nch_i - 1; };
+  auto chunk_hi = [&](int b) {
+    return (TT && !TS) ? (b < nch_i - 1 ? b : nch_i - 1) : nch_i - 1;
+  };
   // the chunk schedule (block, pass, chunk) of the whole CTA, built once: the producer is a table
   // lookup per chunk
   constexpr int MAXS = 2 * NCH * (NCH + 1) / 2 + 2;
@@ -227,20 +225,22 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
     }
     commit_();
   };
-  // a TT merge of a tile with <= 32 rows has one chunk per pass in every block: prefetch 3 chunks
-  // ahead instead of 4 so block b + 2's T / C_e never overwrite block b's before its TRMM
+  // a TT / TS merge of a tile with <= 32 rows has one chunk per pass in every block: prefetch 3
+  // chunks ahead instead of 4 so block b + 2's T / C_e never overwrite block b's before its TRMM
   const bool short3 = TT && nch_i == 1;
 #pragma unroll 1
   for (int d = 0; d < (short3 ? RING - 2 : RING - 1); ++d) issue();
   // explicit structure of the diagonal 32 x 32 block of V_b (GEQRT: unit diagonal, zeros above;
   // TT: zeros below the diagonal); element (r, l) at V[r * sr + l * sl]
   auto fix_diag = [&](double* V, int sr, int sl) {
-    for (int o = tid; o < 1024; o += NT) {
-      const int l = o >> 5, r = o & 31;
-      if (TT) {
-        if (r > l) V[r * sr + l * sl] = 0.0;
-      } else {
-        if (r <= l) V[r * sr + l * sl] = (r == l) ? 1.0 : 0.0;
+    if constexpr (!TS) {  // a square TS reflector block has no structure
+      for (int o = tid; o < 1024; o += NT) {
+        const int l = o >> 5, r = o & 31;
+        if (TT) {
+          if (r > l) V[r * sr + l * sl] = 0.0;
+        } else {
+          if (r <= l) V[r * sr + l * sl] = (r == l) ? 1.0 : 0.0;
+        }
       }
     }
   };
@@ -443,54 +443,94 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
   }
 }
 
+// UNMQR of tile rows i = rows[blockIdx.y] (rows == nullptr: k + blockIdx.y)
+template <int NB, int RQ, int NCG, bool V16>
+__global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ * NCG) : 1)
+    k_unmqr3(const double* __restrict__ A, Geo g, int k, const double* __restrict__ Tbase,
+             const int* __restrict__ rows, double* __restrict__ base, int64_t ldcg, int64_t ncols,
+             const uint8_t* __restrict__ dec) {
+  if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
+  const int i = rows != nullptr ? rows[blockIdx.y] : k + (int)blockIdx.y;
+  qr_update3_body<NB, 0, RQ, NCG, V16>(A, g, k, Tbase, 0, i, base, ldcg, ncols, nullptr);
+}
+
+// TTMQR of the pairs of one level (pair = blockIdx.y)
+template <int NB, int RQ, int NCG, bool V16>
+__global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ * NCG) : 1)
+    k_ttmqr3(const double* __restrict__ A, Geo g, int k, const double* __restrict__ Tbase,
+             const int2* __restrict__ pairs, double* __restrict__ base, int64_t ldcg,
+             int64_t ncols, const uint8_t* __restrict__ dec, double* __restrict__ gmax) {
+  if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
+  const int2 pr = pairs[blockIdx.y];
+  qr_update3_body<NB, 1, RQ, NCG, V16>(A, g, k, Tbase, pr.x, pr.y, base, ldcg, ncols, gmax);
+}
+
+// TSMQR chains of the HQR tree (group = blockIdx.y): the group's pairs in order, each applying
+// Q_i^T to [C_head; C_i] (the head's rows read-modify-written per reflector block, C_i in registers)
+template <int NB, int RQ, int NCG, bool V16>
+__global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ * NCG) : 1)
+    k_tsmqr3(const double* __restrict__ A, Geo g, int k, const double* __restrict__ Tbase,
+             const int2* __restrict__ pairs, const int* __restrict__ off,
+             double* __restrict__ base, int64_t ldcg, int64_t ncols,
+             const uint8_t* __restrict__ dec, double* __restrict__ gmax) {
+  if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
+  for (int p = off[blockIdx.y]; p < off[blockIdx.y + 1]; ++p) {
+    const int2 pr = pairs[p];
+    qr_update3_body<NB, 2, RQ, NCG, V16>(A, g, k, Tbase, pr.x, pr.y, base, ldcg, ncols, gmax);
+    __syncthreads();  // the head's rows and the ring are reused by the next pair
+  }
+}
+
 static size_t upd3_smem(int warps, int W) {
   return sizeof(double) * ((size_t)7 * CH3 + (size_t)warps * 512 + (size_t)2 * W * LD3);
 }
 
 template <int NB, int RQ, int NCG, bool V16>
 static void launch3(const double* A, Geo g, int k, const double* T, const int2* pairs, int npairs,
-                    bool tt, double* base, int64_t ldc, int64_t ncols, const uint8_t* dec,
-                    cudaStream_t st, double* gmax) {
+                    int mode, const int* list, double* base, int64_t ldc, int64_t ncols,
+                    const uint8_t* dec, cudaStream_t st, double* gmax) {
   static unsigned long long attr = 0;
   if (first_on_device(attr)) {
-    smem_optin(k_qr_update3<NB, false, RQ, NCG, V16>);
-    smem_optin(k_qr_update3<NB, true, RQ, NCG, V16>);
+    smem_optin(k_unmqr3<NB, RQ, NCG, V16>);
+    smem_optin(k_ttmqr3<NB, RQ, NCG, V16>);
+    smem_optin(k_tsmqr3<NB, RQ, NCG, V16>);
   }
   const unsigned slabs = (unsigned)((ncols + 16 * NCG - 1) / (16 * NCG));
   const size_t smem = upd3_smem(RQ * NCG, 16 * NCG);
-  if (!tt) {
-    ::hlq::g_launches++;
-    k_qr_update3<NB, false, RQ, NCG, V16><<<dim3(slabs, g.n - k), 32 * RQ * NCG, smem, st>>>(
-        A, g, k, T, nullptr, base, ldc, ncols, dec, nullptr);
-  } else {
-    if (npairs <= 0) return;
-    ::hlq::g_launches++;
-    k_qr_update3<NB, true, RQ, NCG, V16><<<dim3(slabs, npairs), 32 * RQ * NCG, smem, st>>>(
+  if (npairs <= 0) return;
+  ::hlq::g_launches++;
+  if (mode == 0)  // npairs = number of tile rows (list: the rows, or nullptr for k..)
+    k_unmqr3<NB, RQ, NCG, V16><<<dim3(slabs, npairs), 32 * RQ * NCG, smem, st>>>(
+        A, g, k, T, list, base, ldc, ncols, dec);
+  else if (mode == 1)
+    k_ttmqr3<NB, RQ, NCG, V16><<<dim3(slabs, npairs), 32 * RQ * NCG, smem, st>>>(
         A, g, k, T, pairs, base, ldc, ncols, dec, gmax);
-  }
+  else  // npairs = number of groups, list = their pair offsets
+    k_tsmqr3<NB, RQ, NCG, V16><<<dim3(slabs, npairs), 32 * RQ * NCG, smem, st>>>(
+        A, g, k, T, pairs, list, base, ldc, ncols, dec, gmax);
 }
 
-// v3 for every nb <= 320 (instantiated at 64, 128, 192, 256, 320); false -> the caller falls back to v2
+// register-slab kernels for every nb <= 320 (instantiated at 64, 128, 192, 256, 320: a smaller
+// tile size is the next instantiation's ragged case, every row, column and reflector bound being a
+// runtime mask, e.g. the paper's nb = 240 runs on NB = 256).  mode 0: UNMQR of npairs tile rows
+// (list = the rows or nullptr for k..); 1: TTMQR of npairs pairs; 2: TSMQR chains of npairs groups
+// (list = pair offsets).  false: nb has no instantiation.
 bool launch_qr_update3(const double* A, Geo g, int k, const double* T, const int2* pairs,
-                       int npairs, bool tt, double* base, int64_t ldc, int64_t ncols,
-                       const uint8_t* dec, cudaStream_t st, double* gmax) {
+                       int npairs, int mode, const int* list, double* base, int64_t ldc,
+                       int64_t ncols, const uint8_t* dec, cudaStream_t st, double* gmax) {
   if (ncols <= 0) return true;
   // 16-byte V copies need an even leading dimension, a 16-byte aligned matrix and even tile heights
   const bool v16 = ((g.lda & 1) == 0) && ((((uintptr_t)A) & 15) == 0) && ((g.N & 1) == 0) &&
                    ((g.nb & 1) == 0) && ((ldc & 1) == 0) && ((((uintptr_t)base) & 15) == 0);
-  static int ncg = -1;
-  if (ncg < 0) ncg = getenv("HLQ_QR3_NCG") ? atoi(getenv("HLQ_QR3_NCG")) : 2;
-#define HLQ_L3(NBV)                                                                        \
-  case NBV:                                                                                \
-    if (!v16)                                                                              \
-      launch3<NBV, 2, 2, false>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st, gmax); \
-    else if (ncg == 4)                                                                     \
-      launch3<NBV, 2, 4, true>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st, gmax);  \
-    else                                                                                   \
-      launch3<NBV, 2, 2, true>(A, g, k, T, pairs, npairs, tt, base, ldc, ncols, dec, st, gmax);  \
+#define HLQ_L3(NBV)                                                                           \
+  case NBV:                                                                                   \
+    if (!v16)                                                                                 \
+      launch3<NBV, 2, 2, false>(A, g, k, T, pairs, npairs, mode, list, base, ldc, ncols, dec, st, \
+                                gmax);                                                        \
+    else                                                                                      \
+      launch3<NBV, 2, 2, true>(A, g, k, T, pairs, npairs, mode, list, base, ldc, ncols, dec, st,  \
+                               gmax);                                                         \
     return true;
-  // the instantiation with the next tile size up: smaller tiles are its ragged case (every row,
-  // column and reflector bound is a runtime mask), e.g. the paper's nb = 240 runs on NB = 256
   const int nbi = g.nb <= 64 ? 64 : g.nb <= 128 ? 128 : g.nb <= 192 ? 192 : g.nb <= 256 ? 256 : 320;
   switch (nbi) {
     HLQ_L3(64)
@@ -501,6 +541,27 @@ bool launch_qr_update3(const double* A, Geo g, int k, const double* T, const int
     default: return false;
   }
 #undef HLQ_L3
+}
+
+static void must(bool ok, int nb) {
+  if (!ok) {
+    fprintf(stderr, "[hlq] QR update: nb = %d has no register-slab instantiation\n", nb);
+    abort();
+  }
+}
+
+void launch_unmqr_rows(const double* A, Geo g, int k, const double* T, const int* rows, int nrows,
+                       double* base, int64_t ldc, int64_t ncols, const uint8_t* dec,
+                       cudaStream_t st) {
+  must(launch_qr_update3(A, g, k, T, nullptr, nrows, 0, rows, base, ldc, ncols, dec, st, nullptr),
+       g.nb);
+}
+
+void launch_tsmqr_chains(const double* A, Geo g, int k, const double* T, const int2* pairs,
+                         const int* off, int ngroups, double* base, int64_t ldc, int64_t ncols,
+                         const uint8_t* dec, cudaStream_t st, double* gmax) {
+  must(launch_qr_update3(A, g, k, T, pairs, ngroups, 2, off, base, ldc, ncols, dec, st, gmax),
+       g.nb);
 }
 
 }  // namespace hlq

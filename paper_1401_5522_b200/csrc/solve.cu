@@ -5,6 +5,8 @@
 // status scan (non-finite factors, exact zeros on the U/R diagonal).
 #include <math.h>
 
+#include <algorithm>
+
 #include "hlq_internal.cuh"
 
 namespace hlq {
@@ -207,6 +209,246 @@ void launch_solve_back_inv(const double* A, Geo g, int k, const double* Ui, doub
   { ::hlq::g_launches++; k_tri_gemv<false><<<(bk + 31) / 32, 256, 0, st>>>(Ui, g.nb, bk, nullptr, x + k0, t); }
   cudaMemcpyAsync(x + k0, t, sizeof(double) * bk, cudaMemcpyDeviceToDevice, st);
   launch_gemv_sub(x, A + k0 * g.lda, g.lda, k0, bk, x + k0, st);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Persistent block-row solves: one launch per pass over many block rows, so the n sequential
+// dependencies of the solve do not each cost a kernel launch and the factor reads of independent
+// tiles overlap the dependency chain.  Work unit (i, c): block row i, chunk c of G tiles of that
+// row (left of the diagonal in the forward pass, right of it in the back substitution).  Units
+// take tickets in start order (atomic counter) from a host-built table ordered so that a unit only
+// ever waits for units with smaller tickets -- units that are already running -- so the spin waits
+// cannot deadlock.  A chunk publishes its partial sums (pflag); the LAST chunk of row i (the
+// finisher) adds them in chunk order (deterministic), then solves the diagonal tile by blocked
+// substitution and publishes x_i (xflag).  Release/acquire at GPU scope order the data.
+constexpr int PS_T = 256;
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wait_flag(const int* p, int want) {
+  while (ld_acquire(p) != want) __nanosleep(32);
+}
+
+// acc[s][e] += sum over columns c (c = h, h+2, ...) of T(row 2q+256s+e, c) * xs[c]
+__device__ __forceinline__ void gemv_tile(const double* __restrict__ T, int64_t lda, int rows,
+                                          int cols, const double* xs, int q, int h,
+                                          double (&acc)[2][2]) {
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int r = 2 * q + 256 * s;
+    if (r >= rows) continue;
+    const bool two = r + 1 < rows;
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll 8
+    for (int c = h; c < cols; c += 2) {
+      const double* col = T + (int64_t)c * lda + r;
+      const double xv = xs[c];
+      a0 = fma(__ldg(col), xv, a0);
+      if (two) a1 = fma(__ldg(col + 1), xv, a1);
+    }
+    acc[s][0] += a0;
+    acc[s][1] += a1;
+  }
+}
+
+// ys (bi entries, shared) <- L^-1 ys, L = unit lower triangle of the tile at D (ld lda)
+__device__ void tile_lower_unit_solve(const double* __restrict__ D, int64_t lda, int bi, double* ys,
+                                      int tid) {
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int base = 0; base < bi; base += 32) {
+    if (warp == 0) {
+      const int r = base + lane;
+      double lv[32];
+#pragma unroll
+      for (int cc = 0; cc < 32; ++cc)
+        lv[cc] = (cc < lane && r < bi) ? __ldg(D + (int64_t)(base + cc) * lda + r) : 0.0;
+      double v = r < bi ? ys[r] : 0.0;
+#pragma unroll
+      for (int cc = 0; cc < 32; ++cc) {
+        const double xc = __shfl_sync(0xffffffffu, v, cc);
+        if (lane > cc) v = fma(-lv[cc], xc, v);
+      }
+      if (r < bi) ys[r] = v;
+    }
+    __syncthreads();
+    const int pw = min(32, bi - base);
+    for (int r = base + 32 + tid; r < bi; r += PS_T) {
+      double a = 0.0;
+      for (int cc = 0; cc < pw; ++cc) a = fma(__ldg(D + (int64_t)(base + cc) * lda + r), ys[base + cc], a);
+      ys[r] -= a;
+    }
+    __syncthreads();
+  }
+}
+
+// ys <- U^-1 ys, U = upper triangle (non-unit) of the tile at D (ld lda)
+__device__ void tile_upper_solve(const double* __restrict__ D, int64_t lda, int bi, double* ys,
+                                 int tid) {
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int base = (bi - 1) / 32 * 32; base >= 0; base -= 32) {
+    if (warp == 0) {
+      const int r = base + lane;
+      double lv[32];
+#pragma unroll
+      for (int cc = 0; cc < 32; ++cc)
+        lv[cc] = (cc > lane && base + cc < bi) ? __ldg(D + (int64_t)(base + cc) * lda + r) : 0.0;
+      const double d = r < bi ? __ldg(D + (int64_t)r * lda + r) : 1.0;
+      double v = r < bi ? ys[r] : 0.0;
+#pragma unroll
+      for (int cc = 31; cc >= 0; --cc) {
+        if (lane == cc) v = v / d;
+        const double xc = __shfl_sync(0xffffffffu, v, cc);
+        if (lane < cc) v = fma(-lv[cc], xc, v);
+      }
+      if (r < bi) ys[r] = v;
+    }
+    __syncthreads();
+    const int pw = min(32, bi - base);
+    for (int r = tid; r < base; r += PS_T) {
+      double a = 0.0;
+      for (int cc = 0; cc < pw; ++cc) a = fma(__ldg(D + (int64_t)(base + cc) * lda + r), ys[base + cc], a);
+      ys[r] -= a;
+    }
+    __syncthreads();
+  }
+}
+
+// FWD: forward pass of the LU steps [ka, kb) over block rows i >= ka (x_i -= sum_j L_ij x_j, then
+// x_i <- L_ii^-1 P_i x_i for i < kb).  BACK: back substitution over all block rows
+// (x_i <- U_ii^-1 (x_i - sum_{j>i} U_ij x_j)).
+template <bool FWD>
+__global__ void __launch_bounds__(PS_T) k_solve_rows(const double* __restrict__ A, Geo g, int ka,
+                                                     int kb, int G, int cmax,
+                                                     const int2* __restrict__ units,
+                                                     const int* __restrict__ perm_all,
+                                                     double* __restrict__ x, int* __restrict__ xflag,
+                                                     double* __restrict__ part,
+                                                     int* __restrict__ pflag,
+                                                     unsigned* __restrict__ ticket) {
+  __shared__ int2 s_u;
+  __shared__ double xs[HLQ_MAX_NB];
+  __shared__ double ys[HLQ_MAX_NB];
+  __shared__ double red[2][HLQ_MAX_NB];
+  const int tid = threadIdx.x, q = tid & 127, h = tid >> 7;
+  if (tid == 0) s_u = units[atomicAdd(ticket, 1u)];
+  __syncthreads();
+  const int i = s_u.x, c = s_u.y;
+  const int bi = g.bs(i), nb = g.nb;
+  // tiles of this unit, in the order their x_j become available
+  int jfirst, ntiles, cn;
+  if (FWD) {
+    const int jend = min(i, kb);
+    cn = max(1, (jend - ka + G - 1) / G);
+    jfirst = ka + c * G;
+    ntiles = max(0, min(G, jend - jfirst));
+  } else {
+    cn = max(1, (g.n - 1 - i + G - 1) / G);
+    jfirst = g.n - 1 - c * G;  // descending
+    ntiles = max(0, min(G, jfirst - i));
+  }
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  for (int t = 0; t < ntiles; ++t) {
+    const int j = FWD ? jfirst + t : jfirst - t;
+    const int bj = g.bs(j);
+    if (tid == 0) wait_flag(xflag + j, 1);
+    __syncthreads();
+    for (int cc = tid; cc < bj; cc += PS_T) xs[cc] = __ldcg(x + g.r0(j) + cc);
+    __syncthreads();
+    gemv_tile(A + g.r0(j) * g.lda + g.r0(i), g.lda, bi, bj, xs, q, h, acc);
+    __syncthreads();
+  }
+  // the two column halves' partial sums, per row
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int r = 2 * q + 256 * s + e;
+      if (r < bi) red[h][r] = acc[s][e];
+    }
+  __syncthreads();
+  double* my_part = part + ((int64_t)i * cmax + c) * nb;
+  if (c + 1 < cn) {  // not the finisher: publish the partial sums of this chunk
+    for (int r = tid; r < bi; r += PS_T) __stcg(my_part + r, red[0][r] + red[1][r]);
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) st_release(pflag + (int64_t)i * cmax + c, 1);
+    return;
+  }
+  // finisher: r_i = x_i - (sum of the chunk partials in chunk order + own)
+  if (tid == 0)
+    for (int cc = 0; cc < c; ++cc) wait_flag(pflag + (int64_t)i * cmax + cc, 1);
+  __syncthreads();
+  double* xi = x + g.r0(i);
+  for (int r = tid; r < bi; r += PS_T) {
+    double sum = 0.0;
+    for (int cc = 0; cc < c; ++cc) sum += __ldcg(part + ((int64_t)i * cmax + cc) * nb + r);
+    sum += red[0][r] + red[1][r];
+    xs[r] = __ldcg(xi + r) - sum;
+  }
+  __syncthreads();
+  if (FWD && i >= kb) {  // a row below the run: only the update
+    for (int r = tid; r < bi; r += PS_T) xi[r] = xs[r];
+    return;
+  }
+  const double* D = A + g.r0(i) * g.lda + g.r0(i);
+  if (FWD) {
+    const int* perm = perm_all + (int64_t)i * nb;  // row r of P_i x = x[perm[r]]
+    for (int r = tid; r < bi; r += PS_T) ys[r] = xs[perm[r]];
+    __syncthreads();
+    tile_lower_unit_solve(D, g.lda, bi, ys, tid);
+  } else {
+    for (int r = tid; r < bi; r += PS_T) ys[r] = xs[r];
+    __syncthreads();
+    tile_upper_solve(D, g.lda, bi, ys, tid);
+  }
+  for (int r = tid; r < bi; r += PS_T) __stcg(xi + r, ys[r]);
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) st_release(xflag + i, 1);
+}
+
+// Host side: unit table (ticket order) for one pass; the device buffers come from the handle's
+// solve workspace (xflag n ints, pflag n*cmax ints, part n*cmax*nb doubles, ticket, units).
+int solve_rows_cmax(int n, int G) { return std::max(1, (n + G - 1) / G); }
+
+size_t build_solve_units(bool fwd, int n, int ka, int kb, int G, int2* out) {
+  size_t u = 0;
+  if (fwd) {
+    for (int i = ka; i < n; ++i) {
+      const int jend = std::min(i, kb);
+      const int cn = std::max(1, (jend - ka + G - 1) / G);
+      for (int c = 0; c < cn; ++c) out[u++] = make_int2(i, c);
+    }
+  } else {
+    for (int i = n - 1; i >= 0; --i) {
+      const int cn = std::max(1, (n - 1 - i + G - 1) / G);
+      for (int c = 0; c < cn; ++c) out[u++] = make_int2(i, c);
+    }
+  }
+  return u;
+}
+
+void launch_solve_rows(bool fwd, const double* A, Geo g, int ka, int kb, int G, const int2* units,
+                       size_t nunits, const int* perm_all, double* x, int* xflag, double* part,
+                       int* pflag, unsigned* ticket, cudaStream_t st) {
+  if (nunits == 0) return;
+  const int cmax = solve_rows_cmax(g.n, G);
+  cudaMemsetAsync(ticket, 0, sizeof(unsigned), st);
+  cudaMemsetAsync(xflag, 0, sizeof(int) * (size_t)g.n, st);
+  cudaMemsetAsync(pflag, 0, sizeof(int) * (size_t)g.n * cmax, st);
+  ::hlq::g_launches++;
+  if (fwd)
+    k_solve_rows<true><<<(unsigned)nunits, PS_T, 0, st>>>(A, g, ka, kb, G, cmax, units, perm_all,
+                                                          x, xflag, part, pflag, ticket);
+  else
+    k_solve_rows<false><<<(unsigned)nunits, PS_T, 0, st>>>(A, g, ka, kb, G, cmax, units, perm_all,
+                                                           x, xflag, part, pflag, ticket);
 }
 
 // ---------------------------------------------------------------------------------------------

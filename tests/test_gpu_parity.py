@@ -91,7 +91,7 @@ def check_decision_record(fo, f, hinted_run: bool, forced: bool = False, diff: f
 
 
 def run_pair(H, A, b, nb, crit=O.CRIT_MAX, alpha=1.0, D=1, forced=None, mumps_reading=0,
-             invnorm="exact", tie_rel_tol=1e-10, lu_variant="A1", pivot_scope="tile"):
+             invnorm="exact", tie_rel_tol=1e-10, lu_variant="A1", pivot_scope="tile", tree="greedy"):
     N = A.shape[0]
     pre = {}
 
@@ -100,13 +100,15 @@ def run_pair(H, A, b, nb, crit=O.CRIT_MAX, alpha=1.0, D=1, forced=None, mumps_re
         pre[k] = Ab[sl, sl].copy()
     fo = O.hybrid_factor(A, nb, crit, alpha, D=D, forced=forced, mumps_reading=mumps_reading,
                          on_step=hook, invnorm=invnorm, lu_variant=lu_variant,
-                         pivot_scope=pivot_scope)
+                         pivot_scope=pivot_scope, tree=tree)
     fo.pre_tiles = pre
     dA = H.to_colmajor(A)
     kw = dict(tree_domains=D, mumps_reading=mumps_reading,
               invnorm_estimate=1 if invnorm == "estimate" else 0, tie_rel_tol=tie_rel_tol,
               lu_variant=H.LU_A2 if lu_variant == "A2" else H.LU_A1,
-              pivot_scope=H.PIVOT_DOMAIN if pivot_scope == "domain" else H.PIVOT_TILE)
+              pivot_scope=H.PIVOT_DOMAIN if pivot_scope == "domain" else H.PIVOT_TILE,
+              tree=H.TREE_HQR if tree.startswith("hqr") else H.TREE_GREEDY,
+              ts_group=int(tree[3:]) if tree.startswith("hqr") else 0)
     if forced is not None:
         f = H.hlq_factor_ex(dA, N, nb, crit, alpha, forced=forced, **kw)
         fo.hinted_run = False
@@ -458,3 +460,46 @@ def test_domain_pivoting_parity(H, N, nb, D, crit, alpha, gen, forced_f):
     if D == 1:  # LUPP: the solution of LAPACK's dgesv
         assert np.all(fo.dec == O.LU)
         assert np.allclose(x, np.linalg.solve(A, b), rtol=0, atol=1e-9 * np.abs(x).max())
+
+
+# ---------------------------------------------------------------------------------------------
+# Row a9: the HQR tree with square-tile TS eliminations (TSQRT chains, TSMQR chain updates;
+# DESIGN.md reading 34) against the oracle's tree="hqrA"
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("N,nb,tree,D,crit,alpha,forced_f", [
+    (1024, 128, "hqr4", 1, O.CRIT_MAX, 0.0, None),      # all QR: 2 groups of 4 + the TT merge
+    (1024, 128, "hqr2", 1, O.CRIT_MAX, 1.0, None),      # criterion: QQQQQQQL
+    (1024, 64, "hqr4", 1, O.CRIT_MAX, 1.2e4, None),     # LU / QR mix
+    (1000, 128, "hqr3", 1, O.CRIT_MAX, 0.0, None),      # ragged last tile (104 rows) in a group
+    (1000, 64, "hqr5", 2, O.CRIT_MAX, 1.0, None),       # two domains, groups of 5
+    (928, 128, "hqr4", 1, O.CRIT_MAX, 0.0, None),       # last tile of 32 rows (one chunk)
+    (1200, 240, "hqr4", 1, O.CRIT_MAX, 1.0, None),      # the paper's nb = 240
+    (1000, 320, "hqr2", 1, O.CRIT_MAX, 1.0, None),      # nb = 320, ragged
+    (1024, 64, "hqr16", 1, O.CRIT_MAX, 0.0, None),      # one group: flat TS (the chain of 15)
+    (960, 64, "hqr4", 1, O.CRIT_MAX, 1.0, 0.5),         # forced Bernoulli pattern
+    (1024, 128, "hqr4", 1, O.CRIT_SUM, 1e6, None),
+    (1024, 128, "hqr4", 1, O.CRIT_MUMPS, 1.5, None),
+])
+def test_hqr_ts_tree_parity(H, N, nb, tree, D, crit, alpha, forced_f):
+    A, b = (I.normal_system(1, N) if crit == O.CRIT_MUMPS
+            else (I.uniform_matrix(7, N), I.uniform_rhs(7, N)))
+    n = (N + nb - 1) // nb
+    forced = I.bernoulli_pattern(30, n, forced_f) if forced_f is not None else None
+    fo, f, F, x = run_pair(H, A, b, nb, crit, alpha, D=D, forced=forced, tree=tree)
+    check_parity(fo, f, F, x, A, b, forced=forced is not None)
+    # T factors of the TS eliminations (kind 1) and of the group heads' GEQRTs (kind 0)
+    for k, d in fo.qr.items():
+        for i, T in d.T_ts.items():
+            assert np.linalg.norm(f.T(i, k, 1) - T) <= 1e-11 * max(1.0, np.linalg.norm(T))
+        for i, T in d.T_geqrt.items():
+            assert np.linalg.norm(f.T(i, k, 0) - T) <= 1e-11 * max(1.0, np.linalg.norm(T))
+
+
+def test_hqr_tree_a2_variant(H):
+    """HQR with LU variant A2: a QR decision continues from the diagonal tile's GEQRT (the head of
+    its group), the TS chains then kill the rest of the group."""
+    A, b = I.uniform_matrix(0, 1024), I.uniform_rhs(0, 1024)
+    fo, f, F, x = run_pair(H, A, b, 128, O.CRIT_MAX, 1.2e4, lu_variant="A2", tree="hqr4")
+    np.testing.assert_array_equal(f.decisions(), fo.dec)
+    assert O.factor_diff(F, fo.A) <= 1e-10
+    assert O.hpl3(A, x, b) <= 16.0

@@ -340,7 +340,7 @@ def test_all_lu_path_is_restricted_pivot_gaussian_elimination(N, nb):
     assert rel(f.A, G) < 1e-11
 
 
-@pytest.mark.parametrize("tree", ["greedy", "flat"])
+@pytest.mark.parametrize("tree", ["greedy", "flat", "hqr2", "hqr4", "hqr16"])
 @pytest.mark.parametrize("N,nb,D", [(128, 32, 1), (160, 32, 2), (150, 32, 3), (224, 16, 1)])
 def test_all_qr_path_reproduces_householder_R(N, nb, D, tree):
     A, b = I.normal_system(9, N)
@@ -436,6 +436,35 @@ def test_greedy_plan_structure():
         assert live == {k}
         if D == 1:
             assert len(levels) == math.ceil(math.log2(n - k)) if n - k > 1 else len(levels) == 0
+
+
+@pytest.mark.parametrize("a", [1, 2, 3, 4, 7, 40])
+def test_hqr_plan_structure(a):
+    """HQR tree with TS groups of a tiles (DESIGN reading 34): every row
+    i > k is eliminated exactly once; a TS elimination has a live group head as eliminator that is
+    a GEQRT row, the eliminated rows of a group follow their head in ascending order; TT levels run
+    over GEQRT rows only, pairs disjoint, and only row k survives.  a = 1 is the greedy tree."""
+    for n, k, D in ((9, 0, 1), (16, 3, 1), (17, 0, 2), (30, 5, 4), (5, 4, 1), (40, 0, 1)):
+        rows, ts, levels = O.qr_plan(k, n, D, f"hqr{a}")
+        if a == 1:
+            assert (rows, ts, levels) == O.qr_plan(k, n, D, "greedy")
+        live = set(range(k, n))
+        for e, i in ts:
+            assert e in rows and i not in rows and e < i and e % D == i % D
+            assert e in live and i in live
+            live.discard(i)
+        assert set(rows) == live  # every non-head was killed by TS, every head is GEQRT'd
+        for lvl in levels:
+            used = [r for p in lvl for r in p]
+            assert len(used) == len(set(used))
+            for e, i in lvl:
+                assert e in live and i in live and e < i
+            for e, i in lvl:
+                live.discard(i)
+        assert live == {k}
+        # group size: at most a - 1 TS eliminations per head
+        from collections import Counter
+        assert max(Counter(e for e, _ in ts).values(), default=0) <= a - 1
 
 
 def test_table_i_sums_and_table_ii_arithmetic():
