@@ -33,8 +33,9 @@
 extern "C" {
 #endif
 
-/* criteria (Eqs. 2-4) */
-enum { HLQ_CRIT_MAX = 0, HLQ_CRIT_SUM = 1, HLQ_CRIT_MUMPS = 2 };
+/* criteria (Eqs. 2-4) and the paper's Random choice (reading 35: alpha is
+ * the LU percentage, LU iff 100 u_k < alpha with u_k the counter generator's draw k of stream 31) */
+enum { HLQ_CRIT_MAX = 0, HLQ_CRIT_SUM = 1, HLQ_CRIT_MUMPS = 2, HLQ_CRIT_RANDOM = 3 };
 /* decision of a step (Alg. 1 "Perform an LU step" / "Perform a QR step") */
 enum { HLQ_DEC_LU = 0, HLQ_DEC_QR = 1 };
 /* QR elimination tree (Alg. 3 + HQR trees P:296-305; readings 16
@@ -155,6 +156,15 @@ int hlq_get_info(hlq_factors_t f, hlq_info* info);
 int hlq_get_decisions(hlq_factors_t f, uint8_t* dec);       /* n entries, HLQ_DEC_*          */
 int hlq_get_margins(hlq_factors_t f, double* margin);       /* n entries (NaN when forced)   */
 int hlq_get_step_flags(hlq_factors_t f, int32_t* flags);    /* n entries, HLQ_FLAG_* bits    */
+/* Decision log: 2n entries, per step the two sides of the binding inequality of its
+ * criterion -- Max / Sum: alpha / ||A_kk^-1||_1 and max / sum of ||A_ik||_1; MUMPS: alpha |U_jj| and
+ * the estimate of the column with the smallest margin; Random: alpha and 100 u_k; NaN when no
+ * criterion ran (forced, alpha = 0 or inf, zero pivot). */
+int hlq_get_step_log(hlq_factors_t f, double* log2n);
+/* Per-step device times (opt.profile = 1): n entries, ms between the ends of consecutive update
+ * stages on the factorization's stream (with the lookahead, step k+1's panel overlaps step k).
+ * HLQ_ERR_STATE when the handle was not profiled. */
+int hlq_get_step_times(hlq_factors_t f, double* ms);
 int hlq_get_growth(hlq_factors_t f, double* growth);
 int hlq_get_pivots(hlq_factors_t f, int32_t* ipiv);         /* n*nb entries: step k at k*nb, 0-based
                                                                row within the tile (LAPACK sequential

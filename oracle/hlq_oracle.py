@@ -30,7 +30,8 @@ import numpy as np
 from scipy.linalg import solve_triangular
 
 LU, QR = 0, 1
-CRIT_MAX, CRIT_SUM, CRIT_MUMPS = 0, 1, 2
+CRIT_MAX, CRIT_SUM, CRIT_MUMPS, CRIT_RANDOM = 0, 1, 2, 3
+RANDOM_SEED = 31  # the Random criterion's counter stream (reading 35)
 EPS_HPL = 2.0 ** -53  # ledger 20: LAPACK dlamch('E'), as HPL uses ("machine precision")
 
 # status bits (mirrors the meaning, not the code, of include/hlq.h)
@@ -303,6 +304,28 @@ def criterion_max_sum(crit: int, alpha: float, inv_norm: float, s: np.ndarray):
     if math.isnan(lhs) or math.isnan(rhs):
         return False, float("nan")  # ledger 22
     return lhs >= rhs, _rel_margin(lhs, rhs)
+
+
+def _splitmix_unit(seed: int, idx: int) -> float:
+    """The counter-based uniform on [0, 1) of the input recipe (SplitMix64 finalizer of
+    key(seed) + (idx+1) * gamma, top 53 bits), written out with plain Python integers: the
+    Random criterion's draws (each side implements the same generator; no arithmetic is shared)."""
+    M = (1 << 64) - 1
+    gamma = 0x9E3779B97F4A7C15
+
+    def mix(z):
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+        return z ^ (z >> 31)
+    key = mix((seed + gamma) & M)
+    return (mix((key + (idx + 1) * gamma) & M) >> 11) * 2.0 ** -53
+
+
+def criterion_random(alpha: float, k: int) -> bool:
+    """The Random criterion of the paper's experiments (alpha = 50 in P:953):
+    "a random choice between LU and QR at each step"; alpha is the LU percentage:
+    LU iff 100 u_k < alpha, u_k the step's draw (reading 35)."""
+    return _splitmix_unit(RANDOM_SEED, k) * 100.0 < alpha
 
 
 def criterion_mumps(alpha: float, W: np.ndarray, local_max: np.ndarray, away_max: np.ndarray,
@@ -857,9 +880,13 @@ def hybrid_factor(A_in: np.ndarray, nb: int, crit: int = CRIT_MAX, alpha: float 
                 else:
                     inv = inv_norm1_from_lu(W) if invnorm == "exact" else inv_norm1_estimate(W)
                 lu, mg = criterion_max_sum(crit, alpha, inv, s)
+            elif crit == CRIT_RANDOM:
+                lu, mg = criterion_random(alpha, k), float("nan")
             else:
                 lu, mg = criterion_mumps(alpha, W, lmax, amax, mumps_reading)
-            if math.isnan(mg):
+            if crit == CRIT_RANDOM:  # no criterion value: no margin, no near tie
+                d = LU if lu else QR
+            elif math.isnan(mg):
                 status = ST_NONFINITE
                 d = QR
             else:

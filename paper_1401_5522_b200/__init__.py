@@ -5,7 +5,7 @@ This package is the thin Python binding: argument marshalling only, same names a
 There is no CPU fallback: loading fails loudly when the library is missing.
 """
 from ._binding import (  # noqa: F401
-    CRIT_MAX, CRIT_MUMPS, CRIT_SUM, DEC_LU, DEC_QR, LU_A1, LU_A2, PIVOT_TILE, PIVOT_DOMAIN, TREE_GREEDY, TREE_HQR, FLAG_FORCED, FLAG_HINTED, FLAG_NEAR_TIE,
+    CRIT_MAX, CRIT_MUMPS, CRIT_SUM, CRIT_RANDOM, DEC_LU, DEC_QR, LU_A1, LU_A2, PIVOT_TILE, PIVOT_DOMAIN, TREE_GREEDY, TREE_HQR, FLAG_FORCED, FLAG_HINTED, FLAG_NEAR_TIE,
     FLAG_NONFINITE, FLAG_ZERO_PIVOT, HlqError, HlqInfo, HlqOptions, Factors, from_colmajor,
     hlq_abi, hlq_default_options, hlq_factor, hlq_factor_ex, hlq_generate_uniform, hlq_gesv_host,
     hlq_launch_count, hlq_residual, hlq_solve, lib, lib_path, to_colmajor,

@@ -15,7 +15,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.path.join(_HERE, "libhlq.so")
 
-CRIT_MAX, CRIT_SUM, CRIT_MUMPS = 0, 1, 2
+CRIT_MAX, CRIT_SUM, CRIT_MUMPS, CRIT_RANDOM = 0, 1, 2, 3
 DEC_LU, DEC_QR = 0, 1
 LU_A1, LU_A2 = 0, 1  # hlq_options.lu_variant (NEXT f4)
 PIVOT_TILE, PIVOT_DOMAIN = 0, 1  # hlq_options.pivot_scope (NEXT f1)
@@ -63,6 +63,8 @@ def _load():
         "hlq_get_decisions": ([P, P], I32),
         "hlq_get_margins": ([P, P], I32),
         "hlq_get_step_flags": ([P, P], I32),
+        "hlq_get_step_log": ([P, P], I32),
+        "hlq_get_step_times": ([P, P], I32),
         "hlq_get_growth": ([P, P], I32),
         "hlq_get_pivots": ([P, P], I32),
         "hlq_get_T": ([P, I32, I32, I32, P], I32),
@@ -180,6 +182,18 @@ class Factors:
         f = np.zeros(self.n, dtype=np.int32)
         _check(lib.hlq_get_step_flags(self.handle, f.ctypes.data_as(C.c_void_p)), "flags")
         return f
+
+    def step_log(self) -> np.ndarray:
+        """n x 2: the two sides of each step's binding criterion inequality (NaN: no criterion)."""
+        v = np.zeros(2 * self.n, dtype=np.float64)
+        _check(lib.hlq_get_step_log(self.handle, v.ctypes.data_as(C.c_void_p)), "step_log")
+        return v.reshape(-1, 2)
+
+    def step_times(self) -> np.ndarray:
+        """per-step device ms (profiled handles only)."""
+        v = np.zeros(self.n, dtype=np.float64)
+        _check(lib.hlq_get_step_times(self.handle, v.ctypes.data_as(C.c_void_p)), "step_times")
+        return v
 
     def growth(self) -> float:
         g = C.c_double()

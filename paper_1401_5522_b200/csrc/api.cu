@@ -14,6 +14,8 @@
 #include <new>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "handle.cuh"
 
 namespace hlq {
@@ -123,6 +125,22 @@ static cudaStream_t panel_stream(int which = 0) {
   return s[dev][which];
 }
 
+
+// NVTX ranges (factor, solve, every step) when HLQ_NVTX=1; no-ops without a tool attached
+static bool nvtx_on() {
+  static int on = -1;
+  if (on < 0) on = getenv("HLQ_NVTX") ? atoi(getenv("HLQ_NVTX")) != 0 : 0;
+  return on != 0;
+}
+struct NvtxScope {
+  bool on;
+  explicit NvtxScope(const char* name) : on(nvtx_on()) {
+    if (on) nvtxRangePushA(name);
+  }
+  ~NvtxScope() {
+    if (on) nvtxRangePop();
+  }
+};
 
 static int cuda_err(cudaError_t e) {
   if (e == cudaSuccess) return 0;
@@ -236,12 +254,13 @@ const char* hlq_status_string(int code) {
 
 int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double alpha,
                   const hlq_options* opt_in, hlq_factors_t* out) {
+  NvtxScope nvtx_scope("hlq_factor");
   if (!out) return -7;
   *out = nullptr;
   if (!A) return -1;
   if (N <= 0) return -2;
   if (nb <= 0 || nb > HLQ_MAX_NB) return -3;
-  if (criterion < 0 || criterion > 2) return -4;
+  if (criterion < 0 || criterion > 3) return -4;
   if (!(alpha >= 0.0)) return -5;  // rejects NaN and negatives
   hlq_options opt;
   hlq_default_options(&opt);
@@ -319,6 +338,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
          oTt = take(sizeof(double) * ntri * ib * nb), oS = take(sizeof(double) * n),
          oLm = take(sizeof(double) * nb), oAm = take(sizeof(double) * nb), oInv = take(8),
          oZp = take(sizeof(int)), oDec = take(n), oMg = take(sizeof(double) * n),
+         oSl = take(sizeof(double) * 2 * n),
          oFl = take(sizeof(int) * n), oSt = take(sizeof(int) * 4), oFo = take(n), oRd = take(n),
          oRm = take(sizeof(double) * n), oGs = take(sizeof(double) * (n + 1)),
          oPr = take(sizeof(int2) * (npairs + nts + 1)), oHd = take(sizeof(int) * (nheads + noff + 1)), oSc0 = take(sizeof(double) * scr),
@@ -361,6 +381,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   w.zp = (int*)(base + oZp);
   w.dec = (uint8_t*)(base + oDec);
   w.margin = (double*)(base + oMg);
+  w.steplog = (double*)(base + oSl);
   w.flags = (int*)(base + oFl);
   w.status = (int*)(base + oSt);
   w.forced = opt.forced ? (uint8_t*)(base + oFo) : nullptr;
@@ -459,16 +480,28 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   const bool alpha_inf = isinf(alpha);
   Prof& P = f->prof;
   P.on = opt.profile != 0;
+  if (P.on) {  // per-step times (hlq_get_step_times): events on the update stream
+    f->step_ev.assign((size_t)n + 1, nullptr);
+    for (auto& e : f->step_ev) cudaEventCreate(&e);
+    cudaEventRecord(f->step_ev[0], st);
+  }
   auto known_of = [&](int k) {
     if (opt.forced) return opt.forced[k] ? (int)HLQ_DEC_QR : (int)HLQ_DEC_LU;
     if (alpha == 0.0) return (int)HLQ_DEC_QR;
     return -1;
   };
   const bool criterion_needed = !opt.forced && alpha > 0.0 && !alpha_inf;
+  // the statistics (a1) feed Max / Sum / MUMPS; the Random criterion (reading 35) draws instead
+  const bool stats_needed = criterion_needed && criterion != HLQ_CRIT_RANDOM;
   const bool a2 = opt.lu_variant == HLQ_LU_A2;
   const int Dp = f->D;  // diagonal-domain pivoting: the QR tree's domains
   for (int k = 0; k < n; ++k) {
     const DevWork& wk = wpar[k & 1];
+    if (nvtx_on()) {
+      char nm[32];
+      snprintf(nm, sizeof nm, "hlq step %d", k);
+      nvtxRangePushA(nm);
+    }
     const int known = known_of(k);
     const int nl = (int)f->lvl_cnt[k].size();
     // ---- panel stage P(k) on sp: criterion, speculative GETRF, decision, the chosen branch's
@@ -502,7 +535,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
       }
     }
     if (known != HLQ_DEC_QR) {
-      if (criterion_needed) {
+      if (stats_needed) {
         P.begin(HLQ_PROF_CRITERION, sp);
         if (dpiv)
           launch_panel_stats_domain(A, g, k, Dp, wk, sp);
@@ -539,7 +572,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
         launch_tri_inv(g, k, wk, wk.scratch, wk.scratch + (size_t)nb * nb, sp);
       }
       P.end(sp);
-      if (criterion_needed && criterion != HLQ_CRIT_MUMPS) {
+      if (stats_needed && criterion != HLQ_CRIT_MUMPS) {
         P.begin(HLQ_PROF_CRITERION, sp);
         launch_invnorm(g, k, wk, sp, opt.invnorm_estimate, a2 ? 1 : 0);
         P.end(sp);
@@ -627,6 +660,8 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
       launch_lu_growth(w, g, k, st);
       P.end(st);
     }
+    if (P.on) cudaEventRecord(f->step_ev[k + 1], st);  // step k's update stage is done
+    if (nvtx_on()) nvtxRangePop();
   }
   int* scan = w.status + 2;
   launch_final_scan(A, N, lda, scan, st);
@@ -639,6 +674,8 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   int stat[4];
   cudaMemcpyAsync(f->dec.data(), w.dec, n, cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(f->margin.data(), w.margin, sizeof(double) * n, cudaMemcpyDeviceToHost, st);
+  f->steplog.resize(2 * (size_t)n);
+  cudaMemcpyAsync(f->steplog.data(), w.steplog, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(f->flags.data(), w.flags, sizeof(int) * n, cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(f->gstep.data(), w.gstep, sizeof(double) * (n + 1), cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(stat, w.status, sizeof(int) * 4, cudaMemcpyDeviceToHost, st);
@@ -674,6 +711,7 @@ int hlq_factor(double* A, int64_t N, int32_t nb, int32_t criterion, double alpha
 }
 
 int hlq_solve(hlq_factors_t f, const double* b, double* x) {
+  NvtxScope nvtx_scope("hlq_solve");
   if (!f || f->dec.empty()) return -1;
   if (!b) return -2;
   if (!x) return -3;
@@ -842,6 +880,25 @@ int hlq_get_margins(hlq_factors_t f, double* m) {
   memcpy(m, f->margin.data(), sizeof(double) * f->margin.size());
   return 0;
 }
+int hlq_get_step_log(hlq_factors_t f, double* log2n) {
+  if (!f || f->dec.empty()) return -1;
+  if (!log2n) return -2;
+  if (f->steplog.size() != 2 * f->dec.size()) return HLQ_ERR_STATE;
+  memcpy(log2n, f->steplog.data(), sizeof(double) * f->steplog.size());
+  return 0;
+}
+int hlq_get_step_times(hlq_factors_t f, double* ms) {
+  if (!f || f->dec.empty()) return -1;
+  if (!ms) return -2;
+  if (!f->prof.on || f->step_ev.size() != f->dec.size() + 1) return HLQ_ERR_STATE;
+  cudaStreamSynchronize(f->st);
+  for (size_t k = 0; k + 1 < f->step_ev.size(); ++k) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, f->step_ev[k], f->step_ev[k + 1]);
+    ms[k] = t;
+  }
+  return 0;
+}
 int hlq_get_step_flags(hlq_factors_t f, int32_t* fl) {
   if (!f || f->dec.empty()) return -1;
   if (!fl) return -2;
@@ -890,6 +947,8 @@ void hlq_free(hlq_factors_t f) {
   }
   f->prof.collect();
   for (auto e : f->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto e : f->step_ev)
     if (e) cudaEventDestroy(e);
   delete f;
 }

@@ -772,7 +772,8 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
   cudaStream_t st = ds.st, sp = ds.sp;
   const bool has_forced = opt.forced != nullptr;
   const bool has_ref = ds.ctx[0].w.ref_dec != nullptr;
-  const bool criterion_needed = !has_forced && alpha > 0.0 && !isinf(alpha);
+  const bool criterion_needed = !has_forced && alpha > 0.0 && !isinf(alpha) &&
+                                crit != HLQ_CRIT_RANDOM;
   auto known_of = [&](int k) {
     if (has_forced) return opt.forced[k] ? (int)HLQ_DEC_QR : (int)HLQ_DEC_LU;
     if (alpha == 0.0) return (int)HLQ_DEC_QR;
@@ -1531,7 +1532,7 @@ int hlq_factor_dist(hlq_grid_t grid, double* const* A_local, const int64_t* lld,
   if (!A_local) return -2;
   if (N <= 0) return -4;
   if (nb <= 0 || nb > HLQ_MAX_NB) return -5;
-  if (criterion < 0 || criterion > 2) return -6;
+  if (criterion < 0 || criterion > 3) return -6;
   if (!(alpha >= 0.0)) return -7;
   hlq_options opt;
   hlq_default_options(&opt);

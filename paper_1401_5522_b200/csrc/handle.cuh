@@ -90,6 +90,8 @@ struct hlq_factors_s {
   std::vector<double> margin;
   std::vector<int> flags;
   std::vector<double> gstep;
+  std::vector<double> steplog;         // 2n: lhs, rhs of each step's binding criterion inequality
+  std::vector<cudaEvent_t> step_ev;    // profiling: n+1 events on the update stream (step times)
   int status = 0;
   double growth = 0.0;
   bool track_growth = true;

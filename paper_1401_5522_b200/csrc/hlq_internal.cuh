@@ -72,6 +72,7 @@ struct DevWork {
   int* dom_idx;                 // 2*148 partial pivot rows
   unsigned int* dom_counter;    // arrivals of the last-CTA reduction
   const void* tma_maps;         // TMA tensor maps of A for the Schur update (gemm_tma.cu) or null
+  double* steplog;              // 2n: per step the binding criterion inequality's lhs, rhs (or null)
 };
 
 // ---- the HQR tree's TS level of one QR step (DESIGN reading 34); nullptr / ngroups = 0: greedy

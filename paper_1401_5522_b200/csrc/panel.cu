@@ -117,6 +117,13 @@ void launch_tile_norm_max(const double* A, Geo g, int k, double* out, cudaStream
 // a4: the decision.  One block of 256 threads.  Mirrors DESIGN.md readings 3,4,5,7,21,22 and the
 // MUMPS readings (1, 2).  Writes dec[k], margin[k], flags[k]; status[0] |= nonfinite,
 // status[1] |= zero pivot in a forced LU step.
+// Counter-based uniform generator (DESIGN.md "Input recipe"): SplitMix64 finalizer.
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
 __device__ __forceinline__ double rel_margin(double lhs, double rhs) {
   double den = fmax(lhs, rhs);
   if (den == 0.0) return 1.0;
@@ -131,13 +138,16 @@ __global__ void __launch_bounds__(256) k_decide(Geo g, int k, int crit, double a
   __shared__ double sh_growth[512];
   __shared__ double sh_min[256];
   __shared__ int sh_fail[256], sh_nan[256];
-  __shared__ double sh_margin;
+  __shared__ double sh_mlhs[256], sh_mrhs[256];
+  __shared__ double sh_margin, sh_lhs, sh_rhs;
   __shared__ int sh_d, sh_flags;
   const int zp = w.zp[0];
   if (tid == 0) {
     sh_flags = zp ? HLQ_FLAG_ZERO_PIVOT : 0;
     sh_d = -1;
     sh_margin = __longlong_as_double(0x7ff8000000000000LL);  // NaN
+    sh_lhs = sh_margin;
+    sh_rhs = sh_margin;
     if (has_forced) {
       sh_d = w.forced[k] ? HLQ_DEC_QR : HLQ_DEC_LU;  // any nonzero entry = QR
       sh_flags |= HLQ_FLAG_FORCED;
@@ -160,6 +170,8 @@ __global__ void __launch_bounds__(256) k_decide(Geo g, int k, int crit, double a
           double v = w.s[i];
           rhs = (crit == HLQ_CRIT_MAX) ? ((i == k + 1) ? v : nanmax(rhs, v)) : rhs + v;
         }
+        sh_lhs = lhs;
+        sh_rhs = rhs;
         if (isnan(lhs) || isnan(rhs)) {
           sh_d = HLQ_DEC_QR;
           sh_flags |= HLQ_FLAG_NONFINITE;
@@ -168,6 +180,16 @@ __global__ void __launch_bounds__(256) k_decide(Geo g, int k, int crit, double a
           sh_margin = rel_margin(lhs, rhs);
         }
       }
+    } else if (crit == HLQ_CRIT_RANDOM) {
+      // reading 35: LU iff 100 u_k < alpha, u_k = the counter generator's draw k of stream 31
+      if (tid == 0) {
+        const uint64_t GAMMA = 0x9E3779B97F4A7C15ULL;
+        const uint64_t key = mix64(31ULL + GAMMA);
+        const double u = (double)(mix64(key + ((uint64_t)k + 1ULL) * GAMMA) >> 11) * 0x1.0p-53;
+        sh_lhs = alpha;
+        sh_rhs = u * 100.0;
+        sh_d = (u * 100.0 < alpha) ? HLQ_DEC_LU : HLQ_DEC_QR;
+      }
     } else {  // MUMPS (Eq. 4)
       for (int j = tid; j < bk; j += 256) {
         double p = fabs(w.W[(int64_t)j * g.nb + j]);
@@ -175,7 +197,7 @@ __global__ void __launch_bounds__(256) k_decide(Geo g, int k, int crit, double a
         sh_growth[j] = (lm == 0.0) ? (p > 0.0 ? INFINITY : 0.0) : p / lm;
       }
       __syncthreads();
-      double mn = INFINITY;
+      double mn = INFINITY, mlhs = NAN, mrhs = NAN;
       int fail = 0, nn = 0;
       for (int j = tid; j < bk; j += 256) {
         double p = fabs(w.W[(int64_t)j * g.nb + j]);
@@ -193,16 +215,26 @@ __global__ void __launch_bounds__(256) k_decide(Geo g, int k, int crit, double a
         }
         double mj = isinf(est) ? -1.0 : rel_margin(lhs, est);
         if (!(lhs >= est)) fail = 1;
-        mn = fmin(mn, mj);
+        if (mj < mn) {
+          mn = mj;
+          mlhs = lhs;
+          mrhs = est;
+        }
       }
       sh_min[tid] = mn;
       sh_fail[tid] = fail;
       sh_nan[tid] = nn;
+      sh_mlhs[tid] = mlhs;
+      sh_mrhs[tid] = mrhs;
       __syncthreads();
       if (tid == 0) {
         double m = INFINITY;
         int f = 0, q = 0;
         for (int t = 0; t < 256; ++t) {
+          if (sh_min[t] < m) {  // the binding column (first minimum in thread order)
+            sh_lhs = sh_mlhs[t];
+            sh_rhs = sh_mrhs[t];
+          }
           m = fmin(m, sh_min[t]);
           f |= sh_fail[t];
           q |= sh_nan[t];
@@ -234,6 +266,10 @@ __global__ void __launch_bounds__(256) k_decide(Geo g, int k, int crit, double a
     w.dec[k] = (uint8_t)d;
     w.margin[k] = mg;
     w.flags[k] = fl;
+    if (w.steplog != nullptr) {  // the decision log: the binding inequality's two sides
+      w.steplog[2 * k] = sh_lhs;
+      w.steplog[2 * k + 1] = sh_rhs;
+    }
   }
 }
 
@@ -243,12 +279,6 @@ void launch_decide(Geo g, int k, int crit, double alpha, int mumps_reading, doub
 }
 
 // ---------------------------------------------------------------------------------------------
-// Counter-based uniform generator (DESIGN.md "Input recipe"): SplitMix64 finalizer.
-__device__ __forceinline__ uint64_t mix64(uint64_t z) {
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-  return z ^ (z >> 31);
-}
 
 __global__ void k_generate(double* dst, int64_t rows, int64_t cols, int64_t ld, uint64_t key,
                            uint64_t idx0, int64_t idx_ld) {

@@ -503,3 +503,37 @@ def test_hqr_tree_a2_variant(H):
     np.testing.assert_array_equal(f.decisions(), fo.dec)
     assert O.factor_diff(F, fo.A) <= 1e-10
     assert O.hpl3(A, x, b) <= 16.0
+
+
+@pytest.mark.parametrize("alpha", [50.0, 25.0, 0.0, 100.0])
+def test_random_criterion(H, alpha):
+    """The paper's Random choice (alpha = 50 in P:953; reading 35): the GPU draws u_k with
+    its own counter generator and takes LU iff 100 u_k < alpha -- the oracle's decisions exactly."""
+    A, b = I.uniform_matrix(0, 1024) + 4.0 * np.eye(1024), I.uniform_rhs(0, 1024)
+    fo, f, F, x = run_pair(H, A, b, 64, O.CRIT_RANDOM, alpha)
+    np.testing.assert_array_equal(f.decisions(), fo.dec)
+    assert np.all(np.isnan(f.margins()))
+    assert O.factor_diff(F, fo.A) <= 1e-10
+    assert O.hpl3(A, x, b) <= 16.0
+    log = f.step_log()
+    if 0.0 < alpha < 100.0:  # the draws themselves are logged: 100 u_k, bit-identical
+        u = np.array([O._splitmix_unit(O.RANDOM_SEED, k) for k in range(len(fo.dec))]) * 100.0
+        np.testing.assert_array_equal(log[:, 1], u)
+
+
+def test_step_log_and_times(H):
+    """Decision log = the two sides of the Max inequality, equal to the oracle's
+    alpha / ||A_kk^-1|| and max ||A_ik|| within the conditioning gate; per-step device times."""
+    A, b = I.uniform_matrix(0, 1024), I.uniform_rhs(0, 1024)
+    fo = O.hybrid_factor(A, 128, O.CRIT_MAX, 1.2e4)
+    dA = H.to_colmajor(A)
+    f = H.hlq_factor_ex(dA, 1024, 128, O.CRIT_MAX, 1.2e4, profile=1)
+    np.testing.assert_array_equal(f.decisions(), fo.dec)
+    log = f.step_log()
+    for k, st in enumerate(fo.stats):
+        lhs = 1.2e4 / st["inv_norm"]
+        rhs = float(np.max(st["s"])) if st["s"].size else 0.0
+        assert log[k, 0] == pytest.approx(lhs, rel=1e-9)
+        assert log[k, 1] == pytest.approx(rhs, rel=1e-9)
+    t = f.step_times()
+    assert t.shape == (8,) and np.all(t > 0.0)

@@ -728,3 +728,23 @@ def test_noise_floor_variant_same_mathematics():
         g1 = O.hybrid_factor(A + 2 * np.eye(512), 64, forced=forced, D=2, pivot_scope=scope,
                              lu_variant=lu, variant=1)
         assert 0.0 < O.factor_diff(g1.A, g0.A) < 1e-11
+
+
+def test_random_criterion():
+    """Random criterion (P:817, P:953 alpha = 50; reading 35): the draws are the input recipe's
+    counter generator (pinned to hlq_inputs' numpy implementation), LU iff 100 u_k < alpha, the
+    LU share follows alpha, alpha = 0 / >= 100 give all QR / all LU, zero pivots still force QR."""
+    us = np.array([O._splitmix_unit(O.RANDOM_SEED, k) for k in range(400)])
+    np.testing.assert_array_equal(us, I.unit_counter(O.RANDOM_SEED, np.arange(400)))
+    A = I.uniform_matrix(4, 512)
+    f = O.hybrid_factor(A, 16, O.CRIT_RANDOM, 50.0)
+    np.testing.assert_array_equal(f.dec == O.LU, us[:32] * 100.0 < 50.0)
+    assert np.all(np.isnan(f.margin)) and not f.near_tie.any()
+    assert set(O.hybrid_factor(A, 16, O.CRIT_RANDOM, 0.0).dec) == {O.QR}
+    assert set(O.hybrid_factor(A, 16, O.CRIT_RANDOM, 100.0).dec) == {O.LU}
+    share = np.mean(np.array([O._splitmix_unit(O.RANDOM_SEED, k) for k in range(4000)]) < 0.3)
+    assert abs(share - 0.3) < 0.03
+    Z = np.asfortranarray(np.eye(32))
+    Z[0, 0] = 0.0  # exact zero pivot in the first tile (ledger 7): QR whatever the draw
+    Z[1, 0] = 0.0
+    assert O.hybrid_factor(Z, 16, O.CRIT_RANDOM, 100.0).dec[0] == O.QR
