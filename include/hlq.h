@@ -232,6 +232,26 @@ int hlq_nccl_unique_id(void* id128);
  * Collective: every rank must call it.  Errors: -1..-5 arguments, HLQ_ERR_NCCL. */
 int hlq_grid_create_nccl(const void* id128, int32_t nranks, int32_t rank, int32_t P, int32_t Q,
                          hlq_grid_t* out);
+/* Host-staged grid: one process per rank like the NCCL grid (same per-rank code path), but every
+ * collective is handed to the caller's host functions on host buffers: the library synchronises the
+ * stream, copies the device data to a pinned staging buffer, calls the function and copies the
+ * result back.  comm: HLQ_COMM_WORLD (P*Q ranks, rank r = pQ + q), HLQ_COMM_ROW (the Q ranks of
+ * process row p, member index q), HLQ_COMM_COL / HLQ_COMM_COL_PANEL (the P ranks of process column
+ * q, member index p; the two may be one host group since the calls are issued in host order).
+ * allgather: member i's `count` doubles land at recv + i*count; broadcast: root = member index;
+ * allreduce: op 0 = sum, 1 = max (elementwise).  Each returns 0 on success.  Every rank calls the
+ * same collectives in the same order (the host schedule of hlq_factor_dist is rank-independent per
+ * communicator).  Used for multi-process tests without NCCL (e.g. torch.distributed gloo). */
+enum { HLQ_COMM_WORLD = 0, HLQ_COMM_ROW = 1, HLQ_COMM_COL = 2, HLQ_COMM_COL_PANEL = 3 };
+typedef struct {
+  int32_t struct_size; /* = sizeof(hlq_host_comm) */
+  void* ctx;
+  int (*allgather)(void* ctx, int32_t comm, const double* send, double* recv, int64_t count);
+  int (*broadcast)(void* ctx, int32_t comm, double* buf, int64_t count, int32_t root);
+  int (*allreduce)(void* ctx, int32_t comm, double* buf, int64_t count, int32_t op);
+} hlq_host_comm;
+int hlq_grid_create_host(const hlq_host_comm* ops, int32_t nranks, int32_t rank, int32_t P,
+                         int32_t Q, hlq_grid_t* out);
 /* Emulated grid: all P*Q ranks live in this process on the current device and every collective is
  * a stream-ordered device-to-device copy (testing the distributed path on one GPU). */
 int hlq_grid_create_local(int32_t P, int32_t Q, hlq_grid_t* out);

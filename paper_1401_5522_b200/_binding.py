@@ -77,6 +77,7 @@ def _load():
         "hlq_nccl_unique_id": ([P], I32),
         "hlq_grid_create_nccl": ([P, I32, I32, I32, I32, P], I32),
         "hlq_grid_create_local": ([I32, I32, P], I32),
+        "hlq_grid_create_host": ([P, I32, I32, I32, I32, P], I32),
         "hlq_grid_free": ([P], None),
         "hlq_grid_info": ([P, P, P, P, P], I32),
         "hlq_grid_local_shape": ([I64, I32, I32, I32, I32, I32, P, P], I32),
@@ -422,6 +423,60 @@ class Grid:
         if getattr(self, "handle", None) and self.handle.value:
             lib.hlq_grid_free(self.handle)
             self.handle = C.c_void_p(None)
+
+
+HC_ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64)
+HC_BROADCAST = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_int32)
+HC_ALLREDUCE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_int32)
+COMM_WORLD, COMM_ROW, COMM_COL, COMM_COL_PANEL = 0, 1, 2, 3
+
+
+class HostComm(C.Structure):
+    _fields_ = [("struct_size", C.c_int32), ("ctx", C.c_void_p), ("allgather", HC_ALLGATHER),
+                ("broadcast", HC_BROADCAST), ("allreduce", HC_ALLREDUCE)]
+
+
+def grid_host(nranks: int, rank: int, P: int, Q: int, allgather, broadcast, allreduce) -> Grid:
+    """Host-staged grid (hlq_grid_create_host): the collectives are the caller's Python functions on
+    numpy views of the library's pinned host buffers:
+      allgather(comm, send: ndarray[count], recv: ndarray[size*count]),
+      broadcast(comm, buf: ndarray[count], root), allreduce(comm, buf: ndarray[count], op)."""
+    def ag(ctx, comm, send, recv, count):
+        try:
+            s = np.ctypeslib.as_array(C.cast(send, C.POINTER(C.c_double)), shape=(count,))
+            size = Q if comm == COMM_ROW else (P * Q if comm == COMM_WORLD else P)
+            r = np.ctypeslib.as_array(C.cast(recv, C.POINTER(C.c_double)), shape=(size * count,))
+            allgather(comm, s, r)
+            return 0
+        except Exception as e:  # noqa: BLE001  (reported to the library as a failed collective)
+            print("hlq host allgather:", repr(e))
+            return 1
+
+    def bc(ctx, comm, buf, count, root):
+        try:
+            v = np.ctypeslib.as_array(C.cast(buf, C.POINTER(C.c_double)), shape=(count,))
+            broadcast(comm, v, root)
+            return 0
+        except Exception as e:  # noqa: BLE001
+            print("hlq host broadcast:", repr(e))
+            return 1
+
+    def ar(ctx, comm, buf, count, op):
+        try:
+            v = np.ctypeslib.as_array(C.cast(buf, C.POINTER(C.c_double)), shape=(count,))
+            allreduce(comm, v, op)
+            return 0
+        except Exception as e:  # noqa: BLE001
+            print("hlq host allreduce:", repr(e))
+            return 1
+
+    ops = HostComm(C.sizeof(HostComm), None, HC_ALLGATHER(ag), HC_BROADCAST(bc), HC_ALLREDUCE(ar))
+    h = C.c_void_p()
+    _check(lib.hlq_grid_create_host(C.byref(ops), nranks, rank, P, Q, C.byref(h)),
+           "hlq_grid_create_host")
+    g = Grid(h.value)
+    g._ops = ops  # the callbacks must outlive the grid
+    return g
 
 
 def grid_local(P: int, Q: int) -> Grid:

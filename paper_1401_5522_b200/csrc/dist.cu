@@ -101,9 +101,102 @@ int cuda_check(cudaError_t e) {
 struct hlq_grid_s {
   int P = 1, Q = 1;
   int local = 1;       // 1: all P*Q ranks emulated in this process
-  int rank = 0;        // NCCL: this process's world rank (p = rank / Q, q = rank % Q)
+  int rank = 0;        // this process's world rank (p = rank / Q, q = rank % Q)
   ncclComm_t world = nullptr, row = nullptr, col = nullptr, colp = nullptr;  // colp: panel stream
+  // host-staged backend (hlq_grid_create_host): the caller's collectives on host buffers
+  bool host = false;
+  hlq_host_comm ops{};
+  double* stage = nullptr;  // pinned staging buffer (grows)
+  size_t stage_n = 0;
 };
+
+// ---------------------------------------------------------------------------------------------
+// the per-rank collectives of the 2D grid, one entry point per kind: NCCL on the communicator of
+// `comm` (HLQ_COMM_*), or -- host-staged backend -- stream sync, device -> pinned host copy, the
+// caller's host collective on the same communicator, host -> device copy
+namespace {
+ncclComm_t comm_of(hlq_grid_s* g, int comm) {
+  return comm == HLQ_COMM_ROW ? g->row
+         : comm == HLQ_COMM_COL ? g->col
+         : comm == HLQ_COMM_COL_PANEL ? g->colp
+                                      : g->world;
+}
+int comm_size(hlq_grid_s* g, int comm) {
+  return comm == HLQ_COMM_ROW ? g->Q : (comm == HLQ_COMM_WORLD ? g->P * g->Q : g->P);
+}
+double* host_stage(hlq_grid_s* g, size_t n) {
+  if (n > g->stage_n) {
+    if (g->stage) cudaFreeHost(g->stage);
+    g->stage = nullptr;
+    g->stage_n = 0;
+    if (cudaMallocHost((void**)&g->stage, sizeof(double) * n) != cudaSuccess) return nullptr;
+    g->stage_n = n;
+  }
+  return g->stage;
+}
+int host_rc(int r, const char* what) {
+  if (r == 0) return 0;
+  fprintf(stderr, "[hlq] host collective %s failed: %d\n", what, r);
+  return HLQ_ERR_NCCL;
+}
+int xc_allgather(hlq_grid_s* g, int comm, const double* send, double* recv, int64_t count,
+                 cudaStream_t st) {
+  if (count <= 0) return 0;
+  if (!g->host)
+    return nccl_err(g_nccl.AllGather(send, recv, (size_t)count, ncclDouble, comm_of(g, comm), st),
+                    "allgather");
+  const int sz = comm_size(g, comm);
+  double* h = host_stage(g, (size_t)count * (sz + 1));
+  if (!h) return HLQ_ERR_NOMEM;
+  if (cudaMemcpyAsync(h, send, sizeof(double) * count, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return HLQ_ERR_CUDA;
+  int rc = host_rc(g->ops.allgather(g->ops.ctx, comm, h, h + count, count), "allgather");
+  if (rc) return rc;
+  if (cudaMemcpyAsync(recv, h + count, sizeof(double) * count * sz, cudaMemcpyHostToDevice, st) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return HLQ_ERR_CUDA;
+  return 0;
+}
+int xc_bcast(hlq_grid_s* g, int comm, double* buf, int64_t count, int root, cudaStream_t st) {
+  if (count <= 0) return 0;
+  if (!g->host)
+    return nccl_err(g_nccl.Broadcast(buf, buf, (size_t)count, ncclDouble, root, comm_of(g, comm),
+                                     st),
+                    "broadcast");
+  double* h = host_stage(g, (size_t)count);
+  if (!h) return HLQ_ERR_NOMEM;
+  if (cudaMemcpyAsync(h, buf, sizeof(double) * count, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return HLQ_ERR_CUDA;
+  int rc = host_rc(g->ops.broadcast(g->ops.ctx, comm, h, count, root), "broadcast");
+  if (rc) return rc;
+  if (cudaMemcpyAsync(buf, h, sizeof(double) * count, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return HLQ_ERR_CUDA;
+  return 0;
+}
+// op: 0 = sum, 1 = max
+int xc_allreduce(hlq_grid_s* g, int comm, double* buf, int64_t count, int op, cudaStream_t st) {
+  if (count <= 0) return 0;
+  if (!g->host)
+    return nccl_err(g_nccl.AllReduce(buf, buf, (size_t)count, ncclDouble, op ? ncclMax : ncclSum,
+                                     comm_of(g, comm), st),
+                    "allreduce");
+  double* h = host_stage(g, (size_t)count);
+  if (!h) return HLQ_ERR_NOMEM;
+  if (cudaMemcpyAsync(h, buf, sizeof(double) * count, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return HLQ_ERR_CUDA;
+  int rc = host_rc(g->ops.allreduce(g->ops.ctx, comm, h, count, op), "allreduce");
+  if (rc) return rc;
+  if (cudaMemcpyAsync(buf, h, sizeof(double) * count, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return HLQ_ERR_CUDA;
+  return 0;
+}
+}  // namespace
 
 // ---------------------------------------------------------------------------------------------
 // block-cyclic index arithmetic (host and device)
@@ -538,9 +631,8 @@ int col_allgather(DistState& ds, int q, const Buf& send, const Buf& recv, int64_
   if (!ds.gr->local) {
     for (auto& c : ds.ctx)
       if (c.q == q)
-        return nccl_err(g_nccl.AllGather(send(c), recv(c), (size_t)count, ncclDouble,
-                                         panel_comm ? ds.gr->colp : ds.gr->col, st),
-                        "allgather");
+        return xc_allgather(ds.gr, panel_comm ? HLQ_COMM_COL_PANEL : HLQ_COMM_COL, send(c), recv(c),
+                            count, st);
     return 0;
   }
   for (auto& dst : ds.ctx) {
@@ -562,9 +654,7 @@ int row_bcast(DistState& ds, int root, const Buf& buf, const std::function<int64
     for (auto& c : ds.ctx) {
       int64_t n = count(c.p);
       if (n <= 0) return 0;
-      return nccl_err(g_nccl.Broadcast(buf(c), buf(c), (size_t)n, ncclDouble, root, ds.gr->row,
-                                       st),
-                      "broadcast(row)");
+      return xc_bcast(ds.gr, HLQ_COMM_ROW, buf(c), n, root, st);
     }
     return 0;
   }
@@ -588,9 +678,7 @@ int col_bcast(DistState& ds, int q, int root, const Buf& buf, int64_t count) {
   if (!ds.gr->local) {
     for (auto& c : ds.ctx)
       if (c.q == q)
-        return nccl_err(g_nccl.Broadcast(buf(c), buf(c), (size_t)count, ncclDouble, root,
-                                         ds.gr->col, ds.st),
-                        "broadcast(col)");
+        return xc_bcast(ds.gr, HLQ_COMM_COL, buf(c), count, root, ds.st);
     return 0;
   }
   for (auto& src : ds.ctx) {
@@ -1128,10 +1216,7 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
   }
   if (!ds.gr->local) {
     Ctx& c = ds.ctx[0];
-    if ((rc = nccl_err(g_nccl.AllReduce(c.fin, c.fin, (size_t)(n + 5), ncclDouble, ncclMax,
-                                        ds.gr->world, st),
-                       "allreduce")))
-      return rc;
+    if ((rc = xc_allreduce(ds.gr, HLQ_COMM_WORLD, c.fin, n + 5, 1, st))) return rc;
   }
   return cuda_check(cudaGetLastError());
 }
@@ -1311,6 +1396,29 @@ int hlq_grid_create_nccl(const void* id128, int32_t nranks, int32_t rank, int32_
   return 0;
 }
 
+int hlq_grid_create_host(const hlq_host_comm* ops, int32_t nranks, int32_t rank, int32_t P,
+                         int32_t Q, hlq_grid_t* out) {
+  if (!out) return -6;
+  *out = nullptr;
+  if (!ops || ops->struct_size != (int32_t)sizeof(hlq_host_comm) || !ops->allgather ||
+      !ops->broadcast || !ops->allreduce)
+    return -1;
+  if (nranks < 1) return -2;
+  if (rank < 0 || rank >= nranks) return -3;
+  if (P < 1 || P > 16) return -4;
+  if (Q < 1 || Q > 16 || P * Q != nranks) return -5;
+  hlq_grid_s* g = new (std::nothrow) hlq_grid_s();
+  if (!g) return HLQ_ERR_NOMEM;
+  g->P = P;
+  g->Q = Q;
+  g->local = 0;
+  g->rank = rank;
+  g->host = true;
+  g->ops = *ops;
+  *out = g;
+  return 0;
+}
+
 int hlq_grid_create_local(int32_t P, int32_t Q, hlq_grid_t* out) {
   if (!out) return -3;
   *out = nullptr;
@@ -1327,6 +1435,7 @@ int hlq_grid_create_local(int32_t P, int32_t Q, hlq_grid_t* out) {
 
 void hlq_grid_free(hlq_grid_t g) {
   if (!g) return;
+  if (g->stage) cudaFreeHost(g->stage);
   if (g->row) g_nccl.CommDestroy(g->row);
   if (g->col) g_nccl.CommDestroy(g->col);
   if (g->colp) g_nccl.CommDestroy(g->colp);
@@ -1458,10 +1567,7 @@ int hlq_residual_dist(hlq_grid_t grid, double* const* A_local, const int64_t* ll
   }
   // sum the partials over each process row (ascending q), then every rank takes its row's sum
   if (!grid->local) {
-    if (ml[0] > 0 &&
-        (rc = nccl_err(g_nccl.AllReduce(buf, buf, (size_t)(2 * ml[0]), ncclDouble, ncclSum,
-                                        grid->row, st),
-                       "allreduce(row)"))) {
+    if (ml[0] > 0 && (rc = xc_allreduce(grid, HLQ_COMM_ROW, buf, 2 * ml[0], 0, st))) {
       cudaFree(buf);
       return rc;
     }
@@ -1487,9 +1593,7 @@ int hlq_residual_dist(hlq_grid_t grid, double* const* A_local, const int64_t* ll
     k_residual_max<<<64, 256, 0, st>>>(buf + (int64_t)t * 2 * (mmax + 1), ml[t], nb, P, ps[t], b, x,
                                        N, outs + 4 * t);
   }
-  if (!grid->local &&
-      (rc = nccl_err(g_nccl.AllReduce(outs, outs, 3, ncclDouble, ncclMax, grid->world, st),
-                     "allreduce(max)"))) {
+  if (!grid->local && (rc = xc_allreduce(grid, HLQ_COMM_WORLD, outs, 3, 1, st))) {
     cudaFree(buf);
     return rc;
   }
