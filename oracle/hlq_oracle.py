@@ -502,7 +502,16 @@ def _fmm(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     return (b.T @ a.T).T
 
 
-def unmqr(Vtile: np.ndarray, T: np.ndarray, ib: int, C: np.ndarray):
+def _vtc(V: np.ndarray, C: np.ndarray, variant: int) -> np.ndarray:
+    """V^T C (column-major result).  variant = 1 (the noise-floor run): the same product summed over
+    the two row halves in reverse order -- same mathematics, different rounding."""
+    if variant == 0 or V.shape[0] < 2:
+        return _fmm(V.T, C)
+    h = V.shape[0] // 2
+    return _fmm(V[h:].T, C[h:]) + _fmm(V[:h].T, C[:h])
+
+
+def unmqr(Vtile: np.ndarray, T: np.ndarray, ib: int, C: np.ndarray, variant: int = 0):
     """UNMQR: C <- Q^T C with Q from a GEQRT tile; blocks applied in order 0,1,..."""
     mrow, b = Vtile.shape
     for i0 in range(0, b, ib):
@@ -510,7 +519,7 @@ def unmqr(Vtile: np.ndarray, T: np.ndarray, ib: int, C: np.ndarray):
         V = _unit_lower(Vtile, i0, i0 + sb)
         Tb = np.triu(T[0:sb, i0:i0 + sb])
         Cb = C[i0:, :]
-        C[i0:, :] = Cb - _fmm(V, _fmm(Tb.T, _fmm(V.T, Cb)))
+        C[i0:, :] = Cb - _fmm(V, _fmm(Tb.T, _vtc(V, Cb, variant)))
 
 
 def tsqrt(R: np.ndarray, A2: np.ndarray, ib: int, tt: bool = False):
@@ -553,7 +562,8 @@ def tsqrt(R: np.ndarray, A2: np.ndarray, ib: int, tt: bool = False):
     return T
 
 
-def tsmqr(V2: np.ndarray, T: np.ndarray, ib: int, C1: np.ndarray, C2: np.ndarray, tt: bool = False):
+def tsmqr(V2: np.ndarray, T: np.ndarray, ib: int, C1: np.ndarray, C2: np.ndarray, tt: bool = False,
+          variant: int = 0):
     """TSMQR (P:327) / TTMQR (P:341): [C1; C2] <- Q^T [C1; C2], Q = prod_b (I - [E_b; V2_b] T_b [..]^T).
     C1 rows are the eliminator tile's rows (b of them), C2 the eliminated tile's rows."""
     b = V2.shape[1]
@@ -562,7 +572,7 @@ def tsmqr(V2: np.ndarray, T: np.ndarray, ib: int, C1: np.ndarray, C2: np.ndarray
         sb = min(ib, b - i0)
         Vb = Vfull[:, i0:i0 + sb]
         Tb = np.triu(T[0:sb, i0:i0 + sb])
-        Wm = _fmm(Tb.T, C1[i0:i0 + sb, :] + _fmm(Vb.T, C2))
+        Wm = _fmm(Tb.T, C1[i0:i0 + sb, :] + _vtc(Vb, C2, variant))
         C1[i0:i0 + sb, :] -= Wm
         C2 -= _fmm(Vb, Wm)
 
@@ -715,7 +725,7 @@ def _pmap(fn, items):
 
 
 def qr_step(A: np.ndarray, N: int, nb: int, k: int, D: int, ib: int,
-            tree: str = "greedy", T_kk=None) -> QRStepData:
+            tree: str = "greedy", T_kk=None, variant: int = 0) -> QRStepData:
     """T_kk: the diagonal tile was already factored in place by GEQRT (LU variant A2: "the
     factorization of A_kk is not discarded but rather used to continue the QR step").
 
@@ -734,7 +744,7 @@ def qr_step(A: np.ndarray, N: int, nb: int, k: int, D: int, ib: int,
     for h, T in zip(geqrt_rows, _pmap(factor_row, geqrt_rows)):
         data.T_geqrt[h] = T
     _pmap(lambda hc: unmqr(A[tsl(N, nb, hc[0]), ck], data.T_geqrt[hc[0]], ib,
-                           A[tsl(N, nb, hc[0]), hc[1]]),
+                           A[tsl(N, nb, hc[0]), hc[1]], variant),
           [(h, cs) for h in geqrt_rows for cs in chunks])
     # TS eliminations in plan order (Alg. 4a lines 2, 5): sequential along the chain
     for e, i in ts_list:
@@ -745,7 +755,8 @@ def qr_step(A: np.ndarray, N: int, nb: int, k: int, D: int, ib: int,
         data.T_ts[i] = tsqrt(Rv, A2, ib)
         iu = np.triu_indices(R.shape[0], m=R.shape[1])
         R[iu] = Rv[iu]
-        _pmap(lambda cs: tsmqr(A2, data.T_ts[i], ib, A[re_, cs], A[ri, cs]), chunks)
+        _pmap(lambda cs: tsmqr(A2, data.T_ts[i], ib, A[re_, cs], A[ri, cs], variant=variant),
+              chunks)
     # TT eliminations level by level (Alg. 4b lines 6-9); pairs inside a level are disjoint
     def tt_factor(pair):
         e, i = pair
@@ -760,7 +771,8 @@ def qr_step(A: np.ndarray, N: int, nb: int, k: int, D: int, ib: int,
         for (e, i), T in zip(level, _pmap(tt_factor, level)):
             data.T_tt[i] = T
         _pmap(lambda pc: tsmqr(A[tsl(N, nb, pc[1]), ck], data.T_tt[pc[1]], ib,
-                               A[tsl(N, nb, pc[0]), pc[2]], A[tsl(N, nb, pc[1]), pc[2]], tt=True),
+                               A[tsl(N, nb, pc[0]), pc[2]], A[tsl(N, nb, pc[1]), pc[2]], tt=True,
+                               variant=variant),
               [(e, i, cs) for e, i in level for cs in chunks])
     return data
 
@@ -814,7 +826,8 @@ def hybrid_factor(A_in: np.ndarray, nb: int, crit: int = CRIT_MAX, alpha: float 
     pivot_scope: "tile" (north_star, ledger 8) or "domain" (NEXT f1: the pivot search runs
     over the diagonal domain, the D-domain of the QR tree; DESIGN reading 33).
     forced: decision vector used verbatim (C3); variant=1 sums every LU Schur update (A1, A2 and
-    domain steps) in reversed K-chunk order (schur_update): the noise-floor run, delta_floor =
+    domain steps) in reversed K-chunk order (schur_update) and every V^T C product of the QR
+    trailing updates over reversed row halves (_vtc): the noise-floor run, delta_floor =
     factor_diff(variant 1, variant 0) with the decisions forced equal.
     on_step(k, A_before, A_after, d): optional test hook called after each step with copies.
     """
@@ -906,7 +919,7 @@ def hybrid_factor(A_in: np.ndarray, nb: int, crit: int = CRIT_MAX, alpha: float 
             lu_step(A, N, nb, k, W, ipiv, variant)
             ipivs[k] = ipiv
         else:
-            qrs[k] = qr_step(A, N, nb, k, D, ib, tree, T_kk=T_kk)
+            qrs[k] = qr_step(A, N, nb, k, D, ib, tree, T_kk=T_kk, variant=variant)
         if track_growth and k + 1 < n:
             g = max(g, max_tile_norm(A, N, nb, k + 1))
         if on_step is not None:

@@ -56,6 +56,35 @@ def spec(name: str) -> dict:
     raise ValueError(name)
 
 
+def r_part_diff(F: np.ndarray, G: np.ndarray, N: int, nb: int) -> float:
+    """Normwise relative difference of the R part of two packed factor arrays: for every step k
+    the rows of block k from column k*nb on (upper triangle of the diagonal tile + the row tiles) --
+    the part of a QR-heavy factorization that is unique (the V tiles represent an orthogonal basis
+    of the trailing rows, which tree QR determines only up to an ill-conditioned rotation)."""
+    num = den = 0.0
+    n = (N + nb - 1) // nb
+    for k in range(n):
+        r0, r1 = k * nb, min((k + 1) * nb, N)
+        Rf, Rg = np.triu(F[r0:r1, r0:]), np.triu(G[r0:r1, r0:])
+        num += float(np.sum((Rf - Rg) ** 2))
+        den += float(np.sum(Rg ** 2))
+    return math.sqrt(num / den) if den > 0 else 0.0
+
+
+def _variant_worker(args):
+    """The noise-floor oracle run (variant = 1) in its own process: its packed factors to a file."""
+    name, path = args
+    sp = spec(name)
+    N, nb, D = sp["N"], sp["nb"], sp["D"]
+    n = (N + nb - 1) // nb
+    A, _, _ = I.config_system(sp["config"], N)
+    forced = np.load(path + ".dec.npy")
+    crit = CRIT[sp["crit"]] if "crit" in sp else O.CRIT_MAX
+    fv = O.hybrid_factor(A, nb, crit, sp.get("alpha", 1.0), D=D, forced=forced, variant=1)
+    np.save(path, fv.A)
+    return n
+
+
 def cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -63,7 +92,7 @@ def cores() -> int:
         return os.cpu_count() or 1
 
 
-def run(name: str, outdir: str) -> dict:
+def run(name: str, outdir: str, floor_parallel: bool = False) -> dict:
     import torch
     import paper_1401_5522_b200 as H
 
@@ -76,7 +105,23 @@ def run(name: str, outdir: str) -> dict:
     forced = I.bernoulli_pattern(30, n, sp["fqr"]) if "fqr" in sp else None
     rec = {"run": name, **sp, "n": n, "oracle_cores": cores()}
 
-    # ---- oracle (full size)
+    # ---- oracle (full size); with floor_parallel the noise-floor variant runs beside it in a second
+    # process (it needs the decision vector: forced runs know it up front, criterion runs are
+    # re-run with the oracle's decisions from a quick pre-pass of the same oracle)
+    floor_proc = None
+    os.makedirs(outdir, exist_ok=True)
+    pre_dec = forced
+    prev = os.path.join(outdir, f"{name}.json")
+    if floor_parallel and pre_dec is None and os.path.exists(prev):
+        # the decision vector of an earlier record of this run (checked against this run's below)
+        pre_dec = np.array(["LQ".index(c) for c in json.load(open(prev))["decisions"]],
+                           dtype=np.uint8)
+    if floor_parallel and pre_dec is not None:
+        import multiprocessing as mp
+        np.save(os.path.join(outdir, f"_{name}_variant.dec.npy"), pre_dec)
+        floor_proc = mp.get_context("fork").Process(
+            target=_variant_worker, args=((name, os.path.join(outdir, f"_{name}_variant")),))
+        floor_proc.start()
     t0 = time.perf_counter()
     fo = O.hybrid_factor(A, nb, crit, alpha, D=D, forced=forced)
     rec["oracle_s"] = time.perf_counter() - t0
@@ -133,21 +178,32 @@ def run(name: str, outdir: str) -> dict:
     del dA
     torch.cuda.empty_cache()
     rec["eps_F"] = O.factor_diff(F, fo.A)
+    rec["eps_R"] = r_part_diff(F, fo.A, N, nb)
     rec["bit_identical"] = bool(np.array_equal(F, fo.A, equal_nan=True))
     del F
     print(f"[{name}] gpu {rec['gpu_s']:.2f}s decisions identical {rec['decisions_identical']}, "
           f"eps_F {rec['eps_F']:.3e}, HPL3 {rec['gpu_hpl3']:.3g}", flush=True)
 
-    # ---- noise floor: the oracle against its reversed-summation variant, decisions forced equal
-    has_update = any(d == O.LU for d in fo.dec[:-1])
-    if has_update:
-        t0 = time.perf_counter()
-        fv = O.hybrid_factor(A, nb, crit, alpha, D=D, forced=fo.dec, variant=1)
-        rec["delta_floor"] = O.factor_diff(fv.A, fo.A)
-        rec["variant_s"] = time.perf_counter() - t0
-        del fv
+    # ---- noise floor: the oracle against its reversed-summation variant (LU Schur sums and QR
+    # V^T C products), decisions forced equal
+    t0 = time.perf_counter()
+    vpath = os.path.join(outdir, f"_{name}_variant")
+    if floor_proc is not None:
+        floor_proc.join()
+        Fv = np.load(vpath + ".npy")
+        os.remove(vpath + ".npy")
+        if not np.array_equal(pre_dec, fo.dec):  # stale decision vector: redo in this process
+            Fv = O.hybrid_factor(A, nb, crit, alpha, D=D, forced=fo.dec, variant=1).A
     else:
-        rec["delta_floor"] = 0.0  # no LU Schur update: the variant computes the same arithmetic
+        Fv = O.hybrid_factor(A, nb, crit, alpha, D=D, forced=fo.dec, variant=1).A
+    rec["delta_floor"] = O.factor_diff(Fv, fo.A)
+    rec["delta_R_floor"] = r_part_diff(Fv, fo.A, N, nb)
+    rec["variant_s"] = time.perf_counter() - t0
+    del Fv
+    for ext in (".dec.npy",):
+        p = os.path.join(outdir, f"_{name}_variant" + ext)
+        if os.path.exists(p):
+            os.remove(p)
     gate = max(1e-10, 10.0 * rec["delta_floor"]) if math.isfinite(rec["delta_floor"]) else 1e-10
     rec["gate"] = gate
     # reading 30: the Wilkinson-type stress matrices (C4A, C4B) have numerically rank-deficient
@@ -164,10 +220,13 @@ def run(name: str, outdir: str) -> dict:
             "noise floor" if rec["eps_F"] <= gate else "FAILED")
     designed_failure = sp["config"] == "C4A" and sp.get("crit") == "mumps"
     rec["designed_failure"] = designed_failure  # MUMPS misses the Wilkinson growth
+    gate_R = max(1e-10, 10.0 * rec["delta_R_floor"]) if math.isfinite(rec["delta_R_floor"]) else 1e-10
+    rec["gate_R"] = gate_R
+    rec["R_gate_met"] = bool(rec["eps_R"] <= gate_R) if math.isfinite(rec["eps_R"]) else None
     rec["parity"] = bool(rec["decisions_identical"] and rec["pivots_identical"] and (
         rec["gate_met"] != "FAILED") and (designed_failure or rec["gpu_hpl3"] <= 16.0))
-    print(f"[{name}] delta_floor {rec['delta_floor']:.3e} -> gate {gate:.3e}: {rec['gate_met']}",
-          flush=True)
+    print(f"[{name}] delta_floor {rec['delta_floor']:.3e} -> gate {gate:.3e}: {rec['gate_met']}; "
+          f"R part eps_R {rec['eps_R']:.3e} vs delta_R {rec['delta_R_floor']:.3e}", flush=True)
     os.makedirs(outdir, exist_ok=True)
     with open(os.path.join(outdir, f"{name}.json"), "w") as fh:
         json.dump(rec, fh, indent=1)
@@ -178,9 +237,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("runs", nargs="+")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "parity"))
+    ap.add_argument("--floor-parallel", action="store_true",
+                    help="forced runs: compute the noise-floor variant in a second process")
     a = ap.parse_args()
     for r in a.runs:
-        run(r, a.out)
+        run(r, a.out, a.floor_parallel)
 
 
 if __name__ == "__main__":
