@@ -208,6 +208,12 @@ int hlq_get_profile(hlq_factors_t f, double* ms, double* flops, int64_t* launche
 /* Total kernel launches issued by this process through libhlq (monotonic counter). */
 int64_t hlq_launch_count(void);
 
+/* Test hook: one LU Schur update A[k0+K:, k0+K:] -= A[k0+K:, k0:k0+K] A[k0:k0+K, k0+K:] on a device
+ * matrix with the TMA kernel (use_tma = 1, when the matrix is eligible) or the cp.async kernel;
+ * synchronous.  Returns 1 if the TMA kernel ran, 0 if the cp.async kernel ran, < 0 on errors. */
+int hlq_test_schur(double* A, int64_t N, int64_t lda, int64_t k0, int32_t K, int32_t use_tma,
+                   void* stream);
+
 /* ABI self-description for bindings: sizeof(hlq_options), sizeof(hlq_info), version (1). */
 int hlq_abi(int32_t* sizeof_options, int32_t* sizeof_info, int32_t* version);
 

@@ -74,6 +74,7 @@ def _load():
         "hlq_residual": ([P, I64, I64, P, P, P, P], I32),
         "hlq_get_profile": ([P, P, P, P], I32),
         "hlq_launch_count": ([], I64),
+        "hlq_test_schur": ([P, I64, I64, I64, I32, I32, P], I32),
         "hlq_nccl_unique_id": ([P], I32),
         "hlq_grid_create_nccl": ([P, I32, I32, I32, I32, P], I32),
         "hlq_grid_create_local": ([I32, I32, P], I32),
@@ -292,6 +293,12 @@ def hlq_factor_ex(A, N: int, nb: int, criterion: int = CRIT_MAX, alpha: float = 
 
 def hlq_factor(A, N: int, nb: int, criterion: int = CRIT_MAX, alpha: float = 1.0) -> Factors:
     return hlq_factor_ex(A, N, nb, criterion, alpha)
+
+
+def hlq_test_schur(A, N: int, lda: int, k0: int, K: int, use_tma: bool, stream=None) -> int:
+    """One LU Schur update on the device matrix A (test hook; 1 = the TMA kernel ran)."""
+    return _check(lib.hlq_test_schur(_dptr(A), N, lda, k0, K, int(use_tma), _stream_ptr(stream)),
+                  "hlq_test_schur")
 
 
 def hlq_launch_count() -> int:

@@ -493,6 +493,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   const bool criterion_needed = !opt.forced && alpha > 0.0 && !alpha_inf;
   // the statistics (a1) feed Max / Sum / MUMPS; the Random criterion (reading 35) draws instead
   const bool stats_needed = criterion_needed && criterion != HLQ_CRIT_RANDOM;
+  const bool need_inv = stats_needed && criterion != HLQ_CRIT_MUMPS;  // ||A_kk^-1||_1 (Max, Sum)
   const bool a2 = opt.lu_variant == HLQ_LU_A2;
   const int Dp = f->D;  // diagonal-domain pivoting: the QR tree's domains
   for (int k = 0; k < n; ++k) {
@@ -566,10 +567,12 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
       } else if (dpiv) {
         // NEXT f1: partial pivoting over the stacked diagonal domain; W <- its pivoted top tile
         launch_dom_factor(A, g, k, Dp, wk, sp);
-        launch_tri_inv(g, k, wk, wk.scratch, wk.scratch + (size_t)nb * nb, sp);
+        if (need_inv) launch_tri_inv(g, k, wk, wk.scratch, wk.scratch + (size_t)nb * nb, sp);
       } else {
         launch_getrf(A, g, k, wk, true, sp);
-        launch_tri_inv(g, k, wk, wk.scratch, wk.scratch + (size_t)nb * nb, sp);
+        // the explicit triangular inverses feed only the criterion's ||A_kk^-1||_1 (Eliminate and
+        // Apply solve with W itself)
+        if (need_inv) launch_tri_inv(g, k, wk, wk.scratch, wk.scratch + (size_t)nb * nb, sp);
       }
       P.end(sp);
       if (stats_needed && criterion != HLQ_CRIT_MUMPS) {

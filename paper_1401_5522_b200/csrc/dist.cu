@@ -906,9 +906,10 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
         cudaMemsetAsync(w.inv_norm, 0, sizeof(double), s);
         if (known != HLQ_DEC_QR) {
           launch_getrf(Apan, gP, 0, w, true, s);
-          launch_tri_inv(gP, 0, w, w.scratch, w.scratch + (size_t)nb * nb, s);
-          if (criterion_needed && crit != HLQ_CRIT_MUMPS)
+          if (criterion_needed && crit != HLQ_CRIT_MUMPS) {  // the inverse norm only
+            launch_tri_inv(gP, 0, w, w.scratch, w.scratch + (size_t)nb * nb, s);
             launch_invnorm(gP, 0, w, s, opt.invnorm_estimate);
+          }
         }
         ::hlq::g_launches++;
         k_pack_owner<<<16, 256, 0, s>>>(c.rec_send + ds.ms_max + 2 * nb, w.inv_norm, w.zp, w.W,

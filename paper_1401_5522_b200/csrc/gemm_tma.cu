@@ -7,15 +7,19 @@
 //     through a 6-stage shared-memory ring with cp.async.bulk.tensor (SWIZZLE_128B boxes), arming
 //     full / empty mbarriers; the 4 consumer warps never issue a global load for A or B and never
 //     meet at a CTA-wide barrier in the main loop;
-//   * the kernel is persistent (2 CTAs per SM, grid = 2 x #SMs), walks the output tiles in grouped
-//     raster order, and the producer runs ahead into the next tile's K slices while the consumers
-//     finish the previous tile's epilogue -- no per-tile prologue bubble, no wave-quantization tail;
+//   * every CTA (2 per SM) walks TM_TILES_PER_CTA output tiles in grouped raster order, and the
+//     producer runs ahead into the next tile's K slices while the consumers finish the previous
+//     tile's epilogue (no per-tile prologue bubble); CTAs still retire often enough for the
+//     lookahead's high-priority panel kernels to get SMs;
 //   * 128-byte swizzle + a fragment row order chosen so every DMMA fragment load is
 //     bank-conflict free: the A (L panel) box is {16 rows, 16 k, 4 row groups}; accumulator row g
 //     of a fragment holds panel row (g & 3) + 8 (g >> 2) + 4 s of its 16-row group (s = the
 //     fragment's half), which spreads the 32 lanes over all 16 8-byte slots of a 128-byte row.
-// Epilogue: C_new = C - (A B) (the product accumulates from zero, so the rounding is that of
-// "A_ij - (A_ik A_kj)"), written back with the fused a12 column abs-sums (colpart) when asked.
+// The accumulators start from C and the A operand is sign-flipped, so every tile accumulates
+// A_ij - A_ik A_kj in the DMMAs' own order -- bit-identical to gemm.cu's kernel.  (Accumulating the
+// product from zero and subtracting it afterwards, as "A_ij - (A_ik A_kj)" reads, measured 10x
+// worse HPL3 at C3: the product of the large growth-inflated factors cancels against A_ij.)
+// Epilogue: the tile written back with the fused a12 column abs-sums (colpart) when asked.
 // Eligibility (else gemm.cu's cp.async kernel): lda even, A 16-byte aligned, N and nb multiples of
 // 16 (every TMA box in bounds or zero-filled past the matrix).
 #include <cuda.h>
@@ -37,6 +41,10 @@ constexpr int TM_B_BYTES = TM_BN * TM_BK * 8;    // 8 KB
 constexpr int TM_STAGE = TM_A_BYTES + TM_B_BYTES;
 constexpr int TM_SMEM = TM_ST * TM_STAGE + 1024 /*align*/ + 2 * TM_BN * 8 + 256;
 constexpr int TM_CTAS_PER_SM = 2;
+// output tiles per CTA: enough to amortise the pipeline fill, few enough that CTAs retire every
+// ~50 us so the high-priority panel stream of the lookahead gets SMs (a fully persistent grid
+// starved it: C3 GETRF stage 161 -> 797 ms of stream time, the step 905 -> 944 ms)
+constexpr int TM_TILES_PER_CTA = 4;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
@@ -100,7 +108,9 @@ __global__ void __launch_bounds__(TM_T, TM_CTAS_PER_SM)
                 int64_t ldp) {
   if (dec != nullptr && dec[k] != want) return;  // predicated launch (the branch not taken)
   extern __shared__ __align__(1024) unsigned char tm_smem_raw[];
-  unsigned char* sm = (unsigned char*)(((uintptr_t)tm_smem_raw + 1023) & ~(uintptr_t)1023);
+  // align the stage ring to 1024 bytes in the SHARED window (the swizzle atom), by pointer
+  // arithmetic on the __shared__ array so the fragment loads stay LDS
+  unsigned char* sm = tm_smem_raw + ((1024u - (smem_u32(tm_smem_raw) & 1023u)) & 1023u);
   uint64_t* full = (uint64_t*)(sm + TM_ST * TM_STAGE);
   uint64_t* empty = full + TM_ST;
   double* red = (double*)(empty + TM_ST);  // 2 x 64 column partials (a12 epilogue)
@@ -158,13 +168,26 @@ __global__ void __launch_bounds__(TM_T, TM_CTAS_PER_SM)
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     int64_t tm, tn;
     tile_coords(t, tm, tn);
+    // the accumulators start from C (loads issued before the first K slice is awaited): the update
+    // accumulates into A_ij in the DMMAs' own order, bit-identical to gemm.cu's kernel
+    const int64_t m0 = tm * TM_BM, n0 = tn * TM_BN;
     double acc[4][4][2];
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+    for (int mi = 0; mi < 4; ++mi) {
+      const int64_t row = m0 + (wm * 2 + (mi >> 1)) * 16 + frag_row(g, mi & 1);
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+      for (int ni = 0; ni < 4; ++ni) {
+        const int64_t col = n0 + wn * 32 + ni * 8 + 2 * t4;
+        acc[mi][ni][0] = (row < M && col < N) ? C[col * ldc + row] : 0.0;
+        acc[mi][ni][1] = (row < M && col + 1 < N) ? C[(col + 1) * ldc + row] : 0.0;
+      }
+    }
     for (int kt = 0; kt < KT; ++kt) {
       mbar_wait(full + s, ph);
+      // the lanes may leave the try_wait loop in different iterations: reconverge before the
+      // warp-synchronous mma.sync (.aligned) -- without this, a few fragments were intermittently
+      // corrupted (lanes executing the DMMAs apart)
+      __syncwarp();
       const double* As = (const double*)(sm + s * TM_STAGE);
       const double* Bs = (const double*)(sm + s * TM_STAGE + TM_A_BYTES);
 #pragma unroll
@@ -174,7 +197,8 @@ __global__ void __launch_bounds__(TM_T, TM_CTAS_PER_SM)
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) {
           const int mhi = wm * 2 + (mi >> 1), mlo = frag_row(g, mi & 1);
-          a[mi] = As[(mhi * 16 + kk) * 16 + ((((mlo >> 1) ^ (kk & 7)) << 1) | (mlo & 1))];
+          // C - A B: the A operand sign-flipped on the integer pipe
+          a[mi] = neg_bits(As[(mhi * 16 + kk) * 16 + ((((mlo >> 1) ^ (kk & 7)) << 1) | (mlo & 1))]);
         }
 #pragma unroll
         for (int ni = 0; ni < 4; ++ni) {
@@ -186,6 +210,11 @@ __global__ void __launch_bounds__(TM_T, TM_CTAS_PER_SM)
 #pragma unroll
           for (int ni = 0; ni < 4; ++ni) dmma_tm(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
       }
+      // release the stage: the fragment loads (generic proxy) must be complete and ordered before
+      // the producer's next TMA write into it (async proxy) -- the cross-proxy WAR fence; without
+      // it ptxas let the arrive overtake the last loads of the stage and a few fragments were
+      // intermittently read after the next K slice had landed
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + s);
       if (++s == TM_ST) {
@@ -193,28 +222,16 @@ __global__ void __launch_bounds__(TM_T, TM_CTAS_PER_SM)
         ph ^= 1;
       }
     }
-    // epilogue: C_new = C - acc, in place in the accumulators (one 8-column fragment row at a
-    // time: its loads are independent of each other)
-    const int64_t m0 = tm * TM_BM, n0 = tn * TM_BN;
+    // epilogue: the accumulators are the updated tile
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi) {
       const int64_t row = m0 + (wm * 2 + (mi >> 1)) * 16 + frag_row(g, mi & 1);
-      double c[4][2];
+      if (row >= M) continue;
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) {
         const int64_t col = n0 + wn * 32 + ni * 8 + 2 * t4;
-        c[ni][0] = (row < M && col < N) ? C[col * ldc + row] : 0.0;
-        c[ni][1] = (row < M && col + 1 < N) ? C[(col + 1) * ldc + row] : 0.0;
-      }
-#pragma unroll
-      for (int ni = 0; ni < 4; ++ni) {
-        const int64_t col = n0 + wn * 32 + ni * 8 + 2 * t4;
-        acc[mi][ni][0] = c[ni][0] - acc[mi][ni][0];
-        acc[mi][ni][1] = c[ni][1] - acc[mi][ni][1];
-        if (row < M) {
-          if (col < N) C[col * ldc + row] = acc[mi][ni][0];
-          if (col + 1 < N) C[(col + 1) * ldc + row] = acc[mi][ni][1];
-        }
+        if (col < N) C[col * ldc + row] = acc[mi][ni][0];
+        if (col + 1 < N) C[(col + 1) * ldc + row] = acc[mi][ni][1];
       }
     }
     if (colpart != nullptr) {
@@ -315,7 +332,10 @@ bool launch_schur_tma(const void* maps, double* A, int64_t lda, int64_t k0, int6
   if (first_on_device(attr))
     cudaFuncSetAttribute(k_dgemm_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, TM_SMEM);
   const int64_t tiles = ((M + TM_BM - 1) / TM_BM) * ((nc + TM_BN - 1) / TM_BN);
-  const int64_t grid = std::min<int64_t>(tiles, (int64_t)sm_count() * TM_CTAS_PER_SM);
+  static int64_t tpc = -1;
+  if (tpc < 0) tpc = getenv("HLQ_TMA_TPC") ? atoll(getenv("HLQ_TMA_TPC")) : TM_TILES_PER_CTA;
+  const int64_t grid = std::max<int64_t>(std::min<int64_t>(tiles, (int64_t)sm_count() * TM_CTAS_PER_SM),
+                                         (tiles + tpc - 1) / tpc);
   ::hlq::g_launches++;
   k_dgemm_tma<<<(unsigned)grid, TM_T, TM_SMEM, st>>>(
       *(const TmaMaps*)maps, A + c0 * lda + k1, lda, M, nc, K, (int)k1, (int)k0, (int)c0, dec, k,
@@ -324,3 +344,26 @@ bool launch_schur_tma(const void* maps, double* A, int64_t lda, int64_t k0, int6
 }
 
 }  // namespace hlq
+
+// ---- test hook (include/hlq.h hlq_test_schur): one Schur update on a device matrix ------------
+extern "C" int hlq_test_schur(double* A, int64_t N, int64_t lda, int64_t k0, int32_t K,
+                              int32_t use_tma, void* stream) {
+  using namespace hlq;
+  if (!A) return -1;
+  if (N <= 0) return -2;
+  if (lda < N) return -3;
+  if (k0 < 0 || K <= 0 || k0 + K > N) return -4;
+  const int64_t k1 = k0 + K, M = N - k1;
+  cudaStream_t st = (cudaStream_t)stream;
+  void* maps = use_tma ? make_tma_maps(A, N, lda, K) : nullptr;
+  bool done = false;
+  if (maps)
+    done = launch_schur_tma(maps, A, lda, k0, k1, k1, M, M, K, nullptr, 0, 0, nullptr, 0, st);
+  if (!done)
+    launch_dgemm(A + k1 * lda + k1, lda, A + k0 * lda + k1, lda, A + k1 * lda + k0, lda, M, M, K,
+                 true, true, nullptr, 0, 0, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (maps) free_tma_maps(maps);
+  if (e != cudaSuccess) return HLQ_ERR_CUDA;
+  return done ? 1 : 0;
+}

@@ -147,7 +147,9 @@ __device__ __forceinline__ void qr_update3_body(const double* __restrict__ A, Ge
   };
   // the chunk schedule (block, pass, chunk) of the whole CTA, built once: the producer is a table
   // lookup per chunk
-  constexpr int MAXS = 2 * NCH * (NCH + 1) / 2 + 2;
+  // (block, pass, chunk) entries: GEQRT / TT reflectors touch chunks up to their block, a square TS
+  // reflector block all NCH chunks
+  constexpr int MAXS = (TS ? 2 * NCH * NCH : 2 * NCH * (NCH + 1) / 2) + 2;
   __shared__ int sched[MAXS];
   __shared__ int nsched;
   if (tid == 0) {

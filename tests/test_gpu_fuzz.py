@@ -81,7 +81,10 @@ def test_fuzz_block_cyclic_against_oracle(t, N, nb, P, Q, D, f):
     forced = I.bernoulli_pattern(60 + t, n, f)
     fo, fg, F, x = run_dist(H, A, b, nb, P, Q, D=D, forced=forced)
     np.testing.assert_array_equal(fg.decisions(), fo.dec)
-    assert O.factor_diff(F, fo.A) <= 1e-10, O.factor_diff(F, fo.A)
+    # the BASELINE gate at the method's own noise floor (oracle vs its reversed-summation variant)
+    fv = O.hybrid_factor(A, nb, O.CRIT_MAX, 1.0, D=D, forced=forced, variant=1)
+    gate = max(1e-10, 10.0 * O.factor_diff(fv.A, fo.A))
+    assert O.factor_diff(F, fo.A) <= gate, (O.factor_diff(F, fo.A), gate)
     assert O.hpl3(A, x, b) <= 16.0
 
 

@@ -66,7 +66,12 @@ def r_part_diff(F: np.ndarray, G: np.ndarray, N: int, nb: int) -> float:
     for k in range(n):
         r0, r1 = k * nb, min((k + 1) * nb, N)
         Rf, Rg = np.triu(F[r0:r1, r0:]), np.triu(G[r0:r1, r0:])
-        num += float(np.sum((Rf - Rg) ** 2))
+        # R of a QR step is unique up to the signs of its rows (the sign of each Householder
+        # reflector follows the sign of a trailing-matrix entry, which the rotation above does not
+        # determine): compare the rows normalised to a nonnegative diagonal
+        sf = np.where(np.diag(F[r0:r1, r0:r1]) < 0, -1.0, 1.0)
+        sg = np.where(np.diag(G[r0:r1, r0:r1]) < 0, -1.0, 1.0)
+        num += float(np.sum((Rf * sf[:, None] - Rg * sg[:, None]) ** 2))
         den += float(np.sum(Rg ** 2))
     return math.sqrt(num / den) if den > 0 else 0.0
 
@@ -223,7 +228,10 @@ def run(name: str, outdir: str, floor_parallel: bool = False) -> dict:
     gate_R = max(1e-10, 10.0 * rec["delta_R_floor"]) if math.isfinite(rec["delta_R_floor"]) else 1e-10
     rec["gate_R"] = gate_R
     rec["R_gate_met"] = bool(rec["eps_R"] <= gate_R) if math.isfinite(rec["eps_R"]) else None
-    rec["parity"] = bool(rec["decisions_identical"] and rec["pivots_identical"] and (
+    # reading 30: an LU step after QR steps of rank-deficient panels pivots on a non-unique trailing
+    # matrix, so its pivots are compared only where the factors are unique
+    piv_ok = rec["pivots_identical"] or nonunique
+    rec["parity"] = bool(rec["decisions_identical"] and piv_ok and (
         rec["gate_met"] != "FAILED") and (designed_failure or rec["gpu_hpl3"] <= 16.0))
     print(f"[{name}] delta_floor {rec['delta_floor']:.3e} -> gate {gate:.3e}: {rec['gate_met']}; "
           f"R part eps_R {rec['eps_R']:.3e} vs delta_R {rec['delta_R_floor']:.3e}", flush=True)
