@@ -33,13 +33,14 @@
 namespace hlq {
 
 namespace {
-constexpr int TM_BM = 64, TM_BN = 64, TM_BK = 16, TM_ST = 6;
+constexpr int TM_BM = 64, TM_BN = 64, TM_BK = 16, TM_ST = 4;
 constexpr int TM_CONS = 4;                       // consumer warps (2 x 2 warp tiles of 32 x 32)
 constexpr int TM_T = 32 * (TM_CONS + 1);         // + the producer warp
 constexpr int TM_A_BYTES = TM_BM * TM_BK * 8;    // 8 KB
 constexpr int TM_B_BYTES = TM_BN * TM_BK * 8;    // 8 KB
 constexpr int TM_STAGE = TM_A_BYTES + TM_B_BYTES;
-constexpr int TM_SMEM = TM_ST * TM_STAGE + 1024 /*align*/ + 2 * TM_BN * 8 + 256;
+constexpr int TM_C_BYTES = TM_BM * TM_BN * 8;    // 32 KB: the next tile's C, prefetched by TMA
+constexpr int TM_SMEM = TM_ST * TM_STAGE + TM_C_BYTES + 1024 /*align*/ + 2 * TM_BN * 8 + 256;
 constexpr int TM_CTAS_PER_SM = 2;
 // output tiles per CTA: enough to amortise the pipeline fill, few enough that CTAs retire every
 // ~50 us so the high-priority panel stream of the lookahead gets SMs (a fully persistent grid
@@ -99,33 +100,43 @@ __device__ __forceinline__ int frag_row(int g, int s) { return (g & 3) + 8 * (g 
 struct TmaMaps {
   CUtensorMap a;  // 3D {16 rows, columns, row groups of 16} over the whole matrix: the L panel role
   CUtensorMap b;  // 2D {rows, columns} over the whole matrix: the U row-block role
+  CUtensorMap c;  // 3D like a, box {16, 64, 4}: a 64 x 64 output tile
 };
 
 __global__ void __launch_bounds__(TM_T, TM_CTAS_PER_SM)
     k_dgemm_tma(const __grid_constant__ TmaMaps maps, double* __restrict__ C, int64_t ldc,
                 int64_t M, int64_t N, int K, int arow0, int kcol0, int bcol0,
                 const uint8_t* __restrict__ dec, int k, int want, double* __restrict__ colpart,
-                int64_t ldp) {
+                int64_t ldp, int64_t tpc) {
   if (dec != nullptr && dec[k] != want) return;  // predicated launch (the branch not taken)
   extern __shared__ __align__(1024) unsigned char tm_smem_raw[];
   // align the stage ring to 1024 bytes in the SHARED window (the swizzle atom), by pointer
   // arithmetic on the __shared__ array so the fragment loads stay LDS
   unsigned char* sm = tm_smem_raw + ((1024u - (smem_u32(tm_smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = (uint64_t*)(sm + TM_ST * TM_STAGE);
+  double* Cs = (double*)(sm + TM_ST * TM_STAGE);  // the prefetched C tile (swizzled like A)
+  uint64_t* full = (uint64_t*)(sm + TM_ST * TM_STAGE + TM_C_BYTES);
   uint64_t* empty = full + TM_ST;
-  double* red = (double*)(empty + TM_ST);  // 2 x 64 column partials (a12 epilogue)
+  uint64_t* cfull = empty + TM_ST;
+  uint64_t* cempty = cfull + 1;
+  double* red = (double*)(cempty + 1);  // 2 x 64 column partials (a12 epilogue)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < TM_ST; ++s) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, TM_CONS);
     }
+    mbar_init(cfull, 1);
+    mbar_init(cempty, TM_CONS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   const int64_t ntm = (M + TM_BM - 1) / TM_BM, ntn = (N + TM_BN - 1) / TM_BN;
   const int64_t ntiles = ntm * ntn;
   const int KT = K / TM_BK;
+  // this CTA's tiles: a contiguous run of the grouped raster order, so that the tiles in flight at
+  // any time form one window of the matrix (L2 reuse of the L panel rows and U row columns)
+  const int64_t t0 = (int64_t)blockIdx.x * tpc;
+  const int64_t t1 = t0 + tpc < ntiles ? t0 + tpc : ntiles;
   auto tile_coords = [&](int64_t t, int64_t& tm, int64_t& tn) {  // grouped raster (8 tile rows)
     const int64_t per_group = 8 * ntn;
     const int64_t grp = t / per_group;
@@ -139,12 +150,17 @@ __global__ void __launch_bounds__(TM_T, TM_CTAS_PER_SM)
     // ---------------- producer: one lane streams the K slices of every tile of this CTA
     if (lane == 0) {
       int s = 0;
-      unsigned ph = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      unsigned ph = 0, cph = 0;
+      for (int64_t t = t0; t < t1; ++t) {
         int64_t tm, tn;
         tile_coords(t, tm, tn);
         const int rg = (int)((arow0 + tm * TM_BM) >> 4);   // row group of the panel rows
         const int bc = (int)(bcol0 + tn * TM_BN);          // first output column
+        // the tile's C (issued after every K slice of the previous tile: a full tile of lead)
+        mbar_wait(cempty, cph ^ 1);
+        mbar_expect_tx(cfull, TM_C_BYTES);
+        tma_load_3d(Cs, &maps.c, cfull, 0, bc, rg);
+        cph ^= 1;
         for (int kt = 0; kt < KT; ++kt) {
           mbar_wait(empty + s, ph ^ 1);
           unsigned char* st = sm + s * TM_STAGE;
@@ -164,24 +180,31 @@ __global__ void __launch_bounds__(TM_T, TM_CTAS_PER_SM)
   const int g = lane >> 2, t4 = lane & 3;
   const int wm = warp & 1, wn = warp >> 1;
   int s = 0;
-  unsigned ph = 0;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  unsigned ph = 0, cph = 0;
+  for (int64_t t = t0; t < t1; ++t) {
     int64_t tm, tn;
     tile_coords(t, tm, tn);
-    // the accumulators start from C (loads issued before the first K slice is awaited): the update
+    // the accumulators start from C (prefetched by TMA into the swizzled C buffer): the update
     // accumulates into A_ij in the DMMAs' own order, bit-identical to gemm.cu's kernel
     const int64_t m0 = tm * TM_BM, n0 = tn * TM_BN;
     double acc[4][4][2];
+    mbar_wait(cfull, cph);
+    __syncwarp();
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi) {
-      const int64_t row = m0 + (wm * 2 + (mi >> 1)) * 16 + frag_row(g, mi & 1);
+      const int mhi = wm * 2 + (mi >> 1), mlo = frag_row(g, mi & 1);
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) {
-        const int64_t col = n0 + wn * 32 + ni * 8 + 2 * t4;
-        acc[mi][ni][0] = (row < M && col < N) ? C[col * ldc + row] : 0.0;
-        acc[mi][ni][1] = (row < M && col + 1 < N) ? C[(col + 1) * ldc + row] : 0.0;
-      }
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int nn = wn * 32 + ni * 8 + 2 * t4 + h;  // C box: 128-byte row = (mhi, column)
+          acc[mi][ni][h] = Cs[(mhi * 64 + nn) * 16 + ((((mlo >> 1) ^ (nn & 7)) << 1) | (mlo & 1))];
+        }
     }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // (as for the K stages)
+    __syncwarp();
+    if (lane == 0) mbar_arrive(cempty);
+    cph ^= 1;
     for (int kt = 0; kt < KT; ++kt) {
       mbar_wait(full + s, ph);
       // the lanes may leave the try_wait loop in different iterations: reconverge before the
@@ -302,7 +325,11 @@ void* make_tma_maps(const double* A, int64_t N, int64_t lda, int nb) {
   CUresult r2 = fn(&m->b, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)A, gdB, gsB, boxB, estr2,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS) {
+  const cuuint32_t boxC[3] = {16, TM_BN, TM_BM / 16};
+  CUresult r3 = fn(&m->c, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)A, gdA, gsA, boxC, estr3,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS || r3 != CUDA_SUCCESS) {
     free(m);
     return nullptr;
   }
@@ -334,12 +361,13 @@ bool launch_schur_tma(const void* maps, double* A, int64_t lda, int64_t k0, int6
   const int64_t tiles = ((M + TM_BM - 1) / TM_BM) * ((nc + TM_BN - 1) / TM_BN);
   static int64_t tpc = -1;
   if (tpc < 0) tpc = getenv("HLQ_TMA_TPC") ? atoll(getenv("HLQ_TMA_TPC")) : TM_TILES_PER_CTA;
-  const int64_t grid = std::max<int64_t>(std::min<int64_t>(tiles, (int64_t)sm_count() * TM_CTAS_PER_SM),
-                                         (tiles + tpc - 1) / tpc);
+  const int64_t tpc_eff = std::max<int64_t>(
+      1, std::min<int64_t>(tpc, tiles / ((int64_t)sm_count() * TM_CTAS_PER_SM)));
+  const int64_t grid = (tiles + tpc_eff - 1) / tpc_eff;
   ::hlq::g_launches++;
   k_dgemm_tma<<<(unsigned)grid, TM_T, TM_SMEM, st>>>(
       *(const TmaMaps*)maps, A + c0 * lda + k1, lda, M, nc, K, (int)k1, (int)k0, (int)c0, dec, k,
-      want, colpart, ldp ? ldp : nc);
+      want, colpart, ldp ? ldp : nc, tpc_eff);
   return true;
 }
 

@@ -21,7 +21,11 @@ __device__ __forceinline__ double warp_nanmax(double v) {
   return v;
 }
 
-// grid: one block per tile row i in [k, n); 256 threads (8 warps, one column at a time each)
+// grid: (tile rows i in [k, n), column chunks of 32); 256 threads = 8 warps, each warp one column
+// at a time with 16-byte loads of row pairs (all the column's loads issued before the reductions);
+// the tile norm max over the chunks goes to s[i] with an order-independent atomic max (s zeroed by
+// the launcher), so the result does not depend on the chunking
+constexpr int PS_CHUNK = 32;
 __global__ void __launch_bounds__(256) k_panel_stats(const double* __restrict__ A, Geo g, int k,
                                                      int diag, double* __restrict__ s,
                                                      double* __restrict__ local_max,
@@ -30,15 +34,34 @@ __global__ void __launch_bounds__(256) k_panel_stats(const double* __restrict__ 
   const int bi = g.bs(i), bk = g.cbs(k);
   const double* T = g.tile(const_cast<double*>(A), i, k);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool v2 = ((g.lda & 1) == 0) && ((((uintptr_t)T) & 15) == 0);
   __shared__ double red[8];
   double tile_norm = 0.0;
-  for (int c = warp; c < bk; c += 8) {
+  const int cend = min(bk, (int)(blockIdx.y + 1) * PS_CHUNK);
+  for (int c = blockIdx.y * PS_CHUNK + warp; c < cend; c += 8) {
     const double* col = T + (int64_t)c * g.lda;
     double sum = 0.0, mx = 0.0;
-    for (int r = lane; r < bi; r += 32) {
-      double a = fabs(col[r]);
-      sum += a;
-      mx = nanmax(mx, a);
+    if (v2) {
+      double2 v[(HLQ_MAX_NB + 63) / 64];
+#pragma unroll
+      for (int u = 0; u < (HLQ_MAX_NB + 63) / 64; ++u) {
+        const int r = 2 * lane + 64 * u;
+        v[u] = r + 1 < bi ? *reinterpret_cast<const double2*>(col + r)
+                          : make_double2(r < bi ? col[r] : 0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < (HLQ_MAX_NB + 63) / 64; ++u) {
+        const double a = fabs(v[u].x), b = fabs(v[u].y);
+        sum += a;
+        sum += b;
+        mx = nanmax(mx, nanmax(a, b));
+      }
+    } else {
+      for (int r = lane; r < bi; r += 32) {
+        double a = fabs(col[r]);
+        sum += a;
+        mx = nanmax(mx, a);
+      }
     }
     sum = warp_sum(sum);
     mx = warp_nanmax(mx);
@@ -54,10 +77,10 @@ __global__ void __launch_bounds__(256) k_panel_stats(const double* __restrict__ 
   }
   if (lane == 0) red[warp] = tile_norm;
   __syncthreads();
-  if (threadIdx.x == 0 && !(diag && i == k)) {
-    double v = red[0];
+  if (threadIdx.x == 0 && !(diag && i == k) && !(D > 0 && (i - k) % D == 0)) {
+    double v = red[0];  // (the domain's tiles are not in the rhs: their s_i stays 0)
     for (int w = 1; w < 8; ++w) v = nanmax(v, red[w]);
-    s[i] = (D > 0 && (i - k) % D == 0) ? 0.0 : v;  // the domain's tiles are not in the rhs
+    atomic_max_nonneg(&s[i], v);
   }
 }
 
@@ -69,15 +92,19 @@ void launch_panel_stats_to(const double* A, Geo g, int k, int diag, double* s, d
                            double* away_max, cudaStream_t st) {
   cudaMemsetAsync(away_max, 0, sizeof(double) * g.nb, st);
   if (g.n - k <= 0) return;
-  { ::hlq::g_launches++; k_panel_stats<<<g.n - k, 256, 0, st>>>(A, g, k, diag, s, local_max, away_max, 0); }
+  cudaMemsetAsync(s + k, 0, sizeof(double) * (g.n - k), st);
+  const dim3 grid(g.n - k, (g.cbs(k) + PS_CHUNK - 1) / PS_CHUNK);
+  { ::hlq::g_launches++; k_panel_stats<<<grid, 256, 0, st>>>(A, g, k, diag, s, local_max, away_max, 0); }
 }
 
 void launch_panel_stats_domain(const double* A, Geo g, int k, int D, DevWork w, cudaStream_t st) {
   cudaMemsetAsync(w.away_max, 0, sizeof(double) * g.nb, st);
   cudaMemsetAsync(w.local_max, 0, sizeof(double) * g.nb, st);
   if (g.n - k <= 0) return;
+  cudaMemsetAsync(w.s + k, 0, sizeof(double) * (g.n - k), st);
   ::hlq::g_launches++;
-  k_panel_stats<<<g.n - k, 256, 0, st>>>(A, g, k, 1, w.s, w.local_max, w.away_max, D);
+  const dim3 grid(g.n - k, (g.cbs(k) + PS_CHUNK - 1) / PS_CHUNK);
+  k_panel_stats<<<grid, 256, 0, st>>>(A, g, k, 1, w.s, w.local_max, w.away_max, D);
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -235,7 +235,9 @@ __device__ __forceinline__ void wait_flag(const int* p, int want) {
   while (ld_acquire(p) != want) __nanosleep(32);
 }
 
-// acc[s][e] += sum over columns c (c = h, h+2, ...) of T(row 2q+256s+e, c) * xs[c]
+// acc[s][e] += sum over columns c (c = h, h+2, ...) of T(row 2q+256s+e, c) * xs[c]; with V2 (even
+// ld, 16-byte aligned tile) the two rows are one 16-byte load
+template <bool V2>
 __device__ __forceinline__ void gemv_tile(const double* __restrict__ T, int64_t lda, int rows,
                                           int cols, const double* xs, int q, int h,
                                           double (&acc)[2][2]) {
@@ -245,15 +247,38 @@ __device__ __forceinline__ void gemv_tile(const double* __restrict__ T, int64_t 
     if (r >= rows) continue;
     const bool two = r + 1 < rows;
     double a0 = 0.0, a1 = 0.0;
+    if (V2 && two) {
+#pragma unroll 16
+      for (int c = h; c < cols; c += 2) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(T + (int64_t)c * lda + r));
+        const double xv = xs[c];
+        a0 = fma(v.x, xv, a0);
+        a1 = fma(v.y, xv, a1);
+      }
+    } else {
 #pragma unroll 8
-    for (int c = h; c < cols; c += 2) {
-      const double* col = T + (int64_t)c * lda + r;
-      const double xv = xs[c];
-      a0 = fma(__ldg(col), xv, a0);
-      if (two) a1 = fma(__ldg(col + 1), xv, a1);
+      for (int c = h; c < cols; c += 2) {
+        const double* col = T + (int64_t)c * lda + r;
+        const double xv = xs[c];
+        a0 = fma(__ldg(col), xv, a0);
+        if (two) a1 = fma(__ldg(col + 1), xv, a1);
+      }
     }
     acc[s][0] += a0;
     acc[s][1] += a1;
+  }
+}
+
+// L2 prefetch of a tile (rows x cols, column-major, ld lda): one bulk prefetch per column, issued
+// while the unit still waits for the x segment it will multiply (the tile does not depend on it)
+__device__ __forceinline__ void prefetch_tile_l2(const double* T, int64_t lda, int rows, int cols,
+                                                 int tid) {
+  const unsigned bytes = (unsigned)(rows * 8) & ~15u;
+  if (bytes == 0) return;
+  for (int c = tid; c < cols; c += PS_T) {
+    const double* p = T + (int64_t)c * lda;
+    if ((((uintptr_t)p) & 15) == 0)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
   }
 }
 
@@ -279,8 +304,12 @@ __device__ void tile_lower_unit_solve(const double* __restrict__ D, int64_t lda,
     __syncthreads();
     const int pw = min(32, bi - base);
     for (int r = base + 32 + tid; r < bi; r += PS_T) {
+      double l[32];  // all 32 loads in flight before the dependent sum
+#pragma unroll
+      for (int cc = 0; cc < 32; ++cc) l[cc] = cc < pw ? __ldg(D + (int64_t)(base + cc) * lda + r) : 0.0;
       double a = 0.0;
-      for (int cc = 0; cc < pw; ++cc) a = fma(__ldg(D + (int64_t)(base + cc) * lda + r), ys[base + cc], a);
+#pragma unroll
+      for (int cc = 0; cc < 32; ++cc) a = fma(l[cc], cc < pw ? ys[base + cc] : 0.0, a);
       ys[r] -= a;
     }
     __syncthreads();
@@ -311,8 +340,12 @@ __device__ void tile_upper_solve(const double* __restrict__ D, int64_t lda, int 
     __syncthreads();
     const int pw = min(32, bi - base);
     for (int r = tid; r < base; r += PS_T) {
+      double l[32];
+#pragma unroll
+      for (int cc = 0; cc < 32; ++cc) l[cc] = cc < pw ? __ldg(D + (int64_t)(base + cc) * lda + r) : 0.0;
       double a = 0.0;
-      for (int cc = 0; cc < pw; ++cc) a = fma(__ldg(D + (int64_t)(base + cc) * lda + r), ys[base + cc], a);
+#pragma unroll
+      for (int cc = 0; cc < 32; ++cc) a = fma(l[cc], cc < pw ? ys[base + cc] : 0.0, a);
       ys[r] -= a;
     }
     __syncthreads();
@@ -353,6 +386,18 @@ __global__ void __launch_bounds__(PS_T) k_solve_rows(const double* __restrict__ 
     ntiles = max(0, min(G, jfirst - i));
   }
   double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  const bool v2 = ((g.lda & 1) == 0) && ((((uintptr_t)A) & 15) == 0) && ((g.nb & 1) == 0);
+  // the factor tiles do not depend on x: pull this unit's tiles (and the finisher's diagonal tile)
+  // into L2 while the x segments they multiply are still being solved
+  {
+    const int cn0 = FWD ? max(1, (min(i, kb) - ka + G - 1) / G) : max(1, (g.n - 1 - i + G - 1) / G);
+    for (int t = 0; t < ntiles; ++t) {
+      const int j = FWD ? jfirst + t : jfirst - t;
+      prefetch_tile_l2(A + g.r0(j) * g.lda + g.r0(i), g.lda, bi, g.bs(j), tid);
+    }
+    if (c + 1 == cn0 && (!FWD || i < kb))
+      prefetch_tile_l2(A + g.r0(i) * g.lda + g.r0(i), g.lda, bi, bi, tid);
+  }
   for (int t = 0; t < ntiles; ++t) {
     const int j = FWD ? jfirst + t : jfirst - t;
     const int bj = g.bs(j);
@@ -360,7 +405,10 @@ __global__ void __launch_bounds__(PS_T) k_solve_rows(const double* __restrict__ 
     __syncthreads();
     for (int cc = tid; cc < bj; cc += PS_T) xs[cc] = __ldcg(x + g.r0(j) + cc);
     __syncthreads();
-    gemv_tile(A + g.r0(j) * g.lda + g.r0(i), g.lda, bi, bj, xs, q, h, acc);
+    if (v2)
+      gemv_tile<true>(A + g.r0(j) * g.lda + g.r0(i), g.lda, bi, bj, xs, q, h, acc);
+    else
+      gemv_tile<false>(A + g.r0(j) * g.lda + g.r0(i), g.lda, bi, bj, xs, q, h, acc);
     __syncthreads();
   }
   // the two column halves' partial sums, per row
@@ -475,16 +523,28 @@ void launch_residual(const double* A, int64_t N, int64_t lda, const double* x, c
   { ::hlq::g_launches++; k_residual<<<(unsigned)((N + 127) / 128), 128, 0, st>>>(A, N, lda, x, b, out3dev); }
 }
 
-// final status: flag[0] |= any non-finite factor entry, flag[1] |= exact zero on the diagonal
+// final status: flag[0] |= any non-finite factor entry, flag[1] |= exact zero on the diagonal.
+// grid-stride over columns (blockIdx), threads over rows with 16-byte loads where aligned: no
+// per-element 64-bit division
 __global__ void k_final_scan(const double* __restrict__ A, int64_t N, int64_t lda, int* flag) {
   int bad = 0, zero = 0;
-  int64_t total = N * N;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t c = t / N, r = t - c * N;
-    double a = A[c * lda + r];
-    if (!isfinite(a)) bad = 1;
-    if (r == c && a == 0.0) zero = 1;
+  const bool v2 = ((lda & 1) == 0) && ((((uintptr_t)A) & 15) == 0);
+  for (int64_t c = blockIdx.x; c < N; c += gridDim.x) {
+    const double* col = A + c * lda;
+    if (v2) {
+      for (int64_t r = 2 * (int64_t)threadIdx.x; r < N; r += 2 * (int64_t)blockDim.x) {
+        if (r + 1 < N) {
+          const double2 v = *reinterpret_cast<const double2*>(col + r);
+          if (!isfinite(v.x) || !isfinite(v.y)) bad = 1;
+        } else if (!isfinite(col[r])) {
+          bad = 1;
+        }
+      }
+    } else {
+      for (int64_t r = threadIdx.x; r < N; r += blockDim.x)
+        if (!isfinite(col[r])) bad = 1;
+    }
+    if (threadIdx.x == 0 && col[c] == 0.0) zero = 1;
   }
   bad = __syncthreads_or(bad);
   zero = __syncthreads_or(zero);

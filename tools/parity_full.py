@@ -38,6 +38,11 @@ CRIT = {"max": O.CRIT_MAX, "sum": O.CRIT_SUM, "mumps": O.CRIT_MUMPS}
 
 
 def spec(name: str) -> dict:
+    if "@" in name:  # RUN@hqrA: the same run on the HQR tree with TS groups of A tiles
+        base, tree = name.split("@")
+        s = spec(base)
+        s["tree"] = tree
+        return s
     if name.startswith("C3_f"):
         return dict(config="C3", N=32768, nb=256, fqr=float(name[4:]), D=1)
     if name == "C5r":
@@ -76,6 +81,27 @@ def r_part_diff(F: np.ndarray, G: np.ndarray, N: int, nb: int) -> float:
     return math.sqrt(num / den) if den > 0 else 0.0
 
 
+def r_part_diff_raw(F: np.ndarray, G: np.ndarray, N: int, nb: int) -> float:
+    num = den = 0.0
+    for k in range((N + nb - 1) // nb):
+        r0, r1 = k * nb, min((k + 1) * nb, N)
+        Rf, Rg = np.triu(F[r0:r1, r0:]), np.triu(G[r0:r1, r0:])
+        num += float(np.sum((Rf - Rg) ** 2))
+        den += float(np.sum(Rg ** 2))
+    return math.sqrt(num / den) if den > 0 else 0.0
+
+
+def sign_flips(F: np.ndarray, G: np.ndarray, N: int, nb: int) -> dict:
+    """{step: rows of R whose diagonal sign differs} (only the steps that have some)."""
+    out = {}
+    for k in range((N + nb - 1) // nb):
+        r0, r1 = k * nb, min((k + 1) * nb, N)
+        f = int(np.sum(np.sign(np.diag(F[r0:r1, r0:r1])) != np.sign(np.diag(G[r0:r1, r0:r1]))))
+        if f:
+            out[str(k)] = f
+    return out
+
+
 def _variant_worker(args):
     """The noise-floor oracle run (variant = 1) in its own process: its packed factors to a file."""
     name, path = args
@@ -85,7 +111,8 @@ def _variant_worker(args):
     A, _, _ = I.config_system(sp["config"], N)
     forced = np.load(path + ".dec.npy")
     crit = CRIT[sp["crit"]] if "crit" in sp else O.CRIT_MAX
-    fv = O.hybrid_factor(A, nb, crit, sp.get("alpha", 1.0), D=D, forced=forced, variant=1)
+    fv = O.hybrid_factor(A, nb, crit, sp.get("alpha", 1.0), D=D, forced=forced, variant=1,
+                         tree=sp.get("tree", "greedy"))
     np.save(path, fv.A)
     return n
 
@@ -128,7 +155,8 @@ def run(name: str, outdir: str, floor_parallel: bool = False) -> dict:
             target=_variant_worker, args=((name, os.path.join(outdir, f"_{name}_variant")),))
         floor_proc.start()
     t0 = time.perf_counter()
-    fo = O.hybrid_factor(A, nb, crit, alpha, D=D, forced=forced)
+    tree = sp.get("tree", "greedy")
+    fo = O.hybrid_factor(A, nb, crit, alpha, D=D, forced=forced, tree=tree)
     rec["oracle_s"] = time.perf_counter() - t0
     fake = 2.0 / 3.0 * float(N) ** 3
     rec["oracle_tflops"] = fake / rec["oracle_s"] / 1e12
@@ -149,6 +177,8 @@ def run(name: str, outdir: str, floor_parallel: bool = False) -> dict:
     # ---- GPU (the C ABI), the oracle's decisions only at its near ties
     dA = H.to_colmajor(A)
     kw = dict(tree_domains=D)
+    if tree.startswith("hqr"):
+        kw.update(tree=H.TREE_HQR, ts_group=int(tree[3:]))
     if forced is not None:
         kw["forced"] = forced
     elif near.any():
@@ -184,6 +214,8 @@ def run(name: str, outdir: str, floor_parallel: bool = False) -> dict:
     torch.cuda.empty_cache()
     rec["eps_F"] = O.factor_diff(F, fo.A)
     rec["eps_R"] = r_part_diff(F, fo.A, N, nb)
+    rec["eps_R_no_sign_normalisation"] = r_part_diff_raw(F, fo.A, N, nb)
+    rec["row_sign_flips_per_step"] = sign_flips(F, fo.A, N, nb)
     rec["bit_identical"] = bool(np.array_equal(F, fo.A, equal_nan=True))
     del F
     print(f"[{name}] gpu {rec['gpu_s']:.2f}s decisions identical {rec['decisions_identical']}, "
@@ -198,11 +230,12 @@ def run(name: str, outdir: str, floor_parallel: bool = False) -> dict:
         Fv = np.load(vpath + ".npy")
         os.remove(vpath + ".npy")
         if not np.array_equal(pre_dec, fo.dec):  # stale decision vector: redo in this process
-            Fv = O.hybrid_factor(A, nb, crit, alpha, D=D, forced=fo.dec, variant=1).A
+            Fv = O.hybrid_factor(A, nb, crit, alpha, D=D, forced=fo.dec, variant=1, tree=tree).A
     else:
-        Fv = O.hybrid_factor(A, nb, crit, alpha, D=D, forced=fo.dec, variant=1).A
+        Fv = O.hybrid_factor(A, nb, crit, alpha, D=D, forced=fo.dec, variant=1, tree=tree).A
     rec["delta_floor"] = O.factor_diff(Fv, fo.A)
     rec["delta_R_floor"] = r_part_diff(Fv, fo.A, N, nb)
+    rec["variant_row_sign_flips_per_step"] = sign_flips(Fv, fo.A, N, nb)
     rec["variant_s"] = time.perf_counter() - t0
     del Fv
     for ext in (".dec.npy",):
