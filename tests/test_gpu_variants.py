@@ -1,9 +1,11 @@
 """Schedule and kernel-shape variants must not change the factorization (-m gpu).
 
 The speculative QR panel (HLQ_SPEC_QR) only moves the QR branch's panel work to a second stream and a
-copy of the panel, and the DGEMM warp grid (HLQ_DGEMM_TILE) only changes which CTA computes which
-output tile (every element still accumulates its K products in the same order): both must give
-bit-identical factors and decisions.  The environment is read once per process, so each variant
+copy of the panel (its kernels run while d_k is undecided and exit once it is LU), the DGEMM warp grid
+(HLQ_DGEMM_TILE) only changes which CTA computes which output tile, and the TMA-fed Schur update
+(default) and the cp.async kernel (HLQ_DGEMM_TMA=0) accumulate every element's K products in the
+same order: all must give bit-identical factors, decisions and QR-step T factors -- under A1 and A2,
+Max and MUMPS, one and two QR-tree domains.  The environment is read once per process, so each variant
 runs in its own interpreter."""
 import os
 import subprocess
@@ -19,14 +21,26 @@ SCRIPT = r'''
 import sys, numpy as np, torch
 sys.path.insert(0, {root!r})
 import hlq_inputs as I, paper_1401_5522_b200 as H
-N, nb = 1000, 128
+N, nb = 1008, 128  # ragged last tile (112 rows), TMA-eligible (N, nb multiples of 16)
 A = I.normal_system(1, N)[0]
+U = I.uniform_matrix(3, N)
 out = {{}}
-for name, crit, alpha in (("max1", H.CRIT_MAX, 1.0), ("max3e4", H.CRIT_MAX, 3e4), ("lu", H.CRIT_MAX, float("inf"))):
-    dA = H.to_colmajor(A)
-    f = H.hlq_factor_ex(dA, N, nb, crit, alpha)
+# (name, matrix, criterion, alpha, options): mixed LU/QR decisions under A1 and A2, MUMPS, and two
+# QR-tree domains (the speculative QR panel writes the T factors of QR steps directly)
+cases = (("max1", A, H.CRIT_MAX, 1.0, {{}}), ("max3e4", A, H.CRIT_MAX, 3e4, {{}}),
+         ("lu", A, H.CRIT_MAX, float("inf"), {{}}),
+         ("a2_mix", U, H.CRIT_MAX, 1.2e4, dict(lu_variant=H.LU_A2)),
+         ("mumps", A, H.CRIT_MUMPS, 2.1, {{}}),
+         ("dom2", U, H.CRIT_MAX, 1.2e4, dict(tree_domains=2)))
+for name, M, crit, alpha, kw in cases:
+    dA = H.to_colmajor(M)
+    f = H.hlq_factor_ex(dA, N, nb, crit, alpha, **kw)
     out[name + "_F"] = H.from_colmajor(dA)
-    out[name + "_d"] = f.decisions()
+    d = f.decisions()
+    out[name + "_d"] = d
+    n = len(d)
+    T = [f.T(i, k, kind) for k in range(n) if d[k] == 1 for i in range(k, n) for kind in (0, 1)]
+    out[name + "_T"] = np.array(T) if T else np.zeros(0)
     f.free()
 np.savez({path!r}, **out)
 '''
@@ -42,7 +56,7 @@ def _run(env_extra, path):
     return np.load(path)
 
 
-@pytest.mark.parametrize("env", [{"HLQ_SPEC_QR": "0"}, {"HLQ_DGEMM_TILE": "4x2"}])
+@pytest.mark.parametrize("env", [{"HLQ_SPEC_QR": "0"}, {"HLQ_DGEMM_TILE": "4x2"}, {"HLQ_DGEMM_TMA": "0"}])
 def test_variant_is_bit_identical(tmp_path, env):
     base = _run({}, str(tmp_path / "base.npz"))
     var = _run(env, str(tmp_path / "var.npz"))
