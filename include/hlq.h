@@ -283,7 +283,11 @@ int hlq_dist_counts(int64_t N, int32_t nb, int32_t P, int32_t Q, int32_t D, int3
  * process (hlq_grid_info nlocal; rank order), lld: local leading dimensions (NULL or 0 -> mloc).
  * Same criteria, options (forced / ref_dec / ref_margin are the global host vectors, identical on
  * every rank), statuses and getters as hlq_factor_ex except hlq_get_pivots / hlq_get_T
- * (HLQ_ERR_STATE).  ib must be 32.  Collective: every rank calls it with the same arguments.
+ * (HLQ_ERR_STATE).  ib must be 32; tree_domains D must be a multiple of P (0 -> P); tree must be
+ * HLQ_TREE_GREEDY and lu_variant HLQ_LU_A1 (-8 otherwise).  pivot_scope = HLQ_PIVOT_DOMAIN runs
+ * diagonal-domain pivoting: the domain of step k (tiles i = k mod D) lies on process
+ * row k mod P, so its stacked LU and row interchanges stay on that process row (the pivots travel
+ * in the panel package).  Collective: every rank calls it with the same arguments.
  * hlq_solve(f, b, x) on the returned handle: b and x are FULL N-vectors on this process's device
  * (b replicated on every rank; x returned on every rank).
  * Errors: -1 grid, -2 A_local, -3 lld, -4 N, -5 nb, -6 criterion, -7 alpha, -8 options,

@@ -401,24 +401,31 @@ __global__ void k_copy_vec(double* __restrict__ dst, const double* __restrict__ 
     dst[t] = src[t];
 }
 
+// meta: [d_k, margin_k, flags_k, -][perm (nb)][the diagonal domain's stacked pivots (nb)]
 __global__ void k_meta_pack(double* meta, const uint8_t* dec, const double* margin,
-                            const int* flags, const int* perm, int bk, int k, int nb) {
+                            const int* flags, const int* perm, const int* dipiv, int bk, int k,
+                            int nb) {
   if (threadIdx.x == 0) {
     meta[0] = (double)dec[k];
     meta[1] = margin[k];
     meta[2] = (double)flags[k];
   }
-  for (int t = threadIdx.x; t < bk; t += blockDim.x) meta[4 + t] = (double)perm[t];
-  (void)nb;
+  for (int t = threadIdx.x; t < bk; t += blockDim.x) {
+    meta[4 + t] = (double)perm[t];
+    meta[4 + nb + t] = dipiv != nullptr ? (double)dipiv[t] : 0.0;
+  }
 }
 __global__ void k_meta_unpack(const double* meta, uint8_t* dec, double* margin, int* flags,
-                              int* perm, int bk, int k) {
+                              int* perm, int* dipiv, int bk, int k, int nb) {
   if (threadIdx.x == 0) {
     dec[k] = (uint8_t)meta[0];
     margin[k] = meta[1];
     flags[k] = (int)meta[2];
   }
-  for (int t = threadIdx.x; t < bk; t += blockDim.x) perm[t] = (int)meta[4 + t];
+  for (int t = threadIdx.x; t < bk; t += blockDim.x) {
+    perm[t] = (int)meta[4 + t];
+    if (dipiv != nullptr) dipiv[t] = (int)meta[4 + nb + t];
+  }
 }
 
 // final status scan of one rank: non-finite entries, exact zeros on the diagonal of the global
@@ -556,6 +563,7 @@ struct Ctx {
   void* block = nullptr;
   DevWork w{};
   int* ipiv = nullptr;
+  int* dipiv = nullptr;  // diagonal-domain pivoting: per step the stacked pivots (n x nb)
   double *Tg = nullptr, *Ttt = nullptr, *mstore = nullptr;
   double *rec_send = nullptr, *rec_recv = nullptr, *head_send = nullptr, *head_recv = nullptr;
   double *pkg = nullptr, *hr_send = nullptr, *hr_recv = nullptr, *HR = nullptr;
@@ -571,6 +579,7 @@ struct Ctx {
 struct DistState {
   hlq_grid_s* gr = nullptr;
   int P = 1, Q = 1, D = 1, c = 1, S = 1, ib = 32, nb = 0, n = 0;
+  bool dpiv = false;  // diagonal-domain pivoting (NEXT f1 on the grid, DESIGN reading 33)
   int64_t N = 0;
   int ms_max = 0, mt_max = 0;
   int64_t rec_count = 0, seg_cap = 0;
@@ -586,7 +595,7 @@ struct DistState {
   int64_t off_MT(int64_t prow, int ms) const { return off_HM(prow, ms) + (int64_t)S * nb * nb; }
   int64_t off_Li(int64_t prow, int ms) const { return off_MT(prow, ms) + (int64_t)S * ib * nb; }
   int64_t off_meta(int64_t prow, int ms) const { return off_Li(prow, ms) + (int64_t)nb * nb; }
-  int64_t pkg_count(int64_t prow, int ms) const { return off_meta(prow, ms) + 4 + nb; }
+  int64_t pkg_count(int64_t prow, int ms) const { return off_meta(prow, ms) + 4 + 2 * nb; }
   int64_t mstore_stride() const { return (int64_t)S * nb * nb + (int64_t)S * ib * nb; }
   ~DistState() {
     for (auto& c : ctx)
@@ -612,7 +621,7 @@ inline void step_counts(int64_t N, int nb, int P, int Q, int D, int ib, int p, i
   const int ms = std::max(0, cyc_count(n, P, p) - li0);
   const int64_t prow = std::max<int64_t>(0, cyc_extent(N, nb, P, p) - (int64_t)li0 * nb);
   out[2] = prow * nb + 2 * (int64_t)ms * ib * nb + (int64_t)S * nb * nb + (int64_t)S * ib * nb +
-           (int64_t)nb * nb + 4 + nb;
+           (int64_t)nb * nb + 4 + 2 * (int64_t)nb;
   const int lc1 = cyc_below(k + 1, Q, q);
   const int64_t ncl = std::max<int64_t>(0, cyc_extent(N, nb, Q, q) - (int64_t)lc1 * nb);
   out[3] = (int64_t)c * nb * ncl;
@@ -736,7 +745,10 @@ static int dist_alloc(DistState& ds, Ctx& c, const hlq_options& opt, bool has_re
          o_xk = take(8 * (size_t)nb), o_hxs = take(8 * (size_t)cc * nb),
          o_hxr = take(8 * (size_t)P * cc * nb), o_HX = take(8 * (size_t)S * nb),
          o_xg = take(8 * (size_t)P * ds.seg_cap), o_fin = take(8 * (size_t)(n + 8)),
-         o_pr = take(sizeof(int2) * (npairs + 1));
+         o_pr = take(sizeof(int2) * (npairs + 1)),
+         o_wd = take(ds.dpiv ? 8 * (size_t)mloc * nb : 8),
+         o_dp = take(ds.dpiv ? 4 * (size_t)n * nb : 8), o_dk = take(8 * 2 * 148),
+         o_di = take(4 * 2 * 148), o_dc = take(4);
   if (cudaMalloc(&c.block, off) != cudaSuccess) {
     cudaGetLastError();
     c.block = nullptr;
@@ -767,7 +779,13 @@ static int dist_alloc(DistState& ds, Ctx& c, const hlq_options& opt, bool has_re
   w.Ttt = nullptr;
   w.pairs = nullptr;
   w.colpart = nullptr;
+  w.wdom = ds.dpiv ? (double*)(b + o_wd) : nullptr;
+  w.dipiv = ds.dpiv ? (int*)(b + o_dp) : nullptr;
+  w.dom_key = (unsigned long long*)(b + o_dk);
+  w.dom_idx = (int*)(b + o_di);
+  w.dom_counter = (unsigned int*)(b + o_dc);
   c.ipiv = w.ipiv;
+  c.dipiv = w.dipiv;
   c.Tg = (double*)(b + o_Tg);
   c.Ttt = (double*)(b + o_Tt);
   c.mstore = (double*)(b + o_ms);
@@ -829,6 +847,8 @@ static int dist_alloc(DistState& ds, Ctx& c, const hlq_options& opt, bool has_re
   cudaMemsetAsync(w.gstep, 0, sizeof(double) * (n + 1), ds.st);
   cudaMemsetAsync(w.ipiv, 0, sizeof(int) * (size_t)n * nb, ds.st);
   cudaMemsetAsync(w.dec, 0, n, ds.st);
+  cudaMemsetAsync(w.dom_counter, 0, sizeof(unsigned int), ds.st);
+  if (c.dipiv) cudaMemsetAsync(c.dipiv, 0, sizeof(int) * (size_t)n * nb, ds.st);
   cudaMemsetAsync(c.xseg, 0, sizeof(double) * ds.seg_cap, ds.st);
   cudaMemsetAsync(w.scratch, 0, sizeof(double) * (2 * (size_t)nb * nb + nb), ds.st);
   cudaMemsetAsync(c.scrs[1], 0, sizeof(double) * (2 * (size_t)nb * nb + nb), ds.st);
@@ -847,6 +867,15 @@ static Geo panel_geo(const DistState& ds, const Ctx& c, const StepPlan& sp, int6
   (void)bk;
   g.Nc = 0;
   return g;
+}
+
+// the owner's DevWork for the domain kernels, which index step k of a local panel geometry as
+// step 0: the step's stacked and tile pivots and its decision at offset 0
+static DevWork dom_view(const Ctx& c, DevWork w, int k, int nb) {
+  w.ipiv = c.ipiv + (int64_t)k * nb;
+  w.dipiv = c.dipiv + (int64_t)k * nb;
+  w.dec = w.dec + k;
+  return w;
 }
 
 // The factorization schedule: panel stage P(k) (A, X1, B, X2, C, X3) on the high-priority panel
@@ -896,16 +925,24 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
       gP.Nc = bk;
       PR.begin(HLQ_PROF_CRITERION, s);
       cudaMemsetAsync(c.rec_send, 0, sizeof(double) * ds.rec_count, s);
-      if (sp_.ms > 0 && criterion_needed)
-        launch_panel_stats_to(Apan, gP, 0, sp_.diag, c.rec_send, c.rec_send + ds.ms_max + nb,
-                              c.rec_send + ds.ms_max, s);
+      if (sp_.ms > 0 && criterion_needed) {
+        if (ds.dpiv && sp_.diag)  // the whole diagonal domain is local: tiles 0, c, 2c, ...
+          launch_panel_stats_domain_to(Apan, gP, 0, ds.c, c.rec_send,
+                                       c.rec_send + ds.ms_max + nb, c.rec_send + ds.ms_max, s);
+        else
+          launch_panel_stats_to(Apan, gP, 0, sp_.diag, c.rec_send, c.rec_send + ds.ms_max + nb,
+                                c.rec_send + ds.ms_max, s);
+      }
       PR.end(s);
       if (sp_.diag) {
         PR.begin(HLQ_PROF_GETRF, s);
         cudaMemsetAsync(w.zp, 0, sizeof(int), s);
         cudaMemsetAsync(w.inv_norm, 0, sizeof(double), s);
         if (known != HLQ_DEC_QR) {
-          launch_getrf(Apan, gP, 0, w, true, s);
+          if (ds.dpiv)  // partial pivoting over the stacked domain; W <- its pivoted top tile
+            launch_dom_factor(Apan, gP, 0, ds.c, dom_view(c, w, k, nb), s);
+          else
+            launch_getrf(Apan, gP, 0, w, true, s);
           if (criterion_needed && crit != HLQ_CRIT_MUMPS) {  // the inverse norm only
             launch_tri_inv(gP, 0, w, w.scratch, w.scratch + (size_t)nb * nb, s);
             launch_invnorm(gP, 0, w, s, opt.invnorm_estimate);
@@ -942,13 +979,16 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
       int* perm = reinterpret_cast<int*>(w.scratch + (size_t)2 * nb * nb);
       if (known != HLQ_DEC_QR) {
         PR.begin(HLQ_PROF_LU_TRSM, s);
-        if (sp_.diag)
+        if (sp_.diag && !ds.dpiv)
           launch_lu_commit(Apan, gP, 0, w.W, w.ipiv_ws, c.ipiv + (int64_t)k * nb, perm, dk, s);
         const int64_t r0 = sp_.diag ? bk : 0;
         const int64_t M = gP.N - r0;
         // Eliminate with U_kk from the gathered speculative LU W (blocked substitution, trsm.cu)
         if (M > 0)
           launch_trsm_eliminate(Apan, c.lld, r0, 0, M, bk, w.W, nb, dk, 0, HLQ_DEC_LU, s);
+        // domain pivoting: the stacked LU replaces the domain's tiles (the diagonal tile and
+        // the local tiles c, 2c, ...; U_kk^-1 above applies to the tiles off the domain only)
+        if (sp_.diag && ds.dpiv) launch_dom_commit(Apan, gP, 0, ds.c, dom_view(c, w, k, nb), s);
         PR.end(s);
       }
       if (known != HLQ_DEC_LU && sp_.ms > 0) {
@@ -1029,8 +1069,8 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
                       cudaMemcpyDeviceToDevice, s);
       ::hlq::g_launches++;
       k_meta_pack<<<1, 256, 0, s>>>(pk_ + ds.off_meta(prow, sp_.ms), w.dec, w.margin, w.flags,
-                                    reinterpret_cast<int*>(w.scratch + (size_t)2 * nb * nb), bk, k,
-                                    nb);
+                                    reinterpret_cast<int*>(w.scratch + (size_t)2 * nb * nb),
+                                    ds.dpiv ? c.dipiv + (int64_t)k * nb : nullptr, bk, k, nb);
       PR.end(s);
     }
     auto pcount = [&](int p) {
@@ -1071,7 +1111,8 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
       if (part == 0) {
         ::hlq::g_launches++;
         k_meta_unpack<<<1, 256, 0, s>>>(pk_ + ds.off_meta(prow, sp_.ms), w.dec, w.margin, w.flags,
-                                        perm, bk, k);
+                                        perm, ds.dpiv ? c.dipiv + (int64_t)k * nb : nullptr, bk,
+                                        k, nb);
       }
       int64_t co, ncl;
       const int lc1 = part_range(k, c.q, c.nloc, part, co, ncl);
@@ -1085,6 +1126,17 @@ static int dist_factor(DistState& ds, int crit, double alpha, const hlq_options&
       gK.Nc = bk;
       if (known != HLQ_DEC_QR && sp_.diag) {
         PR.begin(HLQ_PROF_LU_UPDATE, s);
+        if (ds.dpiv) {
+          // the domain's row interchanges on this rank's trailing columns (the domain's rows are
+          // all on process row pk), before the Apply (whose permutation is then the identity)
+          Geo gS{};
+          gS.N = prow;
+          gS.lda = c.lld;
+          gS.nb = nb;
+          gS.n = sp_.ms;
+          gS.Nc = bk;
+          launch_dom_swap_cols(base, gS, 0, ds.c, c.dipiv + (int64_t)k * nb, 0, ncl, dk, s);
+        }
         launch_trsm_apply(base, c.lld, 0, 0, ncl, bk, pk_ + ds.off_Li(prow, sp_.ms), nb, perm, dk,
                           0, HLQ_DEC_LU, s);
         PR.end(s);
@@ -1249,8 +1301,14 @@ static int dist_solve(DistState& ds, const std::vector<uint8_t>& dec, const doub
         double* Apan = c.A + (int64_t)lk * nb * c.lld + (int64_t)sp.li0 * nb;
         Geo gP = panel_geo(ds, c, sp, c.lld);
         gP.Nc = bk;
-        launch_solve_lu_fwd(Apan, gP, 0, c.ipiv + (int64_t)k * nb, c.xseg + (int64_t)sp.li0 * nb,
-                            st);
+        if (ds.dpiv) {  // the domain's interchanges on x (its rows are local), then L_kk^-1
+          launch_dom_swap_vec(c.xseg + (int64_t)sp.li0 * nb, gP, 0, ds.c,
+                              c.dipiv + (int64_t)k * nb, st);
+          launch_solve_lu_fwd(Apan, gP, 0, nullptr, c.xseg + (int64_t)sp.li0 * nb, st);
+        } else {
+          launch_solve_lu_fwd(Apan, gP, 0, c.ipiv + (int64_t)k * nb,
+                              c.xseg + (int64_t)sp.li0 * nb, st);
+        }
         cudaMemcpyAsync(c.xk, c.xseg + (int64_t)sp.li0 * nb, sizeof(double) * bk,
                         cudaMemcpyDeviceToDevice, st);
       }
@@ -1652,7 +1710,7 @@ int hlq_factor_dist(hlq_grid_t grid, double* const* A_local, const int64_t* lld,
   if (opt.tie_rel_tol == 0.0) opt.tie_rel_tol = 1e-10;
   if (opt.ib != 32 || D < P || D % P != 0 || D / P > 16 || opt.tree != HLQ_TREE_GREEDY ||
       opt.mumps_reading < 0 || opt.mumps_reading > 1 || opt.lu_variant != HLQ_LU_A1 ||
-      opt.pivot_scope != HLQ_PIVOT_TILE)
+      opt.pivot_scope < HLQ_PIVOT_TILE || opt.pivot_scope > HLQ_PIVOT_DOMAIN)
     return -8;
   hlq_factors_t f = new (std::nothrow) hlq_factors_s();
   if (!f) return HLQ_ERR_NOMEM;
@@ -1682,6 +1740,8 @@ int hlq_factor_dist(hlq_grid_t grid, double* const* A_local, const int64_t* lld,
   ds->D = D;
   ds->c = D / P;
   ds->S = D;
+  ds->dpiv = opt.pivot_scope == HLQ_PIVOT_DOMAIN;
+  f->pivot_scope = opt.pivot_scope;
   ds->ib = opt.ib;
   ds->nb = nb;
   ds->n = n;

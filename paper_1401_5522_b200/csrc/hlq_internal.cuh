@@ -93,6 +93,8 @@ void launch_panel_stats_to(const double* A, Geo g, int k, int diag, double* s, d
 // NEXT f1: statistics split by the diagonal domain (tiles i = k mod D): local_max over the domain,
 // away_max and s_i over the other tiles (s_i = 0 inside the domain)
 void launch_panel_stats_domain(const double* A, Geo g, int k, int D, DevWork w, cudaStream_t st);
+void launch_panel_stats_domain_to(const double* A, Geo g, int k, int D, double* s,
+                                  double* local_max, double* away_max, cudaStream_t st);
 // NEXT f1 (domain.cu): speculative stack factorization into w.wdom / w.dipiv + top tile into W;
 // commit (dec == LU) of the stack over the domain tiles; the domain's interchanges on columns
 // [c0, c1) (dec == LU) and on the solve's vector

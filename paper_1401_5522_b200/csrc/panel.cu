@@ -98,13 +98,20 @@ void launch_panel_stats_to(const double* A, Geo g, int k, int diag, double* s, d
 }
 
 void launch_panel_stats_domain(const double* A, Geo g, int k, int D, DevWork w, cudaStream_t st) {
-  cudaMemsetAsync(w.away_max, 0, sizeof(double) * g.nb, st);
-  cudaMemsetAsync(w.local_max, 0, sizeof(double) * g.nb, st);
+  launch_panel_stats_domain_to(A, g, k, D, w.s, w.local_max, w.away_max, st);
+}
+
+// the same into explicit outputs (the 2D grid's statistics record: the owner of the diagonal tile
+// holds the whole diagonal domain, tiles k, k + D, ... of its local panel)
+void launch_panel_stats_domain_to(const double* A, Geo g, int k, int D, double* s,
+                                  double* local_max, double* away_max, cudaStream_t st) {
+  cudaMemsetAsync(away_max, 0, sizeof(double) * g.nb, st);
+  cudaMemsetAsync(local_max, 0, sizeof(double) * g.nb, st);
   if (g.n - k <= 0) return;
-  cudaMemsetAsync(w.s + k, 0, sizeof(double) * (g.n - k), st);
+  cudaMemsetAsync(s + k, 0, sizeof(double) * (g.n - k), st);
   ::hlq::g_launches++;
   const dim3 grid(g.n - k, (g.cbs(k) + PS_CHUNK - 1) / PS_CHUNK);
-  k_panel_stats<<<grid, 256, 0, st>>>(A, g, k, 1, w.s, w.local_max, w.away_max, D);
+  k_panel_stats<<<grid, 256, 0, st>>>(A, g, k, 1, s, local_max, away_max, D);
 }
 
 // ---------------------------------------------------------------------------------------------

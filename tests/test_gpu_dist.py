@@ -28,7 +28,8 @@ def H():
     return H
 
 
-def run_dist(H, A, b, nb, P, Q, crit=O.CRIT_MAX, alpha=1.0, D=None, forced=None, fo=None):
+def run_dist(H, A, b, nb, P, Q, crit=O.CRIT_MAX, alpha=1.0, D=None, forced=None, fo=None,
+             pivot_scope="tile"):
     N = A.shape[0]
     D = P if D is None else D
     if fo is None:
@@ -37,7 +38,8 @@ def run_dist(H, A, b, nb, P, Q, crit=O.CRIT_MAX, alpha=1.0, D=None, forced=None,
         def hook(k, Ab, Aa, d):
             sl = O.tsl(N, nb, k)
             pre[k] = Ab[sl, sl].copy()
-        fo = O.hybrid_factor(A, nb, crit, alpha, D=D, forced=forced, on_step=hook)
+        fo = O.hybrid_factor(A, nb, crit, alpha, D=D, forced=forced, on_step=hook,
+                             pivot_scope=pivot_scope)
         fo.pre_tiles = pre
     grid = H.grid_local(P, Q)
     locs = []
@@ -46,6 +48,8 @@ def run_dist(H, A, b, nb, P, Q, crit=O.CRIT_MAX, alpha=1.0, D=None, forced=None,
         locs.append(H.to_colmajor(L) if L.size else torch.zeros(0, dtype=torch.float64,
                                                                  device="cuda"))
     kw = dict(tree_domains=D)
+    if pivot_scope == "domain":
+        kw["pivot_scope"] = H.PIVOT_DOMAIN
     if forced is not None:
         f = H.hlq_factor_dist(grid, locs, N, nb, crit, alpha, forced=forced, **kw)
         fo.hinted_run, fo.forced_run = False, True
@@ -95,6 +99,29 @@ def test_grid_domains_match_single_gpu(H, P, Q, D):
     check(fo, f, F, x, A, b)
     dA = H.to_colmajor(A)
     fs = H.hlq_factor_ex(dA, N, nb, O.CRIT_MAX, 1.0, tree_domains=D, **hint_kwargs(fo))
+    np.testing.assert_array_equal(fs.decisions(), f.decisions())
+    assert O.factor_diff(F, H.from_colmajor(dA)) <= 1e-13
+
+
+@pytest.mark.parametrize("P,Q,D,crit,alpha", [
+    (2, 1, 2, O.CRIT_MAX, 300.0), (2, 2, 2, O.CRIT_MAX, 300.0), (1, 2, 2, O.CRIT_MAX, 300.0),
+    (2, 3, 4, O.CRIT_MAX, 300.0), (2, 2, 2, O.CRIT_MUMPS, 2.1), (2, 1, 2, O.CRIT_MAX, math.inf),
+    (1, 1, 1, O.CRIT_MAX, math.inf)])
+def test_grid_domain_pivoting(H, P, Q, D, crit, alpha):
+    """NEXT f1 on the 2D grid (reading 33): the diagonal domain (tiles i = k mod D, P | D)
+    lives on one process row, so the stacked partial-pivoting LU, the domain statistics and the
+    domain's row interchanges are rank-local; the pivots travel in the panel package.  Against the
+    oracle's domain-pivoting run and the single-GPU domain-pivoting path (same kernels)."""
+    N, nb = 1000, 64                       # 16 tiles, ragged last tile of 40
+    A = I.uniform_matrix(2, N)
+    b = I.uniform_rhs(2, N)
+    fo, f, F, x = run_dist(H, A, b, nb, P, Q, crit=crit, alpha=alpha, D=D, pivot_scope="domain")
+    check(fo, f, F, x, A, b)
+    if P == 1 and Q == 1 and D == 1:      # D = 1: LU with partial pivoting over the whole panel
+        assert (fo.dec == 0).all()
+    dA = H.to_colmajor(A)
+    fs = H.hlq_factor_ex(dA, N, nb, crit, alpha, tree_domains=D, pivot_scope=H.PIVOT_DOMAIN,
+                         **hint_kwargs(fo))
     np.testing.assert_array_equal(fs.decisions(), f.decisions())
     assert O.factor_diff(F, H.from_colmajor(dA)) <= 1e-13
 

@@ -34,7 +34,7 @@ def _free_port():
     return p
 
 
-def _rank_main(rank, world, P, Q, port, N, nb, crit, alpha, forced, outdir):
+def _rank_main(rank, world, P, Q, port, N, nb, crit, alpha, forced, outdir, pivot="tile"):
     import torch.distributed as dist
     sys.path.insert(0, ROOT)
     import paper_1401_5522_b200 as H
@@ -79,6 +79,8 @@ def _rank_main(rank, world, P, Q, port, N, nb, crit, alpha, forced, outdir):
     L = H.scatter_block_cyclic(A, nb, P, Q, p, q)
     dA = H.to_colmajor(L) if L.size else torch.zeros(0, dtype=torch.float64, device="cuda")
     kw = dict(tree_domains=P)
+    if pivot == "domain":
+        kw["pivot_scope"] = H.PIVOT_DOMAIN
     if forced is not None:
         kw["forced"] = forced
     f = H.hlq_factor_dist(grid, [dA], N, nb, crit, alpha, **kw)
@@ -99,26 +101,28 @@ def cuda_ok():
     return True
 
 
-@pytest.mark.parametrize("P,Q,N,nb,crit,alpha,f_qr", [
-    (1, 2, 1000, 64, O.CRIT_MAX, 1.2e4, None),   # criterion-decided LU/QR mix, ragged last tile
-    (2, 1, 1000, 64, O.CRIT_MAX, 1.2e4, None),   # two process rows: cross-rank TT head merges
-    (1, 2, 768, 128, O.CRIT_MAX, 1.0, 0.5),      # forced Bernoulli pattern
-    (2, 1, 768, 64, O.CRIT_MAX, 1.0, 1.0),       # all QR, D = 2
+@pytest.mark.parametrize("P,Q,N,nb,crit,alpha,f_qr,pivot", [
+    (1, 2, 1000, 64, O.CRIT_MAX, 1.2e4, None, "tile"),   # criterion-decided LU/QR mix, ragged tile
+    (2, 1, 1000, 64, O.CRIT_MAX, 1.2e4, None, "tile"),   # two process rows: cross-rank TT merges
+    (1, 2, 768, 128, O.CRIT_MAX, 1.0, 0.5, "tile"),      # forced Bernoulli pattern
+    (2, 1, 768, 64, O.CRIT_MAX, 1.0, 1.0, "tile"),       # all QR, D = 2
+    (2, 1, 1000, 64, O.CRIT_MAX, 300.0, None, "domain"),  # diagonal-domain pivoting (NEXT f1)
+    (1, 2, 1000, 64, O.CRIT_MAX, 300.0, None, "domain"),
 ])
-def test_two_process_grid_against_oracle(cuda_ok, P, Q, N, nb, crit, alpha, f_qr):
+def test_two_process_grid_against_oracle(cuda_ok, P, Q, N, nb, crit, alpha, f_qr, pivot):
     import torch.multiprocessing as mp
     import paper_1401_5522_b200 as H
     n = (N + nb - 1) // nb
     forced = I.bernoulli_pattern(30, n, f_qr) if f_qr is not None else None
     A = I.uniform_matrix(11, N)
     b = I.uniform_rhs(11, N)
-    fo = O.hybrid_factor(A, nb, crit, alpha, D=P, forced=forced)
+    fo = O.hybrid_factor(A, nb, crit, alpha, D=P, forced=forced, pivot_scope=pivot)
     assert not np.any(np.isfinite(fo.margin) & (np.abs(fo.margin) < 1e-10))  # no hints needed
     with tempfile.TemporaryDirectory() as td:
         ctx = mp.get_context("spawn")
         port = _free_port()
         procs = [ctx.Process(target=_rank_main, args=(r, P * Q, P, Q, port, N, nb, crit, alpha,
-                                                        forced, td)) for r in range(P * Q)]
+                                                        forced, td, pivot)) for r in range(P * Q)]
         for pr in procs:
             pr.start()
         for pr in procs:
