@@ -4,9 +4,11 @@
 // B200 has no FP64 kind for tcgen05.mma, so the FP64 tensor path is the warp-level DMMA
 // (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4).  What TMA adds here is the operand staging:
 //   * one producer warp (one elected lane) streams 16-deep K slices of the L panel and of the U row
-//     through a 6-stage shared-memory ring with cp.async.bulk.tensor (SWIZZLE_128B boxes), arming
-//     full / empty mbarriers; the 4 consumer warps never issue a global load for A or B and never
-//     meet at a CTA-wide barrier in the main loop;
+//     through a 4-stage shared-memory ring with cp.async.bulk.tensor (SWIZZLE_128B boxes), arming
+//     full / empty mbarriers, and the next tile's C through its own buffer; the consumer warps never
+//     issue a global load for A, B or C and never meet at a CTA-wide barrier in the main loop;
+//   * 8 consumer warps (2 x 4 warp tiles of 32 x 16; 4 per scheduler across the SM's 2 CTAs, so a
+//     warp at a barrier or in its epilogue leaves three others to feed the DMMA pipe);
 //   * every CTA (2 per SM) walks TM_TILES_PER_CTA output tiles in grouped raster order, and the
 //     producer runs ahead into the next tile's K slices while the consumers finish the previous
 //     tile's epilogue (no per-tile prologue bubble); CTAs still retire often enough for the
@@ -34,8 +36,10 @@ namespace hlq {
 
 namespace {
 constexpr int TM_BM = 64, TM_BN = 64, TM_BK = 16, TM_ST = 4;
-constexpr int TM_CONS = 4;                       // consumer warps (2 x 2 warp tiles of 32 x 32)
-constexpr int TM_T = 32 * (TM_CONS + 1);         // + the producer warp
+// consumer warps per CTA: CONS = 4 (2 x 2 warp tiles of 32 x 32) or 8 (2 x 4 warp tiles of 32 x 16:
+// twice the warps per scheduler to cover each other's barrier / epilogue gaps, 0.75 instead of 0.5
+// fragment loads per DMMA); + the producer warp
+constexpr int tm_threads(int cons) { return 32 * (cons + 1); }
 constexpr int TM_A_BYTES = TM_BM * TM_BK * 8;    // 8 KB
 constexpr int TM_B_BYTES = TM_BN * TM_BK * 8;    // 8 KB
 constexpr int TM_STAGE = TM_A_BYTES + TM_B_BYTES;
@@ -103,7 +107,8 @@ struct TmaMaps {
   CUtensorMap c;  // 3D like a, box {16, 64, 4}: a 64 x 64 output tile
 };
 
-__global__ void __launch_bounds__(TM_T, TM_CTAS_PER_SM)
+template <int TM_CONS>
+__global__ void __launch_bounds__(tm_threads(TM_CONS), TM_CTAS_PER_SM)
     k_dgemm_tma(const __grid_constant__ TmaMaps maps, double* __restrict__ C, int64_t ldc,
                 int64_t M, int64_t N, int K, int arow0, int kcol0, int bcol0,
                 const uint8_t* __restrict__ dec, int k, int want, double* __restrict__ colpart,
@@ -176,7 +181,8 @@ __global__ void __launch_bounds__(TM_T, TM_CTAS_PER_SM)
     }
     return;
   }
-  // ---------------- consumers: 4 warps, warp tile 32 x 32 (wm, wn)
+  // ---------------- consumers: TM_CONS warps, warp tile 32 x WTN (wm, wn)
+  constexpr int WN = TM_CONS / 2, WTN = TM_BN / WN, NI = WTN / 8;
   const int g = lane >> 2, t4 = lane & 3;
   const int wm = warp & 1, wn = warp >> 1;
   int s = 0;
@@ -187,17 +193,17 @@ __global__ void __launch_bounds__(TM_T, TM_CTAS_PER_SM)
     // the accumulators start from C (prefetched by TMA into the swizzled C buffer): the update
     // accumulates into A_ij in the DMMAs' own order, bit-identical to gemm.cu's kernel
     const int64_t m0 = tm * TM_BM, n0 = tn * TM_BN;
-    double acc[4][4][2];
+    double acc[4][NI][2];
     mbar_wait(cfull, cph);
     __syncwarp();
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi) {
       const int mhi = wm * 2 + (mi >> 1), mlo = frag_row(g, mi & 1);
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
+      for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int nn = wn * 32 + ni * 8 + 2 * t4 + h;  // C box: 128-byte row = (mhi, column)
+          const int nn = wn * WTN + ni * 8 + 2 * t4 + h;  // C box: 128-byte row = (mhi, column)
           acc[mi][ni][h] = Cs[(mhi * 64 + nn) * 16 + ((((mlo >> 1) ^ (nn & 7)) << 1) | (mlo & 1))];
         }
     }
@@ -216,7 +222,7 @@ __global__ void __launch_bounds__(TM_T, TM_CTAS_PER_SM)
 #pragma unroll
       for (int k4 = 0; k4 < TM_BK; k4 += 4) {
         const int kk = k4 + t4;
-        double a[4], b[4];
+        double a[4], b[NI];
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) {
           const int mhi = wm * 2 + (mi >> 1), mlo = frag_row(g, mi & 1);
@@ -224,14 +230,14 @@ __global__ void __launch_bounds__(TM_T, TM_CTAS_PER_SM)
           a[mi] = neg_bits(As[(mhi * 16 + kk) * 16 + ((((mlo >> 1) ^ (kk & 7)) << 1) | (mlo & 1))]);
         }
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
-          const int nn = wn * 32 + ni * 8 + g;
+        for (int ni = 0; ni < NI; ++ni) {
+          const int nn = wn * WTN + ni * 8 + g;
           b[ni] = Bs[nn * 16 + ((((kk >> 1) ^ g) << 1) | (kk & 1))];
         }
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-          for (int ni = 0; ni < 4; ++ni) dmma_tm(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+          for (int ni = 0; ni < NI; ++ni) dmma_tm(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
       }
       // release the stage: the fragment loads (generic proxy) must be complete and ordered before
       // the producer's next TMA write into it (async proxy) -- the cross-proxy WAR fence; without
@@ -251,8 +257,8 @@ __global__ void __launch_bounds__(TM_T, TM_CTAS_PER_SM)
       const int64_t row = m0 + (wm * 2 + (mi >> 1)) * 16 + frag_row(g, mi & 1);
       if (row >= M) continue;
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) {
-        const int64_t col = n0 + wn * 32 + ni * 8 + 2 * t4;
+      for (int ni = 0; ni < NI; ++ni) {
+        const int64_t col = n0 + wn * WTN + ni * 8 + 2 * t4;
         if (col < N) C[col * ldc + row] = acc[mi][ni][0];
         if (col + 1 < N) C[(col + 1) * ldc + row] = acc[mi][ni][1];
       }
@@ -260,7 +266,7 @@ __global__ void __launch_bounds__(TM_T, TM_CTAS_PER_SM)
     if (colpart != nullptr) {
       // fused a12: per-column |C_new| sums over the tile's 64 rows (rows >= M are exact zeros)
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
+      for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           double v = 0.0;
@@ -269,7 +275,7 @@ __global__ void __launch_bounds__(TM_T, TM_CTAS_PER_SM)
           v += __shfl_xor_sync(0xffffffffu, v, 4);
           v += __shfl_xor_sync(0xffffffffu, v, 8);
           v += __shfl_xor_sync(0xffffffffu, v, 16);
-          if (g == 0) red[wm * TM_BN + wn * 32 + ni * 8 + 2 * t4 + h] = v;
+          if (g == 0) red[wm * TM_BN + wn * WTN + ni * 8 + 2 * t4 + h] = v;
         }
       asm volatile("bar.sync 1, %0;" ::"n"(32 * TM_CONS) : "memory");
       if (tid < TM_BN && n0 + tid < N) colpart[tm * ldp + n0 + tid] = red[tid] + red[TM_BN + tid];
@@ -355,9 +361,15 @@ bool launch_schur_tma(const void* maps, double* A, int64_t lda, int64_t k0, int6
                       int64_t M, int64_t nc, int K, const uint8_t* dec, int k, int want,
                       double* colpart, int64_t ldp, cudaStream_t st) {
   if (!maps || K % TM_BK || k1 % 16 || M <= 0 || nc <= 0) return false;
+  static int cons = -1;
+  // 8 consumer warps by default (C3 step-1 shape: 33.5 TF vs 32.9 with 4; cuBLAS DGEMM on the same
+  // shape 33.0, profiles/r02/schur_vs_cublas.jsonl); HLQ_TMA_CONS=4 selects the 2 x 2 warp grid
+  if (cons < 0) cons = (getenv("HLQ_TMA_CONS") && atoi(getenv("HLQ_TMA_CONS")) == 4) ? 4 : 8;
   static unsigned long long attr = 0;
-  if (first_on_device(attr))
-    cudaFuncSetAttribute(k_dgemm_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, TM_SMEM);
+  if (first_on_device(attr)) {
+    cudaFuncSetAttribute(k_dgemm_tma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, TM_SMEM);
+    cudaFuncSetAttribute(k_dgemm_tma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, TM_SMEM);
+  }
   const int64_t tiles = ((M + TM_BM - 1) / TM_BM) * ((nc + TM_BN - 1) / TM_BN);
   static int64_t tpc = -1;
   if (tpc < 0) tpc = getenv("HLQ_TMA_TPC") ? atoll(getenv("HLQ_TMA_TPC")) : TM_TILES_PER_CTA;
@@ -365,9 +377,14 @@ bool launch_schur_tma(const void* maps, double* A, int64_t lda, int64_t k0, int6
       1, std::min<int64_t>(tpc, tiles / ((int64_t)sm_count() * TM_CTAS_PER_SM)));
   const int64_t grid = (tiles + tpc_eff - 1) / tpc_eff;
   ::hlq::g_launches++;
-  k_dgemm_tma<<<(unsigned)grid, TM_T, TM_SMEM, st>>>(
-      *(const TmaMaps*)maps, A + c0 * lda + k1, lda, M, nc, K, (int)k1, (int)k0, (int)c0, dec, k,
-      want, colpart, ldp ? ldp : nc, tpc_eff);
+  if (cons == 8)
+    k_dgemm_tma<8><<<(unsigned)grid, tm_threads(8), TM_SMEM, st>>>(
+        *(const TmaMaps*)maps, A + c0 * lda + k1, lda, M, nc, K, (int)k1, (int)k0, (int)c0, dec, k,
+        want, colpart, ldp ? ldp : nc, tpc_eff);
+  else
+    k_dgemm_tma<4><<<(unsigned)grid, tm_threads(4), TM_SMEM, st>>>(
+        *(const TmaMaps*)maps, A + c0 * lda + k1, lda, M, nc, K, (int)k1, (int)k0, (int)c0, dec, k,
+        want, colpart, ldp ? ldp : nc, tpc_eff);
   return true;
 }
 

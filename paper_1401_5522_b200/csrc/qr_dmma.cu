@@ -279,21 +279,31 @@ __device__ void panel_factor(double* Vs, int ldc, double* Rs, double* Ts, int R,
           *reinterpret_cast<double2*>(xs + i) = make_double2(a[i], a[i + 1]);
       }
       __syncwarp();
+      // four independent FMA chains (NR is a multiple of 4): the dot product's latency is on the
+      // critical path of every column
+      double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
       if (ilo == 0 && ihi == NR) {  // every row of the warp (no per-row predicates)
 #pragma unroll
-        for (int i = 0; i < NR; i += 2) {
+        for (int i = 0; i < NR; i += 4) {
           const double2 x = *reinterpret_cast<const double2*>(xs + i);
-          part += a[i] * x.x;
-          part += a[i + 1] * x.y;
+          const double2 y = *reinterpret_cast<const double2*>(xs + i + 2);
+          p0 = fma(a[i], x.x, p0);
+          p1 = fma(a[i + 1], x.y, p1);
+          p2 = fma(a[i + 2], y.x, p2);
+          p3 = fma(a[i + 3], y.y, p3);
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < NR; i += 2) {
+        for (int i = 0; i < NR; i += 4) {
           const double2 x = *reinterpret_cast<const double2*>(xs + i);
-          if (i >= ilo && i < ihi) part += a[i] * x.x;
-          if (i + 1 >= ilo && i + 1 < ihi) part += a[i + 1] * x.y;
+          const double2 y = *reinterpret_cast<const double2*>(xs + i + 2);
+          if (i >= ilo && i < ihi) p0 = fma(a[i], x.x, p0);
+          if (i + 1 >= ilo && i + 1 < ihi) p1 = fma(a[i + 1], x.y, p1);
+          if (i + 2 >= ilo && i + 2 < ihi) p2 = fma(a[i + 2], y.x, p2);
+          if (i + 3 >= ilo && i + 3 < ihi) p3 = fma(a[i + 3], y.y, p3);
         }
       }
+      part = (p0 + p1) + (p2 + p3);
     }
     red[(bf * 8 + warp) * 33 + lane] = part;
     if (!TT && l >= rw && l < rw + NR) {
@@ -302,17 +312,19 @@ __device__ void panel_factor(double* Vs, int ldc, double* Rs, double* Ts, int R,
         if (rw + i == l) top[bf * 32 + lane] = a[i];
     }
     __syncthreads();
-    double gsum = 0.0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) gsum += red[(bf * 8 + w) * 33 + lane];
+    // the 8 warp partials as a fixed tree (the same order in every warp: identical gsum)
+    const double* rp = red + bf * 8 * 33 + lane;
+    const double gsum = ((rp[0] + rp[33]) + (rp[2 * 33] + rp[3 * 33])) +
+                        ((rp[4 * 33] + rp[5 * 33]) + (rp[6 * 33] + rp[7 * 33]));
     const double ssq = __shfl_sync(0xffffffffu, gsum, l);
     const double alpha = TT ? Rs[l * 33 + l] : top[bf * 32 + l];
     double tau = 0.0, beta = alpha, rsc = 0.0;
     if (ssq != 0.0) {
       const double nrm = sqrt(alpha * alpha + ssq);
       beta = alpha >= 0.0 ? -nrm : nrm;
-      tau = (beta - alpha) / beta;
-      rsc = 1.0 / (alpha - beta);
+      // two independent correctly rounded divisions (dlarfg's tau and 1 / (alpha - beta))
+      tau = __ddiv_rn(beta - alpha, beta);
+      rsc = __drcp_rn(alpha - beta);
     }
     // lane c: w_c = top_c + V_c . v (c > l), z_q = [V_q(l)] + V_q . v (q < l)
     double topc = 0.0;
@@ -492,7 +504,10 @@ __device__ void qrt_pair(double* __restrict__ A, Geo g, int k, int ib, double* _
     for (int o = tid; o < 32 * 33; o += QD_T) {
       Ts[o] = 0.0;
       int l = o / 33, q = o - l * 33;
-      Rs[o] = (l < sb && q <= l) ? Re[(int64_t)(i0 + l) * g.lda + i0 + q] : 0.0;
+      if (l < sb && q <= l)  // R_e's block triangle, in flight with V's block
+        cpa8(Rs + o, Re + (int64_t)(i0 + l) * g.lda + i0 + q);
+      else
+        Rs[o] = 0.0;
     }
     cpa_wait_all();
     __syncthreads();

@@ -27,6 +27,15 @@ __device__ __forceinline__ void cp8(void* s, const void* g, bool v) {
   int sz = v ? 8 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(g), "r"(sz));
 }
+// the same with a 32-bit shared-window address (no generic -> shared conversion per copy)
+__device__ __forceinline__ void cp16s(unsigned sa, const void* g, bool v) {
+  int sz = v ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(sz));
+}
+__device__ __forceinline__ void cp8s(unsigned sa, const void* g, bool v) {
+  int sz = v ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(g), "r"(sz));
+}
 __device__ __forceinline__ void commit_() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void wait_() {
@@ -118,6 +127,105 @@ __device__ __forceinline__ void qr_update3_body(const double* __restrict__ A, Ge
   double* Cg = base + c0 * ldcg + g.r0(i);
   const int wc = cg * 16;  // first slab column of this warp
 
+  const int nblk = (bk + 31) / 32;
+  const int nch_i = (crows + 31) / 32;
+  auto chunk_lo = [&](int b) { return TT ? 0 : b; };
+  auto chunk_hi = [&](int b) {
+    return (TT && !TS) ? (b < nch_i - 1 ? b : nch_i - 1) : nch_i - 1;
+  };
+  // the chunk schedule (block, pass, chunk) of the whole CTA, built once: the producer is a table
+  // lookup per chunk
+  // (block, pass, chunk) entries: GEQRT / TT reflectors touch chunks up to their block, a square TS
+  // reflector block all NCH chunks
+  constexpr int MAXS = (TS ? 2 * NCH * NCH : 2 * NCH * (NCH + 1) / 2) + 2;
+  int* sched = reinterpret_cast<int*>(CE + 2 * W * LD3);  // (dynamic shared memory, after C_e)
+  // entries of block b start at 2 * (chunks of blocks < b); warp 0, one lane per block (nblk <= 10)
+  auto nch_of = [&](int b) { return chunk_hi(b) >= chunk_lo(b) ? chunk_hi(b) - chunk_lo(b) + 1 : 0; };
+  int S = 0;
+  for (int b = 0; b < nblk; ++b) S += 2 * nch_of(b);  // (uniform, cheap: <= 10 terms)
+  if (warp == 0 && lane < nblk) {
+    const int b = lane;
+    int n = 0;
+    for (int b2 = 0; b2 < b; ++b2) n += 2 * nch_of(b2);
+    const int lo = chunk_lo(b), hi = chunk_hi(b);
+    for (int pass = 0; pass < 2; ++pass)
+      for (int ch = lo; ch <= hi; ++ch) sched[n++] = (b << 16) | (pass << 8) | ch;
+  }
+  __syncthreads();
+  // per-thread copy coordinates (16-byte copies: column l, rows r, r+1 of a 32 x 32 chunk)
+  constexpr int CPT = 512 / NT;   // copies per thread per chunk
+  const int cl0 = tid >> 4, cr = (tid & 15) * 2;
+  int64_t goff[CPT];
+#pragma unroll
+  for (int u = 0; u < CPT; ++u) goff[u] = (int64_t)(cl0 + (NT / 16) * u) * g.lda + cr;
+  int ps = 0;
+  int pslot = 0;  // ring slot of the next chunk
+  const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring);
+  const unsigned ts_s = ring_s + (unsigned)(RING * CH3) * 8u;
+  const unsigned ce_s = ts_s + (unsigned)(2 * CH3 + RQ * NCG * 512) * 8u;
+  auto issue = [&]() {
+    if (ps < S) {
+      const int se = sched[ps];
+      const int pb = se >> 16, pass = (se >> 8) & 1, ch = se & 255;
+      const int i0 = 32 * pb;
+      const int cmax = (bk - i0) < 32 ? (bk - i0) : 32;
+      const double* src = Vt + (int64_t)i0 * g.lda + 32 * ch;
+      const int rmax = crows - 32 * ch;  // valid rows in this chunk
+      const int ld = pass == 0 ? LD3 : LD3B;
+      const unsigned slot_s = ring_s + (unsigned)(pslot * CH3) * 8u;
+      if (V16) {
+        const bool rok = cr < rmax;
+#pragma unroll
+        for (int u = 0; u < CPT; ++u) {
+          const int l = cl0 + (NT / 16) * u;
+          const bool ok = rok && (l < cmax);
+          cp16s(slot_s + (unsigned)(l * ld + cr) * 8u, ok ? src + goff[u] : src, ok);
+        }
+      } else {
+        for (int o = tid; o < 1024; o += NT) {
+          const int l = o >> 5, r = o & 31;
+          const bool ok = (r < rmax) && (l < cmax);
+          cp8s(slot_s + (unsigned)(l * ld + r) * 8u, ok ? src + (int64_t)l * g.lda + r : src, ok);
+        }
+      }
+      if (pass == 0 && ch == chunk_lo(pb)) {
+        const unsigned t_s = ts_s + (unsigned)((pb & 1) * CH3) * 8u;
+#pragma unroll
+        for (int u = 0; u < CPT; ++u) {
+          const int l = cl0 + (NT / 16) * u;
+          const bool ok = l < cmax;
+          cp16s(t_s + (unsigned)(l * LD3 + cr) * 8u, ok ? T + (int64_t)(i0 + l) * 32 + cr : T, ok);
+        }
+        if (TT) {
+          // rows i0.. of C_e for this block (W = C_e(b) + V^T C_i; C_e(b) -= U after the TRMM)
+          const unsigned c_s = ce_s + (unsigned)((pb & 1) * W * LD3) * 8u;
+          const double* cs = base + c0 * ldcg + g.r0(e) + i0;
+          if (V16) {
+            for (int o = tid; o < W * 16; o += NT) {
+              const int j = o >> 4, r = (o & 15) * 2;
+              const bool ok = (j < cvalid) && (r < cmax);
+              cp16s(c_s + (unsigned)(j * LD3 + r) * 8u, ok ? cs + (int64_t)j * ldcg + r : cs, ok);
+            }
+          } else {
+            for (int o = tid; o < W * 32; o += NT) {
+              const int j = o >> 5, r = o & 31;
+              const bool ok = (j < cvalid) && (r < cmax);
+              cp8s(c_s + (unsigned)(j * LD3 + r) * 8u, ok ? cs + (int64_t)j * ldcg + r : cs, ok);
+            }
+          }
+        }
+      }
+      pslot = pslot == RING - 1 ? 0 : pslot + 1;
+      ++ps;
+    }
+    commit_();
+  };
+  // a TT / TS merge of a tile with <= 32 rows has one chunk per pass in every block: prefetch 3
+  // chunks ahead instead of 4 so block b + 2's T / C_e never overwrite block b's before its TRMM
+  const bool short3 = TT && nch_i == 1;
+#pragma unroll 1
+  for (int d = 0; d < (short3 ? RING - 2 : RING - 1); ++d) issue();
+  // the slab's C^T fragments, loaded while the first chunks are in flight
   // ---- C^T fragments: cT[m][j][h] = C(row 8 RB + 2t + h, col wc + 8m + g), RB = RQ j + rh
   double cT[2][NJ][2];
 #pragma unroll
@@ -139,99 +247,6 @@ __device__ __forceinline__ void qr_update3_body(const double* __restrict__ A, Ge
     }
   }
 
-  const int nblk = (bk + 31) / 32;
-  const int nch_i = (crows + 31) / 32;
-  auto chunk_lo = [&](int b) { return TT ? 0 : b; };
-  auto chunk_hi = [&](int b) {
-    return (TT && !TS) ? (b < nch_i - 1 ? b : nch_i - 1) : nch_i - 1;
-  };
-  // the chunk schedule (block, pass, chunk) of the whole CTA, built once: the producer is a table
-  // lookup per chunk
-  // (block, pass, chunk) entries: GEQRT / TT reflectors touch chunks up to their block, a square TS
-  // reflector block all NCH chunks
-  constexpr int MAXS = (TS ? 2 * NCH * NCH : 2 * NCH * (NCH + 1) / 2) + 2;
-  __shared__ int sched[MAXS];
-  __shared__ int nsched;
-  if (tid == 0) {
-    int n = 0;
-    for (int b = 0; b < nblk; ++b) {
-      const int lo = chunk_lo(b), hi = chunk_hi(b);
-      for (int pass = 0; pass < 2; ++pass)
-        for (int ch = lo; ch <= hi; ++ch) sched[n++] = (b << 16) | (pass << 8) | ch;
-    }
-    nsched = n;
-  }
-  __syncthreads();
-  const int S = nsched;
-  // per-thread copy coordinates (16-byte copies: column l, rows r, r+1 of a 32 x 32 chunk)
-  constexpr int CPT = 512 / NT;   // copies per thread per chunk
-  const int cl0 = tid >> 4, cr = (tid & 15) * 2;
-  int64_t goff[CPT];
-#pragma unroll
-  for (int u = 0; u < CPT; ++u) goff[u] = (int64_t)(cl0 + (NT / 16) * u) * g.lda + cr;
-  int ps = 0;
-  double* pslot = ring;
-  auto issue = [&]() {
-    if (ps < S) {
-      const int se = sched[ps];
-      const int pb = se >> 16, pass = (se >> 8) & 1, ch = se & 255;
-      const int i0 = 32 * pb;
-      const int cmax = (bk - i0) < 32 ? (bk - i0) : 32;
-      const double* src = Vt + (int64_t)i0 * g.lda + 32 * ch;
-      const int rmax = crows - 32 * ch;  // valid rows in this chunk
-      const int ld = pass == 0 ? LD3 : LD3B;
-      if (V16) {
-        const bool rok = cr < rmax;
-#pragma unroll
-        for (int u = 0; u < CPT; ++u) {
-          const int l = cl0 + (NT / 16) * u;
-          const bool ok = rok && (l < cmax);
-          cp16(pslot + l * ld + cr, ok ? src + goff[u] : src, ok);
-        }
-      } else {
-        for (int o = tid; o < 1024; o += NT) {
-          const int l = o >> 5, r = o & 31;
-          const bool ok = (r < rmax) && (l < cmax);
-          cp8(pslot + l * ld + r, ok ? src + (int64_t)l * g.lda + r : src, ok);
-        }
-      }
-      if (pass == 0 && ch == chunk_lo(pb)) {
-        double* ts = Ts + (pb & 1) * CH3;
-#pragma unroll
-        for (int u = 0; u < CPT; ++u) {
-          const int l = cl0 + (NT / 16) * u;
-          const bool ok = l < cmax;
-          cp16(ts + l * LD3 + cr, ok ? T + (int64_t)(i0 + l) * 32 + cr : T, ok);
-        }
-        if (TT) {
-          // rows i0.. of C_e for this block (W = C_e(b) + V^T C_i; C_e(b) -= U after the TRMM)
-          double* ce = CE + (pb & 1) * W * LD3;
-          const double* cs = base + c0 * ldcg + g.r0(e) + i0;
-          if (V16) {
-            for (int o = tid; o < W * 16; o += NT) {
-              const int j = o >> 4, r = (o & 15) * 2;
-              const bool ok = (j < cvalid) && (r < cmax);
-              cp16(ce + j * LD3 + r, ok ? cs + (int64_t)j * ldcg + r : cs, ok);
-            }
-          } else {
-            for (int o = tid; o < W * 32; o += NT) {
-              const int j = o >> 5, r = o & 31;
-              const bool ok = (j < cvalid) && (r < cmax);
-              cp8(ce + j * LD3 + r, ok ? cs + (int64_t)j * ldcg + r : cs, ok);
-            }
-          }
-        }
-      }
-      pslot = (pslot == ring + (RING - 1) * CH3) ? ring : pslot + CH3;
-      ++ps;
-    }
-    commit_();
-  };
-  // a TT / TS merge of a tile with <= 32 rows has one chunk per pass in every block: prefetch 3
-  // chunks ahead instead of 4 so block b + 2's T / C_e never overwrite block b's before its TRMM
-  const bool short3 = TT && nch_i == 1;
-#pragma unroll 1
-  for (int d = 0; d < (short3 ? RING - 2 : RING - 1); ++d) issue();
   // explicit structure of the diagonal 32 x 32 block of V_b (GEQRT: unit diagonal, zeros above;
   // TT: zeros below the diagonal); element (r, l) at V[r * sr + l * sl]
   auto fix_diag = [&](double* V, int sr, int sl) {
@@ -484,7 +499,9 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
 }
 
 static size_t upd3_smem(int warps, int W) {
-  return sizeof(double) * ((size_t)7 * CH3 + (size_t)warps * 512 + (size_t)2 * W * LD3);
+  // ring + T ring (7 chunks), W partials, C_e rows (2 x W x LD3), the chunk schedule
+  return sizeof(double) * ((size_t)7 * CH3 + (size_t)warps * 512 + (size_t)2 * W * LD3) +
+         sizeof(int) * (size_t)(2 * 10 * 10 + 2);
 }
 
 template <int NB, int RQ, int NCG, bool V16>

@@ -56,7 +56,8 @@ def _run(env_extra, path):
     return np.load(path)
 
 
-@pytest.mark.parametrize("env", [{"HLQ_SPEC_QR": "0"}, {"HLQ_DGEMM_TILE": "4x2"}, {"HLQ_DGEMM_TMA": "0"}])
+@pytest.mark.parametrize("env", [{"HLQ_SPEC_QR": "0"}, {"HLQ_DGEMM_TILE": "4x2"}, {"HLQ_DGEMM_TMA": "0"},
+                                 {"HLQ_TMA_CONS": "4"}])
 def test_variant_is_bit_identical(tmp_path, env):
     base = _run({}, str(tmp_path / "base.npz"))
     var = _run(env, str(tmp_path / "var.npz"))
