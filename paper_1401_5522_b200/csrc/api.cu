@@ -216,6 +216,30 @@ static void plan_step(int k, int n, int D, int tsa, StepPlanHost& p) {
   halving(dom_heads, p.levels);
 }
 
+// The QR panel of step k as a DAG (qr_dmma.cu k_qr_panel_dag): GEQRT of the factored rows (op 0
+// is tile k), the TS chain pairs in chain order, the TT levels in order; each op records the
+// previous op on its eliminator / head row and on its eliminated row (-1: none).
+static void build_dag(int k, int n, int tsa, const StepPlanHost& p, std::vector<int>& ops) {
+  std::vector<int> last(n, -1);
+  auto add = [&](int kind, int e, int i, int pe, int pi) {
+    const int id = (int)(ops.size() / 5);
+    ops.insert(ops.end(), {kind, e, i, pe, pi});
+    return id;
+  };
+  std::vector<int> geq;
+  if (tsa >= 1 && p.ts_off.size() > 1)
+    geq = p.heads;
+  else
+    for (int i = k; i < n; ++i) geq.push_back(i);
+  for (int i : geq) last[i] = add(0, i, i, -1, -1);
+  for (const int2& pr : p.ts_pairs) last[pr.x] = add(1, pr.x, pr.y, last[pr.x], -1);
+  for (const auto& lv : p.levels)
+    for (const int2& pr : lv) {
+      const int id = add(2, pr.x, pr.y, last[pr.x], last[pr.y]);
+      last[pr.x] = id;
+    }
+}
+
 extern "C" {
 
 int hlq_abi(int32_t* so, int32_t* si, int32_t* ver) {
@@ -320,6 +344,18 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   }
   f->tree = opt.tree;
   f->ts_group = tsa;
+  // the QR panel as one DAG launch per step (HLQ_QR_DAG=0: the level-by-level launches)
+  static int dag_env = -1;
+  if (dag_env < 0) dag_env = getenv("HLQ_QR_DAG") ? atoi(getenv("HLQ_QR_DAG")) : 1;
+  std::vector<std::vector<int>> dag_ops(n);
+  size_t dag_total = 0, dag_max = 0;
+  if (dag_env != 0 && ib == 32) {
+    for (int k = 0; k < n; ++k) {
+      build_dag(k, n, tsa, plans[k], dag_ops[k]);
+      dag_total += dag_ops[k].size();
+      dag_max = std::max(dag_max, dag_ops[k].size() / 5);
+    }
+  }
 
   // workspace layout (bytes, 256-aligned pieces)
   const size_t ntri = (size_t)n * (n + 1) / 2;
@@ -363,6 +399,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   const int scmax = solve_rows_cmax(n, kSolveG);
   const size_t solve_cap = (size_t)2 * n * scmax + 1;
   size_t oSv = take(solve_ws_bytes(n, nb, scmax, solve_cap));
+  size_t oDag = take(sizeof(int) * (dag_total + 1)), oDagP = take(sizeof(int) * (dag_max + 1));
   f->ws_bytes = off;
   f->dev = cur_device();
   f->ws_block = cache_get(0, off);
@@ -424,6 +461,22 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   f->lvl_cnt.assign(n, {});
   f->tsplan.assign(n, QRTsPlan{nullptr, 0, nullptr, nullptr, 0});
   int* hbase = (int*)(base + oHd);
+  f->dag.assign(n, QRDag{nullptr, 0});
+  f->dag_progress = (int*)(base + oDagP);
+  f->dag_epoch = 0;
+  if (dag_total > 0) {
+    std::vector<int> dflat;
+    dflat.reserve(dag_total);
+    int* dbase = (int*)(base + oDag);
+    for (int k = 0; k < n; ++k) {
+      f->dag[k] = QRDag{dbase + dflat.size(), (int)(dag_ops[k].size() / 5)};
+      dflat.insert(dflat.end(), dag_ops[k].begin(), dag_ops[k].end());
+    }
+    if ((rc = cuda_err(cudaMemcpyAsync(dbase, dflat.data(), sizeof(int) * dflat.size(),
+                                       cudaMemcpyHostToDevice, st))))
+      return rc;
+    cudaMemsetAsync(f->dag_progress, 0, sizeof(int) * (dag_max + 1), st);
+  }
   for (int k = 0; k < n; ++k) {
     for (auto& lv : plans[k].levels) {
       f->lvl_ptr[k].push_back(w.pairs + flat.size());
@@ -524,7 +577,8 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
       // predicated on d_k with "undecided" = run: once the criterion decides LU, the remaining
       // speculative launches exit at their first instruction
       launch_qr_panel(w.qpan - k0 * N, gq, k, ib, f->lvl_ptr[k].data(), f->lvl_cnt[k].data(), nl,
-                      wk, sq, /*diag_done=*/a2, /*spec=*/true, &f->tsplan[k]);
+                      wk, sq, /*diag_done=*/a2, /*spec=*/true, &f->tsplan[k], &f->dag[k],
+                      f->dag_progress, ++f->dag_epoch);
       P.end(sq);
       cudaEventRecord(ev_qdone, sq);
     };
@@ -613,7 +667,8 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
     } else if (known != HLQ_DEC_LU) {
       P.begin(HLQ_PROF_QR_GEQRT, sp);
       launch_qr_panel(A, g, k, ib, f->lvl_ptr[k].data(), f->lvl_cnt[k].data(), nl, wk, sp,
-                      /*diag_done=*/a2 && known != HLQ_DEC_QR, /*spec=*/false, &f->tsplan[k]);
+                      /*diag_done=*/a2 && known != HLQ_DEC_QR, /*spec=*/false, &f->tsplan[k],
+                      &f->dag[k], f->dag_progress, ++f->dag_epoch);
       P.end(sp);
     }
     cudaEventRecord(ev_panel, sp);

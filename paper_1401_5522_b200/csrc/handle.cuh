@@ -82,6 +82,9 @@ struct hlq_factors_s {
   size_t ws_bytes = 0;
   int tree = 0, ts_group = 0;  // HLQ_TREE_*, the HQR TS group size (0: greedy)
   std::vector<hlq::QRTsPlan> tsplan;  // per step: the HQR TS level (ngroups = 0: none)
+  std::vector<hlq::QRDag> dag;        // per step: the QR panel as one DAG launch (empty: off)
+  int* dag_progress = nullptr;        // device, per op of a DAG launch
+  int dag_epoch = 0;                  // launches so far (progress values are epoch << 8 | blocks)
   // QR-tree plan: per step k, TT levels l: device pointer + count
   std::vector<std::vector<const int2*>> lvl_ptr;
   std::vector<std::vector<int>> lvl_cnt;

@@ -76,6 +76,13 @@ struct DevWork {
 };
 
 // ---- the HQR tree's TS level of one QR step (DESIGN reading 34); nullptr / ngroups = 0: greedy
+// the QR panel of one step as a dependency DAG (qr_dmma.cu k_qr_panel_dag): device op list
+// (5 ints per op: kind, e, i, previous op on row e, previous op on row i), op 0 = GEQRT of tile k
+struct QRDag {
+  const int* ops;
+  int nops;
+};
+
 struct QRTsPlan {
   const int* heads;      // device: the GEQRT / UNMQR tile rows (the group heads), ascending
   int nheads;
@@ -205,7 +212,12 @@ void launch_gemm_sub(double* C, int64_t ldc, const double* Am, int64_t lda, cons
 // spec: the speculative QR panel (runs while d_k is undecided, see launch_qr_panel_tc)
 void launch_qr_panel(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
                      const int* level_count, int nlevels, const DevWork& w, cudaStream_t st,
-                     bool diag_done = false, bool spec = false, const QRTsPlan* ts = nullptr);
+                     bool diag_done = false, bool spec = false, const QRTsPlan* ts = nullptr,
+                     const QRDag* dag = nullptr, int* progress = nullptr, int epoch = 0);
+// one launch for the whole panel DAG; skip_first: op 0 (GEQRT of tile k) was done by the caller
+void launch_qr_panel_dag(double* A, Geo g, int k, int ib, double* Tg, double* Ttt, const int* ops,
+                         int nops, int* progress, int epoch, const uint8_t* dec, cudaStream_t st,
+                         bool spec, bool skip_first);
 // returns whether every TTMQR level fused the a12 scan into gmax (gmax != nullptr)
 bool launch_qr_update(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
                       const int* level_count, int nlevels, const DevWork& w, int64_t c0,

@@ -164,8 +164,14 @@ void launch_tt_apply(const double* A, Geo g, int k, int ib, const double* Ttt,
 // trailing update).  Predicated on dec[k] (speculative launches also run while it is undecided).
 void launch_qr_panel(double* A, Geo g, int k, int ib, const int2* const* level_pairs,
                      const int* level_count, int nlevels, const DevWork& w, cudaStream_t st,
-                     bool diag_done, bool spec, const QRTsPlan* ts) {
+                     bool diag_done, bool spec, const QRTsPlan* ts, const QRDag* dag,
+                     int* progress, int epoch) {
   const uint8_t* dec = w.dec;
+  if (dag != nullptr && dag->nops > 0) {  // GEQRTs, TS chains and TT levels as one DAG launch
+    launch_qr_panel_dag(A, g, k, ib, w.Tg, w.Ttt, dag->ops, dag->nops, progress, epoch, dec, st,
+                        spec, diag_done);
+    return;
+  }
   if (ts != nullptr && ts->ngroups > 0) {
     // HQR: GEQRT of the group heads (A2: the head k is done), then every group's TSQRT chain
     const int skip = (diag_done && ts->nheads > 0) ? 1 : 0;  // heads[0] == k

@@ -39,9 +39,57 @@ __device__ __forceinline__ void cpa_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
 }
 
+// Block-granular dependencies of the panel DAG (k_qr_panel_dag below): an op publishes, after each
+// 32-column reflector block, how many blocks it has finished (release); an op waits before block b
+// until its predecessors on the same tile rows have finished block b (acquire).  NoSync: the
+// level-by-level launches, where stream order is the dependency.
+struct NoSync {
+  static constexpr bool dag = false;
+  __device__ void before(int) const {}
+  __device__ void after(int) const {}
+};
+struct DagSync {
+  static constexpr bool dag = true;
+  int* progress;  // per op of this launch: base + finished blocks
+  int me, pe, pi;  // this op, the previous op on the eliminator / head row, on the eliminated row
+  int base;        // launch epoch << 8
+  __device__ void before(int b) const {
+    if (threadIdx.x == 0) {
+      const int want = base + b + 1;
+      if (pe >= 0)
+        while (ld_acquire_i(progress + pe) < want) __nanosleep(64);
+      if (pi >= 0)
+        while (ld_acquire_i(progress + pi) < want) __nanosleep(64);
+    }
+    __syncthreads();
+  }
+  __device__ void after(int b) const {  // blocks 0..b are final (b >= 15: the op is complete)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      st_release_i(progress + me, base + b + 1);
+    }
+  }
+  __device__ static int ld_acquire_i(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+  }
+  __device__ static void st_release_i(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  }
+};
+// data written by another CTA of the same launch is read through L2 only (L1 is not coherent)
+template <bool CG>
+__device__ __forceinline__ double ldg_dag(const double* p) {
+  if constexpr (CG) return __ldcg(p);
+  else return *p;
+}
+
 // Asynchronous copy of a column block into shared memory (many bytes in flight per thread):
 // dst[j*ldd + r] = src[j*lds + r] for r < rows, j < cols_valid; zero for rows_pad > r >= rows and
 // for cols_valid <= j < cols_total.  The caller waits (cpa_wait_all) and synchronises.
+template <bool CG = false>
 __device__ __forceinline__ void cp_cols(double* dst, int ldd, const double* src, int64_t lds,
                                         int rows, int rows_pad, int cols_valid, int cols_total,
                                         int tid, int nthr) {
@@ -55,7 +103,7 @@ __device__ __forceinline__ void cp_cols(double* dst, int ldd, const double* src,
       if (j < cols_valid && r + 1 < rows) {
         cpa16(d, src + j * lds + r);
       } else if (j < cols_valid && r < rows) {
-        d[0] = src[j * lds + r];
+        d[0] = ldg_dag<CG>(src + j * lds + r);
         d[1] = 0.0;
       } else {
         d[0] = 0.0;
@@ -65,10 +113,14 @@ __device__ __forceinline__ void cp_cols(double* dst, int ldd, const double* src,
   } else {
     for (int o = tid; o < cols_total * rows_pad; o += nthr) {
       const int j = o / rows_pad, r = o - j * rows_pad;
-      if (j < cols_valid && r < rows)
-        cpa8(dst + j * ldd + r, src + j * lds + r);
-      else
+      if (j < cols_valid && r < rows) {
+        if constexpr (CG)
+          dst[j * ldd + r] = __ldcg(src + j * lds + r);
+        else
+          cpa8(dst + j * ldd + r, src + j * lds + r);
+      } else {
         dst[j * ldd + r] = 0.0;
+      }
     }
   }
 }
@@ -94,7 +146,7 @@ static size_t qd_smem(int nb) {
 // runs inside the warp (Us doubles as the warp's scratch).  W = 64: warp w owns n-frag w.
 // W = 32: warps w and w+4 split K for n-frag w&3; the upper half adds its partial through Us.
 // TT (c1 != nullptr): Wb starts from C1_b (read from global) and C1_b <- C1_b - U is written back.
-template <int W>
+template <int W, bool CG = false>
 __device__ __forceinline__ void gemm1_trmm(const double* Vs, const double* Cs, int ldc, int c_off,
                                            int RK, const double* Ts, double* Us, double* c1,
                                            int64_t ldcg, int64_t c0, int64_t ncols, int sb,
@@ -111,7 +163,8 @@ __device__ __forceinline__ void gemm1_trmm(const double* Vs, const double* Cs, i
     for (int h = 0; h < 2; ++h) {
       int l = mi * 8 + g;
       int64_t col = c0 + nf * 8 + 2 * t + h;
-      acc[mi][h] = (c1 != nullptr && khalf == 0 && l < sb && col < ncols) ? c1[col * ldcg + l] : 0.0;
+      acc[mi][h] = (c1 != nullptr && khalf == 0 && l < sb && col < ncols)
+                       ? ldg_dag<CG>(c1 + col * ldcg + l) : 0.0;
     }
   const double* cb = Cs + (nf * 8 + g) * ldc + c_off + t;
   const double* vb = Vs + g * ldc + t;
@@ -166,7 +219,7 @@ __device__ __forceinline__ void gemm1_trmm(const double* Vs, const double* Cs, i
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       int64_t col = c0 + nf * 8 + j;
-      if (col < ncols) c1[col * ldcg + lane] -= u[j];
+      if (col < ncols) c1[col * ldcg + lane] = ldg_dag<CG>(c1 + col * ldcg + lane) - u[j];
     }
   }
 }
@@ -416,20 +469,15 @@ __device__ __forceinline__ void panel_factor_nb(int nb, double* Vs, int ldc, dou
 // GEQRT of tiles (k + blockIdx.x, k) on tensor cores: per 32-column block, CTA-wide panel
 // factorisation, then the block reflector is applied to the tile's remaining columns in W-column
 // slabs with the same DMMA GEMM1+TRMM / GEMM2 as UNMQR.
-template <int W>
-__global__ void __launch_bounds__(QD_T) k_geqrt_tc(double* __restrict__ A, Geo g, int k, int ib,
-                                                   double* __restrict__ Tg,
-                                                   const uint8_t* __restrict__ dec, int i_first,
-                                                   int spec, const int* __restrict__ rows) {
-  // predicated on d_k == QR; a speculative launch (spec) also runs while d_k is undecided
-  if (dec != nullptr && (spec ? dec[k] == HLQ_DEC_LU : dec[k] != HLQ_DEC_QR)) return;
-  extern __shared__ __align__(16) double sm[];
+template <int W, class SYNC>
+__device__ void geqrt_tile(double* __restrict__ A, Geo g, int k, int ib, double* __restrict__ Tg,
+                           int i, double* sm, const SYNC& sync) {
+  constexpr bool CG = SYNC::dag;
   const int ldc = qd_ldc(g.nb);
   double* Cs = sm;
   double* Vs = Cs + qd_cs(W, g.nb);
   double* Us = Vs + 32 * ldc;
   double* Ts = Us + W * LDU;
-  const int i = rows != nullptr ? rows[blockIdx.x] : i_first + blockIdx.x;
   const int bi = g.bs(i), bk = g.cbs(k);
   double* tile = g.tile(A, i, k);
   double* T = Tg + tri_index(i, k, g.n) * (int64_t)ib * g.nb;
@@ -441,7 +489,7 @@ __global__ void __launch_bounds__(QD_T) k_geqrt_tc(double* __restrict__ A, Geo g
     if (R <= 0) break;
     const int RK = (R + 31) / 32 * 32;
     __syncthreads();
-    cp_cols(Vs, ldc, tile + (int64_t)i0 * g.lda + i0, g.lda, R, RK, sb, 32, tid, QD_T);
+    cp_cols<CG>(Vs, ldc, tile + (int64_t)i0 * g.lda + i0, g.lda, R, RK, sb, 32, tid, QD_T);
     for (int o = tid; o < 32 * 33; o += QD_T) Ts[o] = 0.0;
     cpa_wait_all();
     __syncthreads();
@@ -475,14 +523,30 @@ __global__ void __launch_bounds__(QD_T) k_geqrt_tc(double* __restrict__ A, Geo g
         tile[(int64_t)(c0 + j) * g.lda + i0 + r] = Cs[j * ldc + r];
       }
     }
+    // block-row i0 / ib is final: its reflectors' trailing update is written
+    sync.after(i0 / ib);
   }
+  sync.after(15);  // every block (also after an early exit of a ragged tile)
+}
+
+template <int W>
+__global__ void __launch_bounds__(QD_T) k_geqrt_tc(double* __restrict__ A, Geo g, int k, int ib,
+                                                   double* __restrict__ Tg,
+                                                   const uint8_t* __restrict__ dec, int i_first,
+                                                   int spec, const int* __restrict__ rows) {
+  // predicated on d_k == QR; a speculative launch (spec) also runs while d_k is undecided
+  if (dec != nullptr && (spec ? dec[k] == HLQ_DEC_LU : dec[k] != HLQ_DEC_QR)) return;
+  extern __shared__ __align__(16) double sm[];
+  const int i = rows != nullptr ? rows[blockIdx.x] : i_first + blockIdx.x;
+  geqrt_tile<W>(A, g, k, ib, Tg, i, sm, NoSync{});
 }
 
 // TTQRT (TS = false) / TSQRT (TS = true) of the pair (e, i): [R_e; A_i] -> R_e, the
 // reflectors V in tile (i,k) (TT: its upper triangle; TS: the whole square tile), T
-template <int W, bool TS>
+template <int W, bool TS, class SYNC = NoSync>
 __device__ void qrt_pair(double* __restrict__ A, Geo g, int k, int ib, double* __restrict__ Ttt,
-                         int e, int i, double* sm) {
+                         int e, int i, double* sm, const SYNC& sync = SYNC{}) {
+  constexpr bool CG = SYNC::dag;
   const int ldc = qd_ldc(g.nb);
   double* Cs = sm;
   double* Vs = Cs + qd_cs(W, g.nb);
@@ -499,15 +563,20 @@ __device__ void qrt_pair(double* __restrict__ A, Geo g, int k, int ib, double* _
     const int sb = min(ib, bk - i0);
     const int R2 = TS ? bi : min(bi, i0 + sb);
     const int RK = (R2 + 31) / 32 * 32;
+    sync.before(i0 / ib);  // the predecessors' block rows 0 .. i0 / ib are final
     __syncthreads();
-    cp_cols(Vs, ldc, Ri + (int64_t)i0 * g.lda, g.lda, R2, RK, sb, 32, tid, QD_T);
+    cp_cols<CG>(Vs, ldc, Ri + (int64_t)i0 * g.lda, g.lda, R2, RK, sb, 32, tid, QD_T);
     for (int o = tid; o < 32 * 33; o += QD_T) {
       Ts[o] = 0.0;
       int l = o / 33, q = o - l * 33;
-      if (l < sb && q <= l)  // R_e's block triangle, in flight with V's block
-        cpa8(Rs + o, Re + (int64_t)(i0 + l) * g.lda + i0 + q);
-      else
+      if (l < sb && q <= l) {  // R_e's block triangle, in flight with V's block
+        if constexpr (CG)
+          Rs[o] = __ldcg(Re + (int64_t)(i0 + l) * g.lda + i0 + q);
+        else
+          cpa8(Rs + o, Re + (int64_t)(i0 + l) * g.lda + i0 + q);
+      } else {
         Rs[o] = 0.0;
+      }
     }
     cpa_wait_all();
     __syncthreads();
@@ -533,11 +602,11 @@ __device__ void qrt_pair(double* __restrict__ A, Geo g, int k, int ib, double* _
     for (int c0 = i0 + sb; c0 < bk; c0 += W) {
       const int cv = min(W, bk - c0);
       __syncthreads();
-      cp_cols(Cs, ldc, Ri + (int64_t)c0 * g.lda, g.lda, R2, RK, cv, W, tid, QD_T);
+      cp_cols<CG>(Cs, ldc, Ri + (int64_t)c0 * g.lda, g.lda, R2, RK, cv, W, tid, QD_T);
       cpa_wait_all();
       __syncthreads();
       // Wb = R_e(block rows, slab) + V2^T R_i(slab); U = T^T Wb; R_e(block rows) -= U
-      gemm1_trmm<W>(Vs, Cs, ldc, 0, RK, Ts, Us, Re + i0, g.lda, c0, bk, sb, warp, lane);
+      gemm1_trmm<W, CG>(Vs, Cs, ldc, 0, RK, Ts, Us, Re + i0, g.lda, c0, bk, sb, warp, lane);
       __syncthreads();
       gemm2<W>(Vs, Us, Cs, ldc, 0, RK, warp, lane);
       __syncthreads();
@@ -547,7 +616,9 @@ __device__ void qrt_pair(double* __restrict__ A, Geo g, int k, int ib, double* _
       }
     }
     __syncthreads();
+    sync.after(i0 / ib);  // the eliminator's block row i0 / ib is final
   }
+  sync.after(15);
 }
 
 // TTQRT on pairs (e, i) = pairs[blockIdx.x]: [R_e; R_i] -> R_e, V (upper triangle of tile (i,k)), T
@@ -578,6 +649,55 @@ __global__ void __launch_bounds__(QD_T) k_tsqrt_tc(double* __restrict__ A, Geo g
     qrt_pair<W, true>(A, g, k, ib, Tts, pr.x, pr.y, sm);
     __syncthreads();
   }
+}
+
+// The whole QR panel of a step as ONE launch (GEQRT of the listed tiles, every TS chain pair, every
+// TT level pair): one CTA per op (ops = 5 ints each: kind 0 GEQRT / 1 TSQRT / 2 TTQRT, eliminator or
+// head row e, row i, the previous op on row e and on row i, -1 = none), listed in an order where
+// every predecessor precedes its successors.  An op starts block b once its predecessors have
+// finished block b (DagSync), so a TS chain or the next TT level trails its predecessor by one
+// 32-column block instead of one whole kernel: the panel's critical path becomes
+// (blocks + chain length + levels) block times.  Waiting CTAs only wait for CTAs with smaller
+// indices, which are dispatched first, so the spin waits cannot deadlock.
+template <int W>
+__global__ void __launch_bounds__(QD_T) k_qr_panel_dag(double* __restrict__ A, Geo g, int k, int ib,
+                                                       double* __restrict__ Tg,
+                                                       double* __restrict__ Ttt,
+                                                       const int* __restrict__ ops,
+                                                       int* __restrict__ progress, int base,
+                                                       const uint8_t* __restrict__ dec, int spec,
+                                                       int skip_first) {
+  if (dec != nullptr && (spec ? dec[k] == HLQ_DEC_LU : dec[k] != HLQ_DEC_QR)) return;
+  extern __shared__ __align__(16) double sm[];
+  const int* op = ops + 5 * blockIdx.x;
+  const DagSync sync{progress, (int)blockIdx.x, op[3], op[4], base};
+  if (blockIdx.x == 0 && skip_first) {  // (A2) the caller already factored tile k
+    sync.after(15);
+    return;
+  }
+  if (op[0] == 0)
+    geqrt_tile<W>(A, g, k, ib, Tg, op[2], sm, sync);
+  else if (op[0] == 1)
+    qrt_pair<W, true>(A, g, k, ib, Ttt, op[1], op[2], sm, sync);
+  else
+    qrt_pair<W, false>(A, g, k, ib, Ttt, op[1], op[2], sm, sync);
+}
+
+void launch_qr_panel_dag(double* A, Geo g, int k, int ib, double* Tg, double* Ttt, const int* ops,
+                         int nops, int* progress, int epoch, const uint8_t* dec, cudaStream_t st,
+                         bool spec, bool skip_first) {
+  if (nops <= 0) return;
+  auto go = [&](auto W_) {
+    constexpr int W = decltype(W_)::value;
+    static unsigned long long attr = 0;
+    if (first_on_device(attr)) smem_optin(k_qr_panel_dag<W>);
+    ::hlq::g_launches++;
+    k_qr_panel_dag<W><<<nops, QD_T, qd_smem<W>(g.nb), st>>>(A, g, k, ib, Tg, Ttt, ops, progress,
+                                                           epoch << 8, dec, spec ? 1 : 0,
+                                                           skip_first ? 1 : 0);
+  };
+  if (qd_smem<64>(g.nb) <= 227 * 1024) go(std::integral_constant<int, 64>());
+  else go(std::integral_constant<int, 32>());
 }
 
 template <int W>

@@ -4,8 +4,10 @@ The speculative QR panel (HLQ_SPEC_QR) only moves the QR branch's panel work to 
 copy of the panel (its kernels run while d_k is undecided and exit once it is LU), the DGEMM warp grid
 (HLQ_DGEMM_TILE) only changes which CTA computes which output tile, and the TMA-fed Schur update
 (default) and the cp.async kernel (HLQ_DGEMM_TMA=0) accumulate every element's K products in the
-same order: all must give bit-identical factors, decisions and QR-step T factors -- under A1 and A2,
-Max and MUMPS, one and two QR-tree domains.  The environment is read once per process, so each variant
+same order; the QR panel as one dependency-DAG launch (default) or level by level (HLQ_QR_DAG=0)
+runs the same kernels' arithmetic, and HLQ_QR_REORD=1 only interleaves the QR update's DMMAs
+across accumulators (each accumulator keeps its order): all must give bit-identical factors,
+decisions and QR-step T factors -- under A1 and A2, Max and MUMPS, one and two QR-tree domains.  The environment is read once per process, so each variant
 runs in its own interpreter."""
 import os
 import subprocess
@@ -31,7 +33,9 @@ cases = (("max1", A, H.CRIT_MAX, 1.0, {{}}), ("max3e4", A, H.CRIT_MAX, 3e4, {{}}
          ("lu", A, H.CRIT_MAX, float("inf"), {{}}),
          ("a2_mix", U, H.CRIT_MAX, 1.2e4, dict(lu_variant=H.LU_A2)),
          ("mumps", A, H.CRIT_MUMPS, 2.1, {{}}),
-         ("dom2", U, H.CRIT_MAX, 1.2e4, dict(tree_domains=2)))
+         ("dom2", U, H.CRIT_MAX, 1.2e4, dict(tree_domains=2)),
+         ("hqr4", U, H.CRIT_MAX, 1.2e4, dict(tree=H.TREE_HQR, ts_group=4)),
+         ("hqr3_qr", A, H.CRIT_MAX, 0.0, dict(tree=H.TREE_HQR, ts_group=3, tree_domains=2)))
 for name, M, crit, alpha, kw in cases:
     dA = H.to_colmajor(M)
     f = H.hlq_factor_ex(dA, N, nb, crit, alpha, **kw)
@@ -57,7 +61,8 @@ def _run(env_extra, path):
 
 
 @pytest.mark.parametrize("env", [{"HLQ_SPEC_QR": "0"}, {"HLQ_DGEMM_TILE": "4x2"}, {"HLQ_DGEMM_TMA": "0"},
-                                 {"HLQ_TMA_CONS": "4"}])
+                                 {"HLQ_TMA_CONS": "4"}, {"HLQ_QR_DAG": "0"},
+                                 {"HLQ_QR_REORD": "1"}])
 def test_variant_is_bit_identical(tmp_path, env):
     base = _run({}, str(tmp_path / "base.npz"))
     var = _run(env, str(tmp_path / "var.npz"))
