@@ -169,8 +169,10 @@ int hlq_get_growth(hlq_factors_t f, double* growth);
 int hlq_get_pivots(hlq_factors_t f, int32_t* ipiv);         /* n*nb entries: step k at k*nb, 0-based
                                                                row within the tile (LAPACK sequential
                                                                swaps); only LU steps are meaningful */
-/* Householder T factors of tile (i,k), i >= k, kind 0 = GEQRT, 1 = TTQRT: ib x nb, column-major
- * (ld = ib) into host buffer T.  Errors: -2/-3 bad indices. */
+/* Householder T factors of tile (i,k), i >= k, kind 0 = GEQRT, 1 = the elimination of tile i
+ * (TTQRT, or TSQRT on the HQR tree): ib x nb, column-major (ld = ib) into host buffer T; zeros when
+ * tile i had no such factorization at step k (an LU step, a non-head row's GEQRT, tile k's own
+ * elimination).  Errors: -2/-3 bad indices. */
 int hlq_get_T(hlq_factors_t f, int32_t i, int32_t k, int32_t kind, double* T);
 void hlq_free(hlq_factors_t f);
 const char* hlq_status_string(int code);

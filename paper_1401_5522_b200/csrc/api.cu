@@ -101,9 +101,10 @@ void cache_put(int dev, int slot, void* p, size_t bytes) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 constexpr int kSolveG = 4;  // tiles per work unit of the persistent solve
+constexpr size_t kFlagBytes = 128;  // one solve flag per cache line (solve.cu kFlagStride)
 size_t solve_ws_bytes(int n, int nb, int cmax, size_t units) {
-  return align_up(sizeof(int2) * units, 256) + align_up(sizeof(int) * n, 256) +
-         align_up(sizeof(int) * (size_t)n * cmax, 256) + sizeof(double) * (size_t)n * cmax * nb +
+  return align_up(sizeof(int2) * units, 256) + align_up(kFlagBytes * n, 256) +
+         align_up(kFlagBytes * (size_t)n * cmax, 256) + sizeof(double) * (size_t)n * cmax * nb +
          256;
 }
 
@@ -522,6 +523,10 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   cudaMemsetAsync(w.dom_counter, 0, sizeof(unsigned int), st);
   cudaMemsetAsync(w.gstep, 0, sizeof(double) * (n + 1), st);
   cudaMemsetAsync(w.ipiv, 0, sizeof(int) * (size_t)n * nb, st);
+  // T factors of tiles without that factorization in a step (HQR: no GEQRT of a non-head row; no
+  // TT/TS T for tile k itself; LU steps) read back as zeros, not as a previous call's workspace
+  cudaMemsetAsync(w.Tg, 0, sizeof(double) * ntri * ib * nb, st);
+  cudaMemsetAsync(w.Ttt, 0, sizeof(double) * ntri * ib * nb, st);
   // Two streams: st (the caller's) runs the trailing updates, sp (high priority) runs the panel
   // stage of step k+1 as soon as step k has updated column block k+1 (lookahead depth 1).
   cudaStream_t sp = panel_stream(0), sq = panel_stream(1);
@@ -832,8 +837,8 @@ int hlq_solve(hlq_factors_t f, const double* b, double* x) {
   const size_t used = f->solve_used > f->solve_cap ? f->solve_used : f->solve_cap;
   const int2* units = (const int2*)sw;
   int* xflag = (int*)(sw + align_up(sizeof(int2) * used, 256));
-  int* pflag = (int*)((char*)xflag + align_up(sizeof(int) * n, 256));
-  double* part = (double*)((char*)pflag + align_up(sizeof(int) * (size_t)n * cmax, 256));
+  int* pflag = (int*)((char*)xflag + align_up(kFlagBytes * n, 256));
+  double* part = (double*)((char*)pflag + align_up(kFlagBytes * (size_t)n * cmax, 256));
   unsigned* ticket = (unsigned*)(part + (size_t)n * cmax * g.nb);
   size_t run = 0;
   for (int k = 0; k < n; ++k) {

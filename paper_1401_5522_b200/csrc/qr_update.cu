@@ -92,7 +92,7 @@ __device__ __forceinline__ double2 lds2(const double* p) {
 
 // MODE 0: UNMQR of tile row i (GEQRT reflectors, unit lower); 1: TTMQR of the pair (e, i) (TT
 // reflectors, upper triangular); 2: TSMQR of the pair (e, i) (TS reflectors, square)
-template <int NB, int MODE, int RQ, int NCG, bool V16, bool REORD = false>
+template <int NB, int MODE, int RQ, int NCG, bool V16>
 __device__ __forceinline__ void qr_update3_body(const double* __restrict__ A, Geo g, int k,
                                                 const double* __restrict__ Tbase, int e, int i,
                                                 double* __restrict__ base, int64_t ldcg,
@@ -302,26 +302,6 @@ __device__ __forceinline__ void qr_update3_body(const double* __restrict__ A, Ge
             wT[m][nl][1] += v.y;
           }
       }
-      if constexpr (REORD) {
-        // consecutive DMMAs into different accumulators (an accumulator every 8 issues)
-#pragma unroll
-        for (int q = 0; q < QPC; ++q) {
-          const int rb = rh + RQ * q;
-          double2 bv[4];
-#pragma unroll
-          for (int nl = 0; nl < 4; ++nl) bv[nl] = lds2(V + (8 * nl + gq) * LD3 + 8 * rb + 2 * tq);
-#pragma unroll
-          for (int nl = 0; nl < 4; ++nl)
-#pragma unroll
-            for (int m = 0; m < 2; ++m)
-              dmma_(wT[m][nl][0], wT[m][nl][1], cT[m][QPC * ch + q][0], bv[nl].x);
-#pragma unroll
-          for (int nl = 0; nl < 4; ++nl)
-#pragma unroll
-            for (int m = 0; m < 2; ++m)
-              dmma_(wT[m][nl][0], wT[m][nl][1], cT[m][QPC * ch + q][1], bv[nl].y);
-        }
-      } else {
 #pragma unroll
       for (int q = 0; q < QPC; ++q) {
         const int rb = rh + RQ * q;  // 8-row block within the chunk
@@ -333,9 +313,7 @@ __device__ __forceinline__ void qr_update3_body(const double* __restrict__ A, Ge
             dmma_(wT[m][nl][0], wT[m][nl][1], cT[m][QPC * ch + q][0], bv.x);
             dmma_(wT[m][nl][0], wT[m][nl][1], cT[m][QPC * ch + q][1], bv.y);
           }
-        }
-      }
-      }
+        }      }
     }
     // ---------------- group reduction: W = P_0 + ... + P_{RQ-1} in the same order on every warp
     {
@@ -418,29 +396,6 @@ __device__ __forceinline__ void qr_update3_body(const double* __restrict__ A, Ge
         fix_diag(const_cast<double*>(V), 1, LD3B);
         __syncthreads();
       }
-      if constexpr (REORD) {
-        // per (nl, half) one DMMA into each of the QPC x 2 accumulators
-#pragma unroll
-        for (int nl = 0; nl < 4; ++nl) {
-          double bx[QPC], by[QPC];
-#pragma unroll
-          for (int q = 0; q < QPC; ++q) {
-            const int rb = rh + RQ * q;
-            bx[q] = V[(8 * nl + 2 * tq) * LD3B + 8 * rb + gq];
-            by[q] = V[(8 * nl + 2 * tq + 1) * LD3B + 8 * rb + gq];
-          }
-#pragma unroll
-          for (int q = 0; q < QPC; ++q)
-#pragma unroll
-            for (int m = 0; m < 2; ++m)
-              dmma_(cT[m][QPC * ch + q][0], cT[m][QPC * ch + q][1], uT[m][nl][0], bx[q]);
-#pragma unroll
-          for (int q = 0; q < QPC; ++q)
-#pragma unroll
-            for (int m = 0; m < 2; ++m)
-              dmma_(cT[m][QPC * ch + q][0], cT[m][QPC * ch + q][1], uT[m][nl][1], by[q]);
-        }
-      } else {
 #pragma unroll
       for (int q = 0; q < QPC; ++q) {
         const int rb = rh + RQ * q;
@@ -453,9 +408,7 @@ __device__ __forceinline__ void qr_update3_body(const double* __restrict__ A, Ge
             dmma_(cT[m][QPC * ch + q][0], cT[m][QPC * ch + q][1], uT[m][nl][0], bx);
             dmma_(cT[m][QPC * ch + q][0], cT[m][QPC * ch + q][1], uT[m][nl][1], by);
           }
-        }
-      }
-      }
+        }      }
     }
   }
   wait_<0>();
@@ -506,31 +459,31 @@ __device__ __forceinline__ void qr_update3_body(const double* __restrict__ A, Ge
 }
 
 // UNMQR of tile rows i = rows[blockIdx.y] (rows == nullptr: k + blockIdx.y)
-template <int NB, int RQ, int NCG, bool V16, bool REORD = false>
+template <int NB, int RQ, int NCG, bool V16>
 __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ * NCG) : 1)
     k_unmqr3(const double* __restrict__ A, Geo g, int k, const double* __restrict__ Tbase,
              const int* __restrict__ rows, double* __restrict__ base, int64_t ldcg, int64_t ncols,
              const uint8_t* __restrict__ dec) {
   if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
   const int i = rows != nullptr ? rows[blockIdx.y] : k + (int)blockIdx.y;
-  qr_update3_body<NB, 0, RQ, NCG, V16, REORD>(A, g, k, Tbase, 0, i, base, ldcg, ncols, nullptr);
+  qr_update3_body<NB, 0, RQ, NCG, V16>(A, g, k, Tbase, 0, i, base, ldcg, ncols, nullptr);
 }
 
 // TTMQR of the pairs of one level (pair = blockIdx.y)
-template <int NB, int RQ, int NCG, bool V16, bool REORD = false>
+template <int NB, int RQ, int NCG, bool V16>
 __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ * NCG) : 1)
     k_ttmqr3(const double* __restrict__ A, Geo g, int k, const double* __restrict__ Tbase,
              const int2* __restrict__ pairs, double* __restrict__ base, int64_t ldcg,
              int64_t ncols, const uint8_t* __restrict__ dec, double* __restrict__ gmax) {
   if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
   const int2 pr = pairs[blockIdx.y];
-  qr_update3_body<NB, 1, RQ, NCG, V16, REORD>(A, g, k, Tbase, pr.x, pr.y, base, ldcg, ncols,
+  qr_update3_body<NB, 1, RQ, NCG, V16>(A, g, k, Tbase, pr.x, pr.y, base, ldcg, ncols,
                                               gmax);
 }
 
 // TSMQR chains of the HQR tree (group = blockIdx.y): the group's pairs in order, each applying
 // Q_i^T to [C_head; C_i] (the head's rows read-modify-written per reflector block, C_i in registers)
-template <int NB, int RQ, int NCG, bool V16, bool REORD = false>
+template <int NB, int RQ, int NCG, bool V16>
 __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ * NCG) : 1)
     k_tsmqr3(const double* __restrict__ A, Geo g, int k, const double* __restrict__ Tbase,
              const int2* __restrict__ pairs, const int* __restrict__ off,
@@ -539,7 +492,7 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
   if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
   for (int p = off[blockIdx.y]; p < off[blockIdx.y + 1]; ++p) {
     const int2 pr = pairs[p];
-    qr_update3_body<NB, 2, RQ, NCG, V16, REORD>(A, g, k, Tbase, pr.x, pr.y, base, ldcg, ncols,
+    qr_update3_body<NB, 2, RQ, NCG, V16>(A, g, k, Tbase, pr.x, pr.y, base, ldcg, ncols,
                                                 gmax);
     __syncthreads();  // the head's rows and the ring are reused by the next pair
   }
@@ -551,28 +504,28 @@ static size_t upd3_smem(int warps, int W) {
          sizeof(int) * (size_t)(2 * 10 * 10 + 2);
 }
 
-template <int NB, int RQ, int NCG, bool V16, bool REORD = false>
+template <int NB, int RQ, int NCG, bool V16>
 static void launch3(const double* A, Geo g, int k, const double* T, const int2* pairs, int npairs,
                     int mode, const int* list, double* base, int64_t ldc, int64_t ncols,
                     const uint8_t* dec, cudaStream_t st, double* gmax) {
   static unsigned long long attr = 0;
   if (first_on_device(attr)) {
-    smem_optin(k_unmqr3<NB, RQ, NCG, V16, REORD>);
-    smem_optin(k_ttmqr3<NB, RQ, NCG, V16, REORD>);
-    smem_optin(k_tsmqr3<NB, RQ, NCG, V16, REORD>);
+    smem_optin(k_unmqr3<NB, RQ, NCG, V16>);
+    smem_optin(k_ttmqr3<NB, RQ, NCG, V16>);
+    smem_optin(k_tsmqr3<NB, RQ, NCG, V16>);
   }
   const unsigned slabs = (unsigned)((ncols + 16 * NCG - 1) / (16 * NCG));
   const size_t smem = upd3_smem(RQ * NCG, 16 * NCG);
   if (npairs <= 0) return;
   ::hlq::g_launches++;
   if (mode == 0)  // npairs = number of tile rows (list: the rows, or nullptr for k..)
-    k_unmqr3<NB, RQ, NCG, V16, REORD><<<dim3(slabs, npairs), 32 * RQ * NCG, smem, st>>>(
+    k_unmqr3<NB, RQ, NCG, V16><<<dim3(slabs, npairs), 32 * RQ * NCG, smem, st>>>(
         A, g, k, T, list, base, ldc, ncols, dec);
   else if (mode == 1)
-    k_ttmqr3<NB, RQ, NCG, V16, REORD><<<dim3(slabs, npairs), 32 * RQ * NCG, smem, st>>>(
+    k_ttmqr3<NB, RQ, NCG, V16><<<dim3(slabs, npairs), 32 * RQ * NCG, smem, st>>>(
         A, g, k, T, pairs, base, ldc, ncols, dec, gmax);
   else  // npairs = number of groups, list = their pair offsets
-    k_tsmqr3<NB, RQ, NCG, V16, REORD><<<dim3(slabs, npairs), 32 * RQ * NCG, smem, st>>>(
+    k_tsmqr3<NB, RQ, NCG, V16><<<dim3(slabs, npairs), 32 * RQ * NCG, smem, st>>>(
         A, g, k, T, pairs, list, base, ldc, ncols, dec, gmax);
 }
 
@@ -588,16 +541,11 @@ bool launch_qr_update3(const double* A, Geo g, int k, const double* T, const int
   // 16-byte V copies need an even leading dimension, a 16-byte aligned matrix and even tile heights
   const bool v16 = ((g.lda & 1) == 0) && ((((uintptr_t)A) & 15) == 0) && ((g.N & 1) == 0) &&
                    ((g.nb & 1) == 0) && ((ldc & 1) == 0) && ((((uintptr_t)base) & 15) == 0);
-  static int reord = -1;  // HLQ_QR_REORD=1: the accumulator-interleaved DMMA order (NB 256, 320)
-  if (reord < 0) reord = getenv("HLQ_QR_REORD") ? atoi(getenv("HLQ_QR_REORD")) : 0;
 #define HLQ_L3(NBV)                                                                           \
   case NBV:                                                                                   \
     if (!v16)                                                                                 \
       launch3<NBV, 2, 2, false>(A, g, k, T, pairs, npairs, mode, list, base, ldc, ncols, dec, st, \
                                 gmax);                                                        \
-    else if (reord && NBV >= 256)                                                             \
-      launch3<NBV, 2, 2, true, NBV >= 256>(A, g, k, T, pairs, npairs, mode, list, base, ldc,    \
-                                           ncols, dec, st, gmax);                             \
     else                                                                                      \
       launch3<NBV, 2, 2, true>(A, g, k, T, pairs, npairs, mode, list, base, ldc, ncols, dec, st,  \
                                gmax);                                                         \

@@ -231,8 +231,15 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// each flag on its own 128-byte line (kFlagStride ints) so the pollers of different flags do not
+// share an L2 line; the poll backs off (up to 256 ns) to keep a thousand spinning CTAs off L2
+constexpr int kFlagStride = 32;
 __device__ __forceinline__ void wait_flag(const int* p, int want) {
-  while (ld_acquire(p) != want) __nanosleep(32);
+  unsigned ns = 32;
+  while (ld_acquire(p) != want) {
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+  }
 }
 
 // acc[s][e] += sum over columns c (c = h, h+2, ...) of T(row 2q+256s+e, c) * xs[c]; with V2 (even
@@ -401,7 +408,7 @@ __global__ void __launch_bounds__(PS_T) k_solve_rows(const double* __restrict__ 
   for (int t = 0; t < ntiles; ++t) {
     const int j = FWD ? jfirst + t : jfirst - t;
     const int bj = g.bs(j);
-    if (tid == 0) wait_flag(xflag + j, 1);
+    if (tid == 0) wait_flag(xflag + (int64_t)j * kFlagStride, 1);
     __syncthreads();
     for (int cc = tid; cc < bj; cc += PS_T) xs[cc] = __ldcg(x + g.r0(j) + cc);
     __syncthreads();
@@ -425,12 +432,12 @@ __global__ void __launch_bounds__(PS_T) k_solve_rows(const double* __restrict__ 
     for (int r = tid; r < bi; r += PS_T) __stcg(my_part + r, red[0][r] + red[1][r]);
     __threadfence();
     __syncthreads();
-    if (tid == 0) st_release(pflag + (int64_t)i * cmax + c, 1);
+    if (tid == 0) st_release(pflag + ((int64_t)i * cmax + c) * kFlagStride, 1);
     return;
   }
   // finisher: r_i = x_i - (sum of the chunk partials in chunk order + own)
   if (tid == 0)
-    for (int cc = 0; cc < c; ++cc) wait_flag(pflag + (int64_t)i * cmax + cc, 1);
+    for (int cc = 0; cc < c; ++cc) wait_flag(pflag + ((int64_t)i * cmax + cc) * kFlagStride, 1);
   __syncthreads();
   double* xi = x + g.r0(i);
   for (int r = tid; r < bi; r += PS_T) {
@@ -458,11 +465,12 @@ __global__ void __launch_bounds__(PS_T) k_solve_rows(const double* __restrict__ 
   for (int r = tid; r < bi; r += PS_T) __stcg(xi + r, ys[r]);
   __threadfence();
   __syncthreads();
-  if (tid == 0) st_release(xflag + i, 1);
+  if (tid == 0) st_release(xflag + (int64_t)i * kFlagStride, 1);
 }
 
 // Host side: unit table (ticket order) for one pass; the device buffers come from the handle's
-// solve workspace (xflag n ints, pflag n*cmax ints, part n*cmax*nb doubles, ticket, units).
+// solve workspace (xflag n flags, pflag n*cmax flags -- 128 bytes each --, part n*cmax*nb doubles,
+// ticket, units).
 int solve_rows_cmax(int n, int G) { return std::max(1, (n + G - 1) / G); }
 
 size_t build_solve_units(bool fwd, int n, int ka, int kb, int G, int2* out) {
@@ -488,8 +496,8 @@ void launch_solve_rows(bool fwd, const double* A, Geo g, int ka, int kb, int G, 
   if (nunits == 0) return;
   const int cmax = solve_rows_cmax(g.n, G);
   cudaMemsetAsync(ticket, 0, sizeof(unsigned), st);
-  cudaMemsetAsync(xflag, 0, sizeof(int) * (size_t)g.n, st);
-  cudaMemsetAsync(pflag, 0, sizeof(int) * (size_t)g.n * cmax, st);
+  cudaMemsetAsync(xflag, 0, sizeof(int) * kFlagStride * (size_t)g.n, st);
+  cudaMemsetAsync(pflag, 0, sizeof(int) * kFlagStride * (size_t)g.n * cmax, st);
   ::hlq::g_launches++;
   if (fwd)
     k_solve_rows<true><<<(unsigned)nunits, PS_T, 0, st>>>(A, g, ka, kb, G, cmax, units, perm_all,

@@ -5,8 +5,7 @@ copy of the panel (its kernels run while d_k is undecided and exit once it is LU
 (HLQ_DGEMM_TILE) only changes which CTA computes which output tile, and the TMA-fed Schur update
 (default) and the cp.async kernel (HLQ_DGEMM_TMA=0) accumulate every element's K products in the
 same order; the QR panel as one dependency-DAG launch (default) or level by level (HLQ_QR_DAG=0)
-runs the same kernels' arithmetic, and HLQ_QR_REORD=1 only interleaves the QR update's DMMAs
-across accumulators (each accumulator keeps its order): all must give bit-identical factors,
+runs the same kernels' arithmetic: all must give bit-identical factors,
 decisions and QR-step T factors -- under A1 and A2, Max and MUMPS, one and two QR-tree domains.  The environment is read once per process, so each variant
 runs in its own interpreter."""
 import os
@@ -61,8 +60,7 @@ def _run(env_extra, path):
 
 
 @pytest.mark.parametrize("env", [{"HLQ_SPEC_QR": "0"}, {"HLQ_DGEMM_TILE": "4x2"}, {"HLQ_DGEMM_TMA": "0"},
-                                 {"HLQ_TMA_CONS": "4"}, {"HLQ_QR_DAG": "0"},
-                                 {"HLQ_QR_REORD": "1"}])
+                                 {"HLQ_TMA_CONS": "4"}, {"HLQ_QR_DAG": "0"}])
 def test_variant_is_bit_identical(tmp_path, env):
     base = _run({}, str(tmp_path / "base.npz"))
     var = _run(env, str(tmp_path / "var.npz"))
