@@ -833,6 +833,56 @@ int hlq_solve(hlq_factors_t f, const double* b, double* x) {
                                        cudaMemcpyHostToDevice, st))))
       return rc;
   }
+  if (!f->qsolve_built) {
+    // runs of consecutive QR steps: one DAG of Q^T applies each (qr.cu k_qr_solve_dag); an op
+    // waits for the previous op on each of its rows, across the run's steps
+    f->qsolve_built = true;
+    static int qenv = -1;
+    if (qenv < 0) qenv = getenv("HLQ_QR_SOLVE_DAG") ? atoi(getenv("HLQ_QR_SOLVE_DAG")) : 1;
+    std::vector<int> ops;
+    size_t maxops = 0;
+    for (int k = 0; k < n && qenv != 0;) {
+      if (f->dec[k] != HLQ_DEC_QR) { ++k; continue; }
+      int kb = k;
+      while (kb < n && f->dec[kb] == HLQ_DEC_QR) ++kb;
+      const size_t off = ops.size() / 6;
+      std::vector<int> last(n, -1);
+      auto add = [&](int kind, int e, int i, int step) {
+        const int id = (int)(ops.size() / 6) - (int)off;
+        ops.insert(ops.end(), {kind, e, i, kind == 0 ? -1 : last[e], last[i], step});
+        last[i] = id;
+        if (kind != 0) last[e] = id;
+      };
+      for (int s = k; s < kb; ++s) {
+        StepPlanHost p;
+        plan_step(s, n, f->D, f->ts_group, p);
+        if (f->ts_group >= 1 && p.ts_off.size() > 1) {
+          for (int h : p.heads) add(0, h, h, s);
+          for (const int2& pr : p.ts_pairs) add(1, pr.x, pr.y, s);
+        } else {
+          for (int i = s; i < n; ++i) add(0, i, i, s);
+        }
+        for (const auto& lv : p.levels)
+          for (const int2& pr : lv) add(2, pr.x, pr.y, s);
+      }
+      const size_t cnt = ops.size() / 6 - off;
+      f->qsolve_runs.push_back({k, kb, (int)off, (int)cnt});
+      maxops = std::max(maxops, cnt);
+      k = kb;
+    }
+    if (!ops.empty()) {
+      const size_t ob = align_up(sizeof(int) * ops.size(), 256);
+      if ((rc = cuda_err(cudaMalloc(&f->qsolve_block, ob + sizeof(int) * 32 * maxops)))) {
+        f->qsolve_block = nullptr;
+        f->qsolve_runs.clear();
+        return rc;
+      }
+      f->qsolve_done = (int*)((char*)f->qsolve_block + ob);
+      if ((rc = cuda_err(cudaMemcpyAsync(f->qsolve_block, ops.data(), sizeof(int) * ops.size(),
+                                         cudaMemcpyHostToDevice, st))))
+        return rc;
+    }
+  }
   char* sw = (char*)f->solve_ws;
   const size_t used = f->solve_used > f->solve_cap ? f->solve_used : f->solve_cap;
   const int2* units = (const int2*)sw;
@@ -840,8 +890,16 @@ int hlq_solve(hlq_factors_t f, const double* b, double* x) {
   int* pflag = (int*)((char*)xflag + align_up(kFlagBytes * n, 256));
   double* part = (double*)((char*)pflag + align_up(kFlagBytes * (size_t)n * cmax, 256));
   unsigned* ticket = (unsigned*)(part + (size_t)n * cmax * g.nb);
-  size_t run = 0;
+  size_t run = 0, qrun = 0;
   for (int k = 0; k < n; ++k) {
+    if (qrun < f->qsolve_runs.size() && f->qsolve_runs[qrun][0] == k) {
+      const auto& r = f->qsolve_runs[qrun++];
+      launch_qr_solve_dag(f->A, g, f->ib, f->w.Tg, f->w.Ttt,
+                          (const int*)f->qsolve_block + (size_t)6 * r[2], r[3], f->qsolve_done, x,
+                          st);
+      k = r[1] - 1;
+      continue;
+    }
     if (run < f->solve_runs.size() && f->solve_runs[run].first == k) {
       const int kb = f->solve_runs[run].second;
       launch_solve_rows(true, f->A, g, k, kb, G, units + f->solve_unit_off[run],
@@ -1004,6 +1062,10 @@ void hlq_free(hlq_factors_t f) {
     cache_put(f->dev, 0, f->ws_block, f->ws_bytes);
   }
   if (f->tma_maps) free_tma_maps(f->tma_maps);
+  if (f->qsolve_block) {
+    cudaStreamSynchronize(f->st);
+    cudaFree(f->qsolve_block);
+  }
   if (f->solve_ws_own) {
     cudaStreamSynchronize(f->st);
     cudaFree(f->solve_ws_own);

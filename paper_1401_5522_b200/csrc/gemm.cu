@@ -19,8 +19,6 @@
 
 namespace hlq {
 
-// WN = warps along N: 2 -> CTA tile 128 x 64, 256 threads, 2 CTAs/SM (default);
-//                     4 -> CTA tile 128 x 128, 512 threads, 1 CTA/SM (HLQ_DGEMM_WN=4)
 constexpr int BK = 16, STAGES = 3;
 constexpr int LDB_S = BK + 4;
 // warp grid WM x WN of 32 x 32 warp tiles: CTA tile (32 WM) x (32 WN)
@@ -32,8 +30,6 @@ template <int WN> __host__ __device__ constexpr int gemm_b_stage() { return gemm
 template <int WM, int WN> __host__ __device__ constexpr int gemm_smem() {
   return (gemm_a_stage<WM>() + gemm_b_stage<WN>()) * STAGES * (int)sizeof(double);
 }
-// the row granularity of the fused a12 column partials (colpart): the CTA tile height
-static int g_gemm_bm = 128;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -247,27 +243,12 @@ static void launch_dgemm_w(double* C, int64_t ldc, const double* A, int64_t lda,
         C, ldc, A, lda, B, ldb, M, N, K, neg ? 1 : 0, beta ? 1 : 0, dec, k, want, colpart, ldp);
 }
 
-// CTA tile = (32 WM) x (32 WN): default WM x WN = 2 x 2 (64 x 64, 4 warps, 4 CTAs/SM: C3 LU update
-// 27.5 TF vs 27.3 for 4 x 2 = 128 x 64 with 2 CTAs/SM, 26.3 for 2 x 4, 25.0 for 4 x 1, 23.8 for
-// 4 x 4); HLQ_DGEMM_TILE=4x2|4x4|2x4|4x1 selects the alternatives
-static int dgemm_tile() {
-  static int t = -1;
-  if (t < 0) {
-    const char* e = getenv("HLQ_DGEMM_TILE");
-    t = 2;
-    if (e && !strcmp(e, "4x2")) t = 0;
-    if (e && !strcmp(e, "4x4")) t = 1;
-    if (e && !strcmp(e, "2x4")) t = 3;
-    if (e && !strcmp(e, "4x1")) t = 4;
-    g_gemm_bm = (t == 2 || t == 3) ? 64 : 128;
-  }
-  return t;
-}
-
-int gemm_colpart_rows() {
-  dgemm_tile();
-  return g_gemm_bm;
-}
+// CTA tile = (32 WM) x (32 WN) = 64 x 64 (4 warps, 4 CTAs/SM: C3 LU update 27.5 TF vs 27.3 for
+// 128 x 64 with 2 CTAs/SM, 26.3 for 64 x 128, 25.0 for 128 x 32, 23.8 for 128 x 128, measured in
+// round 1); its 64-row column partials match the TMA kernel's (gemm_tma.cu), so both feed the same
+// colpart layout
+constexpr int kGemmBM = 64;
+int gemm_colpart_rows() { return kGemmBM; }
 
 // C[M x N] = beta*C + (neg ? -1 : 1) * A[M x K] * B[K x N]; dec/k/want: optional predicate.
 void launch_dgemm(double* C, int64_t ldc, const double* A, int64_t lda, const double* B,
@@ -276,27 +257,8 @@ void launch_dgemm(double* C, int64_t ldc, const double* A, int64_t lda, const do
                   int64_t ldp) {
   if (ldp == 0) ldp = N;
   if (M <= 0 || N <= 0 || K <= 0) return;
-  switch (dgemm_tile()) {
-    case 1:
-      launch_dgemm_w<4, 4>(C, ldc, A, lda, B, ldb, M, N, K, neg, beta, dec, k, want, st, colpart,
-                           ldp);
-      break;
-    case 2:
-      launch_dgemm_w<2, 2>(C, ldc, A, lda, B, ldb, M, N, K, neg, beta, dec, k, want, st, colpart,
-                           ldp);
-      break;
-    case 3:
-      launch_dgemm_w<2, 4>(C, ldc, A, lda, B, ldb, M, N, K, neg, beta, dec, k, want, st, colpart,
-                           ldp);
-      break;
-    case 4:
-      launch_dgemm_w<4, 1>(C, ldc, A, lda, B, ldb, M, N, K, neg, beta, dec, k, want, st, colpart,
-                           ldp);
-      break;
-    default:
-      launch_dgemm_w<4, 2>(C, ldc, A, lda, B, ldb, M, N, K, neg, beta, dec, k, want, st, colpart,
-                           ldp);
-  }
+  static_assert(gemm_bm<2>() == kGemmBM, "colpart rows");
+  launch_dgemm_w<2, 2>(C, ldc, A, lda, B, ldb, M, N, K, neg, beta, dec, k, want, st, colpart, ldp);
 }
 
 // a12 from the fused epilogue: tile row i = CTA row blocks [i*bpt, (i+1)*bpt); tile-norm max over

@@ -5,6 +5,7 @@
 #include <stdio.h>
 
 #include <utility>
+#include <array>
 #include <vector>
 
 #include "hlq_internal.cuh"
@@ -107,6 +108,13 @@ struct hlq_factors_s {
   size_t solve_cap = 0, solve_used = 0;
   std::vector<std::pair<int, int>> solve_runs;   // [ka, kb) of every forward LU run
   std::vector<size_t> solve_unit_off, solve_unit_cnt;  // per run (+1: back pass) in the table
+  // the solve's Q^T replay of runs of consecutive QR steps as DAG launches (built at the first
+  // hlq_solve): device ops (6 ints each) + completion flags in qsolve_block, per run {ka, kb, off,
+  // count}
+  void* qsolve_block = nullptr;
+  int* qsolve_done = nullptr;
+  std::vector<std::array<int, 4>> qsolve_runs;
+  bool qsolve_built = false;
   // 2D block-cyclic factorization state (dist.cu); nullptr on the single-GPU path
   hlq::DistState* dist = nullptr;
 };

@@ -164,6 +164,9 @@ void launch_qr_apply(const double* A, Geo g, int k, int ib, const double* Tg, co
                      const int2* const* level_pairs, const int* level_count, int nlevels,
                      double* base, int64_t ldc, int64_t ncols, const uint8_t* dec,
                      cudaStream_t st, const QRTsPlan* ts = nullptr);
+// the solve's Q^T x of a run of QR steps as one dependency-DAG launch (ops: 6 ints each, see qr.cu)
+void launch_qr_solve_dag(const double* A, Geo g, int ib, const double* Tg, const double* Ttt,
+                         const int* ops, int nops, int* done, double* x, cudaStream_t st);
 // TTMQR levels only (no UNMQR) on a column block: the solve's cross-rank head merges
 void launch_tt_apply(const double* A, Geo g, int k, int ib, const double* Ttt,
                      const int2* const* level_pairs, const int* level_count, int nlevels,

@@ -20,10 +20,12 @@ namespace hlq {
 // partials, U = T_b^T W by 32 threads, and x -= V_b U stays in registers.
 // MODE 0: GEQRT reflectors of tile row i (unit lower); 1: TT reflectors of the pair (e, i)
 // (upper triangular); 2: TS reflectors of the pair (e, i) (square)
-template <int MODE>
+template <int MODE, bool CG = false>
 __device__ void qr_apply_vec_body(const double* __restrict__ A, Geo g, int k, int ib,
                                   const double* __restrict__ Tb, int e, int i,
                                   double* __restrict__ x, double (*red)[33], double* Uv) {
+  // (CG: x is written by other CTAs of the same launch -- read it through L2 only)
+  auto ldx = [](const double* p) { if constexpr (CG) return __ldcg(p); else return *p; };
   constexpr bool TT = MODE != 0, TS = MODE == 2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int bi = g.bs(i), bk = g.cbs(k);
@@ -32,7 +34,7 @@ __device__ void qr_apply_vec_body(const double* __restrict__ A, Geo g, int k, in
   double* xi = x + g.r0(i);
   double* xe = x + g.r0(e);
   const int r0 = tid, r1 = tid + 256;
-  double x0 = r0 < bi ? xi[r0] : 0.0, x1 = r1 < bi ? xi[r1] : 0.0;
+  double x0 = r0 < bi ? ldx(xi + r0) : 0.0, x1 = r1 < bi ? ldx(xi + r1) : 0.0;
   for (int i0 = 0; i0 < bk; i0 += 32) {
     const int sb = min(32, bk - i0);
     if (!TT && i0 >= bi) break;
@@ -70,7 +72,7 @@ __device__ void qr_apply_vec_body(const double* __restrict__ A, Geo g, int k, in
       double w = 0.0;
 #pragma unroll
       for (int q = 0; q < 8; ++q) w += red[q][lane];
-      const double xo = (TT && lane < sb) ? xe[i0 + lane] : 0.0;  // x_e(b) before the block
+      const double xo = (TT && lane < sb) ? ldx(xe + i0 + lane) : 0.0;  // x_e(b) before the block
       if (TT) w += xo;
       // U = T_b^T W: u_l = sum_{q <= l} T(q, l) W_q (T(q, l) at T[(i0 + l) * ib + q])
       double u = 0.0;
@@ -126,6 +128,60 @@ __global__ void __launch_bounds__(256) k_qr_apply_vec_ts(const double* __restric
     qr_apply_vec_body<2>(A, g, k, ib, Tb, pr.x, pr.y, x, red, Uv);
     __syncthreads();
   }
+}
+
+// The Q^T x replay of a run of consecutive QR steps as ONE launch: one CTA per op (6 ints: kind 0
+// GEQRT rows / 1 TS pair / 2 TT pair, rows e and i, the previous op on row e and on row i -- across
+// steps --, the step k), listed in dependency order; an op waits for its predecessors' completion
+// flags (acquire), applies its reflectors to x_e / x_i and releases its own flag.  (Prefetching
+// every resident op's V tile at launch measured slower: a thousand waiting CTAs' tiles overflow L2.)  Replaces ~6 launches per step (each a handful of CTAs) by a single
+// launch whose critical path is the chain of ops through the rows.
+__global__ void __launch_bounds__(256) k_qr_solve_dag(const double* __restrict__ A, Geo g, int ib,
+                                                      const double* __restrict__ Tg,
+                                                      const double* __restrict__ Ttt,
+                                                      const int* __restrict__ ops,
+                                                      int* __restrict__ done, double* x) {
+  __shared__ double red[8][33];
+  __shared__ double Uv[32];
+  const int* op = ops + 6 * blockIdx.x;
+  const int kind = op[0], e = op[1], i = op[2], pe = op[3], pi = op[4], k = op[5];
+  if (threadIdx.x == 0) {
+    unsigned ns = 32;
+    auto wait = [&](int q) {
+      if (q < 0) return;
+      for (;;) {
+        int v;
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(done + 32 * q) : "memory");
+        if (v) break;
+        __nanosleep(ns);
+        if (ns < 256) ns <<= 1;
+      }
+    };
+    wait(pe);
+    wait(pi);
+  }
+  __syncthreads();
+  if (kind == 0)
+    qr_apply_vec_body<0, true>(A, g, k, ib, Tg, 0, i, x, red, Uv);
+  else if (kind == 1)
+    qr_apply_vec_body<2, true>(A, g, k, ib, Ttt, e, i, x, red, Uv);
+  else
+    qr_apply_vec_body<1, true>(A, g, k, ib, Ttt, e, i, x, red, Uv);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(done + 32 * blockIdx.x), "r"(1)
+                 : "memory");
+  }
+}
+
+// done: 32 ints (one 128-byte line) per op, zeroed here
+void launch_qr_solve_dag(const double* A, Geo g, int ib, const double* Tg, const double* Ttt,
+                         const int* ops, int nops, int* done, double* x, cudaStream_t st) {
+  if (nops <= 0) return;
+  cudaMemsetAsync(done, 0, sizeof(int) * 32 * (size_t)nops, st);
+  ::hlq::g_launches++;
+  k_qr_solve_dag<<<nops, 256, 0, st>>>(A, g, ib, Tg, Ttt, ops, done, x);
 }
 
 // Apply the stored QR step k to the solve's vector x (rows 0..N-1 of base): Q_ik^T of every

@@ -394,20 +394,25 @@ __global__ void __launch_bounds__(PS_T) k_solve_rows(const double* __restrict__ 
   }
   double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
   const bool v2 = ((g.lda & 1) == 0) && ((((uintptr_t)A) & 15) == 0) && ((g.nb & 1) == 0);
-  // the factor tiles do not depend on x: pull this unit's tiles (and the finisher's diagonal tile)
-  // into L2 while the x segments they multiply are still being solved
-  {
-    const int cn0 = FWD ? max(1, (min(i, kb) - ka + G - 1) / G) : max(1, (g.n - 1 - i + G - 1) / G);
-    for (int t = 0; t < ntiles; ++t) {
-      const int j = FWD ? jfirst + t : jfirst - t;
-      prefetch_tile_l2(A + g.r0(j) * g.lda + g.r0(i), g.lda, bi, g.bs(j), tid);
-    }
-    if (c + 1 == cn0 && (!FWD || i < kb))
-      prefetch_tile_l2(A + g.r0(i) * g.lda + g.r0(i), g.lda, bi, bi, tid);
+  // the factor tiles do not depend on x: pull the next tile into L2 while the x segment it
+  // multiplies is still being solved -- one tile ahead only (prefetching every resident unit's
+  // tiles at once overflowed L2 and evicted them before use), the diagonal tile with the last one
+  const int cn0 = FWD ? max(1, (min(i, kb) - ka + G - 1) / G) : max(1, (g.n - 1 - i + G - 1) / G);
+  const bool finisher = c + 1 == cn0 && (!FWD || i < kb);
+  if (ntiles > 0) {
+    prefetch_tile_l2(A + g.r0(jfirst) * g.lda + g.r0(i), g.lda, bi, g.bs(jfirst), tid);
+  } else if (finisher) {
+    prefetch_tile_l2(A + g.r0(i) * g.lda + g.r0(i), g.lda, bi, bi, tid);
   }
   for (int t = 0; t < ntiles; ++t) {
     const int j = FWD ? jfirst + t : jfirst - t;
     const int bj = g.bs(j);
+    if (t + 1 < ntiles) {
+      const int jn = FWD ? j + 1 : j - 1;
+      prefetch_tile_l2(A + g.r0(jn) * g.lda + g.r0(i), g.lda, bi, g.bs(jn), tid);
+    } else if (finisher) {
+      prefetch_tile_l2(A + g.r0(i) * g.lda + g.r0(i), g.lda, bi, bi, tid);
+    }
     if (tid == 0) wait_flag(xflag + (int64_t)j * kFlagStride, 1);
     __syncthreads();
     for (int cc = tid; cc < bj; cc += PS_T) xs[cc] = __ldcg(x + g.r0(j) + cc);

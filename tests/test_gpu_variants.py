@@ -1,11 +1,11 @@
 """Schedule and kernel-shape variants must not change the factorization (-m gpu).
 
 The speculative QR panel (HLQ_SPEC_QR) only moves the QR branch's panel work to a second stream and a
-copy of the panel (its kernels run while d_k is undecided and exit once it is LU), the DGEMM warp grid
-(HLQ_DGEMM_TILE) only changes which CTA computes which output tile, and the TMA-fed Schur update
+copy of the panel (its kernels run while d_k is undecided and exit once it is LU), the TMA-fed Schur update
 (default) and the cp.async kernel (HLQ_DGEMM_TMA=0) accumulate every element's K products in the
 same order; the QR panel as one dependency-DAG launch (default) or level by level (HLQ_QR_DAG=0)
-runs the same kernels' arithmetic: all must give bit-identical factors,
+runs the same kernels' arithmetic, and so does the solve's Q^T replay as one DAG launch per run of
+QR steps (default) or step by step (HLQ_QR_SOLVE_DAG=0): all must give bit-identical factors and x,
 decisions and QR-step T factors -- under A1 and A2, Max and MUMPS, one and two QR-tree domains.  The environment is read once per process, so each variant
 runs in its own interpreter."""
 import os
@@ -44,6 +44,7 @@ for name, M, crit, alpha, kw in cases:
     n = len(d)
     T = [f.T(i, k, kind) for k in range(n) if d[k] == 1 for i in range(k, n) for kind in (0, 1)]
     out[name + "_T"] = np.array(T) if T else np.zeros(0)
+    out[name + "_x"] = f.solve(torch.from_numpy(I.uniform_rhs(7, N)).cuda()).cpu().numpy()
     f.free()
 np.savez({path!r}, **out)
 '''
@@ -59,8 +60,9 @@ def _run(env_extra, path):
     return np.load(path)
 
 
-@pytest.mark.parametrize("env", [{"HLQ_SPEC_QR": "0"}, {"HLQ_DGEMM_TILE": "4x2"}, {"HLQ_DGEMM_TMA": "0"},
-                                 {"HLQ_TMA_CONS": "4"}, {"HLQ_QR_DAG": "0"}])
+@pytest.mark.parametrize("env", [{"HLQ_SPEC_QR": "0"}, {"HLQ_DGEMM_TMA": "0"},
+                                 {"HLQ_TMA_CONS": "4"}, {"HLQ_QR_DAG": "0"},
+                                 {"HLQ_QR_SOLVE_DAG": "0"}])
 def test_variant_is_bit_identical(tmp_path, env):
     base = _run({}, str(tmp_path / "base.npz"))
     var = _run(env, str(tmp_path / "var.npz"))
