@@ -443,8 +443,6 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   f->solve_ws_in = base + oSv;
   f->tma_maps = make_tma_maps(A, N, lda, nb);
   w.tma_maps = f->tma_maps;
-  f->qu_maps = make_qu_maps(A, N, lda, nb, w.Tg, w.Ttt, (int64_t)ntri);
-  w.qu_maps = f->qu_maps;
   f->solve_cap = solve_cap;
   // per-parity views (lookahead: step k+1's panel runs while step k's update still reads step k's
   // W / ipiv / L^-1 / U^-1 / perm)
@@ -1064,7 +1062,6 @@ void hlq_free(hlq_factors_t f) {
     cache_put(f->dev, 0, f->ws_block, f->ws_bytes);
   }
   if (f->tma_maps) free_tma_maps(f->tma_maps);
-  if (f->qu_maps) free_qu_maps(f->qu_maps);
   if (f->qsolve_block) {
     cudaStreamSynchronize(f->st);
     cudaFree(f->qsolve_block);

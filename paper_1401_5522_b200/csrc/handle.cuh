@@ -102,7 +102,6 @@ struct hlq_factors_s {
   // persistent-solve workspace (allocated at the first hlq_solve): unit tables per forward LU run
   // and for the back substitution, flags, chunk partial sums
   void* tma_maps = nullptr;      // gemm_tma.cu tensor maps of A (host memory) or null
-  void* qu_maps = nullptr;       // qr_update.cu tensor maps of A and the T arrays, or null
   void* solve_ws = nullptr;      // = solve_ws_in, or solve_ws_own when the tables outgrow it
   void* solve_ws_in = nullptr;   // piece of the factorization workspace (table capacity solve_cap)
   void* solve_ws_own = nullptr;  // own allocation (freed by hlq_free)

@@ -72,7 +72,6 @@ struct DevWork {
   int* dom_idx;                 // 2*148 partial pivot rows
   unsigned int* dom_counter;    // arrivals of the last-CTA reduction
   const void* tma_maps;         // TMA tensor maps of A for the Schur update (gemm_tma.cu) or null
-  const void* qu_maps;          // TMA tensor maps of A and the T arrays for the QR update or null
   double* steplog;              // 2n: per step the binding criterion inequality's lhs, rhs (or null)
 };
 
@@ -195,14 +194,6 @@ void launch_lu_update(double* A, Geo g, int k, const DevWork& w, int64_t c0, int
 // TMA-fed Schur update A[k1:k1+M, c0:c0+nc] -= A[k1:, k0:k0+K] A[k0:k0+K, c0:] (false: not eligible)
 void* make_tma_maps(const double* A, int64_t N, int64_t lda, int nb);
 void free_tma_maps(void* m);
-// the TMA-fed QR update (qr_update.cu): maps per factorization, and the current factorization of
-// this host thread's update launches (qu_tma_begin ... qu_tma_end)
-void* make_qu_maps(const double* A, int64_t N, int64_t lda, int nb, const double* Tg,
-                   const double* Ttt, int64_t ntri);
-void free_qu_maps(void* m);
-void qu_tma_begin(const void* maps, const double* A, int64_t lda, const double* Tg,
-                  const double* Ttt);
-void qu_tma_end();
 bool launch_schur_tma(const void* maps, double* A, int64_t lda, int64_t k0, int64_t k1, int64_t c0,
                       int64_t M, int64_t nc, int K, const uint8_t* dec, int k, int want,
                       double* colpart, int64_t ldp, cudaStream_t st);

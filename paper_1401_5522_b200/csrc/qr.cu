@@ -251,13 +251,6 @@ bool launch_qr_update(double* A, Geo g, int k, int ib, const int2* const* level_
   const int64_t ncols = c1 - c0;
   if (ncols <= 0) return true;
   const bool hqr = ts != nullptr && ts->ngroups > 0;
-  // the update's launches may feed their rings by TMA from this factorization's tensor maps
-  struct TmaScope {
-    explicit TmaScope(const DevWork& w, const double* A, int64_t lda) {
-      qu_tma_begin(w.qu_maps, A, lda, w.Tg, w.Ttt);
-    }
-    ~TmaScope() { qu_tma_end(); }
-  } tma_scope(w, A, g.lda);
   bool fused = gmax != nullptr && (nlevels > 0 || hqr);
   double* base = A + c0 * g.lda;
   if (hqr) {
