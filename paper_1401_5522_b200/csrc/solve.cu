@@ -334,11 +334,14 @@ __device__ void tile_upper_solve(const double* __restrict__ D, int64_t lda, int 
 #pragma unroll
       for (int cc = 0; cc < 32; ++cc)
         lv[cc] = (cc > lane && base + cc < bi) ? __ldg(D + (int64_t)(base + cc) * lda + r) : 0.0;
+      // 1 / U_rr for every lane at once: the substitution chain then multiplies instead of
+      // dividing (32 dependent divisions were most of the diagonal tile's latency)
       const double d = r < bi ? __ldg(D + (int64_t)r * lda + r) : 1.0;
+      const double rd = 1.0 / d;
       double v = r < bi ? ys[r] : 0.0;
 #pragma unroll
       for (int cc = 31; cc >= 0; --cc) {
-        if (lane == cc) v = v / d;
+        if (lane == cc) v = v * rd;
         const double xc = __shfl_sync(0xffffffffu, v, cc);
         if (lane < cc) v = fma(-lv[cc], xc, v);
       }
@@ -440,9 +443,10 @@ __global__ void __launch_bounds__(PS_T) k_solve_rows(const double* __restrict__ 
     if (tid == 0) st_release(pflag + ((int64_t)i * cmax + c) * kFlagStride, 1);
     return;
   }
-  // finisher: r_i = x_i - (sum of the chunk partials in chunk order + own)
-  if (tid == 0)
-    for (int cc = 0; cc < c; ++cc) wait_flag(pflag + ((int64_t)i * cmax + cc) * kFlagStride, 1);
+  // finisher: r_i = x_i - (sum of the chunk partials in chunk order + own); thread cc waits for
+  // chunk cc's flag (all polls in flight at once: a sequential poll of up to n/G already-set flags
+  // cost an L2 round trip each on the critical path)
+  for (int cc = tid; cc < c; cc += PS_T) wait_flag(pflag + ((int64_t)i * cmax + cc) * kFlagStride, 1);
   __syncthreads();
   double* xi = x + g.r0(i);
   for (int r = tid; r < bi; r += PS_T) {
