@@ -458,30 +458,13 @@ __device__ __forceinline__ void qr_update3_body(const double* __restrict__ A, Ge
   }
 }
 
-// Experiment (HLQ_QR_DEPHASE=<ns>): the two CTAs resident on an SM run identical chunk loops and
-// tend to reach their chunk barriers together, when neither feeds the DMMA pipe; every second CTA
-// arriving on an SM starts `ns` later (per-SM arrival counter) to offset them by part of a chunk.
-__device__ unsigned g_qu_sm_arrivals[256];
-__device__ __forceinline__ void qu_dephase(int ns) {
-  if (ns <= 0) return;
-  __shared__ unsigned s_late;
-  if (threadIdx.x == 0) {
-    unsigned smid;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    s_late = atomicAdd(&g_qu_sm_arrivals[smid & 255], 1u) & 1u;
-  }
-  __syncthreads();
-  if (s_late) __nanosleep((unsigned)ns);
-}
-
 // UNMQR of tile rows i = rows[blockIdx.y] (rows == nullptr: k + blockIdx.y)
 template <int NB, int RQ, int NCG, bool V16>
 __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ * NCG) : 1)
     k_unmqr3(const double* __restrict__ A, Geo g, int k, const double* __restrict__ Tbase,
              const int* __restrict__ rows, double* __restrict__ base, int64_t ldcg, int64_t ncols,
-             const uint8_t* __restrict__ dec, int dephase) {
+             const uint8_t* __restrict__ dec) {
   if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
-  qu_dephase(dephase);
   const int i = rows != nullptr ? rows[blockIdx.y] : k + (int)blockIdx.y;
   qr_update3_body<NB, 0, RQ, NCG, V16>(A, g, k, Tbase, 0, i, base, ldcg, ncols, nullptr);
 }
@@ -491,10 +474,8 @@ template <int NB, int RQ, int NCG, bool V16>
 __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ * NCG) : 1)
     k_ttmqr3(const double* __restrict__ A, Geo g, int k, const double* __restrict__ Tbase,
              const int2* __restrict__ pairs, double* __restrict__ base, int64_t ldcg,
-             int64_t ncols, const uint8_t* __restrict__ dec, double* __restrict__ gmax,
-             int dephase) {
+             int64_t ncols, const uint8_t* __restrict__ dec, double* __restrict__ gmax) {
   if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
-  qu_dephase(dephase);
   const int2 pr = pairs[blockIdx.y];
   qr_update3_body<NB, 1, RQ, NCG, V16>(A, g, k, Tbase, pr.x, pr.y, base, ldcg, ncols,
                                               gmax);
@@ -507,9 +488,8 @@ __global__ void __launch_bounds__(32 * RQ * NCG, (8 / (RQ * NCG)) > 0 ? 8 / (RQ 
     k_tsmqr3(const double* __restrict__ A, Geo g, int k, const double* __restrict__ Tbase,
              const int2* __restrict__ pairs, const int* __restrict__ off,
              double* __restrict__ base, int64_t ldcg, int64_t ncols,
-             const uint8_t* __restrict__ dec, double* __restrict__ gmax, int dephase) {
+             const uint8_t* __restrict__ dec, double* __restrict__ gmax) {
   if (dec != nullptr && dec[k] != HLQ_DEC_QR) return;
-  qu_dephase(dephase);
   for (int p = off[blockIdx.y]; p < off[blockIdx.y + 1]; ++p) {
     const int2 pr = pairs[p];
     qr_update3_body<NB, 2, RQ, NCG, V16>(A, g, k, Tbase, pr.x, pr.y, base, ldcg, ncols,
@@ -537,18 +517,16 @@ static void launch3(const double* A, Geo g, int k, const double* T, const int2* 
   const unsigned slabs = (unsigned)((ncols + 16 * NCG - 1) / (16 * NCG));
   const size_t smem = upd3_smem(RQ * NCG, 16 * NCG);
   if (npairs <= 0) return;
-  static int dephase = -1;
-  if (dephase < 0) dephase = getenv("HLQ_QR_DEPHASE") ? atoi(getenv("HLQ_QR_DEPHASE")) : 0;
   ::hlq::g_launches++;
   if (mode == 0)  // npairs = number of tile rows (list: the rows, or nullptr for k..)
     k_unmqr3<NB, RQ, NCG, V16><<<dim3(slabs, npairs), 32 * RQ * NCG, smem, st>>>(
-        A, g, k, T, list, base, ldc, ncols, dec, dephase);
+        A, g, k, T, list, base, ldc, ncols, dec);
   else if (mode == 1)
     k_ttmqr3<NB, RQ, NCG, V16><<<dim3(slabs, npairs), 32 * RQ * NCG, smem, st>>>(
-        A, g, k, T, pairs, base, ldc, ncols, dec, gmax, dephase);
+        A, g, k, T, pairs, base, ldc, ncols, dec, gmax);
   else  // npairs = number of groups, list = their pair offsets
     k_tsmqr3<NB, RQ, NCG, V16><<<dim3(slabs, npairs), 32 * RQ * NCG, smem, st>>>(
-        A, g, k, T, pairs, list, base, ldc, ncols, dec, gmax, dephase);
+        A, g, k, T, pairs, list, base, ldc, ncols, dec, gmax);
 }
 
 // register-slab kernels for every nb <= 320 (instantiated at 64, 128, 192, 256, 320: a smaller
