@@ -368,8 +368,9 @@ def main():
             traffic_note = tj.get("_notes", {}).get(f"{args.config}:{dom}")
         except Exception:
             traffic = None
-    kname = {"lu_update": "k_dgemm (LU Schur update + SWPTRSM)",
-             "qr_unmqr": "k_qr_update3 (QR trailing update: UNMQR + TTMQR)"}[dom]
+    kname = {"lu_update": "k_dgemm_tma (TMA-fed LU Schur update; class incl. the SWPTRSM Apply)",
+             "qr_unmqr": "k_unmqr3 / k_tsmqr3 / k_ttmqr3 (QR trailing update: UNMQR, TSMQR "
+                         "chains, TTMQR levels)"}[dom]
     roofline = {"bound": "tensor", "kernel": kname,
                 "achieved": achieved, "peak": FP64_DMMA_PEAK_TF, "unit": "TFLOP/s",
                 "frac": achieved / FP64_DMMA_PEAK_TF, "traffic": traffic,
@@ -555,8 +556,9 @@ def run_distributed(args, cfg, rank, world, local, dev):
     dom = max(("lu_update", "qr_unmqr"), key=lambda c: agg[c]["ms"])
     # this rank's share of the class flops: the trailing update is spread evenly over the grid
     achieved = agg[dom]["flops"] / world / (agg[dom]["ms"] * 1e-3) / 1e12 if agg[dom]["ms"] else 0.0
-    kname = {"lu_update": "k_dgemm (LU Schur update + SWPTRSM)",
-             "qr_unmqr": "k_qr_update3 (QR trailing update: UNMQR + TTMQR)"}[dom]
+    kname = {"lu_update": "k_dgemm_tma (TMA-fed LU Schur update; class incl. the SWPTRSM Apply)",
+             "qr_unmqr": "k_unmqr3 / k_tsmqr3 / k_ttmqr3 (QR trailing update: UNMQR, TSMQR "
+                         "chains, TTMQR levels)"}[dom]
     roofline = {"bound": "tensor", "kernel": kname, "achieved": achieved,
                 "peak": FP64_DMMA_PEAK_TF, "unit": "TFLOP/s", "frac": achieved / FP64_DMMA_PEAK_TF,
                 "traffic": None, "rank": rank,

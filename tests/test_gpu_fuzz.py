@@ -131,3 +131,44 @@ def test_fuzz_criteria_against_oracle(t, N, nb, crit, alpha, gen, variant, scope
                              pivot_scope=scope, variant=1)
         gate = max(1e-10, 10.0 * O.factor_diff(fv.A, fo.A))
         assert O.factor_diff(F, fo.A) <= gate, (O.factor_diff(F, fo.A), gate)
+
+
+def _hqr_cases():
+    rng = np.random.default_rng(4242)
+    cases = []
+    for t in range(40):
+        nb = int(rng.choice([32, 64, 96, 128, 160, 192, 240, 256, 320]))
+        n = int(rng.integers(2, 10))
+        tail = int(rng.choice([0, 1, 31, 32, 33, nb // 2, nb - 1]))
+        N = max(1, (n - 1) * nb + (tail if tail > 0 else nb))
+        f = float(rng.choice([0.5, 1.0, 1.0]))
+        D = int(rng.choice([1, 2, 3]))
+        a = int(rng.choice([2, 3, 4, 8]))
+        variant = str(rng.choice(["A1", "A1", "A2"]))
+        cases.append((t, N, nb, f, D, a, variant))
+    return cases
+
+
+@pytest.mark.parametrize("t,N,nb,f,D,a,variant", _hqr_cases())
+def test_fuzz_hqr_against_oracle(t, N, nb, f, D, a, variant):
+    """The HQR tree (reading 34: TS groups of `a` tiles, greedy TT over the group heads and the
+    domain heads) through the QR panel DAG, the TSMQR chains and the solve DAG, against the
+    oracle's hqrA plan: ragged tails, 1..3 domains, mixed forced patterns, A1 / A2."""
+    import paper_1401_5522_b200 as H
+    A = I.uniform_matrix(300 + t, N) + 2.0 * np.eye(N)
+    b = I.uniform_rhs(300 + t, N)
+    n = (N + nb - 1) // nb
+    forced = I.bernoulli_pattern(60 + t, n, f)
+    fo = O.hybrid_factor(A, nb, O.CRIT_MAX, 1.0, D=D, forced=forced, tree=f"hqr{a}",
+                         lu_variant=variant)
+    dA = H.to_colmajor(A)
+    fg = H.hlq_factor_ex(dA, N, nb, O.CRIT_MAX, 1.0, forced=forced, tree_domains=D,
+                         tree=H.TREE_HQR, ts_group=a,
+                         lu_variant=H.LU_A2 if variant == "A2" else H.LU_A1)
+    np.testing.assert_array_equal(fg.decisions(), fo.dec)
+    F = H.from_colmajor(dA)
+    assert O.factor_diff(F, fo.A) <= 1e-10, O.factor_diff(F, fo.A)
+    x = fg.solve(torch.from_numpy(np.ascontiguousarray(b)).cuda()).cpu().numpy()
+    assert O.hpl3(A, x, b) <= 16.0
+    assert np.allclose(x, O.solve(fo, b), rtol=0, atol=1e-8 * max(1.0, np.abs(x).max()))
+    fg.free()
