@@ -436,6 +436,14 @@ def lu_step(A: np.ndarray, N: int, nb: int, k: int, W: np.ndarray, ipiv: np.ndar
 # Householder kernels (Alg. 4).  LAPACK dlarfg convention (ledger 14); ib-blocked T
 # in forward column-wise dlarft form (ledger 15).
 # ----------------------------------------------------------------------------------------------
+# Diagnostics (no arithmetic): with LARFG_LOG = [] every reflector whose alpha is below
+# LARFG_LOG_RATIO * ||(alpha, x)|| -- a Householder sign decision near its discontinuity at alpha = 0
+# (ledger 14) -- is recorded as (step, alpha, norm).  tools/sign_probe.py and parity_full.py read it.
+LARFG_LOG = None
+LARFG_LOG_RATIO = 1e-6
+LARFG_STEP = -1
+
+
 def larfg(alpha: float, x: np.ndarray):
     """H = I - tau [1; v][1; v]^T with H [alpha; x] = [beta; 0].  Returns (beta, tau, v).
     beta = -sign(alpha)*||(alpha, x)||_2 (sign(0)=+), tau = (beta-alpha)/beta, v = x/(alpha-beta);
@@ -444,6 +452,8 @@ def larfg(alpha: float, x: np.ndarray):
     if ssq == 0.0:
         return alpha, 0.0, np.zeros_like(x)
     nrm = math.sqrt(alpha * alpha + ssq)
+    if LARFG_LOG is not None and abs(alpha) < LARFG_LOG_RATIO * nrm:
+        LARFG_LOG.append((LARFG_STEP, float(alpha), nrm))  # diagnostics only (sign near ties)
     beta = -nrm if alpha >= 0.0 else nrm
     tau = (beta - alpha) / beta
     v = x / (alpha - beta)
@@ -732,6 +742,8 @@ def qr_step(A: np.ndarray, N: int, nb: int, k: int, D: int, ib: int,
     Independent work runs concurrently (_pmap): the GEQRTs of the tiles, the pairs of one TT level
     (disjoint rows), and the column chunks of one trailing update -- Q^T acts on every column
     independently, so applying it chunk by chunk is the same computation."""
+    global LARFG_STEP
+    LARFG_STEP = k
     n = ntiles(N, nb)
     ck = tsl(N, nb, k)
     chunks = [slice(c, min(c + QR_COLS, N)) for c in range(ck.stop, N, QR_COLS)]

@@ -102,6 +102,19 @@ def sign_flips(F: np.ndarray, G: np.ndarray, N: int, nb: int) -> dict:
     return out
 
 
+def sign_flip_detail(F: np.ndarray, G: np.ndarray, N: int, nb: int) -> dict:
+    """{step: {rows, gpu_diag, oracle_diag}} for the rows of R whose diagonal sign differs."""
+    out = {}
+    for k in range((N + nb - 1) // nb):
+        r0, r1 = k * nb, min((k + 1) * nb, N)
+        df, dg = np.diag(F[r0:r1, r0:r1]), np.diag(G[r0:r1, r0:r1])
+        idx = np.nonzero(np.sign(df) != np.sign(dg))[0]
+        if idx.size:
+            out[str(k)] = {"rows": idx.tolist(), "gpu_diag": df[idx].tolist(),
+                           "oracle_diag": dg[idx].tolist()}
+    return out
+
+
 def _variant_worker(args):
     """The noise-floor oracle run (variant = 1) in its own process: its packed factors to a file."""
     name, path = args
@@ -156,7 +169,11 @@ def run(name: str, outdir: str, floor_parallel: bool = False) -> dict:
         floor_proc.start()
     t0 = time.perf_counter()
     tree = sp.get("tree", "greedy")
+    O.LARFG_LOG = []  # reflectors with |alpha| < 1e-6 ||(alpha, x)||: sign decisions near alpha = 0
     fo = O.hybrid_factor(A, nb, crit, alpha, D=D, forced=forced, tree=tree)
+    rec["oracle_small_alpha"] = sorted(O.LARFG_LOG, key=lambda e: abs(e[1]) / e[2])[:50]
+    rec["oracle_small_alpha_count"] = len(O.LARFG_LOG)
+    O.LARFG_LOG = None
     rec["oracle_s"] = time.perf_counter() - t0
     fake = 2.0 / 3.0 * float(N) ** 3
     rec["oracle_tflops"] = fake / rec["oracle_s"] / 1e12
@@ -216,6 +233,7 @@ def run(name: str, outdir: str, floor_parallel: bool = False) -> dict:
     rec["eps_R"] = r_part_diff(F, fo.A, N, nb)
     rec["eps_R_no_sign_normalisation"] = r_part_diff_raw(F, fo.A, N, nb)
     rec["row_sign_flips_per_step"] = sign_flips(F, fo.A, N, nb)
+    rec["row_sign_flip_detail"] = sign_flip_detail(F, fo.A, N, nb)
     rec["bit_identical"] = bool(np.array_equal(F, fo.A, equal_nan=True))
     del F
     print(f"[{name}] gpu {rec['gpu_s']:.2f}s decisions identical {rec['decisions_identical']}, "
