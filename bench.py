@@ -377,6 +377,9 @@ def main():
                 "traffic_note": traffic_note,
                 "peak_source": "measured FP64 DMMA mma.sync m8n8k4 sustained, 148 SMs "
                                "(profiles/r01/peak_dmma.jsonl); cuBLAS DGEMM measured 36.2",
+                "class_note": "class = the update-stream launches (every trailing column block but "
+                              "the lookahead one, whose launches overlap them on the panel stream "
+                              "and are the class 'other', flops counted there)",
                 "share_of_step": agg[dom]["ms"] / t_sum if t_sum else None,
                 "per_class_ms": {c: round(v["ms"] / args.steps, 3) for c, v in agg.items()}}
 

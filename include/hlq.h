@@ -200,7 +200,9 @@ enum {
   HLQ_PROF_QR_TT = 6,      /* (unused since the lookahead split; kept for ABI stability)           */
   HLQ_PROF_GROWTH = 7,     /* tile-norm growth tracking (a12)                                     */
   HLQ_PROF_SOLVE = 8,      /* forward replay + back substitution (a13)                            */
-  HLQ_PROF_OTHER = 9,
+  HLQ_PROF_OTHER = 9,      /* the update of the lookahead column block k+1 (LU or QR branch) when it runs
+                              on the panel stream beside the rest of step k's update (default); its
+                              share of the update flops is counted here, not in classes 3 / 5      */
   HLQ_PROF_NCLASSES = 10
 };
 /* Per class: device milliseconds, algorithmic flops of the EXECUTED branch (Table I counts with

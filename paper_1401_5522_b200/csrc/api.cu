@@ -100,7 +100,17 @@ void cache_put(int dev, int slot, void* p, size_t bytes) {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-constexpr int kSolveG = 4;  // tiles per work unit of the persistent solve
+// tiles per work unit of the persistent solve (HLQ_SOLVE_G overrides, 1..64: measurement knob)
+static int solve_g() {
+  static int gval = -1;
+  if (gval < 0) {
+    const char* e = getenv("HLQ_SOLVE_G");
+    const int v = e ? atoi(e) : 4;
+    gval = v < 1 ? 1 : v > 64 ? 64 : v;
+  }
+  return gval;
+}
+#define kSolveG (solve_g())
 constexpr size_t kFlagBytes = 128;  // one solve flag per cache line (solve.cu kFlagStride)
 size_t solve_ws_bytes(int n, int nb, int cmax, size_t units) {
   return align_up(sizeof(int2) * units, 256) + align_up(kFlagBytes * n, 256) +
@@ -313,7 +323,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   hlq_factors_t f = new (std::nothrow) hlq_factors_s();
   if (!f) return HLQ_ERR_NOMEM;
   *out = f;
-  for (int e = 0; e < 5; ++e) cudaEventCreateWithFlags(&f->ev[e], cudaEventDisableTiming);
+  for (int e = 0; e < 6; ++e) cudaEventCreateWithFlags(&f->ev[e], cudaEventDisableTiming);
   f->A = A;
   f->g.N = N;
   f->g.lda = lda;
@@ -531,7 +541,16 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   // stage of step k+1 as soon as step k has updated column block k+1 (lookahead depth 1).
   cudaStream_t sp = panel_stream(0), sq = panel_stream(1);
   cudaEvent_t ev_ready = f->ev[0], ev_panel = f->ev[1], ev_qsrc = f->ev[2], ev_qdone = f->ev[3],
-              ev_a2 = f->ev[4];
+              ev_a2 = f->ev[4], ev_rest = f->ev[5];
+  // Lookahead column on the panel stream (HLQ_LA_SP=0: on the update stream, before the rest): the
+  // update of column block k+1 by step k is a narrow launch chain (a few hundred CTAs) that the
+  // panel of step k+1 waits for; on sp it overlaps the rest of step k's update, which starts at once
+  // on st, instead of running alone in front of it.  Step k+1's lookahead column waits for step
+  // k's rest (ev_rest), exactly the order the single stream gave.
+  static int la_env = -1;
+  if (la_env < 0) la_env = getenv("HLQ_LA_SP") ? atoi(getenv("HLQ_LA_SP")) : 1;
+  const bool la_sp = la_env != 0;
+  f->la_sp = la_sp;
   if (f->track_growth) launch_tile_norm_max(A, g, 0, w.gstep, st);
   cudaEventRecord(ev_ready, st);
 
@@ -684,16 +703,22 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
     for (int part = 0; part < 2; ++part) {
       const int64_t c0 = (part == 0) ? k1 : std::min(g.N, k1 + nb);
       const int64_t c1 = (part == 0) ? std::min(g.N, k1 + nb) : g.N;
+      cudaStream_t const st_upd = st;
+      cudaStream_t st = (part == 0 && la_sp) ? sp : st_upd;  // (shadows the update stream below)
+      if (part == 0 && la_sp && k > 0) cudaStreamWaitEvent(sp, ev_rest, 0);
       if (c1 > c0) {
+        // (profile: the lookahead column on the panel stream overlaps the rest of the update, so
+        // its bracket is its own class and the dominant class times only the update stream)
+        const bool la_cls = part == 0 && la_sp;
         if (known != HLQ_DEC_QR) {
-          P.begin(HLQ_PROF_LU_UPDATE, st);
+          P.begin(la_cls ? HLQ_PROF_OTHER : HLQ_PROF_LU_UPDATE, st);
           if (dpiv) launch_dom_swap_cols(A, g, k, Dp, w.dipiv + (size_t)k * nb, c0, c1, w.dec, st);
           launch_lu_update(A, g, k, wk, c0, c1, fuse ? w.colpart : nullptr, st, a2);
           P.end(st);
         }
         bool qr_fused = false;
         if (known != HLQ_DEC_LU) {
-          P.begin(HLQ_PROF_QR_UNMQR, st);
+          P.begin(la_cls ? HLQ_PROF_OTHER : HLQ_PROF_QR_UNMQR, st);
           // a12 fused into the TTMQR epilogues: every row i > k is final after its merge
           qr_fused = launch_qr_update(A, g, k, ib, f->lvl_ptr[k].data(), f->lvl_cnt[k].data(), nl,
                                       wk, c0, c1, st,
@@ -718,11 +743,13 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
       }
       if (part == 0) cudaEventRecord(ev_ready, st);
     }
+    if (la_sp) cudaStreamWaitEvent(st, ev_ready, 0);  // the lookahead column (on sp) is done too
     if (fuse && known != HLQ_DEC_QR) {
       P.begin(HLQ_PROF_GROWTH, st);
       launch_lu_growth(w, g, k, st);
       P.end(st);
     }
+    if (la_sp) cudaEventRecord(ev_rest, st);
     if (P.on) cudaEventRecord(f->step_ev[k + 1], st);  // step k's update stage is done
     if (nvtx_on()) nvtxRangePop();
   }
@@ -968,15 +995,22 @@ int hlq_get_profile(hlq_factors_t f, double* ms, double* flops, int64_t* launche
   double fl[HLQ_PROF_NCLASSES] = {0};
   for (int k = 0; k < g.n; ++k) {
     double b = g.bs(k), M = (double)(g.N - g.r0(k) - g.bs(k));
+    // the update flops are proportional to the columns updated: the lookahead column block's
+    // share is its own class when it ran on the panel stream
+    const double la = (f->la_sp && M > 0) ? std::min((double)g.nb, M) / M : 0.0;
     if (f->dec[k] == HLQ_DEC_LU) {
       const bool a2 = f->lu_variant == HLQ_LU_A2;  // Factor and Apply cost twice
       fl[HLQ_PROF_GETRF] += (a2 ? 4.0 : 2.0) / 3.0 * b * b * b;
       fl[HLQ_PROF_LU_TRSM] += M * b * b;             // Table I: TRSM
-      fl[HLQ_PROF_LU_UPDATE] += (a2 ? 2.0 : 1.0) * M * b * b + 2.0 * M * M * b;  // SWPTRSM + GEMM
+      const double u = (a2 ? 2.0 : 1.0) * M * b * b + 2.0 * M * M * b;  // SWPTRSM + GEMM
+      fl[HLQ_PROF_LU_UPDATE] += (1.0 - la) * u;
+      fl[HLQ_PROF_OTHER] += la * u;
     } else {
       double m = M / b;                              // trailing tiles (fractional if ragged)
       fl[HLQ_PROF_QR_GEQRT] += (m + 1.0) * 4.0 / 3.0 * b * b * b + m * 2.0 / 3.0 * b * b * b;
-      fl[HLQ_PROF_QR_UNMQR] += (m + 1.0) * 2.0 * b * b * M + m * 2.0 * b * b * M;
+      const double u = (m + 1.0) * 2.0 * b * b * M + m * 2.0 * b * b * M;
+      fl[HLQ_PROF_QR_UNMQR] += (1.0 - la) * u;
+      fl[HLQ_PROF_OTHER] += la * u;
     }
   }
   for (int c = 0; c < HLQ_PROF_NCLASSES; ++c) {

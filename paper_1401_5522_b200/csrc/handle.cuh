@@ -68,7 +68,8 @@ struct Prof {
 
 struct hlq_factors_s {
   Prof prof;
-  cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  bool la_sp = false;  // the lookahead column's update ran on the panel stream (class OTHER)
+  cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   double* A = nullptr;
   Geo g{};
   int ib = 32, D = 1, crit = 0;

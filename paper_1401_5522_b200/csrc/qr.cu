@@ -130,22 +130,47 @@ __global__ void __launch_bounds__(256) k_qr_apply_vec_ts(const double* __restric
   }
 }
 
-// The Q^T x replay of a run of consecutive QR steps as ONE launch: one CTA per op (6 ints: kind 0
-// GEQRT rows / 1 TS pair / 2 TT pair, rows e and i, the previous op on row e and on row i -- across
-// steps --, the step k), listed in dependency order; an op waits for its predecessors' completion
-// flags (acquire), applies its reflectors to x_e / x_i and releases its own flag.  (Prefetching
-// every resident op's V tile at launch measured slower: a thousand waiting CTAs' tiles overflow L2.)  Replaces ~6 launches per step (each a handful of CTAs) by a single
-// launch whose critical path is the chain of ops through the rows.
-__global__ void __launch_bounds__(256) k_qr_solve_dag(const double* __restrict__ A, Geo g, int ib,
-                                                      const double* __restrict__ Tg,
-                                                      const double* __restrict__ Ttt,
-                                                      const int* __restrict__ ops,
-                                                      int* __restrict__ done, double* x) {
-  __shared__ double red[8][33];
-  __shared__ double Uv[32];
-  const int* op = ops + 6 * blockIdx.x;
-  const int kind = op[0], e = op[1], i = op[2], pe = op[3], pi = op[4], k = op[5];
-  if (threadIdx.x == 0) {
+// The op body of the DAG replay below: qr_apply_vec_body's arithmetic (same products, same
+// summation order: bit-identical x) with everything that does not depend on x taken off the
+// dependency chain -- the op's T factor (ib x nb) goes to shared memory and the first reflector
+// block's V rows to registers BEFORE the op waits for its predecessors; with one row per thread
+// (!BIG: nb <= 256) block b + 1's V rows are loaded into a second register set while block b is
+// computed; x_e(b) is loaded at the top of the block; U = T_b^T W reads W by shared-memory
+// broadcast instead of 32 dependent shuffles.  (ib = 32.)
+template <int MODE, bool BIG>
+__device__ __forceinline__ void qr_apply_vec_dag(const double* __restrict__ A, Geo g, int k, int ib,
+                                                 const double* __restrict__ Tb, int e, int i,
+                                                 double* __restrict__ x, double (*red)[33],
+                                                 double* Uv, double* Wsh, double* Ts,
+                                                 const int* done, int pe, int pi) {
+  constexpr bool TT = MODE != 0, TS = MODE == 2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int bi = g.bs(i), bk = g.cbs(k);
+  const double* V = g.tile(const_cast<double*>(A), i, k);
+  const double* T = Tb + tri_index(i, k, g.n) * (int64_t)ib * g.nb;
+  double* xi = x + g.r0(i);
+  double* xe = x + g.r0(e);
+  const int r0 = tid, r1 = tid + 256;
+  // row r of V_b with the reflector structure made explicit
+  auto loadv = [&](int i0, double (&v)[32], int r) {
+    const int sb = min(32, bk - i0);
+#pragma unroll
+    for (int l = 0; l < 32; ++l) {
+      const int c = i0 + l;
+      const double* col = V + (int64_t)c * g.lda;
+      if (TT)
+        v[l] = (l < sb && r < bi && (TS || r <= c)) ? col[r] : 0.0;
+      else
+        v[l] = (l < sb && r < bi && r >= c) ? (r == c ? 1.0 : col[r]) : 0.0;
+    }
+  };
+  // ---- independent of x: T (column c at Ts[33 c ..], conflict-free) and V_0
+  for (int o = tid; o < bk * 32; o += 256) Ts[(o >> 5) * 33 + (o & 31)] = T[o];
+  double v0[32], v1[BIG ? 32 : 1];
+  loadv(0, v0, r0);
+  if constexpr (BIG) loadv(0, reinterpret_cast<double(&)[32]>(v1), r1);
+  // ---- wait for the previous op on each of the op's rows
+  if (tid == 0) {
     unsigned ns = 32;
     auto wait = [&](int q) {
       if (q < 0) return;
@@ -161,12 +186,105 @@ __global__ void __launch_bounds__(256) k_qr_solve_dag(const double* __restrict__
     wait(pi);
   }
   __syncthreads();
+  // (x is written by other CTAs of the same launch -- read it through L2 only)
+  double x0 = r0 < bi ? __ldcg(xi + r0) : 0.0, x1 = (BIG && r1 < bi) ? __ldcg(xi + r1) : 0.0;
+  for (int i0 = 0; i0 < bk; i0 += 32) {
+    const int sb = min(32, bk - i0);
+    if (!TT && i0 >= bi) break;
+    const bool more = i0 + 32 < bk && (TT || i0 + 32 < bi);
+    double vn[BIG ? 1 : 32];
+    if constexpr (!BIG) {
+      if (more) loadv(i0 + 32, reinterpret_cast<double(&)[32]>(vn), r0);
+    }
+    const double xo = (TT && warp == 0 && lane < sb) ? __ldcg(xe + i0 + lane) : 0.0;  // x_e(b)
+    // W = [x_e(b) +] V_b^T x
+    double p[32];
+#pragma unroll
+    for (int l = 0; l < 32; ++l) {
+      if constexpr (BIG)
+        p[l] = v0[l] * x0 + v1[l] * x1;
+      else
+        p[l] = v0[l] * x0;
+    }
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+      const bool upper = (lane & s) != 0;
+#pragma unroll
+      for (int c = 0; c < s; ++c) {
+        const double send = upper ? p[c] : p[c + s];
+        const double keep = upper ? p[c + s] : p[c];
+        p[c] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+      }
+    }
+    red[warp][lane] = p[0];
+    __syncthreads();
+    if (warp == 0) {
+      double w = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) w += red[q][lane];
+      if (TT) w += xo;
+      Wsh[lane] = w;
+      __syncwarp();
+      // U = T_b^T W: u_l = sum_{q <= l} T(q, l) W_q
+      double u = 0.0;
+      const double* tc = Ts + (i0 + lane) * 33;
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        if (q <= lane && lane < sb) u += tc[q] * Wsh[q];
+      Uv[lane] = u;
+      if (TT && lane < sb) xe[i0 + lane] = xo - u;  // x_e(b) -= U
+    }
+    __syncthreads();
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int l = 0; l < 32; ++l) {
+      a0 += v0[l] * Uv[l];
+      if constexpr (BIG) a1 += v1[l] * Uv[l];
+    }
+    x0 -= a0;
+    if constexpr (BIG) x1 -= a1;
+    // (no barrier here: red / Uv / Wsh are rewritten only after the next block's first barrier,
+    // which every thread reaches after this block's reads)
+    if (more) {
+      if constexpr (BIG) {
+        loadv(i0 + 32, v0, r0);
+        loadv(i0 + 32, reinterpret_cast<double(&)[32]>(v1), r1);
+      } else {
+#pragma unroll
+        for (int l = 0; l < 32; ++l) v0[l] = vn[l];
+      }
+    }
+  }
+  if (r0 < bi) xi[r0] = x0;
+  if (BIG && r1 < bi) xi[r1] = x1;
+}
+
+// The Q^T x replay of a run of consecutive QR steps as ONE launch: one CTA per op (6 ints: kind 0
+// GEQRT rows / 1 TS pair / 2 TT pair, rows e and i, the previous op on row e and on row i -- across
+// steps --, the step k), listed in dependency order; an op waits for its predecessors' completion
+// flags (acquire), applies its reflectors to x_e / x_i and releases its own flag.  (Prefetching
+// every resident op's V tile at launch measured slower: a thousand waiting CTAs' tiles overflow L2;
+// the op body loads only its T factor and first reflector block ahead of the wait.)  Replaces ~6
+// launches per step (each a handful of CTAs) by a single launch whose critical path is the chain of
+// ops through the rows.
+template <bool BIG>
+__global__ void __launch_bounds__(256) k_qr_solve_dag(const double* __restrict__ A, Geo g, int ib,
+                                                      const double* __restrict__ Tg,
+                                                      const double* __restrict__ Ttt,
+                                                      const int* __restrict__ ops,
+                                                      int* __restrict__ done, double* x) {
+  __shared__ double red[8][33];
+  __shared__ double Uv[32];
+  __shared__ double Wsh[32];
+  extern __shared__ __align__(16) double Ts[];  // 33 x nb: the op's T factor
+  const int* op = ops + 6 * blockIdx.x;
+  const int kind = op[0], e = op[1], i = op[2], pe = op[3], pi = op[4], k = op[5];
   if (kind == 0)
-    qr_apply_vec_body<0, true>(A, g, k, ib, Tg, 0, i, x, red, Uv);
+    qr_apply_vec_dag<0, BIG>(A, g, k, ib, Tg, 0, i, x, red, Uv, Wsh, Ts, done, pe, pi);
   else if (kind == 1)
-    qr_apply_vec_body<2, true>(A, g, k, ib, Ttt, e, i, x, red, Uv);
+    qr_apply_vec_dag<2, BIG>(A, g, k, ib, Ttt, e, i, x, red, Uv, Wsh, Ts, done, pe, pi);
   else
-    qr_apply_vec_body<1, true>(A, g, k, ib, Ttt, e, i, x, red, Uv);
+    qr_apply_vec_dag<1, BIG>(A, g, k, ib, Ttt, e, i, x, red, Uv, Wsh, Ts, done, pe, pi);
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -181,7 +299,18 @@ void launch_qr_solve_dag(const double* A, Geo g, int ib, const double* Tg, const
   if (nops <= 0) return;
   cudaMemsetAsync(done, 0, sizeof(int) * 32 * (size_t)nops, st);
   ::hlq::g_launches++;
-  k_qr_solve_dag<<<nops, 256, 0, st>>>(A, g, ib, Tg, Ttt, ops, done, x);
+  const size_t smem = sizeof(double) * 33 * (size_t)g.nb;
+  static unsigned long long attr = 0;
+  if (first_on_device(attr)) {
+    cudaFuncSetAttribute(k_qr_solve_dag<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(double) * 33 * HLQ_MAX_NB));
+    cudaFuncSetAttribute(k_qr_solve_dag<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(double) * 33 * HLQ_MAX_NB));
+  }
+  if (g.nb > 256)
+    k_qr_solve_dag<true><<<nops, 256, smem, st>>>(A, g, ib, Tg, Ttt, ops, done, x);
+  else
+    k_qr_solve_dag<false><<<nops, 256, smem, st>>>(A, g, ib, Tg, Ttt, ops, done, x);
 }
 
 // Apply the stored QR step k to the solve's vector x (rows 0..N-1 of base): Q_ik^T of every

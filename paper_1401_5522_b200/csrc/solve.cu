@@ -289,78 +289,100 @@ __device__ __forceinline__ void prefetch_tile_l2(const double* T, int64_t lda, i
   }
 }
 
-// ys (bi entries, shared) <- L^-1 ys, L = unit lower triangle of the tile at D (ld lda)
-__device__ void tile_lower_unit_solve(const double* __restrict__ D, int64_t lda, int bi, double* ys,
-                                      int tid) {
-  const int lane = tid & 31, warp = tid >> 5;
-  for (int base = 0; base < bi; base += 32) {
-    if (warp == 0) {
-      const int r = base + lane;
-      double lv[32];
+// Diagonal-tile triangular solves of the persistent passes, latency-pipelined (the n tile solves
+// of a pass are its sequential chain; every load below is independent of the right-hand side):
+//   * two chain warps alternate over the 32 x 32 diagonal blocks (warp t & 1 runs the t-th block's
+//     register/shuffle substitution) and load their next block's coefficients right after a chain,
+//     so they land while the other warp chains; the first two blocks are loaded by preload(), which
+//     the finisher calls BEFORE it waits for the other chunks' partial sums;
+//   * warps 2..7 own the rows the block's solution updates and load their 32 coefficients before
+//     the barrier that ends the chain, so after it the update is 32 FMAs from registers.
+// The arithmetic (per-row FMA order, reciprocal pivots) is that of the unpipelined solves.
+template <bool LOWER>
+struct TileSolve {
+  double reg[32];  // chain warps: the block's triangle coefficients; update warps: a row's 32
+  double rd;       // upper: 1 / U_rr of the chain lane's row
+  // block index of chain step t
+  __device__ __forceinline__ static int blk(int t, int nblk) { return LOWER ? t : nblk - 1 - t; }
+  __device__ __forceinline__ void load_chain(const double* __restrict__ D, int64_t lda, int bi,
+                                             int base, int lane) {
+    const int r = base + lane;
 #pragma unroll
-      for (int cc = 0; cc < 32; ++cc)
-        lv[cc] = (cc < lane && r < bi) ? __ldg(D + (int64_t)(base + cc) * lda + r) : 0.0;
-      double v = r < bi ? ys[r] : 0.0;
-#pragma unroll
-      for (int cc = 0; cc < 32; ++cc) {
-        const double xc = __shfl_sync(0xffffffffu, v, cc);
-        if (lane > cc) v = fma(-lv[cc], xc, v);
-      }
-      if (r < bi) ys[r] = v;
+    for (int cc = 0; cc < 32; ++cc) {
+      const bool ok = LOWER ? (cc < lane && r < bi) : (cc > lane && base + cc < bi);
+      reg[cc] = ok ? __ldg(D + (int64_t)(base + cc) * lda + r) : 0.0;
     }
-    __syncthreads();
-    const int pw = min(32, bi - base);
-    for (int r = base + 32 + tid; r < bi; r += PS_T) {
-      double l[32];  // all 32 loads in flight before the dependent sum
-#pragma unroll
-      for (int cc = 0; cc < 32; ++cc) l[cc] = cc < pw ? __ldg(D + (int64_t)(base + cc) * lda + r) : 0.0;
-      double a = 0.0;
-#pragma unroll
-      for (int cc = 0; cc < 32; ++cc) a = fma(l[cc], cc < pw ? ys[base + cc] : 0.0, a);
-      ys[r] -= a;
-    }
-    __syncthreads();
-  }
-}
-
-// ys <- U^-1 ys, U = upper triangle (non-unit) of the tile at D (ld lda)
-__device__ void tile_upper_solve(const double* __restrict__ D, int64_t lda, int bi, double* ys,
-                                 int tid) {
-  const int lane = tid & 31, warp = tid >> 5;
-  for (int base = (bi - 1) / 32 * 32; base >= 0; base -= 32) {
-    if (warp == 0) {
-      const int r = base + lane;
-      double lv[32];
-#pragma unroll
-      for (int cc = 0; cc < 32; ++cc)
-        lv[cc] = (cc > lane && base + cc < bi) ? __ldg(D + (int64_t)(base + cc) * lda + r) : 0.0;
-      // 1 / U_rr for every lane at once: the substitution chain then multiplies instead of
-      // dividing (32 dependent divisions were most of the diagonal tile's latency)
+    if (!LOWER) {
+      // 1 / U_rr for every lane at once: the substitution chain multiplies instead of dividing
       const double d = r < bi ? __ldg(D + (int64_t)r * lda + r) : 1.0;
-      const double rd = 1.0 / d;
-      double v = r < bi ? ys[r] : 0.0;
-#pragma unroll
-      for (int cc = 31; cc >= 0; --cc) {
-        if (lane == cc) v = v * rd;
-        const double xc = __shfl_sync(0xffffffffu, v, cc);
-        if (lane < cc) v = fma(-lv[cc], xc, v);
-      }
-      if (r < bi) ys[r] = v;
+      rd = 1.0 / d;
     }
-    __syncthreads();
-    const int pw = min(32, bi - base);
-    for (int r = tid; r < base; r += PS_T) {
-      double l[32];
-#pragma unroll
-      for (int cc = 0; cc < 32; ++cc) l[cc] = cc < pw ? __ldg(D + (int64_t)(base + cc) * lda + r) : 0.0;
-      double a = 0.0;
-#pragma unroll
-      for (int cc = 0; cc < 32; ++cc) a = fma(l[cc], cc < pw ? ys[base + cc] : 0.0, a);
-      ys[r] -= a;
-    }
-    __syncthreads();
   }
-}
+  __device__ __forceinline__ void preload(const double* __restrict__ D, int64_t lda, int bi,
+                                          int tid) {
+    const int lane = tid & 31, warp = tid >> 5, nblk = (bi + 31) / 32;
+    if (warp < 2 && warp < nblk) load_chain(D, lda, bi, 32 * blk(warp, nblk), lane);
+  }
+  // ys (bi entries, shared) <- L^-1 ys (unit lower) or U^-1 ys (upper, non-unit); preload() first
+  __device__ __forceinline__ void run(const double* __restrict__ D, int64_t lda, int bi,
+                                      double* ys, int tid) {
+    const int lane = tid & 31, warp = tid >> 5, nblk = (bi + 31) / 32;
+    constexpr int UT = PS_T - 64;  // update threads (warps 2..)
+    const int uidx = tid - 64;
+    for (int t = 0; t < nblk; ++t) {
+      const int base = 32 * blk(t, nblk);
+      const int pw = min(32, bi - base);
+      // rows this block's solution updates: below it (lower) / above it (upper)
+      const int ulo = LOWER ? base + 32 : 0, uhi = LOWER ? bi : base;
+      const int r0 = ulo + uidx;
+      const bool upd = warp >= 2 && r0 < uhi;
+      if (upd) {
+#pragma unroll
+        for (int cc = 0; cc < 32; ++cc)
+          reg[cc] = cc < pw ? __ldg(D + (int64_t)(base + cc) * lda + r0) : 0.0;
+      }
+      if (warp == (t & 1)) {
+        const int r = base + lane;
+        double v = r < bi ? ys[r] : 0.0;
+        if (LOWER) {
+#pragma unroll
+          for (int cc = 0; cc < 32; ++cc) {
+            const double xc = __shfl_sync(0xffffffffu, v, cc);
+            if (lane > cc) v = fma(-reg[cc], xc, v);
+          }
+        } else {
+#pragma unroll
+          for (int cc = 31; cc >= 0; --cc) {
+            if (lane == cc) v = v * rd;
+            const double xc = __shfl_sync(0xffffffffu, v, cc);
+            if (lane < cc) v = fma(-reg[cc], xc, v);
+          }
+        }
+        if (r < bi) ys[r] = v;
+        if (t + 2 < nblk) load_chain(D, lda, bi, 32 * blk(t + 2, nblk), lane);
+      }
+      __syncthreads();
+      if (warp >= 2) {
+        if (upd) {
+          double a = 0.0;
+#pragma unroll
+          for (int cc = 0; cc < 32; ++cc) a = fma(reg[cc], cc < pw ? ys[base + cc] : 0.0, a);
+          ys[r0] -= a;
+        }
+        for (int r = r0 + UT; r < uhi; r += UT) {  // (more than UT rows left: nb > 256 or block 0)
+#pragma unroll
+          for (int cc = 0; cc < 32; ++cc)
+            reg[cc] = cc < pw ? __ldg(D + (int64_t)(base + cc) * lda + r) : 0.0;
+          double a = 0.0;
+#pragma unroll
+          for (int cc = 0; cc < 32; ++cc) a = fma(reg[cc], cc < pw ? ys[base + cc] : 0.0, a);
+          ys[r] -= a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+};
 
 // FWD: forward pass of the LU steps [ka, kb) over block rows i >= ka (x_i -= sum_j L_ij x_j, then
 // x_i <- L_ii^-1 P_i x_i for i < kb).  BACK: back substitution over all block rows
@@ -446,31 +468,54 @@ __global__ void __launch_bounds__(PS_T) k_solve_rows(const double* __restrict__ 
   // finisher: r_i = x_i - (sum of the chunk partials in chunk order + own); thread cc waits for
   // chunk cc's flag (all polls in flight at once: a sequential poll of up to n/G already-set flags
   // cost an L2 round trip each on the critical path)
+  const bool solves = !(FWD && i >= kb);
+  const double* D = A + g.r0(i) * g.lda + g.r0(i);
+  TileSolve<FWD> ts;
+  int pr[(HLQ_MAX_NB + PS_T - 1) / PS_T];  // row r of P_i x = x[perm[r]] (forward pass)
+  if (solves) {
+    // everything the diagonal solve loads that does not depend on x, before the waits below
+    ts.preload(D, g.lda, bi, tid);
+    if (FWD) {
+      const int* perm = perm_all + (int64_t)i * nb;
+#pragma unroll
+      for (int u = 0; u < (HLQ_MAX_NB + PS_T - 1) / PS_T; ++u)
+        pr[u] = (tid + u * PS_T < bi) ? __ldg(perm + tid + u * PS_T) : 0;
+    }
+  }
   for (int cc = tid; cc < c; cc += PS_T) wait_flag(pflag + ((int64_t)i * cmax + cc) * kFlagStride, 1);
   __syncthreads();
   double* xi = x + g.r0(i);
   for (int r = tid; r < bi; r += PS_T) {
+    // the partial sums in chunk order, eight loads in flight at a time (a load per dependent add
+    // cost an L2 round trip per chunk on the critical path of every block row)
+    const double* pp = part + (int64_t)i * cmax * nb + r;
     double sum = 0.0;
-    for (int cc = 0; cc < c; ++cc) sum += __ldcg(part + ((int64_t)i * cmax + cc) * nb + r);
+    int cc = 0;
+    for (; cc + 8 <= c; cc += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(pp + (int64_t)(cc + u) * nb);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) sum += v[u];
+    }
+    for (; cc < c; ++cc) sum += __ldcg(pp + (int64_t)cc * nb);
     sum += red[0][r] + red[1][r];
     xs[r] = __ldcg(xi + r) - sum;
   }
   __syncthreads();
-  if (FWD && i >= kb) {  // a row below the run: only the update
+  if (!solves) {  // a row below the run: only the update
     for (int r = tid; r < bi; r += PS_T) xi[r] = xs[r];
     return;
   }
-  const double* D = A + g.r0(i) * g.lda + g.r0(i);
   if (FWD) {
-    const int* perm = perm_all + (int64_t)i * nb;  // row r of P_i x = x[perm[r]]
-    for (int r = tid; r < bi; r += PS_T) ys[r] = xs[perm[r]];
-    __syncthreads();
-    tile_lower_unit_solve(D, g.lda, bi, ys, tid);
+#pragma unroll
+    for (int u = 0; u < (HLQ_MAX_NB + PS_T - 1) / PS_T; ++u)
+      if (tid + u * PS_T < bi) ys[tid + u * PS_T] = xs[pr[u]];
   } else {
     for (int r = tid; r < bi; r += PS_T) ys[r] = xs[r];
-    __syncthreads();
-    tile_upper_solve(D, g.lda, bi, ys, tid);
   }
+  __syncthreads();
+  ts.run(D, g.lda, bi, ys, tid);
   for (int r = tid; r < bi; r += PS_T) __stcg(xi + r, ys[r]);
   __threadfence();
   __syncthreads();

@@ -5,7 +5,8 @@ copy of the panel (its kernels run while d_k is undecided and exit once it is LU
 (default) and the cp.async kernel (HLQ_DGEMM_TMA=0) accumulate every element's K products in the
 same order; the QR panel as one dependency-DAG launch (default) or level by level (HLQ_QR_DAG=0)
 runs the same kernels' arithmetic, and so does the solve's Q^T replay as one DAG launch per run of
-QR steps (default) or step by step (HLQ_QR_SOLVE_DAG=0): all must give bit-identical factors and x,
+QR steps (default) or step by step (HLQ_QR_SOLVE_DAG=0), and the lookahead column's update on the
+panel stream (default) or in front of the rest on the update stream (HLQ_LA_SP=0): all must give bit-identical factors and x,
 decisions and QR-step T factors -- under A1 and A2, Max and MUMPS, one and two QR-tree domains.  The environment is read once per process, so each variant
 runs in its own interpreter."""
 import os
@@ -62,7 +63,7 @@ def _run(env_extra, path):
 
 @pytest.mark.parametrize("env", [{"HLQ_SPEC_QR": "0"}, {"HLQ_DGEMM_TMA": "0"},
                                  {"HLQ_TMA_CONS": "4"}, {"HLQ_QR_DAG": "0"},
-                                 {"HLQ_QR_SOLVE_DAG": "0"}])
+                                 {"HLQ_QR_SOLVE_DAG": "0"}, {"HLQ_LA_SP": "0"}])
 def test_variant_is_bit_identical(tmp_path, env):
     base = _run({}, str(tmp_path / "base.npz"))
     var = _run(env, str(tmp_path / "var.npz"))
