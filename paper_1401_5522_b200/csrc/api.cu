@@ -346,8 +346,13 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   const int tsa = opt.tree == HLQ_TREE_HQR ? opt.ts_group : 0;
   std::vector<StepPlanHost> plans(n);
   size_t npairs = 0, nts = 0, nheads = 0, noff = 0;
+  size_t qs_ops = 0;  // ops of the solve's Q^T replay DAG if every step is QR (hlq_solve)
   for (int k = 0; k < n; ++k) {
     plan_step(k, n, f->D, tsa, plans[k]);
+    qs_ops += (tsa >= 1 && plans[k].ts_off.size() > 1)
+                  ? plans[k].heads.size() + plans[k].ts_pairs.size()
+                  : (size_t)(n - k);
+    for (auto& lv : plans[k].levels) qs_ops += lv.size();
     for (auto& lv : plans[k].levels) npairs += lv.size();
     nts += plans[k].ts_pairs.size();
     nheads += plans[k].heads.size();
@@ -411,6 +416,10 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   const size_t solve_cap = (size_t)2 * n * scmax + 1;
   size_t oSv = take(solve_ws_bytes(n, nb, scmax, solve_cap));
   size_t oDag = take(sizeof(int) * (dag_total + 1)), oDagP = take(sizeof(int) * (dag_max + 1));
+  // the solve's DAG: 6 ints per op + one 128-byte completion flag per op (no allocation, and so
+  // no device synchronisation, inside the first hlq_solve)
+  const size_t qs_tab = align_up(sizeof(int) * 6 * (qs_ops + 1), 256);
+  size_t oQs = take(qs_tab + sizeof(int) * 32 * (qs_ops + 1));
   f->ws_bytes = off;
   f->dev = cur_device();
   f->ws_block = cache_get(0, off);
@@ -451,6 +460,8 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
   w.dom_idx = (int*)(base + oDi);
   w.dom_counter = (unsigned int*)(base + oDc);
   f->solve_ws_in = base + oSv;
+  f->qsolve_ws_in = base + oQs;
+  f->qsolve_cap = qs_ops;
   f->tma_maps = make_tma_maps(A, N, lda, nb);
   w.tma_maps = f->tma_maps;
   f->solve_cap = solve_cap;
@@ -898,14 +909,20 @@ int hlq_solve(hlq_factors_t f, const double* b, double* x) {
       k = kb;
     }
     if (!ops.empty()) {
-      const size_t ob = align_up(sizeof(int) * ops.size(), 256);
-      if ((rc = cuda_err(cudaMalloc(&f->qsolve_block, ob + sizeof(int) * 32 * maxops)))) {
-        f->qsolve_block = nullptr;
-        f->qsolve_runs.clear();
-        return rc;
+      size_t ob = align_up(sizeof(int) * ops.size(), 256);
+      if (ops.size() / 6 <= f->qsolve_cap && f->qsolve_ws_in) {
+        f->qsolve_ops = f->qsolve_ws_in;  // the factorization's workspace piece
+        ob = align_up(sizeof(int) * 6 * (f->qsolve_cap + 1), 256);
+      } else {
+        if ((rc = cuda_err(cudaMalloc(&f->qsolve_block, ob + sizeof(int) * 32 * maxops)))) {
+          f->qsolve_block = nullptr;
+          f->qsolve_runs.clear();
+          return rc;
+        }
+        f->qsolve_ops = f->qsolve_block;
       }
-      f->qsolve_done = (int*)((char*)f->qsolve_block + ob);
-      if ((rc = cuda_err(cudaMemcpyAsync(f->qsolve_block, ops.data(), sizeof(int) * ops.size(),
+      f->qsolve_done = (int*)((char*)f->qsolve_ops + ob);
+      if ((rc = cuda_err(cudaMemcpyAsync(f->qsolve_ops, ops.data(), sizeof(int) * ops.size(),
                                          cudaMemcpyHostToDevice, st))))
         return rc;
     }
@@ -922,7 +939,7 @@ int hlq_solve(hlq_factors_t f, const double* b, double* x) {
     if (qrun < f->qsolve_runs.size() && f->qsolve_runs[qrun][0] == k) {
       const auto& r = f->qsolve_runs[qrun++];
       launch_qr_solve_dag(f->A, g, f->ib, f->w.Tg, f->w.Ttt,
-                          (const int*)f->qsolve_block + (size_t)6 * r[2], r[3], f->qsolve_done, x,
+                          (const int*)f->qsolve_ops + (size_t)6 * r[2], r[3], f->qsolve_done, x,
                           st);
       k = r[1] - 1;
       continue;

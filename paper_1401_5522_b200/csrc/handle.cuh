@@ -112,7 +112,10 @@ struct hlq_factors_s {
   // the solve's Q^T replay of runs of consecutive QR steps as DAG launches (built at the first
   // hlq_solve): device ops (6 ints each) + completion flags in qsolve_block, per run {ka, kb, off,
   // count}
-  void* qsolve_block = nullptr;
+  void* qsolve_block = nullptr;   // own allocation (only when the workspace piece is too small)
+  void* qsolve_ops = nullptr;     // the op table in use (workspace piece or qsolve_block)
+  void* qsolve_ws_in = nullptr;   // the factorization workspace's piece: ops + flags
+  size_t qsolve_cap = 0;          // ops it holds (every step QR)
   int* qsolve_done = nullptr;
   std::vector<std::array<int, 4>> qsolve_runs;
   bool qsolve_built = false;

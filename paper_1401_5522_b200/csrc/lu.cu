@@ -27,14 +27,27 @@ __global__ void k_lu_commit(double* __restrict__ A, Geo g, int k, const double* 
     int c = idx / bk, r = idx - c * bk;
     Akk[(int64_t)c * g.lda + r] = W[(int64_t)c * g.nb + r];
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    for (int r = 0; r < bk; ++r) perm[r] = r;
-    for (int c = 0; c < bk; ++c) {
-      int p = ipiv_ws[c];
-      ipiv[(int64_t)k * g.nb + c] = p;
-      int t = perm[c];
-      perm[c] = perm[p];
-      perm[p] = t;
+  if (blockIdx.x == 0) {
+    // the bk sequential swaps composed in shared memory by one thread (the composition is a serial
+    // chain of dependent loads: from global memory it was most of this kernel's 51 us)
+    __shared__ int sperm[HLQ_MAX_NB], spiv[HLQ_MAX_NB];
+    for (int r = threadIdx.x; r < bk; r += blockDim.x) {
+      sperm[r] = r;
+      spiv[r] = ipiv_ws[r];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int c = 0; c < bk; ++c) {
+        const int p = spiv[c];
+        const int t = sperm[c];
+        sperm[c] = sperm[p];
+        sperm[p] = t;
+      }
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < bk; r += blockDim.x) {
+      perm[r] = sperm[r];
+      ipiv[(int64_t)k * g.nb + r] = spiv[r];
     }
   }
 }

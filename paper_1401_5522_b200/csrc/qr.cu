@@ -267,7 +267,7 @@ __device__ __forceinline__ void qr_apply_vec_dag(const double* __restrict__ A, G
 // the op body loads only its T factor and first reflector block ahead of the wait.)  Replaces ~6
 // launches per step (each a handful of CTAs) by a single launch whose critical path is the chain of
 // ops through the rows.
-template <bool BIG>
+template <bool BIG, bool OLD = false>
 __global__ void __launch_bounds__(256) k_qr_solve_dag(const double* __restrict__ A, Geo g, int ib,
                                                       const double* __restrict__ Tg,
                                                       const double* __restrict__ Ttt,
@@ -279,12 +279,37 @@ __global__ void __launch_bounds__(256) k_qr_solve_dag(const double* __restrict__
   extern __shared__ __align__(16) double Ts[];  // 33 x nb: the op's T factor
   const int* op = ops + 6 * blockIdx.x;
   const int kind = op[0], e = op[1], i = op[2], pe = op[3], pi = op[4], k = op[5];
-  if (kind == 0)
-    qr_apply_vec_dag<0, BIG>(A, g, k, ib, Tg, 0, i, x, red, Uv, Wsh, Ts, done, pe, pi);
-  else if (kind == 1)
-    qr_apply_vec_dag<2, BIG>(A, g, k, ib, Ttt, e, i, x, red, Uv, Wsh, Ts, done, pe, pi);
-  else
-    qr_apply_vec_dag<1, BIG>(A, g, k, ib, Ttt, e, i, x, red, Uv, Wsh, Ts, done, pe, pi);
+  if constexpr (OLD) {  // HLQ_QR_SOLVE_DAG_BODY=0: wait first, then the step-by-step kernels' body
+    if (threadIdx.x == 0) {
+      unsigned ns = 32;
+      auto wait = [&](int q) {
+        if (q < 0) return;
+        for (;;) {
+          int v;
+          asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(done + 32 * q) : "memory");
+          if (v) break;
+          __nanosleep(ns);
+          if (ns < 256) ns <<= 1;
+        }
+      };
+      wait(pe);
+      wait(pi);
+    }
+    __syncthreads();
+    if (kind == 0)
+      qr_apply_vec_body<0, true>(A, g, k, ib, Tg, 0, i, x, red, Uv);
+    else if (kind == 1)
+      qr_apply_vec_body<2, true>(A, g, k, ib, Ttt, e, i, x, red, Uv);
+    else
+      qr_apply_vec_body<1, true>(A, g, k, ib, Ttt, e, i, x, red, Uv);
+  } else {
+    if (kind == 0)
+      qr_apply_vec_dag<0, BIG>(A, g, k, ib, Tg, 0, i, x, red, Uv, Wsh, Ts, done, pe, pi);
+    else if (kind == 1)
+      qr_apply_vec_dag<2, BIG>(A, g, k, ib, Ttt, e, i, x, red, Uv, Wsh, Ts, done, pe, pi);
+    else
+      qr_apply_vec_dag<1, BIG>(A, g, k, ib, Ttt, e, i, x, red, Uv, Wsh, Ts, done, pe, pi);
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -307,7 +332,11 @@ void launch_qr_solve_dag(const double* A, Geo g, int ib, const double* Tg, const
     cudaFuncSetAttribute(k_qr_solve_dag<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(sizeof(double) * 33 * HLQ_MAX_NB));
   }
-  if (g.nb > 256)
+  static int body = -1;
+  if (body < 0) body = getenv("HLQ_QR_SOLVE_DAG_BODY") ? atoi(getenv("HLQ_QR_SOLVE_DAG_BODY")) : 1;
+  if (body == 0)
+    k_qr_solve_dag<true, true><<<nops, 256, 0, st>>>(A, g, ib, Tg, Ttt, ops, done, x);
+  else if (g.nb > 256)
     k_qr_solve_dag<true><<<nops, 256, smem, st>>>(A, g, ib, Tg, Ttt, ops, done, x);
   else
     k_qr_solve_dag<false><<<nops, 256, smem, st>>>(A, g, ib, Tg, Ttt, ops, done, x);
