@@ -541,24 +541,8 @@ bool launch_qr_update3(const double* A, Geo g, int k, const double* T, const int
   // 16-byte V copies need an even leading dimension, a 16-byte aligned matrix and even tile heights
   const bool v16 = ((g.lda & 1) == 0) && ((((uintptr_t)A) & 15) == 0) && ((g.N & 1) == 0) &&
                    ((g.nb & 1) == 0) && ((ldc & 1) == 0) && ((((uintptr_t)base) & 15) == 0);
-  // narrow launches (the lookahead column: one tile column, a few hundred CTAs on the critical
-  // path of the next panel): 16-column slabs with 4 row groups (RQ = 4, NCG = 1) -- twice the CTAs,
-  // each warp a quarter of the chain of DMMAs, so a CTA finishes in about half the time
-  // (HLQ_QR_NARROW=0: the wide shape everywhere)
-  static int narrow_env = -1;
-  if (narrow_env < 0) narrow_env = getenv("HLQ_QR_NARROW") ? atoi(getenv("HLQ_QR_NARROW")) : 0;
-  const bool narrow = narrow_env != 0 && ncols <= g.nb;
 #define HLQ_L3(NBV)                                                                           \
   case NBV:                                                                                   \
-    if (narrow) {                                                                             \
-      if (!v16)                                                                               \
-        launch3<NBV, 4, 1, false>(A, g, k, T, pairs, npairs, mode, list, base, ldc, ncols, dec, \
-                                  st, gmax);                                                  \
-      else                                                                                    \
-        launch3<NBV, 4, 1, true>(A, g, k, T, pairs, npairs, mode, list, base, ldc, ncols, dec,  \
-                                 st, gmax);                                                   \
-      return true;                                                                            \
-    }                                                                                         \
     if (!v16)                                                                                 \
       launch3<NBV, 2, 2, false>(A, g, k, T, pairs, npairs, mode, list, base, ldc, ncols, dec, st, \
                                 gmax);                                                        \
