@@ -748,3 +748,22 @@ def test_random_criterion():
     Z[0, 0] = 0.0  # exact zero pivot in the first tile (ledger 7): QR whatever the draw
     Z[1, 0] = 0.0
     assert O.hybrid_factor(Z, 16, O.CRIT_RANDOM, 100.0).dec[0] == O.QR
+
+
+def test_larfg_small_alpha_log_is_diagnostics_only():
+    """The oracle's reflector log (LARFG_LOG: |alpha| < ratio * ||(alpha, x)||, a Householder sign
+    decision near its discontinuity, DESIGN reading 14) records the constructed near-zero alpha and
+    changes no arithmetic."""
+    rng = np.random.default_rng(5)
+    N, nb = 96, 32
+    A = rng.standard_normal((N, N))
+    A[0, 0] = 1e-9  # the first reflector of step 0 eliminates against alpha = 1e-9
+    f0 = O.hybrid_factor(A, nb, O.CRIT_MAX, 0.0)  # alpha = 0: every step QR
+    O.LARFG_LOG = []
+    try:
+        f1 = O.hybrid_factor(A, nb, O.CRIT_MAX, 0.0)
+        log = list(O.LARFG_LOG)
+    finally:
+        O.LARFG_LOG = None
+    assert np.array_equal(f0.A, f1.A)
+    assert any(k == 0 and al == 1e-9 and abs(al) < 1e-6 * nr for k, al, nr in log)
