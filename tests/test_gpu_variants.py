@@ -63,7 +63,8 @@ def _run(env_extra, path):
 
 @pytest.mark.parametrize("env", [{"HLQ_SPEC_QR": "0"}, {"HLQ_DGEMM_TMA": "0"},
                                  {"HLQ_TMA_CONS": "4"}, {"HLQ_QR_DAG": "0"},
-                                 {"HLQ_QR_SOLVE_DAG": "0"}, {"HLQ_LA_SP": "0"}])
+                                 {"HLQ_QR_SOLVE_DAG": "0"}, {"HLQ_QR_SOLVE_DAG_BODY": "0"},
+                                 {"HLQ_LA_SP": "0"}])
 def test_variant_is_bit_identical(tmp_path, env):
     base = _run({}, str(tmp_path / "base.npz"))
     var = _run(env, str(tmp_path / "var.npz"))

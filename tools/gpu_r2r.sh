@@ -1,11 +1,7 @@
-# QR update: CTA dephasing experiment (HLQ_QR_DEPHASE ns) on C3 all-QR hqr4 and C2.
+# Last job of the round: ncu evidence at the final kernels (tools/gpu_ncu_r2b.sh), then C5 at full size.
 set -u
+timeout 900 python -m pytest tests/test_gpu_variants.py -m gpu -q -p no:cacheprovider > gpurun_out/pytest_variants_final.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_variants_final.log
+bash tools/gpu_ncu_r2b.sh
 O=gpurun_out/r2r
 mkdir -p $O
-B="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
-for d in 0 250 500 1000; do
-  HLQ_QR_DEPHASE=$d timeout 900 $B --fqr 1.0 --tree hqr4 > $O/c3f1_hqr4_d$d.log 2>&1
-done
-for d in 0 500; do
-  HLQ_QR_DEPHASE=$d timeout 900 $B --config C2 --criterion max --alpha 1 --tree hqr4 > $O/c2_hqr4_d$d.log 2>&1
-done
+timeout 1800 python bench.py --config C5 --criterion max --alpha 1 --domains 2 --tree hqr4 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/c5_full_hqr4.log 2>&1
