@@ -444,11 +444,16 @@ LARFG_LOG_RATIO = 1e-6
 LARFG_STEP = -1
 
 
-def larfg(alpha: float, x: np.ndarray):
+def larfg(alpha: float, x: np.ndarray, rev: bool = False):
     """H = I - tau [1; v][1; v]^T with H [alpha; x] = [beta; 0].  Returns (beta, tau, v).
     beta = -sign(alpha)*||(alpha, x)||_2 (sign(0)=+), tau = (beta-alpha)/beta, v = x/(alpha-beta);
-    x == 0 -> tau = 0, H = I."""
-    ssq = float(np.dot(x, x)) if x.size else 0.0
+    x == 0 -> tau = 0, H = I.  rev (noise-floor variant 2 only): the sum of squares taken in
+    reverse order -- the same mathematics, another rounding of the norm."""
+    if rev:
+        xr = x[::-1]
+        ssq = float(np.dot(xr, xr)) if x.size else 0.0
+    else:
+        ssq = float(np.dot(x, x)) if x.size else 0.0
     if ssq == 0.0:
         return alpha, 0.0, np.zeros_like(x)
     nrm = math.sqrt(alpha * alpha + ssq)
@@ -460,7 +465,7 @@ def larfg(alpha: float, x: np.ndarray):
     return beta, tau, v
 
 
-def geqrt(Tile: np.ndarray, ib: int):
+def geqrt(Tile: np.ndarray, ib: int, rev: bool = False):
     """GEQRT: Householder QR of one tile, V (unit lower, below the diagonal) and R in place,
     T stored as ib x b (block bi occupies columns bi*ib .. , its sb x sb upper triangle).
     Returns the T array.  Blocked as PLASMA: per ib-panel, dgeqr2 + dlarft, then dlarfb on the rest."""
@@ -471,7 +476,7 @@ def geqrt(Tile: np.ndarray, ib: int):
         for j in range(i0, i0 + sb):
             if j >= mrow:
                 break  # wide ragged tile: reflectors j >= mrow are the identity (tau = 0, T = 0)
-            beta, tau, v = larfg(Tile[j, j], Tile[j + 1:, j].copy())
+            beta, tau, v = larfg(Tile[j, j], Tile[j + 1:, j].copy(), rev)
             Tile[j, j] = beta
             Tile[j + 1:, j] = v
             # apply H_j to the remaining columns of the panel
@@ -532,7 +537,7 @@ def unmqr(Vtile: np.ndarray, T: np.ndarray, ib: int, C: np.ndarray, variant: int
         C[i0:, :] = Cb - _fmm(V, _fmm(Tb.T, _vtc(V, Cb, variant)))
 
 
-def tsqrt(R: np.ndarray, A2: np.ndarray, ib: int, tt: bool = False):
+def tsqrt(R: np.ndarray, A2: np.ndarray, ib: int, tt: bool = False, rev: bool = False):
     """TSQRT: QR of [R (upper b x b); A2 (m2 x b)].  R updated in place, V2 stored in A2
     (the top part of each reflector is e_j, implicit), T returned (ib x b).
     tt=True gives TTQRT: A2 is upper triangular and V2 stays upper triangular; the
@@ -546,7 +551,7 @@ def tsqrt(R: np.ndarray, A2: np.ndarray, ib: int, tt: bool = False):
     for i0 in range(0, b, ib):
         sb = min(ib, b - i0)
         for j in range(i0, i0 + sb):
-            beta, tau, v = larfg(R[j, j], A2[:, j].copy())
+            beta, tau, v = larfg(R[j, j], A2[:, j].copy(), rev)
             R[j, j] = beta
             A2[:, j] = v
             if j + 1 < i0 + sb and tau != 0.0:
@@ -752,7 +757,7 @@ def qr_step(A: np.ndarray, N: int, nb: int, k: int, D: int, ib: int,
     # GEQRT + UNMQR (Alg. 4a lines 1, 4; Alg. 4b lines 1-2, 4-5); rows are independent
     def factor_row(h):
         rh = tsl(N, nb, h)
-        return T_kk if (h == k and T_kk is not None) else geqrt(A[rh, ck], ib)
+        return T_kk if (h == k and T_kk is not None) else geqrt(A[rh, ck], ib, variant >= 2)
     for h, T in zip(geqrt_rows, _pmap(factor_row, geqrt_rows)):
         data.T_geqrt[h] = T
     _pmap(lambda hc: unmqr(A[tsl(N, nb, hc[0]), ck], data.T_geqrt[hc[0]], ib,
@@ -764,7 +769,7 @@ def qr_step(A: np.ndarray, N: int, nb: int, k: int, D: int, ib: int,
         R = A[re_, ck]
         Rv = np.triu(R)
         A2 = A[ri, ck]
-        data.T_ts[i] = tsqrt(Rv, A2, ib)
+        data.T_ts[i] = tsqrt(Rv, A2, ib, rev=variant >= 2)
         iu = np.triu_indices(R.shape[0], m=R.shape[1])
         R[iu] = Rv[iu]
         _pmap(lambda cs: tsmqr(A2, data.T_ts[i], ib, A[re_, cs], A[ri, cs], variant=variant),
@@ -775,7 +780,7 @@ def qr_step(A: np.ndarray, N: int, nb: int, k: int, D: int, ib: int,
         re_, ri = tsl(N, nb, e), tsl(N, nb, i)
         R = A[re_, ck]
         Rv = np.triu(R)
-        T = tsqrt(Rv, A[ri, ck], ib, tt=True)
+        T = tsqrt(Rv, A[ri, ck], ib, tt=True, rev=variant >= 2)
         iu = np.triu_indices(R.shape[0], m=R.shape[1])
         R[iu] = Rv[iu]
         return T
@@ -837,7 +842,9 @@ def hybrid_factor(A_in: np.ndarray, nb: int, crit: int = CRIT_MAX, alpha: float 
     Q_kk^T, a QR step continues from that factorization).
     pivot_scope: "tile" (north_star, ledger 8) or "domain" (NEXT f1: the pivot search runs
     over the diagonal domain, the D-domain of the QR tree; DESIGN reading 33).
-    forced: decision vector used verbatim (C3); variant=1 sums every LU Schur update (A1, A2 and
+    forced: decision vector used verbatim (C3); variant=2 is variant 1 plus the reflector norms of
+    the QR panel kernels summed in reverse order (a rounding change inside the panel factorizations,
+    where the GPU's arithmetic also differs from the oracle's); variant=1 sums every LU Schur update (A1, A2 and
     domain steps) in reversed K-chunk order (schur_update) and every V^T C product of the QR
     trailing updates over reversed row halves (_vtc): the noise-floor run, delta_floor =
     factor_diff(variant 1, variant 0) with the decisions forced equal.
