@@ -767,3 +767,21 @@ def test_larfg_small_alpha_log_is_diagnostics_only():
         O.LARFG_LOG = None
     assert np.array_equal(f0.A, f1.A)
     assert any(k == 0 and al == 1e-9 and abs(al) < 1e-6 * nr for k, al, nr in log)
+
+
+def test_noise_floor_variant2_same_mathematics():
+    """variant = 2 (variant 1 plus the reflector norms of the QR panel kernels summed in reverse
+    order) is the same all-QR factorization up to rounding for both trees: R and V within rounding
+    noise of variant 0, not bit-identical to it nor to variant 1 (the panel rounding really
+    differs), and the solve from its factors solves the system."""
+    A = I.normal_system(2, 512)[0]
+    b = I.uniform_rhs(7, 512)
+    forced = np.ones(8, dtype=np.uint8)
+    for tree in ("greedy", "hqr3"):
+        f0 = O.hybrid_factor(A, 64, forced=forced, tree=tree)
+        f1 = O.hybrid_factor(A, 64, forced=forced, tree=tree, variant=1)
+        f2 = O.hybrid_factor(A, 64, forced=forced, tree=tree, variant=2)
+        assert 0.0 < O.factor_diff(f2.A, f0.A) < 1e-11
+        assert O.factor_diff(f2.A, f1.A) > 0.0
+        x = O.solve(f2, b)
+        assert np.linalg.norm(A @ x - b) / (np.linalg.norm(A) * np.linalg.norm(x)) < 1e-13
