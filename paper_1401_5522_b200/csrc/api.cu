@@ -110,7 +110,6 @@ static int solve_g() {
   }
   return gval;
 }
-#define kSolveG (solve_g())
 constexpr size_t kFlagBytes = 128;  // one solve flag per cache line (solve.cu kFlagStride)
 size_t solve_ws_bytes(int n, int nb, int cmax, size_t units) {
   return align_up(sizeof(int2) * units, 256) + align_up(kFlagBytes * n, 256) +
@@ -412,7 +411,7 @@ int hlq_factor_ex(double* A, int64_t N, int32_t nb, int32_t criterion, double al
          oDc = take(sizeof(unsigned int)),
          oQp = take(spec_qr ? sizeof(double) * (size_t)N * nb : 8);
   // persistent-solve workspace (hlq_solve): unit tables (capacity 2 n cmax), flags, partials
-  const int scmax = solve_rows_cmax(n, kSolveG);
+  const int scmax = solve_rows_cmax(n, solve_g());
   const size_t solve_cap = (size_t)2 * n * scmax + 1;
   size_t oSv = take(solve_ws_bytes(n, nb, scmax, solve_cap));
   size_t oDag = take(sizeof(int) * (dag_total + 1)), oDagP = take(sizeof(int) * (dag_max + 1));
@@ -829,7 +828,7 @@ int hlq_solve(hlq_factors_t f, const double* b, double* x) {
   // A2: Q_kk^T; QR: the stored reflectors of the tree), then block back substitution with U_kk /
   // R_kk.  Runs of consecutive A1 LU steps and the back substitution are single persistent
   // launches (solve.cu k_solve_rows); QR, A2 and domain-pivoting steps replay step by step.
-  const int n = g.n, G = kSolveG, cmax = solve_rows_cmax(n, G);
+  const int n = g.n, G = solve_g(), cmax = solve_rows_cmax(n, G);
   if (!f->solve_ws) {
     auto eligible = [&](int k) {
       return f->dec[k] == HLQ_DEC_LU && f->lu_variant == HLQ_LU_A1 &&
